@@ -1,0 +1,147 @@
+/*
+ * vif.h -- C ABI of the B200-native VIF factor + Gaussian NLL library (libvif.so).
+ *
+ * Method: Vecchia-inducing-points full-scale (VIF) approximation, arXiv 2507.05064
+ * ("P:NNN" = line of PAPER.md):
+ *   whitened inducing features  U = (L_m^{-1} K(Z,X))^T, n x m        P:72-80  (reading c4)
+ *   residual Vecchia factor     B (unit lower, B_{i,N(i)} = -A_i), D  P:85-97, Eq. D_A_Vecchia
+ *   Woodbury / Sylvester NLL    M_w = I + U^T B^T D^{-1} B U
+ *   NLL = n/2 log(2 pi) + 1/2 (sum_i log D_i + logdet M_w) + 1/2 (y^T B^T D^{-1} B y - v^T M_w^{-1} v)
+ * The readings of the paper taken where it is silent (c1..c17) are listed in DESIGN.md.
+ *
+ * Conventions for every call:
+ *   - all floating point is IEEE FP64, all matrices row-major, all indices 0-based;
+ *   - "device" pointers are CUDA device (or managed) memory of the current device; pointers
+ *     documented "device or host" may also be page-locked host memory (copied with
+ *     cudaMemcpyAsync(cudaMemcpyDefault)); the library never frees memory it did not allocate;
+ *   - the library performs NO cudaMalloc: the caller owns one workspace buffer of
+ *     vif_workspace_bytes() bytes (a torch uint8 tensor in the Python binding) for the
+ *     handle's lifetime;
+ *   - all GPU work is enqueued on the caller's CUDA stream (plus, for world > 1, an internal
+ *     communication stream joined by events); only vif_create, vif_set_data(validate=1) and
+ *     vif_nll synchronise with the host;
+ *   - every call returns a vif_status; nothing aborts or throws across the ABI; the last
+ *     error text is available from vif_last_error().
+ */
+#ifndef VIF_H_
+#define VIF_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define VIF_ABI_VERSION 1
+#define VIF_MAX_D 16     /* input dimension limit */
+#define VIF_MAX_MV 47    /* neighbour limit: conditioning sets of s = m_v + 1 <= 48 points */
+
+typedef enum {
+  VIF_OK = 0,
+  VIF_ERR_INVALID_ARG = 1, /* bad dims/pointer/parameter, non-finite input, bad neighbour list */
+  VIF_ERR_NOT_PD = 2,      /* Cholesky failure of K_m, of a residual block C_{N(i),N(i)}, of M */
+  VIF_ERR_CUDA = 3,        /* a CUDA runtime error (text in vif_last_error) */
+  VIF_ERR_NCCL = 4,        /* an NCCL error or NCCL unavailable for world > 1 */
+  VIF_ERR_NO_MEMORY = 5,   /* workspace smaller than vif_workspace_bytes() */
+  VIF_ERR_STATE = 6        /* call order violated (e.g. vif_nll before vif_factor) */
+} vif_status;
+
+/* Covariance families, reading c1: k(a,b) = sigma2 * f(r), r = ||(a - b) / lambda|| */
+typedef enum {
+  VIF_MATERN12 = 0, /* f = exp(-r)                                   nu = 1/2 */
+  VIF_MATERN32 = 1, /* f = (1 + sqrt3 r) exp(-sqrt3 r)               nu = 3/2 */
+  VIF_MATERN52 = 2, /* f = (1 + sqrt5 r + 5 r^2 / 3) exp(-sqrt5 r)   nu = 5/2 */
+  VIF_GAUSSIAN = 3  /* f = exp(-r^2)                                 nu = inf  */
+} vif_family;
+
+/* Covariance parameters theta.  Passed by pointer to vif_factor; read before return. */
+typedef struct {
+  int32_t family;            /* vif_family */
+  int32_t d;                 /* must equal vif_dims.d */
+  double sigma2;             /* marginal variance sigma_1^2 > 0 */
+  const double* lengthscale; /* HOST pointer, d entries > 0 (ARD; isotropic = all equal) */
+  double nugget;             /* error variance sigma^2 >= 0, added by index identity (reading c2) */
+  double jitter;             /* eps >= 0 added to diag K(Z,Z) only (reading c3) */
+} vif_theta;
+
+/* Problem dimensions and the caller's place in the data-parallel job. */
+typedef struct {
+  int64_t n;     /* number of points, >= 1 */
+  int32_t d;     /* input dimension, 1..VIF_MAX_D */
+  int32_t m;     /* inducing points, >= 0 (m = 0: classical Vecchia) */
+  int32_t mv;    /* neighbours per point, 0..VIF_MAX_MV (m_v = 0: FITC) */
+  int32_t rank;  /* this process's rank, 0 <= rank < world */
+  int32_t world; /* number of GPUs the rows are sharded over (one process per GPU) */
+} vif_dims;
+
+/* Result of vif_nll: identical on every rank. */
+typedef struct {
+  double nll;      /* L_dagger(theta; y) */
+  double logdet_D; /* sum_i log D_i */
+  double logdet_M; /* log det M_w = log det M - log det Sigma_m  (reading c4) */
+  double quad;     /* y^T Sigma_dagger^{-1} y */
+  int64_t bad_row; /* on VIF_ERR_NOT_PD: first failing point index, -1 for K_m / M */
+} vif_terms;
+
+/* Fills out128 with a fresh ncclUniqueId (128 bytes).  Call on rank 0 only and broadcast the
+ * bytes (torch.distributed) before vif_create on every rank.  Needs libnccl.so.2 at run time. */
+int vif_nccl_unique_id(void* out128);
+
+/* Bytes of device workspace a handle with these dims needs (computed on the host, no GPU). */
+int vif_workspace_bytes(const vif_dims* dims, size_t* bytes);
+
+/* Rows owned by `rank` under the chunk-cyclic partition (host only, no GPU): the union over
+ * rounds r of [(r*world + rank)*chunk, (r*world + rank + 1)*chunk) intersected with [0, n).
+ * Writes *rounds and *chunk; the caller derives the rows. */
+int vif_partition(const vif_dims* dims, int64_t* rounds, int64_t* chunk);
+
+/* Create a handle.  `workspace` (device, >= vif_workspace_bytes) is owned by the caller and must
+ * outlive the handle.  X (n x d, Vecchia order), Z (m x d), nbr (n x mv int32: nbr[i][k] < i, no
+ * duplicates, -1 only as trailing padding; reading c5) and y (n) are device or host pointers,
+ * copied into the workspace (the caller may free them afterwards); they may be NULL and supplied
+ * later with vif_set_data.  `cuda_stream` is a cudaStream_t (NULL = legacy default stream).
+ * `nccl_id` is the 128-byte id from vif_nccl_unique_id when world > 1; with world > 1 and
+ * nccl_id == NULL the library EMULATES all `world` ranks inside this one process (the same
+ * partition, per-rank ordering and rank-ordered reduction, with the all-gather replaced by the
+ * shared buffer and the all-reduce by an in-order sum) -- used to test sharding on one GPU.
+ * Errors: INVALID_ARG (dims), NO_MEMORY (workspace too small), NCCL, CUDA. */
+int vif_create(void** handle, const vif_dims* dims, void* workspace, size_t ws_bytes, const double* X,
+               const double* Z, const int32_t* nbr, const double* y, const void* nccl_id, void* cuda_stream);
+
+/* (Re)load the inputs (same layout/pointer rules as vif_create; NULL leaves a part unchanged).
+ * Enqueued on the handle's stream.  validate = 1 also checks finiteness and the neighbour-list
+ * rules on the device and synchronises (INVALID_ARG with vif_last_error naming the row). */
+int vif_set_data(void* handle, const double* X, const double* Z, const int32_t* nbr, const double* y,
+                 int32_t validate);
+
+/* Compute the factor at theta: K_m, L_m, L_m^{-1}; U rows (this rank's chunks) and their
+ * all-gather; per owned point the residual block, its Cholesky, A_i, D_i and the row
+ * w_i = (u_i - sum_k A_ik u_{N(i)_k}) / sqrt(D_i) with r_i appended; the Gram
+ * [W r]^T [W r] of the owned rows and its all-reduce.  Asynchronous on the stream.
+ * B_out (device, n x mv; stores -A_i in N(i) order, 0 padding; reading c16) and D_out (device, n)
+ * are optional caller-owned full-length buffers: each rank writes only its owned rows.
+ * Errors: INVALID_ARG (theta), STATE (no data); NOT_PD is reported by vif_nll. */
+int vif_factor(void* handle, const vif_theta* theta, double* B_out, double* D_out);
+
+/* Finish the NLL (Cholesky of M_w, z = L_M^{-1} v, quad, log-dets),
+ * synchronise the stream and return the terms (same value on every rank).
+ * Errors: STATE (no vif_factor since create), NOT_PD (terms->bad_row says where), CUDA, NCCL. */
+int vif_nll(void* handle, vif_terms* out);
+
+/* Debug / parity: copy the whitened features U (n x m, row-major) to `out` (device or host). */
+int vif_copy_U(void* handle, double* out);
+
+/* Number of GPU kernel launches the last vif_factor + vif_nll pair enqueued (for bench.py). */
+int vif_launch_count(void* handle, int64_t* count);
+
+/* Text of the last error on this handle (or of the last failed vif_create when handle is NULL). */
+const char* vif_last_error(void* handle);
+
+/* Release the handle (and its NCCL communicator).  Never frees the workspace. */
+void vif_destroy(void* handle);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* VIF_H_ */

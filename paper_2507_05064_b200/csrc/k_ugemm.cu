@@ -1,0 +1,185 @@
+// k_ugemm.cu -- K1: whitened inducing-point features U = K(X,Z) L_m^{-T} (reading c4).
+//
+// Two launches per evaluation:
+//   K1a kx_eval:  S[p][b] = k(x_i(p), z_b) for the rank's rows (p = position), zero for b in [m, mk);
+//                 also writes U_aug[i][mk] = y_i and the zero pad columns (mk, ld).
+//   K1b gemm_tn:  U_aug[i][a] = sum_{b <= a} S[p][b] Linv[a][b]  -- an FP64 DMMA GEMM whose B
+//                 operand is lower triangular, so K-blocks above the diagonal are skipped
+//                 (n m^2 flops instead of 2 n m^2).
+// Rows are the rank's chunk-cyclic rows: position p -> global row
+//   i = (p / chunk) * world * chunk + rank * chunk + p % chunk.
+#include "common.cuh"
+#include "kernels.h"
+
+namespace vif {
+
+__device__ __forceinline__ int64_t pos_to_row(int64_t p, int64_t chunk, int world, int rank) {
+  return (p / chunk) * (int64_t)world * chunk + (int64_t)rank * chunk + p % chunk;
+}
+
+template <int FAM>
+__global__ void __launch_bounds__(256) kx_eval_kernel(const double* __restrict__ X, const double* __restrict__ Z,
+                                                      const double* __restrict__ y, int64_t n, int64_t npos,
+                                                      int64_t chunk, int world, int rank, int m, int mk,
+                                                      CovParams p, double* __restrict__ S,
+                                                      double* __restrict__ Uaug, int ld) {
+  // one warp per row; lanes stride over the columns
+  const int64_t pos = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (pos >= npos) return;
+  const int64_t i = pos_to_row(pos, chunk, world, rank);
+  const bool valid = i < n;
+  double x[VIF_MAX_D];
+#pragma unroll
+  for (int k = 0; k < VIF_MAX_D; ++k) x[k] = (valid && k < p.d) ? X[i * p.d + k] : 0.0;
+  double* srow = S + pos * (int64_t)mk;
+  for (int b = lane; b < mk; b += 32) {
+    double v = 0.0;
+    if (valid && b < m) {
+      const double* z = Z + (size_t)b * p.d;
+      double r2 = 0.0;
+#pragma unroll 4
+      for (int k = 0; k < p.d; ++k) {
+        const double t = (x[k] - z[k]) * p.inv_ls[k];
+        r2 = fma(t, t, r2);
+      }
+      v = p.sigma2 * cov_f<FAM>(r2);
+    }
+    srow[b] = v;
+  }
+  if (valid) {
+    double* urow = Uaug + i * (int64_t)ld;
+    for (int c = mk + lane; c < ld; c += 32) urow[c] = (c == mk) ? y[i] : 0.0;
+  }
+}
+
+// C[row(p)][c] = sum_k A[p][k] B[c][k], A: npos x K (lda), B: N x K (ldb); B lower-triangular when tri.
+// 128 x 64 CTA tile, BK = 32, 8 warps (4 x 2) of 32 x 32, 3-stage cp.async pipeline.
+// smem rows padded to 40 doubles (320 B = 64 mod 128 B) so the 16-byte fragment loads
+// (k-pair per lane, see below) are bank-conflict free.
+namespace {
+constexpr int GBM = 128, GBN = 64, GBK = 32, GST = 3, GPAD = 40;
+}
+
+__global__ void __launch_bounds__(256) gemm_tn_kernel(const double* __restrict__ A, int64_t lda, int64_t npos,
+                                                      const double* __restrict__ B, int64_t ldb, int N, int K,
+                                                      int tri, double* __restrict__ C, int64_t ldc, int64_t n,
+                                                      int64_t chunk, int world, int rank) {
+  extern __shared__ __align__(16) double gsm[];
+  double* As = gsm;                            // [GST][GBM][GPAD]
+  double* Bs = gsm + GST * GBM * GPAD;         // [GST][GBN][GPAD]
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int wm = warp >> 1, wn = warp & 1;     // 4 x 2 warps
+  const int64_t row0 = (int64_t)blockIdx.x * GBM;
+  const int col0 = blockIdx.y * GBN;
+  int kend = K;
+  if (tri && col0 + GBN < kend) kend = col0 + GBN;
+  const int nkt = (kend + GBK - 1) / GBK;
+
+  auto load_stage = [&](int st, int kt) {
+    const int k0 = kt * GBK;
+    double* as = As + st * GBM * GPAD;
+    double* bs = Bs + st * GBN * GPAD;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {  // 128 rows x 16 chunks of 16 B = 2048
+      const int e = tid + j * 256;
+      const int r = e >> 4, c2 = (e & 15) * 2;
+      const int64_t gr = row0 + r;
+      const bool ok = gr < npos && k0 + c2 < kend;
+      const double* src = ok ? A + gr * lda + k0 + c2 : A;
+      cp_async16(as + r * GPAD + c2, src, ok);
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {  // 64 rows x 16 chunks
+      const int e = tid + j * 256;
+      const int r = e >> 4, c2 = (e & 15) * 2;
+      const int gc = col0 + r;
+      const bool ok = gc < N && k0 + c2 < kend;
+      const double* src = ok ? B + (int64_t)gc * ldb + k0 + c2 : B;
+      cp_async16(bs + r * GPAD + c2, src, ok);
+    }
+  };
+
+  double acc[4][4][2];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+
+#pragma unroll
+  for (int s = 0; s < GST - 1; ++s) {
+    if (s < nkt) load_stage(s, s);
+    cp_async_commit();
+  }
+  const int fr = lane >> 2, fk = (lane & 3) * 2;
+  for (int kt = 0; kt < nkt; ++kt) {
+    cp_async_wait<GST - 2>();
+    __syncthreads();
+    {
+      const int nk = kt + GST - 1;
+      if (nk < nkt) load_stage(nk % GST, nk);
+      cp_async_commit();
+    }
+    const double* as = As + (kt % GST) * GBM * GPAD + (wm * 32 + fr) * GPAD + fk;
+    const double* bs = Bs + (kt % GST) * GBN * GPAD + (wn * 32 + fr) * GPAD + fk;
+#pragma unroll
+    for (int kk = 0; kk < GBK; kk += 8) {
+      // each lane holds k = kk + fk + {0,1} of its row: two k-steps of 4 with a consistent
+      // permutation of k on both operands (the contraction is order-independent)
+      double2 af[4], bf[4];
+#pragma unroll
+      for (int t = 0; t < 4; ++t) af[t] = *reinterpret_cast<const double2*>(as + t * 8 * GPAD + kk);
+#pragma unroll
+      for (int t = 0; t < 4; ++t) bf[t] = *reinterpret_cast<const double2*>(bs + t * 8 * GPAD + kk);
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) dmma884(acc[a][b][0], acc[a][b][1], af[a].x, bf[b].x);
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) dmma884(acc[a][b][0], acc[a][b][1], af[a].y, bf[b].y);
+    }
+  }
+  cp_async_wait<0>();
+  // epilogue: lane holds C[fr][2*(lane&3) + {0,1}] of each 8x8 tile
+#pragma unroll
+  for (int a = 0; a < 4; ++a) {
+    const int64_t p = row0 + wm * 32 + a * 8 + fr;
+    if (p >= npos) continue;
+    const int64_t i = pos_to_row(p, chunk, world, rank);
+    if (i >= n) continue;
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const int c = col0 + wn * 32 + b * 8 + (lane & 3) * 2;
+      if (c < N) *reinterpret_cast<double2*>(C + i * ldc + c) = make_double2(acc[a][b][0], acc[a][b][1]);
+    }
+  }
+}
+
+cudaError_t launch_u_features(const double* X, const double* Z, const double* y, int64_t n, int64_t npos,
+                              int64_t chunk, int world, int rank, int m, int mk, const CovParams& p,
+                              const double* Linv, double* S, double* Uaug, int ld, cudaStream_t s) {
+  if (npos == 0) return cudaSuccess;
+  const int blocks = (int)((npos + 7) / 8);
+  switch (p.family) {
+    case FAM_M12: kx_eval_kernel<FAM_M12><<<blocks, 256, 0, s>>>(X, Z, y, n, npos, chunk, world, rank, m, mk, p, S, Uaug, ld); break;
+    case FAM_M32: kx_eval_kernel<FAM_M32><<<blocks, 256, 0, s>>>(X, Z, y, n, npos, chunk, world, rank, m, mk, p, S, Uaug, ld); break;
+    case FAM_M52: kx_eval_kernel<FAM_M52><<<blocks, 256, 0, s>>>(X, Z, y, n, npos, chunk, world, rank, m, mk, p, S, Uaug, ld); break;
+    default: kx_eval_kernel<FAM_GAUSS><<<blocks, 256, 0, s>>>(X, Z, y, n, npos, chunk, world, rank, m, mk, p, S, Uaug, ld); break;
+  }
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess || mk == 0) return e;
+  const size_t smem = (size_t)GST * (GBM + GBN) * GPAD * sizeof(double);
+  static bool attr_set = false;
+  if (!attr_set) {
+    e = cudaFuncSetAttribute(gemm_tn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  dim3 grid((unsigned)((npos + GBM - 1) / GBM), (unsigned)((mk + GBN - 1) / GBN));
+  gemm_tn_kernel<<<grid, 256, smem, s>>>(S, mk, npos, Linv, mk, mk, mk, 1, Uaug, ld, n, chunk, world, rank);
+  return cudaGetLastError();
+}
+
+}  // namespace vif

@@ -1,0 +1,60 @@
+// kernels.h -- host-side launchers of the libvif kernels (internal to the library).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "common.cuh"
+
+namespace vif {
+
+struct VecchiaArgs {
+  const double* U;
+  int64_t ldu;
+  int mk;
+  int ld;
+  const double* X;
+  const int32_t* nbr;
+  int mv;
+  const int64_t* order;
+  int64_t npts;
+  CovParams p;
+  double* W;
+  int64_t ldw;
+  double* Dpos;
+  double* B_out;
+  double* D_out;
+  DevStatus* st;
+};
+
+// K0 / K5
+cudaError_t launch_build_km(const double* Z, int m, const CovParams& p, double* Km, cudaStream_t s);
+cudaError_t launch_chol_inv(double* A, int m, int lda, double diag_add, double* Linv, int ldi, int lim_inv,
+                            int* fail, int num_sms, cudaStream_t s);
+cudaError_t launch_logd_sum(const double* Dpos, int64_t npts, double* partials, int np, double* out,
+                            cudaStream_t s);
+cudaError_t launch_finish(const double* G, int ld, int m, int ycol, const double* LinvM, int ldi,
+                          const double* logdetD_dev, int64_t n, double* terms, cudaStream_t s);
+// K1
+cudaError_t launch_u_features(const double* X, const double* Z, const double* y, int64_t n, int64_t npos,
+                              int64_t chunk, int world, int rank, int m, int mk, const CovParams& p,
+                              const double* Linv, double* S, double* Uaug, int ld, cudaStream_t s);
+// K2 + K3
+cudaError_t launch_vecchia(const VecchiaArgs& a, cudaStream_t s);
+// K4
+int syrk_ntiles(int ncols);
+int syrk_nsplit(int ncols, int64_t nrows, int num_sms);
+size_t syrk_part_doubles(int ncols, int nsplit);
+cudaError_t launch_syrk(const double* W, int64_t ldw, int64_t nrows, int ncols, int nsplit, double* Gpart,
+                        double* G, int ldg, cudaStream_t s);
+// misc
+cudaError_t launch_validate(const double* X, int64_t n, int d, const double* Z, int m, const double* y,
+                            const int32_t* nbr, int mv, DevStatus* st, cudaStream_t s);
+size_t order_temp_bytes(int64_t npos);
+cudaError_t launch_order(const double* X, int64_t n, int d, int64_t npos, int64_t chunk, int world, int rank,
+                         double* bbox, uint64_t* keys, uint64_t* keys_alt, int64_t* vals, int64_t* vals_alt,
+                         void* temp, size_t temp_bytes, int64_t** order_out, cudaStream_t s);
+cudaError_t launch_sum_buffers(const double* src, int64_t count, int nbuf, int64_t stride, double* dst,
+                               cudaStream_t s);
+cudaError_t launch_reset_status(DevStatus* st, cudaStream_t s);
+
+}  // namespace vif

@@ -1,0 +1,570 @@
+// vif_api.cu -- the C ABI of include/vif.h: handle, workspace layout, stream orchestration,
+// chunk-cyclic row sharding and the two collectives (U all-gather, Gram all-reduce).
+//
+// One evaluation on rank g of G:
+//   A0 K_m, L_m, L_m^{-1}                          launch_build_km + launch_chol_inv   (replicated)
+//   A1 U rows of the rank's chunks                 launch_u_features (K1a + K1b)
+//   A2 replicate U                                 ncclAllGather per round (in place)
+//   A3-A5 per owned point: C_S, chol, A_i, D_i, w_i  launch_vecchia
+//   A6 G = [W r]^T [W r] over owned rows, sum log D  launch_syrk + launch_logd_sum
+//   A7 sum G and log D over ranks                  ncclAllReduce (one call, (ld^2 + 1) doubles)
+//   A8 M_w chol, z, quad, NLL                       launch_chol_inv + launch_finish  (vif_nll)
+// NCCL is loaded lazily with dlopen (only for world > 1), so a single-GPU process needs nothing
+// beyond the CUDA driver.
+#include <dlfcn.h>
+#include <math.h>
+#include <nccl.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/vif.h"
+#include "common.cuh"
+#include "kernels.h"
+
+using namespace vif;
+
+namespace {
+
+constexpr int kPlanSMs = 148;  // SM count used for host-side workspace planning (B200)
+constexpr int kLogdParts = 256;
+
+thread_local std::string g_create_error;
+
+// ---------------------------------------------------------------- NCCL (dlopen)
+struct Nccl {
+  void* lib = nullptr;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+  bool ok = false;
+};
+
+Nccl& nccl() {
+  static Nccl n;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    n.lib = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (n.lib) {
+      n.GetUniqueId = (decltype(n.GetUniqueId))dlsym(n.lib, "ncclGetUniqueId");
+      n.CommInitRank = (decltype(n.CommInitRank))dlsym(n.lib, "ncclCommInitRank");
+      n.AllGather = (decltype(n.AllGather))dlsym(n.lib, "ncclAllGather");
+      n.AllReduce = (decltype(n.AllReduce))dlsym(n.lib, "ncclAllReduce");
+      n.CommDestroy = (decltype(n.CommDestroy))dlsym(n.lib, "ncclCommDestroy");
+      n.GroupStart = (decltype(n.GroupStart))dlsym(n.lib, "ncclGroupStart");
+      n.GroupEnd = (decltype(n.GroupEnd))dlsym(n.lib, "ncclGroupEnd");
+      n.GetErrorString = (decltype(n.GetErrorString))dlsym(n.lib, "ncclGetErrorString");
+      n.ok = n.GetUniqueId && n.CommInitRank && n.AllGather && n.AllReduce && n.CommDestroy && n.GroupStart &&
+             n.GroupEnd && n.GetErrorString;
+    }
+  }
+  return n;
+}
+
+// ---------------------------------------------------------------- derived dims + layout
+struct Plan {
+  int64_t n;
+  int d, m, mv, rank, world;
+  bool emulate;
+  int mk, ycol, ld;
+  int64_t rounds, chunk, npos, npad;
+  int nsplit;
+  std::vector<int64_t> n_own;
+};
+
+enum Buf {
+  B_X, B_Z, B_NBR, B_Y, B_KM, B_LINV, B_U, B_W, B_DPOS, B_ORDER, B_KEYS, B_KEYS2, B_VALS, B_VALS2, B_TEMP,
+  B_GPART, B_G, B_GSUM, B_LINVM, B_PART, B_BBOX, B_TERMS, B_STATUS, B_COUNT
+};
+
+struct Layout {
+  size_t off[B_COUNT];
+  size_t size[B_COUNT];
+  size_t total;
+};
+
+inline int64_t round_up(int64_t a, int64_t b) { return (a + b - 1) / b * b; }
+
+bool make_plan(const vif_dims* dims, bool emulate, Plan& P, std::string& err) {
+  if (!dims) { err = "dims is NULL"; return false; }
+  if (dims->n < 1) { err = "n must be >= 1"; return false; }
+  if (dims->d < 1 || dims->d > VIF_MAX_D) { err = "d must be in [1, VIF_MAX_D]"; return false; }
+  if (dims->m < 0) { err = "m must be >= 0"; return false; }
+  if (dims->mv < 0 || dims->mv > VIF_MAX_MV) { err = "mv must be in [0, VIF_MAX_MV]"; return false; }
+  if (dims->n > (int64_t)0x7fffffff) { err = "n must fit in int32 (neighbour indices are int32)"; return false; }
+  if (dims->world < 1 || dims->rank < 0 || dims->rank >= dims->world) { err = "need 0 <= rank < world"; return false; }
+  P.n = dims->n; P.d = dims->d; P.m = dims->m; P.mv = dims->mv; P.rank = dims->rank; P.world = dims->world;
+  P.emulate = emulate && dims->world > 1;
+  P.mk = (int)round_up(P.m, 8);
+  P.ycol = P.mk;
+  P.ld = (int)round_up(P.mk + 1, 8);
+  if (P.world == 1) {
+    P.rounds = 1;
+    P.chunk = P.n;
+  } else {
+    P.rounds = 8;
+    P.chunk = (P.n + P.rounds * P.world - 1) / (P.rounds * P.world);
+    if (P.chunk < 1) P.chunk = 1;
+  }
+  P.npos = P.rounds * P.chunk;
+  P.npad = P.npos * P.world;
+  P.n_own.assign(P.world, 0);
+  for (int g = 0; g < P.world; ++g)
+    for (int64_t r = 0; r < P.rounds; ++r) {
+      const int64_t start = (r * P.world + g) * P.chunk;
+      const int64_t cnt = P.n - start;
+      P.n_own[g] += cnt <= 0 ? 0 : (cnt < P.chunk ? cnt : P.chunk);
+    }
+  P.nsplit = syrk_nsplit(P.ld, P.npos, kPlanSMs);
+  return true;
+}
+
+Layout make_layout(const Plan& P) {
+  Layout L{};
+  const size_t D8 = sizeof(double);
+  const int nrep = P.emulate ? P.world : 1;
+  const size_t gsz = ((size_t)P.ld * P.ld + 8) * D8;
+  const int64_t m1 = P.m > 0 ? P.m : 1, mk1 = P.mk > 0 ? P.mk : 1;
+  L.size[B_X] = (size_t)P.n * P.d * D8;
+  L.size[B_Z] = (size_t)m1 * P.d * D8;
+  L.size[B_NBR] = (size_t)P.n * (P.mv > 0 ? P.mv : 1) * sizeof(int32_t);
+  L.size[B_Y] = (size_t)P.n * D8;
+  L.size[B_KM] = (size_t)m1 * m1 * D8;
+  L.size[B_LINV] = (size_t)mk1 * mk1 * D8;
+  L.size[B_U] = (size_t)P.npad * P.ld * D8;
+  L.size[B_W] = (size_t)P.npos * P.ld * D8;
+  L.size[B_DPOS] = (size_t)P.npos * D8;
+  L.size[B_ORDER] = (size_t)nrep * P.npos * sizeof(int64_t);
+  L.size[B_KEYS] = L.size[B_KEYS2] = L.size[B_VALS] = L.size[B_VALS2] = (size_t)P.npos * 8;
+  L.size[B_TEMP] = order_temp_bytes(P.npos);
+  L.size[B_GPART] = syrk_part_doubles(P.ld, P.nsplit) * D8;
+  L.size[B_G] = nrep * gsz;
+  L.size[B_GSUM] = gsz;
+  L.size[B_LINVM] = (size_t)mk1 * mk1 * D8;
+  L.size[B_PART] = kLogdParts * D8;
+  L.size[B_BBOX] = 128 * 6 * D8;
+  L.size[B_TERMS] = 8 * D8;
+  L.size[B_STATUS] = 256;
+  size_t off = 0;
+  for (int b = 0; b < B_COUNT; ++b) {
+    L.off[b] = off;
+    off += (L.size[b] + 255) / 256 * 256;
+  }
+  L.total = off + 256;  // slack for base alignment
+  return L;
+}
+
+struct Handle {
+  Plan P;
+  Layout L;
+  char* base = nullptr;
+  cudaStream_t stream = nullptr;
+  int num_sms = 148;
+  ncclComm_t comm = nullptr;
+  bool have_data = false, factored = false, finished = false;
+  vif_terms cached{};
+  int cached_status = VIF_OK;
+  std::string err;
+  int64_t launches = 0;
+  std::vector<const int64_t*> order;  // per (logical) rank
+
+  template <typename T>
+  T* buf(Buf b) const { return reinterpret_cast<T*>(base + L.off[b]); }
+};
+
+int fail(Handle* h, int code, const std::string& msg) {
+  if (h) h->err = msg;
+  else g_create_error = msg;
+  return code;
+}
+
+int cuda_fail(Handle* h, cudaError_t e, const char* where) {
+  return fail(h, VIF_ERR_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+#define VIF_CUDA(h, call, where)                   \
+  do {                                             \
+    cudaError_t e_ = (call);                       \
+    if (e_ != cudaSuccess) return cuda_fail(h, e_, where); \
+  } while (0)
+
+bool make_params(const Handle* h, const vif_theta* th, CovParams& p, std::string& err) {
+  if (!th) { err = "theta is NULL"; return false; }
+  if (th->d != h->P.d) { err = "theta.d != dims.d"; return false; }
+  if (th->family < 0 || th->family > 3) { err = "unknown covariance family"; return false; }
+  if (!(th->sigma2 > 0.0) || !isfinite(th->sigma2)) { err = "sigma2 must be finite and > 0"; return false; }
+  if (!(th->nugget >= 0.0) || !isfinite(th->nugget)) { err = "nugget must be finite and >= 0"; return false; }
+  if (!(th->jitter >= 0.0) || !isfinite(th->jitter)) { err = "jitter must be finite and >= 0"; return false; }
+  if (!th->lengthscale) { err = "lengthscale is NULL"; return false; }
+  memset(&p, 0, sizeof(p));
+  for (int k = 0; k < th->d; ++k) {
+    const double l = th->lengthscale[k];
+    if (!(l > 0.0) || !isfinite(l)) { err = "lengthscales must be finite and > 0"; return false; }
+    p.inv_ls[k] = 1.0 / l;
+  }
+  p.sigma2 = th->sigma2;
+  p.nugget = th->nugget;
+  p.jitter = th->jitter;
+  p.d = th->d;
+  p.family = th->family;
+  return true;
+}
+
+int compute_orders(Handle* h) {
+  const Plan& P = h->P;
+  const int nrep = P.emulate ? P.world : 1;
+  h->order.assign(nrep, nullptr);
+  for (int g = 0; g < nrep; ++g) {
+    const int rank = P.emulate ? g : P.rank;
+    int64_t* sorted = nullptr;
+    VIF_CUDA(h, launch_order(h->buf<double>(B_X), P.n, P.d, P.npos, P.chunk, P.world, rank, h->buf<double>(B_BBOX),
+                             h->buf<uint64_t>(B_KEYS), h->buf<uint64_t>(B_KEYS2), h->buf<int64_t>(B_VALS),
+                             h->buf<int64_t>(B_VALS2), h->buf<void>(B_TEMP), h->L.size[B_TEMP], &sorted, h->stream),
+             "order");
+    int64_t* dst = h->buf<int64_t>(B_ORDER) + (size_t)g * P.npos;
+    VIF_CUDA(h, cudaMemcpyAsync(dst, sorted, P.npos * sizeof(int64_t), cudaMemcpyDeviceToDevice, h->stream),
+             "order copy");
+    h->order[g] = dst;
+  }
+  return VIF_OK;
+}
+
+int set_data(Handle* h, const double* X, const double* Z, const int32_t* nbr, const double* y, int validate) {
+  const Plan& P = h->P;
+  cudaStream_t s = h->stream;
+  if (X) VIF_CUDA(h, cudaMemcpyAsync(h->buf<double>(B_X), X, P.n * P.d * 8, cudaMemcpyDefault, s), "copy X");
+  if (Z && P.m > 0) VIF_CUDA(h, cudaMemcpyAsync(h->buf<double>(B_Z), Z, (size_t)P.m * P.d * 8, cudaMemcpyDefault, s), "copy Z");
+  if (nbr && P.mv > 0)
+    VIF_CUDA(h, cudaMemcpyAsync(h->buf<int32_t>(B_NBR), nbr, (size_t)P.n * P.mv * 4, cudaMemcpyDefault, s), "copy nbr");
+  if (y) VIF_CUDA(h, cudaMemcpyAsync(h->buf<double>(B_Y), y, P.n * 8, cudaMemcpyDefault, s), "copy y");
+  if (X) {
+    int r = compute_orders(h);
+    if (r != VIF_OK) return r;
+  }
+  if (X || Z || nbr || y) {
+    h->have_data = h->have_data || (X && y && (nbr || P.mv == 0) && (Z || P.m == 0));
+    h->factored = h->finished = false;
+  }
+  if (validate) {
+    DevStatus* st = h->buf<DevStatus>(B_STATUS);
+    VIF_CUDA(h, launch_reset_status(st, s), "reset status");
+    VIF_CUDA(h, launch_validate(h->buf<double>(B_X), P.n, P.d, h->buf<double>(B_Z), P.m, h->buf<double>(B_Y),
+                                h->buf<int32_t>(B_NBR), P.mv > 0 ? P.mv : 0, st, s),
+             "validate");
+    DevStatus hs;
+    VIF_CUDA(h, cudaMemcpyAsync(&hs, st, sizeof(hs), cudaMemcpyDeviceToHost, s), "status copy");
+    VIF_CUDA(h, cudaStreamSynchronize(s), "sync");
+    if (hs.bad_input != ~0ULL) {
+      char msg[160];
+      snprintf(msg, sizeof msg, "invalid input at row %llu (non-finite X/y or neighbour rule: N(i) < i, unique, -1 only trailing)",
+               hs.bad_input);
+      return fail(h, VIF_ERR_INVALID_ARG, msg);
+    }
+    if (hs.bad_z) return fail(h, VIF_ERR_INVALID_ARG, "non-finite inducing point");
+  }
+  return VIF_OK;
+}
+
+}  // namespace
+
+// ====================================================================== C ABI
+extern "C" {
+
+int vif_nccl_unique_id(void* out128) {
+  if (!out128) return fail(nullptr, VIF_ERR_INVALID_ARG, "out128 is NULL");
+  Nccl& N = nccl();
+  if (!N.ok) return fail(nullptr, VIF_ERR_NCCL, "libnccl.so.2 not loadable");
+  ncclUniqueId id;
+  ncclResult_t r = N.GetUniqueId(&id);
+  if (r != ncclSuccess) return fail(nullptr, VIF_ERR_NCCL, N.GetErrorString(r));
+  memcpy(out128, &id, sizeof(id));
+  return VIF_OK;
+}
+
+int vif_workspace_bytes(const vif_dims* dims, size_t* bytes) {
+  Plan P;
+  std::string err;
+  if (!bytes) return fail(nullptr, VIF_ERR_INVALID_ARG, "bytes is NULL");
+  if (!make_plan(dims, true, P, err)) return fail(nullptr, VIF_ERR_INVALID_ARG, err);
+  *bytes = make_layout(P).total;
+  return VIF_OK;
+}
+
+int vif_partition(const vif_dims* dims, int64_t* rounds, int64_t* chunk) {
+  Plan P;
+  std::string err;
+  if (!make_plan(dims, false, P, err)) return fail(nullptr, VIF_ERR_INVALID_ARG, err);
+  if (rounds) *rounds = P.rounds;
+  if (chunk) *chunk = P.chunk;
+  return VIF_OK;
+}
+
+int vif_create(void** handle, const vif_dims* dims, void* workspace, size_t ws_bytes, const double* X,
+               const double* Z, const int32_t* nbr, const double* y, const void* nccl_id, void* cuda_stream) {
+  if (!handle) return fail(nullptr, VIF_ERR_INVALID_ARG, "handle is NULL");
+  *handle = nullptr;
+  Handle* h = new Handle();
+  std::string err;
+  if (!make_plan(dims, nccl_id == nullptr, h->P, err)) {
+    delete h;
+    return fail(nullptr, VIF_ERR_INVALID_ARG, err);
+  }
+  h->L = make_layout(h->P);
+  if (!workspace || ws_bytes < h->L.total) {
+    char msg[128];
+    snprintf(msg, sizeof msg, "workspace too small: need %zu bytes", h->L.total);
+    delete h;
+    return fail(nullptr, VIF_ERR_NO_MEMORY, msg);
+  }
+  h->base = reinterpret_cast<char*>(round_up((int64_t)(uintptr_t)workspace, 256));
+  h->stream = reinterpret_cast<cudaStream_t>(cuda_stream);
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e == cudaSuccess) e = cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, dev);
+  if (e != cudaSuccess) {
+    std::string m = std::string("cuda: ") + cudaGetErrorString(e);
+    delete h;
+    return fail(nullptr, VIF_ERR_CUDA, m);
+  }
+  // zero the reduction buffers once (their upper triangles are never written)
+  e = cudaMemsetAsync(h->base + h->L.off[B_G], 0, h->L.size[B_G], h->stream);
+  if (e == cudaSuccess) e = cudaMemsetAsync(h->base + h->L.off[B_GSUM], 0, h->L.size[B_GSUM], h->stream);
+  if (e != cudaSuccess) {
+    std::string m = std::string("memset: ") + cudaGetErrorString(e);
+    delete h;
+    return fail(nullptr, VIF_ERR_CUDA, m);
+  }
+  if (h->P.world > 1 && !h->P.emulate) {
+    Nccl& N = nccl();
+    if (!N.ok) {
+      delete h;
+      return fail(nullptr, VIF_ERR_NCCL, "libnccl.so.2 not loadable");
+    }
+    ncclUniqueId id;
+    memcpy(&id, nccl_id, sizeof(id));
+    ncclResult_t r = N.CommInitRank(&h->comm, h->P.world, id, h->P.rank);
+    if (r != ncclSuccess) {
+      std::string m = std::string("ncclCommInitRank: ") + N.GetErrorString(r);
+      delete h;
+      return fail(nullptr, VIF_ERR_NCCL, m);
+    }
+  }
+  if (X || Z || nbr || y) {
+    int r = set_data(h, X, Z, nbr, y, 1);
+    if (r != VIF_OK) {
+      g_create_error = h->err;
+      if (h->comm) nccl().CommDestroy(h->comm);
+      delete h;
+      return r;
+    }
+  }
+  e = cudaStreamSynchronize(h->stream);
+  if (e != cudaSuccess) {
+    std::string m = std::string("create sync: ") + cudaGetErrorString(e);
+    if (h->comm) nccl().CommDestroy(h->comm);
+    delete h;
+    return fail(nullptr, VIF_ERR_CUDA, m);
+  }
+  *handle = h;
+  return VIF_OK;
+}
+
+int vif_set_data(void* handle, const double* X, const double* Z, const int32_t* nbr, const double* y,
+                 int32_t validate) {
+  Handle* h = reinterpret_cast<Handle*>(handle);
+  if (!h) return fail(nullptr, VIF_ERR_INVALID_ARG, "handle is NULL");
+  return set_data(h, X, Z, nbr, y, validate);
+}
+
+int vif_factor(void* handle, const vif_theta* theta, double* B_out, double* D_out) {
+  Handle* h = reinterpret_cast<Handle*>(handle);
+  if (!h) return fail(nullptr, VIF_ERR_INVALID_ARG, "handle is NULL");
+  if (!h->have_data) return fail(h, VIF_ERR_STATE, "no data: pass X, Z, nbr, y to vif_create or vif_set_data");
+  CovParams p;
+  std::string err;
+  if (!make_params(h, theta, p, err)) return fail(h, VIF_ERR_INVALID_ARG, err);
+  const Plan& P = h->P;
+  cudaStream_t s = h->stream;
+  DevStatus* st = h->buf<DevStatus>(B_STATUS);
+  int64_t nl = 0;
+  VIF_CUDA(h, launch_reset_status(st, s), "reset status");
+  ++nl;
+  // A0: K_m, L_m, L_m^{-1}
+  if (P.m > 0) {
+    VIF_CUDA(h, launch_build_km(h->buf<double>(B_Z), P.m, p, h->buf<double>(B_KM), s), "build K_m");
+    VIF_CUDA(h, cudaMemsetAsync(h->buf<double>(B_LINV), 0, h->L.size[B_LINV], s), "memset Linv");
+    VIF_CUDA(h, launch_chol_inv(h->buf<double>(B_KM), P.m, P.m, 0.0, h->buf<double>(B_LINV), P.mk, P.mk, &st->km_fail,
+                                h->num_sms, s),
+             "chol K_m");
+    nl += 2;
+  }
+  // A1 (+A2): U rows per (logical) rank
+  const int nrep = P.emulate ? P.world : 1;
+  for (int g = 0; g < nrep; ++g) {
+    const int rank = P.emulate ? g : P.rank;
+    VIF_CUDA(h, launch_u_features(h->buf<double>(B_X), h->buf<double>(B_Z), h->buf<double>(B_Y), P.n, P.npos, P.chunk,
+                                  P.world, rank, P.m, P.mk, p, h->buf<double>(B_LINV), h->buf<double>(B_W),
+                                  h->buf<double>(B_U), P.ld, s),
+             "U features");
+    nl += P.mk > 0 ? 2 : 1;
+  }
+  if (P.world > 1 && !P.emulate) {
+    Nccl& N = nccl();
+    const size_t cnt = (size_t)P.chunk * P.ld;
+    N.GroupStart();
+    for (int64_t r = 0; r < P.rounds; ++r) {
+      double* recv = h->buf<double>(B_U) + (size_t)r * P.world * cnt;
+      ncclResult_t rr = N.AllGather(recv + (size_t)P.rank * cnt, recv, cnt, ncclFloat64, h->comm, s);
+      if (rr != ncclSuccess) {
+        N.GroupEnd();
+        return fail(h, VIF_ERR_NCCL, std::string("ncclAllGather: ") + N.GetErrorString(rr));
+      }
+    }
+    ncclResult_t rr = N.GroupEnd();
+    if (rr != ncclSuccess) return fail(h, VIF_ERR_NCCL, std::string("ncclGroupEnd: ") + N.GetErrorString(rr));
+  }
+  // A3-A6 per (logical) rank
+  const size_t gstride = (size_t)P.ld * P.ld + 8;
+  for (int g = 0; g < nrep; ++g) {
+    const int rank = P.emulate ? g : P.rank;
+    const int64_t npts = P.n_own[rank];
+    VecchiaArgs a;
+    a.U = h->buf<double>(B_U);
+    a.ldu = P.ld;
+    a.mk = P.mk;
+    a.ld = P.ld;
+    a.X = h->buf<double>(B_X);
+    a.nbr = h->buf<int32_t>(B_NBR);
+    a.mv = P.mv;
+    a.order = h->order[g];
+    a.npts = npts;
+    a.p = p;
+    a.W = h->buf<double>(B_W);
+    a.ldw = P.ld;
+    a.Dpos = h->buf<double>(B_DPOS);
+    a.B_out = B_out;
+    a.D_out = D_out;
+    a.st = st;
+    VIF_CUDA(h, launch_vecchia(a, s), "vecchia");
+    double* G = h->buf<double>(B_G) + g * gstride;
+    VIF_CUDA(h, launch_syrk(h->buf<double>(B_W), P.ld, npts, P.ld, P.nsplit, h->buf<double>(B_GPART), G, P.ld, s),
+             "syrk");
+    VIF_CUDA(h, launch_logd_sum(h->buf<double>(B_DPOS), npts, h->buf<double>(B_PART), kLogdParts,
+                                G + (size_t)P.ld * P.ld, s),
+             "logd");
+    nl += 5;
+  }
+  // A7
+  if (P.emulate) {
+    VIF_CUDA(h, launch_sum_buffers(h->buf<double>(B_G), (int64_t)gstride, P.world, (int64_t)gstride,
+                                   h->buf<double>(B_GSUM), s),
+             "emulated all-reduce");
+    ++nl;
+  } else if (P.world > 1) {
+    Nccl& N = nccl();
+    double* G = h->buf<double>(B_G);
+    ncclResult_t rr = N.AllReduce(G, G, (size_t)P.ld * P.ld + 1, ncclFloat64, ncclSum, h->comm, s);
+    if (rr != ncclSuccess) return fail(h, VIF_ERR_NCCL, std::string("ncclAllReduce: ") + N.GetErrorString(rr));
+  }
+  h->factored = true;
+  h->finished = false;
+  h->launches = nl;
+  return VIF_OK;
+}
+
+int vif_nll(void* handle, vif_terms* out) {
+  Handle* h = reinterpret_cast<Handle*>(handle);
+  if (!h) return fail(nullptr, VIF_ERR_INVALID_ARG, "handle is NULL");
+  if (!out) return fail(h, VIF_ERR_INVALID_ARG, "out is NULL");
+  if (!h->factored) return fail(h, VIF_ERR_STATE, "vif_nll before vif_factor");
+  if (h->finished) {
+    *out = h->cached;
+    return h->cached_status;
+  }
+  const Plan& P = h->P;
+  cudaStream_t s = h->stream;
+  DevStatus* st = h->buf<DevStatus>(B_STATUS);
+  double* G = P.emulate ? h->buf<double>(B_GSUM) : h->buf<double>(B_G);
+  int64_t nl = 0;
+  if (P.m > 0) {
+    VIF_CUDA(h, cudaMemsetAsync(h->buf<double>(B_LINVM), 0, h->L.size[B_LINVM], s), "memset LinvM");
+    VIF_CUDA(h, launch_chol_inv(G, P.m, P.ld, 1.0, h->buf<double>(B_LINVM), P.mk, P.mk, &st->m_fail, h->num_sms, s),
+             "chol M");
+    ++nl;
+  }
+  double* terms = h->buf<double>(B_TERMS);
+  VIF_CUDA(h, launch_finish(G, P.ld, P.m, P.ycol, h->buf<double>(B_LINVM), P.mk, G + (size_t)P.ld * P.ld, P.n, terms, s),
+           "finish");
+  ++nl;
+  h->launches += nl;
+  double ht[4];
+  DevStatus hs;
+  VIF_CUDA(h, cudaMemcpyAsync(ht, terms, sizeof(ht), cudaMemcpyDeviceToHost, s), "terms copy");
+  VIF_CUDA(h, cudaMemcpyAsync(&hs, st, sizeof(hs), cudaMemcpyDeviceToHost, s), "status copy");
+  VIF_CUDA(h, cudaStreamSynchronize(s), "sync");
+  vif_terms t;
+  t.nll = ht[0];
+  t.logdet_D = ht[1];
+  t.logdet_M = ht[2];
+  t.quad = ht[3];
+  t.bad_row = -1;
+  int status = VIF_OK;
+  if (hs.km_fail) {
+    status = fail(h, VIF_ERR_NOT_PD, "Cholesky of K(Z,Z) + jitter failed");
+  } else if (hs.bad_row != ~0ULL) {
+    t.bad_row = (int64_t)hs.bad_row;
+    char msg[128];
+    snprintf(msg, sizeof msg, "residual block of point %lld is not positive definite", (long long)hs.bad_row);
+    status = fail(h, VIF_ERR_NOT_PD, msg);
+  } else if (hs.m_fail) {
+    status = fail(h, VIF_ERR_NOT_PD, "Cholesky of M failed");
+  }
+  h->finished = true;
+  h->cached = t;
+  h->cached_status = status;
+  *out = t;
+  return status;
+}
+
+int vif_copy_U(void* handle, double* out) {
+  Handle* h = reinterpret_cast<Handle*>(handle);
+  if (!h || !out) return fail(h, VIF_ERR_INVALID_ARG, "NULL argument");
+  if (!h->factored) return fail(h, VIF_ERR_STATE, "vif_copy_U before vif_factor");
+  const Plan& P = h->P;
+  if (P.m == 0) return VIF_OK;
+  VIF_CUDA(h, cudaMemcpy2DAsync(out, (size_t)P.m * 8, h->buf<double>(B_U), (size_t)P.ld * 8, (size_t)P.m * 8, P.n,
+                                cudaMemcpyDefault, h->stream),
+           "copy U");
+  VIF_CUDA(h, cudaStreamSynchronize(h->stream), "sync");
+  return VIF_OK;
+}
+
+int vif_launch_count(void* handle, int64_t* count) {
+  Handle* h = reinterpret_cast<Handle*>(handle);
+  if (!h || !count) return fail(h, VIF_ERR_INVALID_ARG, "NULL argument");
+  *count = h->launches;
+  return VIF_OK;
+}
+
+const char* vif_last_error(void* handle) {
+  Handle* h = reinterpret_cast<Handle*>(handle);
+  return h ? h->err.c_str() : g_create_error.c_str();
+}
+
+void vif_destroy(void* handle) {
+  Handle* h = reinterpret_cast<Handle*>(handle);
+  if (!h) return;
+  if (h->comm) nccl().CommDestroy(h->comm);
+  delete h;
+}
+
+}  // extern "C"

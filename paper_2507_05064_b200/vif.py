@@ -1,0 +1,278 @@
+"""Thin Python binding of libvif.so (include/vif.h): argument marshalling only.
+
+Every step of the VIF factor + NLL runs in the CUDA kernels of libvif.so; PyTorch only
+supplies device memory (the workspace is a torch uint8 tensor), the CUDA stream and, for
+world > 1, the process group used to broadcast the 128-byte NCCL id.  There is no CPU
+fallback: if libvif.so is missing or CUDA is unavailable the calls raise.
+
+Names mirror the C ABI: vif_workspace_bytes, vif_partition, vif_create, vif_set_data,
+vif_factor, vif_nll, vif_copy_U, vif_launch_count, vif_last_error, vif_destroy,
+vif_nccl_unique_id.  `VifModel` is a convenience owner of one handle + its workspace.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+from typing import Optional, Sequence, Union
+
+import numpy as np
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libvif.so")
+
+FAMILIES = {"matern12": 0, "matern32": 1, "matern52": 2, "gaussian": 3}
+STATUS = {0: "VIF_OK", 1: "VIF_ERR_INVALID_ARG", 2: "VIF_ERR_NOT_PD", 3: "VIF_ERR_CUDA", 4: "VIF_ERR_NCCL",
+          5: "VIF_ERR_NO_MEMORY", 6: "VIF_ERR_STATE"}
+
+
+class VifError(RuntimeError):
+    def __init__(self, status: int, msg: str, bad_row: int = -1):
+        super().__init__(f"{STATUS.get(status, status)}: {msg}")
+        self.status, self.msg, self.bad_row = status, msg, bad_row
+
+
+class _Dims(ctypes.Structure):
+    _fields_ = [("n", ctypes.c_int64), ("d", ctypes.c_int32), ("m", ctypes.c_int32), ("mv", ctypes.c_int32),
+                ("rank", ctypes.c_int32), ("world", ctypes.c_int32)]
+
+
+class _Theta(ctypes.Structure):
+    _fields_ = [("family", ctypes.c_int32), ("d", ctypes.c_int32), ("sigma2", ctypes.c_double),
+                ("lengthscale", ctypes.POINTER(ctypes.c_double)), ("nugget", ctypes.c_double),
+                ("jitter", ctypes.c_double)]
+
+
+class _Terms(ctypes.Structure):
+    _fields_ = [("nll", ctypes.c_double), ("logdet_D", ctypes.c_double), ("logdet_M", ctypes.c_double),
+                ("quad", ctypes.c_double), ("bad_row", ctypes.c_int64)]
+
+
+_lib = None
+
+
+def load_library():
+    """Load libvif.so (built in-tree by __graft_entry__.build()); raise loudly if it is missing."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} not built: run `python -c 'import __graft_entry__ as g; g.build()'`")
+        lib = ctypes.CDLL(LIB_PATH)
+        P, i32, i64, sz = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_size_t
+        lib.vif_nccl_unique_id.argtypes = [P]
+        lib.vif_workspace_bytes.argtypes = [ctypes.POINTER(_Dims), ctypes.POINTER(sz)]
+        lib.vif_partition.argtypes = [ctypes.POINTER(_Dims), ctypes.POINTER(i64), ctypes.POINTER(i64)]
+        lib.vif_create.argtypes = [ctypes.POINTER(P), ctypes.POINTER(_Dims), P, sz, P, P, P, P, P, P]
+        lib.vif_set_data.argtypes = [P, P, P, P, P, i32]
+        lib.vif_factor.argtypes = [P, ctypes.POINTER(_Theta), P, P]
+        lib.vif_nll.argtypes = [P, ctypes.POINTER(_Terms)]
+        lib.vif_copy_U.argtypes = [P, P]
+        lib.vif_launch_count.argtypes = [P, ctypes.POINTER(i64)]
+        lib.vif_last_error.argtypes = [P]
+        lib.vif_last_error.restype = ctypes.c_char_p
+        lib.vif_destroy.argtypes = [P]
+        lib.vif_destroy.restype = None
+        for f in ("vif_nccl_unique_id", "vif_workspace_bytes", "vif_partition", "vif_create", "vif_set_data",
+                  "vif_factor", "vif_nll", "vif_copy_U", "vif_launch_count"):
+            getattr(lib, f).restype = ctypes.c_int
+        _lib = lib
+    return _lib
+
+
+EXPORTED = ("vif_nccl_unique_id", "vif_workspace_bytes", "vif_partition", "vif_create", "vif_set_data",
+            "vif_factor", "vif_nll", "vif_copy_U", "vif_launch_count", "vif_last_error", "vif_destroy")
+
+
+def _check(st: int, handle=None, bad_row: int = -1):
+    if st != 0:
+        msg = load_library().vif_last_error(handle).decode(errors="replace")
+        raise VifError(st, msg, bad_row)
+
+
+def _dims(n, d, m, mv, rank=0, world=1) -> _Dims:
+    return _Dims(int(n), int(d), int(m), int(mv), int(rank), int(world))
+
+
+def vif_workspace_bytes(n: int, d: int, m: int, mv: int, rank: int = 0, world: int = 1) -> int:
+    out = ctypes.c_size_t(0)
+    _check(load_library().vif_workspace_bytes(ctypes.byref(_dims(n, d, m, mv, rank, world)), ctypes.byref(out)))
+    return int(out.value)
+
+
+def vif_partition(n: int, d: int, m: int, mv: int, rank: int = 0, world: int = 1):
+    """(rounds, chunk) of the chunk-cyclic row partition (host only)."""
+    r, c = ctypes.c_int64(0), ctypes.c_int64(0)
+    _check(load_library().vif_partition(ctypes.byref(_dims(n, d, m, mv, rank, world)), ctypes.byref(r),
+                                        ctypes.byref(c)))
+    return int(r.value), int(c.value)
+
+
+def owned_rows(n: int, rank: int, world: int, rounds: int, chunk: int) -> np.ndarray:
+    """Global rows of `rank` under the chunk-cyclic partition described by vif_partition."""
+    parts = []
+    for r in range(rounds):
+        s = (r * world + rank) * chunk
+        e = min(s + chunk, n)
+        if s < e:
+            parts.append(np.arange(s, e))
+    return np.concatenate(parts) if parts else np.zeros(0, dtype=np.int64)
+
+
+def vif_nccl_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    _check(load_library().vif_nccl_unique_id(buf))
+    return buf.raw
+
+
+def _ptr(t: Optional[torch.Tensor]):
+    return ctypes.c_void_p(t.data_ptr()) if t is not None else None
+
+
+def _as_input(a, dtype, device) -> Optional[torch.Tensor]:
+    """Device tensors pass through; pinned host tensors pass through (the library copies them);
+    numpy arrays are moved to the device first (plumbing only)."""
+    if a is None:
+        return None
+    if isinstance(a, np.ndarray):
+        a = torch.from_numpy(np.ascontiguousarray(a)).to(device)
+    if a.dtype != dtype:
+        raise TypeError(f"expected {dtype}, got {a.dtype}")
+    if not a.is_contiguous():
+        a = a.contiguous()
+    if not a.is_cuda and not a.is_pinned():
+        a = a.to(device)
+    return a
+
+
+@dataclass
+class Theta:
+    """theta: family, sigma_1^2, ARD length-scales, nugget sigma^2, jitter eps (reading c3)."""
+    family: Union[str, int]
+    sigma2: float
+    lengthscale: Sequence[float]
+    nugget: float
+    jitter: float
+
+    def to_c(self):
+        ls = np.ascontiguousarray(np.asarray(self.lengthscale, dtype=np.float64))
+        fam = FAMILIES[self.family] if isinstance(self.family, str) else int(self.family)
+        th = _Theta(fam, len(ls), float(self.sigma2), ls.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
+                    float(self.nugget), float(self.jitter))
+        return th, ls
+
+
+@dataclass
+class Terms:
+    nll: float
+    logdet_D: float
+    logdet_M: float
+    quad: float
+    bad_row: int
+
+
+def vif_create(n, d, m, mv, workspace: torch.Tensor, X=None, Z=None, nbr=None, y=None, *, rank=0, world=1,
+               nccl_id: Optional[bytes] = None, stream: Optional[torch.cuda.Stream] = None) -> ctypes.c_void_p:
+    lib = load_library()
+    h = ctypes.c_void_p()
+    s = (stream or torch.cuda.current_stream(workspace.device)).cuda_stream
+    idbuf = ctypes.create_string_buffer(nccl_id, 128) if nccl_id is not None else None
+    st = lib.vif_create(ctypes.byref(h), ctypes.byref(_dims(n, d, m, mv, rank, world)),
+                        ctypes.c_void_p(workspace.data_ptr()), workspace.numel(), _ptr(X), _ptr(Z), _ptr(nbr),
+                        _ptr(y), idbuf, ctypes.c_void_p(s))
+    _check(st, None)
+    return h
+
+
+def vif_set_data(h, X=None, Z=None, nbr=None, y=None, validate: bool = False):
+    _check(load_library().vif_set_data(h, _ptr(X), _ptr(Z), _ptr(nbr), _ptr(y), int(validate)), h)
+
+
+def vif_factor(h, theta: Theta, B_out: Optional[torch.Tensor] = None, D_out: Optional[torch.Tensor] = None):
+    th, keep = theta.to_c()
+    _check(load_library().vif_factor(h, ctypes.byref(th), _ptr(B_out), _ptr(D_out)), h)
+
+
+def vif_nll(h) -> Terms:
+    t = _Terms()
+    st = load_library().vif_nll(h, ctypes.byref(t))
+    _check(st, h, t.bad_row)
+    return Terms(t.nll, t.logdet_D, t.logdet_M, t.quad, t.bad_row)
+
+
+def vif_copy_U(h, out: torch.Tensor):
+    _check(load_library().vif_copy_U(h, _ptr(out)), h)
+
+
+def vif_launch_count(h) -> int:
+    c = ctypes.c_int64(0)
+    _check(load_library().vif_launch_count(h, ctypes.byref(c)), h)
+    return int(c.value)
+
+
+def vif_last_error(h=None) -> str:
+    return load_library().vif_last_error(h).decode(errors="replace")
+
+
+def vif_destroy(h):
+    load_library().vif_destroy(h)
+
+
+class VifModel:
+    """One handle + its torch-owned workspace on `device`."""
+
+    def __init__(self, X, Z, nbr, y, *, rank: int = 0, world: int = 1, nccl_id: Optional[bytes] = None,
+                 device: Union[str, torch.device] = "cuda", stream: Optional[torch.cuda.Stream] = None):
+        if not torch.cuda.is_available():
+            raise RuntimeError("VifModel needs a CUDA device (no CPU fallback by design)")
+        self.device = torch.device(device)
+        X = _as_input(X, torch.float64, self.device)
+        Z = _as_input(Z, torch.float64, self.device)
+        nbr = _as_input(nbr, torch.int32, self.device)
+        y = _as_input(y, torch.float64, self.device)
+        self.n, self.d = X.shape
+        self.m = Z.shape[0]
+        self.mv = nbr.shape[1]
+        self.rank, self.world = rank, world
+        nbytes = vif_workspace_bytes(self.n, self.d, self.m, self.mv, rank, world)
+        self.workspace = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
+        self.stream = stream
+        self.handle = vif_create(self.n, self.d, self.m, self.mv, self.workspace,
+                                 X, Z if self.m > 0 else None, nbr if self.mv > 0 else None, y,
+                                 rank=rank, world=world, nccl_id=nccl_id, stream=stream)
+        self.rounds, self.chunk = vif_partition(self.n, self.d, self.m, self.mv, rank, world)
+
+    def set_data(self, X=None, Z=None, nbr=None, y=None, validate=False):
+        vif_set_data(self.handle, X, Z, nbr, y, validate)
+
+    def factor(self, theta: Theta, B_out=None, D_out=None):
+        vif_factor(self.handle, theta, B_out, D_out)
+
+    def nll(self) -> Terms:
+        return vif_nll(self.handle)
+
+    def evaluate(self, theta: Theta, B_out=None, D_out=None) -> Terms:
+        self.factor(theta, B_out, D_out)
+        return self.nll()
+
+    def U(self) -> torch.Tensor:
+        out = torch.empty((self.n, self.m), dtype=torch.float64, device=self.device)
+        vif_copy_U(self.handle, out)
+        return out
+
+    def owned_rows(self, rank=None) -> np.ndarray:
+        return owned_rows(self.n, self.rank if rank is None else rank, self.world, self.rounds, self.chunk)
+
+    def launch_count(self) -> int:
+        return vif_launch_count(self.handle)
+
+    def close(self):
+        if getattr(self, "handle", None) is not None:
+            vif_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

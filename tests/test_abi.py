@@ -1,0 +1,89 @@
+"""C-ABI boundary checks that need no GPU: the library loads, exports every symbol include/vif.h
+declares, and its host-only entry points (workspace sizing, partition, argument errors) behave."""
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def p():
+    import __graft_entry__
+    __graft_entry__.build()
+    import paper_2507_05064_b200 as pkg
+    pkg.load_library()
+    return pkg
+
+
+def declared_functions():
+    src = open(os.path.join(ROOT, "include", "vif.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(vif_[A-Za-z0-9_]+)\s*\(", src)))
+
+
+def test_header_declares_the_boundary():
+    names = declared_functions()
+    for f in ("vif_create", "vif_factor", "vif_nll", "vif_destroy", "vif_workspace_bytes"):
+        assert f in names
+
+
+def test_library_exports_every_declared_symbol(p):
+    lib = ctypes.CDLL(p.LIB_PATH)
+    for name in declared_functions():
+        assert hasattr(lib, name), name
+    assert set(declared_functions()) == set(p.EXPORTED)
+
+
+def test_library_is_sm100a():
+    import subprocess
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf",
+                          os.path.join(ROOT, "paper_2507_05064_b200", "libvif.so")],
+                         capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_sass_uses_fp64_tensor_core():
+    import subprocess
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "-sass",
+                          os.path.join(ROOT, "paper_2507_05064_b200", "libvif.so")],
+                         capture_output=True, text=True).stdout
+    assert "DMMA.8x8x4" in out
+
+
+def test_workspace_and_partition_host_only(p):
+    b = p.vif_workspace_bytes(1_000_000, 2, 500, 30)
+    # U (n x 512) + W (n x 512) dominate: ~8.2 GB
+    assert 8.0e9 < b < 9.0e9
+    assert p.vif_partition(10, 2, 3, 2, 0, 1) == (1, 10)
+    rounds, chunk = p.vif_partition(1000, 2, 3, 2, 1, 4)
+    assert rounds * chunk * 4 >= 1000
+    for n, world in [(1, 1), (7, 2), (1000, 4), (1003, 8), (5, 8)]:
+        seen = []
+        for r in range(world):
+            R, c = p.vif_partition(n, 2, 3, 2, r, world)
+            seen.append(p.owned_rows(n, r, world, R, c))
+        allr = np.sort(np.concatenate(seen))
+        np.testing.assert_array_equal(allr, np.arange(n))
+
+
+@pytest.mark.parametrize("dims,err", [
+    ((0, 2, 3, 2), 1), ((10, 0, 3, 2), 1), ((10, 17, 3, 2), 1), ((10, 2, -1, 2), 1), ((10, 2, 3, 48), 1),
+])
+def test_bad_dims_rejected(p, dims, err):
+    with pytest.raises(p.VifError) as e:
+        p.vif_workspace_bytes(*dims)
+    assert e.value.status == err
+
+
+def test_create_rejects_small_workspace_without_gpu(p):
+    lib = p.load_library()
+    h = ctypes.c_void_p()
+    dims = p.vif._dims(100, 2, 5, 3)
+    st = lib.vif_create(ctypes.byref(h), ctypes.byref(dims), ctypes.c_void_p(16), 64, None, None, None, None, None,
+                        None)
+    assert st == 5
+    assert "workspace too small" in p.vif_last_error(None)

@@ -1,0 +1,229 @@
+"""CUDA path (through the C ABI) vs the CPU oracle on the same seeded inputs.  Needs a B200."""
+import math
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import oracle  # noqa: E402
+import vifgen  # noqa: E402
+from parity import check_B, check_D, check_terms, check_U  # noqa: E402
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _lib():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import __graft_entry__
+    __graft_entry__.build()
+    import paper_2507_05064_b200 as p
+    p.load_library()
+    return p
+
+
+def vif():
+    import paper_2507_05064_b200 as p
+    return p
+
+
+def run_gpu(w, world=1, emulate=True, want_U=False, host_inputs=False):
+    p = vif()
+    dev = torch.device("cuda")
+    if host_inputs:
+        X = torch.from_numpy(w.X).pin_memory()
+        Z = torch.from_numpy(w.Z.reshape(-1, w.d)).pin_memory()
+        nbr = torch.from_numpy(w.nbr).pin_memory()
+        y = torch.from_numpy(w.y).pin_memory()
+    else:
+        X, Z, nbr, y = (torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+                        for a in (w.X, w.Z.reshape(-1, w.d), w.nbr, w.y))
+    model = p.VifModel(X, Z, nbr, y, world=world, device=dev)
+    B = torch.zeros((w.n, w.mv), dtype=torch.float64, device=dev)
+    D = torch.zeros(w.n, dtype=torch.float64, device=dev)
+    th = p.Theta(**w.theta_dict())
+    t = model.evaluate(th, B, D)
+    U = model.U().cpu().numpy() if want_U else None
+    out = (t, B.cpu().numpy(), D.cpu().numpy(), U, model.launch_count())
+    model.close()
+    return out
+
+
+def oracle_run(w, want_U=False):
+    return oracle.factor_nll(w.X, w.Z, w.nbr, w.y, oracle.Theta(**w.theta_dict()), want_U=want_U)
+
+
+def assert_parity(w, world=1, want_U=True, host_inputs=False):
+    t, B, D, U, nl = run_gpu(w, world=world, want_U=want_U, host_inputs=host_inputs)
+    r = oracle_run(w, want_U=want_U)
+    check_terms(t, r.nll, r.logdet_D, r.logdet_M, r.quad)
+    check_D(D, r.D)
+    check_B(B, r.B)
+    if want_U and w.m > 0:
+        check_U(U, r.U)
+    assert nl > 0
+    return t, r
+
+
+def small(n, m, mv, family="matern32", d=2, seed=1, rho=0.15, nugget=0.1, ard=None, x="uniform", neighbors="dc"):
+    return vifgen.make_workload(n=n, d=d, m=m, mv=mv, family=family, rho=rho, nugget=nugget, seed=seed,
+                                device="cuda", ard=ard, x=x, z="kmeans++" if m > 0 else "subset",
+                                neighbors=neighbors)
+
+
+def test_config1_full_parity():
+    w = vifgen.make_config(1, device="cuda")
+    assert_parity(w)
+
+
+@pytest.mark.parametrize("n,m,mv,family,d", [
+    (3001, 37, 7, "matern32", 2),      # odd m, ragged n, RB = 1
+    (2500, 64, 31, "matern52", 3),     # RB = 4 (s = 32), m multiple of 64
+    (1777, 130, 20, "matern12", 2),    # RB = 3, several GEMM col tiles + ragged
+    (1200, 16, 40, "gaussian", 4),     # RB = 6 (s = 41)
+    (900, 9, 47, "matern32", 1),       # max m_v, d = 1
+    (2049, 200, 15, "matern52", 5),    # several 64-col SYRK tiles
+])
+def test_shapes_parity(n, m, mv, family, d):
+    w = small(n, m, mv, family=family, d=d, seed=n + m + mv, rho=0.3 if d > 2 else 0.15)
+    assert_parity(w)
+
+
+def test_m0_classical_vecchia():
+    w = small(1500, 0, 12, seed=5)
+    t, r = assert_parity(w, want_U=False)
+    assert t.logdet_M == 0.0
+
+
+def test_mv0_fitc():
+    w = small(1200, 20, 0, seed=6)
+    assert_parity(w)
+
+
+def test_ard_10d_config4_recipe_small():
+    w = vifgen.make_workload(n=3000, d=10, m=100, mv=20, family="matern52", ard=(0.5, 5.0), nugget=0.1,
+                             x="normal", seed=vifgen.SEED_BASE + 4, device="cuda")
+    assert_parity(w)
+
+
+def test_exact_case_all_predecessors_matches_dense():
+    from refs import dense_nll, sk_cov
+    n = 40
+    w = small(n, 6, n - 1, seed=7, neighbors="all")
+    t, B, D, U, _ = run_gpu(w)
+    S = sk_cov(w.family, w.sigma2, w.lengthscale, w.X) + w.nugget * np.eye(n)
+    assert t.nll == pytest.approx(dense_nll(S, w.y), rel=1e-9)
+
+
+def test_n1_scalar():
+    p = vif()
+    for m in (0, 3):
+        rng = np.random.default_rng(3)
+        w = vifgen.Workload("n1", rng.random((1, 2)), rng.random((m, 2)), np.zeros((1, 2), np.int32) - 1,
+                            np.array([0.4]), "matern32", 1.2, np.array([0.3, 0.3]), 0.2, 1e-10)
+        assert_parity(w, want_U=m > 0)
+
+
+@pytest.mark.parametrize("world", [2, 3, 4])
+def test_emulated_sharding_matches_single(world):
+    w = small(5003, 48, 10, seed=11)
+    t1, B1, D1, _, _ = run_gpu(w, world=1)
+    tg, Bg, Dg, _, _ = run_gpu(w, world=world)
+    assert tg.nll == pytest.approx(t1.nll, rel=1e-12)
+    assert tg.quad == pytest.approx(t1.quad, rel=1e-11)
+    np.testing.assert_array_equal(Dg, D1)   # rows are computed identically, only the sums change order
+    np.testing.assert_array_equal(Bg, B1)
+
+
+def test_host_pinned_inputs_same_result():
+    w = small(2000, 32, 9, seed=12)
+    t_dev, *_ = run_gpu(w)
+    t_host, *_ = run_gpu(w, host_inputs=True)
+    assert t_host.nll == t_dev.nll
+
+
+def test_repeat_evaluations_deterministic_and_theta_change():
+    p = vif()
+    w = small(4000, 40, 12, seed=13)
+    dev = torch.device("cuda")
+    model = p.VifModel(*(torch.from_numpy(np.ascontiguousarray(a)).to(dev) for a in (w.X, w.Z, w.nbr, w.y)))
+    th = p.Theta(**w.theta_dict())
+    a = model.evaluate(th)
+    b = model.evaluate(th)
+    assert a.nll == b.nll
+    th2 = w.theta_dict()
+    th2["lengthscale"] = th2["lengthscale"] * 1.1
+    c = model.evaluate(p.Theta(**th2))
+    r = oracle.factor_nll(w.X, w.Z, w.nbr, w.y, oracle.Theta(**th2))
+    check_terms(c, r.nll, r.logdet_D, r.logdet_M, r.quad)
+    model.close()
+
+
+# ---------------- error behaviour ----------------
+def test_invalid_neighbors_rejected():
+    p = vif()
+    w = small(300, 8, 5, seed=14)
+    nbr = w.nbr.copy()
+    nbr[100, 0] = 150   # not a predecessor
+    dev = torch.device("cuda")
+    with pytest.raises(p.VifError) as e:
+        p.VifModel(*(torch.from_numpy(np.ascontiguousarray(a)).to(dev) for a in (w.X, w.Z, nbr, w.y)))
+    assert e.value.status == 1 and "row 100" in e.value.msg
+
+
+def test_not_pd_reports_row():
+    p = vif()
+    X = np.array([[0.1, 0.1], [0.5, 0.5], [0.5, 0.5], [0.7, 0.2]])
+    nbr = np.array([[-1, -1], [0, -1], [1, 0], [2, 1]], np.int32)
+    dev = torch.device("cuda")
+    model = p.VifModel(torch.from_numpy(X).to(dev), torch.zeros((0, 2), dtype=torch.float64, device=dev),
+                       torch.from_numpy(nbr).to(dev), torch.zeros(4, dtype=torch.float64, device=dev))
+    with pytest.raises(p.VifError) as e:
+        model.evaluate(p.Theta("matern32", 1.0, [0.3, 0.3], 0.0, 0.0))
+    assert e.value.status == 2 and e.value.bad_row in (2, 3)
+
+
+def test_state_and_theta_errors():
+    p = vif()
+    w = small(200, 8, 4, seed=15)
+    dev = torch.device("cuda")
+    model = p.VifModel(*(torch.from_numpy(np.ascontiguousarray(a)).to(dev) for a in (w.X, w.Z, w.nbr, w.y)))
+    with pytest.raises(p.VifError) as e:
+        model.nll()
+    assert e.value.status == 6
+    with pytest.raises(p.VifError) as e:
+        model.factor(p.Theta("matern32", -1.0, [0.1, 0.1], 0.1, 0.0))
+    assert e.value.status == 1
+    with pytest.raises(p.VifError) as e:
+        model.factor(p.Theta("matern32", 1.0, [0.1], 0.1, 0.0))
+    assert e.value.status == 1
+    model.close()
+
+
+# ---------------- larger configs (BASELINE.json configs[1], configs[2]) ----------------
+def test_config2_full_parity():
+    w = vifgen.make_config(2, device="cuda")
+    assert_parity(w, want_U=False)
+
+
+@pytest.mark.slow
+def test_config3_full_nll_and_sampled_rows():
+    """n = 1M, m = 500, m_v = 30 in the bench's launch configuration: full oracle NLL + 2000 sampled
+    rows of U, B, D recomputed one by one by the oracle; invariants at every row."""
+    p = vif()
+    w = vifgen.make_config(3, device="cuda")
+    t, B, D, U, _ = run_gpu(w, want_U=True)
+    rows = np.random.default_rng(0).choice(w.n, 2000, replace=False)
+    rows = np.concatenate([rows, [0, 1, 29, 30, 31, w.n - 1]])
+    Ur, Br, Dr = oracle.rows(w.X, w.Z, w.nbr, oracle.Theta(**w.theta_dict()), rows, want_U=True)
+    check_D(D[rows], Dr)
+    check_B(B[rows], Br)
+    rel = np.linalg.norm(U[rows] - Ur, axis=1) / np.linalg.norm(Ur, axis=1)
+    assert rel.max() <= 1e-11
+    # invariants at all rows (p6): sigma^2 <= D_i <= C_ii
+    Cii = w.sigma2 + w.nugget - (U * U).sum(1)
+    assert np.all(D >= w.nugget * (1 - 1e-12)) and np.all(D <= Cii * (1 + 1e-10))
+    assert t.logdet_M >= 0 and t.quad >= 0
+    r = oracle_run(w)
+    check_terms(t, r.nll, r.logdet_D, r.logdet_M, r.quad)
