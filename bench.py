@@ -1,0 +1,386 @@
+#!/usr/bin/env python3
+"""Benchmark: VIF factor + NLL evaluations, points/s at n = 1M (BASELINE.json configs[2]).
+
+One "step" = one whole pass of the hot path (vif_factor + vif_nll: K_m, L_m^-1, U, all-gather,
+per-point residual Vecchia rows, W, SYRK, all-reduce, M Cholesky, NLL) over the n = 1M workload,
+with inputs already resident in HBM; theta alternates between the data-generating value and the
+range x 1.1 so nothing theta-dependent can be reused across steps.  U (4.1 GB) and W (4.1 GB) are
+rewritten every step, far larger than the 126 MB L2.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config 3] [--impl vif|reference]
+
+Multi-GPU: launched by torchrun, one process per GPU; rows are sharded chunk-cyclically, U is
+all-gathered and the Gram all-reduced by NCCL inside libvif; the problem size stays n = 1M
+(strong scaling).  Rank 0 prints one JSON line.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "VIF factor+NLL evals: points/s at n=1M (1/2/4/8 B200), % FP64-tensor/HBM roofline"
+FP64_PEAK_TFLOPS = 37.1   # measured: tools/microbench_fp64.cu DMMA.8x8x4 register loop (profiles/r01_fp64_peaks.json)
+FP64_CUBLAS_TFLOPS = 35.5  # measured: cuBLAS DGEMM 8192^3 (torch.matmul float64)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=3)
+    ap.add_argument("--n", type=int, default=None, help="override n (same recipe)")
+    ap.add_argument("--impl", default="vif", choices=["vif", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target CPU seconds of the oracle sample")
+    return ap.parse_args()
+
+
+# ------------------------------------------------------------------------------------ clocks
+class ClockSampler:
+    """Samples SM clock + throttle reasons through NVML during the timed region."""
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+               0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+               0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
+
+    def __init__(self, device_index: int):
+        self.samples, self.reasons = [], set()
+        self.max_mhz = None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            import torch
+            h = None
+            try:
+                props = torch.cuda.get_device_properties(device_index)
+                bus = f"{props.pci_domain_id:08x}:{props.pci_bus_id:02x}:{props.pci_device_id:02x}.0"
+                h = pynvml.nvmlDeviceGetHandleByPciBusId(bus.encode())
+            except Exception:
+                h = pynvml.nvmlDeviceGetHandleByIndex(device_index)
+            self.nvml, self.h = pynvml, h
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+        except Exception as e:  # pragma: no cover
+            self.nvml, self.h = None, None
+            self.error = str(e)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nvml.nvmlDeviceGetClockInfo(self.h, self.nvml.NVML_CLOCK_SM))
+                r = self.nvml.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.02)
+
+    def __enter__(self):
+        if self.h is not None:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.h is not None:
+            self.t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": 0}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons - {"gpu_idle"}), "samples": len(self.samples)}
+
+
+# ------------------------------------------------------------------------------------ flops
+def per_point_flops(s, m):
+    """SURVEY 8(d) algorithmic FP64 work per point, split by kernel (FMA = 2, symmetric once)."""
+    mv = s - 1
+    return {"ufeat": float(m) * m,                                   # A1  U = K L^-T (triangular)
+            "vecchia": s * (s + 1.0) * m + s ** 3 / 3.0 + mv ** 2 + 2.0 * mv * m,  # A3 + A4 + A5
+            "syrk": (m + 1.0) * (m + 2.0)}                            # A6
+
+
+def workload_flops(nbr, m):
+    s = (nbr >= 0).sum(1).astype(np.float64) + 1.0 if nbr.shape[1] > 0 else np.ones(nbr.shape[0])
+    f = per_point_flops(s, m)
+    return {k: float(np.sum(v)) if np.ndim(v) else float(v) * len(s) for k, v in f.items()}
+
+
+def describe(w, cid):
+    return {"workload": f"config{cid}: n={w.n}, d={w.d}, {w.family}, m={w.m} inducing, m_v={w.mv}, "
+                        f"nugget={w.nugget}, random ordering, correlation-distance neighbours",
+            "n": w.n, "d": w.d, "m": w.m, "mv": w.mv, "family": w.family,
+            "l2": "inputs > L2: U and W (n x 512 fp64 = 4.1 GB each) rewritten every step",
+            "theta": "alternating data-generating theta and range x 1.1"}
+
+
+def thetas(w):
+    t0 = w.theta_dict()
+    t1 = w.theta_dict()
+    t1["lengthscale"] = t1["lengthscale"] * 1.1
+    return t0, t1
+
+
+# ------------------------------------------------------------------------------------ CPU oracle
+def cpu_oracle_sample(w, target_s):
+    """Time the oracle (as it stands) on a prefix of the same workload: X[:ns], nbr[:ns] (neighbours are
+    predecessors, so a prefix is self-contained), same Z, theta, m, m_v.  Returns (points/s, cores, sample, s)."""
+    import oracle
+    th = oracle.Theta(**w.theta_dict())
+    ns = min(w.n, 4000)
+    t = time.perf_counter()
+    oracle.factor_nll(w.X[:ns], w.Z, w.nbr[:ns], w.y[:ns], th, want_BD=False)
+    dt = time.perf_counter() - t
+    ns2 = int(min(w.n, max(ns, ns * target_s / max(dt, 1e-3))))
+    t = time.perf_counter()
+    oracle.factor_nll(w.X[:ns2], w.Z, w.nbr[:ns2], w.y[:ns2], th, want_BD=False)
+    dt2 = time.perf_counter() - t
+    return ns2 / dt2, oracle.num_threads(), ns2, dt2
+
+
+# ------------------------------------------------------------------------------------ main
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    import torch
+    import torch.distributed as dist
+
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+
+    import vifgen
+    cid = args.config
+
+    # ---------------- input generation (timed separately, rank 0, broadcast) ----------------
+    t_gen = time.perf_counter()
+    if rank == 0:
+        w = vifgen.make_config(cid, device=str(dev), n=args.n)
+    else:
+        w = None
+    gen_s = time.perf_counter() - t_gen
+
+    if args.impl == "reference":
+        if rank == 0:
+            run_reference(args, w, cid, world, gen_s)
+        if world > 1:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+
+    import __graft_entry__
+    __graft_entry__.build()
+    import paper_2507_05064_b200 as vp
+
+    if world > 1:
+        meta = [None]
+        if rank == 0:
+            meta = [dict(n=w.n, d=w.d, m=w.m, mv=w.mv, theta=w.theta_dict(), name=w.name, timings=w.timings)]
+        dist.broadcast_object_list(meta, src=0)
+        meta = meta[0]
+        if rank == 0:
+            X, Z, nbr, y = (torch.from_numpy(np.ascontiguousarray(a)).to(dev) for a in (w.X, w.Z, w.nbr, w.y))
+        else:
+            X = torch.empty((meta["n"], meta["d"]), dtype=torch.float64, device=dev)
+            Z = torch.empty((meta["m"], meta["d"]), dtype=torch.float64, device=dev)
+            nbr = torch.empty((meta["n"], meta["mv"]), dtype=torch.int32, device=dev)
+            y = torch.empty(meta["n"], dtype=torch.float64, device=dev)
+        for t in (X, Z, nbr, y):
+            dist.broadcast(t, src=0)
+        if rank != 0:
+            th = meta["theta"]
+            w = vifgen.Workload(meta["name"], X.cpu().numpy(), Z.cpu().numpy(), nbr.cpu().numpy(), y.cpu().numpy(),
+                                th["family"], th["sigma2"], np.asarray(th["lengthscale"]), th["nugget"], th["jitter"],
+                                meta["timings"])
+        uid = [vp.vif_nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        nccl_id = uid[0]
+    else:
+        X, Z, nbr, y = (torch.from_numpy(np.ascontiguousarray(a)).to(dev) for a in (w.X, w.Z, w.nbr, w.y))
+        nccl_id = None
+
+    stream = torch.cuda.current_stream(dev)
+    t_create = time.perf_counter()
+    model = vp.VifModel(X, Z, nbr, y, rank=rank, world=world, nccl_id=nccl_id, device=dev, stream=stream)
+    create_s = time.perf_counter() - t_create
+    th = [vp.Theta(**t) for t in thetas(w)]
+
+    def step(k):
+        model.factor(th[k % 2])
+        return model.nll()
+
+    for k in range(args.warmup):
+        step(k)
+    launches_per_step = model.launch_count()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    # ---------------- timed region (device events on the library's stream) ----------------
+    model.profile(True)
+    sampler = ClockSampler(local)
+    barrier()
+    torch.cuda.synchronize(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with sampler:
+        e0.record(stream)
+        last = None
+        for k in range(args.steps):
+            last = step(k)
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+    barrier()
+    ms = e0.elapsed_time(e1) / args.steps
+    stages, nev = model.stage_times()
+    model.profile(False)
+    ms_t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+    ms_max = float(ms_t.item())
+
+    # ---------------- end-to-end through the public API with HOST buffers ----------------
+    hX, hZ, hnbr, hy = (torch.from_numpy(np.ascontiguousarray(a)).pin_memory() for a in (w.X, w.Z, w.nbr, w.y))
+    h2d = sum(t.numel() * t.element_size() for t in (hX, hZ, hnbr, hy))
+    d2h = 4 * 8 + 8  # vif_terms (4 doubles + bad_row) read back by vif_nll
+    e2e_steps = max(3, min(args.steps, 10))
+    for k in range(2):
+        model.set_data(hX, hZ, hnbr, hy)
+        step(k)
+    barrier()
+    torch.cuda.synchronize(dev)
+    f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    f0.record(stream)
+    for k in range(e2e_steps):
+        model.set_data(hX, hZ, hnbr, hy)
+        step(k)
+    f1.record(stream)
+    torch.cuda.synchronize(dev)
+    barrier()
+    e2e_ms = torch.tensor([f0.elapsed_time(f1) / e2e_steps], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
+    e2e_ms = float(e2e_ms.item())
+
+    if rank == 0:
+        fl = workload_flops(w.nbr, w.m)
+        # per-rank share of the row-sharded kernels (strong scaling: each rank does ~1/world of the rows)
+        share = 1.0 / world
+        stage_avg = {k: v / max(nev, 1) for k, v in stages.items()}
+        names = list(stage_avg.keys())
+        kern = {"ufeat": names[1], "vecchia": names[3], "syrk": names[4]}
+        fl_launch = {k: fl[k] * share for k in kern}
+        achieved = {k: fl_launch[k] / (stage_avg[kern[k]] * 1e-3) / 1e12 if stage_avg[kern[k]] > 0 else 0.0
+                    for k in kern}
+        dom = max(kern, key=lambda k: stage_avg[kern[k]])
+        total_flops = sum(fl.values())
+        traffic = None
+        tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+        if os.path.exists(tpath):
+            try:
+                tr = json.load(open(tpath))
+                traffic = tr.get(f"config{cid}", {}).get(dom)
+            except Exception:
+                traffic = None
+        cpu = None
+        if not args.no_cpu_baseline:
+            v, cores, ns, dt = cpu_oracle_sample(w, args.cpu_seconds)
+            cpu = {"value": v, "unit": "points/s", "cores": cores, "kind": "oracle",
+                   "sample": f"oracle (C, OpenMP, {cores} threads) on the first {ns} points of the same workload "
+                             f"(same Z, theta, m, m_v; neighbours are predecessors so the prefix is self-contained); "
+                             f"{dt:.1f} s"}
+        out = {
+            "metric": METRIC,
+            "value": w.n / (ms_max * 1e-3),
+            "unit": "points/s",
+            "n_gpus": world,
+            "steps": args.steps,
+            "warmup": args.warmup,
+            "ms_per_step": ms_max,
+            "higher_is_better": True,
+            "scaling": "strong",
+            "vs_baseline": None,
+            "dtype": "f64",
+            "data": "synthetic (seeded; BASELINE.json configs recipe, see DESIGN.md)",
+            "config": dict(describe(w, cid), parallelism=f"rows chunk-cyclic over {world} GPU(s); U all-gather + "
+                                                          f"Gram all-reduce (NCCL)" if world > 1 else "single GPU"),
+            "roofline": {"bound": "tensor", "kernel": kern[dom], "achieved": achieved[dom], "peak": FP64_PEAK_TFLOPS,
+                         "unit": "TFLOP/s", "frac": achieved[dom] / FP64_PEAK_TFLOPS, "traffic": traffic,
+                         "peak_source": "measured FP64 DMMA peak on this pool's B200 (tools/microbench_fp64.cu; "
+                                        "MEASURED_PEAKS.json has no FP64 entry); cuBLAS DGEMM 35.5",
+                         "flops_per_launch": fl_launch[dom], "avg_launch_ms": stage_avg[kern[dom]],
+                         "per_kernel": {k: {"stage": kern[k], "avg_ms": stage_avg[kern[k]], "tflops": achieved[k],
+                                            "frac": achieved[k] / FP64_PEAK_TFLOPS} for k in kern},
+                         "path_effective_tflops": total_flops / (ms_max * 1e-3) / 1e12 / 1.0,
+                         "path_frac": total_flops / (ms_max * 1e-3) / 1e12 / FP64_PEAK_TFLOPS},
+            "cpu_baseline": cpu,
+            "e2e": {"value": w.n / (e2e_ms * 1e-3), "unit": "points/s", "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms,
+                    "note": "vif_set_data from pinned host X, Z, nbr, y (+ processing-order sort) + vif_factor + "
+                            "vif_nll (terms read back)"},
+            "clocks": sampler.summary(),
+            "gpu_launches": launches_per_step * args.steps,
+            "stages_ms_per_step": stage_avg,
+            "nll": last.nll,
+            "input_generation_s": {"total": gen_s, **{k: round(v, 3) for k, v in w.timings.items()}},
+            "create_s": create_s,
+        }
+        print(json.dumps(out), flush=True)
+    model.close()
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def run_reference(args, w, cid, world, gen_s):
+    """--impl reference: the oracle, as it stands, on the host cores; each step a bounded prefix sample."""
+    import oracle
+    th = oracle.Theta(**w.theta_dict())
+    # size the sample so one step takes ~ (150 s / (steps + warmup)) of CPU time, at most 10 s
+    per_step = min(10.0, 150.0 / max(1, args.steps + args.warmup))
+    ns = min(w.n, 4000)
+    t = time.perf_counter()
+    oracle.factor_nll(w.X[:ns], w.Z, w.nbr[:ns], w.y[:ns], th, want_BD=False)
+    dt = time.perf_counter() - t
+    ns = int(min(w.n, max(ns, ns * per_step / max(dt, 1e-3))))
+    for _ in range(args.warmup):
+        oracle.factor_nll(w.X[:ns], w.Z, w.nbr[:ns], w.y[:ns], th, want_BD=False)
+    t = time.perf_counter()
+    for _ in range(args.steps):
+        r = oracle.factor_nll(w.X[:ns], w.Z, w.nbr[:ns], w.y[:ns], th, want_BD=False)
+    dt = (time.perf_counter() - t) / args.steps
+    v = ns / dt
+    cores = oracle.num_threads()
+    sample = (f"oracle (C, OpenMP, {cores} threads) on the first {ns} of the {w.n} points of the same workload "
+              f"(same Z, theta, m, m_v), {dt:.2f} s per step")
+    out = {"impl": "reference", "metric": METRIC, "value": v, "unit": "points/s", "n_gpus": world,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
+           "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+           "data": "synthetic (seeded; BASELINE.json configs recipe, see DESIGN.md)",
+           "config": dict(describe(w, cid), parallelism="CPU oracle (host cores)"),
+           "cpu_baseline": {"value": v, "unit": "points/s", "cores": cores, "kind": "oracle", "sample": sample},
+           "e2e": {"value": v, "unit": "points/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+           "nll_sample": r.nll, "input_generation_s": gen_s}
+    print(json.dumps(out), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -135,6 +135,16 @@ int vif_copy_U(void* handle, double* out);
 /* Number of GPU kernel launches the last vif_factor + vif_nll pair enqueued (for bench.py). */
 int vif_launch_count(void* handle, int64_t* count);
 
+/* Per-stage device timing (CUDA events recorded on the handle's stream around each stage; adds
+ * no synchronisation).  Stages: see vif_stage_name(0 .. VIF_NUM_STAGES-1).  vif_profile(h, 1)
+ * enables and zeroes the accumulators; every vif_nll then adds the elapsed milliseconds of each
+ * stage of that evaluation; vif_stage_times copies the VIF_NUM_STAGES cumulative sums and the
+ * number of evaluations accumulated. */
+#define VIF_NUM_STAGES 8
+int vif_profile(void* handle, int32_t enable);
+int vif_stage_times(void* handle, double* ms_out, int64_t* evaluations);
+const char* vif_stage_name(int32_t stage);
+
 /* Text of the last error on this handle (or of the last failed vif_create when handle is NULL). */
 const char* vif_last_error(void* handle);
 

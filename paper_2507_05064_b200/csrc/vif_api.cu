@@ -163,6 +163,12 @@ Layout make_layout(const Plan& P) {
   return L;
 }
 
+enum Stage { S_KM = 0, S_UFEAT, S_GATHER, S_VECCHIA, S_SYRK, S_REDUCE, S_CHOLM, S_FINISH, S_COUNT };
+const char* kStageNames[S_COUNT] = {
+    "K0 K_m + chol/inv (cooperative)", "K1 U features (kx_eval + gemm_tn)", "A2 U all-gather (NCCL)",
+    "K2+K3 vecchia rows (gather + DMMA Gram + chol + W row)", "K4 syrk (DMMA split-K + reduce)",
+    "A6/A7 sum log D + all-reduce", "K5 chol/inv of M (cooperative)", "K5 finish (z, quad, NLL)"};
+
 struct Handle {
   Plan P;
   Layout L;
@@ -176,6 +182,20 @@ struct Handle {
   std::string err;
   int64_t launches = 0;
   std::vector<const int64_t*> order;  // per (logical) rank
+  // profiling
+  bool prof = false;
+  cudaEvent_t ev[S_COUNT][2] = {};
+  bool ev_used[S_COUNT] = {};
+  double stage_ms[S_COUNT] = {};
+  int64_t prof_evals = 0;
+
+  void mark(int stage, int which) {
+    if (!prof) return;
+    if (!ev[stage][which]) cudaEventCreate(&ev[stage][which]);
+    if (which == 0 && ev_used[stage]) return;  // keep the first begin of a multi-part stage
+    cudaEventRecord(ev[stage][which], stream);
+    if (which == 0) ev_used[stage] = true;
+  }
 
   template <typename T>
   T* buf(Buf b) const { return reinterpret_cast<T*>(base + L.off[b]); }
@@ -396,9 +416,11 @@ int vif_factor(void* handle, const vif_theta* theta, double* B_out, double* D_ou
   cudaStream_t s = h->stream;
   DevStatus* st = h->buf<DevStatus>(B_STATUS);
   int64_t nl = 0;
+  for (int k = 0; k < S_COUNT; ++k) h->ev_used[k] = false;
   VIF_CUDA(h, launch_reset_status(st, s), "reset status");
   ++nl;
   // A0: K_m, L_m, L_m^{-1}
+  h->mark(S_KM, 0);
   if (P.m > 0) {
     VIF_CUDA(h, launch_build_km(h->buf<double>(B_Z), P.m, p, h->buf<double>(B_KM), s), "build K_m");
     VIF_CUDA(h, cudaMemsetAsync(h->buf<double>(B_LINV), 0, h->L.size[B_LINV], s), "memset Linv");
@@ -407,8 +429,10 @@ int vif_factor(void* handle, const vif_theta* theta, double* B_out, double* D_ou
              "chol K_m");
     nl += 2;
   }
+  h->mark(S_KM, 1);
   // A1 (+A2): U rows per (logical) rank
   const int nrep = P.emulate ? P.world : 1;
+  h->mark(S_UFEAT, 0);
   for (int g = 0; g < nrep; ++g) {
     const int rank = P.emulate ? g : P.rank;
     VIF_CUDA(h, launch_u_features(h->buf<double>(B_X), h->buf<double>(B_Z), h->buf<double>(B_Y), P.n, P.npos, P.chunk,
@@ -417,6 +441,8 @@ int vif_factor(void* handle, const vif_theta* theta, double* B_out, double* D_ou
              "U features");
     nl += P.mk > 0 ? 2 : 1;
   }
+  h->mark(S_UFEAT, 1);
+  h->mark(S_GATHER, 0);
   if (P.world > 1 && !P.emulate) {
     Nccl& N = nccl();
     const size_t cnt = (size_t)P.chunk * P.ld;
@@ -432,6 +458,7 @@ int vif_factor(void* handle, const vif_theta* theta, double* B_out, double* D_ou
     ncclResult_t rr = N.GroupEnd();
     if (rr != ncclSuccess) return fail(h, VIF_ERR_NCCL, std::string("ncclGroupEnd: ") + N.GetErrorString(rr));
   }
+  h->mark(S_GATHER, 1);
   // A3-A6 per (logical) rank
   const size_t gstride = (size_t)P.ld * P.ld + 8;
   for (int g = 0; g < nrep; ++g) {
@@ -454,10 +481,15 @@ int vif_factor(void* handle, const vif_theta* theta, double* B_out, double* D_ou
     a.B_out = B_out;
     a.D_out = D_out;
     a.st = st;
+    h->mark(S_VECCHIA, 0);
     VIF_CUDA(h, launch_vecchia(a, s), "vecchia");
+    h->mark(S_VECCHIA, 1);
     double* G = h->buf<double>(B_G) + g * gstride;
+    h->mark(S_SYRK, 0);
     VIF_CUDA(h, launch_syrk(h->buf<double>(B_W), P.ld, npts, P.ld, P.nsplit, h->buf<double>(B_GPART), G, P.ld, s),
              "syrk");
+    h->mark(S_SYRK, 1);
+    h->mark(S_REDUCE, 0);
     VIF_CUDA(h, launch_logd_sum(h->buf<double>(B_DPOS), npts, h->buf<double>(B_PART), kLogdParts,
                                 G + (size_t)P.ld * P.ld, s),
              "logd");
@@ -475,6 +507,7 @@ int vif_factor(void* handle, const vif_theta* theta, double* B_out, double* D_ou
     ncclResult_t rr = N.AllReduce(G, G, (size_t)P.ld * P.ld + 1, ncclFloat64, ncclSum, h->comm, s);
     if (rr != ncclSuccess) return fail(h, VIF_ERR_NCCL, std::string("ncclAllReduce: ") + N.GetErrorString(rr));
   }
+  h->mark(S_REDUCE, 1);
   h->factored = true;
   h->finished = false;
   h->launches = nl;
@@ -495,15 +528,19 @@ int vif_nll(void* handle, vif_terms* out) {
   DevStatus* st = h->buf<DevStatus>(B_STATUS);
   double* G = P.emulate ? h->buf<double>(B_GSUM) : h->buf<double>(B_G);
   int64_t nl = 0;
+  h->mark(S_CHOLM, 0);
   if (P.m > 0) {
     VIF_CUDA(h, cudaMemsetAsync(h->buf<double>(B_LINVM), 0, h->L.size[B_LINVM], s), "memset LinvM");
     VIF_CUDA(h, launch_chol_inv(G, P.m, P.ld, 1.0, h->buf<double>(B_LINVM), P.mk, P.mk, &st->m_fail, h->num_sms, s),
              "chol M");
     ++nl;
   }
+  h->mark(S_CHOLM, 1);
   double* terms = h->buf<double>(B_TERMS);
+  h->mark(S_FINISH, 0);
   VIF_CUDA(h, launch_finish(G, P.ld, P.m, P.ycol, h->buf<double>(B_LINVM), P.mk, G + (size_t)P.ld * P.ld, P.n, terms, s),
            "finish");
+  h->mark(S_FINISH, 1);
   ++nl;
   h->launches += nl;
   double ht[4];
@@ -511,6 +548,14 @@ int vif_nll(void* handle, vif_terms* out) {
   VIF_CUDA(h, cudaMemcpyAsync(ht, terms, sizeof(ht), cudaMemcpyDeviceToHost, s), "terms copy");
   VIF_CUDA(h, cudaMemcpyAsync(&hs, st, sizeof(hs), cudaMemcpyDeviceToHost, s), "status copy");
   VIF_CUDA(h, cudaStreamSynchronize(s), "sync");
+  if (h->prof) {
+    for (int k = 0; k < S_COUNT; ++k) {
+      if (!h->ev_used[k]) continue;
+      float ms = 0.f;
+      if (cudaEventElapsedTime(&ms, h->ev[k][0], h->ev[k][1]) == cudaSuccess) h->stage_ms[k] += ms;
+    }
+    ++h->prof_evals;
+  }
   vif_terms t;
   t.nll = ht[0];
   t.logdet_D = ht[1];
@@ -555,6 +600,25 @@ int vif_launch_count(void* handle, int64_t* count) {
   return VIF_OK;
 }
 
+int vif_profile(void* handle, int32_t enable) {
+  Handle* h = reinterpret_cast<Handle*>(handle);
+  if (!h) return fail(nullptr, VIF_ERR_INVALID_ARG, "handle is NULL");
+  h->prof = enable != 0;
+  for (int k = 0; k < S_COUNT; ++k) h->stage_ms[k] = 0.0;
+  h->prof_evals = 0;
+  return VIF_OK;
+}
+
+int vif_stage_times(void* handle, double* ms_out, int64_t* evaluations) {
+  Handle* h = reinterpret_cast<Handle*>(handle);
+  if (!h || !ms_out) return fail(h, VIF_ERR_INVALID_ARG, "NULL argument");
+  for (int k = 0; k < S_COUNT; ++k) ms_out[k] = h->stage_ms[k];
+  if (evaluations) *evaluations = h->prof_evals;
+  return VIF_OK;
+}
+
+const char* vif_stage_name(int32_t stage) { return stage >= 0 && stage < S_COUNT ? kStageNames[stage] : ""; }
+
 const char* vif_last_error(void* handle) {
   Handle* h = reinterpret_cast<Handle*>(handle);
   return h ? h->err.c_str() : g_create_error.c_str();
@@ -564,6 +628,9 @@ void vif_destroy(void* handle) {
   Handle* h = reinterpret_cast<Handle*>(handle);
   if (!h) return;
   if (h->comm) nccl().CommDestroy(h->comm);
+  for (int k = 0; k < S_COUNT; ++k)
+    for (int j = 0; j < 2; ++j)
+      if (h->ev[k][j]) cudaEventDestroy(h->ev[k][j]);
   delete h;
 }
 

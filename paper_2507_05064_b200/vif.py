@@ -71,17 +71,23 @@ def load_library():
         lib.vif_launch_count.argtypes = [P, ctypes.POINTER(i64)]
         lib.vif_last_error.argtypes = [P]
         lib.vif_last_error.restype = ctypes.c_char_p
+        lib.vif_profile.argtypes = [P, i32]
+        lib.vif_stage_times.argtypes = [P, P, ctypes.POINTER(i64)]
+        lib.vif_stage_name.argtypes = [i32]
+        lib.vif_stage_name.restype = ctypes.c_char_p
         lib.vif_destroy.argtypes = [P]
         lib.vif_destroy.restype = None
         for f in ("vif_nccl_unique_id", "vif_workspace_bytes", "vif_partition", "vif_create", "vif_set_data",
-                  "vif_factor", "vif_nll", "vif_copy_U", "vif_launch_count"):
+                  "vif_factor", "vif_nll", "vif_copy_U", "vif_launch_count", "vif_profile", "vif_stage_times"):
             getattr(lib, f).restype = ctypes.c_int
         _lib = lib
     return _lib
 
 
 EXPORTED = ("vif_nccl_unique_id", "vif_workspace_bytes", "vif_partition", "vif_create", "vif_set_data",
-            "vif_factor", "vif_nll", "vif_copy_U", "vif_launch_count", "vif_last_error", "vif_destroy")
+            "vif_factor", "vif_nll", "vif_copy_U", "vif_launch_count", "vif_profile", "vif_stage_times",
+            "vif_stage_name", "vif_last_error", "vif_destroy")
+NUM_STAGES = 8
 
 
 def _check(st: int, handle=None, bad_row: int = -1):
@@ -210,6 +216,22 @@ def vif_launch_count(h) -> int:
     return int(c.value)
 
 
+def vif_profile(h, enable: bool = True):
+    _check(load_library().vif_profile(h, int(enable)), h)
+
+
+def vif_stage_times(h):
+    """(list of cumulative ms per stage, evaluations accumulated)"""
+    arr = (ctypes.c_double * NUM_STAGES)()
+    ev = ctypes.c_int64(0)
+    _check(load_library().vif_stage_times(h, arr, ctypes.byref(ev)), h)
+    return list(arr), int(ev.value)
+
+
+def vif_stage_name(i: int) -> str:
+    return load_library().vif_stage_name(int(i)).decode()
+
+
 def vif_last_error(h=None) -> str:
     return load_library().vif_last_error(h).decode(errors="replace")
 
@@ -262,6 +284,13 @@ class VifModel:
 
     def owned_rows(self, rank=None) -> np.ndarray:
         return owned_rows(self.n, self.rank if rank is None else rank, self.world, self.rounds, self.chunk)
+
+    def profile(self, enable: bool = True):
+        vif_profile(self.handle, enable)
+
+    def stage_times(self):
+        ms, ev = vif_stage_times(self.handle)
+        return {vif_stage_name(i): v for i, v in enumerate(ms)}, ev
 
     def launch_count(self) -> int:
         return vif_launch_count(self.handle)
