@@ -30,16 +30,37 @@ struct CovParams {
 
 enum { FAM_M12 = 0, FAM_M32 = 1, FAM_M52 = 2, FAM_GAUSS = 3 };
 
+// 1/sqrt(x) for x > 0: MUFU.RSQ64H seed + two Newton steps (relative error ~1 ulp).  Inline: the
+// libdevice sqrt/div/rsqrt carry an out-of-line slow path whose CALL forces register spills in
+// the unrolled per-point Cholesky.  x <= 0 gives NaN/inf, which the callers test for.
+__device__ __forceinline__ double rsqrt_nr(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  double r = fma(-x * y, y, 1.0);
+  y = fma(0.5 * y, r, y);
+  r = fma(-x * y, y, 1.0);
+  return fma(0.5 * y, r, y);
+}
+
+__device__ __forceinline__ double sqrt_nr(double x) { return x > 0.0 ? x * rsqrt_nr(x) : 0.0; }
+
+// single-precision approximate square root (MUFU.SQRT, no slow path) for index arithmetic
+__device__ __forceinline__ float sqrtf_fast(float x) {
+  float y;
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
 // f(r) as a function of r^2 (reading c1)
 template <int FAM>
 __device__ __forceinline__ double cov_f(double r2) {
   if (FAM == FAM_M12) {
-    return exp(-sqrt(r2));
+    return exp(-sqrt_nr(r2));
   } else if (FAM == FAM_M32) {
-    const double t = 1.7320508075688772 * sqrt(r2);
+    const double t = 1.7320508075688772 * sqrt_nr(r2);
     return (1.0 + t) * exp(-t);
   } else if (FAM == FAM_M52) {
-    const double t = 2.23606797749979 * sqrt(r2);
+    const double t = 2.23606797749979 * sqrt_nr(r2);
     return (1.0 + t + (5.0 / 3.0) * r2) * exp(-t);
   } else {
     return exp(-r2);

@@ -17,6 +17,7 @@
 // B_out[i] = -A_i (reading c16) and D_out[i].
 #include "common.cuh"
 #include "kernels.h"
+#include <stdlib.h>
 
 namespace vif {
 
@@ -28,7 +29,7 @@ __host__ __device__ constexpr int vecchia_warp_doubles() {
 }
 
 template <int FAM, int RB, int NB>
-__global__ void __launch_bounds__(VW * 32) vecchia_kernel(
+__global__ void __launch_bounds__(VW * 32) vecchia_smem_kernel(
     const double* __restrict__ U, int64_t ldu, int mk, int ld, const double* __restrict__ X,
     const int32_t* __restrict__ nbr, int mv, const int64_t* __restrict__ order, int64_t npts, CovParams p,
     double* __restrict__ W, int64_t ldw, double* __restrict__ Dpos, double* __restrict__ B_out,
@@ -211,21 +212,258 @@ __global__ void __launch_bounds__(VW * 32) vecchia_kernel(
   }
 }
 
+
+// ------------------------------------------------------------------------------------------
+// Register variant for s <= 32 (RB <= 4): the same five steps with the per-point scalar work
+// reorganised so that it does not starve the DMMA pipe of the other resident warps:
+//   - the s(s+1)/2 kernel evaluations are spread evenly over the lanes (flat lower-triangle
+//     index), with the conditioning-set coordinates staged in shared memory;
+//   - the Cholesky keeps row `lane` in registers (compile-time indexed, fully unrolled); column j
+//     is broadcast through shared memory (double-buffered), so step j costs one store and
+//     SP - j broadcast loads + FMAs per lane;
+//   - the back substitution uses a shuffle per step;
+//   - the W pass issues all s row loads of a 64-column chunk before the FMAs.
+template <int RB>
+__host__ __device__ constexpr int vreg_warp_doubles(int d) {
+  return RB * 8 * (RB * 8 + 1) + 2 * RB * 8 + RB * 8 + RB * 8 * d;  // C, colbuf[2], coef, xs
+}
+
+template <int FAM, int RB, int NB, int MINB>
+__global__ void __launch_bounds__(VW * 32, MINB) vecchia_reg_kernel(
+    const double* __restrict__ U, int64_t ldu, int mk, int ld, const double* __restrict__ X,
+    const int32_t* __restrict__ nbr, int mv, const int64_t* __restrict__ order, int64_t npts, CovParams p,
+    double* __restrict__ W, int64_t ldw, double* __restrict__ Dpos, double* __restrict__ B_out,
+    double* __restrict__ D_out, DevStatus* __restrict__ st) {
+  constexpr int SP = RB * 8;
+  constexpr int CS = SP + 1;
+  constexpr int NT = RB * (RB + 1) / 2;
+  static_assert(SP <= 32, "register variant needs s <= 32");
+  extern __shared__ __align__(16) double vsm[];
+  __shared__ int Sidx_all[VW][SP];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double* C = vsm + warp * vreg_warp_doubles<RB>(p.d);
+  double* colbuf = C + SP * CS;   // [2][SP]
+  double* coef = colbuf + 2 * SP; // [SP]
+  double* xs = coef + SP;         // [SP][d]
+  int* Sidx = Sidx_all[warp];
+  const int64_t pos = (int64_t)blockIdx.x * VW + warp;
+  if (pos >= npts) return;
+  const int64_t i = order[pos];
+
+  // ---- conditioning set and its coordinates ----
+  const int nb0 = lane < mv ? nbr[i * mv + lane] : -1;
+  const int q = __popc(__ballot_sync(0xffffffffu, nb0 >= 0));
+  const int s = q + 1;
+  const int myidx = lane < q ? nb0 : (lane == q ? (int)i : -1);
+  if (lane < SP) Sidx[lane] = myidx;
+  if (lane < s)
+    for (int k = 0; k < p.d; ++k) xs[lane * p.d + k] = X[(int64_t)myidx * p.d + k];
+  __syncwarp();
+
+  // ---- 1. Gram on DMMA (identical to the shared-memory variant) ----
+  double acc[NT][2];
+#pragma unroll
+  for (int t = 0; t < NT; ++t) acc[t][0] = acc[t][1] = 0.0;
+  const double* rp[RB];
+#pragma unroll
+  for (int R = 0; R < RB; ++R) {
+    const int gi = Sidx[R * 8 + (lane >> 2)];
+    rp[R] = gi >= 0 ? U + (int64_t)gi * ldu + 2 * (lane & 3) : nullptr;
+  }
+  double2 f[NB][RB];
+  auto load = [&](int k0) {
+#pragma unroll
+    for (int b = 0; b < NB; ++b)
+#pragma unroll
+      for (int R = 0; R < RB; ++R) {
+        const int k = k0 + b * 8;
+        f[b][R] = (rp[R] != nullptr && k < mk) ? __ldg(reinterpret_cast<const double2*>(rp[R] + k))
+                                               : make_double2(0.0, 0.0);
+      }
+  };
+  if (mk > 0) load(0);
+  for (int k0 = 0; k0 < mk; k0 += 8 * NB) {
+    double2 g[NB][RB];
+#pragma unroll
+    for (int b = 0; b < NB; ++b)
+#pragma unroll
+      for (int R = 0; R < RB; ++R) g[b][R] = f[b][R];
+    if (k0 + 8 * NB < mk) load(k0 + 8 * NB);
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+      int t = 0;
+#pragma unroll
+      for (int R1 = 0; R1 < RB; ++R1)
+#pragma unroll
+        for (int R2 = 0; R2 <= R1; ++R2, ++t) dmma884(acc[t][0], acc[t][1], g[b][R1].x, g[b][R2].x);
+      t = 0;
+#pragma unroll
+      for (int R1 = 0; R1 < RB; ++R1)
+#pragma unroll
+        for (int R2 = 0; R2 <= R1; ++R2, ++t) dmma884(acc[t][0], acc[t][1], g[b][R1].y, g[b][R2].y);
+    }
+  }
+  // Gram tiles -> shared memory
+  {
+    int t = 0;
+#pragma unroll
+    for (int R1 = 0; R1 < RB; ++R1)
+#pragma unroll
+      for (int R2 = 0; R2 <= R1; ++R2, ++t) {
+        const int r = R1 * 8 + (lane >> 2), c = R2 * 8 + 2 * (lane & 3);
+        C[r * CS + c] = acc[t][0];
+        C[r * CS + c + 1] = acc[t][1];
+      }
+  }
+  __syncwarp();
+
+  // ---- 2. C_S = K(X_S, X_S) - G_S + sigma^2 I on the lower triangle, evenly over lanes ----
+  const int ne = s * (s + 1) / 2;
+  for (int e = lane; e < ne; e += 32) {
+    int r = (int)((sqrtf_fast(8.0f * (float)e + 1.0f) - 1.0f) * 0.5f);
+    if ((r + 1) * (r + 2) / 2 <= e) ++r;
+    if (r * (r + 1) / 2 > e) --r;
+    const int c = e - r * (r + 1) / 2;
+    double v = cov<FAM>(xs + r * p.d, xs + c * p.d, p) - C[r * CS + c];
+    if (r == c) v += p.nugget;
+    C[r * CS + c] = v;
+  }
+  __syncwarp();
+
+  // ---- 3. Cholesky, row `lane` in registers; padded rows (>= s) are identity ----
+  double crow[SP];
+#pragma unroll
+  for (int c = 0; c < SP; ++c) {
+    double v = 0.0;
+    if (lane < s) {
+      if (c <= lane) v = C[lane * CS + c];
+    } else if (c == lane) {
+      v = 1.0;
+    }
+    crow[c] = v;
+  }
+  bool ok = true;
+  double Di = 0.0, myinv = 1.0;
+#pragma unroll
+  for (int j = 0; j < SP; ++j) {
+    const double djj = __shfl_sync(0xffffffffu, crow[j], j);
+    if (j < s) {
+      ok = ok && (djj > 0.0);
+      if (j == s - 1) Di = djj;
+    }
+    // one inline reciprocal square root per step (no out-of-line div/sqrt subroutines):
+    // lane j gets djj / sqrt(djj) = l_jj, lanes below get l_rj = c_rj / l_jj
+    const double y = rsqrt_nr(djj);
+    const double lrj = crow[j] * y;
+    crow[j] = lrj;
+    if (lane == j) myinv = y;
+    if (j + 1 < SP) {
+      double* cb = colbuf + (j & 1) * SP;
+      if (lane < SP) cb[lane] = lrj;
+      __syncwarp();
+#pragma unroll
+      for (int c = j + 1; c < SP; ++c) crow[c] = fma(-lrj, cb[c], crow[c]);
+    }
+  }
+  if (!ok) {
+    if (lane == 0) atomicMin(&st->bad_row, (unsigned long long)i);
+    for (int c = 2 * lane; c < ld; c += 64) *reinterpret_cast<double2*>(W + pos * ldw + c) = make_double2(0.0, 0.0);
+    if (lane == 0) {
+      Dpos[pos] = 1.0;
+      if (D_out) D_out[i] = __longlong_as_double(0x7ff8000000000000LL);
+    }
+    return;
+  }
+  // rows of L to shared memory (row-major) for the back substitution
+#pragma unroll
+  for (int c = 0; c < SP; ++c)
+    if (lane < SP) C[lane * CS + c] = crow[c];
+  __syncwarp();
+
+  // ---- 4. A_i^T = L_NN^{-T} l, l = row q of L; lane k holds x_k ----
+  {
+    const double inv_diag = myinv;  // 1 / own diagonal
+    double a = lane < q ? C[q * CS + lane] : 0.0;
+    for (int j = q - 1; j >= 0; --j) {
+      const double xj = __shfl_sync(0xffffffffu, a * inv_diag, j);
+      if (lane == j) a = xj;
+      else if (lane < j) a = fma(-C[j * CS + lane], xj, a);
+    }
+    const double rs = rsqrt_nr(Di);
+    // coefficients of the W row: -A_ik / sqrt(D) for k < q, 1 / sqrt(D) for i itself, 0 beyond
+    if (lane < SP) coef[lane] = lane < q ? -a * rs : (lane == q ? rs : 0.0);
+    if (B_out && lane < mv) B_out[i * mv + lane] = lane < q ? -a : 0.0;
+  }
+  __syncwarp();
+
+  // ---- 5. w_i, r_i over ld columns: 512 columns per pass (8 chunks of 64 per lane-pair),
+  //         rows two at a time -> 16 independent 16-byte loads in flight per lane ----
+  for (int c0 = 0; c0 < ld; c0 += 512) {
+    double2 o[8];
+#pragma unroll
+    for (int t = 0; t < 8; ++t) o[t] = make_double2(0.0, 0.0);
+    for (int k = 0; k < s; k += 2) {
+      double2 u0[8], u1[8];
+      const double* r0 = U + (int64_t)Sidx[k] * ldu + c0 + 2 * lane;
+      const bool has1 = k + 1 < s;
+      const double* r1 = has1 ? U + (int64_t)Sidx[k + 1] * ldu + c0 + 2 * lane : r0;
+#pragma unroll
+      for (int t = 0; t < 8; ++t) {
+        const bool in = c0 + 2 * lane + 64 * t < ld;
+        u0[t] = in ? __ldg(reinterpret_cast<const double2*>(r0 + 64 * t)) : make_double2(0.0, 0.0);
+        u1[t] = (in && has1) ? __ldg(reinterpret_cast<const double2*>(r1 + 64 * t)) : make_double2(0.0, 0.0);
+      }
+      const double f0 = coef[k], f1 = has1 ? coef[k + 1] : 0.0;
+#pragma unroll
+      for (int t = 0; t < 8; ++t) {
+        o[t].x = fma(f0, u0[t].x, o[t].x);
+        o[t].y = fma(f0, u0[t].y, o[t].y);
+        o[t].x = fma(f1, u1[t].x, o[t].x);
+        o[t].y = fma(f1, u1[t].y, o[t].y);
+      }
+    }
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      const int c = c0 + 2 * lane + 64 * t;
+      if (c < ld) *reinterpret_cast<double2*>(W + pos * ldw + c) = o[t];
+    }
+  }
+  if (lane == 0) {
+    Dpos[pos] = Di;
+    if (D_out) D_out[i] = Di;
+  }
+}
+
 template <int FAM, int RB>
 static cudaError_t launch_rb(const VecchiaArgs& a, cudaStream_t s) {
   constexpr int NB = RB <= 4 ? 2 : 1;
-  const size_t smem = (size_t)VW * vecchia_warp_doubles<RB>() * sizeof(double);
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(vecchia_kernel<FAM, RB, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
   const unsigned blocks = (unsigned)((a.npts + VW - 1) / VW);
-  vecchia_kernel<FAM, RB, NB><<<blocks, VW * 32, smem, s>>>(a.U, a.ldu, a.mk, a.ld, a.X, a.nbr, a.mv, a.order,
-                                                            a.npts, a.p, a.W, a.ldw, a.Dpos, a.B_out, a.D_out,
-                                                            a.st);
+  if constexpr (RB <= 4) {
+    const size_t smem = (size_t)VW * vreg_warp_doubles<RB>(a.p.d) * sizeof(double);
+    static const char* occ_env = getenv("VIF_VREG_MINB");
+    const bool three = occ_env && occ_env[0] == '3';
+    auto kern = three ? vecchia_reg_kernel<FAM, RB, NB, 3> : vecchia_reg_kernel<FAM, RB, NB, 4>;
+    static size_t attr[2] = {0, 0};
+    if (attr[three] < smem) {
+      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return e;
+      attr[three] = smem;
+    }
+    kern<<<blocks, VW * 32, smem, s>>>(a.U, a.ldu, a.mk, a.ld, a.X, a.nbr, a.mv, a.order, a.npts, a.p, a.W, a.ldw,
+                                       a.Dpos, a.B_out, a.D_out, a.st);
+  } else {
+    const size_t smem = (size_t)VW * vecchia_warp_doubles<RB>() * sizeof(double);
+    static bool attr = false;
+    if (!attr) {
+      cudaError_t e = cudaFuncSetAttribute(vecchia_smem_kernel<FAM, RB, NB>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return e;
+      attr = true;
+    }
+    vecchia_smem_kernel<FAM, RB, NB><<<blocks, VW * 32, smem, s>>>(a.U, a.ldu, a.mk, a.ld, a.X, a.nbr, a.mv,
+                                                                   a.order, a.npts, a.p, a.W, a.ldw, a.Dpos,
+                                                                   a.B_out, a.D_out, a.st);
+  }
   return cudaGetLastError();
 }
 
