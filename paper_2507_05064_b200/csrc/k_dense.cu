@@ -5,10 +5,15 @@
 //       logdet M_w = 2 sum log (L_M)_jj;  NLL = n/2 log 2pi + (sum log D + logdet M_w + quad)/2
 //
 //
-// Both factorizations use one cooperative persistent kernel (one CTA per SM, grid-wide sync
-// between the phases of a right-looking blocked Cholesky with 32x32 tiles, then a wavefront
-// over the tile diagonals for the triangular inverse).  These are O(m^3/3) once per
-// evaluation: 4e7 flops at m = 500, 1.1e9 at m = 1500 -- < 1% of the O(n m^2) work.
+// chol_inv_kernel: one cooperative persistent kernel (grid = SMs), 32 x 32 tiles, right-looking:
+//   per panel k: (A) one warp factors the diagonal tile in registers (row per lane, column
+//   broadcast through shared memory, inline rsqrt) and inverts it (column-oriented substitution);
+//   (B) L_ik = A_ik inv(L_kk)^T for i > k; (C) trailing update A_ij -= L_ik L_jk^T; grid sync between.
+//   If the inverse is wanted (K0 only), it is completed by recursive doubling over the tile grid:
+//   inv([[P,0],[C,Q]]) = [[P^-1, 0], [-Q^-1 C P^-1, Q^-1]] with block sizes 1, 2, 4, ... tiles,
+//   two fully parallel GEMM steps per level (log2(m/32) levels) instead of a sequential wavefront.
+// K5 needs only the diagonal-tile inverses (they drive the blocked forward solve in finish_kernel).
+// These are O(m^3/3) once per evaluation: 4e7 flops at m = 500.
 #include <cooperative_groups.h>
 
 #include "common.cuh"
@@ -22,13 +27,6 @@ namespace {
 
 constexpr int TB = 32;  // tile size
 
-// element (r, c) of the symmetric input (lower part stored), identity beyond m
-__device__ __forceinline__ double ld_sym(const double* A, int lda, int m, int r, int c, double diag_add) {
-  if (r < m && c < m) return __ldcg(A + (size_t)r * lda + c) + (r == c ? diag_add : 0.0);
-  return r == c ? 1.0 : 0.0;
-}
-
-// load tile (ti, tj) of a lower-stored matrix into smem, zero beyond `lim`
 __device__ __forceinline__ void load_tile(double (*T)[TB + 1], const double* A, int lda, int lim, int ti, int tj) {
   for (int e = threadIdx.x; e < TB * TB; e += blockDim.x) {
     const int r = e / TB, c = e % TB;
@@ -41,7 +39,7 @@ __device__ __forceinline__ void store_tile(const double (*T)[TB + 1], double* A,
   for (int e = threadIdx.x; e < TB * TB; e += blockDim.x) {
     const int r = e / TB, c = e % TB;
     const int gr = ti * TB + r, gc = tj * TB + c;
-    if (gr < lim && gc < lim) A[(size_t)gr * lda + gc] = T[r][c];
+    if (gr < lim && gc < lim) __stcg(A + (size_t)gr * lda + gc, T[r][c]);
   }
 }
 
@@ -50,78 +48,103 @@ struct Smem {
   double P[TB][TB + 1];
   double Q[TB][TB + 1];
   double R[TB][TB + 1];
+  double cb[2][TB];
 };
+
+// acc[j] (rows r0 + 8j, column c) += sign * P Q^T  (TRANSB) or P Q
+template <bool TRANSB>
+__device__ __forceinline__ void tile_mac(const Smem& sm, double acc[4], int r0, int c) {
+#pragma unroll 8
+  for (int t = 0; t < TB; ++t) {
+    const double q = TRANSB ? sm.Q[c][t] : sm.Q[t][c];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[j] = fma(sm.P[r0 + 8 * j][t], q, acc[j]);
+  }
+}
+
+// warp 0: factor sm.T (lower, SPD) in place and write inv(L) into sm.P
+__device__ void factor_diag_tile(Smem& sm, int* fail) {
+  const int lane = threadIdx.x & 31;
+  double crow[TB];
+#pragma unroll
+  for (int c = 0; c < TB; ++c) crow[c] = c <= lane ? sm.T[lane][c] : 0.0;
+  bool ok = true;
+  double myinv = 1.0;
+#pragma unroll
+  for (int j = 0; j < TB; ++j) {
+    const double djj = __shfl_sync(0xffffffffu, crow[j], j);
+    ok = ok && (djj > 0.0);
+    const double y = rsqrt_nr(djj);
+    const double lrj = crow[j] * y;
+    crow[j] = lrj;
+    if (lane == j) myinv = y;
+    if (j + 1 < TB) {
+      sm.cb[j & 1][lane] = lrj;
+      __syncwarp();
+#pragma unroll
+      for (int c = j + 1; c < TB; ++c) crow[c] = fma(-lrj, sm.cb[j & 1][c], crow[c]);
+    }
+  }
+  if (!ok && lane == 0) atomicExch(fail, 1);
+#pragma unroll
+  for (int c = 0; c < TB; ++c) sm.T[lane][c] = c <= lane ? crow[c] : 0.0;
+  __syncwarp();
+  // inverse: lane = column c of X with L X = I; column-oriented forward substitution
+  double x[TB];
+#pragma unroll
+  for (int r = 0; r < TB; ++r) x[r] = r == lane ? 1.0 : 0.0;
+#pragma unroll
+  for (int q = 0; q < TB; ++q) {
+    const double inv_qq = __shfl_sync(0xffffffffu, myinv, q);
+    x[q] *= inv_qq;
+#pragma unroll
+    for (int r = q + 1; r < TB; ++r) x[r] = fma(-sm.T[r][q], x[q], x[r]);
+  }
+#pragma unroll
+  for (int r = 0; r < TB; ++r) sm.P[r][lane] = x[r];
+  __syncwarp();
+}
 
 }  // namespace
 
-// In-place Cholesky of the m x m symmetric matrix A (+ diag_add * I), lower part; writes the lower
-// triangular inverse to Linv (lim_inv x lim_inv, ld ldi, upper part left untouched: caller zeroes).
+// In-place Cholesky of the m x m symmetric matrix A (+ diag_add * I), lower part (the upper part is
+// scratch afterwards).  Linv (lim_inv x lim_inv, ld ldi, pre-zeroed by the caller) receives the
+// inverses of the diagonal tiles, and the full lower inverse when full_inverse != 0.
 // fail: set to 1 on a non-positive pivot.
 __global__ void __launch_bounds__(256) chol_inv_kernel(double* A, int m, int lda, double diag_add, double* Linv,
-                                                       int ldi, int lim_inv, int* fail) {
+                                                       int ldi, int lim_inv, int full_inverse, double* Tscr,
+                                                       int* fail) {
   cg::grid_group grid = cg::this_grid();
   __shared__ Smem sm;
   const int nt = (m + TB - 1) / TB;
   const int tid = threadIdx.x;
-  const int lane = tid & 31;
   const int c = tid & 31, r0 = tid >> 5;  // thread -> (rows r0 + 8j, col c)
 
   for (int k = 0; k < nt; ++k) {
-    // ---- phase A: factor the diagonal tile and invert it (block 0) ----
+    // ---- A: factor + invert the diagonal tile ----
     if (blockIdx.x == 0) {
       for (int e = tid; e < TB * TB; e += blockDim.x) {
         const int r = e / TB, cc = e % TB;
-        sm.T[r][cc] = cc <= r ? ld_sym(A, lda, m, k * TB + r, k * TB + cc, diag_add) : 0.0;
+        const int gr = k * TB + r, gc = k * TB + cc;
+        double v;
+        if (gr < m && gc < m) v = cc <= r ? __ldcg(A + (size_t)gr * lda + gc) + (r == cc ? diag_add : 0.0) : 0.0;
+        else v = r == cc ? 1.0 : 0.0;  // identity padding beyond m
+        sm.T[r][cc] = v;
       }
       __syncthreads();
-      if (tid < 32) {
-        for (int j = 0; j < TB; ++j) {
-          const double djj = sm.T[j][j];
-          if (!(djj > 0.0) && lane == 0) atomicExch(fail, 1);
-          const double ljj = sqrt(djj);
-          __syncwarp();
-          if (lane > j) sm.T[lane][j] /= ljj;
-          __syncwarp();
-          if (lane == j) sm.T[j][j] = ljj;
-          if (lane > j) {
-            const double lrj = sm.T[lane][j];
-            for (int cc = j + 1; cc <= lane; ++cc) sm.T[lane][cc] -= lrj * sm.T[cc][j];
-          }
-          __syncwarp();
-        }
-        // inverse of the lower-triangular tile, lane = column
-        for (int r = 0; r < TB; ++r) {
-          double v;
-          if (r < lane) {
-            v = 0.0;
-          } else if (r == lane) {
-            v = 1.0 / sm.T[r][r];
-          } else {
-            double s = 0.0;
-            for (int q = lane; q < r; ++q) s += sm.T[r][q] * sm.P[q][lane];
-            v = -s / sm.T[r][r];
-          }
-          sm.P[r][lane] = v;
-        }
-      }
+      if (tid < 32) factor_diag_tile(sm, fail);
       __syncthreads();
       store_tile(sm.T, A, lda, m, k, k);
       store_tile(sm.P, Linv, ldi, lim_inv, k, k);
-      // identity padding of Linv beyond m inside the diagonal tile is stored when lim_inv > m
     }
     grid.sync();
-    // ---- phase B: L_ik = A_ik L_kk^{-T} for i > k ----
+    // ---- B: L_ik = A_ik inv(L_kk)^T ----
     for (int i = k + 1 + blockIdx.x; i < nt; i += gridDim.x) {
       load_tile(sm.P, A, lda, m, i, k);
       load_tile(sm.Q, Linv, ldi, lim_inv, k, k);
       __syncthreads();
       double acc[4] = {0, 0, 0, 0};
-#pragma unroll 8
-      for (int t = 0; t < TB; ++t) {
-        const double q = sm.Q[c][t];
-#pragma unroll
-        for (int j = 0; j < 4; ++j) acc[j] += sm.P[r0 + 8 * j][t] * q;
-      }
+      tile_mac<true>(sm, acc, r0, c);
       __syncthreads();
 #pragma unroll
       for (int j = 0; j < 4; ++j) sm.P[r0 + 8 * j][c] = acc[j];
@@ -130,7 +153,7 @@ __global__ void __launch_bounds__(256) chol_inv_kernel(double* A, int m, int lda
       __syncthreads();
     }
     grid.sync();
-    // ---- phase C: trailing update A_ij -= L_ik L_jk^T, k < j <= i ----
+    // ---- C: trailing update A_ij -= L_ik L_jk^T, k < j <= i ----
     const int ntr = nt - k - 1;
     const int cnt = ntr * (ntr + 1) / 2;
     for (int t = blockIdx.x; t < cnt; t += gridDim.x) {
@@ -143,12 +166,7 @@ __global__ void __launch_bounds__(256) chol_inv_kernel(double* A, int m, int lda
       load_tile(sm.R, A, lda, m, i, j);
       __syncthreads();
       double acc[4] = {0, 0, 0, 0};
-#pragma unroll 8
-      for (int q = 0; q < TB; ++q) {
-        const double b = sm.Q[c][q];
-#pragma unroll
-        for (int jx = 0; jx < 4; ++jx) acc[jx] += sm.P[r0 + 8 * jx][q] * b;
-      }
+      tile_mac<true>(sm, acc, r0, c);
 #pragma unroll
       for (int jx = 0; jx < 4; ++jx) sm.R[r0 + 8 * jx][c] -= acc[jx];
       __syncthreads();
@@ -157,39 +175,50 @@ __global__ void __launch_bounds__(256) chol_inv_kernel(double* A, int m, int lda
     }
     grid.sync();
   }
-  // ---- triangular inverse, wavefront over tile diagonals t = i - j ----
-  for (int t = 1; t < nt; ++t) {
-    for (int j = blockIdx.x; j + t < nt; j += gridDim.x) {
-      const int i = j + t;
+  if (!full_inverse) return;
+  // ---- recursive doubling: blocks of 2h tiles starting at b = 2h * blk ----
+  // T = C inv(P) goes to the scratch Tscr (same shape as Linv) at tile (r, c).
+  for (int h = 1; h < nt; h *= 2) {
+    const int nblk = (nt + 2 * h - 1) / (2 * h);
+    // step 1: T_rc = sum_{q in [b, b+h)} L_rq Linv_qc   for r in [b+h, b+2h), c in [b, b+h)
+    for (int w = blockIdx.x; w < nblk * h * h; w += gridDim.x) {
+      const int blk = w / (h * h), rc = w % (h * h);
+      const int b = blk * 2 * h;
+      const int r = b + h + rc / h, cc = b + rc % h;
+      if (r >= nt) continue;
       double acc[4] = {0, 0, 0, 0};
-      for (int k = j; k < i; ++k) {
-        load_tile(sm.P, A, lda, m, i, k);          // L_ik
-        load_tile(sm.Q, Linv, ldi, lim_inv, k, j);  // Linv_kj
+      for (int q = cc; q < b + h; ++q) {  // Linv_qc = 0 for q < c
+        load_tile(sm.P, A, lda, m, r, q);
+        load_tile(sm.Q, Linv, ldi, lim_inv, q, cc);
         __syncthreads();
-#pragma unroll 8
-        for (int q = 0; q < TB; ++q) {
-          const double b = sm.Q[q][c];
-#pragma unroll
-          for (int jx = 0; jx < 4; ++jx) acc[jx] += sm.P[r0 + 8 * jx][q] * b;
-        }
+        tile_mac<false>(sm, acc, r0, c);
         __syncthreads();
       }
 #pragma unroll
       for (int jx = 0; jx < 4; ++jx) sm.R[r0 + 8 * jx][c] = acc[jx];
-      load_tile(sm.P, Linv, ldi, lim_inv, i, i);  // Linv_ii
       __syncthreads();
-      double out[4] = {0, 0, 0, 0};
-#pragma unroll 8
-      for (int q = 0; q < TB; ++q) {
-        const double b = sm.R[q][c];
-#pragma unroll
-        for (int jx = 0; jx < 4; ++jx) out[jx] -= sm.P[r0 + 8 * jx][q] * b;
+      store_tile(sm.R, Tscr, ldi, lim_inv, r, cc);
+      __syncthreads();
+    }
+    grid.sync();
+    // step 2: Linv_rc = - sum_{q in [b+h, r]} Linv_rq T_qc
+    for (int w = blockIdx.x; w < nblk * h * h; w += gridDim.x) {
+      const int blk = w / (h * h), rc = w % (h * h);
+      const int b = blk * 2 * h;
+      const int r = b + h + rc / h, cc = b + rc % h;
+      if (r >= nt) continue;
+      double acc[4] = {0, 0, 0, 0};
+      for (int q = b + h; q <= r; ++q) {
+        load_tile(sm.P, Linv, ldi, lim_inv, r, q);
+        load_tile(sm.Q, Tscr, ldi, lim_inv, q, cc);
+        __syncthreads();
+        tile_mac<false>(sm, acc, r0, c);
+        __syncthreads();
       }
-      __syncthreads();
 #pragma unroll
-      for (int jx = 0; jx < 4; ++jx) sm.R[r0 + 8 * jx][c] = out[jx];
+      for (int jx = 0; jx < 4; ++jx) sm.R[r0 + 8 * jx][c] = -acc[jx];
       __syncthreads();
-      store_tile(sm.R, Linv, ldi, lim_inv, i, j);
+      store_tile(sm.R, Linv, ldi, lim_inv, r, cc);
       __syncthreads();
     }
     grid.sync();
@@ -233,36 +262,62 @@ __global__ void sum_partials_kernel(const double* __restrict__ partials, int np,
   }
 }
 
-// Finish (after the all-reduce and the Cholesky of M_w): terms[0..3] = nll, logdetD, logdetM, quad.
-// G: lower (ld x ld) Gram with rows/cols [0,m) overwritten by L_M; row ycol holds G_Wr, G_rr.
+// Finish (after the all-reduce and the Cholesky of M_w), one CTA:
+//   z = L_M^{-1} g by blocked forward substitution (g = G_Wr = row ycol of G; the diagonal-tile
+//   inverses come from chol_inv_kernel), quad = G_rr - z.z, logdet M_w = 2 sum log L_jj, NLL.
+// terms[0..3] = nll, logdetD, logdetM, quad.
 __global__ void __launch_bounds__(1024) finish_kernel(const double* __restrict__ G, int ld, int m, int ycol,
-                                                      const double* __restrict__ LinvM, int ldi, double logdetD,
+                                                      const double* __restrict__ Dinv, int ldi,
                                                       const double* __restrict__ logdetD_dev, int64_t n,
                                                       double* __restrict__ terms) {
-  __shared__ double zsq[32];
-  __shared__ double ldm[32];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  double zs = 0.0, ls = 0.0;
-  for (int a = warp; a < m; a += 32) {
-    double acc = 0.0;
-    for (int b = lane; b <= a; b += 32) acc += LinvM[(size_t)a * ldi + b] * G[(size_t)ycol * ld + b];
+  __shared__ double z[2048];
+  __shared__ double rhs[TB];
+  __shared__ double part[32];
+  __shared__ double red[32];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int nt = (m + TB - 1) / TB;
+  for (int k = 0; k < nt; ++k) {
+    // rhs_r = g_r - sum_{c < 32k} L[r][c] z_c : warp w takes row r = 32k + w, lanes over c (coalesced)
+    const int r = k * TB + warp;
+    double s = 0.0;
+    if (r < m)
+      for (int cc = lane; cc < k * TB; cc += 32) s = fma(G[(size_t)r * ld + cc], z[cc], s);
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    zs += acc * acc;
-    if (lane == 0) ls += 2.0 * log(G[(size_t)a * ld + a]);
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) rhs[warp] = r < m ? G[(size_t)ycol * ld + r] - s : 0.0;
+    __syncthreads();
+    if (warp == 0) {
+      // z_block = inv(L_kk) rhs  (diagonal-tile inverse stored at Dinv tile (k, k))
+      const int rr = k * TB + lane;
+      double zz = 0.0;
+      if (rr < m)
+        for (int cc = 0; cc <= lane; ++cc) zz = fma(Dinv[(size_t)rr * ldi + k * TB + cc], rhs[cc], zz);
+      if (rr < m) z[rr] = zz;
+    }
+    __syncthreads();
+  }
+  double zs = 0.0, ls = 0.0;
+  for (int a = tid; a < m; a += blockDim.x) {
+    zs += z[a] * z[a];
+    ls += 2.0 * log(G[(size_t)a * ld + a]);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    zs += __shfl_xor_sync(0xffffffffu, zs, o);
+    ls += __shfl_xor_sync(0xffffffffu, ls, o);
   }
   if (lane == 0) {
-    zsq[warp] = zs;
-    ldm[warp] = ls;
+    part[warp] = zs;
+    red[warp] = ls;
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
+  if (tid == 0) {
     double z2 = 0.0, lm = 0.0;
     for (int w = 0; w < 32; ++w) {
-      z2 += zsq[w];
-      lm += ldm[w];
+      z2 += part[w];
+      lm += red[w];
     }
-    const double lD = logdetD_dev ? *logdetD_dev : logdetD;
+    const double lD = *logdetD_dev;
     const double quad = G[(size_t)ycol * ld + ycol] - z2;
     terms[0] = 0.5 * (double)n * 1.8378770664093453 + 0.5 * (lD + lm) + 0.5 * quad;  // log(2 pi)
     terms[1] = lD;
@@ -286,7 +341,7 @@ cudaError_t launch_build_km(const double* Z, int m, const CovParams& p, double* 
 }
 
 cudaError_t launch_chol_inv(double* A, int m, int lda, double diag_add, double* Linv, int ldi, int lim_inv,
-                            int* fail, int num_sms, cudaStream_t s) {
+                            int full_inverse, double* Tscr, int* fail, int num_sms, cudaStream_t s) {
   if (m == 0) return cudaSuccess;
   int blocks_per_sm = 0;
   cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, chol_inv_kernel, 256, 0);
@@ -294,10 +349,10 @@ cudaError_t launch_chol_inv(double* A, int m, int lda, double diag_add, double* 
   if (blocks_per_sm < 1) return cudaErrorLaunchOutOfResources;
   const int nt = (m + TB - 1) / TB;
   int grid = num_sms;
-  const int need = nt * (nt + 1) / 2;
+  const int need = nt * nt;
   if (grid > need) grid = need;
   if (grid < 1) grid = 1;
-  void* args[] = {&A, &m, &lda, &diag_add, &Linv, &ldi, &lim_inv, &fail};
+  void* args[] = {&A, &m, &lda, &diag_add, &Linv, &ldi, &lim_inv, &full_inverse, &Tscr, &fail};
   return cudaLaunchCooperativeKernel((void*)chol_inv_kernel, dim3(grid), dim3(256), args, 0, s);
 }
 
@@ -308,9 +363,10 @@ cudaError_t launch_logd_sum(const double* Dpos, int64_t npts, double* partials, 
   return cudaGetLastError();
 }
 
-cudaError_t launch_finish(const double* G, int ld, int m, int ycol, const double* LinvM, int ldi,
+cudaError_t launch_finish(const double* G, int ld, int m, int ycol, const double* Dinv, int ldi,
                           const double* logdetD_dev, int64_t n, double* terms, cudaStream_t s) {
-  finish_kernel<<<1, 1024, 0, s>>>(G, ld, m, ycol, LinvM, ldi, 0.0, logdetD_dev, n, terms);
+  if (m > 2048) return cudaErrorInvalidValue;
+  finish_kernel<<<1, 1024, 0, s>>>(G, ld, m, ycol, Dinv, ldi, logdetD_dev, n, terms);
   return cudaGetLastError();
 }
 

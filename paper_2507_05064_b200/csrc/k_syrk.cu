@@ -83,6 +83,7 @@ __global__ void __launch_bounds__(128) syrk_kernel(const double* __restrict__ W,
       if (nk < nkt) load_stage(nk % SS, nk);
       cp_async_commit();
     }
+    if (diag && wn > wm) continue;  // 32x32 sub-tile above the diagonal: nothing to compute
     const double* as = As + (kt % SS) * SK * SPAD + fk * SPAD + wm * 32 + fc;
     const double* bs = (diag ? As : Bs) + (kt % SS) * SK * SPAD + fk * SPAD + wn * 32 + fc;
 #pragma unroll
@@ -133,8 +134,22 @@ int syrk_ntiles(int ncols) {
 
 int syrk_nsplit(int ncols, int64_t nrows, int num_sms) {
   const int nt = syrk_ntiles(ncols);
-  int64_t ns = (4LL * 2 * num_sms + nt - 1) / nt;  // ~4 waves at 2 CTAs / SM
-  const int64_t max_by_rows = (nrows + 255) / 256;  // at least 256 rows per split
+  const int64_t slots = 2LL * num_sms;                 // 2 CTAs / SM
+  const int64_t base = (4 * slots + nt - 1) / nt;      // >= ~4 waves
+  const int64_t max_by_rows = (nrows + 255) / 256;     // at least 256 rows per split
+  // pick the split count in [base, 2 base] whose last wave is fullest (no half-empty tail wave)
+  int64_t best = base;
+  double best_eff = 0.0;
+  for (int64_t ns = base; ns <= 2 * base; ++ns) {
+    const int64_t ctas = nt * ns;
+    const double eff = (double)ctas / (double)(slots * ((ctas + slots - 1) / slots));
+    if (eff > best_eff + 1e-9) {
+      best_eff = eff;
+      best = ns;
+    }
+    if (eff > 0.995) break;
+  }
+  int64_t ns = best;
   if (ns > max_by_rows) ns = max_by_rows;
   if (ns < 1) ns = 1;
   return (int)ns;

@@ -10,6 +10,7 @@
 //   i = (p / chunk) * world * chunk + rank * chunk + p % chunk.
 #include "common.cuh"
 #include "kernels.h"
+#include <stdlib.h>
 
 namespace vif {
 
@@ -58,10 +59,13 @@ __global__ void __launch_bounds__(256) kx_eval_kernel(const double* __restrict__
 // smem rows padded to 40 doubles (320 B = 64 mod 128 B) so the 16-byte fragment loads
 // (k-pair per lane, see below) are bank-conflict free.
 namespace {
-constexpr int GBM = 128, GBN = 64, GBK = 32, GST = 3, GPAD = 40;
+// BK = 16 keeps the ring at 110 KB so two CTAs (16 warps) share an SM and one CTA's prologue /
+// epilogue overlaps the other's main loop (rows padded to 24 doubles = 64 mod 128 B)
+constexpr int GBM = 128, GBN = 64, GBK = 16, GST = 3, GPAD = GBK + 8;
+constexpr int GCH = GBK / 2;  // 16-byte chunks per tile row
 }
 
-__global__ void __launch_bounds__(256) gemm_tn_kernel(const double* __restrict__ A, int64_t lda, int64_t npos,
+__global__ void __launch_bounds__(256, 2) gemm_tn_kernel(const double* __restrict__ A, int64_t lda, int64_t npos,
                                                       const double* __restrict__ B, int64_t ldb, int N, int K,
                                                       int tri, double* __restrict__ C, int64_t ldc, int64_t n,
                                                       int64_t chunk, int world, int rank) {
@@ -70,29 +74,34 @@ __global__ void __launch_bounds__(256) gemm_tn_kernel(const double* __restrict__
   double* Bs = gsm + GST * GBM * GPAD;         // [GST][GBN][GPAD]
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int wm = warp >> 1, wn = warp & 1;     // 4 x 2 warps
-  const int64_t row0 = (int64_t)blockIdx.x * GBM;
-  const int col0 = blockIdx.y * GBN;
+  // 1-D grid, column block fastest: the ncb CTAs that share an A row block run together and
+  // read it from L2 instead of DRAM
+  const int ncb = (N + GBN - 1) / GBN;
+  const int64_t row0 = (int64_t)(blockIdx.x / ncb) * GBM;
+  const int col0 = (blockIdx.x % ncb) * GBN;
   int kend = K;
   if (tri && col0 + GBN < kend) kend = col0 + GBN;
   const int nkt = (kend + GBK - 1) / GBK;
+  // a warp's 32 columns end at col0 + 32 (wn + 1): with a triangular B it skips later K-tiles
+  const int kend_w = tri ? min(kend, col0 + 32 * (wn + 1)) : kend;
 
   auto load_stage = [&](int st, int kt) {
     const int k0 = kt * GBK;
     double* as = As + st * GBM * GPAD;
     double* bs = Bs + st * GBN * GPAD;
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {  // 128 rows x 16 chunks of 16 B = 2048
+    for (int j = 0; j < GBM * GCH / 256; ++j) {  // A: GBM rows x GCH chunks of 16 B
       const int e = tid + j * 256;
-      const int r = e >> 4, c2 = (e & 15) * 2;
+      const int r = e / GCH, c2 = (e % GCH) * 2;
       const int64_t gr = row0 + r;
       const bool ok = gr < npos && k0 + c2 < kend;
       const double* src = ok ? A + gr * lda + k0 + c2 : A;
       cp_async16(as + r * GPAD + c2, src, ok);
     }
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {  // 64 rows x 16 chunks
+    for (int j = 0; j < GBN * GCH / 256; ++j) {  // B: GBN rows x GCH chunks
       const int e = tid + j * 256;
-      const int r = e >> 4, c2 = (e & 15) * 2;
+      const int r = e / GCH, c2 = (e % GCH) * 2;
       const int gc = col0 + r;
       const bool ok = gc < N && k0 + c2 < kend;
       const double* src = ok ? B + (int64_t)gc * ldb + k0 + c2 : B;
@@ -120,6 +129,7 @@ __global__ void __launch_bounds__(256) gemm_tn_kernel(const double* __restrict__
       if (nk < nkt) load_stage(nk % GST, nk);
       cp_async_commit();
     }
+    if (kt * GBK >= kend_w) continue;
     const double* as = As + (kt % GST) * GBM * GPAD + (wm * 32 + fr) * GPAD + fk;
     const double* bs = Bs + (kt % GST) * GBN * GPAD + (wn * 32 + fr) * GPAD + fk;
 #pragma unroll
@@ -170,6 +180,11 @@ cudaError_t launch_u_features(const double* X, const double* Z, const double* y,
   }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess || mk == 0) return e;
+  // default: this file's 128x64 / 8-warp / 2-CTA kernel; VIF_GEMM128=1 selects the 128x128 engine
+  // of k_gemm.cu (measured slower on B200, profiles/r01_notes.md)
+  static const char* e128 = getenv("VIF_GEMM128");
+  if (e128 && e128[0] == '1')
+    return launch_gemm_tn_tri(S, mk, npos, Linv, mk, mk, Uaug, ld, n, chunk, world, rank, s);
   const size_t smem = (size_t)GST * (GBM + GBN) * GPAD * sizeof(double);
   static bool attr_set = false;
   if (!attr_set) {
@@ -177,7 +192,7 @@ cudaError_t launch_u_features(const double* X, const double* Z, const double* y,
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  dim3 grid((unsigned)((npos + GBM - 1) / GBM), (unsigned)((mk + GBN - 1) / GBN));
+  const unsigned grid = (unsigned)(((npos + GBM - 1) / GBM) * ((mk + GBN - 1) / GBN));
   gemm_tn_kernel<<<grid, 256, smem, s>>>(S, mk, npos, Linv, mk, mk, mk, 1, Uaug, ld, n, chunk, world, rank);
   return cudaGetLastError();
 }

@@ -29,10 +29,10 @@ struct VecchiaArgs {
 // K0 / K5
 cudaError_t launch_build_km(const double* Z, int m, const CovParams& p, double* Km, cudaStream_t s);
 cudaError_t launch_chol_inv(double* A, int m, int lda, double diag_add, double* Linv, int ldi, int lim_inv,
-                            int* fail, int num_sms, cudaStream_t s);
+                            int full_inverse, double* Tscr, int* fail, int num_sms, cudaStream_t s);
 cudaError_t launch_logd_sum(const double* Dpos, int64_t npts, double* partials, int np, double* out,
                             cudaStream_t s);
-cudaError_t launch_finish(const double* G, int ld, int m, int ycol, const double* LinvM, int ldi,
+cudaError_t launch_finish(const double* G, int ld, int m, int ycol, const double* Dinv, int ldi,
                           const double* logdetD_dev, int64_t n, double* terms, cudaStream_t s);
 // K1
 cudaError_t launch_u_features(const double* X, const double* Z, const double* y, int64_t n, int64_t npos,
@@ -46,6 +46,15 @@ int syrk_nsplit(int ncols, int64_t nrows, int num_sms);
 size_t syrk_part_doubles(int ncols, int nsplit);
 cudaError_t launch_syrk(const double* W, int64_t ldw, int64_t nrows, int ncols, int nsplit, double* Gpart,
                         double* G, int ldg, cudaStream_t s);
+// K1b / K4 on the 128x128 engine (k_gemm.cu)
+cudaError_t launch_gemm_tn_tri(const double* S, int64_t lds, int64_t npos, const double* Linv, int ldl, int N,
+                               double* U, int64_t ldu, int64_t n, int64_t chunk, int world, int rank,
+                               cudaStream_t s);
+int syrk_nt_ntiles(int ncols);
+int syrk_nt_nsplit(int ncols, int64_t nrows, int num_sms);
+size_t syrk_nt_part_doubles(int ncols, int nsplit);
+cudaError_t launch_syrk_nt(const double* W, int64_t ldw, int64_t nrows, int ncols, int nsplit, double* Gpart,
+                           double* G, int ldg, cudaStream_t s);
 // misc
 cudaError_t launch_validate(const double* X, int64_t n, int d, const double* Z, int m, const double* y,
                             const int32_t* nbr, int mv, DevStatus* st, cudaStream_t s);

@@ -77,13 +77,13 @@ struct Plan {
   bool emulate;
   int mk, ycol, ld;
   int64_t rounds, chunk, npos, npad;
-  int nsplit;
+  int nsplit, nsplit_old;
   std::vector<int64_t> n_own;
 };
 
 enum Buf {
   B_X, B_Z, B_NBR, B_Y, B_KM, B_LINV, B_U, B_W, B_DPOS, B_ORDER, B_KEYS, B_KEYS2, B_VALS, B_VALS2, B_TEMP,
-  B_GPART, B_G, B_GSUM, B_LINVM, B_PART, B_BBOX, B_TERMS, B_STATUS, B_COUNT
+  B_GPART, B_G, B_GSUM, B_LINVM, B_TSCR, B_PART, B_BBOX, B_TERMS, B_STATUS, B_COUNT
 };
 
 struct Layout {
@@ -124,7 +124,8 @@ bool make_plan(const vif_dims* dims, bool emulate, Plan& P, std::string& err) {
       const int64_t cnt = P.n - start;
       P.n_own[g] += cnt <= 0 ? 0 : (cnt < P.chunk ? cnt : P.chunk);
     }
-  P.nsplit = syrk_nsplit(P.ld, P.npos, kPlanSMs);
+  P.nsplit = syrk_nt_nsplit(P.ld, P.npos, kPlanSMs);
+  P.nsplit_old = syrk_nsplit(P.ld, P.npos, kPlanSMs);
   return true;
 }
 
@@ -146,10 +147,11 @@ Layout make_layout(const Plan& P) {
   L.size[B_ORDER] = (size_t)nrep * P.npos * sizeof(int64_t);
   L.size[B_KEYS] = L.size[B_KEYS2] = L.size[B_VALS] = L.size[B_VALS2] = (size_t)P.npos * 8;
   L.size[B_TEMP] = order_temp_bytes(P.npos);
-  L.size[B_GPART] = syrk_part_doubles(P.ld, P.nsplit) * D8;
+  L.size[B_GPART] = std::max(syrk_nt_part_doubles(P.ld, P.nsplit), syrk_part_doubles(P.ld, P.nsplit_old)) * D8;
   L.size[B_G] = nrep * gsz;
   L.size[B_GSUM] = gsz;
   L.size[B_LINVM] = (size_t)mk1 * mk1 * D8;
+  L.size[B_TSCR] = (size_t)mk1 * mk1 * D8;
   L.size[B_PART] = kLogdParts * D8;
   L.size[B_BBOX] = 128 * 6 * D8;
   L.size[B_TERMS] = 8 * D8;
@@ -424,8 +426,8 @@ int vif_factor(void* handle, const vif_theta* theta, double* B_out, double* D_ou
   if (P.m > 0) {
     VIF_CUDA(h, launch_build_km(h->buf<double>(B_Z), P.m, p, h->buf<double>(B_KM), s), "build K_m");
     VIF_CUDA(h, cudaMemsetAsync(h->buf<double>(B_LINV), 0, h->L.size[B_LINV], s), "memset Linv");
-    VIF_CUDA(h, launch_chol_inv(h->buf<double>(B_KM), P.m, P.m, 0.0, h->buf<double>(B_LINV), P.mk, P.mk, &st->km_fail,
-                                h->num_sms, s),
+    VIF_CUDA(h, launch_chol_inv(h->buf<double>(B_KM), P.m, P.m, 0.0, h->buf<double>(B_LINV), P.mk, P.mk, 1,
+                                h->buf<double>(B_TSCR), &st->km_fail, h->num_sms, s),
              "chol K_m");
     nl += 2;
   }
@@ -486,8 +488,14 @@ int vif_factor(void* handle, const vif_theta* theta, double* B_out, double* D_ou
     h->mark(S_VECCHIA, 1);
     double* G = h->buf<double>(B_G) + g * gstride;
     h->mark(S_SYRK, 0);
-    VIF_CUDA(h, launch_syrk(h->buf<double>(B_W), P.ld, npts, P.ld, P.nsplit, h->buf<double>(B_GPART), G, P.ld, s),
-             "syrk");
+    // default: 64x64 / 4-warp / 2-CTA SYRK (k_syrk.cu); VIF_SYRK128=1 selects the 128x128 engine
+    static const char* syrk128 = getenv("VIF_SYRK128");
+    if (!(syrk128 && syrk128[0] == '1'))
+      VIF_CUDA(h, launch_syrk(h->buf<double>(B_W), P.ld, npts, P.ld, P.nsplit_old, h->buf<double>(B_GPART), G, P.ld, s),
+               "syrk");
+    else
+      VIF_CUDA(h, launch_syrk_nt(h->buf<double>(B_W), P.ld, npts, P.ld, P.nsplit, h->buf<double>(B_GPART), G, P.ld, s),
+               "syrk");
     h->mark(S_SYRK, 1);
     h->mark(S_REDUCE, 0);
     VIF_CUDA(h, launch_logd_sum(h->buf<double>(B_DPOS), npts, h->buf<double>(B_PART), kLogdParts,
@@ -531,7 +539,8 @@ int vif_nll(void* handle, vif_terms* out) {
   h->mark(S_CHOLM, 0);
   if (P.m > 0) {
     VIF_CUDA(h, cudaMemsetAsync(h->buf<double>(B_LINVM), 0, h->L.size[B_LINVM], s), "memset LinvM");
-    VIF_CUDA(h, launch_chol_inv(G, P.m, P.ld, 1.0, h->buf<double>(B_LINVM), P.mk, P.mk, &st->m_fail, h->num_sms, s),
+    VIF_CUDA(h, launch_chol_inv(G, P.m, P.ld, 1.0, h->buf<double>(B_LINVM), P.mk, P.mk, 0, nullptr, &st->m_fail,
+                                h->num_sms, s),
              "chol M");
     ++nl;
   }

@@ -1,5 +1,6 @@
 #!/bin/bash
 # ncu --set full of the vecchia kernel at the config-3 recipe (n=300k) after a plain run of the same command.
+# usage: tools/ncu_vecchia.sh TAG [kernel-regex]   (env vars such as VIF_VECCHIA_VARIANT pass through)
 CMD="python bench.py --n 300000 --steps 2 --warmup 1 --no-cpu-baseline"
 TAG=${1:-cur}
 $CMD > gpurun_out/ncu_plain_$TAG.log 2>&1 && \
