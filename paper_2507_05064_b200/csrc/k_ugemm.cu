@@ -24,22 +24,26 @@ __global__ void __launch_bounds__(256) kx_eval_kernel(const double* __restrict__
                                                       int64_t chunk, int world, int rank, int m, int mk,
                                                       CovParams p, double* __restrict__ S,
                                                       double* __restrict__ Uaug, int ld) {
-  // one warp per row; lanes stride over the columns
-  const int64_t pos = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
-  const int lane = threadIdx.x & 31;
-  if (pos >= npos) return;
-  const int64_t i = pos_to_row(pos, chunk, world, rank);
+  // one warp per row; lanes stride over the columns.  Z and the 8 row coordinates are staged in
+  // shared memory (broadcast reads; a runtime-indexed register array would live in local memory).
+  extern __shared__ double kx_zs[];        // m x d
+  __shared__ double kx_x[8][VIF_MAX_D];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t pos = (int64_t)blockIdx.x * 8 + warp;
+  for (int e = threadIdx.x; e < m * p.d; e += blockDim.x) kx_zs[e] = Z[e];
+  const int64_t i = pos < npos ? pos_to_row(pos, chunk, world, rank) : n;
   const bool valid = i < n;
-  double x[VIF_MAX_D];
-#pragma unroll
-  for (int k = 0; k < VIF_MAX_D; ++k) x[k] = (valid && k < p.d) ? X[i * p.d + k] : 0.0;
+  if (lane < p.d) kx_x[warp][lane] = valid ? X[i * p.d + lane] : 0.0;
+  __syncthreads();
+  if (pos >= npos) return;
+  const double* x = kx_x[warp];
   double* srow = S + pos * (int64_t)mk;
+#pragma unroll 4
   for (int b = lane; b < mk; b += 32) {
     double v = 0.0;
     if (valid && b < m) {
-      const double* z = Z + (size_t)b * p.d;
+      const double* z = kx_zs + b * p.d;
       double r2 = 0.0;
-#pragma unroll 4
       for (int k = 0; k < p.d; ++k) {
         const double t = (x[k] - z[k]) * p.inv_ls[k];
         r2 = fma(t, t, r2);
@@ -172,12 +176,25 @@ cudaError_t launch_u_features(const double* X, const double* Z, const double* y,
                               const double* Linv, double* S, double* Uaug, int ld, cudaStream_t s) {
   if (npos == 0) return cudaSuccess;
   const int blocks = (int)((npos + 7) / 8);
+  const size_t zbytes = (size_t)m * p.d * sizeof(double);
+  auto go = [&](auto kern) -> cudaError_t {
+    static size_t attr = 0;  // one per instantiation of the generic lambda
+    if (zbytes > 48 * 1024 && attr < zbytes) {
+      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)zbytes);
+      if (e != cudaSuccess) return e;
+      attr = zbytes;
+    }
+    kern<<<blocks, 256, zbytes, s>>>(X, Z, y, n, npos, chunk, world, rank, m, mk, p, S, Uaug, ld);
+    return cudaSuccess;
+  };
+  cudaError_t e0 = cudaSuccess;
   switch (p.family) {
-    case FAM_M12: kx_eval_kernel<FAM_M12><<<blocks, 256, 0, s>>>(X, Z, y, n, npos, chunk, world, rank, m, mk, p, S, Uaug, ld); break;
-    case FAM_M32: kx_eval_kernel<FAM_M32><<<blocks, 256, 0, s>>>(X, Z, y, n, npos, chunk, world, rank, m, mk, p, S, Uaug, ld); break;
-    case FAM_M52: kx_eval_kernel<FAM_M52><<<blocks, 256, 0, s>>>(X, Z, y, n, npos, chunk, world, rank, m, mk, p, S, Uaug, ld); break;
-    default: kx_eval_kernel<FAM_GAUSS><<<blocks, 256, 0, s>>>(X, Z, y, n, npos, chunk, world, rank, m, mk, p, S, Uaug, ld); break;
+    case FAM_M12: e0 = go(kx_eval_kernel<FAM_M12>); break;
+    case FAM_M32: e0 = go(kx_eval_kernel<FAM_M32>); break;
+    case FAM_M52: e0 = go(kx_eval_kernel<FAM_M52>); break;
+    default: e0 = go(kx_eval_kernel<FAM_GAUSS>); break;
   }
+  if (e0 != cudaSuccess) return e0;
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess || mk == 0) return e;
   // default: this file's 128x64 / 8-warp / 2-CTA kernel; VIF_GEMM128=1 selects the 128x128 engine
