@@ -13,7 +13,9 @@
 namespace vif {
 
 namespace {
-constexpr int ST = 64, SK = 32, SS = 3, SPAD = 72;
+// SK = 16: a 55 KB ring, four CTAs (16 warps) per SM
+constexpr int ST = 64, SK = 16, SS = 3, SPAD = 72;
+constexpr int SMINB = 4;
 }
 
 __device__ __forceinline__ void tile_ij(int t, int& I, int& J) {
@@ -23,7 +25,7 @@ __device__ __forceinline__ void tile_ij(int t, int& I, int& J) {
   J = t - i * (i + 1) / 2;
 }
 
-__global__ void __launch_bounds__(128) syrk_kernel(const double* __restrict__ W, int64_t ldw, int64_t nrows,
+__global__ void __launch_bounds__(128, SMINB) syrk_kernel(const double* __restrict__ W, int64_t ldw, int64_t nrows,
                                                    int ncols, int ntiles, int64_t rows_per_split,
                                                    double* __restrict__ Gpart) {
   extern __shared__ __align__(16) double ssm[];
@@ -47,7 +49,7 @@ __global__ void __launch_bounds__(128) syrk_kernel(const double* __restrict__ W,
     double* as = As + st * SK * SPAD;
     double* bs = Bs + st * SK * SPAD;
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {  // 32 rows x 32 chunks of 16 B = 1024
+    for (int j = 0; j < SK * 32 / 128; ++j) {  // SK rows x 32 chunks of 16 B
       const int e = tid + j * 128;
       const int r = e >> 5, c2 = (e & 31) * 2;
       const int64_t gr = k0 + r;
@@ -134,7 +136,7 @@ int syrk_ntiles(int ncols) {
 
 int syrk_nsplit(int ncols, int64_t nrows, int num_sms) {
   const int nt = syrk_ntiles(ncols);
-  const int64_t slots = 2LL * num_sms;                 // 2 CTAs / SM
+  const int64_t slots = (int64_t)SMINB * num_sms;      // CTAs resident at once
   const int64_t base = (4 * slots + nt - 1) / nt;      // >= ~4 waves
   const int64_t max_by_rows = (nrows + 255) / 256;     // at least 256 rows per split
   // pick the split count in [base, 2 base] whose last wave is fullest (no half-empty tail wave)

@@ -971,6 +971,8 @@ static cudaError_t launch_rb(const VecchiaArgs& a, cudaStream_t s) {
       case 44: kern = vecchia_reg_kernel<FAM, RB, 4, 4>; break;
       case 33: kern = vecchia_reg_kernel<FAM, RB, 3, 3>; break;
       case 43: kern = vecchia_reg_kernel<FAM, RB, 4, 3>; break;
+      case 25: kern = vecchia_reg_kernel<FAM, RB, 2, 5>; break;
+      case 26: kern = vecchia_reg_kernel<FAM, RB, 2, 6>; break;
       default: kern = vecchia_reg_kernel<FAM, RB, 3, 4>; break;
     }
     static size_t attr = 0;
