@@ -36,7 +36,8 @@ __device__ __forceinline__ int64_t pos_to_row_g(int64_t p, int64_t chunk, int wo
 __global__ void __launch_bounds__(512, 1) gemm_tn_tri_kernel(const double* __restrict__ A, int64_t lda, int64_t npos,
                                                              const double* __restrict__ B, int64_t ldb, int N,
                                                              double* __restrict__ C, int64_t ldc, int64_t n,
-                                                             int64_t chunk, int world, int rank, int ncb) {
+                                                             int64_t chunk, int world, int rank, int64_t pos0,
+                                                             int ncb) {
   extern __shared__ __align__(16) double esm[];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int wm = warp >> 2, wn = warp & 3;
@@ -115,7 +116,7 @@ __global__ void __launch_bounds__(512, 1) gemm_tn_tri_kernel(const double* __res
   for (int a = 0; a < 4; ++a) {
     const int64_t p = row0 + wm * 32 + a * 8 + fr;
     if (p >= npos) continue;
-    const int64_t i = pos_to_row_g(p, chunk, world, rank);
+    const int64_t i = pos_to_row_g(pos0 + p, chunk, world, rank);
     if (i >= n) continue;
 #pragma unroll
     for (int b = 0; b < 4; ++b) {
@@ -238,7 +239,7 @@ __global__ void syrk_nt_reduce_kernel(const double* __restrict__ Gpart, int ntil
 // ------------------------------------------------------------------------------------------ host
 cudaError_t launch_gemm_tn_tri(const double* S, int64_t lds, int64_t npos, const double* Linv, int ldl, int N,
                                double* U, int64_t ldu, int64_t n, int64_t chunk, int world, int rank,
-                               cudaStream_t s) {
+                               int64_t pos0, cudaStream_t s) {
   if (npos == 0 || N == 0) return cudaSuccess;
   const size_t smem = (size_t)ES * TN_STAGE * sizeof(double);
   static bool attr = false;
@@ -250,7 +251,7 @@ cudaError_t launch_gemm_tn_tri(const double* S, int64_t lds, int64_t npos, const
   const int ncb = (N + EB - 1) / EB;
   const int64_t nrb = (npos + EB - 1) / EB;
   gemm_tn_tri_kernel<<<(unsigned)(nrb * ncb), 512, smem, s>>>(S, lds, npos, Linv, ldl, N, U, ldu, n, chunk, world,
-                                                              rank, ncb);
+                                                              rank, pos0, ncb);
   return cudaGetLastError();
 }
 

@@ -125,7 +125,7 @@ __global__ void morton_kernel(const double* __restrict__ X, int64_t n, int d, in
       l = fmin(l, part[b * 6 + threadIdx.x]);
       h = fmax(h, part[b * 6 + 3 + threadIdx.x]);
     }
-    const int bits = dd == 1 ? 62 : (dd == 2 ? 31 : 21);
+    const int bits = dd == 1 ? 48 : (dd == 2 ? 24 : 16);  // 48-bit Morton code; round index above
     const double span = h > l ? h - l : 1.0;
     lo[threadIdx.x] = l;
     sc[threadIdx.x] = (double)((1ULL << bits) - 1) / span;
@@ -145,7 +145,9 @@ __global__ void morton_kernel(const double* __restrict__ X, int64_t n, int d, in
       if (dd == 1) key = c[0];
       else if (dd == 2) key = spread2(c[0]) | (spread2(c[1]) << 1);
       else key = spread3(c[0]) | (spread3(c[1]) << 1) | (spread3(c[2]) << 2);
-      key &= 0x7fffffffffffffffULL;  // keep ~0 as the "invalid" sentinel
+      // positions are grouped by round (chunk-cyclic round = pos / chunk), Morton order inside a
+      // round, so the Vecchia rows of round r can run as soon as round r of U is gathered
+      key = ((uint64_t)(pos / chunk) << 48) | (key & 0xffffffffffffULL);
     }
     keys[pos] = key;
     vals[pos] = i;

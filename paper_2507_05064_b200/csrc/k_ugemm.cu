@@ -21,8 +21,8 @@ __device__ __forceinline__ int64_t pos_to_row(int64_t p, int64_t chunk, int worl
 template <int FAM>
 __global__ void __launch_bounds__(256) kx_eval_kernel(const double* __restrict__ X, const double* __restrict__ Z,
                                                       const double* __restrict__ y, int64_t n, int64_t npos,
-                                                      int64_t chunk, int world, int rank, int m, int mk,
-                                                      CovParams p, double* __restrict__ S,
+                                                      int64_t chunk, int world, int rank, int64_t pos0, int m,
+                                                      int mk, CovParams p, double* __restrict__ S,
                                                       double* __restrict__ Uaug, int ld) {
   // one warp per row; lanes stride over the columns.  Z and the 8 row coordinates are staged in
   // shared memory (broadcast reads; a runtime-indexed register array would live in local memory).
@@ -31,7 +31,7 @@ __global__ void __launch_bounds__(256) kx_eval_kernel(const double* __restrict__
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t pos = (int64_t)blockIdx.x * 8 + warp;
   for (int e = threadIdx.x; e < m * p.d; e += blockDim.x) kx_zs[e] = Z[e];
-  const int64_t i = pos < npos ? pos_to_row(pos, chunk, world, rank) : n;
+  const int64_t i = pos < npos ? pos_to_row(pos0 + pos, chunk, world, rank) : n;
   const bool valid = i < n;
   if (lane < p.d) kx_x[warp][lane] = valid ? X[i * p.d + lane] : 0.0;
   __syncthreads();
@@ -72,7 +72,7 @@ constexpr int GCH = GBK / 2;  // 16-byte chunks per tile row
 __global__ void __launch_bounds__(256, 2) gemm_tn_kernel(const double* __restrict__ A, int64_t lda, int64_t npos,
                                                       const double* __restrict__ B, int64_t ldb, int N, int K,
                                                       int tri, double* __restrict__ C, int64_t ldc, int64_t n,
-                                                      int64_t chunk, int world, int rank) {
+                                                      int64_t chunk, int world, int rank, int64_t pos0) {
   extern __shared__ __align__(16) double gsm[];
   double* As = gsm;                            // [GST][GBM][GPAD]
   double* Bs = gsm + GST * GBM * GPAD;         // [GST][GBN][GPAD]
@@ -161,7 +161,7 @@ __global__ void __launch_bounds__(256, 2) gemm_tn_kernel(const double* __restric
   for (int a = 0; a < 4; ++a) {
     const int64_t p = row0 + wm * 32 + a * 8 + fr;
     if (p >= npos) continue;
-    const int64_t i = pos_to_row(p, chunk, world, rank);
+    const int64_t i = pos_to_row(pos0 + p, chunk, world, rank);
     if (i >= n) continue;
 #pragma unroll
     for (int b = 0; b < 4; ++b) {
@@ -171,8 +171,8 @@ __global__ void __launch_bounds__(256, 2) gemm_tn_kernel(const double* __restric
   }
 }
 
-cudaError_t launch_u_features(const double* X, const double* Z, const double* y, int64_t n, int64_t npos,
-                              int64_t chunk, int world, int rank, int m, int mk, const CovParams& p,
+cudaError_t launch_u_features(const double* X, const double* Z, const double* y, int64_t n, int64_t pos0,
+                              int64_t npos, int64_t chunk, int world, int rank, int m, int mk, const CovParams& p,
                               const double* Linv, double* S, double* Uaug, int ld, cudaStream_t s) {
   if (npos == 0) return cudaSuccess;
   const int blocks = (int)((npos + 7) / 8);
@@ -184,7 +184,7 @@ cudaError_t launch_u_features(const double* X, const double* Z, const double* y,
       if (e != cudaSuccess) return e;
       attr = zbytes;
     }
-    kern<<<blocks, 256, zbytes, s>>>(X, Z, y, n, npos, chunk, world, rank, m, mk, p, S, Uaug, ld);
+    kern<<<blocks, 256, zbytes, s>>>(X, Z, y, n, npos, chunk, world, rank, pos0, m, mk, p, S + pos0 * mk, Uaug, ld);
     return cudaSuccess;
   };
   cudaError_t e0 = cudaSuccess;
@@ -201,7 +201,7 @@ cudaError_t launch_u_features(const double* X, const double* Z, const double* y,
   // of k_gemm.cu (measured slower on B200, profiles/r01_notes.md)
   static const char* e128 = getenv("VIF_GEMM128");
   if (e128 && e128[0] == '1')
-    return launch_gemm_tn_tri(S, mk, npos, Linv, mk, mk, Uaug, ld, n, chunk, world, rank, s);
+    return launch_gemm_tn_tri(S + pos0 * mk, mk, npos, Linv, mk, mk, Uaug, ld, n, chunk, world, rank, pos0, s);
   const size_t smem = (size_t)GST * (GBM + GBN) * GPAD * sizeof(double);
   static bool attr_set = false;
   if (!attr_set) {
@@ -210,7 +210,8 @@ cudaError_t launch_u_features(const double* X, const double* Z, const double* y,
     attr_set = true;
   }
   const unsigned grid = (unsigned)(((npos + GBM - 1) / GBM) * ((mk + GBN - 1) / GBN));
-  gemm_tn_kernel<<<grid, 256, smem, s>>>(S, mk, npos, Linv, mk, mk, mk, 1, Uaug, ld, n, chunk, world, rank);
+  gemm_tn_kernel<<<grid, 256, smem, s>>>(S + pos0 * mk, mk, npos, Linv, mk, mk, mk, 1, Uaug, ld, n, chunk, world, rank,
+                                         pos0);
   return cudaGetLastError();
 }
 

@@ -35,8 +35,8 @@ cudaError_t launch_logd_sum(const double* Dpos, int64_t npts, double* partials, 
 cudaError_t launch_finish(const double* G, int ld, int m, int ycol, const double* Dinv, int ldi,
                           const double* logdetD_dev, int64_t n, double* terms, cudaStream_t s);
 // K1
-cudaError_t launch_u_features(const double* X, const double* Z, const double* y, int64_t n, int64_t npos,
-                              int64_t chunk, int world, int rank, int m, int mk, const CovParams& p,
+cudaError_t launch_u_features(const double* X, const double* Z, const double* y, int64_t n, int64_t pos0,
+                              int64_t npos, int64_t chunk, int world, int rank, int m, int mk, const CovParams& p,
                               const double* Linv, double* S, double* Uaug, int ld, cudaStream_t s);
 // K2 + K3
 cudaError_t launch_vecchia(const VecchiaArgs& a, cudaStream_t s);
@@ -49,7 +49,7 @@ cudaError_t launch_syrk(const double* W, int64_t ldw, int64_t nrows, int ncols, 
 // K1b / K4 on the 128x128 engine (k_gemm.cu)
 cudaError_t launch_gemm_tn_tri(const double* S, int64_t lds, int64_t npos, const double* Linv, int ldl, int N,
                                double* U, int64_t ldu, int64_t n, int64_t chunk, int world, int rank,
-                               cudaStream_t s);
+                               int64_t pos0, cudaStream_t s);
 int syrk_nt_ntiles(int ncols);
 int syrk_nt_nsplit(int ncols, int64_t nrows, int num_sms);
 size_t syrk_nt_part_doubles(int ncols, int nsplit);

@@ -178,6 +178,8 @@ struct Handle {
   cudaStream_t stream = nullptr;
   int num_sms = 148;
   ncclComm_t comm = nullptr;
+  cudaStream_t cstream = nullptr;            // communication stream (world > 1 with NCCL)
+  std::vector<cudaEvent_t> ev_k1, ev_ag;     // per round: K1 done / all-gather done
   bool have_data = false, factored = false, finished = false;
   vif_terms cached{};
   int cached_status = VIF_OK;
@@ -379,6 +381,18 @@ int vif_create(void** handle, const vif_dims* dims, void* workspace, size_t ws_b
       delete h;
       return fail(nullptr, VIF_ERR_NCCL, m);
     }
+    e = cudaStreamCreateWithFlags(&h->cstream, cudaStreamNonBlocking);
+    h->ev_k1.assign(h->P.rounds, nullptr);
+    h->ev_ag.assign(h->P.rounds, nullptr);
+    for (int64_t k = 0; k < h->P.rounds && e == cudaSuccess; ++k) {
+      e = cudaEventCreateWithFlags(&h->ev_k1[k], cudaEventDisableTiming);
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h->ev_ag[k], cudaEventDisableTiming);
+    }
+    if (e != cudaSuccess) {
+      std::string m = std::string("comm stream/events: ") + cudaGetErrorString(e);
+      vif_destroy(h);
+      return fail(nullptr, VIF_ERR_CUDA, m);
+    }
   }
   if (X || Z || nbr || y) {
     int r = set_data(h, X, Z, nbr, y, 1);
@@ -432,63 +446,75 @@ int vif_factor(void* handle, const vif_theta* theta, double* B_out, double* D_ou
     nl += 2;
   }
   h->mark(S_KM, 1);
-  // A1 (+A2): U rows per (logical) rank
+  // A1-A6 in chunk-cyclic rounds.  Round r of a rank = positions [r*chunk, (r+1)*chunk);
+  // vif_set_data groups the processing order by round (Morton order inside a round).  Per rank:
+  //   compute stream: K1(round 0..R-1), then for each r: [wait AG(r)] vecchia rows of round r
+  //   comm stream:    AG(r) right after K1(r)
+  // so the all-gather of round r overlaps K1 of later rounds and the vecchia rows of earlier rounds
+  // (the rows of round r only condition on predecessors, i.e. on rounds <= r).
   const int nrep = P.emulate ? P.world : 1;
+  const bool nccl_path = P.world > 1 && !P.emulate;
+  const size_t gstride = (size_t)P.ld * P.ld + 8;
   h->mark(S_UFEAT, 0);
-  for (int g = 0; g < nrep; ++g) {
-    const int rank = P.emulate ? g : P.rank;
-    VIF_CUDA(h, launch_u_features(h->buf<double>(B_X), h->buf<double>(B_Z), h->buf<double>(B_Y), P.n, P.npos, P.chunk,
-                                  P.world, rank, P.m, P.mk, p, h->buf<double>(B_LINV), h->buf<double>(B_W),
-                                  h->buf<double>(B_U), P.ld, s),
-             "U features");
-    nl += P.mk > 0 ? 2 : 1;
+  for (int64_t r = 0; r < P.rounds; ++r) {
+    for (int g = 0; g < nrep; ++g) {
+      const int rank = P.emulate ? g : P.rank;
+      VIF_CUDA(h, launch_u_features(h->buf<double>(B_X), h->buf<double>(B_Z), h->buf<double>(B_Y), P.n, r * P.chunk,
+                                    P.chunk, P.chunk, P.world, rank, P.m, P.mk, p, h->buf<double>(B_LINV),
+                                    h->buf<double>(B_W), h->buf<double>(B_U), P.ld, s),
+               "U features");
+      nl += P.mk > 0 ? 2 : 1;
+    }
+    if (nccl_path) {
+      Nccl& N = nccl();
+      const size_t cnt = (size_t)P.chunk * P.ld;
+      double* recv = h->buf<double>(B_U) + (size_t)r * P.world * cnt;
+      VIF_CUDA(h, cudaEventRecord(h->ev_k1[r], s), "event");
+      VIF_CUDA(h, cudaStreamWaitEvent(h->cstream, h->ev_k1[r], 0), "event wait");
+      ncclResult_t rr = N.AllGather(recv + (size_t)P.rank * cnt, recv, cnt, ncclFloat64, h->comm, h->cstream);
+      if (rr != ncclSuccess) return fail(h, VIF_ERR_NCCL, std::string("ncclAllGather: ") + N.GetErrorString(rr));
+      VIF_CUDA(h, cudaEventRecord(h->ev_ag[r], h->cstream), "event");
+    }
   }
   h->mark(S_UFEAT, 1);
-  h->mark(S_GATHER, 0);
-  if (P.world > 1 && !P.emulate) {
-    Nccl& N = nccl();
-    const size_t cnt = (size_t)P.chunk * P.ld;
-    N.GroupStart();
-    for (int64_t r = 0; r < P.rounds; ++r) {
-      double* recv = h->buf<double>(B_U) + (size_t)r * P.world * cnt;
-      ncclResult_t rr = N.AllGather(recv + (size_t)P.rank * cnt, recv, cnt, ncclFloat64, h->comm, s);
-      if (rr != ncclSuccess) {
-        N.GroupEnd();
-        return fail(h, VIF_ERR_NCCL, std::string("ncclAllGather: ") + N.GetErrorString(rr));
-      }
-    }
-    ncclResult_t rr = N.GroupEnd();
-    if (rr != ncclSuccess) return fail(h, VIF_ERR_NCCL, std::string("ncclGroupEnd: ") + N.GetErrorString(rr));
-  }
+  h->mark(S_GATHER, 0);  // the gathers run on the comm stream, overlapped with the stages below
   h->mark(S_GATHER, 1);
-  // A3-A6 per (logical) rank
-  const size_t gstride = (size_t)P.ld * P.ld + 8;
   for (int g = 0; g < nrep; ++g) {
     const int rank = P.emulate ? g : P.rank;
     const int64_t npts = P.n_own[rank];
-    VecchiaArgs a;
-    a.U = h->buf<double>(B_U);
-    a.ldu = P.ld;
-    a.mk = P.mk;
-    a.ld = P.ld;
-    a.X = h->buf<double>(B_X);
-    a.nbr = h->buf<int32_t>(B_NBR);
-    a.mv = P.mv;
-    a.order = h->order[g];
-    a.npts = npts;
-    a.p = p;
-    a.W = h->buf<double>(B_W);
-    a.ldw = P.ld;
-    a.Dpos = h->buf<double>(B_DPOS);
-    a.B_out = B_out;
-    a.D_out = D_out;
-    a.st = st;
     h->mark(S_VECCHIA, 0);
-    VIF_CUDA(h, launch_vecchia(a, s), "vecchia");
+    int64_t off = 0;
+    for (int64_t r = 0; r < P.rounds; ++r) {
+      const int64_t start = (r * P.world + rank) * P.chunk;
+      const int64_t cnt = P.n - start <= 0 ? 0 : (P.n - start < P.chunk ? P.n - start : P.chunk);
+      if (nccl_path) VIF_CUDA(h, cudaStreamWaitEvent(s, h->ev_ag[r], 0), "event wait");
+      if (cnt > 0) {
+        VecchiaArgs a;
+        a.U = h->buf<double>(B_U);
+        a.ldu = P.ld;
+        a.mk = P.mk;
+        a.ld = P.ld;
+        a.X = h->buf<double>(B_X);
+        a.nbr = h->buf<int32_t>(B_NBR);
+        a.mv = P.mv;
+        a.order = h->order[g] + off;
+        a.npts = cnt;
+        a.p = p;
+        a.W = h->buf<double>(B_W) + (size_t)off * P.ld;
+        a.ldw = P.ld;
+        a.Dpos = h->buf<double>(B_DPOS) + off;
+        a.B_out = B_out;
+        a.D_out = D_out;
+        a.st = st;
+        VIF_CUDA(h, launch_vecchia(a, s), "vecchia");
+        ++nl;
+      }
+      off += cnt;
+    }
     h->mark(S_VECCHIA, 1);
     double* G = h->buf<double>(B_G) + g * gstride;
     h->mark(S_SYRK, 0);
-    // default: 64x64 / 4-warp / 2-CTA SYRK (k_syrk.cu); VIF_SYRK128=1 selects the 128x128 engine
+    // default: 64x64 / 4-warp SYRK (k_syrk.cu); VIF_SYRK128=1 selects the 128x128 engine
     static const char* syrk128 = getenv("VIF_SYRK128");
     if (!(syrk128 && syrk128[0] == '1'))
       VIF_CUDA(h, launch_syrk(h->buf<double>(B_W), P.ld, npts, P.ld, P.nsplit_old, h->buf<double>(B_GPART), G, P.ld, s),
@@ -501,7 +527,7 @@ int vif_factor(void* handle, const vif_theta* theta, double* B_out, double* D_ou
     VIF_CUDA(h, launch_logd_sum(h->buf<double>(B_DPOS), npts, h->buf<double>(B_PART), kLogdParts,
                                 G + (size_t)P.ld * P.ld, s),
              "logd");
-    nl += 5;
+    nl += 4;
   }
   // A7
   if (P.emulate) {
@@ -637,6 +663,11 @@ void vif_destroy(void* handle) {
   Handle* h = reinterpret_cast<Handle*>(handle);
   if (!h) return;
   if (h->comm) nccl().CommDestroy(h->comm);
+  for (cudaEvent_t ev : h->ev_k1)
+    if (ev) cudaEventDestroy(ev);
+  for (cudaEvent_t ev : h->ev_ag)
+    if (ev) cudaEventDestroy(ev);
+  if (h->cstream) cudaStreamDestroy(h->cstream);
   for (int k = 0; k < S_COUNT; ++k)
     for (int j = 0; j < 2; ++j)
       if (h->ev[k][j]) cudaEventDestroy(h->ev[k][j]);
