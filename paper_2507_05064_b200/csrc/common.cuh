@@ -33,13 +33,15 @@ enum { FAM_M12 = 0, FAM_M32 = 1, FAM_M52 = 2, FAM_GAUSS = 3 };
 // 1/sqrt(x) for x > 0: MUFU.RSQ64H seed + two Newton steps (relative error ~1 ulp).  Inline: the
 // libdevice sqrt/div/rsqrt carry an out-of-line slow path whose CALL forces register spills in
 // the unrolled per-point Cholesky.  x <= 0 gives NaN/inf, which the callers test for.
+// One third-order step y (1 + r/2 + 3r^2/8), r = 1 - x y^2, instead of two Newton steps: the seed
+// error e (~2^-23) becomes O(e^3), and the dependent FP64 chain is 4 ops instead of 6 (each
+// dependent FP64 op waits ~16 cycles per DMMA-issuing warp on the SMSP: tools/dmma_mix.cu).
 __device__ __forceinline__ double rsqrt_nr(double x) {
   double y;
   asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
-  double r = fma(-x * y, y, 1.0);
-  y = fma(0.5 * y, r, y);
-  r = fma(-x * y, y, 1.0);
-  return fma(0.5 * y, r, y);
+  const double r = fma(-x * y, y, 1.0);
+  const double p = fma(0.375, r, 0.5);
+  return fma(y * r, p, y);
 }
 
 __device__ __forceinline__ double sqrt_nr(double x) { return x > 0.0 ? x * rsqrt_nr(x) : 0.0; }

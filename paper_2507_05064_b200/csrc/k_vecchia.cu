@@ -23,6 +23,10 @@ namespace vif {
 
 constexpr int VW = 4;  // warps per block
 
+// timing probe only (VIF_DEBUG_VECCHIA env, read at every launch): bit 0 skips the Gram phase,
+// bit 1 skips the scalar phases.  Never set in tests or bench.py.
+__constant__ int g_vif_debug;
+
 template <int RB>
 __host__ __device__ constexpr int vecchia_warp_doubles() {
   return RB * 8 * (RB * 8 + 1) + RB * 8;  // C (SP x (SP+1)) + coef (SP)
@@ -306,7 +310,7 @@ __global__ void __launch_bounds__(VW * 32, MINB) vecchia_reg_kernel(
     const int gi = Sidx[R * 8 + (lane >> 2)];
     rp[R] = gi >= 0 ? U + (int64_t)gi * ldu + 2 * (lane & 3) : nullptr;
   }
-  gram_ring<RB, NB>(rp, mk, acc);
+  if (!(g_vif_debug & 1)) gram_ring<RB, NB>(rp, mk, acc);  // debug probe: bit 0 skips the Gram
   // Gram tiles -> shared memory
   {
     int t = 0;
@@ -321,6 +325,10 @@ __global__ void __launch_bounds__(VW * 32, MINB) vecchia_reg_kernel(
   }
   __syncwarp();
 
+  if (g_vif_debug & 2) {  // debug probe: bit 1 skips steps 2-5 (timing only; outputs invalid)
+    if (lane == 0) Dpos[pos] = 1.0 + 1e-30 * C[0];
+    return;
+  }
   // ---- 2. C_S = K(X_S, X_S) - G_S + sigma^2 I on the lower triangle, evenly over lanes ----
   const int ne = s * (s + 1) / 2;
   for (int e = lane; e < ne; e += 32) {
@@ -980,6 +988,16 @@ static cudaError_t launch_rb(const VecchiaArgs& a, cudaStream_t s) {
       cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       if (e != cudaSuccess) return e;
       attr = smem;
+    }
+    {
+      const char* dbg = getenv("VIF_DEBUG_VECCHIA");
+      static int last = 0;
+      const int v = dbg ? atoi(dbg) : 0;
+      if (v != last) {
+        cudaMemcpyToSymbolAsync(g_vif_debug, &v, sizeof(int), 0, cudaMemcpyHostToDevice, s);
+        cudaStreamSynchronize(s);
+        last = v;
+      }
     }
     kern<<<blocks, VW * 32, smem, s>>>(a.U, a.ldu, a.mk, a.ld, a.X, a.nbr, a.mv, a.order, a.npts, a.p, a.W, a.ldw,
                                        a.Dpos, a.B_out, a.D_out, a.st);
