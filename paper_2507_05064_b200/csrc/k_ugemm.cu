@@ -25,15 +25,18 @@ __global__ void __launch_bounds__(256) kx_eval_kernel(const double* __restrict__
                                                       int mk, CovParams p, double* __restrict__ S,
                                                       double* __restrict__ Uaug, int ld) {
   // one warp per row; lanes stride over the columns.  Z and the 8 row coordinates are staged in
-  // shared memory (broadcast reads; a runtime-indexed register array would live in local memory).
+  // shared memory pre-scaled for cov_fast (broadcast reads; a runtime-indexed register array would
+  // live in local memory).
   extern __shared__ double kx_zs[];        // m x d
   __shared__ double kx_x[8][VIF_MAX_D];
+  __shared__ double tbl[64];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t pos = (int64_t)blockIdx.x * 8 + warp;
-  for (int e = threadIdx.x; e < m * p.d; e += blockDim.x) kx_zs[e] = Z[e];
+  exp_table_init(tbl, p.sigma2, threadIdx.x);
+  for (int e = threadIdx.x; e < m * p.d; e += blockDim.x) kx_zs[e] = Z[e] * (fam_scale<FAM>() * p.inv_ls[e % p.d]);
   const int64_t i = pos < npos ? pos_to_row(pos0 + pos, chunk, world, rank) : n;
   const bool valid = i < n;
-  if (lane < p.d) kx_x[warp][lane] = valid ? X[i * p.d + lane] : 0.0;
+  if (lane < p.d) kx_x[warp][lane] = valid ? X[i * p.d + lane] * (fam_scale<FAM>() * p.inv_ls[lane]) : 0.0;
   __syncthreads();
   if (pos >= npos) return;
   const double* x = kx_x[warp];
@@ -41,15 +44,7 @@ __global__ void __launch_bounds__(256) kx_eval_kernel(const double* __restrict__
 #pragma unroll 4
   for (int b = lane; b < mk; b += 32) {
     double v = 0.0;
-    if (valid && b < m) {
-      const double* z = kx_zs + b * p.d;
-      double r2 = 0.0;
-      for (int k = 0; k < p.d; ++k) {
-        const double t = (x[k] - z[k]) * p.inv_ls[k];
-        r2 = fma(t, t, r2);
-      }
-      v = p.sigma2 * cov_f<FAM>(r2);
-    }
+    if (valid && b < m) v = cov_fast<FAM>(x, kx_zs + b * p.d, p.d, tbl);
     srow[b] = v;
   }
   if (valid) {
