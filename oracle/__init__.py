@@ -58,6 +58,8 @@ def _load():
         _lib.oracle_partial.argtypes = [i64, i32, i32, P, P, P, P, P, i64, P, P, P, P, P]
         _lib.oracle_finish.argtypes = [i64, i32, P, P, P, P]
         _lib.oracle_num_threads.restype = ctypes.c_int
+        _lib.oracle_grad.argtypes = [i64, i32, i32, P, P, P, P, P, P, P, P]
+        _lib.oracle_dcov_matrix.argtypes = [P, P, i64, P, i64, P]
     return _lib
 
 
@@ -187,6 +189,43 @@ def finish(n, G, v, sums):
     if st != 0:
         raise OracleError(st, -1)
     return terms
+
+
+@dataclass
+class GradResult:
+    """dNLL/dtheta for theta = (sigma_1^2, lambda_1..lambda_d, sigma^2) and, per parameter, the
+    three derivative terms (d sum log D, d logdet M_w, d quad) whose halves sum to it."""
+    grad: np.ndarray
+    parts: np.ndarray
+
+
+def grad(X, Z, nbr, y, theta: Theta) -> GradResult:
+    """Oracle gradient of the VIF NLL (Appendix A; oracle.c oracle_grad)."""
+    lib = _load()
+    X, Z, y = _f64(X), _f64(Z).reshape(-1, X.shape[1]), _f64(y)
+    nbr = np.ascontiguousarray(nbr, dtype=np.int32)
+    n, mv = nbr.shape
+    m = Z.shape[0]
+    P = X.shape[1] + 2
+    g = np.zeros(P)
+    parts = np.zeros((P, 3))
+    bad = ctypes.c_int64(-1)
+    th, keep = theta._c()
+    st = lib.oracle_grad(n, m, mv, _p(X), _p(Z), _p(nbr), _p(y), ctypes.byref(th), _p(g), _p(parts),
+                         ctypes.byref(bad))
+    if st != 0:
+        raise OracleError(st, bad.value)
+    return GradResult(g, parts)
+
+
+def dcov_matrix(theta: Theta, A: np.ndarray, B: np.ndarray) -> np.ndarray:
+    """dk(A_i, B_j)/dtheta_p for p = sigma_1^2, lambda_1..lambda_d: shape (d+1, na, nb)."""
+    lib = _load()
+    A, B = _f64(A), _f64(B)
+    th, keep = theta._c()
+    out = np.empty((A.shape[1] + 1, A.shape[0], B.shape[0]))
+    lib.oracle_dcov_matrix(ctypes.byref(th), _p(A), A.shape[0], _p(B), B.shape[0], _p(out))
+    return out
 
 
 def num_threads() -> int:

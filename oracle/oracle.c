@@ -437,3 +437,311 @@ int oracle_num_threads(void) {
   return 1;
 #endif
 }
+
+/* =====================================================================================
+ * Gradient of the VIF Gaussian NLL with respect to theta = (sigma_1^2, lambda_1..lambda_d,
+ * sigma^2)  (P:126-133 and Appendix A).
+ *
+ * The paper's gradient is 1/2 tr(Sigma_dagger^{-1} dSigma_dagger) - 1/2 y^T Sigma_dagger^{-1}
+ * dSigma_dagger Sigma_dagger^{-1} y with dSigma_dagger = dSigma_s + dSigma_l, dB and dD from
+ * Appendix A.  It is evaluated here without n x n matrices by differentiating the three terms
+ * of the Woodbury/Sylvester form of the NLL that the factor above computes:
+ *   NLL = n/2 log 2pi + 1/2 sum log D_i + 1/2 logdet M_w + 1/2 quad,
+ *   M_w = I + sum w_i w_i^T / D_i,  v = sum w_i r_i / D_i,  quad = sum r_i^2/D_i - v^T M_w^{-1} v.
+ * Per parameter p (reading g1 in DESIGN.md):
+ *   dK_m, dk_i        kernel derivatives (or_dcov), jitter eps held fixed
+ *   Phi = L_m^{-1} dK_m L_m^{-T},  Phi_low = tril(Phi) with halved diagonal  (d L_m = L_m Phi_low)
+ *   du_i = L_m^{-1} dk_i - Phi_low u_i                                       (derivative of u_i)
+ *   dC(a,b) = dk(x_a,x_b) - (du_a.u_b + u_a.du_b) + [p = nugget][a = b]     (App. A brackets)
+ *   dA_i = C_NN^{-1} (dC_Ni - dC_NN A_i^T),  dD_i = dC_ii - 2 A_i.dC_Ni + A_i dC_NN A_i^T
+ *                                                                            (App. A: dB = -dA)
+ *   dw_i = du_i - sum_k (dA_ik u_Nk + A_ik du_Nk),  dr_i = -dA_i . y_N
+ *   dM = sum (dw w^T + w dw^T)/D - w w^T dD/D^2,  dv = sum (dw r + w dr)/D - w r dD/D^2
+ *   dlogdetD = sum dD/D,  dlogdetM = tr(M_w^{-1} dM),
+ *   dquad = sum (2 r dr/D - r^2 dD/D^2) - 2 z.dv + z^T dM z,   z = M_w^{-1} v
+ *   dNLL = 1/2 (dlogdetD + dlogdetM + dquad).
+ * Pinned in tests/test_oracle_grad.py against central finite differences of oracle_factor_nll,
+ * against the exact-GP gradient in the all-predecessor case, and against the paper's dense
+ * formula (P:128-131 with Appendix A) assembled in numpy.
+ * ===================================================================================== */
+
+/* dk(a,b)/dtheta_p, p = 0 (sigma_1^2), 1..d (lambda_j); the nugget has no kernel derivative.
+ * k = sigma_1^2 f(r): dk/dsigma_1^2 = f(r); dk/dlambda_j = sigma_1^2 (-f'(r)/r) Delta_j^2/lambda_j^3. */
+static void or_dcov(const or_theta *th, const double *a, const double *b, double *dk) {
+  double r2 = 0.0;
+  for (int k = 0; k < th->d; ++k) {
+    double t = (a[k] - b[k]) / th->lengthscale[k];
+    r2 += t * t;
+  }
+  double r = sqrt(r2), f, h; /* h = -f'(r)/r */
+  switch (th->family) {
+    case 0: f = exp(-r); h = r > 0.0 ? exp(-r) / r : 0.0; break;
+    case 1: f = (1.0 + sqrt(3.0) * r) * exp(-sqrt(3.0) * r); h = 3.0 * exp(-sqrt(3.0) * r); break;
+    case 2:
+      f = (1.0 + sqrt(5.0) * r + 5.0 * r2 / 3.0) * exp(-sqrt(5.0) * r);
+      h = (5.0 / 3.0) * (1.0 + sqrt(5.0) * r) * exp(-sqrt(5.0) * r);
+      break;
+    default: f = exp(-r2); h = 2.0 * exp(-r2); break;
+  }
+  dk[0] = f;
+  for (int j = 0; j < th->d; ++j) {
+    double lj = th->lengthscale[j], dj = a[j] - b[j];
+    dk[1 + j] = th->sigma2 * h * dj * dj / (lj * lj * lj);
+  }
+}
+
+/* exported: d (kernel) matrices for the pins: out[p][i][j] = dk(A_i, B_j)/dtheta_p, p < d+1 */
+int oracle_dcov_matrix(const or_theta *th, const double *A, int64_t na, const double *B, int64_t nb,
+                       double *out) {
+  int np = th->d + 1;
+  double dk[1 + 16 + 1];
+  for (int64_t i = 0; i < na; ++i)
+    for (int64_t j = 0; j < nb; ++j) {
+      or_dcov(th, A + i * th->d, B + j * th->d, dk);
+      for (int p = 0; p < np; ++p) out[((size_t)p * na + i) * nb + j] = dk[p];
+    }
+  return OR_OK;
+}
+
+/* per-row quantities of the factor (same arithmetic as oracle_factor_nll steps 3-4) */
+typedef struct {
+  int q;
+  double D, r;
+} or_rowinfo;
+
+int oracle_grad(int64_t n, int m, int mv, const double *X, const double *Z, const int32_t *nbr,
+                const double *y, const or_theta *th, double *grad, double *parts, int64_t *bad_row) {
+  *bad_row = -1;
+  const int d = th->d, P = d + 2;
+  if (n < 1 || m < 0 || mv < 0 || d < 1 || d > 16) return OR_INVALID;
+  const int m1 = m > 0 ? m : 1, s_max = mv + 1;
+  double *Lm = NULL, *U = NULL, *dU = NULL, *Phi = NULL, *dKm = NULL;
+  double *A = (double *)malloc(sizeof(double) * (size_t)n * (mv > 0 ? mv : 1));
+  double *W = (double *)malloc(sizeof(double) * (size_t)n * m1);
+  or_rowinfo *info = (or_rowinfo *)malloc(sizeof(or_rowinfo) * (size_t)n);
+  if (!A || !W || !info) { free(A); free(W); free(info); return OR_NOMEM; }
+  int status = OR_OK;
+  if (m > 0) {
+    Lm = (double *)malloc(sizeof(double) * (size_t)m * m);
+    U = (double *)malloc(sizeof(double) * (size_t)n * m);
+    dU = (double *)malloc(sizeof(double) * (size_t)n * m);
+    Phi = (double *)malloc(sizeof(double) * (size_t)m * m);
+    dKm = (double *)malloc(sizeof(double) * (size_t)m * m);
+    if (!Lm || !U || !dU || !Phi || !dKm) { status = OR_NOMEM; goto done; }
+    if (or_build_Lm(th, Z, m, Lm) != OR_OK) { status = OR_NOT_PD; goto done; }
+#pragma omp parallel for schedule(static)
+    for (int64_t i = 0; i < n; ++i) or_u_row(th, Z, m, Lm, X + i * d, U + i * (size_t)m);
+  }
+  /* ---- pass 0: A_i, D_i, w_i, r_i (steps 3-4 of the factor) and M_w, v ---- */
+  {
+    int64_t badr = -1;
+#pragma omp parallel
+    {
+      int32_t *S = (int32_t *)malloc(sizeof(int32_t) * s_max);
+      double *uS = (double *)malloc(sizeof(double) * (size_t)s_max * m1);
+      double *work = (double *)malloc(sizeof(double) * (size_t)s_max * s_max);
+#pragma omp for schedule(static)
+      for (int64_t i = 0; i < n; ++i) {
+        const int32_t *row = nbr + i * mv;
+        int q = or_count_nbrs(row, mv), s = q + 1;
+        for (int p = 0; p < q; ++p) S[p] = row[p];
+        S[q] = (int32_t)i;
+        for (int p = 0; p < s; ++p)
+          for (int k = 0; k < m; ++k) uS[(size_t)p * m + k] = U[(size_t)S[p] * m + k];
+        double Di, *a = A + i * mv;
+        int b = or_vecchia_row(th, X, S, s, uS, m, work, a, &Di);
+        if (b >= 0 || !(Di > 0.0)) {
+#pragma omp critical
+          { if (badr < 0 || i < badr) badr = i; }
+          continue;
+        }
+        double r = y[i];
+        for (int p = 0; p < q; ++p) r -= a[p] * y[S[p]];
+        for (int k = 0; k < m; ++k) {
+          double t = uS[(size_t)q * m + k];
+          for (int p = 0; p < q; ++p) t -= a[p] * uS[(size_t)p * m + k];
+          W[i * (size_t)m + k] = t;
+        }
+        info[i].q = q;
+        info[i].D = Di;
+        info[i].r = r;
+      }
+      free(S); free(uS); free(work);
+    }
+    if (badr >= 0) { *bad_row = badr; status = OR_NOT_PD; goto done; }
+  }
+  /* M_w, v (serial, row order), Minv = M_w^{-1}, z = M_w^{-1} v */
+  double *M = (double *)calloc((size_t)m1 * m1 * 2 + 2 * m1, sizeof(double));
+  double *Minv = M + (size_t)m1 * m1, *v = Minv + (size_t)m1 * m1, *z = v + m1;
+  for (int64_t i = 0; i < n; ++i) {
+    const double *w = W + i * (size_t)m;
+    for (int k = 0; k < m; ++k) {
+      for (int l = 0; l < m; ++l) M[(size_t)k * m + l] += w[k] * w[l] / info[i].D;
+      v[k] += w[k] * info[i].r / info[i].D;
+    }
+  }
+  if (m > 0) {
+    for (int k = 0; k < m; ++k) M[(size_t)k * m + k] += 1.0;
+    if (or_chol(M, m, m) >= 0) { free(M); status = OR_NOT_PD; goto done; }
+    for (int c = 0; c < m; ++c) { /* column c of M^{-1}: L L^T x = e_c */
+      double *e = (double *)calloc(m, sizeof(double));
+      e[c] = 1.0;
+      or_fwd(M, m, m, e);
+      or_bwd(M, m, m, e);
+      for (int k = 0; k < m; ++k) Minv[(size_t)k * m + c] = e[k];
+      free(e);
+    }
+    for (int k = 0; k < m; ++k) z[k] = v[k];
+    or_fwd(M, m, m, z);
+    or_bwd(M, m, m, z);
+  }
+  /* ---- one pass per parameter ---- */
+  for (int p = 0; p < P; ++p) {
+    const int is_nugget = p == d + 1;
+    if (m > 0) {
+      if (is_nugget) {
+        memset(dU, 0, sizeof(double) * (size_t)n * m);
+      } else {
+        /* dK_m and Phi = L^{-1} dK_m L^{-T} (column solves; dK_m symmetric) */
+        double dk[1 + 16 + 1];
+        for (int a = 0; a < m; ++a)
+          for (int b = 0; b < m; ++b) {
+            or_dcov(th, Z + (size_t)a * d, Z + (size_t)b * d, dk);
+            dKm[(size_t)a * m + b] = dk[p];
+          }
+        double *col = (double *)malloc(sizeof(double) * m);
+        for (int c = 0; c < m; ++c) { /* T = L^{-1} dK_m, column c; stored transposed in Phi */
+          for (int k = 0; k < m; ++k) col[k] = dKm[(size_t)k * m + c];
+          or_fwd(Lm, m, m, col);
+          for (int k = 0; k < m; ++k) Phi[(size_t)c * m + k] = col[k]; /* Phi = T^T = dK L^{-T} */
+        }
+        double *T2 = (double *)malloc(sizeof(double) * (size_t)m * m);
+        for (int c = 0; c < m; ++c) { /* L^{-1} (dK L^{-T}), column c */
+          for (int k = 0; k < m; ++k) col[k] = Phi[(size_t)k * m + c];
+          or_fwd(Lm, m, m, col);
+          for (int k = 0; k < m; ++k) T2[(size_t)k * m + c] = col[k];
+        }
+        for (int a = 0; a < m; ++a)
+          for (int b = 0; b < m; ++b)
+            Phi[(size_t)a * m + b] = b < a ? T2[(size_t)a * m + b] : (b == a ? 0.5 * T2[(size_t)a * m + a] : 0.0);
+        free(T2);
+        free(col);
+#pragma omp parallel for schedule(static)
+        for (int64_t i = 0; i < n; ++i) {
+          double dkk[1 + 16 + 1], *du = dU + i * (size_t)m;
+          for (int a = 0; a < m; ++a) {
+            or_dcov(th, Z + (size_t)a * d, X + i * d, dkk);
+            du[a] = dkk[p];
+          }
+          or_fwd(Lm, m, m, du);
+          const double *u = U + i * (size_t)m;
+          for (int a = 0; a < m; ++a) {
+            double t = 0.0;
+            for (int b = 0; b <= a; ++b) t += Phi[(size_t)a * m + b] * u[b];
+            du[a] -= t;
+          }
+        }
+      }
+    }
+    /* row pass: dD, dw, dr -> dM, dv, scalars; per-thread partials merged in thread order */
+    int nthreads = 1;
+#ifdef _OPENMP
+    nthreads = omp_get_max_threads();
+#endif
+    const size_t stride = (size_t)m1 * m1 + m1 + 2;
+    double *part = (double *)calloc((size_t)nthreads * stride, sizeof(double));
+#pragma omp parallel num_threads(nthreads)
+    {
+      int tid = 0;
+#ifdef _OPENMP
+      tid = omp_get_thread_num();
+#endif
+      double *dM = part + (size_t)tid * stride, *dv = dM + (size_t)m1 * m1, *sc = dv + m1;
+      int32_t *S = (int32_t *)malloc(sizeof(int32_t) * s_max);
+      double *C = (double *)malloc(sizeof(double) * (size_t)s_max * s_max);
+      double *dC = (double *)malloc(sizeof(double) * (size_t)s_max * s_max);
+      double *da = (double *)malloc(sizeof(double) * s_max);
+      double *dw = (double *)malloc(sizeof(double) * m1);
+#pragma omp for schedule(static)
+      for (int64_t i = 0; i < n; ++i) {
+        const int q = info[i].q, s = q + 1;
+        const int32_t *row = nbr + i * mv;
+        for (int k = 0; k < q; ++k) S[k] = row[k];
+        S[q] = (int32_t)i;
+        const double *a = A + i * mv;
+        const double Di = info[i].D, ri = info[i].r;
+        /* C and dC on S (App. A brackets) */
+        for (int u1 = 0; u1 < s; ++u1)
+          for (int u2 = 0; u2 < s; ++u2) {
+            const double *xa = X + (size_t)S[u1] * d, *xb = X + (size_t)S[u2] * d;
+            double dk[1 + 16 + 1];
+            or_dcov(th, xa, xb, dk);
+            double c = or_cov(th, xa, xb), dc = is_nugget ? 0.0 : dk[p];
+            for (int k = 0; k < m; ++k) {
+              const double ua = U[(size_t)S[u1] * m + k], ub = U[(size_t)S[u2] * m + k];
+              c -= ua * ub;
+              dc -= dU[(size_t)S[u1] * m + k] * ub + ua * dU[(size_t)S[u2] * m + k];
+            }
+            if (u1 == u2) { c += th->nugget; if (is_nugget) dc += 1.0; }
+            C[(size_t)u1 * s + u2] = c;
+            dC[(size_t)u1 * s + u2] = dc;
+          }
+        /* dA = C_NN^{-1} (dC_Ni - dC_NN a),  dD */
+        double dD = dC[(size_t)q * s + q];
+        for (int k = 0; k < q; ++k) {
+          double t = dC[(size_t)k * s + q];
+          for (int l = 0; l < q; ++l) t -= dC[(size_t)k * s + l] * a[l];
+          da[k] = t;
+          dD -= 2.0 * a[k] * dC[(size_t)k * s + q];
+          for (int l = 0; l < q; ++l) dD += a[k] * dC[(size_t)k * s + l] * a[l];
+        }
+        if (q > 0) {
+          or_chol(C, q, s); /* succeeded in pass 0 */
+          or_fwd(C, q, s, da);
+          or_bwd(C, q, s, da);
+        }
+        /* dw, dr */
+        double dr = 0.0;
+        for (int k = 0; k < q; ++k) dr -= da[k] * y[S[k]];
+        for (int c = 0; c < m; ++c) {
+          double t = dU[(size_t)i * m + c];
+          for (int k = 0; k < q; ++k) t -= da[k] * U[(size_t)S[k] * m + c] + a[k] * dU[(size_t)S[k] * m + c];
+          dw[c] = t;
+        }
+        const double *w = W + i * (size_t)m;
+        const double iD = 1.0 / Di, iD2 = dD / (Di * Di);
+        for (int k = 0; k < m; ++k) {
+          for (int l = 0; l < m; ++l) dM[(size_t)k * m + l] += (dw[k] * w[l] + w[k] * dw[l]) * iD - w[k] * w[l] * iD2;
+          dv[k] += (dw[k] * ri + w[k] * dr) * iD - w[k] * ri * iD2;
+        }
+        sc[0] += dD * iD;                               /* dlogdetD */
+        sc[1] += 2.0 * ri * dr * iD - ri * ri * iD2;    /* d sum r^2/D */
+      }
+      free(S); free(C); free(dC); free(da); free(dw);
+    }
+    double *acc = (double *)calloc(stride, sizeof(double));
+    for (int t = 0; t < nthreads; ++t)
+      for (size_t k = 0; k < stride; ++k) acc[k] += part[(size_t)t * stride + k];
+    double *dM = acc, *dv = acc + (size_t)m1 * m1, *sc = dv + m1;
+    double dlogdetM = 0.0, dquad = sc[1];
+    for (int k = 0; k < m; ++k) {
+      for (int l = 0; l < m; ++l) {
+        dlogdetM += Minv[(size_t)k * m + l] * dM[(size_t)l * m + k];
+        dquad += z[k] * dM[(size_t)k * m + l] * z[l];
+      }
+      dquad -= 2.0 * z[k] * dv[k];
+    }
+    grad[p] = 0.5 * (sc[0] + dlogdetM + dquad);
+    if (parts) {
+      parts[3 * p + 0] = sc[0];
+      parts[3 * p + 1] = dlogdetM;
+      parts[3 * p + 2] = dquad;
+    }
+    free(acc);
+    free(part);
+  }
+  free(M);
+done:
+  free(A); free(W); free(info); free(Lm); free(U); free(dU); free(Phi); free(dKm);
+  return status;
+}

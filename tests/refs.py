@@ -45,3 +45,26 @@ def B_matrix(nbr, Bvals):
             if j >= 0:
                 B[i, j] = Bvals[i, k]
     return B
+
+
+def sk_cov_grad(family, sigma2, lengthscale, A):
+    """K(A, A) and dK/dtheta for theta = (sigma_1^2, lambda_1..lambda_d) from scikit-learn's
+    analytic kernel gradients (eval_gradient=True returns dK/dlog(length_scale_j))."""
+    ls = np.asarray(lengthscale, dtype=np.float64)
+    A = np.atleast_2d(A)
+    if family == "gaussian":
+        k = RBF(length_scale=ls / np.sqrt(2.0))
+    else:
+        k = Matern(length_scale=ls, nu=NU[family])
+    K, G = k(A, eval_gradient=True)        # G[..., j] = dK / dlog ls_j (ls_j proportional to lambda_j)
+    if G.shape[2] == 1 and len(ls) > 1:     # isotropic fallback never used (ls is an array)
+        raise ValueError("expected per-dimension gradients")
+    dK = [K] + [sigma2 * G[:, :, j] / ls[j] for j in range(len(ls))]
+    return sigma2 * K, np.stack(dK)
+
+
+def dense_grad(S, dS, y):
+    """Gaussian NLL gradient with covariance S: 1/2 tr(S^{-1} dS_p) - 1/2 a^T dS_p a, a = S^{-1} y."""
+    Si = np.linalg.inv(S)
+    a = Si @ y
+    return np.array([0.5 * np.trace(Si @ d) - 0.5 * a @ d @ a for d in dS])
