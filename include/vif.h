@@ -129,6 +129,20 @@ int vif_factor(void* handle, const vif_theta* theta, double* B_out, double* D_ou
  * Errors: STATE (no vif_factor since create), NOT_PD (terms->bad_row says where), CUDA, NCCL. */
 int vif_nll(void* handle, vif_terms* out);
 
+/* Gradient of the NLL (dB, dD of Appendix A) with respect to
+ * theta = (sigma_1^2, lambda_1, ..., lambda_d, sigma^2): d + 2 partial derivatives; the jitter is
+ * held fixed (an isotropic range rho has dNLL/drho = sum_j dNLL/dlambda_j).
+ * vif_grad_workspace_bytes: size of the second, caller-owned device workspace the gradient needs
+ * (Q (ld x ld), g rows and dU (n x ld each), m x m scratch; ld = roundup(roundup(m,8)+1, 8)).
+ * vif_grad runs vif_factor + vif_nll at theta, then per parameter dK(Z,Z), Phi = L_m^{-1} dK_m
+ * L_m^{-T}, dK(X,Z), dU and one pass over the points (Gram, cross-Gram, Cholesky, dA_i, dD_i), and
+ * synchronises.  grad: host, d + 2 doubles.  terms (optional): as vif_nll.
+ * Errors: INVALID_ARG (theta; world > 1 or m_v > 31: not supported by this version), NO_MEMORY
+ * (grad workspace too small), NOT_PD (as vif_nll), CUDA. */
+int vif_grad_workspace_bytes(const vif_dims* dims, size_t* bytes);
+int vif_grad(void* handle, const vif_theta* theta, void* grad_workspace, size_t grad_ws_bytes, double* grad,
+             vif_terms* terms);
+
 /* Debug / parity: copy the whitened features U (n x m, row-major) to `out` (device or host). */
 int vif_copy_U(void* handle, double* out);
 

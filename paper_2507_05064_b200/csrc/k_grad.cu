@@ -1,0 +1,464 @@
+// k_grad.cu -- gradient of the VIF Gaussian NLL with respect to
+// theta = (sigma_1^2, lambda_1..lambda_d, sigma^2)   (Appendix A).
+//
+// Differentiating NLL = n/2 log 2pi + 1/2 sum log D_i + NLL_G(G), G = sum_i a_i a_i^T,
+// a_i = [w_i, r_i] = sum_k c_ik U_aug[S_k] (c_i = [-A_i, 1] / sqrt(D_i), reading c4):
+//   dNLL_G = tr(Q dG) = sum_i g_i . da_i,   g_i = 2 Q a_i,
+//   Q = [[ (M_w^{-1} + z z^T)/2, -z/2 ], [ -z^T/2, 1/2 ]],  z = M_w^{-1} G_Wr   (reading g1),
+//   da_i = sum_k dc_ik U_aug[S_k] + c_ik dU_aug[S_k],
+//   dU = dK(X,Z) L_m^{-T} - U Phi_low^T,  Phi_low = tril(L_m^{-1} dK_m L_m^{-T}), halved diagonal,
+//   dc_i from dA_i = C_NN^{-1} (dC_Ni - dC_NN A_i^T), dD_i = dC_ii - 2 A_i.dC_Ni + A_i dC_NN A_i^T,
+//   dC_S = dK_SS + [p = nugget] I - (dU_S U_S^T + U_S dU_S^T)           (Appendix A brackets).
+// Per parameter p:   dK_m -> Phi (two DMMA GEMMs) -> Phi_low;  dK(X,Z) (kx_deriv_kernel) -> dU (two
+// triangular DMMA GEMMs, gemm_tn);  one warp per point (vecchia_grad_kernel): Gram and the symmetric
+// cross-Gram dU_S U_S^T + U_S dU_S^T on DMMA, the dots g_i . U_aug[S_k] and g_i . dU_aug[S_k] in the
+// same pass over the gathered rows, then Cholesky, A_i, D_i, dA_i, dD_i and the point's contribution
+// 1/2 dD_i/D_i + sum_k dc_ik (g_i.U_S_k) + c_ik (g_i.dU_S_k); block partials, fixed-order reduction.
+#include "common.cuh"
+#include "kernels.h"
+
+namespace vif {
+
+namespace {
+
+// dk(a,b)/dtheta_p for p = 0 (sigma_1^2) and p = 1..d (lambda_{p-1}); exact libdevice arithmetic.
+// k = sigma_1^2 f(r): dk/dsigma_1^2 = f(r), dk/dlambda_j = sigma_1^2 h(r) Delta_j^2 / lambda_j^3 with
+// h = -f'(r)/r: M12 e^{-r}/r, M32 3 e^{-sqrt3 r}, M52 5/3 (1 + sqrt5 r) e^{-sqrt5 r}, Gaussian 2 e^{-r^2}.
+template <int FAM>
+__device__ __forceinline__ double dcov(const double* __restrict__ a, const double* __restrict__ b, int pidx,
+                                       const CovParams& p) {
+  double r2 = 0.0;
+  for (int k = 0; k < p.d; ++k) {
+    const double t = (a[k] - b[k]) * p.inv_ls[k];
+    r2 = fma(t, t, r2);
+  }
+  const double r = sqrt(r2);
+  if (pidx == 0) {
+    if (FAM == FAM_M12) return exp(-r);
+    if (FAM == FAM_M32) return (1.0 + 1.7320508075688772 * r) * exp(-1.7320508075688772 * r);
+    if (FAM == FAM_M52) return (1.0 + 2.23606797749979 * r + (5.0 / 3.0) * r2) * exp(-2.23606797749979 * r);
+    return exp(-r2);
+  }
+  double h;
+  if (FAM == FAM_M12) h = r > 0.0 ? exp(-r) / r : 0.0;
+  else if (FAM == FAM_M32) h = 3.0 * exp(-1.7320508075688772 * r);
+  else if (FAM == FAM_M52) h = (5.0 / 3.0) * (1.0 + 2.23606797749979 * r) * exp(-2.23606797749979 * r);
+  else h = 2.0 * exp(-r2);
+  const int j = pidx - 1;
+  const double il = p.inv_ls[j], dj = a[j] - b[j];
+  return p.sigma2 * h * dj * dj * il * il * il;
+}
+
+template <int FAM>
+__global__ void dkm_kernel(const double* __restrict__ Z, int m, int mk, int pidx, CovParams p,
+                           double* __restrict__ out) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= (int64_t)mk * mk) return;
+  const int a = (int)(e / mk), b = (int)(e % mk);
+  out[e] = (a < m && b < m) ? dcov<FAM>(Z + (size_t)a * p.d, Z + (size_t)b * p.d, pidx, p) : 0.0;
+}
+
+// Phi_low = tril(Phi) with halved diagonal, zero above (so the triangular GEMM may read whole blocks)
+__global__ void phi_low_kernel(const double* __restrict__ Phi, int mk, double* __restrict__ out) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= (int64_t)mk * mk) return;
+  const int a = (int)(e / mk), b = (int)(e % mk);
+  out[e] = b < a ? Phi[e] : (b == a ? 0.5 * Phi[e] : 0.0);
+}
+
+// S[pos][b] = dk(x_pos, z_b)/dtheta_p (single rank: row i = pos), zero for b in [m, mk)
+template <int FAM>
+__global__ void __launch_bounds__(256) kx_deriv_kernel(const double* __restrict__ X, const double* __restrict__ Z,
+                                                       int64_t npos, int m, int mk, int pidx, CovParams p,
+                                                       double* __restrict__ S) {
+  extern __shared__ double zs[];  // m x d
+  __shared__ double xrow[8][VIF_MAX_D];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t pos = (int64_t)blockIdx.x * 8 + warp;
+  for (int e = threadIdx.x; e < m * p.d; e += blockDim.x) zs[e] = Z[e];
+  if (lane < p.d) xrow[warp][lane] = pos < npos ? X[pos * p.d + lane] : 0.0;
+  __syncthreads();
+  if (pos >= npos) return;
+  double* srow = S + pos * (int64_t)mk;
+#pragma unroll 4
+  for (int b = lane; b < mk; b += 32) srow[b] = b < m ? dcov<FAM>(xrow[warp], zs + b * p.d, pidx, p) : 0.0;
+}
+
+// zh = Linv g (g = G[ycol][0..m)), Linv lower (ld ldi)
+__global__ void zhalf_kernel(const double* __restrict__ Linv, int ldi, const double* __restrict__ G, int ldg,
+                             int ycol, int m, double* __restrict__ zh) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= m) return;
+  double s = 0.0;
+  for (int j = 0; j <= k; ++j) s = fma(Linv[(size_t)k * ldi + j], G[(size_t)ycol * ldg + j], s);
+  zh[k] = s;
+}
+
+// z = Linv^T zh  (z = M_w^{-1} G_Wr)
+__global__ void zfull_kernel(const double* __restrict__ Linv, int ldi, const double* __restrict__ zh, int m,
+                             double* __restrict__ z) {
+  const int a = blockIdx.x * blockDim.x + threadIdx.x;
+  if (a >= m) return;
+  double s = 0.0;
+  for (int k = a; k < m; ++k) s = fma(Linv[(size_t)k * ldi + a], zh[k], s);
+  z[a] = s;
+}
+
+// Q2 = 2 Q (ld x ld): [[M^{-1} + z z^T, -z], [-z^T, 1]] on the W columns [0, m) and the y column;
+// M^{-1} = Linv^T Linv
+__global__ void q_kernel(const double* __restrict__ Linv, int ldi, const double* __restrict__ z, int m, int ycol,
+                         int ld, double* __restrict__ Q2) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= (int64_t)ld * ld) return;
+  const int a = (int)(e / ld), b = (int)(e % ld);
+  double v = 0.0;
+  if (a < m && b < m) {
+    const int k0 = a > b ? a : b;
+    for (int k = k0; k < m; ++k) v = fma(Linv[(size_t)k * ldi + a], Linv[(size_t)k * ldi + b], v);
+    v = fma(z[a], z[b], v);
+  } else if (a < m && b == ycol) {
+    v = -z[a];
+  } else if (a == ycol && b < m) {
+    v = -z[b];
+  } else if (a == ycol && b == ycol) {
+    v = 1.0;
+  }
+  Q2[e] = v;
+}
+
+__global__ void grad_reduce_kernel(const double* __restrict__ part, int64_t nparts, double* __restrict__ out) {
+  __shared__ double red[1024];
+  double s = 0.0;
+  for (int64_t k = threadIdx.x; k < nparts; k += blockDim.x) s += part[k];  // fixed assignment and order
+  red[threadIdx.x] = s;
+  __syncthreads();
+  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+    if ((int)threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *out = red[0];
+}
+
+constexpr int GW = 4;  // warps (points) per block
+
+template <int RB>
+__host__ __device__ constexpr int grad_warp_doubles(int d) {
+  return 2 * (RB * 8) * (RB * 8 + 1) + 3 * (RB * 8) + RB * 8 * d;  // C, dC, abuf, gam, gamd, xs
+}
+
+template <int FAM, int RB>
+__global__ void __launch_bounds__(GW * 32, 3) vecchia_grad_kernel(
+    const double* __restrict__ U, const double* __restrict__ dU, const double* __restrict__ Gam, int64_t ldu, int mk,
+    int ld, const double* __restrict__ X, const int32_t* __restrict__ nbr, int mv, const int64_t* __restrict__ order,
+    int64_t npts, CovParams p, int pidx, double* __restrict__ part) {
+  constexpr int SP = RB * 8;
+  constexpr int CS = SP + 1;
+  constexpr int NT = RB * (RB + 1) / 2;
+  static_assert(SP <= 32, "gradient kernel needs s <= 32");
+  extern __shared__ __align__(16) double gsm_[];
+  __shared__ int Sidx_all[GW][SP];
+  __shared__ double wsum[GW];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double* C = gsm_ + warp * grad_warp_doubles<RB>(p.d);
+  double* dC = C + SP * CS;
+  double* abuf = dC + SP * CS;
+  double* gam_s = abuf + SP;
+  double* gamd_s = gam_s + SP;
+  double* xs = gamd_s + SP;
+  int* Sidx = Sidx_all[warp];
+  const int64_t pos = (int64_t)blockIdx.x * GW + warp;
+  double contrib = 0.0;
+  if (pos < npts) {
+    const int64_t i = order[pos];
+    const int nb0 = lane < mv ? nbr[i * mv + lane] : -1;
+    const int q = __popc(__ballot_sync(0xffffffffu, nb0 >= 0));
+    const int s = q + 1;
+    const int myidx = lane < q ? nb0 : (lane == q ? (int)i : -1);
+    if (lane < SP) Sidx[lane] = myidx;
+    if (lane < s)
+      for (int k = 0; k < p.d; ++k) xs[lane * p.d + k] = X[(int64_t)myidx * p.d + k];
+    __syncwarp();
+
+    // ---- Gram, symmetric cross-Gram and the g_i dots in one pass over the gathered rows ----
+    double acc[NT][2], dacc[NT][2], gm[RB], gmd[RB];
+#pragma unroll
+    for (int t = 0; t < NT; ++t) acc[t][0] = acc[t][1] = dacc[t][0] = dacc[t][1] = 0.0;
+#pragma unroll
+    for (int R = 0; R < RB; ++R) gm[R] = gmd[R] = 0.0;
+    const double* rp[RB];
+    const double* drp[RB];
+#pragma unroll
+    for (int R = 0; R < RB; ++R) {
+      const int gi = Sidx[R * 8 + (lane >> 2)];
+      rp[R] = gi >= 0 ? U + (int64_t)gi * ldu + 2 * (lane & 3) : nullptr;
+      drp[R] = (gi >= 0 && dU) ? dU + (int64_t)gi * ldu + 2 * (lane & 3) : nullptr;
+    }
+    const double* grow = Gam + pos * (int64_t)ld + 2 * (lane & 3);
+    for (int k0 = 0; k0 < ld; k0 += 8) {
+      const double2 g2 = __ldg(reinterpret_cast<const double2*>(grow + k0));
+      double2 f[RB], df[RB];
+#pragma unroll
+      for (int R = 0; R < RB; ++R) {
+        f[R] = rp[R] ? __ldg(reinterpret_cast<const double2*>(rp[R] + k0)) : make_double2(0.0, 0.0);
+        df[R] = drp[R] ? __ldg(reinterpret_cast<const double2*>(drp[R] + k0)) : make_double2(0.0, 0.0);
+      }
+#pragma unroll
+      for (int R = 0; R < RB; ++R) {
+        gm[R] = fma(f[R].x, g2.x, fma(f[R].y, g2.y, gm[R]));
+        gmd[R] = fma(df[R].x, g2.x, fma(df[R].y, g2.y, gmd[R]));
+      }
+      if (k0 < mk) {  // the Gram runs over the whitened columns only (not y, not the padding)
+        int t = 0;
+#pragma unroll
+        for (int R1 = 0; R1 < RB; ++R1)
+#pragma unroll
+          for (int R2 = 0; R2 <= R1; ++R2, ++t) {
+            dmma884(acc[t][0], acc[t][1], f[R1].x, f[R2].x);
+            dmma884(acc[t][0], acc[t][1], f[R1].y, f[R2].y);
+            if (dU) {
+              dmma884(dacc[t][0], dacc[t][1], df[R1].x, f[R2].x);
+              dmma884(dacc[t][0], dacc[t][1], df[R1].y, f[R2].y);
+              dmma884(dacc[t][0], dacc[t][1], f[R1].x, df[R2].x);
+              dmma884(dacc[t][0], dacc[t][1], f[R1].y, df[R2].y);
+            }
+          }
+      }
+    }
+    // dots: the 4 lanes of a row hold partial sums over their k-pairs
+#pragma unroll
+    for (int R = 0; R < RB; ++R) {
+      gm[R] += __shfl_xor_sync(0xffffffffu, gm[R], 1);
+      gm[R] += __shfl_xor_sync(0xffffffffu, gm[R], 2);
+      gmd[R] += __shfl_xor_sync(0xffffffffu, gmd[R], 1);
+      gmd[R] += __shfl_xor_sync(0xffffffffu, gmd[R], 2);
+      if ((lane & 3) == 0) {
+        gam_s[R * 8 + (lane >> 2)] = gm[R];
+        gamd_s[R * 8 + (lane >> 2)] = gmd[R];
+      }
+    }
+    {
+      int t = 0;
+#pragma unroll
+      for (int R1 = 0; R1 < RB; ++R1)
+#pragma unroll
+        for (int R2 = 0; R2 <= R1; ++R2, ++t) {
+          const int r = R1 * 8 + (lane >> 2), c = R2 * 8 + 2 * (lane & 3);
+          C[r * CS + c] = acc[t][0];
+          C[r * CS + c + 1] = acc[t][1];
+          dC[r * CS + c] = dacc[t][0];
+          dC[r * CS + c + 1] = dacc[t][1];
+        }
+    }
+    __syncwarp();
+    // ---- C_S = K + sigma^2 I - G,  dC_S = dK + [nugget] I - dG (lower triangle) ----
+    const int ne = s * (s + 1) / 2;
+    for (int e = lane; e < ne; e += 32) {
+      int r = (int)((sqrtf_fast(8.0f * (float)e + 1.0f) - 1.0f) * 0.5f);
+      if ((r + 1) * (r + 2) / 2 <= e) ++r;
+      if (r * (r + 1) / 2 > e) --r;
+      const int c = e - r * (r + 1) / 2;
+      const double* xa = xs + r * p.d;
+      const double* xb = xs + c * p.d;
+      double v = cov<FAM>(xa, xb, p) - C[r * CS + c];
+      double dv = (pidx <= p.d ? dcov<FAM>(xa, xb, pidx, p) : 0.0) - dC[r * CS + c];
+      if (r == c) {
+        v += p.nugget;
+        if (pidx == p.d + 1) dv += 1.0;
+      }
+      C[r * CS + c] = v;
+      dC[r * CS + c] = dv;
+    }
+    __syncwarp();
+
+    // ---- Cholesky of C_S (i last), row `lane` in registers; padded rows identity ----
+    double crow[SP];
+#pragma unroll
+    for (int c = 0; c < SP; ++c) {
+      double v = 0.0;
+      if (lane < s) {
+        if (c <= lane) v = C[lane * CS + c];
+      } else if (c == lane) {
+        v = 1.0;
+      }
+      crow[c] = v;
+    }
+    bool ok = true;
+    double Di = 0.0, myinv = 1.0;
+    double* colbuf = abuf;  // [SP], reused: the broadcast column of step j (single buffer + syncs)
+#pragma unroll
+    for (int j = 0; j < SP; ++j) {
+      const double djj = __shfl_sync(0xffffffffu, crow[j], j);
+      if (j < s) {
+        ok = ok && (djj > 0.0);
+        if (j == s - 1) Di = djj;
+      }
+      const double y = rsqrt_nr(djj);
+      const double lrj = crow[j] * y;
+      crow[j] = lrj;
+      if (lane == j) myinv = y;
+      if (j + 1 < SP) {
+        __syncwarp();
+        if (lane < SP) colbuf[lane] = lrj;
+        __syncwarp();
+#pragma unroll
+        for (int c = j + 1; c < SP; ++c) crow[c] = fma(-lrj, colbuf[c], crow[c]);
+      }
+    }
+    __syncwarp();
+#pragma unroll
+    for (int c = 0; c < SP; ++c)
+      if (lane < SP) C[lane * CS + c] = crow[c];
+    __syncwarp();
+    // A_i^T = L_NN^{-T} l (lane k holds a_k)
+    double a = lane < q ? C[q * CS + lane] : 0.0;
+    for (int j = q - 1; j >= 0; --j) {
+      const double xj = __shfl_sync(0xffffffffu, a * myinv, j);
+      if (lane == j) a = xj;
+      else if (lane < j) a = fma(-C[j * CS + lane], xj, a);
+    }
+    if (lane >= q) a = 0.0;
+    if (lane < SP) abuf[lane] = a;
+    __syncwarp();
+    // u = dC_NN A^T, b = dC_Ni - u
+    double u = 0.0;
+    if (lane < q)
+      for (int c = 0; c < q; ++c) u = fma(dC[c <= lane ? lane * CS + c : c * CS + lane], abuf[c], u);
+    double bv = lane < q ? dC[q * CS + lane] - u : 0.0;
+    // dD_i = dC_ii - 2 A.dC_Ni + A.u
+    double dterm = lane < q ? fma(-2.0 * a, dC[q * CS + lane], a * u) : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) dterm += __shfl_xor_sync(0xffffffffu, dterm, o);
+    const double dD = dC[q * CS + q] + dterm;
+    // dA^T = C_NN^{-1} b: forward L z = b (column of L in registers), back L^T x = z (rows in smem)
+#pragma unroll
+    for (int j = 0; j < SP; ++j) {
+      if (j < q) {
+        const double zj = __shfl_sync(0xffffffffu, bv * myinv, j);
+        if (lane == j) bv = zj;
+        else if (lane > j) bv = fma(-crow[j], zj, bv);
+      }
+    }
+    for (int j = q - 1; j >= 0; --j) {
+      const double xj = __shfl_sync(0xffffffffu, bv * myinv, j);
+      if (lane == j) bv = xj;
+      else if (lane < j) bv = fma(-C[j * CS + lane], xj, bv);
+    }
+    const double da = lane < q ? bv : 0.0;
+    // c_i = [-A_i, 1]/sqrt(D_i), dc_i; contribution of the point
+    const double rs = rsqrt_nr(Di);
+    const double hD = 0.5 * dD / Di;
+    const double ck = lane < q ? -a * rs : (lane == q ? rs : 0.0);
+    const double dck = (lane < q ? -da * rs : 0.0) - ck * hD;
+    double cl = lane <= q ? fma(dck, gam_s[lane], ck * gamd_s[lane]) : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) cl += __shfl_xor_sync(0xffffffffu, cl, o);
+    contrib = ok ? hD + cl : __longlong_as_double(0x7ff8000000000000LL);
+  }
+  if (lane == 0) wsum[warp] = contrib;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int w = 0; w < GW; ++w) s += wsum[w];
+    part[blockIdx.x] = s;
+  }
+}
+
+template <int FAM, int RB>
+cudaError_t launch_grad_rb(const GradPointArgs& a, cudaStream_t s) {
+  const size_t smem = (size_t)GW * grad_warp_doubles<RB>(a.p.d) * sizeof(double);
+  static size_t attr = 0;
+  if (attr < smem) {
+    cudaError_t e = cudaFuncSetAttribute(vecchia_grad_kernel<FAM, RB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+    if (e != cudaSuccess) return e;
+    attr = smem;
+  }
+  const unsigned blocks = (unsigned)((a.npts + GW - 1) / GW);
+  vecchia_grad_kernel<FAM, RB><<<blocks, GW * 32, smem, s>>>(a.U, a.dU, a.Gam, a.ldu, a.mk, a.ld, a.X, a.nbr, a.mv,
+                                                             a.order, a.npts, a.p, a.pidx, a.part);
+  return cudaGetLastError();
+}
+
+template <int FAM>
+cudaError_t launch_grad_fam(const GradPointArgs& a, cudaStream_t s) {
+  switch ((a.mv + 1 + 7) / 8) {
+    case 1: return launch_grad_rb<FAM, 1>(a, s);
+    case 2: return launch_grad_rb<FAM, 2>(a, s);
+    case 3: return launch_grad_rb<FAM, 3>(a, s);
+    default: return launch_grad_rb<FAM, 4>(a, s);
+  }
+}
+
+}  // namespace
+
+int64_t grad_point_nparts(int64_t npts) { return (npts + GW - 1) / GW; }
+
+cudaError_t launch_grad_points(const GradPointArgs& a, double* out, cudaStream_t s) {
+  if (a.mv > 31) return cudaErrorNotSupported;
+  if (a.npts > 0) {
+    cudaError_t e;
+    switch (a.p.family) {
+      case FAM_M12: e = launch_grad_fam<FAM_M12>(a, s); break;
+      case FAM_M32: e = launch_grad_fam<FAM_M32>(a, s); break;
+      case FAM_M52: e = launch_grad_fam<FAM_M52>(a, s); break;
+      default: e = launch_grad_fam<FAM_GAUSS>(a, s); break;
+    }
+    if (e != cudaSuccess) return e;
+  }
+  grad_reduce_kernel<<<1, 1024, 0, s>>>(a.part, grad_point_nparts(a.npts), out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_dkm(const double* Z, int m, int mk, int pidx, const CovParams& p, double* out, cudaStream_t s) {
+  const int64_t tot = (int64_t)mk * mk;
+  const unsigned blocks = (unsigned)((tot + 255) / 256);
+  switch (p.family) {
+    case FAM_M12: dkm_kernel<FAM_M12><<<blocks, 256, 0, s>>>(Z, m, mk, pidx, p, out); break;
+    case FAM_M32: dkm_kernel<FAM_M32><<<blocks, 256, 0, s>>>(Z, m, mk, pidx, p, out); break;
+    case FAM_M52: dkm_kernel<FAM_M52><<<blocks, 256, 0, s>>>(Z, m, mk, pidx, p, out); break;
+    default: dkm_kernel<FAM_GAUSS><<<blocks, 256, 0, s>>>(Z, m, mk, pidx, p, out); break;
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_phi_low(const double* Phi, int mk, double* out, cudaStream_t s) {
+  const int64_t tot = (int64_t)mk * mk;
+  phi_low_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(Phi, mk, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_kx_deriv(const double* X, const double* Z, int64_t npos, int m, int mk, int pidx,
+                            const CovParams& p, double* S, cudaStream_t s) {
+  if (npos == 0) return cudaSuccess;
+  const unsigned blocks = (unsigned)((npos + 7) / 8);
+  const size_t zbytes = (size_t)m * p.d * sizeof(double);
+  auto go = [&](auto kern) -> cudaError_t {
+    static size_t attr = 0;
+    if (zbytes > 48 * 1024 && attr < zbytes) {
+      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)zbytes);
+      if (e != cudaSuccess) return e;
+      attr = zbytes;
+    }
+    kern<<<blocks, 256, zbytes, s>>>(X, Z, npos, m, mk, pidx, p, S);
+    return cudaGetLastError();
+  };
+  switch (p.family) {
+    case FAM_M12: return go(kx_deriv_kernel<FAM_M12>);
+    case FAM_M32: return go(kx_deriv_kernel<FAM_M32>);
+    case FAM_M52: return go(kx_deriv_kernel<FAM_M52>);
+    default: return go(kx_deriv_kernel<FAM_GAUSS>);
+  }
+}
+
+cudaError_t launch_grad_q(const double* LinvM, int ldi, const double* G, int ldg, int ycol, int m, int ld,
+                          double* zh, double* z, double* Q2, cudaStream_t s) {
+  if (m > 0) {
+    zhalf_kernel<<<(m + 127) / 128, 128, 0, s>>>(LinvM, ldi, G, ldg, ycol, m, zh);
+    zfull_kernel<<<(m + 127) / 128, 128, 0, s>>>(LinvM, ldi, zh, m, z);
+  }
+  const int64_t tot = (int64_t)ld * ld;
+  q_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(LinvM, ldi, z, m, ycol, ld, Q2);
+  return cudaGetLastError();
+}
+
+}  // namespace vif

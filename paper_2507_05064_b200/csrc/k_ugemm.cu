@@ -67,7 +67,8 @@ constexpr int GCH = GBK / 2;  // 16-byte chunks per tile row
 __global__ void __launch_bounds__(256, 2) gemm_tn_kernel(const double* __restrict__ A, int64_t lda, int64_t npos,
                                                       const double* __restrict__ B, int64_t ldb, int N, int K,
                                                       int tri, double* __restrict__ C, int64_t ldc, int64_t n,
-                                                      int64_t chunk, int world, int rank, int64_t pos0) {
+                                                      int64_t chunk, int world, int rank, int64_t pos0,
+                                                      double alpha, int accum) {
   extern __shared__ __align__(16) double gsm[];
   double* As = gsm;                            // [GST][GBM][GPAD]
   double* Bs = gsm + GST * GBM * GPAD;         // [GST][GBN][GPAD]
@@ -161,7 +162,16 @@ __global__ void __launch_bounds__(256, 2) gemm_tn_kernel(const double* __restric
 #pragma unroll
     for (int b = 0; b < 4; ++b) {
       const int c = col0 + wn * 32 + b * 8 + (lane & 3) * 2;
-      if (c < N) *reinterpret_cast<double2*>(C + i * ldc + c) = make_double2(acc[a][b][0], acc[a][b][1]);
+      if (c < N) {
+        double2* dst = reinterpret_cast<double2*>(C + i * ldc + c);
+        double2 v = make_double2(alpha * acc[a][b][0], alpha * acc[a][b][1]);
+        if (accum) {  // C += alpha A B^T (gradient path)
+          const double2 o = *dst;
+          v.x += o.x;
+          v.y += o.y;
+        }
+        *dst = v;
+      }
     }
   }
 }
@@ -206,7 +216,24 @@ cudaError_t launch_u_features(const double* X, const double* Z, const double* y,
   }
   const unsigned grid = (unsigned)(((npos + GBM - 1) / GBM) * ((mk + GBN - 1) / GBN));
   gemm_tn_kernel<<<grid, 256, smem, s>>>(S + pos0 * mk, mk, npos, Linv, mk, mk, mk, 1, Uaug, ld, n, chunk, world, rank,
-                                         pos0);
+                                         pos0, 1.0, 0);
+  return cudaGetLastError();
+}
+
+// C[p][c] (+)= alpha sum_k A[p][k] B[c][k] for p < nrows, c < N (single rank: row p -> p); B lower
+// triangular (k <= c) when tri.  Used by the gradient path (dU, Phi, Gamma).
+cudaError_t launch_gemm_tn(const double* A, int64_t lda, int64_t nrows, const double* B, int64_t ldb, int N, int K,
+                           int tri, double* C, int64_t ldc, double alpha, int accum, cudaStream_t s) {
+  if (nrows == 0 || N == 0) return cudaSuccess;
+  const size_t smem = (size_t)GST * (GBM + GBN) * GPAD * sizeof(double);
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(gemm_tn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  const unsigned grid = (unsigned)(((nrows + GBM - 1) / GBM) * ((N + GBN - 1) / GBN));
+  gemm_tn_kernel<<<grid, 256, smem, s>>>(A, lda, nrows, B, ldb, N, K, tri, C, ldc, nrows, nrows, 1, 0, 0, alpha, accum);
   return cudaGetLastError();
 }
 

@@ -55,6 +55,33 @@ int syrk_nt_nsplit(int ncols, int64_t nrows, int num_sms);
 size_t syrk_nt_part_doubles(int ncols, int nsplit);
 cudaError_t launch_syrk_nt(const double* W, int64_t ldw, int64_t nrows, int ncols, int nsplit, double* Gpart,
                            double* G, int ldg, cudaStream_t s);
+// gradient (k_grad.cu)
+struct GradPointArgs {
+  const double* U;
+  const double* dU;   // NULL for the nugget (dU = 0)
+  const double* Gam;  // g_i rows by processing position (npts x ld)
+  int64_t ldu;
+  int mk;
+  int ld;
+  const double* X;
+  const int32_t* nbr;
+  int mv;
+  const int64_t* order;
+  int64_t npts;
+  CovParams p;
+  int pidx;      // 0: sigma_1^2, 1..d: lambda_j, d+1: nugget
+  double* part;  // grad_point_nparts(npts) block partials
+};
+int64_t grad_point_nparts(int64_t npts);
+cudaError_t launch_grad_points(const GradPointArgs& a, double* out, cudaStream_t s);
+cudaError_t launch_dkm(const double* Z, int m, int mk, int pidx, const CovParams& p, double* out, cudaStream_t s);
+cudaError_t launch_phi_low(const double* Phi, int mk, double* out, cudaStream_t s);
+cudaError_t launch_kx_deriv(const double* X, const double* Z, int64_t npos, int m, int mk, int pidx,
+                            const CovParams& p, double* S, cudaStream_t s);
+cudaError_t launch_grad_q(const double* LinvM, int ldi, const double* G, int ldg, int ycol, int m, int ld,
+                          double* zh, double* z, double* Q2, cudaStream_t s);
+cudaError_t launch_gemm_tn(const double* A, int64_t lda, int64_t nrows, const double* B, int64_t ldb, int N, int K,
+                           int tri, double* C, int64_t ldc, double alpha, int accum, cudaStream_t s);
 // misc
 cudaError_t launch_validate(const double* X, int64_t n, int d, const double* Z, int m, const double* y,
                             const int32_t* nbr, int mv, DevStatus* st, cudaStream_t s);

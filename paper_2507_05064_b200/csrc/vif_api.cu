@@ -298,6 +298,32 @@ int set_data(Handle* h, const double* X, const double* Z, const int32_t* nbr, co
   return VIF_OK;
 }
 
+// ---------------------------------------------------------------- gradient workspace
+enum GBuf { G_Q2, G_GAM, G_DU, G_DKM, G_TT, G_PHI, G_PHILOW, G_LINVM, G_MCOPY, G_TSCR, G_ZH, G_Z, G_PART, G_OUT,
+            G_COUNT };
+
+Layout make_grad_layout(const Plan& P) {
+  Layout L{};
+  const size_t D8 = sizeof(double);
+  const int64_t mk1 = P.mk > 0 ? P.mk : 1;
+  L.size[G_Q2] = (size_t)P.ld * P.ld * D8;
+  L.size[G_GAM] = (size_t)P.npos * P.ld * D8;
+  L.size[G_DU] = (size_t)P.npad * P.ld * D8;
+  L.size[G_DKM] = L.size[G_TT] = L.size[G_PHI] = L.size[G_PHILOW] = L.size[G_LINVM] = L.size[G_TSCR] =
+      (size_t)mk1 * mk1 * D8;
+  L.size[G_MCOPY] = (size_t)P.ld * P.ld * D8;
+  L.size[G_ZH] = L.size[G_Z] = (size_t)mk1 * D8;
+  L.size[G_PART] = (size_t)grad_point_nparts(P.npos) * D8;
+  L.size[G_OUT] = (size_t)(P.d + 2) * D8;
+  size_t off = 0;
+  for (int b = 0; b < G_COUNT; ++b) {
+    L.off[b] = off;
+    off += (L.size[b] + 255) / 256 * 256;
+  }
+  L.total = off + 256;
+  return L;
+}
+
 }  // namespace
 
 // ====================================================================== C ABI
@@ -613,6 +639,96 @@ int vif_nll(void* handle, vif_terms* out) {
   h->cached_status = status;
   *out = t;
   return status;
+}
+
+int vif_grad_workspace_bytes(const vif_dims* dims, size_t* bytes) {
+  Plan P;
+  std::string err;
+  if (!bytes) return fail(nullptr, VIF_ERR_INVALID_ARG, "bytes is NULL");
+  if (!make_plan(dims, true, P, err)) return fail(nullptr, VIF_ERR_INVALID_ARG, err);
+  *bytes = make_grad_layout(P).total;
+  return VIF_OK;
+}
+
+int vif_grad(void* handle, const vif_theta* theta, void* gws, size_t gws_bytes, double* grad, vif_terms* terms) {
+  Handle* h = reinterpret_cast<Handle*>(handle);
+  if (!h) return fail(nullptr, VIF_ERR_INVALID_ARG, "handle is NULL");
+  if (!grad) return fail(h, VIF_ERR_INVALID_ARG, "grad is NULL");
+  const Plan& P = h->P;
+  if (P.world != 1) return fail(h, VIF_ERR_INVALID_ARG, "vif_grad: single-rank handles only in this version");
+  if (P.mv > 31) return fail(h, VIF_ERR_INVALID_ARG, "vif_grad: m_v <= 31 only in this version");
+  const Layout GL = make_grad_layout(P);
+  if (!gws || gws_bytes < GL.total) {
+    char msg[128];
+    snprintf(msg, sizeof msg, "grad workspace too small: need %zu bytes", GL.total);
+    return fail(h, VIF_ERR_NO_MEMORY, msg);
+  }
+  char* gb = reinterpret_cast<char*>(round_up((int64_t)(uintptr_t)gws, 256));
+  auto gbuf = [&](GBuf b) { return reinterpret_cast<double*>(gb + GL.off[b]); };
+  CovParams p;
+  std::string err;
+  if (!make_params(h, theta, p, err)) return fail(h, VIF_ERR_INVALID_ARG, err);
+  int r = vif_factor(handle, theta, nullptr, nullptr);
+  if (r != VIF_OK) return r;
+  cudaStream_t s = h->stream;
+  const int m = P.m, mk = P.mk, ld = P.ld;
+  double* G = h->buf<double>(B_G);
+  VIF_CUDA(h, cudaMemcpyAsync(gbuf(G_MCOPY), G, (size_t)ld * ld * 8, cudaMemcpyDeviceToDevice, s), "copy G");
+  vif_terms t;
+  r = vif_nll(handle, &t);
+  if (terms) *terms = t;
+  if (r != VIF_OK) return r;
+  DevStatus* st = h->buf<DevStatus>(B_STATUS);
+  // M_w^{-1} = L_M^{-T} L_M^{-1} (full inverse of the Cholesky factor), z, Q2 = 2 Q
+  if (m > 0) {
+    VIF_CUDA(h, cudaMemsetAsync(gbuf(G_LINVM), 0, GL.size[G_LINVM], s), "memset");
+    VIF_CUDA(h, launch_chol_inv(gbuf(G_MCOPY), m, ld, 1.0, gbuf(G_LINVM), mk, mk, 1, gbuf(G_TSCR), &st->m_fail,
+                                h->num_sms, s),
+             "chol M (full inverse)");
+  }
+  VIF_CUDA(h, launch_grad_q(gbuf(G_LINVM), mk, G, ld, P.ycol, m, ld, gbuf(G_ZH), gbuf(G_Z), gbuf(G_Q2), s), "Q");
+  // g rows: Gamma = W (2Q), rows by processing position
+  double* W = h->buf<double>(B_W);
+  VIF_CUDA(h, launch_gemm_tn(W, ld, P.npos, gbuf(G_Q2), ld, ld, ld, 0, gbuf(G_GAM), ld, 1.0, 0, s), "Gamma");
+  VIF_CUDA(h, cudaMemsetAsync(gbuf(G_DU), 0, GL.size[G_DU], s), "memset dU");
+  const double* Linv = h->buf<double>(B_LINV);
+  const double* U = h->buf<double>(B_U);
+  double* S = W;  // W is dead once Gamma is formed: reuse it as the dK(X,Z) scratch
+  for (int pi = 0; pi < P.d + 2; ++pi) {
+    const bool kernel_param = pi <= P.d;
+    const double* dUp = nullptr;
+    if (kernel_param && m > 0) {
+      VIF_CUDA(h, launch_dkm(h->buf<double>(B_Z), m, mk, pi, p, gbuf(G_DKM), s), "dK_m");
+      VIF_CUDA(h, launch_gemm_tn(Linv, mk, mk, gbuf(G_DKM), mk, mk, mk, 0, gbuf(G_TT), mk, 1.0, 0, s), "Linv dK_m");
+      VIF_CUDA(h, launch_gemm_tn(Linv, mk, mk, gbuf(G_TT), mk, mk, mk, 0, gbuf(G_PHI), mk, 1.0, 0, s), "Phi");
+      VIF_CUDA(h, launch_phi_low(gbuf(G_PHI), mk, gbuf(G_PHILOW), s), "Phi_low");
+      VIF_CUDA(h, launch_kx_deriv(h->buf<double>(B_X), h->buf<double>(B_Z), P.n, m, mk, pi, p, S, s), "dK(X,Z)");
+      VIF_CUDA(h, launch_gemm_tn(S, mk, P.n, Linv, mk, mk, mk, 1, gbuf(G_DU), ld, 1.0, 0, s), "dK L^-T");
+      VIF_CUDA(h, launch_gemm_tn(U, ld, P.n, gbuf(G_PHILOW), mk, mk, mk, 1, gbuf(G_DU), ld, -1.0, 1, s), "U Phi^T");
+      dUp = gbuf(G_DU);
+    }
+    GradPointArgs a;
+    a.U = U;
+    a.dU = dUp;
+    a.Gam = gbuf(G_GAM);
+    a.ldu = ld;
+    a.mk = mk;
+    a.ld = ld;
+    a.X = h->buf<double>(B_X);
+    a.nbr = h->buf<int32_t>(B_NBR);
+    a.mv = P.mv;
+    a.order = h->order[0];
+    a.npts = P.n_own[0];
+    a.p = p;
+    a.pidx = pi;
+    a.part = gbuf(G_PART);
+    VIF_CUDA(h, launch_grad_points(a, gbuf(G_OUT) + pi, s), "gradient points");
+  }
+  VIF_CUDA(h, cudaMemcpyAsync(grad, gbuf(G_OUT), (size_t)(P.d + 2) * 8, cudaMemcpyDeviceToHost, s), "grad copy");
+  VIF_CUDA(h, cudaStreamSynchronize(s), "sync");
+  for (int pi = 0; pi < P.d + 2; ++pi)
+    if (!isfinite(grad[pi])) return fail(h, VIF_ERR_NOT_PD, "gradient: a residual block or M is not positive definite");
+  return VIF_OK;
 }
 
 int vif_copy_U(void* handle, double* out) {

@@ -77,8 +77,11 @@ def load_library():
         lib.vif_stage_name.restype = ctypes.c_char_p
         lib.vif_destroy.argtypes = [P]
         lib.vif_destroy.restype = None
+        lib.vif_grad_workspace_bytes.argtypes = [ctypes.POINTER(_Dims), ctypes.POINTER(sz)]
+        lib.vif_grad.argtypes = [P, ctypes.POINTER(_Theta), P, sz, P, ctypes.POINTER(_Terms)]
         for f in ("vif_nccl_unique_id", "vif_workspace_bytes", "vif_partition", "vif_create", "vif_set_data",
-                  "vif_factor", "vif_nll", "vif_copy_U", "vif_launch_count", "vif_profile", "vif_stage_times"):
+                  "vif_factor", "vif_nll", "vif_copy_U", "vif_launch_count", "vif_profile", "vif_stage_times",
+                  "vif_grad_workspace_bytes", "vif_grad"):
             getattr(lib, f).restype = ctypes.c_int
         _lib = lib
     return _lib
@@ -86,7 +89,7 @@ def load_library():
 
 EXPORTED = ("vif_nccl_unique_id", "vif_workspace_bytes", "vif_partition", "vif_create", "vif_set_data",
             "vif_factor", "vif_nll", "vif_copy_U", "vif_launch_count", "vif_profile", "vif_stage_times",
-            "vif_stage_name", "vif_last_error", "vif_destroy")
+            "vif_stage_name", "vif_last_error", "vif_destroy", "vif_grad_workspace_bytes", "vif_grad")
 NUM_STAGES = 8
 
 
@@ -206,6 +209,23 @@ def vif_nll(h) -> Terms:
     return Terms(t.nll, t.logdet_D, t.logdet_M, t.quad, t.bad_row)
 
 
+def vif_grad_workspace_bytes(n: int, d: int, m: int, mv: int, rank: int = 0, world: int = 1) -> int:
+    b = ctypes.c_size_t(0)
+    _check(load_library().vif_grad_workspace_bytes(ctypes.byref(_dims(n, d, m, mv, rank, world)), ctypes.byref(b)))
+    return int(b.value)
+
+
+def vif_grad(h, theta: Theta, grad_workspace: torch.Tensor):
+    """(Terms, dNLL/dtheta) for theta = (sigma_1^2, lambda_1..lambda_d, sigma^2) (P:126-133)."""
+    th, keep = theta.to_c()
+    g = np.zeros(len(keep) + 2)
+    t = _Terms()
+    st = load_library().vif_grad(h, ctypes.byref(th), ctypes.c_void_p(grad_workspace.data_ptr()),
+                                 grad_workspace.numel(), g.ctypes.data_as(ctypes.c_void_p), ctypes.byref(t))
+    _check(st, h, t.bad_row)
+    return Terms(t.nll, t.logdet_D, t.logdet_M, t.quad, t.bad_row), g
+
+
 def vif_copy_U(h, out: torch.Tensor):
     _check(load_library().vif_copy_U(h, _ptr(out)), h)
 
@@ -276,6 +296,14 @@ class VifModel:
     def evaluate(self, theta: Theta, B_out=None, D_out=None) -> Terms:
         self.factor(theta, B_out, D_out)
         return self.nll()
+
+    def grad(self, theta: Theta):
+        """NLL terms and dNLL/dtheta, theta = (sigma_1^2, lambda_1..lambda_d, sigma^2); the second
+        workspace is allocated on first use and kept."""
+        if getattr(self, "grad_workspace", None) is None:
+            nbytes = vif_grad_workspace_bytes(self.n, self.d, self.m, self.mv, self.rank, self.world)
+            self.grad_workspace = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
+        return vif_grad(self.handle, theta, self.grad_workspace)
 
     def U(self) -> torch.Tensor:
         out = torch.empty((self.n, self.m), dtype=torch.float64, device=self.device)

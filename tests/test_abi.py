@@ -87,3 +87,12 @@ def test_create_rejects_small_workspace_without_gpu(p):
                         None)
     assert st == 5
     assert "workspace too small" in p.vif_last_error(None)
+
+
+def test_grad_workspace_sizing(p):
+    a = p.vif.vif_grad_workspace_bytes(1000, 2, 50, 10)
+    b = p.vif.vif_grad_workspace_bytes(2000, 2, 50, 10)
+    # Q, g rows and dU: (2 n + ld) x ld doubles at least
+    assert a >= (2 * 1000 + 64) * 64 * 8 and b > a
+    with pytest.raises(p.VifError):
+        p.vif.vif_grad_workspace_bytes(0, 2, 50, 10)

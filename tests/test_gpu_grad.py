@@ -1,0 +1,155 @@
+"""CUDA gradient of the NLL (vif_grad, through the C ABI) vs the oracle gradient.
+
+theta = (sigma_1^2, lambda_1..lambda_d, sigma^2).  Bar: per component |g - g_ref| <= 1e-8 x
+max(|g_ref|, term scale), the term scale being half the sum of |d sum log D|, |d logdet M_w|,
+|d quad| (the gradient at the data-generating theta is a small difference of large terms).
+At n = 1M (config 3) the oracle is too slow; there the GPU gradient is checked against
+Richardson-extrapolated central differences of the GPU's own NLL (a property at any size)."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import oracle  # noqa: E402
+import vifgen  # noqa: E402
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _lib():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import __graft_entry__
+    __graft_entry__.build()
+    import paper_2507_05064_b200 as p
+    p.load_library()
+    return p
+
+
+def vif():
+    import paper_2507_05064_b200 as p
+    return p
+
+
+def model_of(w):
+    p = vif()
+    dev = torch.device("cuda")
+    X, Z, nbr, y = (torch.from_numpy(np.ascontiguousarray(a)).to(dev) for a in (w.X, w.Z.reshape(-1, w.d), w.nbr, w.y))
+    return p.VifModel(X, Z, nbr, y, device=dev)
+
+
+def small(n, m, mv, family="matern32", seed=1, rho=0.15, nugget=0.1, d=2, ard=None, neighbors="dc"):
+    return vifgen.make_workload(n=n, d=d, m=m, mv=mv, family=family, rho=rho, nugget=nugget, seed=seed,
+                                device="cuda", ard=ard, z="kmeans++" if m > 0 else "subset", neighbors=neighbors)
+
+
+def check(g, r, rtol=1e-8):
+    scale = np.maximum(np.abs(r.grad), 0.5 * np.abs(r.parts).sum(axis=1))
+    err = np.abs(g - r.grad) / scale
+    assert np.all(err <= rtol), (g, r.grad, err)
+
+
+def grad_parity(w, rtol=1e-8):
+    p = vif()
+    model = model_of(w)
+    terms, g = model.grad(p.Theta(**w.theta_dict()))
+    r = oracle.grad(w.X, w.Z, w.nbr, w.y, oracle.Theta(**w.theta_dict()))
+    ro = oracle.factor_nll(w.X, w.Z, w.nbr, w.y, oracle.Theta(**w.theta_dict()), want_BD=False)
+    assert terms.nll == pytest.approx(ro.nll, rel=1e-8)
+    check(g, r, rtol)
+    model.close()
+    return g, r
+
+
+def test_grad_config1():
+    grad_parity(vifgen.make_config(1, device="cuda"))
+
+
+@pytest.mark.parametrize("family", ["matern12", "matern32", "matern52", "gaussian"])
+@pytest.mark.parametrize("n,m,mv", [(700, 37, 13), (513, 64, 31), (300, 9, 1)])
+def test_grad_shapes(family, n, m, mv):
+    grad_parity(small(n, m, mv, family=family, seed=n + mv))
+
+
+def test_grad_m0_vecchia():
+    grad_parity(small(600, 0, 12, seed=5))
+
+
+def test_grad_mv0_fitc():
+    grad_parity(small(600, 40, 0, seed=6))
+
+
+def test_grad_ard_10d():
+    grad_parity(small(800, 60, 15, family="matern52", d=10, ard=(0.5, 5.0), seed=7, nugget=0.1))
+
+
+def test_grad_exact_case_all_predecessors():
+    grad_parity(small(32, 6, 31, neighbors="all", seed=8))
+
+
+def test_grad_off_theta():
+    w = small(900, 30, 10, seed=9)
+    th = dict(w.theta_dict())
+    th["sigma2"] *= 1.6
+    th["lengthscale"] = np.asarray(th["lengthscale"]) * 0.7
+    th["nugget"] *= 2.2
+    p = vif()
+    model = model_of(w)
+    _, g = model.grad(p.Theta(**th))
+    r = oracle.grad(w.X, w.Z, w.nbr, w.y, oracle.Theta(**th))
+    check(g, r)
+    assert np.all(np.abs(r.grad) > 1.0)
+    model.close()
+
+
+def test_grad_repeat_deterministic_and_matches_nll():
+    w = small(500, 20, 8, seed=10)
+    p = vif()
+    model = model_of(w)
+    th = p.Theta(**w.theta_dict())
+    t1, g1 = model.grad(th)
+    t2, g2 = model.grad(th)
+    assert np.array_equal(g1, g2) and t1.nll == t2.nll
+    assert model.evaluate(th).nll == t1.nll
+    model.close()
+
+
+def test_grad_rejects_unsupported():
+    p = vif()
+    w = small(200, 8, 40, seed=11)
+    model = model_of(w)
+    with pytest.raises(p.VifError) as e:
+        model.grad(p.Theta(**w.theta_dict()))
+    assert e.value.status == 1
+    model.close()
+
+
+@pytest.mark.slow
+def test_grad_config2_full():
+    grad_parity(vifgen.make_config(2, device="cuda"))
+
+
+@pytest.mark.slow
+def test_grad_config3_vs_gpu_finite_differences():
+    """n = 1M: analytic GPU gradient vs Richardson central differences of the GPU NLL."""
+    w = vifgen.make_config(3, device="cuda")
+    p = vif()
+    model = model_of(w)
+    base = w.theta_dict()
+    v0 = np.concatenate([[base["sigma2"]], np.asarray(base["lengthscale"], float), [base["nugget"]]])
+    d = w.d
+
+    def nll(v):
+        th = p.Theta(base["family"], float(v[0]), np.array(v[1:1 + d]), float(v[1 + d]), base["jitter"])
+        return model.evaluate(th).nll
+
+    terms, g = model.grad(p.Theta(**base))
+    for k in range(len(v0)):
+        h = 1e-4 * v0[k]
+        e = np.eye(len(v0))[k]
+        cen = lambda hh: (nll(v0 + hh * e) - nll(v0 - hh * e)) / (2 * hh)
+        fd = (4 * cen(h / 2) - cen(h)) / 3
+        # term scale of the NLL (|NLL| << its terms at the data-generating theta)
+        scale = max(abs(g[k]), 1e-7 * (abs(terms.logdet_D) + abs(terms.logdet_M) + abs(terms.quad)) / v0[k])
+        assert abs(g[k] - fd) <= 1e-6 * scale + 1e-6 * abs(fd), (k, g[k], fd)
+    model.close()
