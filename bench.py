@@ -44,6 +44,7 @@ def parse():
     ap.add_argument("--n", type=int, default=None, help="override n (same recipe)")
     ap.add_argument("--impl", default="vif", choices=["vif", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-grad", action="store_true", help="skip the NLL-gradient timing (vif_grad)")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target CPU seconds of the oracle sample")
     return ap.parse_args()
 
@@ -280,6 +281,24 @@ def main():
         dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
     e2e_ms = float(e2e_ms.item())
 
+    # ---------------- NLL gradient (vif_grad, single GPU): reported beside the headline ----------------
+    grad = None
+    if world == 1 and not args.no_grad and w.mv <= 31:
+        model.grad(th[0])
+        g_steps = 3
+        torch.cuda.synchronize(dev)
+        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        g0.record(stream)
+        for k in range(g_steps):
+            gterms, gvec = model.grad(th[k % 2])
+        g1.record(stream)
+        torch.cuda.synchronize(dev)
+        gms = g0.elapsed_time(g1) / g_steps
+        grad = {"ms_per_eval": gms, "points_per_s": w.n / (gms * 1e-3), "params": len(gvec),
+                "grad_at_theta1": [float(x) for x in gvec],
+                "note": "vif_grad: factor + NLL + d+2 partial derivatives (sigma_1^2, lambda_1..d, sigma^2; "
+                        "P:126-133, App. A), device events around the synchronous calls"}
+
     if rank == 0:
         fl = workload_flops(w.nbr, w.m)
         # per-rank share of the row-sharded kernels (strong scaling: each rank does ~1/world of the rows)
@@ -340,6 +359,7 @@ def main():
             "gpu_launches": launches_per_step * args.steps,
             "stages_ms_per_step": stage_avg,
             "nll": last.nll,
+            "grad": grad,
             "input_generation_s": {"total": gen_s, **{k: round(v, 3) for k, v in w.timings.items()}},
             "create_s": create_s,
         }
