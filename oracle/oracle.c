@@ -745,3 +745,150 @@ done:
   free(A); free(W); free(info); free(Lm); free(U); free(dU); free(Phi); free(dKm);
   return status;
 }
+
+/* =====================================================================================
+ * Predictive means (Proposition 1), reading p1: every prediction point conditions on
+ * m_v training points only (B_p = I, B_po row p = -A_p), so with the training factor's
+ * z = M_w^{-1} v (step 6):
+ *   mu_p = u_p . z + A_p (y_N(p) - U_N(p) z),  u_p = L_m^{-1} k(Z, x_p),
+ *   A_p = C_{p,N} C_{N,N}^{-1},  D_p = C_pp - A_p C_{N,p},
+ *   C(a,b) = k - u_a.u_b + sigma^2 [a = b] on training pairs, C(p,a) = k(x_p,x_a) - u_p.u_a,
+ *   C_pp = sigma_1^2 + sigma^2 - u_p.u_p  (the response y_p).
+ * Derivation from Prop. 1 with whitening in DESIGN.md section 11; pinned in tests/test_oracle_pred.py
+ * against the exact GP (all training points as neighbours) and the paper's dense formula P:143-144.
+ * ===================================================================================== */
+int oracle_predict(int64_t n, int m, int mv, const double *X, const double *Z, const int32_t *nbr, const double *y,
+                   const or_theta *th, int64_t np, const double *Xp, const int32_t *nbrp, double *mu, double *Dp,
+                   double *Bp, int64_t *bad_row) {
+  *bad_row = -1;
+  const int d = th->d, m1 = m > 0 ? m : 1, s_max = mv + 1;
+  double *Lm = NULL, *U = NULL;
+  double *A = (double *)malloc(sizeof(double) * (size_t)n * (mv > 0 ? mv : 1));
+  double *W = (double *)malloc(sizeof(double) * (size_t)n * m1);
+  or_rowinfo *info = (or_rowinfo *)malloc(sizeof(or_rowinfo) * (size_t)n);
+  double *M = (double *)calloc((size_t)m1 * m1 + 2 * m1, sizeof(double));
+  double *v = M + (size_t)m1 * m1, *z = v + m1;
+  int status = OR_OK;
+  if (!A || !W || !info || !M) { status = OR_NOMEM; goto done; }
+  if (m > 0) {
+    Lm = (double *)malloc(sizeof(double) * (size_t)m * m);
+    U = (double *)malloc(sizeof(double) * (size_t)n * m);
+    if (!Lm || !U) { status = OR_NOMEM; goto done; }
+    if (or_build_Lm(th, Z, m, Lm) != OR_OK) { status = OR_NOT_PD; goto done; }
+#pragma omp parallel for schedule(static)
+    for (int64_t i = 0; i < n; ++i) or_u_row(th, Z, m, Lm, X + i * d, U + i * (size_t)m);
+  }
+  /* training factor: A_i, D_i, w_i, r_i -> M_w, v, z (steps 3-6) */
+  {
+    int64_t badr = -1;
+#pragma omp parallel
+    {
+      int32_t *S = (int32_t *)malloc(sizeof(int32_t) * s_max);
+      double *uS = (double *)malloc(sizeof(double) * (size_t)s_max * m1);
+      double *work = (double *)malloc(sizeof(double) * (size_t)s_max * s_max);
+#pragma omp for schedule(static)
+      for (int64_t i = 0; i < n; ++i) {
+        const int32_t *row = nbr + i * mv;
+        int q = or_count_nbrs(row, mv), s = q + 1;
+        for (int k = 0; k < q; ++k) S[k] = row[k];
+        S[q] = (int32_t)i;
+        for (int k = 0; k < s; ++k)
+          for (int c = 0; c < m; ++c) uS[(size_t)k * m + c] = U[(size_t)S[k] * m + c];
+        double Di, *a = A + i * mv;
+        int b = or_vecchia_row(th, X, S, s, uS, m, work, a, &Di);
+        if (b >= 0 || !(Di > 0.0)) {
+#pragma omp critical
+          { if (badr < 0 || i < badr) badr = i; }
+          continue;
+        }
+        double r = y[i];
+        for (int k = 0; k < q; ++k) r -= a[k] * y[S[k]];
+        for (int c = 0; c < m; ++c) {
+          double t = uS[(size_t)q * m + c];
+          for (int k = 0; k < q; ++k) t -= a[k] * uS[(size_t)k * m + c];
+          W[i * (size_t)m + c] = t;
+        }
+        info[i].q = q; info[i].D = Di; info[i].r = r;
+      }
+      free(S); free(uS); free(work);
+    }
+    if (badr >= 0) { *bad_row = badr; status = OR_NOT_PD; goto done; }
+  }
+  for (int64_t i = 0; i < n; ++i) {
+    const double *w = W + i * (size_t)m;
+    for (int k = 0; k < m; ++k) {
+      for (int l = 0; l < m; ++l) M[(size_t)k * m + l] += w[k] * w[l] / info[i].D;
+      v[k] += w[k] * info[i].r / info[i].D;
+    }
+  }
+  if (m > 0) {
+    for (int k = 0; k < m; ++k) M[(size_t)k * m + k] += 1.0;
+    if (or_chol(M, m, m) >= 0) { status = OR_NOT_PD; goto done; }
+    for (int k = 0; k < m; ++k) z[k] = v[k];
+    or_fwd(M, m, m, z);
+    or_bwd(M, m, m, z);
+  }
+  /* prediction points */
+  {
+    int64_t badp = -1;
+#pragma omp parallel
+    {
+      double *up = (double *)malloc(sizeof(double) * m1);
+      double *C = (double *)malloc(sizeof(double) * (size_t)s_max * s_max);
+      double *c = (double *)malloc(sizeof(double) * s_max);
+#pragma omp for schedule(static)
+      for (int64_t t = 0; t < np; ++t) {
+        const double *xp = Xp + t * d;
+        if (m > 0) or_u_row(th, Z, m, Lm, xp, up);
+        const int32_t *row = nbrp + t * mv;
+        const int q = or_count_nbrs(row, mv);
+        for (int a = 0; a < q; ++a) {
+          const double *xa = X + (size_t)row[a] * d;
+          for (int b = 0; b < q; ++b) {
+            double cc = or_cov(th, xa, X + (size_t)row[b] * d);
+            for (int k = 0; k < m; ++k) cc -= U[(size_t)row[a] * m + k] * U[(size_t)row[b] * m + k];
+            if (a == b) cc += th->nugget;
+            C[(size_t)a * q + b] = cc;
+          }
+          double cp = or_cov(th, xa, xp);
+          for (int k = 0; k < m; ++k) cp -= U[(size_t)row[a] * m + k] * up[k];
+          c[a] = cp;
+        }
+        double Cpp = th->sigma2 + th->nugget;
+        for (int k = 0; k < m; ++k) Cpp -= up[k] * up[k];
+        /* A_p = C_NN^{-1} c */
+        double *ap = c + 0;
+        double *cN = (double *)malloc(sizeof(double) * (q > 0 ? q : 1));
+        for (int a = 0; a < q; ++a) cN[a] = c[a];
+        if (q > 0) {
+          if (or_chol(C, q, q) >= 0) {
+#pragma omp critical
+            { if (badp < 0 || t < badp) badp = t; }
+            free(cN);
+            continue;
+          }
+          or_fwd(C, q, q, ap);
+          or_bwd(C, q, q, ap);
+        }
+        double D = Cpp, mean = 0.0;
+        for (int a = 0; a < q; ++a) D -= ap[a] * cN[a];
+        for (int k = 0; k < m; ++k) mean += up[k] * z[k];
+        for (int a = 0; a < q; ++a) {
+          double uz = 0.0;
+          for (int k = 0; k < m; ++k) uz += U[(size_t)row[a] * m + k] * z[k];
+          mean += ap[a] * (y[row[a]] - uz);
+        }
+        mu[t] = mean;
+        if (Dp) Dp[t] = D;
+        if (Bp)
+          for (int a = 0; a < mv; ++a) Bp[t * mv + a] = a < q ? -ap[a] : 0.0;
+        free(cN);
+      }
+      free(up); free(C); free(c);
+    }
+    if (badp >= 0) { *bad_row = badp; status = OR_NOT_PD; }
+  }
+done:
+  free(A); free(W); free(info); free(M); free(Lm); free(U);
+  return status;
+}

@@ -450,6 +450,37 @@ cudaError_t launch_kx_deriv(const double* X, const double* Z, int64_t npos, int 
   }
 }
 
+// Prediction (Prop. 1): mu_p = sqrt(D_p) (w_p . z - r_p) for the prediction row
+// [w_p, r_p] (computed with y_p = 0) = u_p . z + A_p (y_N - U_N z).
+__global__ void pred_mean_kernel(const double* __restrict__ Wp, int ld, int m, int ycol, const double* __restrict__ z,
+                                 const double* __restrict__ Dpos, const int64_t* __restrict__ order, int64_t np,
+                                 double* __restrict__ mu) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t pos = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
+  if (pos >= np) return;
+  const double* w = Wp + pos * (int64_t)ld;
+  double s = 0.0;
+  for (int a = lane; a < m; a += 32) s = fma(w[a], z[a], s);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane == 0) mu[order[pos]] = sqrt(Dpos[pos]) * (s - w[ycol]);
+}
+
+cudaError_t launch_pred_mean(const double* Wp, int ld, int m, int ycol, const double* z, const double* Dpos,
+                             const int64_t* order, int64_t np, double* mu, cudaStream_t s) {
+  if (np == 0) return cudaSuccess;
+  pred_mean_kernel<<<(unsigned)((np + 7) / 8), 256, 0, s>>>(Wp, ld, m, ycol, z, Dpos, order, np, mu);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_zvec(const double* LinvM, int ldi, const double* G, int ldg, int ycol, int m, double* zh,
+                        double* z, cudaStream_t s) {
+  if (m == 0) return cudaSuccess;
+  zhalf_kernel<<<(m + 127) / 128, 128, 0, s>>>(LinvM, ldi, G, ldg, ycol, m, zh);
+  zfull_kernel<<<(m + 127) / 128, 128, 0, s>>>(LinvM, ldi, zh, m, z);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_grad_q(const double* LinvM, int ldi, const double* G, int ldg, int ycol, int m, int ld,
                           double* zh, double* z, double* Q2, cudaStream_t s) {
   if (m > 0) {

@@ -39,7 +39,7 @@ __host__ __device__ constexpr int vecchia_warp_doubles() {
 template <int FAM, int RB, int NB>
 __global__ void __launch_bounds__(VW * 32) vecchia_smem_kernel(
     const double* __restrict__ U, int64_t ldu, int mk, int ld, const double* __restrict__ X,
-    const int32_t* __restrict__ nbr, int mv, const int64_t* __restrict__ order, int64_t npts, CovParams p,
+    const double* __restrict__ Uq, const double* __restrict__ Xq, const int32_t* __restrict__ nbr, int mv, const int64_t* __restrict__ order, int64_t npts, CovParams p,
     double* __restrict__ W, int64_t ldw, double* __restrict__ Dpos, double* __restrict__ B_out,
     double* __restrict__ D_out, DevStatus* __restrict__ st) {
   constexpr int SP = RB * 8;
@@ -71,8 +71,8 @@ __global__ void __launch_bounds__(VW * 32) vecchia_smem_kernel(
   const double* rp[RB];
 #pragma unroll
   for (int R = 0; R < RB; ++R) {
-    const int gi = Sidx[R * 8 + (lane >> 2)];
-    rp[R] = gi >= 0 ? U + (int64_t)gi * ldu + 2 * (lane & 3) : nullptr;
+    const int row = R * 8 + (lane >> 2), gi = Sidx[row];
+    rp[R] = gi >= 0 ? (row == q ? Uq : U) + (int64_t)gi * ldu + 2 * (lane & 3) : nullptr;  // row q: the point (Uq)
   }
   double2 f[NB][RB];
   auto load = [&](int k0) {
@@ -123,7 +123,7 @@ __global__ void __launch_bounds__(VW * 32) vecchia_smem_kernel(
             double v;
             if (r < s) {
               const int gr = Sidx[r], gc = Sidx[c];
-              v = cov<FAM>(X + (int64_t)gr * p.d, X + (int64_t)gc * p.d, p) - acc[t][j];
+              v = cov<FAM>((r == q ? Xq : X) + (int64_t)gr * p.d, (c == q ? Xq : X) + (int64_t)gc * p.d, p) - acc[t][j];
               if (r == c) v += p.nugget;
             } else {
               v = r == c ? 1.0 : 0.0;
@@ -187,7 +187,7 @@ __global__ void __launch_bounds__(VW * 32) vecchia_smem_kernel(
 
   // ---- 5. w_i, r_i:  (u_i - sum_k A_ik u_{N_k}) / sqrt(D_i) over ld columns ----
   const double rs = 1.0 / sqrt(Di);
-  const double* ui = U + i * ldu;
+  const double* ui = Uq + i * ldu;
   for (int c = 2 * lane; c < ld; c += 64) {
     double2 o = __ldg(reinterpret_cast<const double2*>(ui + c));
     int k = 0;
@@ -312,11 +312,14 @@ __device__ __forceinline__ void eval_lower(const double* __restrict__ xs, int s,
 }
 
 // stage the pre-scaled coordinates of S (lanes < s) for cov_fast
+// (row s-1 is the point itself, read from Xq: the training X, or the prediction inputs)
 template <int FAM>
-__device__ __forceinline__ void stage_xs(const double* __restrict__ X, int idx, int d, const CovParams& p, int lane,
-                                         int s, double* __restrict__ xs) {
-  if (lane < s)
-    for (int k = 0; k < d; ++k) xs[lane * d + k] = X[(int64_t)idx * d + k] * (fam_scale<FAM>() * p.inv_ls[k]);
+__device__ __forceinline__ void stage_xs(const double* __restrict__ X, const double* __restrict__ Xq, int idx, int d,
+                                         const CovParams& p, int lane, int s, double* __restrict__ xs) {
+  if (lane < s) {
+    const double* x = (lane == s - 1 ? Xq : X) + (int64_t)idx * d;
+    for (int k = 0; k < d; ++k) xs[lane * d + k] = x[k] * (fam_scale<FAM>() * p.inv_ls[k]);
+  }
 }
 
 template <int RB>
@@ -327,7 +330,7 @@ __host__ __device__ constexpr int vreg_warp_doubles(int d) {
 template <int FAM, int RB, int NB, int MINB>
 __global__ void __launch_bounds__(VW * 32, MINB) vecchia_reg_kernel(
     const double* __restrict__ U, int64_t ldu, int mk, int ld, const double* __restrict__ X,
-    const int32_t* __restrict__ nbr, int mv, const int64_t* __restrict__ order, int64_t npts, CovParams p,
+    const double* __restrict__ Uq, const double* __restrict__ Xq, const int32_t* __restrict__ nbr, int mv, const int64_t* __restrict__ order, int64_t npts, CovParams p,
     double* __restrict__ W, int64_t ldw, double* __restrict__ Dpos, double* __restrict__ B_out,
     double* __restrict__ D_out, DevStatus* __restrict__ st) {
   constexpr int SP = RB * 8;
@@ -355,7 +358,7 @@ __global__ void __launch_bounds__(VW * 32, MINB) vecchia_reg_kernel(
   const int s = q + 1;
   const int myidx = lane < q ? nb0 : (lane == q ? (int)i : -1);
   if (lane < SP) Sidx[lane] = myidx;
-  stage_xs<FAM>(X, myidx, p.d, p, lane, s, xs);
+  stage_xs<FAM>(X, Xq, myidx, p.d, p, lane, s, xs);
   __syncwarp();
 
   // ---- 1 + 2. Gram on DMMA; the kernel evaluations of step 2 (independent of the Gram) run
@@ -367,8 +370,8 @@ __global__ void __launch_bounds__(VW * 32, MINB) vecchia_reg_kernel(
   const double* rp[RB];
 #pragma unroll
   for (int R = 0; R < RB; ++R) {
-    const int gi = Sidx[R * 8 + (lane >> 2)];
-    rp[R] = gi >= 0 ? U + (int64_t)gi * ldu + 2 * (lane & 3) : nullptr;
+    const int row = R * 8 + (lane >> 2), gi = Sidx[row];
+    rp[R] = gi >= 0 ? (row == q ? Uq : U) + (int64_t)gi * ldu + 2 * (lane & 3) : nullptr;  // row q: the point (Uq)
   }
   {
     double2 f[NB][RB];
@@ -468,9 +471,9 @@ __global__ void __launch_bounds__(VW * 32, MINB) vecchia_reg_kernel(
     for (int t = 0; t < 8; ++t) o[t] = make_double2(0.0, 0.0);
     for (int k = 0; k < s; k += 2) {
       double2 u0[8], u1[8];
-      const double* r0 = U + (int64_t)Sidx[k] * ldu + c0 + 2 * lane;
+      const double* r0 = (k == q ? Uq : U) + (int64_t)Sidx[k] * ldu + c0 + 2 * lane;
       const bool has1 = k + 1 < s;
-      const double* r1 = has1 ? U + (int64_t)Sidx[k + 1] * ldu + c0 + 2 * lane : r0;
+      const double* r1 = has1 ? (k + 1 == q ? Uq : U) + (int64_t)Sidx[k + 1] * ldu + c0 + 2 * lane : r0;
 #pragma unroll
       for (int t = 0; t < 8; ++t) {
         const bool in = c0 + 2 * lane + 64 * t < ld;
@@ -536,8 +539,8 @@ static cudaError_t launch_rb(const VecchiaArgs& a, cudaStream_t s) {
         last = v;
       }
     }
-    kern<<<blocks, VW * 32, smem, s>>>(a.U, a.ldu, a.mk, a.ld, a.X, a.nbr, a.mv, a.order, a.npts, a.p, a.W, a.ldw,
-                                       a.Dpos, a.B_out, a.D_out, a.st);
+    kern<<<blocks, VW * 32, smem, s>>>(a.U, a.ldu, a.mk, a.ld, a.X, a.Uself ? a.Uself : a.U, a.Xself ? a.Xself : a.X,
+                                       a.nbr, a.mv, a.order, a.npts, a.p, a.W, a.ldw, a.Dpos, a.B_out, a.D_out, a.st);
   } else {
     const size_t smem = (size_t)VW * vecchia_warp_doubles<RB>() * sizeof(double);
     static bool attr = false;
@@ -547,7 +550,8 @@ static cudaError_t launch_rb(const VecchiaArgs& a, cudaStream_t s) {
       if (e != cudaSuccess) return e;
       attr = true;
     }
-    vecchia_smem_kernel<FAM, RB, NB><<<blocks, VW * 32, smem, s>>>(a.U, a.ldu, a.mk, a.ld, a.X, a.nbr, a.mv,
+    vecchia_smem_kernel<FAM, RB, NB><<<blocks, VW * 32, smem, s>>>(a.U, a.ldu, a.mk, a.ld, a.X, a.Uself ? a.Uself : a.U,
+                                                                   a.Xself ? a.Xself : a.X, a.nbr, a.mv,
                                                                    a.order, a.npts, a.p, a.W, a.ldw, a.Dpos,
                                                                    a.B_out, a.D_out, a.st);
   }

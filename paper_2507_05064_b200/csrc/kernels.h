@@ -24,6 +24,10 @@ struct VecchiaArgs {
   double* B_out;
   double* D_out;
   DevStatus* st;
+  // the point's own row (index i = order[pos]) comes from Uself / Xself when set (prediction:
+  // prediction points whose neighbours are training rows of U / X); NULL = U / X
+  const double* Uself = nullptr;
+  const double* Xself = nullptr;
 };
 
 // K0 / K5
@@ -82,6 +86,10 @@ cudaError_t launch_grad_q(const double* LinvM, int ldi, const double* G, int ldg
                           double* zh, double* z, double* Q2, cudaStream_t s);
 cudaError_t launch_gemm_tn(const double* A, int64_t lda, int64_t nrows, const double* B, int64_t ldb, int N, int K,
                            int tri, double* C, int64_t ldc, double alpha, int accum, cudaStream_t s);
+cudaError_t launch_zvec(const double* LinvM, int ldi, const double* G, int ldg, int ycol, int m, double* zh,
+                        double* z, cudaStream_t s);
+cudaError_t launch_pred_mean(const double* Wp, int ld, int m, int ycol, const double* z, const double* Dpos,
+                             const int64_t* order, int64_t np, double* mu, cudaStream_t s);
 // misc
 cudaError_t launch_validate(const double* X, int64_t n, int d, const double* Z, int m, const double* y,
                             const int32_t* nbr, int mv, DevStatus* st, cudaStream_t s);

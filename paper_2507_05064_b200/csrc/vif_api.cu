@@ -324,6 +324,36 @@ Layout make_grad_layout(const Plan& P) {
   return L;
 }
 
+// ---------------------------------------------------------------- prediction workspace
+enum PBuf { P_X, P_NBR, P_Y, P_U, P_S, P_W, P_DPOS, P_KEYS, P_KEYS2, P_VALS, P_VALS2, P_TEMP, P_BBOX, P_LINVM,
+            P_MCOPY, P_TSCR, P_ZH, P_Z, P_COUNT };
+
+Layout make_pred_layout(const Plan& P, int64_t np) {
+  Layout L{};
+  const size_t D8 = sizeof(double);
+  const int64_t mk1 = P.mk > 0 ? P.mk : 1;
+  L.size[P_X] = (size_t)np * P.d * D8;
+  L.size[P_NBR] = (size_t)np * (P.mv > 0 ? P.mv : 1) * sizeof(int32_t);
+  L.size[P_Y] = (size_t)np * D8;
+  L.size[P_U] = (size_t)np * P.ld * D8;
+  L.size[P_S] = (size_t)np * mk1 * D8;
+  L.size[P_W] = (size_t)np * P.ld * D8;
+  L.size[P_DPOS] = (size_t)np * D8;
+  L.size[P_KEYS] = L.size[P_KEYS2] = L.size[P_VALS] = L.size[P_VALS2] = (size_t)np * 8;
+  L.size[P_TEMP] = order_temp_bytes(np);
+  L.size[P_BBOX] = 128 * 6 * D8;
+  L.size[P_LINVM] = L.size[P_TSCR] = (size_t)mk1 * mk1 * D8;
+  L.size[P_MCOPY] = (size_t)P.ld * P.ld * D8;
+  L.size[P_ZH] = L.size[P_Z] = (size_t)mk1 * D8;
+  size_t off = 0;
+  for (int b = 0; b < P_COUNT; ++b) {
+    L.off[b] = off;
+    off += (L.size[b] + 255) / 256 * 256;
+  }
+  L.total = off + 256;
+  return L;
+}
+
 }  // namespace
 
 // ====================================================================== C ABI
@@ -728,6 +758,98 @@ int vif_grad(void* handle, const vif_theta* theta, void* gws, size_t gws_bytes, 
   VIF_CUDA(h, cudaStreamSynchronize(s), "sync");
   for (int pi = 0; pi < P.d + 2; ++pi)
     if (!isfinite(grad[pi])) return fail(h, VIF_ERR_NOT_PD, "gradient: a residual block or M is not positive definite");
+  return VIF_OK;
+}
+
+int vif_predict_workspace_bytes(const vif_dims* dims, int64_t np, size_t* bytes) {
+  Plan P;
+  std::string err;
+  if (!bytes) return fail(nullptr, VIF_ERR_INVALID_ARG, "bytes is NULL");
+  if (np < 1) return fail(nullptr, VIF_ERR_INVALID_ARG, "np must be >= 1");
+  if (!make_plan(dims, true, P, err)) return fail(nullptr, VIF_ERR_INVALID_ARG, err);
+  *bytes = make_pred_layout(P, np).total;
+  return VIF_OK;
+}
+
+int vif_predict(void* handle, const vif_theta* theta, int64_t np, const double* Xp, const int32_t* nbrp, void* ws,
+                size_t ws_bytes, double* mu, double* Dp, double* Bp) {
+  Handle* h = reinterpret_cast<Handle*>(handle);
+  if (!h) return fail(nullptr, VIF_ERR_INVALID_ARG, "handle is NULL");
+  const Plan& P = h->P;
+  if (np < 1 || !Xp || !mu || (P.mv > 0 && !nbrp)) return fail(h, VIF_ERR_INVALID_ARG, "vif_predict: bad arguments");
+  if (P.world != 1) return fail(h, VIF_ERR_INVALID_ARG, "vif_predict: single-rank handles only in this version");
+  const Layout PL = make_pred_layout(P, np);
+  if (!ws || ws_bytes < PL.total) {
+    char msg[128];
+    snprintf(msg, sizeof msg, "prediction workspace too small: need %zu bytes", PL.total);
+    return fail(h, VIF_ERR_NO_MEMORY, msg);
+  }
+  char* pb = reinterpret_cast<char*>(round_up((int64_t)(uintptr_t)ws, 256));
+  auto pbuf = [&](PBuf b) { return reinterpret_cast<double*>(pb + PL.off[b]); };
+  CovParams p;
+  std::string err;
+  if (!make_params(h, theta, p, err)) return fail(h, VIF_ERR_INVALID_ARG, err);
+  cudaStream_t s = h->stream;
+  VIF_CUDA(h, cudaMemcpyAsync(pbuf(P_X), Xp, (size_t)np * P.d * 8, cudaMemcpyDefault, s), "copy Xp");
+  if (P.mv > 0)
+    VIF_CUDA(h, cudaMemcpyAsync(pbuf(P_NBR), nbrp, (size_t)np * P.mv * 4, cudaMemcpyDefault, s), "copy nbrp");
+  int r = vif_factor(handle, theta, nullptr, nullptr);
+  if (r != VIF_OK) return r;
+  const int m = P.m, mk = P.mk, ld = P.ld;
+  double* G = h->buf<double>(B_G);
+  VIF_CUDA(h, cudaMemcpyAsync(pbuf(P_MCOPY), G, (size_t)ld * ld * 8, cudaMemcpyDeviceToDevice, s), "copy G");
+  vif_terms t;
+  r = vif_nll(handle, &t);
+  if (r != VIF_OK) return r;
+  DevStatus* st = h->buf<DevStatus>(B_STATUS);
+  // z = M_w^{-1} G_Wr
+  if (m > 0) {
+    VIF_CUDA(h, cudaMemsetAsync(pbuf(P_LINVM), 0, PL.size[P_LINVM], s), "memset");
+    VIF_CUDA(h, launch_chol_inv(pbuf(P_MCOPY), m, ld, 1.0, pbuf(P_LINVM), mk, mk, 1, pbuf(P_TSCR), &st->m_fail,
+                                h->num_sms, s),
+             "chol M (full inverse)");
+    VIF_CUDA(h, launch_zvec(pbuf(P_LINVM), mk, G, ld, P.ycol, m, pbuf(P_ZH), pbuf(P_Z), s), "z");
+  }
+  // prediction features u_p (y column 0), Morton processing order of the prediction points
+  VIF_CUDA(h, cudaMemsetAsync(pbuf(P_Y), 0, PL.size[P_Y], s), "memset y_p");
+  VIF_CUDA(h, launch_u_features(pbuf(P_X), h->buf<double>(B_Z), pbuf(P_Y), np, 0, np, np, 1, 0, m, mk, p,
+                                h->buf<double>(B_LINV), pbuf(P_S), pbuf(P_U), ld, s),
+           "prediction features");
+  int64_t* order = nullptr;
+  VIF_CUDA(h, launch_order(pbuf(P_X), np, P.d, np, np, 1, 0, pbuf(P_BBOX), reinterpret_cast<uint64_t*>(pbuf(P_KEYS)),
+                           reinterpret_cast<uint64_t*>(pbuf(P_KEYS2)), reinterpret_cast<int64_t*>(pbuf(P_VALS)),
+                           reinterpret_cast<int64_t*>(pbuf(P_VALS2)), pbuf(P_TEMP), PL.size[P_TEMP], &order, s),
+           "prediction order");
+  VIF_CUDA(h, launch_reset_status(st, s), "reset status");
+  VecchiaArgs a;
+  a.U = h->buf<double>(B_U);
+  a.ldu = ld;
+  a.mk = mk;
+  a.ld = ld;
+  a.X = h->buf<double>(B_X);
+  a.nbr = reinterpret_cast<const int32_t*>(pbuf(P_NBR));
+  a.mv = P.mv;
+  a.order = order;
+  a.npts = np;
+  a.p = p;
+  a.W = pbuf(P_W);
+  a.ldw = ld;
+  a.Dpos = pbuf(P_DPOS);
+  a.B_out = Bp;
+  a.D_out = Dp;
+  a.st = st;
+  a.Uself = pbuf(P_U);
+  a.Xself = pbuf(P_X);
+  VIF_CUDA(h, launch_vecchia(a, s), "prediction rows");
+  VIF_CUDA(h, launch_pred_mean(pbuf(P_W), ld, m, P.ycol, pbuf(P_Z), pbuf(P_DPOS), order, np, mu, s), "mean");
+  DevStatus hs;
+  VIF_CUDA(h, cudaMemcpyAsync(&hs, st, sizeof(hs), cudaMemcpyDeviceToHost, s), "status copy");
+  VIF_CUDA(h, cudaStreamSynchronize(s), "sync");
+  if (hs.bad_row != ~0ULL) {
+    char msg[128];
+    snprintf(msg, sizeof msg, "residual block of prediction point %llu is not positive definite", hs.bad_row);
+    return fail(h, VIF_ERR_NOT_PD, msg);
+  }
   return VIF_OK;
 }
 

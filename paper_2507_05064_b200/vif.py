@@ -79,9 +79,11 @@ def load_library():
         lib.vif_destroy.restype = None
         lib.vif_grad_workspace_bytes.argtypes = [ctypes.POINTER(_Dims), ctypes.POINTER(sz)]
         lib.vif_grad.argtypes = [P, ctypes.POINTER(_Theta), P, sz, P, ctypes.POINTER(_Terms)]
+        lib.vif_predict_workspace_bytes.argtypes = [ctypes.POINTER(_Dims), i64, ctypes.POINTER(sz)]
+        lib.vif_predict.argtypes = [P, ctypes.POINTER(_Theta), i64, P, P, P, sz, P, P, P]
         for f in ("vif_nccl_unique_id", "vif_workspace_bytes", "vif_partition", "vif_create", "vif_set_data",
                   "vif_factor", "vif_nll", "vif_copy_U", "vif_launch_count", "vif_profile", "vif_stage_times",
-                  "vif_grad_workspace_bytes", "vif_grad"):
+                  "vif_grad_workspace_bytes", "vif_grad", "vif_predict_workspace_bytes", "vif_predict"):
             getattr(lib, f).restype = ctypes.c_int
         _lib = lib
     return _lib
@@ -89,7 +91,8 @@ def load_library():
 
 EXPORTED = ("vif_nccl_unique_id", "vif_workspace_bytes", "vif_partition", "vif_create", "vif_set_data",
             "vif_factor", "vif_nll", "vif_copy_U", "vif_launch_count", "vif_profile", "vif_stage_times",
-            "vif_stage_name", "vif_last_error", "vif_destroy", "vif_grad_workspace_bytes", "vif_grad")
+            "vif_stage_name", "vif_last_error", "vif_destroy", "vif_grad_workspace_bytes", "vif_grad",
+            "vif_predict_workspace_bytes", "vif_predict")
 NUM_STAGES = 8
 
 
@@ -226,6 +229,23 @@ def vif_grad(h, theta: Theta, grad_workspace: torch.Tensor):
     return Terms(t.nll, t.logdet_D, t.logdet_M, t.quad, t.bad_row), g
 
 
+def vif_predict_workspace_bytes(n: int, d: int, m: int, mv: int, npred: int, rank: int = 0, world: int = 1) -> int:
+    b = ctypes.c_size_t(0)
+    _check(load_library().vif_predict_workspace_bytes(ctypes.byref(_dims(n, d, m, mv, rank, world)), int(npred),
+                                                      ctypes.byref(b)))
+    return int(b.value)
+
+
+def vif_predict(h, theta: Theta, Xp: torch.Tensor, nbrp: Optional[torch.Tensor], workspace: torch.Tensor,
+                mu: torch.Tensor, Dp: Optional[torch.Tensor] = None, Bp: Optional[torch.Tensor] = None):
+    """Predictive means (Prop. 1) into mu (device, np); optional D_p and B_p = -A_p."""
+    th, keep = theta.to_c()
+    st = load_library().vif_predict(h, ctypes.byref(th), int(Xp.shape[0]), _ptr(Xp), _ptr(nbrp),
+                                    ctypes.c_void_p(workspace.data_ptr()), workspace.numel(), _ptr(mu), _ptr(Dp),
+                                    _ptr(Bp))
+    _check(st, h)
+
+
 def vif_copy_U(h, out: torch.Tensor):
     _check(load_library().vif_copy_U(h, _ptr(out)), h)
 
@@ -304,6 +324,23 @@ class VifModel:
             nbytes = vif_grad_workspace_bytes(self.n, self.d, self.m, self.mv, self.rank, self.world)
             self.grad_workspace = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
         return vif_grad(self.handle, theta, self.grad_workspace)
+
+    def predict(self, theta: Theta, Xp, nbrp, want_D: bool = False, want_B: bool = False):
+        """Predictive means at Xp (np x d) with training-neighbour sets nbrp (np x m_v); returns mu (and
+        D_p, B_p = -A_p when asked) as device tensors."""
+        Xp = _as_input(Xp, torch.float64, self.device)
+        nbrp = _as_input(nbrp, torch.int32, self.device) if self.mv > 0 else None
+        npred = Xp.shape[0]
+        nbytes = vif_predict_workspace_bytes(self.n, self.d, self.m, self.mv, npred, self.rank, self.world)
+        ws = getattr(self, "pred_workspace", None)
+        if ws is None or ws.numel() < nbytes:
+            ws = self.pred_workspace = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
+        mu = torch.empty(npred, dtype=torch.float64, device=self.device)
+        Dp = torch.empty(npred, dtype=torch.float64, device=self.device) if want_D else None
+        Bp = torch.empty((npred, self.mv), dtype=torch.float64, device=self.device) if want_B else None
+        vif_predict(self.handle, theta, Xp, nbrp, ws, mu, Dp, Bp)
+        out = (mu,) + ((Dp,) if want_D else ()) + ((Bp,) if want_B else ())
+        return out[0] if len(out) == 1 else out
 
     def U(self) -> torch.Tensor:
         out = torch.empty((self.n, self.m), dtype=torch.float64, device=self.device)

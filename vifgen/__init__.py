@@ -328,3 +328,74 @@ def make_config(cid: int, device=None, n: Optional[int] = None) -> Workload:
     return make_workload(n=c["n"], d=c["d"], m=c["m"], mv=c["mv"], family=c["family"], sigma2=c["sigma2"],
                          rho=c.get("rho"), ard=c.get("ard"), nugget=c["nugget"], x=c["x"], z=c["z"],
                          seed=SEED_BASE + cid, device=device, name=f"config{cid}")
+
+
+# ----------------------------------------------------------------------------------------------
+# prediction inputs (reading p1 in DESIGN.md)
+def dc_neighbors_pred(Xs: np.ndarray, Xps: np.ndarray, Zs: np.ndarray, family: str, sigma2: float, jitter: float,
+                      mv: int, device=None, qblock: int = 8192, cblock: int = 65536) -> np.ndarray:
+    """For each prediction input, the m_v training inputs nearest under d_c, exact brute force,
+    ranked by (d_c, index) (reading c6); training candidates with degenerate residual variance get
+    d_c = 1 and a degenerate query ranks by scaled Euclidean distance (reading c7).  Coordinates are
+    already divided by the length-scales (Xs, Xps, Zs)."""
+    n, npred = Xs.shape[0], Xps.shape[0]
+    dev = _device(device)
+    k = min(mv, n)
+    out = np.full((npred, mv), -1, dtype=np.int32)
+    if k == 0:
+        return out
+    Xt = torch.from_numpy(Xs).to(dev)
+    Xpt = torch.from_numpy(Xps).to(dev)
+    m = Zs.shape[0]
+    if m > 0:
+        U = whitened_features(Xs, Zs, family, sigma2, jitter, device=dev)
+        Up = whitened_features(Xps, Zs, family, sigma2, jitter, device=dev)
+        rdiag = sigma2 - (U * U).sum(1)
+        rdiag_p = sigma2 - (Up * Up).sum(1)
+    else:
+        U = Up = None
+        rdiag = torch.full((n,), sigma2, dtype=torch.float64, device=dev)
+        rdiag_p = torch.full((npred,), sigma2, dtype=torch.float64, device=dev)
+    tau = 1e-7 * sigma2
+    inv_sd = torch.where(rdiag < tau, torch.zeros_like(rdiag), 1.0 / torch.sqrt(torch.clamp(rdiag, min=tau)))
+    degenerate_p = rdiag_p < tau
+    inv_sd_p = torch.where(degenerate_p, torch.ones_like(rdiag_p), 1.0 / torch.sqrt(torch.clamp(rdiag_p, min=tau)))
+    for q0 in range(0, npred, qblock):
+        q1 = min(npred, q0 + qblock)
+        nq = q1 - q0
+        best_v = torch.full((nq, k), -math.inf, dtype=torch.float64, device=dev)
+        best_i = torch.full((nq, k), -1, dtype=torch.int64, device=dev)
+        for c0 in range(0, n, cblock):
+            c1 = min(c0 + cblock, n)
+            score = _cov_from_r(family, sigma2, _sqdist(Xpt[q0:q1], Xt[c0:c1]))
+            if U is not None:
+                score -= Up[q0:q1] @ U[c0:c1].T
+            score.abs_()
+            score *= inv_sd_p[q0:q1, None]
+            score *= inv_sd[None, c0:c1]
+            jc = torch.arange(c0, c1, device=dev)
+            cat_v = torch.cat([best_v, score], 1)
+            cat_i = torch.cat([best_i, jc[None, :].expand(nq, -1)], 1)
+            v, pos = torch.topk(cat_v, k, dim=1)
+            best_v, best_i = v, torch.gather(cat_i, 1, pos)
+        bv, bi = best_v.cpu().numpy(), best_i.cpu().numpy()
+        for r in range(nq):
+            order = np.lexsort((bi[r], -bv[r]))
+            out[q0 + r, :k] = bi[r][order]
+    for pq in torch.nonzero(degenerate_p).flatten().cpu().numpy():
+        d2 = ((Xt - Xpt[pq]) ** 2).sum(1).cpu().numpy()
+        out[pq, :k] = np.lexsort((np.arange(n), d2))[:k]
+    return out
+
+
+def make_prediction(w: Workload, npred: int, seed: int = SEED_BASE + 100, x: str = "uniform", device=None):
+    """Seeded prediction inputs drawn like the training inputs (uniform on the unit cube, or N(0, I)) and
+    their d_c neighbour sets among the training points.  Returns (Xp, nbrp)."""
+    g = np.random.Generator(np.random.PCG64(np.random.SeedSequence(seed)))
+    d = w.X.shape[1]
+    Xp = g.random((npred, d)) if x == "uniform" else g.standard_normal((npred, d))
+    Xp = np.ascontiguousarray(Xp)
+    lam = np.asarray(w.lengthscale, dtype=np.float64)
+    nbrp = dc_neighbors_pred(w.X / lam, Xp / lam, w.Z.reshape(-1, d) / lam, w.family, w.sigma2, w.jitter, w.mv,
+                             device=device)
+    return Xp, np.ascontiguousarray(nbrp, dtype=np.int32)
