@@ -45,6 +45,7 @@ def parse():
     ap.add_argument("--impl", default="vif", choices=["vif", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-grad", action="store_true", help="skip the NLL-gradient timing (vif_grad)")
+    ap.add_argument("--npred", type=int, default=100000, help="prediction points for the vif_predict timing (0: skip)")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target CPU seconds of the oracle sample")
     return ap.parse_args()
 
@@ -299,6 +300,29 @@ def main():
                 "note": "vif_grad: factor + NLL + d+2 partial derivatives (sigma_1^2, lambda_1..d, sigma^2; "
                         "P:126-133, App. A), device events around the synchronous calls"}
 
+    # ---------------- predictive means (vif_predict, single GPU) ----------------
+    pred = None
+    if world == 1 and args.npred > 0:
+        t_pg = time.perf_counter()
+        Xp, nbrp = vifgen.make_prediction(w, args.npred, x="normal" if cid == 4 else "uniform", device=str(dev))
+        pgen = time.perf_counter() - t_pg
+        Xp_d, nbrp_d = torch.from_numpy(Xp).to(dev), torch.from_numpy(nbrp).to(dev)
+        model.predict(th[0], Xp_d, nbrp_d)
+        p_steps = 3
+        torch.cuda.synchronize(dev)
+        q0, q1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        q0.record(stream)
+        for k in range(p_steps):
+            mu = model.predict(th[k % 2], Xp_d, nbrp_d)
+        q1.record(stream)
+        torch.cuda.synchronize(dev)
+        pms = q0.elapsed_time(q1) / p_steps
+        pred = {"ms_per_call": pms, "npred": args.npred,
+                "note": "vif_predict: factor + NLL at theta (training, n points) + prediction features + "
+                        "Vecchia rows of the prediction points + means (Prop. 1, P:137-152); "
+                        f"prediction inputs and their d_c neighbours generated in {pgen:.1f} s (not timed)",
+                "mu_mean": float(mu.mean().item())}
+
     if rank == 0:
         fl = workload_flops(w.nbr, w.m)
         # per-rank share of the row-sharded kernels (strong scaling: each rank does ~1/world of the rows)
@@ -360,6 +384,7 @@ def main():
             "stages_ms_per_step": stage_avg,
             "nll": last.nll,
             "grad": grad,
+            "predict": pred,
             "input_generation_s": {"total": gen_s, **{k: round(v, 3) for k, v in w.timings.items()}},
             "create_s": create_s,
         }
