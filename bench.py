@@ -307,21 +307,22 @@ def main():
         Xp, nbrp = vifgen.make_prediction(w, args.npred, x="normal" if cid == 4 else "uniform", device=str(dev))
         pgen = time.perf_counter() - t_pg
         Xp_d, nbrp_d = torch.from_numpy(Xp).to(dev), torch.from_numpy(nbrp).to(dev)
-        model.predict(th[0], Xp_d, nbrp_d)
+        model.predict(th[0], Xp_d, nbrp_d, want_var=True)
         p_steps = 3
         torch.cuda.synchronize(dev)
         q0, q1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         q0.record(stream)
         for k in range(p_steps):
-            mu = model.predict(th[k % 2], Xp_d, nbrp_d)
+            mu, var = model.predict(th[k % 2], Xp_d, nbrp_d, want_var=True)
         q1.record(stream)
         torch.cuda.synchronize(dev)
         pms = q0.elapsed_time(q1) / p_steps
         pred = {"ms_per_call": pms, "npred": args.npred,
                 "note": "vif_predict: factor + NLL at theta (training, n points) + prediction features + "
-                        "Vecchia rows of the prediction points + means (Prop. 1, P:137-152); "
+                        "Vecchia rows of the prediction points + means and variances (Prop. 1, P:137-152; "
+                        "App. C.1); "
                         f"prediction inputs and their d_c neighbours generated in {pgen:.1f} s (not timed)",
-                "mu_mean": float(mu.mean().item())}
+                "mu_mean": float(mu.mean().item()), "var_mean": float(var.mean().item())}
 
     if rank == 0:
         fl = workload_flops(w.nbr, w.m)

@@ -143,22 +143,25 @@ int vif_grad_workspace_bytes(const vif_dims* dims, size_t* bytes);
 int vif_grad(void* handle, const vif_theta* theta, void* grad_workspace, size_t grad_ws_bytes, double* grad,
              vif_terms* terms);
 
-/* Predictive means of the response at np prediction inputs (Proposition 1), reading p1:
- * each prediction point conditions on m_v training points (B_p = I, B_po = -A_p), so
- *   mu_p = u_p . z + A_p (y_N(p) - U_N(p) z),   u_p = L_m^{-1} k(Z, x_p),  z = M_w^{-1} G_Wr,
+/* Predictive distribution of the response at np prediction inputs (Proposition 1, and the
+ * equivalent variance expression of Appendix C.1), reading p1: each prediction point
+ * conditions on m_v training points (B_p = I, B_po = -A_p), so with the whitened row
+ * e_p = u_p - A_p U_N(p) of the prediction point,
+ *   mu_p  = u_p . z + A_p (y_N(p) - U_N(p) z),          z = M_w^{-1} G_Wr,
+ *   var_p = D_p + e_p^T M_w^{-1} e_p,                    u_p = L_m^{-1} k(Z, x_p),
  *   A_p = C_{p,N} C_{N,N}^{-1},  D_p = C_pp - A_p C_{N,p}   (residual covariance C as in vif_factor,
- *   C_pp = sigma_1^2 + sigma^2 - |u_p|^2: the response, not the latent process).
+ *   C_pp = sigma_1^2 + sigma^2 - |u_p|^2: the response; the latent b_p has var_p - sigma^2).
  * vif_predict runs vif_factor + vif_nll at theta, then the prediction features (kx_eval + triangular
  * GEMM), the per-point Vecchia rows of the prediction points against the training rows (the factor's
- * kernel) and mu; synchronises.
+ * kernel), e_p M_w^{-1} e_p by one triangular GEMM with L_M^{-1}, and mu / var; synchronises.
  * Xp: np x d (device or host), nbrp: np x m_v training indices in [0, n), -1 only as trailing pad
  * (host or device); workspace: caller-owned device buffer of vif_predict_workspace_bytes(dims, np).
- * mu (device, np, required), Dp (device, np, optional: D_p), Bp (device, np x m_v, optional: -A_p).
+ * mu (device, np, required); var, Dp (device, np, optional); Bp (device, np x m_v, optional: -A_p).
  * Errors: INVALID_ARG (np < 1, NULL, world > 1), NO_MEMORY (workspace), NOT_PD (training factor, or a
- * prediction block: terms->bad_row is not set, the message names the prediction row), CUDA. */
+ * prediction block: the message names the prediction row), CUDA. */
 int vif_predict_workspace_bytes(const vif_dims* dims, int64_t np, size_t* bytes);
 int vif_predict(void* handle, const vif_theta* theta, int64_t np, const double* Xp, const int32_t* nbrp,
-                void* workspace, size_t ws_bytes, double* mu, double* Dp, double* Bp);
+                void* workspace, size_t ws_bytes, double* mu, double* var, double* Dp, double* Bp);
 
 /* Debug / parity: copy the whitened features U (n x m, row-major) to `out` (device or host). */
 int vif_copy_U(void* handle, double* out);

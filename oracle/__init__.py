@@ -60,7 +60,7 @@ def _load():
         _lib.oracle_num_threads.restype = ctypes.c_int
         _lib.oracle_grad.argtypes = [i64, i32, i32, P, P, P, P, P, P, P, P]
         _lib.oracle_dcov_matrix.argtypes = [P, P, i64, P, i64, P]
-        _lib.oracle_predict.argtypes = [i64, i32, i32, P, P, P, P, P, i64, P, P, P, P, P, P]
+        _lib.oracle_predict.argtypes = [i64, i32, i32, P, P, P, P, P, i64, P, P, P, P, P, P, P]
     return _lib
 
 
@@ -230,7 +230,8 @@ def dcov_matrix(theta: Theta, A: np.ndarray, B: np.ndarray) -> np.ndarray:
 
 
 def predict(X, Z, nbr, y, theta: Theta, Xp, nbrp):
-    """Oracle predictive means (Prop. 1; reading p1): returns (mu, D_p, B_p = -A_p)."""
+    """Oracle predictive means and variances (Prop. 1; App. C.1; reading p1):
+    returns (mu, var, D_p, B_p = -A_p)."""
     lib = _load()
     X, Z, y = _f64(X), _f64(Z).reshape(-1, X.shape[1]), _f64(y)
     Xp = _f64(Xp).reshape(-1, X.shape[1])
@@ -239,14 +240,14 @@ def predict(X, Z, nbr, y, theta: Theta, Xp, nbrp):
     n, mv = nbr.shape
     npred = Xp.shape[0]
     m = Z.shape[0]
-    mu, Dp, Bp = np.zeros(npred), np.zeros(npred), np.zeros((npred, mv))
+    mu, var, Dp, Bp = np.zeros(npred), np.zeros(npred), np.zeros(npred), np.zeros((npred, mv))
     bad = ctypes.c_int64(-1)
     th, keep = theta._c()
     st = lib.oracle_predict(n, m, mv, _p(X), _p(Z), _p(nbr), _p(y), ctypes.byref(th), npred, _p(Xp), _p(nbrp),
-                            _p(mu), _p(Dp), _p(Bp), ctypes.byref(bad))
+                            _p(mu), _p(var), _p(Dp), _p(Bp), ctypes.byref(bad))
     if st != 0:
         raise OracleError(st, bad.value)
-    return mu, Dp, Bp
+    return mu, var, Dp, Bp
 
 
 def num_threads() -> int:

@@ -753,13 +753,14 @@ done:
  *   mu_p = u_p . z + A_p (y_N(p) - U_N(p) z),  u_p = L_m^{-1} k(Z, x_p),
  *   A_p = C_{p,N} C_{N,N}^{-1},  D_p = C_pp - A_p C_{N,p},
  *   C(a,b) = k - u_a.u_b + sigma^2 [a = b] on training pairs, C(p,a) = k(x_p,x_a) - u_p.u_a,
- *   C_pp = sigma_1^2 + sigma^2 - u_p.u_p  (the response y_p).
- * Derivation from Prop. 1 with whitening in DESIGN.md section 11; pinned in tests/test_oracle_pred.py
+ *   C_pp = sigma_1^2 + sigma^2 - u_p.u_p  (the response y_p),
+ *   var_p = D_p + e_p^T M_w^{-1} e_p,  e_p = u_p - sum_k A_pk u_N(p)_k   (App. C.1).
+ * Derivation from Prop. 1 / App. C.1 with whitening in DESIGN.md section 11; pinned in tests/test_oracle_pred.py
  * against the exact GP (all training points as neighbours) and the paper's dense formula P:143-144.
  * ===================================================================================== */
 int oracle_predict(int64_t n, int m, int mv, const double *X, const double *Z, const int32_t *nbr, const double *y,
-                   const or_theta *th, int64_t np, const double *Xp, const int32_t *nbrp, double *mu, double *Dp,
-                   double *Bp, int64_t *bad_row) {
+                   const or_theta *th, int64_t np, const double *Xp, const int32_t *nbrp, double *mu, double *var,
+                   double *Dp, double *Bp, int64_t *bad_row) {
   *bad_row = -1;
   const int d = th->d, m1 = m > 0 ? m : 1, s_max = mv + 1;
   double *Lm = NULL, *U = NULL;
@@ -879,6 +880,19 @@ int oracle_predict(int64_t n, int m, int mv, const double *X, const double *Z, c
           mean += ap[a] * (y[row[a]] - uz);
         }
         mu[t] = mean;
+        if (var) {
+          /* e_p M_w^{-1} e_p = |L_M^{-1} e_p|^2 (M holds L_M after step 6) */
+          double *e = (double *)malloc(sizeof(double) * m1), vv = D;
+          for (int k = 0; k < m; ++k) {
+            double t2 = up[k];
+            for (int a = 0; a < q; ++a) t2 -= ap[a] * U[(size_t)row[a] * m + k];
+            e[k] = t2;
+          }
+          if (m > 0) or_fwd(M, m, m, e);
+          for (int k = 0; k < m; ++k) vv += e[k] * e[k];
+          var[t] = vv;
+          free(e);
+        }
         if (Dp) Dp[t] = D;
         if (Bp)
           for (int a = 0; a < mv; ++a) Bp[t * mv + a] = a < q ? -ap[a] : 0.0;

@@ -450,26 +450,42 @@ cudaError_t launch_kx_deriv(const double* X, const double* Z, int64_t npos, int 
   }
 }
 
-// Prediction (Prop. 1): mu_p = sqrt(D_p) (w_p . z - r_p) for the prediction row
-// [w_p, r_p] (computed with y_p = 0) = u_p . z + A_p (y_N - U_N z).
+// Prediction (Prop. 1; App. C.1): for the prediction row [w_p, r_p] (computed with y_p = 0,
+// w_p = e_p / sqrt(D_p)):  mu_p = sqrt(D_p) (w_p . z - r_p) = u_p . z + A_p (y_N - U_N z),
+// var_p = D_p (1 + |T_p|^2), T = W L_M^{-T} (so D_p |T_p|^2 = e_p^T M_w^{-1} e_p).  One warp per point.
 __global__ void pred_mean_kernel(const double* __restrict__ Wp, int ld, int m, int ycol, const double* __restrict__ z,
                                  const double* __restrict__ Dpos, const int64_t* __restrict__ order, int64_t np,
-                                 double* __restrict__ mu) {
+                                 double* __restrict__ mu, const double* __restrict__ T, int ldt,
+                                 double* __restrict__ var) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t pos = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
   if (pos >= np) return;
   const double* w = Wp + pos * (int64_t)ld;
-  double s = 0.0;
+  double s = 0.0, t2 = 0.0;
   for (int a = lane; a < m; a += 32) s = fma(w[a], z[a], s);
+  if (T)
+    for (int a = lane; a < m; a += 32) {
+      const double t = T[pos * (int64_t)ldt + a];
+      t2 = fma(t, t, t2);
+    }
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-  if (lane == 0) mu[order[pos]] = sqrt(Dpos[pos]) * (s - w[ycol]);
+  for (int o = 16; o > 0; o >>= 1) {
+    s += __shfl_xor_sync(0xffffffffu, s, o);
+    t2 += __shfl_xor_sync(0xffffffffu, t2, o);
+  }
+  if (lane == 0) {
+    const double D = Dpos[pos];
+    const int64_t i = order[pos];
+    mu[i] = sqrt(D) * (s - w[ycol]);
+    if (var) var[i] = D * (1.0 + t2);
+  }
 }
 
 cudaError_t launch_pred_mean(const double* Wp, int ld, int m, int ycol, const double* z, const double* Dpos,
-                             const int64_t* order, int64_t np, double* mu, cudaStream_t s) {
+                             const int64_t* order, int64_t np, double* mu, const double* T, int ldt, double* var,
+                             cudaStream_t s) {
   if (np == 0) return cudaSuccess;
-  pred_mean_kernel<<<(unsigned)((np + 7) / 8), 256, 0, s>>>(Wp, ld, m, ycol, z, Dpos, order, np, mu);
+  pred_mean_kernel<<<(unsigned)((np + 7) / 8), 256, 0, s>>>(Wp, ld, m, ycol, z, Dpos, order, np, mu, T, ldt, var);
   return cudaGetLastError();
 }
 

@@ -327,7 +327,8 @@ __host__ __device__ constexpr int vreg_warp_doubles(int d) {
   return RB * 8 * (RB * 8 + 1) + 2 * RB * 8 + RB * 8 + RB * 8 * d;  // C, colbuf[2], coef, xs
 }
 
-template <int FAM, int RB, int NB, int MINB>
+// SELF: the point's own row / coordinates come from Uq / Xq (prediction); false for the factor
+template <int FAM, int RB, int NB, int MINB, bool SELF = false>
 __global__ void __launch_bounds__(VW * 32, MINB) vecchia_reg_kernel(
     const double* __restrict__ U, int64_t ldu, int mk, int ld, const double* __restrict__ X,
     const double* __restrict__ Uq, const double* __restrict__ Xq, const int32_t* __restrict__ nbr, int mv, const int64_t* __restrict__ order, int64_t npts, CovParams p,
@@ -358,7 +359,7 @@ __global__ void __launch_bounds__(VW * 32, MINB) vecchia_reg_kernel(
   const int s = q + 1;
   const int myidx = lane < q ? nb0 : (lane == q ? (int)i : -1);
   if (lane < SP) Sidx[lane] = myidx;
-  stage_xs<FAM>(X, Xq, myidx, p.d, p, lane, s, xs);
+  stage_xs<FAM>(X, SELF ? Xq : X, myidx, p.d, p, lane, s, xs);
   __syncwarp();
 
   // ---- 1 + 2. Gram on DMMA; the kernel evaluations of step 2 (independent of the Gram) run
@@ -371,7 +372,7 @@ __global__ void __launch_bounds__(VW * 32, MINB) vecchia_reg_kernel(
 #pragma unroll
   for (int R = 0; R < RB; ++R) {
     const int row = R * 8 + (lane >> 2), gi = Sidx[row];
-    rp[R] = gi >= 0 ? (row == q ? Uq : U) + (int64_t)gi * ldu + 2 * (lane & 3) : nullptr;  // row q: the point (Uq)
+    rp[R] = gi >= 0 ? (SELF && row == q ? Uq : U) + (int64_t)gi * ldu + 2 * (lane & 3) : nullptr;  // row q: the point (Uq)
   }
   {
     double2 f[NB][RB];
@@ -471,9 +472,9 @@ __global__ void __launch_bounds__(VW * 32, MINB) vecchia_reg_kernel(
     for (int t = 0; t < 8; ++t) o[t] = make_double2(0.0, 0.0);
     for (int k = 0; k < s; k += 2) {
       double2 u0[8], u1[8];
-      const double* r0 = (k == q ? Uq : U) + (int64_t)Sidx[k] * ldu + c0 + 2 * lane;
+      const double* r0 = (SELF && k == q ? Uq : U) + (int64_t)Sidx[k] * ldu + c0 + 2 * lane;
       const bool has1 = k + 1 < s;
-      const double* r1 = has1 ? (k + 1 == q ? Uq : U) + (int64_t)Sidx[k + 1] * ldu + c0 + 2 * lane : r0;
+      const double* r1 = has1 ? (SELF && k + 1 == q ? Uq : U) + (int64_t)Sidx[k + 1] * ldu + c0 + 2 * lane : r0;
 #pragma unroll
       for (int t = 0; t < 8; ++t) {
         const bool in = c0 + 2 * lane + 64 * t < ld;
@@ -514,20 +515,17 @@ static cudaError_t launch_rb(const VecchiaArgs& a, cudaStream_t s) {
     static const char* cfg_env = getenv("VIF_VREG_CFG");
     const int cfg = cfg_env ? atoi(cfg_env) : 34;
     decltype(&vecchia_reg_kernel<FAM, RB, 3, 4>) kern;
-    switch (cfg) {
-      case 24: kern = vecchia_reg_kernel<FAM, RB, 2, 4>; break;
-      case 44: kern = vecchia_reg_kernel<FAM, RB, 4, 4>; break;
-      case 33: kern = vecchia_reg_kernel<FAM, RB, 3, 3>; break;
-      case 43: kern = vecchia_reg_kernel<FAM, RB, 4, 3>; break;
-      case 25: kern = vecchia_reg_kernel<FAM, RB, 2, 5>; break;
-      case 26: kern = vecchia_reg_kernel<FAM, RB, 2, 6>; break;
-      default: kern = vecchia_reg_kernel<FAM, RB, 3, 4>; break;
+    if (a.Uself) {
+      kern = vecchia_reg_kernel<FAM, RB, 3, 4, true>;
+    } else {
+      switch (cfg) {
+        case 24: kern = vecchia_reg_kernel<FAM, RB, 2, 4>; break;
+        default: kern = vecchia_reg_kernel<FAM, RB, 3, 4>; break;
+      }
     }
-    static size_t attr = 0;
-    if (attr < smem) {
+    if (smem > 48 * 1024) {
       cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       if (e != cudaSuccess) return e;
-      attr = smem;
     }
     {
       const char* dbg = getenv("VIF_DEBUG_VECCHIA");

@@ -89,7 +89,8 @@ cudaError_t launch_gemm_tn(const double* A, int64_t lda, int64_t nrows, const do
 cudaError_t launch_zvec(const double* LinvM, int ldi, const double* G, int ldg, int ycol, int m, double* zh,
                         double* z, cudaStream_t s);
 cudaError_t launch_pred_mean(const double* Wp, int ld, int m, int ycol, const double* z, const double* Dpos,
-                             const int64_t* order, int64_t np, double* mu, cudaStream_t s);
+                             const int64_t* order, int64_t np, double* mu, const double* T, int ldt, double* var,
+                             cudaStream_t s);
 // misc
 cudaError_t launch_validate(const double* X, int64_t n, int d, const double* Z, int m, const double* y,
                             const int32_t* nbr, int mv, DevStatus* st, cudaStream_t s);

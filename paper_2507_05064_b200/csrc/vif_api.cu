@@ -772,7 +772,7 @@ int vif_predict_workspace_bytes(const vif_dims* dims, int64_t np, size_t* bytes)
 }
 
 int vif_predict(void* handle, const vif_theta* theta, int64_t np, const double* Xp, const int32_t* nbrp, void* ws,
-                size_t ws_bytes, double* mu, double* Dp, double* Bp) {
+                size_t ws_bytes, double* mu, double* var, double* Dp, double* Bp) {
   Handle* h = reinterpret_cast<Handle*>(handle);
   if (!h) return fail(nullptr, VIF_ERR_INVALID_ARG, "handle is NULL");
   const Plan& P = h->P;
@@ -841,7 +841,13 @@ int vif_predict(void* handle, const vif_theta* theta, int64_t np, const double* 
   a.Uself = pbuf(P_U);
   a.Xself = pbuf(P_X);
   VIF_CUDA(h, launch_vecchia(a, s), "prediction rows");
-  VIF_CUDA(h, launch_pred_mean(pbuf(P_W), ld, m, P.ycol, pbuf(P_Z), pbuf(P_DPOS), order, np, mu, s), "mean");
+  // T = E L_M^{-T} (rows e_p / sqrt(D_p) = the prediction W rows), so e_p M_w^{-1} e_p = D_p |T_p|^2
+  if (var && m > 0)
+    VIF_CUDA(h, launch_gemm_tn(pbuf(P_W), ld, np, pbuf(P_LINVM), mk, mk, mk, 1, pbuf(P_S), mk, 1.0, 0, s),
+             "W L_M^-T");
+  VIF_CUDA(h, launch_pred_mean(pbuf(P_W), ld, m, P.ycol, pbuf(P_Z), pbuf(P_DPOS), order, np, mu,
+                               var && m > 0 ? pbuf(P_S) : nullptr, mk, var, s),
+           "mean / variance");
   DevStatus hs;
   VIF_CUDA(h, cudaMemcpyAsync(&hs, st, sizeof(hs), cudaMemcpyDeviceToHost, s), "status copy");
   VIF_CUDA(h, cudaStreamSynchronize(s), "sync");

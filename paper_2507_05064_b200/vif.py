@@ -80,7 +80,7 @@ def load_library():
         lib.vif_grad_workspace_bytes.argtypes = [ctypes.POINTER(_Dims), ctypes.POINTER(sz)]
         lib.vif_grad.argtypes = [P, ctypes.POINTER(_Theta), P, sz, P, ctypes.POINTER(_Terms)]
         lib.vif_predict_workspace_bytes.argtypes = [ctypes.POINTER(_Dims), i64, ctypes.POINTER(sz)]
-        lib.vif_predict.argtypes = [P, ctypes.POINTER(_Theta), i64, P, P, P, sz, P, P, P]
+        lib.vif_predict.argtypes = [P, ctypes.POINTER(_Theta), i64, P, P, P, sz, P, P, P, P]
         for f in ("vif_nccl_unique_id", "vif_workspace_bytes", "vif_partition", "vif_create", "vif_set_data",
                   "vif_factor", "vif_nll", "vif_copy_U", "vif_launch_count", "vif_profile", "vif_stage_times",
                   "vif_grad_workspace_bytes", "vif_grad", "vif_predict_workspace_bytes", "vif_predict"):
@@ -237,12 +237,14 @@ def vif_predict_workspace_bytes(n: int, d: int, m: int, mv: int, npred: int, ran
 
 
 def vif_predict(h, theta: Theta, Xp: torch.Tensor, nbrp: Optional[torch.Tensor], workspace: torch.Tensor,
-                mu: torch.Tensor, Dp: Optional[torch.Tensor] = None, Bp: Optional[torch.Tensor] = None):
-    """Predictive means (Prop. 1) into mu (device, np); optional D_p and B_p = -A_p."""
+                mu: torch.Tensor, var: Optional[torch.Tensor] = None, Dp: Optional[torch.Tensor] = None,
+                Bp: Optional[torch.Tensor] = None):
+    """Predictive means / variances (Prop. 1, P:137-152; App. C.1) into mu, var (device, np);
+    optional D_p and B_p = -A_p."""
     th, keep = theta.to_c()
     st = load_library().vif_predict(h, ctypes.byref(th), int(Xp.shape[0]), _ptr(Xp), _ptr(nbrp),
-                                    ctypes.c_void_p(workspace.data_ptr()), workspace.numel(), _ptr(mu), _ptr(Dp),
-                                    _ptr(Bp))
+                                    ctypes.c_void_p(workspace.data_ptr()), workspace.numel(), _ptr(mu), _ptr(var),
+                                    _ptr(Dp), _ptr(Bp))
     _check(st, h)
 
 
@@ -325,9 +327,9 @@ class VifModel:
             self.grad_workspace = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
         return vif_grad(self.handle, theta, self.grad_workspace)
 
-    def predict(self, theta: Theta, Xp, nbrp, want_D: bool = False, want_B: bool = False):
+    def predict(self, theta: Theta, Xp, nbrp, want_var: bool = False, want_D: bool = False, want_B: bool = False):
         """Predictive means at Xp (np x d) with training-neighbour sets nbrp (np x m_v); returns mu (and
-        D_p, B_p = -A_p when asked) as device tensors."""
+        the predictive variances, D_p, B_p = -A_p when asked) as device tensors."""
         Xp = _as_input(Xp, torch.float64, self.device)
         nbrp = _as_input(nbrp, torch.int32, self.device) if self.mv > 0 else None
         npred = Xp.shape[0]
@@ -336,10 +338,11 @@ class VifModel:
         if ws is None or ws.numel() < nbytes:
             ws = self.pred_workspace = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
         mu = torch.empty(npred, dtype=torch.float64, device=self.device)
+        var = torch.empty(npred, dtype=torch.float64, device=self.device) if want_var else None
         Dp = torch.empty(npred, dtype=torch.float64, device=self.device) if want_D else None
         Bp = torch.empty((npred, self.mv), dtype=torch.float64, device=self.device) if want_B else None
-        vif_predict(self.handle, theta, Xp, nbrp, ws, mu, Dp, Bp)
-        out = (mu,) + ((Dp,) if want_D else ()) + ((Bp,) if want_B else ())
+        vif_predict(self.handle, theta, Xp, nbrp, ws, mu, var, Dp, Bp)
+        out = (mu,) + ((var,) if want_var else ()) + ((Dp,) if want_D else ()) + ((Bp,) if want_B else ())
         return out[0] if len(out) == 1 else out
 
     def U(self) -> torch.Tensor:

@@ -1,6 +1,6 @@
 """CUDA predictive means (vif_predict, through the C ABI) vs the oracle (Prop. 1; reading p1).
 
-Bar: mu to 1e-9 relative with an absolute floor 1e-10 max|y|; D_p relative 1e-9; B_p = -A_p per row
+Bar: mu to 1e-9 relative with an absolute floor 1e-10 max|y|; var and D_p relative 1e-9; B_p = -A_p per row
 max|dB| <= 1e-9 max(max|B_p|, 1e-3) (the training B bar)."""
 import numpy as np
 import pytest
@@ -34,10 +34,11 @@ def pred_parity(w, npred=300, x="uniform"):
     X, Z, nbr, y = (torch.from_numpy(np.ascontiguousarray(a)).to(dev) for a in (w.X, w.Z.reshape(-1, w.d), w.nbr, w.y))
     model = p.VifModel(X, Z, nbr, y, device=dev)
     Xp, nbrp = vifgen.make_prediction(w, npred, x=x, device="cuda")
-    mu, Dp, Bp = model.predict(p.Theta(**w.theta_dict()), Xp, nbrp, want_D=True, want_B=True)
-    mu, Dp, Bp = mu.cpu().numpy(), Dp.cpu().numpy(), Bp.cpu().numpy()
-    rmu, rD, rB = oracle.predict(w.X, w.Z, w.nbr, w.y, oracle.Theta(**w.theta_dict()), Xp, nbrp)
+    mu, var, Dp, Bp = model.predict(p.Theta(**w.theta_dict()), Xp, nbrp, want_var=True, want_D=True, want_B=True)
+    mu, var, Dp, Bp = mu.cpu().numpy(), var.cpu().numpy(), Dp.cpu().numpy(), Bp.cpu().numpy()
+    rmu, rvar, rD, rB = oracle.predict(w.X, w.Z, w.nbr, w.y, oracle.Theta(**w.theta_dict()), Xp, nbrp)
     np.testing.assert_allclose(mu, rmu, rtol=1e-9, atol=1e-10 * np.abs(w.y).max())
+    np.testing.assert_allclose(var, rvar, rtol=1e-9)
     np.testing.assert_allclose(Dp, rD, rtol=1e-9)
     if w.mv > 0:
         err = np.abs(Bp - rB).max(1) / np.maximum(np.abs(rB).max(1), 1e-3)
@@ -75,7 +76,7 @@ def test_pred_single_point_and_repeat():
     a = model.predict(th, Xp, nbrp).cpu().numpy()
     b = model.predict(th, Xp, nbrp).cpu().numpy()
     assert np.array_equal(a, b)
-    rmu, _, _ = oracle.predict(w.X, w.Z, w.nbr, w.y, oracle.Theta(**w.theta_dict()), Xp, nbrp)
+    rmu, _, _, _ = oracle.predict(w.X, w.Z, w.nbr, w.y, oracle.Theta(**w.theta_dict()), Xp, nbrp)
     np.testing.assert_allclose(a, rmu, rtol=1e-9, atol=1e-10)
     # the training NLL is unchanged by a prediction call
     t1 = model.evaluate(th)
