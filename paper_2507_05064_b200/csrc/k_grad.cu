@@ -9,11 +9,14 @@
 //   dU = dK(X,Z) L_m^{-T} - U Phi_low^T,  Phi_low = tril(L_m^{-1} dK_m L_m^{-T}), halved diagonal,
 //   dc_i from dA_i = C_NN^{-1} (dC_Ni - dC_NN A_i^T), dD_i = dC_ii - 2 A_i.dC_Ni + A_i dC_NN A_i^T,
 //   dC_S = dK_SS + [p = nugget] I - (dU_S U_S^T + U_S dU_S^T)           (Appendix A brackets).
-// Per parameter p:   dK_m -> Phi (two DMMA GEMMs) -> Phi_low;  dK(X,Z) (kx_deriv_kernel) -> dU (two
-// triangular DMMA GEMMs, gemm_tn);  one warp per point (vecchia_grad_kernel): Gram and the symmetric
-// cross-Gram dU_S U_S^T + U_S dU_S^T on DMMA, the dots g_i . U_aug[S_k] and g_i . dU_aug[S_k] in the
-// same pass over the gathered rows, then Cholesky, A_i, D_i, dA_i, dD_i and the point's contribution
+// Once: grad_state_kernel (one warp per point): Gram on DMMA and the dots g_i . U_aug[S_k] in one pass
+// over the gathered rows, C_S, register Cholesky, A_i, D_i -> a per-point state (L packed, A_i,
+// 1/L_jj, dots, D_i).  Per parameter p: dK_m -> Phi (two DMMA GEMMs) -> Phi_low;  dK(X,Z)
+// (kx_deriv_kernel) -> dU (two triangular DMMA GEMMs, gemm_tn);  grad_param_kernel: the cross product
+// X = dU_S U_S^T (all RB^2 tiles; dG = X + X^T) and the dots g_i . dU_aug[S_k] in one pass, dC_S, then
+// with the state dA_i, dD_i (two triangular solves) and the point's contribution
 // 1/2 dD_i/D_i + sum_k dc_ik (g_i.U_S_k) + c_ik (g_i.dU_S_k); block partials, fixed-order reduction.
+// The nugget's pass has dU = 0 and dC_S = I: no gathers.
 #include "common.cuh"
 #include "kernels.h"
 
@@ -143,30 +146,183 @@ constexpr int GW = 4;  // warps (points) per block
 
 template <int RB>
 __host__ __device__ constexpr int grad_warp_doubles(int d) {
-  return 2 * (RB * 8) * (RB * 8 + 1) + 3 * (RB * 8) + RB * 8 * d;  // C, dC, abuf, gam, gamd, xs
+  return 2 * (RB * 8) * (RB * 8 + 1) + 3 * (RB * 8) + RB * 8 * d;  // C, dC (or X), abuf, gam, gamd, xs
+}
+// per-point state of pass 0, by position: L (packed lower, SP rows incl. the identity padding), A_i,
+// 1/L_jj, g_i . U_aug[S_k], D_i, ok
+template <int RB>
+__host__ __device__ constexpr int state_doubles() {
+  return (RB * 8) * (RB * 8 + 1) / 2 + 3 * (RB * 8) + 2;
 }
 
+// per-warp setup shared by both passes: S, its (unscaled) coordinates, row pointers
+#define GRAD_WARP_SETUP                                                                          \
+  constexpr int SP = RB * 8;                                                                     \
+  constexpr int CS = SP + 1;                                                                     \
+  extern __shared__ __align__(16) double gsm_[];                                                 \
+  __shared__ int Sidx_all[GW][SP];                                                               \
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;                                    \
+  double* C = gsm_ + warp * grad_warp_doubles<RB>(p.d);                                          \
+  double* dC = C + SP * CS;                                                                      \
+  double* abuf = dC + SP * CS;                                                                   \
+  double* gam_s = abuf + SP;                                                                     \
+  double* gamd_s = gam_s + SP;                                                                   \
+  double* xs = gamd_s + SP;                                                                      \
+  int* Sidx = Sidx_all[warp];                                                                    \
+  const int64_t pos = (int64_t)blockIdx.x * GW + warp;
+
+// ---- pass 0 (once): Gram, g_i dots, C_S, Cholesky, A_i, D_i -> state[pos] ----
 template <int FAM, int RB>
-__global__ void __launch_bounds__(GW * 32, 3) vecchia_grad_kernel(
+__global__ void __launch_bounds__(GW * 32, 4) grad_state_kernel(
+    const double* __restrict__ U, const double* __restrict__ Gam, int64_t ldu, int mk, int ld,
+    const double* __restrict__ X, const int32_t* __restrict__ nbr, int mv, const int64_t* __restrict__ order,
+    int64_t npts, CovParams p, double* __restrict__ state) {
+  GRAD_WARP_SETUP
+  constexpr int NT = RB * (RB + 1) / 2;
+  constexpr int LP = SP * (SP + 1) / 2;
+  static_assert(SP <= 32, "gradient kernels need s <= 32");
+  if (pos >= npts) return;
+  const int64_t i = order[pos];
+  const int nb0 = lane < mv ? nbr[i * mv + lane] : -1;
+  const int q = __popc(__ballot_sync(0xffffffffu, nb0 >= 0));
+  const int s = q + 1;
+  const int myidx = lane < q ? nb0 : (lane == q ? (int)i : -1);
+  if (lane < SP) Sidx[lane] = myidx;
+  if (lane < s)
+    for (int k = 0; k < p.d; ++k) xs[lane * p.d + k] = X[(int64_t)myidx * p.d + k];
+  __syncwarp();
+  double acc[NT][2], gm[RB];
+#pragma unroll
+  for (int t = 0; t < NT; ++t) acc[t][0] = acc[t][1] = 0.0;
+#pragma unroll
+  for (int R = 0; R < RB; ++R) gm[R] = 0.0;
+  const double* rp[RB];
+#pragma unroll
+  for (int R = 0; R < RB; ++R) {
+    const int gi = Sidx[R * 8 + (lane >> 2)];
+    rp[R] = gi >= 0 ? U + (int64_t)gi * ldu + 2 * (lane & 3) : nullptr;
+  }
+  const double* grow = Gam + pos * (int64_t)ld + 2 * (lane & 3);
+  for (int k0 = 0; k0 < ld; k0 += 8) {
+    const double2 g2 = __ldg(reinterpret_cast<const double2*>(grow + k0));
+    double2 f[RB];
+#pragma unroll
+    for (int R = 0; R < RB; ++R)
+      f[R] = rp[R] ? __ldg(reinterpret_cast<const double2*>(rp[R] + k0)) : make_double2(0.0, 0.0);
+#pragma unroll
+    for (int R = 0; R < RB; ++R) gm[R] = fma(f[R].x, g2.x, fma(f[R].y, g2.y, gm[R]));
+    if (k0 < mk) {
+      int t = 0;
+#pragma unroll
+      for (int R1 = 0; R1 < RB; ++R1)
+#pragma unroll
+        for (int R2 = 0; R2 <= R1; ++R2, ++t) {
+          dmma884(acc[t][0], acc[t][1], f[R1].x, f[R2].x);
+          dmma884(acc[t][0], acc[t][1], f[R1].y, f[R2].y);
+        }
+    }
+  }
+#pragma unroll
+  for (int R = 0; R < RB; ++R) {
+    gm[R] += __shfl_xor_sync(0xffffffffu, gm[R], 1);
+    gm[R] += __shfl_xor_sync(0xffffffffu, gm[R], 2);
+    if ((lane & 3) == 0) gam_s[R * 8 + (lane >> 2)] = gm[R];
+  }
+  {
+    int t = 0;
+#pragma unroll
+    for (int R1 = 0; R1 < RB; ++R1)
+#pragma unroll
+      for (int R2 = 0; R2 <= R1; ++R2, ++t) {
+        const int r = R1 * 8 + (lane >> 2), c = R2 * 8 + 2 * (lane & 3);
+        C[r * CS + c] = acc[t][0];
+        C[r * CS + c + 1] = acc[t][1];
+      }
+  }
+  __syncwarp();
+  const int ne = s * (s + 1) / 2;
+  for (int e = lane; e < ne; e += 32) {
+    int r = (int)((sqrtf_fast(8.0f * (float)e + 1.0f) - 1.0f) * 0.5f);
+    if ((r + 1) * (r + 2) / 2 <= e) ++r;
+    if (r * (r + 1) / 2 > e) --r;
+    const int c = e - r * (r + 1) / 2;
+    double v = cov<FAM>(xs + r * p.d, xs + c * p.d, p) - C[r * CS + c];
+    if (r == c) v += p.nugget;
+    C[r * CS + c] = v;
+  }
+  __syncwarp();
+  double crow[SP];
+#pragma unroll
+  for (int c = 0; c < SP; ++c) {
+    double v = 0.0;
+    if (lane < s) {
+      if (c <= lane) v = C[lane * CS + c];
+    } else if (c == lane) {
+      v = 1.0;
+    }
+    crow[c] = v;
+  }
+  bool ok = true;
+  double Di = 0.0, myinv = 1.0;
+  double* colbuf = abuf;
+#pragma unroll
+  for (int j = 0; j < SP; ++j) {
+    const double djj = __shfl_sync(0xffffffffu, crow[j], j);
+    if (j < s) {
+      ok = ok && (djj > 0.0);
+      if (j == s - 1) Di = djj;
+    }
+    const double y = rsqrt_nr(djj);
+    const double lrj = crow[j] * y;
+    crow[j] = lrj;
+    if (lane == j) myinv = y;
+    if (j + 1 < SP) {
+      __syncwarp();
+      if (lane < SP) colbuf[lane] = lrj;
+      __syncwarp();
+#pragma unroll
+      for (int c = j + 1; c < SP; ++c) crow[c] = fma(-lrj, colbuf[c], crow[c]);
+    }
+  }
+  __syncwarp();
+#pragma unroll
+  for (int c = 0; c < SP; ++c)
+    if (lane < SP) C[lane * CS + c] = crow[c];
+  __syncwarp();
+  double a = lane < q ? C[q * CS + lane] : 0.0;
+  for (int j = q - 1; j >= 0; --j) {
+    const double xj = __shfl_sync(0xffffffffu, a * myinv, j);
+    if (lane == j) a = xj;
+    else if (lane < j) a = fma(-C[j * CS + lane], xj, a);
+  }
+  if (lane >= q) a = 0.0;
+  double* st = state + pos * (int64_t)state_doubles<RB>();
+  // L rows (packed lower), lane r writes row r
+  if (lane < SP) {
+    double* row = st + lane * (lane + 1) / 2;
+#pragma unroll
+    for (int c = 0; c < SP; ++c)
+      if (c <= lane) row[c] = crow[c];
+    st[LP + lane] = a;
+    st[LP + SP + lane] = myinv;
+    st[LP + 2 * SP + lane] = gam_s[lane];
+  }
+  if (lane == 0) {
+    st[LP + 3 * SP] = Di;
+    st[LP + 3 * SP + 1] = ok ? 1.0 : 0.0;
+  }
+}
+
+// ---- pass per parameter: cross-Gram X = dU_S U_S^T (all RB^2 tiles), g_i . dU_aug[S_k], dC_S,
+// dA_i, dD_i and the point's contribution, with L, A_i, D_i, g_i . U_aug[S_k] from the state ----
+template <int FAM, int RB>
+__global__ void __launch_bounds__(GW * 32, 4) grad_param_kernel(
     const double* __restrict__ U, const double* __restrict__ dU, const double* __restrict__ Gam, int64_t ldu, int mk,
     int ld, const double* __restrict__ X, const int32_t* __restrict__ nbr, int mv, const int64_t* __restrict__ order,
-    int64_t npts, CovParams p, int pidx, double* __restrict__ part) {
-  constexpr int SP = RB * 8;
-  constexpr int CS = SP + 1;
-  constexpr int NT = RB * (RB + 1) / 2;
-  static_assert(SP <= 32, "gradient kernel needs s <= 32");
-  extern __shared__ __align__(16) double gsm_[];
-  __shared__ int Sidx_all[GW][SP];
+    int64_t npts, CovParams p, int pidx, const double* __restrict__ state, double* __restrict__ part) {
+  GRAD_WARP_SETUP
+  constexpr int LP = SP * (SP + 1) / 2;
   __shared__ double wsum[GW];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  double* C = gsm_ + warp * grad_warp_doubles<RB>(p.d);
-  double* dC = C + SP * CS;
-  double* abuf = dC + SP * CS;
-  double* gam_s = abuf + SP;
-  double* gamd_s = gam_s + SP;
-  double* xs = gamd_s + SP;
-  int* Sidx = Sidx_all[warp];
-  const int64_t pos = (int64_t)blockIdx.x * GW + warp;
   double contrib = 0.0;
   if (pos < npts) {
     const int64_t i = order[pos];
@@ -177,159 +333,103 @@ __global__ void __launch_bounds__(GW * 32, 3) vecchia_grad_kernel(
     if (lane < SP) Sidx[lane] = myidx;
     if (lane < s)
       for (int k = 0; k < p.d; ++k) xs[lane * p.d + k] = X[(int64_t)myidx * p.d + k];
+    if (lane < SP) gamd_s[lane] = 0.0;
     __syncwarp();
-
-    // ---- Gram, symmetric cross-Gram and the g_i dots in one pass over the gathered rows ----
-    double acc[NT][2], dacc[NT][2], gm[RB], gmd[RB];
+    if (dU) {
+      double xacc[RB][RB][2], gmd[RB];
 #pragma unroll
-    for (int t = 0; t < NT; ++t) acc[t][0] = acc[t][1] = dacc[t][0] = dacc[t][1] = 0.0;
+      for (int R1 = 0; R1 < RB; ++R1) {
+        gmd[R1] = 0.0;
 #pragma unroll
-    for (int R = 0; R < RB; ++R) gm[R] = gmd[R] = 0.0;
-    const double* rp[RB];
-    const double* drp[RB];
-#pragma unroll
-    for (int R = 0; R < RB; ++R) {
-      const int gi = Sidx[R * 8 + (lane >> 2)];
-      rp[R] = gi >= 0 ? U + (int64_t)gi * ldu + 2 * (lane & 3) : nullptr;
-      drp[R] = (gi >= 0 && dU) ? dU + (int64_t)gi * ldu + 2 * (lane & 3) : nullptr;
-    }
-    const double* grow = Gam + pos * (int64_t)ld + 2 * (lane & 3);
-    for (int k0 = 0; k0 < ld; k0 += 8) {
-      const double2 g2 = __ldg(reinterpret_cast<const double2*>(grow + k0));
-      double2 f[RB], df[RB];
+        for (int R2 = 0; R2 < RB; ++R2) xacc[R1][R2][0] = xacc[R1][R2][1] = 0.0;
+      }
+      const double* rp[RB];
+      const double* drp[RB];
 #pragma unroll
       for (int R = 0; R < RB; ++R) {
-        f[R] = rp[R] ? __ldg(reinterpret_cast<const double2*>(rp[R] + k0)) : make_double2(0.0, 0.0);
-        df[R] = drp[R] ? __ldg(reinterpret_cast<const double2*>(drp[R] + k0)) : make_double2(0.0, 0.0);
+        const int gi = Sidx[R * 8 + (lane >> 2)];
+        rp[R] = gi >= 0 ? U + (int64_t)gi * ldu + 2 * (lane & 3) : nullptr;
+        drp[R] = gi >= 0 ? dU + (int64_t)gi * ldu + 2 * (lane & 3) : nullptr;
       }
+      const double* grow = Gam + pos * (int64_t)ld + 2 * (lane & 3);
+      for (int k0 = 0; k0 < ld; k0 += 8) {
+        const double2 g2 = __ldg(reinterpret_cast<const double2*>(grow + k0));
+        double2 f[RB], df[RB];
 #pragma unroll
-      for (int R = 0; R < RB; ++R) {
-        gm[R] = fma(f[R].x, g2.x, fma(f[R].y, g2.y, gm[R]));
-        gmd[R] = fma(df[R].x, g2.x, fma(df[R].y, g2.y, gmd[R]));
-      }
-      if (k0 < mk) {  // the Gram runs over the whitened columns only (not y, not the padding)
-        int t = 0;
+        for (int R = 0; R < RB; ++R) {
+          f[R] = rp[R] ? __ldg(reinterpret_cast<const double2*>(rp[R] + k0)) : make_double2(0.0, 0.0);
+          df[R] = drp[R] ? __ldg(reinterpret_cast<const double2*>(drp[R] + k0)) : make_double2(0.0, 0.0);
+        }
 #pragma unroll
-        for (int R1 = 0; R1 < RB; ++R1)
+        for (int R = 0; R < RB; ++R) gmd[R] = fma(df[R].x, g2.x, fma(df[R].y, g2.y, gmd[R]));
+        if (k0 < mk) {
 #pragma unroll
-          for (int R2 = 0; R2 <= R1; ++R2, ++t) {
-            dmma884(acc[t][0], acc[t][1], f[R1].x, f[R2].x);
-            dmma884(acc[t][0], acc[t][1], f[R1].y, f[R2].y);
-            if (dU) {
-              dmma884(dacc[t][0], dacc[t][1], df[R1].x, f[R2].x);
-              dmma884(dacc[t][0], dacc[t][1], df[R1].y, f[R2].y);
-              dmma884(dacc[t][0], dacc[t][1], f[R1].x, df[R2].x);
-              dmma884(dacc[t][0], dacc[t][1], f[R1].y, df[R2].y);
+          for (int R1 = 0; R1 < RB; ++R1)
+#pragma unroll
+            for (int R2 = 0; R2 < RB; ++R2) {
+              dmma884(xacc[R1][R2][0], xacc[R1][R2][1], df[R1].x, f[R2].x);
+              dmma884(xacc[R1][R2][0], xacc[R1][R2][1], df[R1].y, f[R2].y);
             }
-          }
+        }
       }
-    }
-    // dots: the 4 lanes of a row hold partial sums over their k-pairs
 #pragma unroll
-    for (int R = 0; R < RB; ++R) {
-      gm[R] += __shfl_xor_sync(0xffffffffu, gm[R], 1);
-      gm[R] += __shfl_xor_sync(0xffffffffu, gm[R], 2);
-      gmd[R] += __shfl_xor_sync(0xffffffffu, gmd[R], 1);
-      gmd[R] += __shfl_xor_sync(0xffffffffu, gmd[R], 2);
-      if ((lane & 3) == 0) {
-        gam_s[R * 8 + (lane >> 2)] = gm[R];
-        gamd_s[R * 8 + (lane >> 2)] = gmd[R];
+      for (int R = 0; R < RB; ++R) {
+        gmd[R] += __shfl_xor_sync(0xffffffffu, gmd[R], 1);
+        gmd[R] += __shfl_xor_sync(0xffffffffu, gmd[R], 2);
+        if ((lane & 3) == 0) gamd_s[R * 8 + (lane >> 2)] = gmd[R];
       }
-    }
-    {
-      int t = 0;
+      // X = dU_S U_S^T (full) into C (free until the state's L is loaded)
 #pragma unroll
       for (int R1 = 0; R1 < RB; ++R1)
 #pragma unroll
-        for (int R2 = 0; R2 <= R1; ++R2, ++t) {
+        for (int R2 = 0; R2 < RB; ++R2) {
           const int r = R1 * 8 + (lane >> 2), c = R2 * 8 + 2 * (lane & 3);
-          C[r * CS + c] = acc[t][0];
-          C[r * CS + c + 1] = acc[t][1];
-          dC[r * CS + c] = dacc[t][0];
-          dC[r * CS + c + 1] = dacc[t][1];
+          C[r * CS + c] = xacc[R1][R2][0];
+          C[r * CS + c + 1] = xacc[R1][R2][1];
         }
     }
     __syncwarp();
-    // ---- C_S = K + sigma^2 I - G,  dC_S = dK + [nugget] I - dG (lower triangle) ----
+    // dC_S (lower) = dK + [nugget] I - (X + X^T)
     const int ne = s * (s + 1) / 2;
     for (int e = lane; e < ne; e += 32) {
       int r = (int)((sqrtf_fast(8.0f * (float)e + 1.0f) - 1.0f) * 0.5f);
       if ((r + 1) * (r + 2) / 2 <= e) ++r;
       if (r * (r + 1) / 2 > e) --r;
       const int c = e - r * (r + 1) / 2;
-      const double* xa = xs + r * p.d;
-      const double* xb = xs + c * p.d;
-      double v = cov<FAM>(xa, xb, p) - C[r * CS + c];
-      double dv = (pidx <= p.d ? dcov<FAM>(xa, xb, pidx, p) : 0.0) - dC[r * CS + c];
-      if (r == c) {
-        v += p.nugget;
-        if (pidx == p.d + 1) dv += 1.0;
-      }
-      C[r * CS + c] = v;
-      dC[r * CS + c] = dv;
+      double v = pidx <= p.d ? dcov<FAM>(xs + r * p.d, xs + c * p.d, pidx, p) : 0.0;
+      if (dU) v -= C[r * CS + c] + C[c * CS + r];
+      if (r == c && pidx == p.d + 1) v += 1.0;
+      dC[r * CS + c] = v;
     }
     __syncwarp();
-
-    // ---- Cholesky of C_S (i last), row `lane` in registers; padded rows identity ----
-    double crow[SP];
-#pragma unroll
-    for (int c = 0; c < SP; ++c) {
-      double v = 0.0;
-      if (lane < s) {
-        if (c <= lane) v = C[lane * CS + c];
-      } else if (c == lane) {
-        v = 1.0;
-      }
-      crow[c] = v;
+    // state: L rows into C, A, 1/L_jj, gam, D, ok
+    const double* st = state + pos * (int64_t)state_doubles<RB>();
+    for (int e = lane; e < LP; e += 32) {
+      int r = (int)((sqrtf_fast(8.0f * (float)e + 1.0f) - 1.0f) * 0.5f);
+      if ((r + 1) * (r + 2) / 2 <= e) ++r;
+      if (r * (r + 1) / 2 > e) --r;
+      const int c = e - r * (r + 1) / 2;
+      C[r * CS + c] = st[e];
     }
-    bool ok = true;
-    double Di = 0.0, myinv = 1.0;
-    double* colbuf = abuf;  // [SP], reused: the broadcast column of step j (single buffer + syncs)
-#pragma unroll
-    for (int j = 0; j < SP; ++j) {
-      const double djj = __shfl_sync(0xffffffffu, crow[j], j);
-      if (j < s) {
-        ok = ok && (djj > 0.0);
-        if (j == s - 1) Di = djj;
-      }
-      const double y = rsqrt_nr(djj);
-      const double lrj = crow[j] * y;
-      crow[j] = lrj;
-      if (lane == j) myinv = y;
-      if (j + 1 < SP) {
-        __syncwarp();
-        if (lane < SP) colbuf[lane] = lrj;
-        __syncwarp();
-#pragma unroll
-        for (int c = j + 1; c < SP; ++c) crow[c] = fma(-lrj, colbuf[c], crow[c]);
-      }
-    }
-    __syncwarp();
-#pragma unroll
-    for (int c = 0; c < SP; ++c)
-      if (lane < SP) C[lane * CS + c] = crow[c];
-    __syncwarp();
-    // A_i^T = L_NN^{-T} l (lane k holds a_k)
-    double a = lane < q ? C[q * CS + lane] : 0.0;
-    for (int j = q - 1; j >= 0; --j) {
-      const double xj = __shfl_sync(0xffffffffu, a * myinv, j);
-      if (lane == j) a = xj;
-      else if (lane < j) a = fma(-C[j * CS + lane], xj, a);
-    }
-    if (lane >= q) a = 0.0;
+    const double a = lane < SP ? st[LP + lane] : 0.0;
+    const double myinv = lane < SP ? st[LP + SP + lane] : 1.0;
+    if (lane < SP) gam_s[lane] = st[LP + 2 * SP + lane];
+    const double Di = st[LP + 3 * SP];
+    const bool ok = st[LP + 3 * SP + 1] != 0.0;
     if (lane < SP) abuf[lane] = a;
     __syncwarp();
-    // u = dC_NN A^T, b = dC_Ni - u
+    double crow[SP];
+#pragma unroll
+    for (int c = 0; c < SP; ++c) crow[c] = (lane < SP && c <= lane) ? C[lane * CS + c] : 0.0;
+    // u = dC_NN A^T, b = dC_Ni - u, dD_i
     double u = 0.0;
     if (lane < q)
       for (int c = 0; c < q; ++c) u = fma(dC[c <= lane ? lane * CS + c : c * CS + lane], abuf[c], u);
     double bv = lane < q ? dC[q * CS + lane] - u : 0.0;
-    // dD_i = dC_ii - 2 A.dC_Ni + A.u
     double dterm = lane < q ? fma(-2.0 * a, dC[q * CS + lane], a * u) : 0.0;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) dterm += __shfl_xor_sync(0xffffffffu, dterm, o);
     const double dD = dC[q * CS + q] + dterm;
-    // dA^T = C_NN^{-1} b: forward L z = b (column of L in registers), back L^T x = z (rows in smem)
 #pragma unroll
     for (int j = 0; j < SP; ++j) {
       if (j < q) {
@@ -344,7 +444,6 @@ __global__ void __launch_bounds__(GW * 32, 3) vecchia_grad_kernel(
       else if (lane < j) bv = fma(-C[j * CS + lane], xj, bv);
     }
     const double da = lane < q ? bv : 0.0;
-    // c_i = [-A_i, 1]/sqrt(D_i), dc_i; contribution of the point
     const double rs = rsqrt_nr(Di);
     const double hD = 0.5 * dD / Di;
     const double ck = lane < q ? -a * rs : (lane == q ? rs : 0.0);
@@ -357,35 +456,52 @@ __global__ void __launch_bounds__(GW * 32, 3) vecchia_grad_kernel(
   if (lane == 0) wsum[warp] = contrib;
   __syncthreads();
   if (threadIdx.x == 0) {
-    double s = 0.0;
-    for (int w = 0; w < GW; ++w) s += wsum[w];
-    part[blockIdx.x] = s;
+    double sum = 0.0;
+    for (int w = 0; w < GW; ++w) sum += wsum[w];
+    part[blockIdx.x] = sum;
   }
 }
 
 template <int FAM, int RB>
-cudaError_t launch_grad_rb(const GradPointArgs& a, cudaStream_t s) {
+cudaError_t launch_grad_rb(const GradPointArgs& a, bool state_pass, cudaStream_t s) {
   const size_t smem = (size_t)GW * grad_warp_doubles<RB>(a.p.d) * sizeof(double);
-  static size_t attr = 0;
-  if (attr < smem) {
-    cudaError_t e = cudaFuncSetAttribute(vecchia_grad_kernel<FAM, RB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem);
-    if (e != cudaSuccess) return e;
-    attr = smem;
-  }
   const unsigned blocks = (unsigned)((a.npts + GW - 1) / GW);
-  vecchia_grad_kernel<FAM, RB><<<blocks, GW * 32, smem, s>>>(a.U, a.dU, a.Gam, a.ldu, a.mk, a.ld, a.X, a.nbr, a.mv,
-                                                             a.order, a.npts, a.p, a.pidx, a.part);
+  if (state_pass) {
+    if (smem > 48 * 1024) {
+      cudaError_t e = cudaFuncSetAttribute(grad_state_kernel<FAM, RB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)smem);
+      if (e != cudaSuccess) return e;
+    }
+    grad_state_kernel<FAM, RB><<<blocks, GW * 32, smem, s>>>(a.U, a.Gam, a.ldu, a.mk, a.ld, a.X, a.nbr, a.mv,
+                                                             a.order, a.npts, a.p, a.state);
+  } else {
+    if (smem > 48 * 1024) {
+      cudaError_t e = cudaFuncSetAttribute(grad_param_kernel<FAM, RB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)smem);
+      if (e != cudaSuccess) return e;
+    }
+    grad_param_kernel<FAM, RB><<<blocks, GW * 32, smem, s>>>(a.U, a.dU, a.Gam, a.ldu, a.mk, a.ld, a.X, a.nbr, a.mv,
+                                                             a.order, a.npts, a.p, a.pidx, a.state, a.part);
+  }
   return cudaGetLastError();
 }
 
 template <int FAM>
-cudaError_t launch_grad_fam(const GradPointArgs& a, cudaStream_t s) {
+cudaError_t launch_grad_fam(const GradPointArgs& a, bool state_pass, cudaStream_t s) {
   switch ((a.mv + 1 + 7) / 8) {
-    case 1: return launch_grad_rb<FAM, 1>(a, s);
-    case 2: return launch_grad_rb<FAM, 2>(a, s);
-    case 3: return launch_grad_rb<FAM, 3>(a, s);
-    default: return launch_grad_rb<FAM, 4>(a, s);
+    case 1: return launch_grad_rb<FAM, 1>(a, state_pass, s);
+    case 2: return launch_grad_rb<FAM, 2>(a, state_pass, s);
+    case 3: return launch_grad_rb<FAM, 3>(a, state_pass, s);
+    default: return launch_grad_rb<FAM, 4>(a, state_pass, s);
+  }
+}
+
+cudaError_t launch_grad_any(const GradPointArgs& a, bool state_pass, cudaStream_t s) {
+  switch (a.p.family) {
+    case FAM_M12: return launch_grad_fam<FAM_M12>(a, state_pass, s);
+    case FAM_M32: return launch_grad_fam<FAM_M32>(a, state_pass, s);
+    case FAM_M52: return launch_grad_fam<FAM_M52>(a, state_pass, s);
+    default: return launch_grad_fam<FAM_GAUSS>(a, state_pass, s);
   }
 }
 
@@ -393,16 +509,24 @@ cudaError_t launch_grad_fam(const GradPointArgs& a, cudaStream_t s) {
 
 int64_t grad_point_nparts(int64_t npts) { return (npts + GW - 1) / GW; }
 
+size_t grad_state_doubles(int mv) {
+  switch ((mv + 1 + 7) / 8) {
+    case 1: return state_doubles<1>();
+    case 2: return state_doubles<2>();
+    case 3: return state_doubles<3>();
+    default: return state_doubles<4>();
+  }
+}
+
+cudaError_t launch_grad_state(const GradPointArgs& a, cudaStream_t s) {
+  if (a.mv > 31) return cudaErrorNotSupported;
+  return a.npts > 0 ? launch_grad_any(a, true, s) : cudaSuccess;
+}
+
 cudaError_t launch_grad_points(const GradPointArgs& a, double* out, cudaStream_t s) {
   if (a.mv > 31) return cudaErrorNotSupported;
   if (a.npts > 0) {
-    cudaError_t e;
-    switch (a.p.family) {
-      case FAM_M12: e = launch_grad_fam<FAM_M12>(a, s); break;
-      case FAM_M32: e = launch_grad_fam<FAM_M32>(a, s); break;
-      case FAM_M52: e = launch_grad_fam<FAM_M52>(a, s); break;
-      default: e = launch_grad_fam<FAM_GAUSS>(a, s); break;
-    }
+    cudaError_t e = launch_grad_any(a, false, s);
     if (e != cudaSuccess) return e;
   }
   grad_reduce_kernel<<<1, 1024, 0, s>>>(a.part, grad_point_nparts(a.npts), out);

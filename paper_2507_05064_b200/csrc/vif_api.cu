@@ -300,7 +300,7 @@ int set_data(Handle* h, const double* X, const double* Z, const int32_t* nbr, co
 
 // ---------------------------------------------------------------- gradient workspace
 enum GBuf { G_Q2, G_GAM, G_DU, G_DKM, G_TT, G_PHI, G_PHILOW, G_LINVM, G_MCOPY, G_TSCR, G_ZH, G_Z, G_PART, G_OUT,
-            G_COUNT };
+            G_STATE, G_COUNT };
 
 Layout make_grad_layout(const Plan& P) {
   Layout L{};
@@ -315,6 +315,7 @@ Layout make_grad_layout(const Plan& P) {
   L.size[G_ZH] = L.size[G_Z] = (size_t)mk1 * D8;
   L.size[G_PART] = (size_t)grad_point_nparts(P.npos) * D8;
   L.size[G_OUT] = (size_t)(P.d + 2) * D8;
+  L.size[G_STATE] = (size_t)P.npos * grad_state_doubles(P.mv) * D8;
   size_t off = 0;
   for (int b = 0; b < G_COUNT; ++b) {
     L.off[b] = off;
@@ -724,6 +725,23 @@ int vif_grad(void* handle, const vif_theta* theta, void* gws, size_t gws_bytes, 
   const double* Linv = h->buf<double>(B_LINV);
   const double* U = h->buf<double>(B_U);
   double* S = W;  // W is dead once Gamma is formed: reuse it as the dK(X,Z) scratch
+  GradPointArgs a;
+  a.U = U;
+  a.dU = nullptr;
+  a.Gam = gbuf(G_GAM);
+  a.ldu = ld;
+  a.mk = mk;
+  a.ld = ld;
+  a.X = h->buf<double>(B_X);
+  a.nbr = h->buf<int32_t>(B_NBR);
+  a.mv = P.mv;
+  a.order = h->order[0];
+  a.npts = P.n_own[0];
+  a.p = p;
+  a.pidx = -1;
+  a.part = gbuf(G_PART);
+  a.state = gbuf(G_STATE);
+  VIF_CUDA(h, launch_grad_state(a, s), "gradient state");
   for (int pi = 0; pi < P.d + 2; ++pi) {
     const bool kernel_param = pi <= P.d;
     const double* dUp = nullptr;
@@ -737,21 +755,8 @@ int vif_grad(void* handle, const vif_theta* theta, void* gws, size_t gws_bytes, 
       VIF_CUDA(h, launch_gemm_tn(U, ld, P.n, gbuf(G_PHILOW), mk, mk, mk, 1, gbuf(G_DU), ld, -1.0, 1, s), "U Phi^T");
       dUp = gbuf(G_DU);
     }
-    GradPointArgs a;
-    a.U = U;
     a.dU = dUp;
-    a.Gam = gbuf(G_GAM);
-    a.ldu = ld;
-    a.mk = mk;
-    a.ld = ld;
-    a.X = h->buf<double>(B_X);
-    a.nbr = h->buf<int32_t>(B_NBR);
-    a.mv = P.mv;
-    a.order = h->order[0];
-    a.npts = P.n_own[0];
-    a.p = p;
     a.pidx = pi;
-    a.part = gbuf(G_PART);
     VIF_CUDA(h, launch_grad_points(a, gbuf(G_OUT) + pi, s), "gradient points");
   }
   VIF_CUDA(h, cudaMemcpyAsync(grad, gbuf(G_OUT), (size_t)(P.d + 2) * 8, cudaMemcpyDeviceToHost, s), "grad copy");
