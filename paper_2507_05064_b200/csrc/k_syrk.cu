@@ -176,4 +176,27 @@ cudaError_t launch_syrk(const double* W, int64_t ldw, int64_t nrows, int ncols, 
   return cudaGetLastError();
 }
 
+// per-round SYRK partials only (the reduction over all rounds' splits is launch_syrk_reduce)
+cudaError_t launch_syrk_part(const double* W, int64_t ldw, int64_t nrows, int ncols, int nsplit, double* Gpart,
+                             cudaStream_t s) {
+  const int nt = syrk_ntiles(ncols);
+  const int64_t rps = nrows > 0 ? (nrows + nsplit - 1) / nsplit : 0;
+  const size_t smem = (size_t)2 * SS * SK * SPAD * sizeof(double);
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(syrk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  syrk_kernel<<<nt * nsplit, 128, smem, s>>>(W, ldw, nrows, ncols, nt, rps, Gpart);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_syrk_reduce(const double* Gpart, int ntiles, int nsplit_total, int ncols, double* G, int ldg,
+                               cudaStream_t s) {
+  const int64_t tot = (int64_t)ntiles * ST * ST;
+  syrk_reduce_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(Gpart, ntiles, nsplit_total, ncols, G, ldg);
+  return cudaGetLastError();
+}
+
 }  // namespace vif

@@ -22,7 +22,7 @@ template <int FAM>
 __global__ void __launch_bounds__(256) kx_eval_kernel(const double* __restrict__ X, const double* __restrict__ Z,
                                                       const double* __restrict__ y, int64_t n, int64_t npos,
                                                       int64_t chunk, int world, int rank, int64_t pos0, int m,
-                                                      int mk, CovParams p, double* __restrict__ S,
+                                                      int mk, CovParams p, double* __restrict__ S, int lds,
                                                       double* __restrict__ Uaug, int ld) {
   // one warp per row; lanes stride over the columns.  Z and the 8 row coordinates are staged in
   // shared memory pre-scaled for cov_fast (broadcast reads; a runtime-indexed register array would
@@ -40,7 +40,7 @@ __global__ void __launch_bounds__(256) kx_eval_kernel(const double* __restrict__
   __syncthreads();
   if (pos >= npos) return;
   const double* x = kx_x[warp];
-  double* srow = S + pos * (int64_t)mk;
+  double* srow = S + pos * (int64_t)lds;
 #pragma unroll 4
   for (int b = lane; b < mk; b += 32) {
     double v = 0.0;
@@ -178,7 +178,8 @@ __global__ void __launch_bounds__(256, 2) gemm_tn_kernel(const double* __restric
 
 cudaError_t launch_u_features(const double* X, const double* Z, const double* y, int64_t n, int64_t pos0,
                               int64_t npos, int64_t chunk, int world, int rank, int m, int mk, const CovParams& p,
-                              const double* Linv, double* S, double* Uaug, int ld, cudaStream_t s) {
+                              const double* Linv, double* S, double* Uaug, int ld, cudaStream_t s, int lds) {
+  if (lds <= 0) lds = mk;
   if (npos == 0) return cudaSuccess;
   const int blocks = (int)((npos + 7) / 8);
   const size_t zbytes = (size_t)m * p.d * sizeof(double);
@@ -189,7 +190,8 @@ cudaError_t launch_u_features(const double* X, const double* Z, const double* y,
       if (e != cudaSuccess) return e;
       attr = zbytes;
     }
-    kern<<<blocks, 256, zbytes, s>>>(X, Z, y, n, npos, chunk, world, rank, pos0, m, mk, p, S + pos0 * mk, Uaug, ld);
+    kern<<<blocks, 256, zbytes, s>>>(X, Z, y, n, npos, chunk, world, rank, pos0, m, mk, p, S + pos0 * lds, lds,
+                                     Uaug, ld);
     return cudaSuccess;
   };
   cudaError_t e0 = cudaSuccess;
@@ -206,7 +208,7 @@ cudaError_t launch_u_features(const double* X, const double* Z, const double* y,
   // of k_gemm.cu (measured slower on B200, profiles/r01_notes.md)
   static const char* e128 = getenv("VIF_GEMM128");
   if (e128 && e128[0] == '1')
-    return launch_gemm_tn_tri(S + pos0 * mk, mk, npos, Linv, mk, mk, Uaug, ld, n, chunk, world, rank, pos0, s);
+    return launch_gemm_tn_tri(S + pos0 * lds, lds, npos, Linv, mk, mk, Uaug, ld, n, chunk, world, rank, pos0, s);
   const size_t smem = (size_t)GST * (GBM + GBN) * GPAD * sizeof(double);
   static bool attr_set = false;
   if (!attr_set) {
@@ -215,7 +217,7 @@ cudaError_t launch_u_features(const double* X, const double* Z, const double* y,
     attr_set = true;
   }
   const unsigned grid = (unsigned)(((npos + GBM - 1) / GBM) * ((mk + GBN - 1) / GBN));
-  gemm_tn_kernel<<<grid, 256, smem, s>>>(S + pos0 * mk, mk, npos, Linv, mk, mk, mk, 1, Uaug, ld, n, chunk, world, rank,
+  gemm_tn_kernel<<<grid, 256, smem, s>>>(S + pos0 * lds, lds, npos, Linv, mk, mk, mk, 1, Uaug, ld, n, chunk, world, rank,
                                          pos0, 1.0, 0);
   return cudaGetLastError();
 }

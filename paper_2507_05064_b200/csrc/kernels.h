@@ -41,7 +41,7 @@ cudaError_t launch_finish(const double* G, int ld, int m, int ycol, const double
 // K1
 cudaError_t launch_u_features(const double* X, const double* Z, const double* y, int64_t n, int64_t pos0,
                               int64_t npos, int64_t chunk, int world, int rank, int m, int mk, const CovParams& p,
-                              const double* Linv, double* S, double* Uaug, int ld, cudaStream_t s);
+                              const double* Linv, double* S, double* Uaug, int ld, cudaStream_t s, int lds = 0);
 // K2 + K3
 cudaError_t launch_vecchia(const VecchiaArgs& a, cudaStream_t s);
 // K4
@@ -50,6 +50,10 @@ int syrk_nsplit(int ncols, int64_t nrows, int num_sms);
 size_t syrk_part_doubles(int ncols, int nsplit);
 cudaError_t launch_syrk(const double* W, int64_t ldw, int64_t nrows, int ncols, int nsplit, double* Gpart,
                         double* G, int ldg, cudaStream_t s);
+cudaError_t launch_syrk_part(const double* W, int64_t ldw, int64_t nrows, int ncols, int nsplit, double* Gpart,
+                             cudaStream_t s);
+cudaError_t launch_syrk_reduce(const double* Gpart, int ntiles, int nsplit_total, int ncols, double* G, int ldg,
+                               cudaStream_t s);
 // K1b / K4 on the 128x128 engine (k_gemm.cu)
 cudaError_t launch_gemm_tn_tri(const double* S, int64_t lds, int64_t npos, const double* Linv, int ldl, int N,
                                double* U, int64_t ldu, int64_t n, int64_t chunk, int world, int rank,

@@ -30,6 +30,7 @@ namespace {
 
 constexpr int kPlanSMs = 148;  // SM count used for host-side workspace planning (B200)
 constexpr int kLogdParts = 256;
+constexpr int64_t kSingleRounds = 1;  // measured: 2 / 4 / 8 rounds are 2-7% slower (kernels barely co-run)
 
 thread_local std::string g_create_error;
 
@@ -77,7 +78,7 @@ struct Plan {
   bool emulate;
   int mk, ycol, ld;
   int64_t rounds, chunk, npos, npad;
-  int nsplit, nsplit_old;
+  int nsplit, nsplit_old, nsplit_round;
   std::vector<int64_t> n_own;
 };
 
@@ -108,8 +109,15 @@ bool make_plan(const vif_dims* dims, bool emulate, Plan& P, std::string& err) {
   P.ycol = P.mk;
   P.ld = (int)round_up(P.mk + 1, 8);
   if (P.world == 1) {
-    P.rounds = 1;
-    P.chunk = P.n;
+    // single GPU: R rounds on three streams (K1 of round r+1 and the SYRK of round r-1 run beside
+    // the vecchia rows of round r and fill the DMMA pipe while those warps are in their scalar
+    // phases); VIF_ROUNDS overrides, 1 = the plain serial schedule
+    static const char* env = getenv("VIF_ROUNDS");
+    int64_t R = env ? atoll(env) : kSingleRounds;
+    if (R < 1) R = 1;
+    if (P.n < R * 1024) R = 1;
+    P.rounds = R;
+    P.chunk = (P.n + R - 1) / R;
   } else {
     P.rounds = 8;
     P.chunk = (P.n + P.rounds * P.world - 1) / (P.rounds * P.world);
@@ -126,6 +134,7 @@ bool make_plan(const vif_dims* dims, bool emulate, Plan& P, std::string& err) {
     }
   P.nsplit = syrk_nt_nsplit(P.ld, P.npos, kPlanSMs);
   P.nsplit_old = syrk_nsplit(P.ld, P.npos, kPlanSMs);
+  P.nsplit_round = syrk_nsplit(P.ld, P.chunk, kPlanSMs);
   return true;
 }
 
@@ -147,7 +156,8 @@ Layout make_layout(const Plan& P) {
   L.size[B_ORDER] = (size_t)nrep * P.npos * sizeof(int64_t);
   L.size[B_KEYS] = L.size[B_KEYS2] = L.size[B_VALS] = L.size[B_VALS2] = (size_t)P.npos * 8;
   L.size[B_TEMP] = order_temp_bytes(P.npos);
-  L.size[B_GPART] = std::max(syrk_nt_part_doubles(P.ld, P.nsplit), syrk_part_doubles(P.ld, P.nsplit_old)) * D8;
+  L.size[B_GPART] = std::max(std::max(syrk_nt_part_doubles(P.ld, P.nsplit), syrk_part_doubles(P.ld, P.nsplit_old)),
+                             (size_t)P.rounds * syrk_part_doubles(P.ld, P.nsplit_round)) * D8;
   L.size[B_G] = nrep * gsz;
   L.size[B_GSUM] = gsz;
   L.size[B_LINVM] = (size_t)mk1 * mk1 * D8;
@@ -180,6 +190,10 @@ struct Handle {
   ncclComm_t comm = nullptr;
   cudaStream_t cstream = nullptr;            // communication stream (world > 1 with NCCL)
   std::vector<cudaEvent_t> ev_k1, ev_ag;     // per round: K1 done / all-gather done
+  // single-GPU rounds: K1 and SYRK streams, round events (vecchia done), K0 / SYRK done
+  cudaStream_t s_k1 = nullptr, s_sy = nullptr;
+  std::vector<cudaEvent_t> ev_v;
+  cudaEvent_t ev_k0 = nullptr, ev_sy = nullptr;
   bool have_data = false, factored = false, finished = false;
   vif_terms cached{};
   int cached_status = VIF_OK;
@@ -451,6 +465,23 @@ int vif_create(void** handle, const vif_dims* dims, void* workspace, size_t ws_b
       return fail(nullptr, VIF_ERR_CUDA, m);
     }
   }
+  if (h->P.world == 1 && h->P.rounds > 1) {
+    e = cudaStreamCreateWithFlags(&h->s_k1, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&h->s_sy, cudaStreamNonBlocking);
+    h->ev_k1.assign(h->P.rounds, nullptr);
+    h->ev_v.assign(h->P.rounds, nullptr);
+    for (int64_t k = 0; k < h->P.rounds && e == cudaSuccess; ++k) {
+      e = cudaEventCreateWithFlags(&h->ev_k1[k], cudaEventDisableTiming);
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h->ev_v[k], cudaEventDisableTiming);
+    }
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h->ev_k0, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h->ev_sy, cudaEventDisableTiming);
+    if (e != cudaSuccess) {
+      std::string m = std::string("round streams/events: ") + cudaGetErrorString(e);
+      vif_destroy(h);
+      return fail(nullptr, VIF_ERR_CUDA, m);
+    }
+  }
   if (X || Z || nbr || y) {
     int r = set_data(h, X, Z, nbr, y, 1);
     if (r != VIF_OK) {
@@ -503,6 +534,89 @@ int vif_factor(void* handle, const vif_theta* theta, double* B_out, double* D_ou
     nl += 2;
   }
   h->mark(S_KM, 1);
+  if (P.world == 1 && P.rounds > 1) {
+    // single GPU, R rounds on three streams:
+    //   s_k1: K1(0) K1(1) ... K1(R-1)                       (after K0)
+    //   s   : [K1(r)] vecchia(r) for r = 0..R-1              (round r conditions on rounds <= r)
+    //   s_sy: [vecchia(r)] SYRK partials of round r          (into their own slice of GPART)
+    //   s   : [all SYRK] fixed-order reduction of the R x nsplit partials, sum log D
+    // The K1 scratch of round r is the W rows of round r (row stride ld), so it never overlaps the W
+    // rows that earlier rounds' vecchia launches are writing.
+    const int nt = syrk_ntiles(P.ld);
+    const size_t part_round = syrk_part_doubles(P.ld, P.nsplit_round);
+    VIF_CUDA(h, cudaEventRecord(h->ev_k0, s), "event");
+    VIF_CUDA(h, cudaStreamWaitEvent(h->s_k1, h->ev_k0, 0), "event wait");
+    VIF_CUDA(h, cudaStreamWaitEvent(h->s_sy, h->ev_k0, 0), "event wait");
+    h->mark(S_UFEAT, 0);
+    for (int64_t r = 0; r < P.rounds; ++r) {
+      const int64_t cnt = std::min<int64_t>(P.chunk, P.n - r * P.chunk);
+      if (cnt > 0) {
+        VIF_CUDA(h, launch_u_features(h->buf<double>(B_X), h->buf<double>(B_Z), h->buf<double>(B_Y), P.n,
+                                      r * P.chunk, cnt, P.chunk, 1, 0, P.m, P.mk, p, h->buf<double>(B_LINV),
+                                      h->buf<double>(B_W), h->buf<double>(B_U), P.ld, h->s_k1, P.ld),
+                 "U features");
+        nl += P.mk > 0 ? 2 : 1;
+      }
+      VIF_CUDA(h, cudaEventRecord(h->ev_k1[r], h->s_k1), "event");
+    }
+    h->mark(S_UFEAT, 1);
+    h->mark(S_VECCHIA, 0);
+    double* G = h->buf<double>(B_G);
+    for (int64_t r = 0; r < P.rounds; ++r) {
+      const int64_t off = r * P.chunk;
+      const int64_t cnt = std::min<int64_t>(P.chunk, P.n - off);
+      VIF_CUDA(h, cudaStreamWaitEvent(s, h->ev_k1[r], 0), "event wait");
+      if (cnt > 0) {
+        VecchiaArgs a;
+        a.U = h->buf<double>(B_U);
+        a.ldu = P.ld;
+        a.mk = P.mk;
+        a.ld = P.ld;
+        a.X = h->buf<double>(B_X);
+        a.nbr = h->buf<int32_t>(B_NBR);
+        a.mv = P.mv;
+        a.order = h->order[0] + off;
+        a.npts = cnt;
+        a.p = p;
+        a.W = h->buf<double>(B_W) + (size_t)off * P.ld;
+        a.ldw = P.ld;
+        a.Dpos = h->buf<double>(B_DPOS) + off;
+        a.B_out = B_out;
+        a.D_out = D_out;
+        a.st = st;
+        VIF_CUDA(h, launch_vecchia(a, s), "vecchia");
+        ++nl;
+      }
+      VIF_CUDA(h, cudaEventRecord(h->ev_v[r], s), "event");
+      VIF_CUDA(h, cudaStreamWaitEvent(h->s_sy, h->ev_v[r], 0), "event wait");
+      if (cnt > 0) {
+        VIF_CUDA(h, launch_syrk_part(h->buf<double>(B_W) + (size_t)off * P.ld, P.ld, cnt, P.ld, P.nsplit_round,
+                                     h->buf<double>(B_GPART) + (size_t)r * part_round, h->s_sy),
+                 "syrk");
+        ++nl;
+      } else {
+        VIF_CUDA(h, cudaMemsetAsync(h->buf<double>(B_GPART) + (size_t)r * part_round, 0, part_round * 8, h->s_sy),
+                 "memset");
+      }
+    }
+    h->mark(S_VECCHIA, 1);
+    VIF_CUDA(h, cudaEventRecord(h->ev_sy, h->s_sy), "event");
+    VIF_CUDA(h, cudaStreamWaitEvent(s, h->ev_sy, 0), "event wait");
+    h->mark(S_SYRK, 0);
+    VIF_CUDA(h, launch_syrk_reduce(h->buf<double>(B_GPART), nt, (int)(P.rounds * P.nsplit_round), P.ld, G, P.ld, s),
+             "syrk reduce");
+    h->mark(S_SYRK, 1);
+    h->mark(S_REDUCE, 0);
+    VIF_CUDA(h, launch_logd_sum(h->buf<double>(B_DPOS), P.n, h->buf<double>(B_PART), kLogdParts,
+                                G + (size_t)P.ld * P.ld, s),
+             "logd");
+    h->mark(S_REDUCE, 1);
+    nl += 3;
+    h->factored = true;
+    h->finished = false;
+    h->launches = nl;
+    return VIF_OK;
+  }
   // A1-A6 in chunk-cyclic rounds.  Round r of a rank = positions [r*chunk, (r+1)*chunk);
   // vif_set_data groups the processing order by round (Morton order inside a round).  Per rank:
   //   compute stream: K1(round 0..R-1), then for each r: [wait AG(r)] vecchia rows of round r
@@ -917,6 +1031,12 @@ void vif_destroy(void* handle) {
   for (cudaEvent_t ev : h->ev_ag)
     if (ev) cudaEventDestroy(ev);
   if (h->cstream) cudaStreamDestroy(h->cstream);
+  for (cudaEvent_t ev : h->ev_v)
+    if (ev) cudaEventDestroy(ev);
+  if (h->ev_k0) cudaEventDestroy(h->ev_k0);
+  if (h->ev_sy) cudaEventDestroy(h->ev_sy);
+  if (h->s_k1) cudaStreamDestroy(h->s_k1);
+  if (h->s_sy) cudaStreamDestroy(h->s_sy);
   for (int k = 0; k < S_COUNT; ++k)
     for (int j = 0; j < 2; ++j)
       if (h->ev[k][j]) cudaEventDestroy(h->ev[k][j]);
