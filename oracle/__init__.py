@@ -60,6 +60,8 @@ def _load():
         _lib.oracle_num_threads.restype = ctypes.c_int
         _lib.oracle_grad.argtypes = [i64, i32, i32, P, P, P, P, P, P, P, P]
         _lib.oracle_dcov_matrix.argtypes = [P, P, i64, P, i64, P]
+        _lib.oracle_dc_neighbors.argtypes = [i64, i32, i32, P, P, P, P, P]
+        _lib.oracle_dc_scores.argtypes = [i64, i32, P, P, P, i64, P, P, P]
         _lib.oracle_predict.argtypes = [i64, i32, i32, P, P, P, P, P, i64, P, P, P, P, P, P, P]
     return _lib
 
@@ -248,6 +250,35 @@ def predict(X, Z, nbr, y, theta: Theta, Xp, nbrp):
     if st != 0:
         raise OracleError(st, bad.value)
     return mu, var, Dp, Bp
+
+
+def dc_neighbors(X, Z, theta: Theta, mv: int):
+    """Oracle correlation-distance neighbour sets (readings c5-c7): (nbr n x mv, scores)."""
+    lib = _load()
+    X, Z = _f64(X), _f64(Z).reshape(-1, X.shape[1])
+    n, m = X.shape[0], Z.shape[0]
+    nbr = np.empty((n, mv), dtype=np.int32)
+    sc = np.empty((n, mv))
+    th, keep = theta._c()
+    st = lib.oracle_dc_neighbors(n, m, mv, _p(X), _p(Z), ctypes.byref(th), _p(nbr), _p(sc))
+    if st != 0:
+        raise OracleError(st, -1)
+    return nbr, sc
+
+
+def dc_scores(X, Z, theta: Theta, qi, cj):
+    """Scores (|corr|, 0 for degenerate candidates, -dist^2 for degenerate queries) of (qi, cj) pairs."""
+    lib = _load()
+    X, Z = _f64(X), _f64(Z).reshape(-1, X.shape[1])
+    qi = np.ascontiguousarray(qi, dtype=np.int64)
+    cj = np.ascontiguousarray(cj, dtype=np.int64)
+    out = np.empty(qi.shape[0])
+    th, keep = theta._c()
+    st = lib.oracle_dc_scores(X.shape[0], Z.shape[0], _p(X), _p(Z), ctypes.byref(th), qi.shape[0], _p(qi), _p(cj),
+                              _p(out))
+    if st != 0:
+        raise OracleError(st, -1)
+    return out
 
 
 def num_threads() -> int:

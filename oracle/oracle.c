@@ -906,3 +906,128 @@ done:
   free(A); free(W); free(info); free(M); free(Lm); free(U);
   return status;
 }
+
+/* =====================================================================================
+ * Correlation-distance neighbour sets, exact brute force.
+ *   rho_c(i,j) = k(x_i,x_j) - u_i.u_j   (residual process without the nugget)
+ *   d_c(i,j) = sqrt(1 - |rho_c(i,j)| / sqrt(rho_c(i,i) rho_c(j,j)))
+ * N(i) = the m_v predecessors j < i with the smallest d_c, ranked by (d_c, index) (reading c6);
+ * i <= m_v: all predecessors (reading c5).  Reading c7: a candidate whose residual variance
+ * rho_c(j,j) < 1e-7 sigma_1^2 gets d_c = 1; a query with such a variance ranks its predecessors by the
+ * length-scale-scaled Euclidean distance.  The paper's cover tree (Alg. 3-4) returns the same sets.
+ * Scores compared: |corr| descending (= d_c ascending), or -dist^2 for degenerate queries.
+ * ===================================================================================== */
+int oracle_dc_neighbors(int64_t n, int m, int mv, const double *X, const double *Z, const or_theta *th,
+                        int32_t *nbr_out, double *score_out) {
+  const int d = th->d;
+  double *Lm = NULL, *U = NULL, *rd = NULL;
+  int status = OR_OK;
+  rd = (double *)malloc(sizeof(double) * (size_t)n);
+  if (!rd) return OR_NOMEM;
+  if (m > 0) {
+    Lm = (double *)malloc(sizeof(double) * (size_t)m * m);
+    U = (double *)malloc(sizeof(double) * (size_t)n * m);
+    if (!Lm || !U) { status = OR_NOMEM; goto done; }
+    if (or_build_Lm(th, Z, m, Lm) != OR_OK) { status = OR_NOT_PD; goto done; }
+#pragma omp parallel for schedule(static)
+    for (int64_t i = 0; i < n; ++i) or_u_row(th, Z, m, Lm, X + i * d, U + i * (size_t)m);
+  }
+  for (int64_t i = 0; i < n; ++i) {
+    double v = th->sigma2;
+    for (int k = 0; k < m; ++k) v -= U[i * (size_t)m + k] * U[i * (size_t)m + k];
+    rd[i] = v;
+  }
+  {
+    const double tau = 1e-7 * th->sigma2;
+#pragma omp parallel
+    {
+      double *bv = (double *)malloc(sizeof(double) * (mv > 0 ? mv : 1));
+      int32_t *bi = (int32_t *)malloc(sizeof(int32_t) * (mv > 0 ? mv : 1));
+#pragma omp for schedule(dynamic, 64)
+      for (int64_t i = 0; i < n; ++i) {
+        int cnt = 0;
+        const int qdeg = rd[i] < tau;
+        for (int64_t j = 0; j < i; ++j) {
+          double sc;
+          if (qdeg) {
+            double d2 = 0.0;
+            for (int k = 0; k < d; ++k) {
+              double t = (X[i * d + k] - X[j * d + k]) / th->lengthscale[k];
+              d2 += t * t;
+            }
+            sc = -d2;
+          } else if (rd[j] < tau) {
+            sc = 0.0; /* d_c = 1 */
+          } else {
+            double c = or_cov(th, X + i * d, X + j * d);
+            for (int k = 0; k < m; ++k) c -= U[i * (size_t)m + k] * U[j * (size_t)m + k];
+            sc = fabs(c) / sqrt(rd[i] * rd[j]);
+          }
+          /* insert (sc desc, j asc); j increases, so equal scores keep earlier indices first */
+          if (cnt < mv || sc > bv[cnt - 1]) {
+            int pos = cnt < mv ? cnt : mv - 1;
+            while (pos > 0 && sc > bv[pos - 1]) {
+              bv[pos] = bv[pos - 1];
+              bi[pos] = bi[pos - 1];
+              --pos;
+            }
+            bv[pos] = sc;
+            bi[pos] = (int32_t)j;
+            if (cnt < mv) ++cnt;
+          }
+        }
+        for (int k = 0; k < mv; ++k) {
+          nbr_out[i * mv + k] = k < cnt ? bi[k] : -1;
+          if (score_out) score_out[i * mv + k] = k < cnt ? bv[k] : -INFINITY;
+        }
+      }
+      free(bv);
+      free(bi);
+    }
+  }
+done:
+  free(Lm); free(U); free(rd);
+  return status;
+}
+
+/* score of given (i, j) pairs under the same rules (for validity checks of other implementations) */
+int oracle_dc_scores(int64_t n, int m, const double *X, const double *Z, const or_theta *th, int64_t npairs,
+                     const int64_t *qi, const int64_t *cj, double *score) {
+  const int d = th->d;
+  double *Lm = NULL;
+  if (m > 0) {
+    Lm = (double *)malloc(sizeof(double) * (size_t)m * m);
+    if (or_build_Lm(th, Z, m, Lm) != OR_OK) { free(Lm); return OR_NOT_PD; }
+  }
+  const double tau = 1e-7 * th->sigma2;
+#pragma omp parallel
+  {
+    double *ui = (double *)malloc(sizeof(double) * (m > 0 ? m : 1));
+    double *uj = (double *)malloc(sizeof(double) * (m > 0 ? m : 1));
+#pragma omp for schedule(static)
+    for (int64_t t = 0; t < npairs; ++t) {
+      const int64_t i = qi[t], j = cj[t];
+      if (m > 0) {
+        or_u_row(th, Z, m, Lm, X + i * d, ui);
+        or_u_row(th, Z, m, Lm, X + j * d, uj);
+      }
+      double ri = th->sigma2, rj = th->sigma2, c = or_cov(th, X + i * d, X + j * d);
+      for (int k = 0; k < m; ++k) { ri -= ui[k] * ui[k]; rj -= uj[k] * uj[k]; c -= ui[k] * uj[k]; }
+      if (ri < tau) {
+        double d2 = 0.0;
+        for (int k = 0; k < d; ++k) {
+          double q = (X[i * d + k] - X[j * d + k]) / th->lengthscale[k];
+          d2 += q * q;
+        }
+        score[t] = -d2;
+      } else if (rj < tau) {
+        score[t] = 0.0;
+      } else {
+        score[t] = fabs(c) / sqrt(ri * rj);
+      }
+    }
+    free(ui); free(uj);
+  }
+  free(Lm);
+  return OR_OK;
+}
