@@ -163,6 +163,17 @@ int vif_predict_workspace_bytes(const vif_dims* dims, int64_t np, size_t* bytes)
 int vif_predict(void* handle, const vif_theta* theta, int64_t np, const double* Xp, const int32_t* nbrp,
                 void* workspace, size_t ws_bytes, double* mu, double* var, double* Dp, double* Bp);
 
+/* Correlation-distance neighbour sets (the paper's cover tree, Alg. 3-4, returns the same
+ * sets): for every point i of the handle's X (Vecchia order) the mv predecessors j < i with the
+ * smallest d_c(i,j) = sqrt(1 - |rho_c(i,j)| / sqrt(rho_c(i,i) rho_c(j,j))), rho_c = k - u_i.u_j at theta
+ * (no nugget), ranked by (d_c, index); i <= mv: all predecessors; readings c5-c7 (a point
+ * whose residual variance is below 1e-7 sigma_1^2 scores d_c = 1 as a candidate and ranks its own
+ * predecessors by length-scale-scaled Euclidean distance).  Exact brute force (n^2 m / 2 FMA on the
+ * FP64 tensor cores).  nbr_out: device, n x mv int32, -1 padded; mv in [1, VIF_MAX_MV] (independent of
+ * dims.mv).  Uses the handle's workspace (invalidates a previous vif_factor: call vif_factor again).
+ * Single rank.  Errors: INVALID_ARG, NOT_PD (K(Z,Z) + jitter), CUDA. */
+int vif_neighbors(void* handle, const vif_theta* theta, int32_t mv, int32_t* nbr_out);
+
 /* Debug / parity: copy the whitened features U (n x m, row-major) to `out` (device or host). */
 int vif_copy_U(void* handle, double* out);
 

@@ -98,6 +98,10 @@ cudaError_t launch_zvec(const double* LinvM, int ldi, const double* G, int ldg, 
 cudaError_t launch_pred_mean(const double* Wp, int ld, int m, int ycol, const double* z, const double* Dpos,
                              const int64_t* order, int64_t np, double* mu, const double* T, int ldt, double* var,
                              cudaStream_t s);
+// correlation-distance neighbours (k_knn.cu)
+size_t knn_smem_bytes(int mv);
+cudaError_t launch_knn(const double* U, int64_t ldu, int m, int mk, const double* X, int64_t n, const CovParams& p,
+                       double* isd, int* deg, int mv, int32_t* out, cudaStream_t s);
 // misc
 cudaError_t launch_validate(const double* X, int64_t n, int d, const double* Z, int m, const double* y,
                             const int32_t* nbr, int mv, DevStatus* st, cudaStream_t s);

@@ -978,6 +978,42 @@ int vif_predict(void* handle, const vif_theta* theta, int64_t np, const double* 
   return VIF_OK;
 }
 
+int vif_neighbors(void* handle, const vif_theta* theta, int32_t mv, int32_t* nbr_out) {
+  Handle* h = reinterpret_cast<Handle*>(handle);
+  if (!h) return fail(nullptr, VIF_ERR_INVALID_ARG, "handle is NULL");
+  const Plan& P = h->P;
+  if (!nbr_out || mv < 1 || mv > VIF_MAX_MV) return fail(h, VIF_ERR_INVALID_ARG, "vif_neighbors: bad arguments");
+  if (P.world != 1) return fail(h, VIF_ERR_INVALID_ARG, "vif_neighbors: single-rank handles only");
+  if (!h->have_data) return fail(h, VIF_ERR_STATE, "no data");
+  CovParams p;
+  std::string err;
+  if (!make_params(h, theta, p, err)) return fail(h, VIF_ERR_INVALID_ARG, err);
+  cudaStream_t s = h->stream;
+  DevStatus* st = h->buf<DevStatus>(B_STATUS);
+  h->factored = h->finished = false;
+  VIF_CUDA(h, launch_reset_status(st, s), "reset status");
+  // u_i for all points (K0 + K1 of the factor, single round)
+  if (P.m > 0) {
+    VIF_CUDA(h, launch_build_km(h->buf<double>(B_Z), P.m, p, h->buf<double>(B_KM), s), "build K_m");
+    VIF_CUDA(h, cudaMemsetAsync(h->buf<double>(B_LINV), 0, h->L.size[B_LINV], s), "memset Linv");
+    VIF_CUDA(h, launch_chol_inv(h->buf<double>(B_KM), P.m, P.m, 0.0, h->buf<double>(B_LINV), P.mk, P.mk, 1,
+                                h->buf<double>(B_TSCR), &st->km_fail, h->num_sms, s),
+             "chol K_m");
+    VIF_CUDA(h, launch_u_features(h->buf<double>(B_X), h->buf<double>(B_Z), h->buf<double>(B_Y), P.n, 0, P.n, P.n, 1, 0,
+                                  P.m, P.mk, p, h->buf<double>(B_LINV), h->buf<double>(B_W), h->buf<double>(B_U),
+                                  P.ld, s),
+             "U features");
+  }
+  VIF_CUDA(h, launch_knn(h->buf<double>(B_U), P.ld, P.m, P.mk, h->buf<double>(B_X), P.n, p, h->buf<double>(B_DPOS),
+                         reinterpret_cast<int*>(h->buf<uint64_t>(B_KEYS)), mv, nbr_out, s),
+           "neighbour search");
+  DevStatus hs;
+  VIF_CUDA(h, cudaMemcpyAsync(&hs, st, sizeof(hs), cudaMemcpyDeviceToHost, s), "status copy");
+  VIF_CUDA(h, cudaStreamSynchronize(s), "sync");
+  if (hs.km_fail) return fail(h, VIF_ERR_NOT_PD, "Cholesky of K(Z,Z) + jitter failed");
+  return VIF_OK;
+}
+
 int vif_copy_U(void* handle, double* out) {
   Handle* h = reinterpret_cast<Handle*>(handle);
   if (!h || !out) return fail(h, VIF_ERR_INVALID_ARG, "NULL argument");

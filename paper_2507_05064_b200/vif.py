@@ -81,9 +81,11 @@ def load_library():
         lib.vif_grad.argtypes = [P, ctypes.POINTER(_Theta), P, sz, P, ctypes.POINTER(_Terms)]
         lib.vif_predict_workspace_bytes.argtypes = [ctypes.POINTER(_Dims), i64, ctypes.POINTER(sz)]
         lib.vif_predict.argtypes = [P, ctypes.POINTER(_Theta), i64, P, P, P, sz, P, P, P, P]
+        lib.vif_neighbors.argtypes = [P, ctypes.POINTER(_Theta), i32, P]
         for f in ("vif_nccl_unique_id", "vif_workspace_bytes", "vif_partition", "vif_create", "vif_set_data",
                   "vif_factor", "vif_nll", "vif_copy_U", "vif_launch_count", "vif_profile", "vif_stage_times",
-                  "vif_grad_workspace_bytes", "vif_grad", "vif_predict_workspace_bytes", "vif_predict"):
+                  "vif_grad_workspace_bytes", "vif_grad", "vif_predict_workspace_bytes", "vif_predict",
+                  "vif_neighbors"):
             getattr(lib, f).restype = ctypes.c_int
         _lib = lib
     return _lib
@@ -92,7 +94,7 @@ def load_library():
 EXPORTED = ("vif_nccl_unique_id", "vif_workspace_bytes", "vif_partition", "vif_create", "vif_set_data",
             "vif_factor", "vif_nll", "vif_copy_U", "vif_launch_count", "vif_profile", "vif_stage_times",
             "vif_stage_name", "vif_last_error", "vif_destroy", "vif_grad_workspace_bytes", "vif_grad",
-            "vif_predict_workspace_bytes", "vif_predict")
+            "vif_predict_workspace_bytes", "vif_predict", "vif_neighbors")
 NUM_STAGES = 8
 
 
@@ -248,6 +250,12 @@ def vif_predict(h, theta: Theta, Xp: torch.Tensor, nbrp: Optional[torch.Tensor],
     _check(st, h)
 
 
+def vif_neighbors(h, theta: Theta, mv: int, out: torch.Tensor):
+    """Correlation-distance neighbour sets into out (device, n x mv int32)."""
+    th, keep = theta.to_c()
+    _check(load_library().vif_neighbors(h, ctypes.byref(th), int(mv), _ptr(out)), h)
+
+
 def vif_copy_U(h, out: torch.Tensor):
     _check(load_library().vif_copy_U(h, _ptr(out)), h)
 
@@ -344,6 +352,12 @@ class VifModel:
         vif_predict(self.handle, theta, Xp, nbrp, ws, mu, var, Dp, Bp)
         out = (mu,) + ((var,) if want_var else ()) + ((Dp,) if want_D else ()) + ((Bp,) if want_B else ())
         return out[0] if len(out) == 1 else out
+
+    def neighbors(self, theta: Theta, mv: int) -> torch.Tensor:
+        """N(i) under d_c at theta for the handle's X (Vecchia order): device n x mv int32, -1 padded."""
+        out = torch.empty((self.n, mv), dtype=torch.int32, device=self.device)
+        vif_neighbors(self.handle, theta, mv, out)
+        return out
 
     def U(self) -> torch.Tensor:
         out = torch.empty((self.n, self.m), dtype=torch.float64, device=self.device)
