@@ -46,6 +46,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-grad", action="store_true", help="skip the NLL-gradient timing (vif_grad)")
     ap.add_argument("--npred", type=int, default=100000, help="prediction points for the vif_predict timing (0: skip)")
+    ap.add_argument("--no-knn", action="store_true", help="skip the vif_neighbors timing")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target CPU seconds of the oracle sample")
     return ap.parse_args()
 
@@ -324,6 +325,24 @@ def main():
                         f"prediction inputs and their d_c neighbours generated in {pgen:.1f} s (not timed)",
                 "mu_mean": float(mu.mean().item()), "var_mean": float(var.mean().item())}
 
+    # ---------------- correlation-distance neighbour search (vif_neighbors, single GPU) ----------------
+    knn = None
+    if world == 1 and not args.no_knn:
+        torch.cuda.synchronize(dev)
+        k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        k0.record(stream)
+        g = model.neighbors(th[0], w.mv)
+        k1.record(stream)
+        torch.cuda.synchronize(dev)
+        ks = k0.elapsed_time(k1) * 1e-3
+        same = float((g.cpu().numpy() == w.nbr).all(1).mean())
+        knn = {"s": ks, "rows_equal_to_generator": same, "generator_s": w.timings.get("neighbors"),
+               "tflops": w.n * (w.n - 1) / 2 * w.m * 2 / ks / 1e12,
+               "note": "vif_neighbors: exact d_c neighbour sets (P:499-513) by brute force on DMMA (n^2 m / 2 FMA); "
+                       "generator_s = the torch brute force of the input generator (vifgen) on the same GPU"}
+        model.factor(th[0])  # vif_neighbors invalidates the factor; leave the handle evaluated
+        model.nll()
+
     if rank == 0:
         fl = workload_flops(w.nbr, w.m)
         # per-rank share of the row-sharded kernels (strong scaling: each rank does ~1/world of the rows)
@@ -386,6 +405,7 @@ def main():
             "nll": last.nll,
             "grad": grad,
             "predict": pred,
+            "neighbors": knn,
             "input_generation_s": {"total": gen_s, **{k: round(v, 3) for k, v in w.timings.items()}},
             "create_s": create_s,
         }
