@@ -17,7 +17,7 @@ namespace vif {
 
 namespace {
 
-constexpr int KQ = 64, KBK = 16, KST = 3, KPAD = KBK + 8, KMAXMV = 47;
+constexpr int KQ = 64, KBK = 16, KST = 2, KPAD = KBK + 8, KMAXMV = 47;  // rows padded to 24 doubles (64 mod 128 B)
 
 // residual variance rd_i = sigma_1^2 - |u_i|^2, its 1/sqrt and degeneracy (c7)
 __global__ void resvar_kernel(const double* __restrict__ U, int ldu, int m, int64_t n, double sigma2,
@@ -41,15 +41,15 @@ __global__ void resvar_kernel(const double* __restrict__ U, int ldu, int m, int6
 }
 
 template <int FAM>
-__global__ void __launch_bounds__(256, 1) knn_kernel(const double* __restrict__ U, int64_t ldu, int mk,
+__global__ void __launch_bounds__(256, 2) knn_kernel(const double* __restrict__ U, int64_t ldu, int mk,
                                                     const double* __restrict__ X, int64_t n, CovParams p,
                                                     const double* __restrict__ isd, const int* __restrict__ deg,
                                                     int mv, int32_t* __restrict__ out) {
   extern __shared__ __align__(16) double ksm[];
   double* As = ksm;                              // [KST][KQ][KPAD]
   double* Bs = As + KST * KQ * KPAD;             // [KST][KQ][KPAD]
-  double* Sc = Bs + KST * KQ * KPAD;             // [KQ][KQ + 1] scores
-  double* lv = Sc + KQ * (KQ + 1);               // [KQ][mv] list scores
+  double* Sc = As;                               // [KQ][KQ + 1] scores, aliased on the idle A/B stages
+  double* lv = Bs + KST * KQ * KPAD;             // [KQ][mv] list scores
   int* li = reinterpret_cast<int*>(lv + KQ * mv);  // [KQ][mv] list indices
   __shared__ double xq[KQ][VIF_MAX_D], xc[KQ][VIF_MAX_D];
   __shared__ double isq[KQ], isc[KQ];
@@ -190,9 +190,10 @@ __global__ void __launch_bounds__(256, 1) knn_kernel(const double* __restrict__ 
 
 }  // namespace
 
+static_assert(2 * KST * KQ * KPAD >= KQ * (KQ + 1), "score tile must fit in the staging buffers");
+
 size_t knn_smem_bytes(int mv) {
-  return sizeof(double) * ((size_t)2 * KST * KQ * KPAD + (size_t)KQ * (KQ + 1) + (size_t)KQ * mv) +
-         sizeof(int) * (size_t)KQ * mv;
+  return sizeof(double) * ((size_t)2 * KST * KQ * KPAD + (size_t)KQ * mv) + sizeof(int) * (size_t)KQ * mv;
 }
 
 cudaError_t launch_knn(const double* U, int64_t ldu, int m, int mk, const double* X, int64_t n, const CovParams& p,
