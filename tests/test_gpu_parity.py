@@ -227,3 +227,34 @@ def test_config3_full_nll_and_sampled_rows():
     assert t.logdet_M >= 0 and t.quad >= 0
     r = oracle_run(w)
     check_terms(t, r.nll, r.logdet_D, r.logdet_M, r.quad)
+
+
+def test_rounds_schedule_same_result():
+    """The optional single-GPU round schedule (VIF_ROUNDS, three streams) gives the serial result:
+    B and D bit-identical, NLL to 1e-12 (only the SYRK summation order differs).  The knob is read
+    once per process, hence the subprocess."""
+    import json
+    import os
+    import subprocess
+    import sys
+    code = r'''
+import json, sys, numpy as np, torch
+sys.path.insert(0, %r)
+import __graft_entry__; __graft_entry__.build()
+import paper_2507_05064_b200 as p, vifgen
+w = vifgen.make_workload(n=9000, d=2, m=40, mv=12, seed=77, device="cuda")
+dev = torch.device("cuda")
+m = p.VifModel(*(torch.from_numpy(np.ascontiguousarray(a)).to(dev) for a in (w.X, w.Z, w.nbr, w.y)))
+B = torch.zeros((w.n, w.mv), dtype=torch.float64, device=dev); D = torch.zeros(w.n, dtype=torch.float64, device=dev)
+t = m.evaluate(p.Theta(**w.theta_dict()), B, D)
+np.save(sys.argv[1], np.concatenate([B.cpu().numpy().ravel(), D.cpu().numpy(), [t.nll]]))
+''' % os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for R in ("1", "4"):
+        path = f"/tmp/vif_rounds_{R}.npy"
+        env = dict(os.environ, VIF_ROUNDS=R)
+        subprocess.run([sys.executable, "-c", code, path], env=env, check=True)
+        outs.append(np.load(path))
+    a, b = outs
+    assert np.array_equal(a[:-1], b[:-1])
+    assert b[-1] == pytest.approx(a[-1], rel=1e-12)
