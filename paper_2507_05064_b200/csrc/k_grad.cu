@@ -52,6 +52,32 @@ __device__ __forceinline__ double dcov(const double* __restrict__ a, const doubl
   return p.sigma2 * h * dj * dj * il * il * il;
 }
 
+// dk/dtheta_p from pre-scaled coordinates (a~ = fam_scale a / lambda) and the exp table (cov_fast):
+// with Delta~_j = a~_j - b~_j and E = sigma_1^2 e^{-t}:  dk/dsigma_1^2 = k / sigma_1^2;
+// dk/dlambda_j = E Delta~_j^2 / lambda_j x {1/t (M12), 1 (M32), (1+t)/3 (M52), 2 (Gaussian, t = r^2)}.
+template <int FAM>
+__device__ __forceinline__ double dcov_fast(const double* __restrict__ a, const double* __restrict__ b, int pidx,
+                                            const CovParams& p, const double* __restrict__ tbl) {
+  double t2 = 0.0;
+  for (int k = 0; k < p.d; ++k) {
+    const double dk = a[k] - b[k];
+    t2 = fma(dk, dk, t2);
+  }
+  const double t = FAM == FAM_GAUSS ? t2 : sqrt_fast(t2);
+  const double E = sig2_exp_neg(t, tbl);
+  if (pidx == 0) {
+    const double f = FAM == FAM_M12 || FAM == FAM_GAUSS ? E : (FAM == FAM_M32 ? fma(E, t, E) : fma(E, fma(t2, 1.0 / 3.0, t), E));
+    return f / p.sigma2;
+  }
+  const int j = pidx - 1;
+  const double dj = a[j] - b[j];
+  const double g = E * dj * dj * p.inv_ls[j];
+  if (FAM == FAM_M12) return t > 0.0 ? g / t : 0.0;
+  if (FAM == FAM_M32) return g;
+  if (FAM == FAM_M52) return fma(g, t, g) * (1.0 / 3.0);
+  return 2.0 * g;
+}
+
 template <int FAM>
 __global__ void dkm_kernel(const double* __restrict__ Z, int m, int mk, int pidx, CovParams p,
                            double* __restrict__ out) {
@@ -181,6 +207,9 @@ __global__ void __launch_bounds__(GW * 32, 4) grad_state_kernel(
   constexpr int NT = RB * (RB + 1) / 2;
   constexpr int LP = SP * (SP + 1) / 2;
   static_assert(SP <= 32, "gradient kernels need s <= 32");
+  __shared__ double tbl[64];
+  exp_table_init(tbl, p.sigma2, threadIdx.x);
+  __syncthreads();
   if (pos >= npts) return;
   const int64_t i = order[pos];
   const int nb0 = lane < mv ? nbr[i * mv + lane] : -1;
@@ -189,7 +218,7 @@ __global__ void __launch_bounds__(GW * 32, 4) grad_state_kernel(
   const int myidx = lane < q ? nb0 : (lane == q ? (int)i : -1);
   if (lane < SP) Sidx[lane] = myidx;
   if (lane < s)
-    for (int k = 0; k < p.d; ++k) xs[lane * p.d + k] = X[(int64_t)myidx * p.d + k];
+    for (int k = 0; k < p.d; ++k) xs[lane * p.d + k] = X[(int64_t)myidx * p.d + k] * (fam_scale<FAM>() * p.inv_ls[k]);
   __syncwarp();
   double acc[NT][2], gm[RB];
 #pragma unroll
@@ -246,7 +275,7 @@ __global__ void __launch_bounds__(GW * 32, 4) grad_state_kernel(
     if ((r + 1) * (r + 2) / 2 <= e) ++r;
     if (r * (r + 1) / 2 > e) --r;
     const int c = e - r * (r + 1) / 2;
-    double v = cov<FAM>(xs + r * p.d, xs + c * p.d, p) - C[r * CS + c];
+    double v = cov_fast<FAM>(xs + r * p.d, xs + c * p.d, p.d, tbl) - C[r * CS + c];
     if (r == c) v += p.nugget;
     C[r * CS + c] = v;
   }
@@ -323,6 +352,9 @@ __global__ void __launch_bounds__(GW * 32, 4) grad_param_kernel(
   GRAD_WARP_SETUP
   constexpr int LP = SP * (SP + 1) / 2;
   __shared__ double wsum[GW];
+  __shared__ double tbl[64];
+  exp_table_init(tbl, p.sigma2, threadIdx.x);
+  __syncthreads();
   double contrib = 0.0;
   if (pos < npts) {
     const int64_t i = order[pos];
@@ -332,17 +364,19 @@ __global__ void __launch_bounds__(GW * 32, 4) grad_param_kernel(
     const int myidx = lane < q ? nb0 : (lane == q ? (int)i : -1);
     if (lane < SP) Sidx[lane] = myidx;
     if (lane < s)
-      for (int k = 0; k < p.d; ++k) xs[lane * p.d + k] = X[(int64_t)myidx * p.d + k];
+      for (int k = 0; k < p.d; ++k) xs[lane * p.d + k] = X[(int64_t)myidx * p.d + k] * (fam_scale<FAM>() * p.inv_ls[k]);
     if (lane < SP) gamd_s[lane] = 0.0;
     __syncwarp();
     if (dU) {
-      double xacc[RB][RB][2], gmd[RB];
+      // symmetric cross-Gram dG = dU_S U_S^T + U_S dU_S^T on the RB(RB+1)/2 lower tiles (two DMMAs per
+      // tile and k-step) and the g_i . dU_aug dots; loads of chunk k + 8 are issued before the DMMAs of
+      // chunk k (two register stages)
+      constexpr int NT = RB * (RB + 1) / 2;
+      double dacc[NT][2], gmd[RB];
 #pragma unroll
-      for (int R1 = 0; R1 < RB; ++R1) {
-        gmd[R1] = 0.0;
+      for (int t = 0; t < NT; ++t) dacc[t][0] = dacc[t][1] = 0.0;
 #pragma unroll
-        for (int R2 = 0; R2 < RB; ++R2) xacc[R1][R2][0] = xacc[R1][R2][1] = 0.0;
-      }
+      for (int R = 0; R < RB; ++R) gmd[R] = 0.0;
       const double* rp[RB];
       const double* drp[RB];
 #pragma unroll
@@ -352,25 +386,39 @@ __global__ void __launch_bounds__(GW * 32, 4) grad_param_kernel(
         drp[R] = gi >= 0 ? dU + (int64_t)gi * ldu + 2 * (lane & 3) : nullptr;
       }
       const double* grow = Gam + pos * (int64_t)ld + 2 * (lane & 3);
-      for (int k0 = 0; k0 < ld; k0 += 8) {
-        const double2 g2 = __ldg(reinterpret_cast<const double2*>(grow + k0));
-        double2 f[RB], df[RB];
+      double2 f[RB], df[RB], g2;
+      auto load = [&](int k0, double2 (&ff)[RB], double2 (&dff)[RB], double2& gg) {
+        gg = k0 < ld ? __ldg(reinterpret_cast<const double2*>(grow + k0)) : make_double2(0.0, 0.0);
 #pragma unroll
         for (int R = 0; R < RB; ++R) {
-          f[R] = rp[R] ? __ldg(reinterpret_cast<const double2*>(rp[R] + k0)) : make_double2(0.0, 0.0);
-          df[R] = drp[R] ? __ldg(reinterpret_cast<const double2*>(drp[R] + k0)) : make_double2(0.0, 0.0);
+          ff[R] = (rp[R] && k0 < ld) ? __ldg(reinterpret_cast<const double2*>(rp[R] + k0)) : make_double2(0.0, 0.0);
+          dff[R] = (drp[R] && k0 < ld) ? __ldg(reinterpret_cast<const double2*>(drp[R] + k0)) : make_double2(0.0, 0.0);
         }
+      };
+      load(0, f, df, g2);
+      for (int k0 = 0; k0 < ld; k0 += 8) {
+        double2 fn[RB], dfn[RB], gn;
+        load(k0 + 8, fn, dfn, gn);
 #pragma unroll
         for (int R = 0; R < RB; ++R) gmd[R] = fma(df[R].x, g2.x, fma(df[R].y, g2.y, gmd[R]));
         if (k0 < mk) {
+          int t = 0;
 #pragma unroll
           for (int R1 = 0; R1 < RB; ++R1)
 #pragma unroll
-            for (int R2 = 0; R2 < RB; ++R2) {
-              dmma884(xacc[R1][R2][0], xacc[R1][R2][1], df[R1].x, f[R2].x);
-              dmma884(xacc[R1][R2][0], xacc[R1][R2][1], df[R1].y, f[R2].y);
+            for (int R2 = 0; R2 <= R1; ++R2, ++t) {
+              dmma884(dacc[t][0], dacc[t][1], df[R1].x, f[R2].x);
+              dmma884(dacc[t][0], dacc[t][1], df[R1].y, f[R2].y);
+              dmma884(dacc[t][0], dacc[t][1], f[R1].x, df[R2].x);
+              dmma884(dacc[t][0], dacc[t][1], f[R1].y, df[R2].y);
             }
         }
+#pragma unroll
+        for (int R = 0; R < RB; ++R) {
+          f[R] = fn[R];
+          df[R] = dfn[R];
+        }
+        g2 = gn;
       }
 #pragma unroll
       for (int R = 0; R < RB; ++R) {
@@ -378,26 +426,27 @@ __global__ void __launch_bounds__(GW * 32, 4) grad_param_kernel(
         gmd[R] += __shfl_xor_sync(0xffffffffu, gmd[R], 2);
         if ((lane & 3) == 0) gamd_s[R * 8 + (lane >> 2)] = gmd[R];
       }
-      // X = dU_S U_S^T (full) into C (free until the state's L is loaded)
+      // dG lower tiles into dC
+      int t = 0;
 #pragma unroll
       for (int R1 = 0; R1 < RB; ++R1)
 #pragma unroll
-        for (int R2 = 0; R2 < RB; ++R2) {
+        for (int R2 = 0; R2 <= R1; ++R2, ++t) {
           const int r = R1 * 8 + (lane >> 2), c = R2 * 8 + 2 * (lane & 3);
-          C[r * CS + c] = xacc[R1][R2][0];
-          C[r * CS + c + 1] = xacc[R1][R2][1];
+          dC[r * CS + c] = dacc[t][0];
+          dC[r * CS + c + 1] = dacc[t][1];
         }
     }
     __syncwarp();
-    // dC_S (lower) = dK + [nugget] I - (X + X^T)
+    // dC_S (lower) = dK + [nugget] I - dG
     const int ne = s * (s + 1) / 2;
     for (int e = lane; e < ne; e += 32) {
       int r = (int)((sqrtf_fast(8.0f * (float)e + 1.0f) - 1.0f) * 0.5f);
       if ((r + 1) * (r + 2) / 2 <= e) ++r;
       if (r * (r + 1) / 2 > e) --r;
       const int c = e - r * (r + 1) / 2;
-      double v = pidx <= p.d ? dcov<FAM>(xs + r * p.d, xs + c * p.d, pidx, p) : 0.0;
-      if (dU) v -= C[r * CS + c] + C[c * CS + r];
+      double v = pidx <= p.d ? dcov_fast<FAM>(xs + r * p.d, xs + c * p.d, pidx, p, tbl) : 0.0;
+      if (dU) v -= dC[r * CS + c];
       if (r == c && pidx == p.d + 1) v += 1.0;
       dC[r * CS + c] = v;
     }
