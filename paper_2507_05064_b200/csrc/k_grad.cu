@@ -174,6 +174,10 @@ template <int RB>
 __host__ __device__ constexpr int grad_warp_doubles(int d) {
   return 2 * (RB * 8) * (RB * 8 + 1) + 3 * (RB * 8) + RB * 8 * d;  // C, dC (or X), abuf, gam, gamd, xs
 }
+template <int RB>
+__host__ __device__ constexpr int param_warp_doubles(int d) {
+  return (RB * 8) * (RB * 8 + 1) + 3 * (RB * 8) + RB * 8 * d;  // dC, abuf, gam, gamd, xs
+}
 // per-point state of pass 0, by position: L (packed lower, SP rows incl. the identity padding), A_i,
 // 1/L_jj, g_i . U_aug[S_k], D_i, ok
 template <int RB>
@@ -349,7 +353,18 @@ __global__ void __launch_bounds__(GW * 32, 4) grad_param_kernel(
     const double* __restrict__ U, const double* __restrict__ dU, const double* __restrict__ Gam, int64_t ldu, int mk,
     int ld, const double* __restrict__ X, const int32_t* __restrict__ nbr, int mv, const int64_t* __restrict__ order,
     int64_t npts, CovParams p, int pidx, const double* __restrict__ state, double* __restrict__ part) {
-  GRAD_WARP_SETUP
+  constexpr int SP = RB * 8;
+  constexpr int CS = SP + 1;
+  extern __shared__ __align__(16) double gsm_[];
+  __shared__ int Sidx_all[GW][SP];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double* dC = gsm_ + warp * param_warp_doubles<RB>(p.d);  // L comes from the state (global, L1)
+  double* abuf = dC + SP * CS;
+  double* gam_s = abuf + SP;
+  double* gamd_s = gam_s + SP;
+  double* xs = gamd_s + SP;
+  int* Sidx = Sidx_all[warp];
+  const int64_t pos = (int64_t)blockIdx.x * GW + warp;
   constexpr int LP = SP * (SP + 1) / 2;
   __shared__ double wsum[GW];
   __shared__ double tbl[64];
@@ -451,15 +466,8 @@ __global__ void __launch_bounds__(GW * 32, 4) grad_param_kernel(
       dC[r * CS + c] = v;
     }
     __syncwarp();
-    // state: L rows into C, A, 1/L_jj, gam, D, ok
+    // state: A, 1/L_jj, gam, D, ok; rows of L are read from it directly (packed lower)
     const double* st = state + pos * (int64_t)state_doubles<RB>();
-    for (int e = lane; e < LP; e += 32) {
-      int r = (int)((sqrtf_fast(8.0f * (float)e + 1.0f) - 1.0f) * 0.5f);
-      if ((r + 1) * (r + 2) / 2 <= e) ++r;
-      if (r * (r + 1) / 2 > e) --r;
-      const int c = e - r * (r + 1) / 2;
-      C[r * CS + c] = st[e];
-    }
     const double a = lane < SP ? st[LP + lane] : 0.0;
     const double myinv = lane < SP ? st[LP + SP + lane] : 1.0;
     if (lane < SP) gam_s[lane] = st[LP + 2 * SP + lane];
@@ -469,7 +477,7 @@ __global__ void __launch_bounds__(GW * 32, 4) grad_param_kernel(
     __syncwarp();
     double crow[SP];
 #pragma unroll
-    for (int c = 0; c < SP; ++c) crow[c] = (lane < SP && c <= lane) ? C[lane * CS + c] : 0.0;
+    for (int c = 0; c < SP; ++c) crow[c] = (lane < SP && c <= lane) ? st[lane * (lane + 1) / 2 + c] : 0.0;
     // u = dC_NN A^T, b = dC_Ni - u, dD_i
     double u = 0.0;
     if (lane < q)
@@ -490,7 +498,7 @@ __global__ void __launch_bounds__(GW * 32, 4) grad_param_kernel(
     for (int j = q - 1; j >= 0; --j) {
       const double xj = __shfl_sync(0xffffffffu, bv * myinv, j);
       if (lane == j) bv = xj;
-      else if (lane < j) bv = fma(-C[j * CS + lane], xj, bv);
+      else if (lane < j) bv = fma(-st[j * (j + 1) / 2 + lane], xj, bv);
     }
     const double da = lane < q ? bv : 0.0;
     const double rs = rsqrt_nr(Di);
@@ -524,12 +532,13 @@ cudaError_t launch_grad_rb(const GradPointArgs& a, bool state_pass, cudaStream_t
     grad_state_kernel<FAM, RB><<<blocks, GW * 32, smem, s>>>(a.U, a.Gam, a.ldu, a.mk, a.ld, a.X, a.nbr, a.mv,
                                                              a.order, a.npts, a.p, a.state);
   } else {
-    if (smem > 48 * 1024) {
+    const size_t psmem = (size_t)GW * param_warp_doubles<RB>(a.p.d) * sizeof(double);
+    if (psmem > 48 * 1024) {
       cudaError_t e = cudaFuncSetAttribute(grad_param_kernel<FAM, RB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           (int)smem);
+                                           (int)psmem);
       if (e != cudaSuccess) return e;
     }
-    grad_param_kernel<FAM, RB><<<blocks, GW * 32, smem, s>>>(a.U, a.dU, a.Gam, a.ldu, a.mk, a.ld, a.X, a.nbr, a.mv,
+    grad_param_kernel<FAM, RB><<<blocks, GW * 32, psmem, s>>>(a.U, a.dU, a.Gam, a.ldu, a.mk, a.ld, a.X, a.nbr, a.mv,
                                                              a.order, a.npts, a.p, a.pidx, a.state, a.part);
   }
   return cudaGetLastError();
