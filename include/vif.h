@@ -115,6 +115,14 @@ int vif_create(void** handle, const vif_dims* dims, void* workspace, size_t ws_b
 int vif_set_data(void* handle, const double* X, const double* Z, const int32_t* nbr, const double* y,
                  int32_t validate);
 
+/* Double-buffered input staging for pipelined use: copy X, Z, nbr, y (all required; host pinned or
+ * device) into the handle's second input slot on an internal copy stream and sort its processing
+ * order there; the next vif_factor / vif_neighbors (and vif_grad / vif_predict through them) swaps the
+ * slot in, after the copies.  Returns at once; the current slot is untouched, so a vif_nll of the
+ * evaluation already enqueued stays valid, and the copies overlap its compute.  No validation.
+ * Errors: INVALID_ARG (missing array), CUDA. */
+int vif_stage_data(void* handle, const double* X, const double* Z, const int32_t* nbr, const double* y);
+
 /* Compute the factor at theta: K_m, L_m, L_m^{-1}; U rows (this rank's chunks) and their
  * all-gather; per owned point the residual block, its Cholesky, A_i, D_i and the row
  * w_i = (u_i - sum_k A_ik u_{N(i)_k}) / sqrt(D_i) with r_i appended; the Gram

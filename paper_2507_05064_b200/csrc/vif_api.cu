@@ -84,8 +84,24 @@ struct Plan {
 
 enum Buf {
   B_X, B_Z, B_NBR, B_Y, B_KM, B_LINV, B_U, B_W, B_DPOS, B_ORDER, B_KEYS, B_KEYS2, B_VALS, B_VALS2, B_TEMP,
-  B_GPART, B_G, B_GSUM, B_LINVM, B_TSCR, B_PART, B_BBOX, B_TERMS, B_STATUS, B_COUNT
+  B_GPART, B_G, B_GSUM, B_LINVM, B_TSCR, B_PART, B_BBOX, B_TERMS, B_STATUS,
+  // second input slot (vif_stage_data: inputs of the next evaluation copied while this one runs)
+  B_X2, B_Z2, B_NBR2, B_Y2, B_ORDER2,
+  // sort scratch of the staging path (its sort runs on the copy stream, beside the main stream's work)
+  B_SKEYS, B_SKEYS2, B_SVALS, B_SVALS2, B_STEMP, B_SBBOX, B_COUNT
 };
+
+inline Buf slot_buf(Buf b, int sl) {
+  if (sl == 0) return b;
+  switch (b) {
+    case B_X: return B_X2;
+    case B_Z: return B_Z2;
+    case B_NBR: return B_NBR2;
+    case B_Y: return B_Y2;
+    case B_ORDER: return B_ORDER2;
+    default: return b;
+  }
+}
 
 struct Layout {
   size_t off[B_COUNT];
@@ -166,6 +182,17 @@ Layout make_layout(const Plan& P) {
   L.size[B_BBOX] = 128 * 6 * D8;
   L.size[B_TERMS] = 8 * D8;
   L.size[B_STATUS] = 256;
+  L.size[B_X2] = L.size[B_X];
+  L.size[B_Z2] = L.size[B_Z];
+  L.size[B_NBR2] = L.size[B_NBR];
+  L.size[B_Y2] = L.size[B_Y];
+  L.size[B_ORDER2] = L.size[B_ORDER];
+  L.size[B_SKEYS] = L.size[B_KEYS];
+  L.size[B_SKEYS2] = L.size[B_KEYS2];
+  L.size[B_SVALS] = L.size[B_VALS];
+  L.size[B_SVALS2] = L.size[B_VALS2];
+  L.size[B_STEMP] = L.size[B_TEMP];
+  L.size[B_SBBOX] = L.size[B_BBOX];
   size_t off = 0;
   for (int b = 0; b < B_COUNT; ++b) {
     L.off[b] = off;
@@ -199,7 +226,11 @@ struct Handle {
   int cached_status = VIF_OK;
   std::string err;
   int64_t launches = 0;
-  std::vector<const int64_t*> order;  // per (logical) rank
+  // input slots: `slot` holds the inputs the next evaluation uses; vif_stage_data fills the other one
+  // on s_copy (ev_ready), swapped in by the next vif_factor / vif_neighbors; ev_free[k] = last use of k
+  int slot = 0, pending = -1;
+  cudaStream_t s_copy = nullptr;
+  cudaEvent_t ev_ready[2] = {}, ev_free[2] = {};
   // profiling
   bool prof = false;
   cudaEvent_t ev[S_COUNT][2] = {};
@@ -216,7 +247,11 @@ struct Handle {
   }
 
   template <typename T>
-  T* buf(Buf b) const { return reinterpret_cast<T*>(base + L.off[b]); }
+  T* buf(Buf b) const { return reinterpret_cast<T*>(base + L.off[slot_buf(b, slot)]); }
+  template <typename T>
+  T* buf_slot(Buf b, int sl) const { return reinterpret_cast<T*>(base + L.off[slot_buf(b, sl)]); }
+  // processing order of (logical) rank g for the current input slot
+  const int64_t* ord(int g) const { return buf<int64_t>(B_ORDER) + (size_t)g * P.npos; }
 };
 
 int fail(Handle* h, int code, const std::string& msg) {
@@ -257,35 +292,52 @@ bool make_params(const Handle* h, const vif_theta* th, CovParams& p, std::string
   return true;
 }
 
-int compute_orders(Handle* h) {
+int compute_orders(Handle* h, int sl, cudaStream_t strm, bool staging = false) {
   const Plan& P = h->P;
   const int nrep = P.emulate ? P.world : 1;
-  h->order.assign(nrep, nullptr);
   for (int g = 0; g < nrep; ++g) {
     const int rank = P.emulate ? g : P.rank;
     int64_t* sorted = nullptr;
-    VIF_CUDA(h, launch_order(h->buf<double>(B_X), P.n, P.d, P.npos, P.chunk, P.world, rank, h->buf<double>(B_BBOX),
-                             h->buf<uint64_t>(B_KEYS), h->buf<uint64_t>(B_KEYS2), h->buf<int64_t>(B_VALS),
-                             h->buf<int64_t>(B_VALS2), h->buf<void>(B_TEMP), h->L.size[B_TEMP], &sorted, h->stream),
+    VIF_CUDA(h, launch_order(h->buf_slot<double>(B_X, sl), P.n, P.d, P.npos, P.chunk, P.world, rank,
+                             h->buf<double>(staging ? B_SBBOX : B_BBOX), h->buf<uint64_t>(staging ? B_SKEYS : B_KEYS),
+                             h->buf<uint64_t>(staging ? B_SKEYS2 : B_KEYS2), h->buf<int64_t>(staging ? B_SVALS : B_VALS),
+                             h->buf<int64_t>(staging ? B_SVALS2 : B_VALS2), h->buf<void>(staging ? B_STEMP : B_TEMP),
+                             h->L.size[B_TEMP], &sorted, strm),
              "order");
-    int64_t* dst = h->buf<int64_t>(B_ORDER) + (size_t)g * P.npos;
-    VIF_CUDA(h, cudaMemcpyAsync(dst, sorted, P.npos * sizeof(int64_t), cudaMemcpyDeviceToDevice, h->stream),
-             "order copy");
-    h->order[g] = dst;
+    int64_t* dst = h->buf_slot<int64_t>(B_ORDER, sl) + (size_t)g * P.npos;
+    VIF_CUDA(h, cudaMemcpyAsync(dst, sorted, P.npos * sizeof(int64_t), cudaMemcpyDeviceToDevice, strm), "order copy");
   }
+  return VIF_OK;
+}
+
+// make a staged input slot current (the work on the stream waits for its copies)
+int apply_pending(Handle* h) {
+  if (h->pending < 0) return VIF_OK;
+  VIF_CUDA(h, cudaStreamWaitEvent(h->stream, h->ev_ready[h->pending], 0), "event wait");
+  h->slot = h->pending;
+  h->pending = -1;
+  return VIF_OK;
+}
+
+int mark_inputs_used(Handle* h) {
+  if (h->ev_free[h->slot]) VIF_CUDA(h, cudaEventRecord(h->ev_free[h->slot], h->stream), "event");
   return VIF_OK;
 }
 
 int set_data(Handle* h, const double* X, const double* Z, const int32_t* nbr, const double* y, int validate) {
   const Plan& P = h->P;
   cudaStream_t s = h->stream;
+  {
+    int r = apply_pending(h);
+    if (r != VIF_OK) return r;
+  }
   if (X) VIF_CUDA(h, cudaMemcpyAsync(h->buf<double>(B_X), X, P.n * P.d * 8, cudaMemcpyDefault, s), "copy X");
   if (Z && P.m > 0) VIF_CUDA(h, cudaMemcpyAsync(h->buf<double>(B_Z), Z, (size_t)P.m * P.d * 8, cudaMemcpyDefault, s), "copy Z");
   if (nbr && P.mv > 0)
     VIF_CUDA(h, cudaMemcpyAsync(h->buf<int32_t>(B_NBR), nbr, (size_t)P.n * P.mv * 4, cudaMemcpyDefault, s), "copy nbr");
   if (y) VIF_CUDA(h, cudaMemcpyAsync(h->buf<double>(B_Y), y, P.n * 8, cudaMemcpyDefault, s), "copy y");
   if (X) {
-    int r = compute_orders(h);
+    int r = compute_orders(h, h->slot, s);
     if (r != VIF_OK) return r;
   }
   if (X || Z || nbr || y) {
@@ -465,6 +517,16 @@ int vif_create(void** handle, const vif_dims* dims, void* workspace, size_t ws_b
       return fail(nullptr, VIF_ERR_CUDA, m);
     }
   }
+  e = cudaStreamCreateWithFlags(&h->s_copy, cudaStreamNonBlocking);
+  for (int k = 0; k < 2 && e == cudaSuccess; ++k) {
+    e = cudaEventCreateWithFlags(&h->ev_ready[k], cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h->ev_free[k], cudaEventDisableTiming);
+  }
+  if (e != cudaSuccess) {
+    std::string m = std::string("copy stream/events: ") + cudaGetErrorString(e);
+    vif_destroy(h);
+    return fail(nullptr, VIF_ERR_CUDA, m);
+  }
   if (h->P.world == 1 && h->P.rounds > 1) {
     e = cudaStreamCreateWithFlags(&h->s_k1, cudaStreamNonBlocking);
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&h->s_sy, cudaStreamNonBlocking);
@@ -509,6 +571,31 @@ int vif_set_data(void* handle, const double* X, const double* Z, const int32_t* 
   return set_data(h, X, Z, nbr, y, validate);
 }
 
+int vif_stage_data(void* handle, const double* X, const double* Z, const int32_t* nbr, const double* y) {
+  Handle* h = reinterpret_cast<Handle*>(handle);
+  if (!h) return fail(nullptr, VIF_ERR_INVALID_ARG, "handle is NULL");
+  const Plan& P = h->P;
+  if (!X || !y || (P.m > 0 && !Z) || (P.mv > 0 && !nbr))
+    return fail(h, VIF_ERR_INVALID_ARG, "vif_stage_data: X, Z (m > 0), nbr (m_v > 0) and y are all required");
+  const int t = h->pending >= 0 ? h->pending : h->slot ^ 1;  // the slot no queued evaluation reads
+  cudaStream_t c = h->s_copy;
+  VIF_CUDA(h, cudaStreamWaitEvent(c, h->ev_free[t], 0), "event wait");
+  VIF_CUDA(h, cudaMemcpyAsync(h->buf_slot<double>(B_X, t), X, P.n * P.d * 8, cudaMemcpyDefault, c), "copy X");
+  if (P.m > 0)
+    VIF_CUDA(h, cudaMemcpyAsync(h->buf_slot<double>(B_Z, t), Z, (size_t)P.m * P.d * 8, cudaMemcpyDefault, c),
+             "copy Z");
+  if (P.mv > 0)
+    VIF_CUDA(h, cudaMemcpyAsync(h->buf_slot<int32_t>(B_NBR, t), nbr, (size_t)P.n * P.mv * 4, cudaMemcpyDefault, c),
+             "copy nbr");
+  VIF_CUDA(h, cudaMemcpyAsync(h->buf_slot<double>(B_Y, t), y, P.n * 8, cudaMemcpyDefault, c), "copy y");
+  int r = compute_orders(h, t, c, true);
+  if (r != VIF_OK) return r;
+  VIF_CUDA(h, cudaEventRecord(h->ev_ready[t], c), "event");
+  h->pending = t;
+  h->have_data = true;
+  return VIF_OK;
+}
+
 int vif_factor(void* handle, const vif_theta* theta, double* B_out, double* D_out) {
   Handle* h = reinterpret_cast<Handle*>(handle);
   if (!h) return fail(nullptr, VIF_ERR_INVALID_ARG, "handle is NULL");
@@ -518,6 +605,10 @@ int vif_factor(void* handle, const vif_theta* theta, double* B_out, double* D_ou
   if (!make_params(h, theta, p, err)) return fail(h, VIF_ERR_INVALID_ARG, err);
   const Plan& P = h->P;
   cudaStream_t s = h->stream;
+  {
+    int r = apply_pending(h);
+    if (r != VIF_OK) return r;
+  }
   DevStatus* st = h->buf<DevStatus>(B_STATUS);
   int64_t nl = 0;
   for (int k = 0; k < S_COUNT; ++k) h->ev_used[k] = false;
@@ -575,7 +666,7 @@ int vif_factor(void* handle, const vif_theta* theta, double* B_out, double* D_ou
         a.X = h->buf<double>(B_X);
         a.nbr = h->buf<int32_t>(B_NBR);
         a.mv = P.mv;
-        a.order = h->order[0] + off;
+        a.order = h->ord(0) + off;
         a.npts = cnt;
         a.p = p;
         a.W = h->buf<double>(B_W) + (size_t)off * P.ld;
@@ -615,7 +706,7 @@ int vif_factor(void* handle, const vif_theta* theta, double* B_out, double* D_ou
     h->factored = true;
     h->finished = false;
     h->launches = nl;
-    return VIF_OK;
+    return mark_inputs_used(h);
   }
   // A1-A6 in chunk-cyclic rounds.  Round r of a rank = positions [r*chunk, (r+1)*chunk);
   // vif_set_data groups the processing order by round (Morton order inside a round).  Per rank:
@@ -668,7 +759,7 @@ int vif_factor(void* handle, const vif_theta* theta, double* B_out, double* D_ou
         a.X = h->buf<double>(B_X);
         a.nbr = h->buf<int32_t>(B_NBR);
         a.mv = P.mv;
-        a.order = h->order[g] + off;
+        a.order = h->ord(g) + off;
         a.npts = cnt;
         a.p = p;
         a.W = h->buf<double>(B_W) + (size_t)off * P.ld;
@@ -716,7 +807,7 @@ int vif_factor(void* handle, const vif_theta* theta, double* B_out, double* D_ou
   h->factored = true;
   h->finished = false;
   h->launches = nl;
-  return VIF_OK;
+  return mark_inputs_used(h);
 }
 
 int vif_nll(void* handle, vif_terms* out) {
@@ -849,7 +940,7 @@ int vif_grad(void* handle, const vif_theta* theta, void* gws, size_t gws_bytes, 
   a.X = h->buf<double>(B_X);
   a.nbr = h->buf<int32_t>(B_NBR);
   a.mv = P.mv;
-  a.order = h->order[0];
+  a.order = h->ord(0);
   a.npts = P.n_own[0];
   a.p = p;
   a.pidx = -1;
@@ -872,6 +963,10 @@ int vif_grad(void* handle, const vif_theta* theta, void* gws, size_t gws_bytes, 
     a.dU = dUp;
     a.pidx = pi;
     VIF_CUDA(h, launch_grad_points(a, gbuf(G_OUT) + pi, s), "gradient points");
+  }
+  {
+    int r2 = mark_inputs_used(h);
+    if (r2 != VIF_OK) return r2;
   }
   VIF_CUDA(h, cudaMemcpyAsync(grad, gbuf(G_OUT), (size_t)(P.d + 2) * 8, cudaMemcpyDeviceToHost, s), "grad copy");
   VIF_CUDA(h, cudaStreamSynchronize(s), "sync");
@@ -967,6 +1062,10 @@ int vif_predict(void* handle, const vif_theta* theta, int64_t np, const double* 
   VIF_CUDA(h, launch_pred_mean(pbuf(P_W), ld, m, P.ycol, pbuf(P_Z), pbuf(P_DPOS), order, np, mu,
                                var && m > 0 ? pbuf(P_S) : nullptr, mk, var, s),
            "mean / variance");
+  {
+    int r2 = mark_inputs_used(h);
+    if (r2 != VIF_OK) return r2;
+  }
   DevStatus hs;
   VIF_CUDA(h, cudaMemcpyAsync(&hs, st, sizeof(hs), cudaMemcpyDeviceToHost, s), "status copy");
   VIF_CUDA(h, cudaStreamSynchronize(s), "sync");
@@ -989,6 +1088,10 @@ int vif_neighbors(void* handle, const vif_theta* theta, int32_t mv, int32_t* nbr
   std::string err;
   if (!make_params(h, theta, p, err)) return fail(h, VIF_ERR_INVALID_ARG, err);
   cudaStream_t s = h->stream;
+  {
+    int r = apply_pending(h);
+    if (r != VIF_OK) return r;
+  }
   DevStatus* st = h->buf<DevStatus>(B_STATUS);
   h->factored = h->finished = false;
   VIF_CUDA(h, launch_reset_status(st, s), "reset status");
@@ -1007,6 +1110,10 @@ int vif_neighbors(void* handle, const vif_theta* theta, int32_t mv, int32_t* nbr
   VIF_CUDA(h, launch_knn(h->buf<double>(B_U), P.ld, P.m, P.mk, h->buf<double>(B_X), P.n, p, h->buf<double>(B_DPOS),
                          reinterpret_cast<int*>(h->buf<uint64_t>(B_KEYS)), mv, nbr_out, s),
            "neighbour search");
+  {
+    int r = mark_inputs_used(h);
+    if (r != VIF_OK) return r;
+  }
   DevStatus hs;
   VIF_CUDA(h, cudaMemcpyAsync(&hs, st, sizeof(hs), cudaMemcpyDeviceToHost, s), "status copy");
   VIF_CUDA(h, cudaStreamSynchronize(s), "sync");
@@ -1072,6 +1179,11 @@ void vif_destroy(void* handle) {
   if (h->ev_k0) cudaEventDestroy(h->ev_k0);
   if (h->ev_sy) cudaEventDestroy(h->ev_sy);
   if (h->s_k1) cudaStreamDestroy(h->s_k1);
+  for (int k = 0; k < 2; ++k) {
+    if (h->ev_ready[k]) cudaEventDestroy(h->ev_ready[k]);
+    if (h->ev_free[k]) cudaEventDestroy(h->ev_free[k]);
+  }
+  if (h->s_copy) cudaStreamDestroy(h->s_copy);
   if (h->s_sy) cudaStreamDestroy(h->s_sy);
   for (int k = 0; k < S_COUNT; ++k)
     for (int j = 0; j < 2; ++j)

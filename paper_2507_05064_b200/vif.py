@@ -82,10 +82,11 @@ def load_library():
         lib.vif_predict_workspace_bytes.argtypes = [ctypes.POINTER(_Dims), i64, ctypes.POINTER(sz)]
         lib.vif_predict.argtypes = [P, ctypes.POINTER(_Theta), i64, P, P, P, sz, P, P, P, P]
         lib.vif_neighbors.argtypes = [P, ctypes.POINTER(_Theta), i32, P]
+        lib.vif_stage_data.argtypes = [P, P, P, P, P]
         for f in ("vif_nccl_unique_id", "vif_workspace_bytes", "vif_partition", "vif_create", "vif_set_data",
                   "vif_factor", "vif_nll", "vif_copy_U", "vif_launch_count", "vif_profile", "vif_stage_times",
                   "vif_grad_workspace_bytes", "vif_grad", "vif_predict_workspace_bytes", "vif_predict",
-                  "vif_neighbors"):
+                  "vif_neighbors", "vif_stage_data"):
             getattr(lib, f).restype = ctypes.c_int
         _lib = lib
     return _lib
@@ -94,7 +95,7 @@ def load_library():
 EXPORTED = ("vif_nccl_unique_id", "vif_workspace_bytes", "vif_partition", "vif_create", "vif_set_data",
             "vif_factor", "vif_nll", "vif_copy_U", "vif_launch_count", "vif_profile", "vif_stage_times",
             "vif_stage_name", "vif_last_error", "vif_destroy", "vif_grad_workspace_bytes", "vif_grad",
-            "vif_predict_workspace_bytes", "vif_predict", "vif_neighbors")
+            "vif_predict_workspace_bytes", "vif_predict", "vif_neighbors", "vif_stage_data")
 NUM_STAGES = 8
 
 
@@ -200,6 +201,11 @@ def vif_create(n, d, m, mv, workspace: torch.Tensor, X=None, Z=None, nbr=None, y
 
 def vif_set_data(h, X=None, Z=None, nbr=None, y=None, validate: bool = False):
     _check(load_library().vif_set_data(h, _ptr(X), _ptr(Z), _ptr(nbr), _ptr(y), int(validate)), h)
+
+
+def vif_stage_data(h, X, Z, nbr, y):
+    """Stage the next evaluation's inputs into the second slot (copies overlap the current evaluation)."""
+    _check(load_library().vif_stage_data(h, _ptr(X), _ptr(Z), _ptr(nbr), _ptr(y)), h)
 
 
 def vif_factor(h, theta: Theta, B_out: Optional[torch.Tensor] = None, D_out: Optional[torch.Tensor] = None):
@@ -316,6 +322,10 @@ class VifModel:
 
     def set_data(self, X=None, Z=None, nbr=None, y=None, validate=False):
         vif_set_data(self.handle, X, Z, nbr, y, validate)
+
+    def stage_data(self, X, Z, nbr, y):
+        """Inputs of the next evaluation (pinned host or device tensors), copied while this one runs."""
+        vif_stage_data(self.handle, X, Z if self.m > 0 else None, nbr if self.mv > 0 else None, y)
 
     def factor(self, theta: Theta, B_out=None, D_out=None):
         vif_factor(self.handle, theta, B_out, D_out)

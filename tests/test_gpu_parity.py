@@ -258,3 +258,38 @@ np.save(sys.argv[1], np.concatenate([B.cpu().numpy().ravel(), D.cpu().numpy(), [
     a, b = outs
     assert np.array_equal(a[:-1], b[:-1])
     assert b[-1] == pytest.approx(a[-1], rel=1e-12)
+
+
+def test_stage_data_pipelined_matches_set_data():
+    """vif_stage_data (second input slot, copy stream) gives exactly the results of vif_set_data, in the
+    pipelined order factor(k) -> stage(k+1) -> nll(k), with pinned-host inputs, and across a switch
+    between two different data sets (and back to set_data)."""
+    p = vif()
+    dev = torch.device("cuda")
+    wa = small(3000, 40, 12, seed=101)
+    wb = small(3000, 40, 12, seed=102)
+
+    def pinned(w):
+        return tuple(torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
+                     for a in (w.X, w.Z.reshape(-1, w.d), w.nbr, w.y))
+    ha, hb = pinned(wa), pinned(wb)
+    th = p.Theta(**wa.theta_dict())
+    ref = []
+    for h in (ha, hb):
+        m = p.VifModel(*(t.to(dev) for t in h), device=dev)
+        ref.append(m.evaluate(th).nll)
+        m.close()
+    model = p.VifModel(*(t.to(dev) for t in ha), device=dev)
+    seq = [ha, hb, hb, ha, hb, ha]
+    model.stage_data(*seq[0])
+    got = []
+    for k in range(len(seq)):
+        model.factor(th)
+        if k + 1 < len(seq):
+            model.stage_data(*seq[k + 1])
+        got.append(model.nll().nll)
+    want = [ref[0] if s is ha else ref[1] for s in seq]
+    assert got == want
+    model.set_data(*ha)
+    assert model.evaluate(th).nll == ref[0]
+    model.close()
