@@ -165,7 +165,9 @@ int vif_grad(void* handle, const vif_theta* theta, void* grad_workspace, size_t 
  * Xp: np x d (device or host), nbrp: np x m_v training indices in [0, n), -1 only as trailing pad
  * (host or device); workspace: caller-owned device buffer of vif_predict_workspace_bytes(dims, np).
  * mu (device, np, required); var, Dp (device, np, optional); Bp (device, np x m_v, optional: -A_p).
- * Errors: INVALID_ARG (np < 1, NULL, world > 1), NO_MEMORY (workspace), NOT_PD (training factor, or a
+ * Multi-rank: every rank passes all np inputs and full-length outputs; rank g predicts the contiguous
+ * slice [g ceil(np/G), (g+1) ceil(np/G)) and writes only that slice (as vif_factor's B_out / D_out).
+ * Errors: INVALID_ARG (np < 1, NULL), NO_MEMORY (workspace), NOT_PD (training factor, or a
  * prediction block: the message names the prediction row), CUDA. */
 int vif_predict_workspace_bytes(const vif_dims* dims, int64_t np, size_t* bytes);
 int vif_predict(void* handle, const vif_theta* theta, int64_t np, const double* Xp, const int32_t* nbrp,

@@ -991,7 +991,6 @@ int vif_predict(void* handle, const vif_theta* theta, int64_t np, const double* 
   if (!h) return fail(nullptr, VIF_ERR_INVALID_ARG, "handle is NULL");
   const Plan& P = h->P;
   if (np < 1 || !Xp || !mu || (P.mv > 0 && !nbrp)) return fail(h, VIF_ERR_INVALID_ARG, "vif_predict: bad arguments");
-  if (P.world != 1) return fail(h, VIF_ERR_INVALID_ARG, "vif_predict: single-rank handles only in this version");
   const Layout PL = make_pred_layout(P, np);
   if (!ws || ws_bytes < PL.total) {
     char msg[128];
@@ -1004,17 +1003,34 @@ int vif_predict(void* handle, const vif_theta* theta, int64_t np, const double* 
   std::string err;
   if (!make_params(h, theta, p, err)) return fail(h, VIF_ERR_INVALID_ARG, err);
   cudaStream_t s = h->stream;
-  VIF_CUDA(h, cudaMemcpyAsync(pbuf(P_X), Xp, (size_t)np * P.d * 8, cudaMemcpyDefault, s), "copy Xp");
-  if (P.mv > 0)
-    VIF_CUDA(h, cudaMemcpyAsync(pbuf(P_NBR), nbrp, (size_t)np * P.mv * 4, cudaMemcpyDefault, s), "copy nbrp");
+  // ranks (NCCL) predict contiguous slices of the prediction points and write only their slice of the
+  // outputs; an emulated multi-rank handle (one process) predicts all of them
+  {
+    const int64_t per = P.emulate ? np : (np + P.world - 1) / P.world;
+    const int64_t lo = P.emulate ? 0 : std::min<int64_t>(np, P.rank * per);
+    const int64_t hi = std::min<int64_t>(np, lo + per);
+    Xp += lo * P.d;
+    if (nbrp) nbrp += lo * P.mv;
+    mu += lo;
+    if (var) var += lo;
+    if (Dp) Dp += lo;
+    if (Bp) Bp += lo * P.mv;
+    np = hi - lo;
+  }
+  if (np > 0) {
+    VIF_CUDA(h, cudaMemcpyAsync(pbuf(P_X), Xp, (size_t)np * P.d * 8, cudaMemcpyDefault, s), "copy Xp");
+    if (P.mv > 0)
+      VIF_CUDA(h, cudaMemcpyAsync(pbuf(P_NBR), nbrp, (size_t)np * P.mv * 4, cudaMemcpyDefault, s), "copy nbrp");
+  }
   int r = vif_factor(handle, theta, nullptr, nullptr);
   if (r != VIF_OK) return r;
   const int m = P.m, mk = P.mk, ld = P.ld;
-  double* G = h->buf<double>(B_G);
+  double* G = h->buf<double>(P.emulate ? B_GSUM : B_G);  // the (all-)reduced Gram
   VIF_CUDA(h, cudaMemcpyAsync(pbuf(P_MCOPY), G, (size_t)ld * ld * 8, cudaMemcpyDeviceToDevice, s), "copy G");
   vif_terms t;
   r = vif_nll(handle, &t);
   if (r != VIF_OK) return r;
+  if (np == 0) return VIF_OK;
   DevStatus* st = h->buf<DevStatus>(B_STATUS);
   // z = M_w^{-1} G_Wr
   if (m > 0) {

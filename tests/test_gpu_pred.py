@@ -28,11 +28,11 @@ def small(n, m, mv, family="matern32", seed=1, rho=0.15, nugget=0.1, d=2, ard=No
                                 device="cuda", ard=ard, z="kmeans++" if m > 0 else "subset")
 
 
-def pred_parity(w, npred=300, x="uniform"):
+def pred_parity(w, npred=300, x="uniform", world=1):
     import paper_2507_05064_b200 as p
     dev = torch.device("cuda")
     X, Z, nbr, y = (torch.from_numpy(np.ascontiguousarray(a)).to(dev) for a in (w.X, w.Z.reshape(-1, w.d), w.nbr, w.y))
-    model = p.VifModel(X, Z, nbr, y, device=dev)
+    model = p.VifModel(X, Z, nbr, y, world=world, device=dev)
     Xp, nbrp = vifgen.make_prediction(w, npred, x=x, device="cuda")
     mu, var, Dp, Bp = model.predict(p.Theta(**w.theta_dict()), Xp, nbrp, want_var=True, want_D=True, want_B=True)
     mu, var, Dp, Bp = mu.cpu().numpy(), var.cpu().numpy(), Dp.cpu().numpy(), Bp.cpu().numpy()
@@ -54,6 +54,12 @@ def test_pred_config1():
 @pytest.mark.parametrize("n,m,mv", [(700, 37, 13), (513, 64, 31), (400, 9, 40)])
 def test_pred_shapes(family, n, m, mv):
     pred_parity(small(n, m, mv, family=family, seed=n + mv), npred=257)
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_pred_emulated_world(world):
+    """An emulated multi-rank handle (one process) reduces the Gram over its ranks and predicts all points."""
+    pred_parity(small(900, 40, 15, seed=world), npred=301, world=world)
 
 
 def test_pred_m0_and_mv0():
