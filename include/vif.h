@@ -144,8 +144,10 @@ int vif_nll(void* handle, vif_terms* out);
  * (Q (ld x ld), g rows and dU (n x ld each), m x m scratch; ld = roundup(roundup(m,8)+1, 8)).
  * vif_grad runs vif_factor + vif_nll at theta, then per parameter dK(Z,Z), Phi = L_m^{-1} dK_m
  * L_m^{-T}, dK(X,Z), dU and one pass over the points (Gram, cross-Gram, Cholesky, dA_i, dD_i), and
- * synchronises.  grad: host, d + 2 doubles.  terms (optional): as vif_nll.
- * Errors: INVALID_ARG (theta; world > 1 or m_v > 31: not supported by this version), NO_MEMORY
+ * synchronises.  grad: host, d + 2 doubles, identical on every rank.  terms (optional): as vif_nll.
+ * Multi-rank: each rank sums its own points' terms (its dU over all n rows is formed locally) and one
+ * all-reduce of the d + 2 partial sums follows; an emulated handle sums its virtual ranks in order.
+ * Errors: INVALID_ARG (theta; m_v > 31: not supported by this version), NO_MEMORY
  * (grad workspace too small), NOT_PD (as vif_nll), CUDA. */
 int vif_grad_workspace_bytes(const vif_dims* dims, size_t* bytes);
 int vif_grad(void* handle, const vif_theta* theta, void* grad_workspace, size_t grad_ws_bytes, double* grad,

@@ -167,8 +167,9 @@ Layout make_layout(const Plan& P) {
   L.size[B_KM] = (size_t)m1 * m1 * D8;
   L.size[B_LINV] = (size_t)mk1 * mk1 * D8;
   L.size[B_U] = (size_t)P.npad * P.ld * D8;
-  L.size[B_W] = (size_t)P.npos * P.ld * D8;
-  L.size[B_DPOS] = (size_t)P.npos * D8;
+  // an emulated multi-rank handle keeps every virtual rank's W and D rows (vif_grad reads them back)
+  L.size[B_W] = (size_t)nrep * P.npos * P.ld * D8;
+  L.size[B_DPOS] = (size_t)nrep * P.npos * D8;
   L.size[B_ORDER] = (size_t)nrep * P.npos * sizeof(int64_t);
   L.size[B_KEYS] = L.size[B_KEYS2] = L.size[B_VALS] = L.size[B_VALS2] = (size_t)P.npos * 8;
   L.size[B_TEMP] = order_temp_bytes(P.npos);
@@ -380,7 +381,7 @@ Layout make_grad_layout(const Plan& P) {
   L.size[G_MCOPY] = (size_t)P.ld * P.ld * D8;
   L.size[G_ZH] = L.size[G_Z] = (size_t)mk1 * D8;
   L.size[G_PART] = (size_t)grad_point_nparts(P.npos) * D8;
-  L.size[G_OUT] = (size_t)(P.d + 2) * D8;
+  L.size[G_OUT] = (size_t)(P.d + 2) * (P.emulate ? P.world : 1) * D8;
   L.size[G_STATE] = (size_t)P.npos * grad_state_doubles(P.mv) * D8;
   size_t off = 0;
   for (int b = 0; b < G_COUNT; ++b) {
@@ -744,6 +745,8 @@ int vif_factor(void* handle, const vif_theta* theta, double* B_out, double* D_ou
   for (int g = 0; g < nrep; ++g) {
     const int rank = P.emulate ? g : P.rank;
     const int64_t npts = P.n_own[rank];
+    double* Wg = h->buf<double>(B_W) + (size_t)g * P.npos * P.ld;
+    double* Dg = h->buf<double>(B_DPOS) + (size_t)g * P.npos;
     h->mark(S_VECCHIA, 0);
     int64_t off = 0;
     for (int64_t r = 0; r < P.rounds; ++r) {
@@ -762,9 +765,9 @@ int vif_factor(void* handle, const vif_theta* theta, double* B_out, double* D_ou
         a.order = h->ord(g) + off;
         a.npts = cnt;
         a.p = p;
-        a.W = h->buf<double>(B_W) + (size_t)off * P.ld;
+        a.W = Wg + (size_t)off * P.ld;
         a.ldw = P.ld;
-        a.Dpos = h->buf<double>(B_DPOS) + off;
+        a.Dpos = Dg + off;
         a.B_out = B_out;
         a.D_out = D_out;
         a.st = st;
@@ -779,14 +782,14 @@ int vif_factor(void* handle, const vif_theta* theta, double* B_out, double* D_ou
     // default: 64x64 / 4-warp SYRK (k_syrk.cu); VIF_SYRK128=1 selects the 128x128 engine
     static const char* syrk128 = getenv("VIF_SYRK128");
     if (!(syrk128 && syrk128[0] == '1'))
-      VIF_CUDA(h, launch_syrk(h->buf<double>(B_W), P.ld, npts, P.ld, P.nsplit_old, h->buf<double>(B_GPART), G, P.ld, s),
+      VIF_CUDA(h, launch_syrk(Wg, P.ld, npts, P.ld, P.nsplit_old, h->buf<double>(B_GPART), G, P.ld, s),
                "syrk");
     else
-      VIF_CUDA(h, launch_syrk_nt(h->buf<double>(B_W), P.ld, npts, P.ld, P.nsplit, h->buf<double>(B_GPART), G, P.ld, s),
+      VIF_CUDA(h, launch_syrk_nt(Wg, P.ld, npts, P.ld, P.nsplit, h->buf<double>(B_GPART), G, P.ld, s),
                "syrk");
     h->mark(S_SYRK, 1);
     h->mark(S_REDUCE, 0);
-    VIF_CUDA(h, launch_logd_sum(h->buf<double>(B_DPOS), npts, h->buf<double>(B_PART), kLogdParts,
+    VIF_CUDA(h, launch_logd_sum(Dg, npts, h->buf<double>(B_PART), kLogdParts,
                                 G + (size_t)P.ld * P.ld, s),
              "logd");
     nl += 4;
@@ -891,7 +894,6 @@ int vif_grad(void* handle, const vif_theta* theta, void* gws, size_t gws_bytes, 
   if (!h) return fail(nullptr, VIF_ERR_INVALID_ARG, "handle is NULL");
   if (!grad) return fail(h, VIF_ERR_INVALID_ARG, "grad is NULL");
   const Plan& P = h->P;
-  if (P.world != 1) return fail(h, VIF_ERR_INVALID_ARG, "vif_grad: single-rank handles only in this version");
   if (P.mv > 31) return fail(h, VIF_ERR_INVALID_ARG, "vif_grad: m_v <= 31 only in this version");
   const Layout GL = make_grad_layout(P);
   if (!gws || gws_bytes < GL.total) {
@@ -908,7 +910,7 @@ int vif_grad(void* handle, const vif_theta* theta, void* gws, size_t gws_bytes, 
   if (r != VIF_OK) return r;
   cudaStream_t s = h->stream;
   const int m = P.m, mk = P.mk, ld = P.ld;
-  double* G = h->buf<double>(B_G);
+  double* G = h->buf<double>(P.emulate ? B_GSUM : B_G);  // the (all-)reduced Gram
   VIF_CUDA(h, cudaMemcpyAsync(gbuf(G_MCOPY), G, (size_t)ld * ld * 8, cudaMemcpyDeviceToDevice, s), "copy G");
   vif_terms t;
   r = vif_nll(handle, &t);
@@ -923,46 +925,70 @@ int vif_grad(void* handle, const vif_theta* theta, void* gws, size_t gws_bytes, 
              "chol M (full inverse)");
   }
   VIF_CUDA(h, launch_grad_q(gbuf(G_LINVM), mk, G, ld, P.ycol, m, ld, gbuf(G_ZH), gbuf(G_Z), gbuf(G_Q2), s), "Q");
-  // g rows: Gamma = W (2Q), rows by processing position
-  double* W = h->buf<double>(B_W);
-  VIF_CUDA(h, launch_gemm_tn(W, ld, P.npos, gbuf(G_Q2), ld, ld, ld, 0, gbuf(G_GAM), ld, 1.0, 0, s), "Gamma");
-  VIF_CUDA(h, cudaMemsetAsync(gbuf(G_DU), 0, GL.size[G_DU], s), "memset dU");
+  // Per rank (every virtual rank of an emulated handle): Gamma = W (2Q) for its rows by processing position,
+  // the per-point state, then one pass per parameter.  dU = dK(X,Z) L^-T - U Phi_low^T is needed on all n
+  // rows (neighbours live on any rank); each rank forms it itself, in row blocks through the rank's own
+  // W, which is dead once Gamma is formed.
+  const int nrep = P.emulate ? P.world : 1;
   const double* Linv = h->buf<double>(B_LINV);
   const double* U = h->buf<double>(B_U);
-  double* S = W;  // W is dead once Gamma is formed: reuse it as the dK(X,Z) scratch
-  GradPointArgs a;
-  a.U = U;
-  a.dU = nullptr;
-  a.Gam = gbuf(G_GAM);
-  a.ldu = ld;
-  a.mk = mk;
-  a.ld = ld;
-  a.X = h->buf<double>(B_X);
-  a.nbr = h->buf<int32_t>(B_NBR);
-  a.mv = P.mv;
-  a.order = h->ord(0);
-  a.npts = P.n_own[0];
-  a.p = p;
-  a.pidx = -1;
-  a.part = gbuf(G_PART);
-  a.state = gbuf(G_STATE);
-  VIF_CUDA(h, launch_grad_state(a, s), "gradient state");
-  for (int pi = 0; pi < P.d + 2; ++pi) {
-    const bool kernel_param = pi <= P.d;
-    const double* dUp = nullptr;
-    if (kernel_param && m > 0) {
-      VIF_CUDA(h, launch_dkm(h->buf<double>(B_Z), m, mk, pi, p, gbuf(G_DKM), s), "dK_m");
-      VIF_CUDA(h, launch_gemm_tn(Linv, mk, mk, gbuf(G_DKM), mk, mk, mk, 0, gbuf(G_TT), mk, 1.0, 0, s), "Linv dK_m");
-      VIF_CUDA(h, launch_gemm_tn(Linv, mk, mk, gbuf(G_TT), mk, mk, mk, 0, gbuf(G_PHI), mk, 1.0, 0, s), "Phi");
-      VIF_CUDA(h, launch_phi_low(gbuf(G_PHI), mk, gbuf(G_PHILOW), s), "Phi_low");
-      VIF_CUDA(h, launch_kx_deriv(h->buf<double>(B_X), h->buf<double>(B_Z), P.n, m, mk, pi, p, S, s), "dK(X,Z)");
-      VIF_CUDA(h, launch_gemm_tn(S, mk, P.n, Linv, mk, mk, mk, 1, gbuf(G_DU), ld, 1.0, 0, s), "dK L^-T");
-      VIF_CUDA(h, launch_gemm_tn(U, ld, P.n, gbuf(G_PHILOW), mk, mk, mk, 1, gbuf(G_DU), ld, -1.0, 1, s), "U Phi^T");
-      dUp = gbuf(G_DU);
+  const int nparam = P.d + 2;
+  // columns mk..ld-1 of dU (the y column and the padding) stay zero: d y / d theta = 0
+  VIF_CUDA(h, cudaMemsetAsync(gbuf(G_DU), 0, GL.size[G_DU], s), "memset dU");
+  for (int g = 0; g < nrep; ++g) {
+    const int rank = P.emulate ? g : P.rank;
+    double* W = h->buf<double>(B_W) + (size_t)g * P.npos * ld;
+    VIF_CUDA(h, launch_gemm_tn(W, ld, P.npos, gbuf(G_Q2), ld, ld, ld, 0, gbuf(G_GAM), ld, 1.0, 0, s), "Gamma");
+    double* S = W;
+    GradPointArgs a;
+    a.U = U;
+    a.dU = nullptr;
+    a.Gam = gbuf(G_GAM);
+    a.ldu = ld;
+    a.mk = mk;
+    a.ld = ld;
+    a.X = h->buf<double>(B_X);
+    a.nbr = h->buf<int32_t>(B_NBR);
+    a.mv = P.mv;
+    a.order = h->ord(g);
+    a.npts = P.n_own[rank];
+    a.p = p;
+    a.pidx = -1;
+    a.part = gbuf(G_PART);
+    a.state = gbuf(G_STATE);
+    VIF_CUDA(h, launch_grad_state(a, s), "gradient state");
+    for (int pi = 0; pi < nparam; ++pi) {
+      const bool kernel_param = pi <= P.d;
+      const double* dUp = nullptr;
+      if (kernel_param && m > 0) {
+        VIF_CUDA(h, launch_dkm(h->buf<double>(B_Z), m, mk, pi, p, gbuf(G_DKM), s), "dK_m");
+        VIF_CUDA(h, launch_gemm_tn(Linv, mk, mk, gbuf(G_DKM), mk, mk, mk, 0, gbuf(G_TT), mk, 1.0, 0, s), "Linv dK_m");
+        VIF_CUDA(h, launch_gemm_tn(Linv, mk, mk, gbuf(G_TT), mk, mk, mk, 0, gbuf(G_PHI), mk, 1.0, 0, s), "Phi");
+        VIF_CUDA(h, launch_phi_low(gbuf(G_PHI), mk, gbuf(G_PHILOW), s), "Phi_low");
+        const int64_t blk = std::max<int64_t>(1, (P.npos * ld) / mk);  // rows of dK(X,Z) that fit in S
+        for (int64_t r0 = 0; r0 < P.n; r0 += blk) {
+          const int64_t rows = std::min<int64_t>(blk, P.n - r0);
+          double* dUr = gbuf(G_DU) + (size_t)r0 * ld;
+          VIF_CUDA(h, launch_kx_deriv(h->buf<double>(B_X) + (size_t)r0 * P.d, h->buf<double>(B_Z), rows, m, mk, pi, p,
+                                      S, s),
+                   "dK(X,Z)");
+          VIF_CUDA(h, launch_gemm_tn(S, mk, rows, Linv, mk, mk, mk, 1, dUr, ld, 1.0, 0, s), "dK L^-T");
+          VIF_CUDA(h, launch_gemm_tn(U + (size_t)r0 * ld, ld, rows, gbuf(G_PHILOW), mk, mk, mk, 1, dUr, ld, -1.0, 1, s),
+                   "U Phi^T");
+        }
+        dUp = gbuf(G_DU);
+      }
+      a.dU = dUp;
+      a.pidx = pi;
+      VIF_CUDA(h, launch_grad_points(a, gbuf(G_OUT) + (size_t)g * nparam + pi, s), "gradient points");
     }
-    a.dU = dUp;
-    a.pidx = pi;
-    VIF_CUDA(h, launch_grad_points(a, gbuf(G_OUT) + pi, s), "gradient points");
+  }
+  if (nrep > 1) {
+    VIF_CUDA(h, launch_sum_buffers(gbuf(G_OUT), nparam, nrep, nparam, gbuf(G_OUT), s), "emulated all-reduce");
+  } else if (P.world > 1) {
+    Nccl& N = nccl();
+    ncclResult_t rr = N.AllReduce(gbuf(G_OUT), gbuf(G_OUT), (size_t)nparam, ncclFloat64, ncclSum, h->comm, s);
+    if (rr != ncclSuccess) return fail(h, VIF_ERR_NCCL, std::string("ncclAllReduce: ") + N.GetErrorString(rr));
   }
   {
     int r2 = mark_inputs_used(h);

@@ -31,11 +31,11 @@ def vif():
     return p
 
 
-def model_of(w):
+def model_of(w, world=1):
     p = vif()
     dev = torch.device("cuda")
     X, Z, nbr, y = (torch.from_numpy(np.ascontiguousarray(a)).to(dev) for a in (w.X, w.Z.reshape(-1, w.d), w.nbr, w.y))
-    return p.VifModel(X, Z, nbr, y, device=dev)
+    return p.VifModel(X, Z, nbr, y, world=world, device=dev)
 
 
 def small(n, m, mv, family="matern32", seed=1, rho=0.15, nugget=0.1, d=2, ard=None, neighbors="dc"):
@@ -49,9 +49,9 @@ def check(g, r, rtol=1e-8):
     assert np.all(err <= rtol), (g, r.grad, err)
 
 
-def grad_parity(w, rtol=1e-8):
+def grad_parity(w, rtol=1e-8, world=1):
     p = vif()
-    model = model_of(w)
+    model = model_of(w, world)
     terms, g = model.grad(p.Theta(**w.theta_dict()))
     r = oracle.grad(w.X, w.Z, w.nbr, w.y, oracle.Theta(**w.theta_dict()))
     ro = oracle.factor_nll(w.X, w.Z, w.nbr, w.y, oracle.Theta(**w.theta_dict()), want_BD=False)
@@ -69,6 +69,12 @@ def test_grad_config1():
 @pytest.mark.parametrize("n,m,mv", [(700, 37, 13), (513, 64, 31), (300, 9, 1)])
 def test_grad_shapes(family, n, m, mv):
     grad_parity(small(n, m, mv, family=family, seed=n + mv))
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_grad_emulated_world(world):
+    """Emulated multi-rank handle: per-rank point sums (dU formed in several row blocks) + the reduction."""
+    grad_parity(small(1100, 45, 17, seed=world, d=3, ard=(0.5, 2.0)), world=world)
 
 
 def test_grad_m0_vecchia():
