@@ -65,6 +65,7 @@ class Workload:
     nugget: float
     jitter: float
     timings: Dict[str, float] = field(default_factory=dict)
+    latent: Optional[np.ndarray] = None  # latent GP draw of a Laplace workload (y then holds 0/1 labels)
 
     @property
     def n(self):
@@ -281,14 +282,17 @@ def draw_y(Xs: np.ndarray, family: str, sigma2: float, nugget: float, rng: np.ra
 def make_workload(n: int, d: int, m: int, mv: int, family: str = "matern32", sigma2: float = 1.0,
                   rho: Optional[float] = 0.1, ard: Optional[tuple] = None, nugget: float = 0.1,
                   x: str = "uniform", z: str = "kmeans++", seed: int = SEED_BASE, device=None,
-                  name: str = "custom", neighbors: str = "dc", permute: bool = True) -> Workload:
+                  name: str = "custom", neighbors: str = "dc", permute: bool = True,
+                  lengthscale: Optional[tuple] = None) -> Workload:
     t0 = time.perf_counter()
     ss = np.random.SeedSequence(seed)
     g_x, g_perm, g_z, g_lam, g_y = (np.random.Generator(np.random.PCG64(s)) for s in ss.spawn(5))
     X = g_x.random((n, d)) if x == "uniform" else g_x.standard_normal((n, d))
     if permute:
         X = X[g_perm.permutation(n)]
-    if ard is not None:
+    if lengthscale is not None:
+        lam = np.asarray(lengthscale, dtype=np.float64)
+    elif ard is not None:
         lo, hi = ard
         lam = np.exp(g_lam.uniform(math.log(lo), math.log(hi), size=d))
     else:
@@ -399,3 +403,37 @@ def make_prediction(w: Workload, npred: int, seed: int = SEED_BASE + 100, x: str
     nbrp = dc_neighbors_pred(w.X / lam, Xp / lam, w.Z.reshape(-1, d) / lam, w.family, w.sigma2, w.jitter, w.mv,
                              device=device)
     return Xp, np.ascontiguousarray(nbrp, dtype=np.int32)
+
+
+# ----------------------------------------------------------------------------------------------
+# VIF-Laplace inputs
+LAPLACE_LENGTHSCALE = (0.15, 0.30, 0.45, 0.60, 0.75)  # d = 5, ARD Gaussian covariance
+
+
+def make_laplace_workload(n: int, d: int = 5, m: int = 200, mv: int = 30, family: str = "gaussian",
+                          sigma2: float = 1.0, lengthscale: Optional[tuple] = None, rho: Optional[float] = None,
+                          seed: int = SEED_BASE + 40, device=None, neighbors: str = "dc",
+                          z: str = "kmeans++") -> Workload:
+    """Binary responses from a latent GP: b = zero-mean GP draw (no error term), y_i ~
+    Bernoulli(1 / (1 + exp(-b_i))).  Same recipe as make_workload with nugget 0 (the latent process has
+    no error variance); the Bernoulli draw uses a sixth child stream.  ``w.y`` holds the labels
+    (0.0 / 1.0) and ``w.latent`` the draw b."""
+    if lengthscale is None and rho is None:
+        lengthscale = LAPLACE_LENGTHSCALE[:d] if d <= len(LAPLACE_LENGTHSCALE) else None
+        rho = None if lengthscale is not None else 0.3
+    w = make_workload(n=n, d=d, m=m, mv=mv, family=family, sigma2=sigma2, rho=rho, nugget=0.0, z=z, seed=seed,
+                      device=device, name="laplace", neighbors=neighbors, lengthscale=lengthscale)
+    rng = np.random.Generator(np.random.PCG64(np.random.SeedSequence(seed).spawn(6)[5]))
+    b = w.y
+    w.latent = b
+    w.y = (rng.random(n) < 1.0 / (1.0 + np.exp(-b))).astype(np.float64)
+    return w
+
+
+def make_probes(n: int, m: int, nprobe: int, seed: int = SEED_BASE + 41):
+    """Standard normal draws for the SLQ probe vectors z_i = D_V^{1/2} eps2_i + U eps1_i:
+    eps1 (m x ell) and eps2 (n x ell), row-major."""
+    rng = np.random.Generator(np.random.PCG64(seed))
+    eps1 = np.ascontiguousarray(rng.standard_normal((m, nprobe)))
+    eps2 = np.ascontiguousarray(rng.standard_normal((n, nprobe)))
+    return eps1, eps2
