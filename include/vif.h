@@ -186,6 +186,67 @@ int vif_predict(void* handle, const vif_theta* theta, int64_t np, const double* 
  * Single rank.  Errors: INVALID_ARG, NOT_PD (K(Z,Z) + jitter), CUDA. */
 int vif_neighbors(void* handle, const vif_theta* theta, int32_t mv, int32_t* nbr_out);
 
+/* ---- VIF-Laplace iterative path (Bernoulli likelihood, logit link; Sect. 2-3) ----
+ * Latent b ~ N(0, Sigma_dagger), Sigma_dagger = B^{-1} D B^{-T} + U U^T with B, D the residual Vecchia
+ * factor WITHOUT error variance (vif_factor at nugget 0) and U the whitened features;
+ * y_i | b_i ~ Bernoulli(1 / (1 + exp(-b_i))).  L^VIFLA = -log p(y|b~) + b~^T Sigma_dagger^{-1} b~ / 2
+ * + log det(Sigma_dagger W + I) / 2 at the mode b~, W = diag(pi (1 - pi)).
+ *   mode: Newton with each step's solve in the form (pcls2),
+ *         (W^{-1} + Sigma_dagger) x = Sigma_dagger (W b + y - pi), b <- W^{-1} x, by preconditioned CG
+ *         with the FITC preconditioner P = D_V + U U^T, D_V = diag(sigma_1^2 - |u_i|^2) + W^{-1}
+ *         (App. FITC; reading l2: k = m, the VIF's inducing points);
+ *   quad: b~^T Sigma_dagger^{-1} b~ exactly through the factor's Woodbury form (reading l5);
+ *   log det: SLQ (slq_v2): log det W + (n / ell) sum_i e1^T log(T_i) e1 + log det P, T_i the
+ *         Lanczos matrices from the CG coefficients of the solves with z_i = D_V^{1/2} eps2_i + U eps1_i
+ *         (readings l6, l7).
+ * Vectors are row-major n x ncol by point index (the Vecchia order).  Single rank in this version. */
+typedef struct {
+  int32_t max_newton; /* Newton steps cap */
+  double newton_tol;  /* stop when |psi_t - psi_{t-1}| <= tol |psi_{t-1}|, psi = log p(y|b) - b^T a / 2 */
+  int32_t max_cg;     /* CG iterations cap per solve (<= the prepared max_cg) */
+  double cg_tol;      /* Newton solves: stop at ||r|| <= cg_tol ||rhs|| */
+  int32_t nprobe;     /* ell SLQ probe vectors (0: mode and quadratic term only) */
+  double slq_tol;     /* probe solves: stop at ||r|| <= slq_tol ||z_i|| */
+} vif_la_opts;
+
+typedef struct {
+  double nll;          /* L^VIFLA (NaN without probes) */
+  double neg_loglik;   /* -log p(y | b~) */
+  double quad;         /* b~^T Sigma_dagger^{-1} b~ */
+  double logdet;       /* SLQ estimate of log det(Sigma_dagger W + I) (NaN without probes) */
+  double logdet_W;     /* log det W at the mode */
+  double logdet_P;     /* log det of the FITC preconditioner at the mode */
+  int32_t newton_iters;
+  int32_t cg_iters;    /* CG iterations summed over the Newton steps */
+  int32_t slq_iters_max;
+  double slq_iters_mean;
+} vif_la_terms;
+
+enum { VIF_LA_SIGMA = 0, VIF_LA_A = 1, VIF_LA_BINV = 2, VIF_LA_BTINV = 3, VIF_LA_FITC_SOLVE = 4 };
+
+/* Size of the caller-owned device workspace for up to nprobe (<= 64) probe columns and max_cg CG
+ * iterations per solve (~ (8 nprobe + 12 + m_v) n doubles plus n x ld for the FITC rows). */
+int vif_la_workspace_bytes(const vif_dims* dims, int32_t nprobe, int32_t max_cg, size_t* bytes);
+/* vif_factor + vif_nll at theta with the nugget forced to 0, then B, D, |u_i|^2 and the transposed
+ * neighbour structure (children lists for B^{-T}) into the workspace; synchronises.  Any later
+ * vif_factor / vif_grad / vif_predict / vif_neighbors call on the handle invalidates it (VIF_ERR_STATE).
+ * Errors: INVALID_ARG (world > 1, nprobe, max_cg), NO_MEMORY, NOT_PD, CUDA. */
+int vif_la_prepare(void* handle, const vif_theta* theta, int32_t nprobe, int32_t max_cg, void* workspace,
+                   size_t ws_bytes);
+/* Operators of the path on ncol (<= max(1, nprobe)) device columns v (n x ncol) -> out:
+ * VIF_LA_SIGMA Sigma_dagger v;  VIF_LA_A (W^{-1} + Sigma_dagger) v;  VIF_LA_BINV B^{-1} v;
+ * VIF_LA_BTINV B^{-T} v;  VIF_LA_FITC_SOLVE P^{-1} v.  winv (device, n): W^{-1}, required by A and
+ * FITC_SOLVE.  The triangular solves are sync-free (one warp per row, rows claimed in dependency order,
+ * release/acquire flags).  Synchronises.  Errors: INVALID_ARG, STATE, NOT_PD (M_V), CUDA. */
+int vif_la_apply(void* handle, void* workspace, int32_t op, int32_t ncol, const double* v, const double* winv,
+                 double* out);
+/* Mode, quadratic term and (with opts.nprobe > 0) the SLQ log-determinant and L^VIFLA.  y: device, n
+ * labels in {0, 1}; eps1 (device, m x nprobe) and eps2 (device, n x nprobe): standard normal draws of
+ * the probe vectors (row-major); b_mode (optional, device or host, n).  Synchronises.
+ * Errors: INVALID_ARG, STATE, NOT_PD (non-finite Newton iterate, M_V), CUDA. */
+int vif_la_nll(void* handle, void* workspace, const double* y, const vif_la_opts* opts, const double* eps1,
+               const double* eps2, double* b_mode, vif_la_terms* out);
+
 /* Debug / parity: copy the whitened features U (n x m, row-major) to `out` (device or host). */
 int vif_copy_U(void* handle, double* out);
 

@@ -152,6 +152,7 @@ __global__ void __launch_bounds__(256, 2) gemm_tn_kernel(const double* __restric
     }
   }
   cp_async_wait<0>();
+  const bool pair = !((N | ldc) & 1);  // 16-byte stores need an even N and ldc
   // epilogue: lane holds C[fr][2*(lane&3) + {0,1}] of each 8x8 tile
 #pragma unroll
   for (int a = 0; a < 4; ++a) {
@@ -163,14 +164,20 @@ __global__ void __launch_bounds__(256, 2) gemm_tn_kernel(const double* __restric
     for (int b = 0; b < 4; ++b) {
       const int c = col0 + wn * 32 + b * 8 + (lane & 3) * 2;
       if (c < N) {
-        double2* dst = reinterpret_cast<double2*>(C + i * ldc + c);
-        double2 v = make_double2(alpha * acc[a][b][0], alpha * acc[a][b][1]);
-        if (accum) {  // C += alpha A B^T (gradient path)
-          const double2 o = *dst;
-          v.x += o.x;
-          v.y += o.y;
+        if (pair) {
+          double2* dst = reinterpret_cast<double2*>(C + i * ldc + c);
+          double2 v = make_double2(alpha * acc[a][b][0], alpha * acc[a][b][1]);
+          if (accum) {  // C += alpha A B^T (gradient path)
+            const double2 o = *dst;
+            v.x += o.x;
+            v.y += o.y;
+          }
+          *dst = v;
+        } else {  // odd N or ldc (Laplace path: one right-hand side)
+          double* dst = C + i * ldc + c;
+          dst[0] = alpha * acc[a][b][0] + (accum ? dst[0] : 0.0);
+          if (c + 1 < N) dst[1] = alpha * acc[a][b][1] + (accum ? dst[1] : 0.0);
         }
-        *dst = v;
       }
     }
   }

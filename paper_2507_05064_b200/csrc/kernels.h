@@ -102,6 +102,50 @@ cudaError_t launch_pred_mean(const double* Wp, int ld, int m, int ycol, const do
 size_t knn_smem_bytes(int mv);
 cudaError_t launch_knn(const double* U, int64_t ldu, int m, int mk, const double* X, int64_t n, const CovParams& p,
                        double* isd, int* deg, int mv, int32_t* out, cudaStream_t s);
+// VIF-Laplace iterative path (k_laplace.cu)
+cudaError_t launch_la_transpose_struct(const int32_t* nbr, int64_t n, int mv, int* cnt, int* cursor, int* tptr,
+                                       int* tpos, cudaStream_t s);
+cudaError_t launch_la_trsv_fwd(const int32_t* nbr, const double* Bc, int mv, int64_t n, int ncol, const double* v,
+                               const double* scale, double* x, const double* v2, const double* w2, double* out2,
+                               int* flags, int epoch, unsigned long long* ticket, cudaStream_t s);
+cudaError_t launch_la_trsv_bwd(const int* tptr, const int* tpos, const double* Bc, int mv, int64_t n, int ncol,
+                               const double* u, double* y, int* flags, int epoch, unsigned long long* ticket,
+                               cudaStream_t s);
+int la_ts_nsplit(int64_t n);
+cudaError_t launch_la_tsgemm(const double* U, int64_t ldu, int mk, int64_t n, const double* V, int ncol,
+                             const int64_t* vrow, const double* rs, double* part, double* Ct, double alpha,
+                             cudaStream_t s);
+int la_red_nsplit(int64_t n);
+cudaError_t launch_la_reduce(int op, const double* a, const double* b, int64_t n, int ncol, double* part,
+                             double* out, cudaStream_t s);
+cudaError_t launch_la_newton_prep(const double* y, const double* b, int64_t n, double* W, double* winv, double* v,
+                                  double* x0, cudaStream_t s);
+cudaError_t launch_la_newton_update(const double* x, const double* v, const double* winv, int64_t n, double* b,
+                                    double* a, cudaStream_t s);
+cudaError_t launch_la_fitc_rows(const double* U, int64_t ldu, int mk, int ld, int64_t n, const double* unorm2,
+                                double sigma2, const double* winv, double* DV, double* dvinv, double* S,
+                                cudaStream_t s);
+cudaError_t launch_la_rownorm2(const double* U, int64_t ldu, int mk, int64_t n, double* out, cudaStream_t s);
+cudaError_t launch_la_rowscale(const double* in, const double* r, int use_sqrt, int64_t n, int ncol, double* out,
+                               cudaStream_t s);
+cudaError_t launch_la_sub_rowscale(const double* a, const double* b, const double* r, int64_t n, int ncol, double* out,
+                                   cudaStream_t s);
+cudaError_t launch_la_residual(const double* b, int64_t tot, double* r, cudaStream_t s);
+cudaError_t launch_la_cg_alpha(const double* rz, const double* pq, const int* active, int ncol, double* alpha,
+                               double* hist_a, cudaStream_t s);
+cudaError_t launch_la_cg_xr(const double* alpha, const double* p, const double* q, int64_t n, int ncol, double* x,
+                            double* r, cudaStream_t s);
+cudaError_t launch_la_cg_beta(const double* rz_new, double* rz, const int* active, int ncol, double* beta,
+                              double* hist_b, cudaStream_t s);
+cudaError_t launch_la_cg_p(const double* beta, const int* active, const double* z, int64_t n, int ncol, double* p,
+                           cudaStream_t s);
+cudaError_t launch_la_transpose(const double* in, int rows, int cols, int ldin, double* out, int ldout, cudaStream_t s);
+cudaError_t launch_la_logdiag(const double* A, int m, int lda, double* out, cudaStream_t s);
+cudaError_t launch_la_slq(const double* hist_a, const double* hist_b, const int* iters, int ncol, int kmax,
+                          double* scratch, double* out, cudaStream_t s);
+cudaError_t launch_la_bapply(const int32_t* nbr, const double* Bc, int mv, int64_t n, const double* D, const double* b,
+                             double* s, cudaStream_t st);
+cudaError_t launch_la_finish(const double* fin, const double* slq, int64_t n, int ell, double* out, cudaStream_t s);
 // misc
 cudaError_t launch_validate(const double* X, int64_t n, int d, const double* Z, int m, const double* y,
                             const int32_t* nbr, int mv, DevStatus* st, cudaStream_t s);

@@ -232,6 +232,11 @@ struct Handle {
   int slot = 0, pending = -1;
   cudaStream_t s_copy = nullptr;
   cudaEvent_t ev_ready[2] = {}, ev_free[2] = {};
+  // VIF-Laplace state (vif_la_prepare): valid while fgen == la_gen (every vif_factor bumps fgen)
+  uint64_t fgen = 0, la_gen = ~0ull;
+  const void* la_ws = nullptr;
+  int la_epoch = 0, la_nprobe = 0, la_maxcg = 0;
+  double la_sigma2 = 0.0;
   // profiling
   bool prof = false;
   cudaEvent_t ev[S_COUNT][2] = {};
@@ -420,6 +425,225 @@ Layout make_pred_layout(const Plan& P, int64_t np) {
   }
   L.total = off + 256;
   return L;
+}
+
+// ---------------------------------------------------------------- VIF-Laplace workspace
+enum LBuf {
+  L_B, L_D, L_FLAGS, L_TPTR, L_TPOS, L_CNT, L_CUR, L_TICKET, L_UN2, L_W, L_WINV, L_V, L_BM, L_A, L_DV, L_DVINV,
+  L_S, L_GV, L_LVINV, L_LVT, L_MVINV, L_TSCR, L_GPART, L_TSPART, L_CT, L_CT2, L_RPART, L_SC, L_ACTIVE, L_ITERS,
+  L_HA, L_HB, L_SLQS, L_X, L_R, L_Z, L_P, L_Q, L_T1, L_T2, L_RHS, L_E1T, L_GM, L_LMINV, L_COUNT
+};
+// per-column scalar arrays inside L_SC (each kLaCols doubles)
+enum LScal { SC_RZ, SC_RZN, SC_PQ, SC_ALPHA, SC_BETA, SC_RR, SC_BN, SC_SLQ, SC_MISC, SC_OUT, SC_COUNT };
+constexpr int kLaCols = 64;  // maximum columns (probe vectors) of one block solve
+
+struct LaLayout {
+  size_t off[L_COUNT];
+  size_t size[L_COUNT];
+  size_t total;
+};
+
+LaLayout make_la_layout(const Plan& P, int nprobe, int max_cg) {
+  LaLayout L{};
+  const size_t D8 = sizeof(double);
+  const int64_t n = P.n, mv1 = P.mv > 0 ? P.mv : 1, mk1 = P.mk > 0 ? P.mk : 1;
+  const int ncol = nprobe > 1 ? nprobe : 1;
+  const int kmax = max_cg > 1 ? max_cg : 1;
+  const int ns_syrk = syrk_nsplit(P.ld, n, kPlanSMs);
+  L.size[L_B] = (size_t)n * mv1 * D8;
+  L.size[L_D] = L.size[L_UN2] = L.size[L_W] = L.size[L_WINV] = L.size[L_V] = L.size[L_BM] = L.size[L_A] =
+      L.size[L_DV] = L.size[L_DVINV] = (size_t)n * D8;
+  L.size[L_FLAGS] = L.size[L_CNT] = L.size[L_CUR] = (size_t)n * sizeof(int);
+  L.size[L_TPTR] = (size_t)(n + 1) * sizeof(int);
+  L.size[L_TPOS] = (size_t)n * mv1 * sizeof(int);
+  L.size[L_TICKET] = 64;
+  L.size[L_S] = (size_t)n * P.ld * D8;
+  L.size[L_GV] = (size_t)P.ld * P.ld * D8;
+  L.size[L_LVINV] = L.size[L_LVT] = L.size[L_MVINV] = L.size[L_TSCR] = L.size[L_LMINV] = (size_t)mk1 * mk1 * D8;
+  L.size[L_GM] = (size_t)P.ld * P.ld * D8;
+  L.size[L_GPART] = syrk_part_doubles(P.ld, ns_syrk) * D8;
+  L.size[L_TSPART] = (size_t)la_ts_nsplit(n) * ncol * mk1 * D8;
+  L.size[L_CT] = L.size[L_CT2] = L.size[L_E1T] = (size_t)ncol * mk1 * D8;
+  L.size[L_RPART] = (size_t)la_red_nsplit(n > mk1 ? n : mk1) * ncol * D8;
+  L.size[L_SC] = (size_t)SC_COUNT * kLaCols * D8;
+  L.size[L_ACTIVE] = L.size[L_ITERS] = (size_t)kLaCols * sizeof(int);
+  L.size[L_HA] = L.size[L_HB] = (size_t)kmax * ncol * D8;
+  L.size[L_SLQS] = (size_t)3 * kmax * ncol * D8;
+  L.size[L_X] = L.size[L_R] = L.size[L_Z] = L.size[L_P] = L.size[L_Q] = L.size[L_T1] = L.size[L_T2] =
+      L.size[L_RHS] = (size_t)n * ncol * D8;
+  size_t off = 0;
+  for (int b = 0; b < L_COUNT; ++b) {
+    L.off[b] = off;
+    off += (L.size[b] + 255) / 256 * 256;
+  }
+  L.total = off + 256;
+  return L;
+}
+
+// VIF-Laplace helpers: buffers of a prepared workspace and the operators of the iterative path
+struct LaCtx {
+  Handle* h;
+  LaLayout L;
+  char* base;
+  cudaStream_t s;
+  double* d(LBuf b) const { return reinterpret_cast<double*>(base + L.off[b]); }
+  int* i(LBuf b) const { return reinterpret_cast<int*>(base + L.off[b]); }
+  double* sc(int k) const { return d(L_SC) + (size_t)k * kLaCols; }
+  unsigned long long* ticket() const { return reinterpret_cast<unsigned long long*>(base + L.off[L_TICKET]); }
+  int* fitc_fail() const { return reinterpret_cast<int*>(base + L.off[L_TICKET] + 8); }
+  const double* U() const { return h->buf<double>(B_U); }
+  const int32_t* nbr() const { return h->buf<int32_t>(B_NBR); }
+};
+
+LaCtx la_ctx(Handle* h, void* ws) {
+  LaCtx c{h, make_la_layout(h->P, h->la_nprobe, h->la_maxcg), nullptr, h->stream};
+  c.base = reinterpret_cast<char*>(round_up((int64_t)(uintptr_t)ws, 256));
+  return c;
+}
+
+// out = Sigma_dagger v (+ winv o v): B^{-1} D B^{-T} v + U (U^T v); v, out: n x ncol
+int la_sigma(LaCtx& c, int ncol, const double* v, double* out, const double* winv) {
+  Handle* h = c.h;
+  const Plan& P = h->P;
+  if (P.mk > 0)
+    VIF_CUDA(h, launch_la_tsgemm(c.U(), P.ld, P.mk, P.n, v, ncol, nullptr, nullptr, c.d(L_TSPART), c.d(L_CT), 1.0,
+                                 c.s),
+             "U^T v");
+  VIF_CUDA(h, launch_la_trsv_bwd(c.i(L_TPTR), c.i(L_TPOS), c.d(L_B), P.mv, P.n, ncol, v, c.d(L_T1), c.i(L_FLAGS),
+                                 ++h->la_epoch, c.ticket(), c.s),
+           "B^-T");
+  double* x = winv ? c.d(L_T2) : out;
+  VIF_CUDA(h, launch_la_trsv_fwd(c.nbr(), c.d(L_B), P.mv, P.n, ncol, c.d(L_T1), c.d(L_D), x, v, winv,
+                                 winv ? out : nullptr, c.i(L_FLAGS), ++h->la_epoch, c.ticket(), c.s),
+           "B^-1");
+  if (P.mk > 0)
+    VIF_CUDA(h, launch_gemm_tn(c.U(), P.ld, P.n, c.d(L_CT), P.mk, ncol, P.mk, 0, out, ncol, 1.0, 1, c.s), "U C");
+  return VIF_OK;
+}
+
+// FITC preconditioner at W (App. FITC): D_V, M_V = I + U^T D_V^{-1} U, M_V^{-1}, log det M_V
+int la_fitc_build(LaCtx& c, const double* winv) {
+  Handle* h = c.h;
+  const Plan& P = h->P;
+  double* ldmv = c.sc(SC_MISC) + 5;
+  VIF_CUDA(h, launch_la_fitc_rows(c.U(), P.ld, P.mk, P.ld, P.n, c.d(L_UN2), h->la_sigma2, winv, c.d(L_DV),
+                                  c.d(L_DVINV), c.d(L_S), c.s),
+           "FITC rows");
+  if (P.mk == 0) {
+    VIF_CUDA(h, cudaMemsetAsync(ldmv, 0, sizeof(double), c.s), "memset");
+    return VIF_OK;
+  }
+  const int ns = syrk_nsplit(P.ld, P.n, kPlanSMs);
+  VIF_CUDA(h, launch_syrk(c.d(L_S), P.ld, P.n, P.ld, ns, c.d(L_GPART), c.d(L_GV), P.ld, c.s), "FITC syrk");
+  VIF_CUDA(h, cudaMemsetAsync(c.d(L_LVINV), 0, c.L.size[L_LVINV], c.s), "memset");
+  VIF_CUDA(h, launch_chol_inv(c.d(L_GV), P.m, P.ld, 1.0, c.d(L_LVINV), P.mk, P.mk, 1, c.d(L_TSCR), c.fitc_fail(),
+                              h->num_sms, c.s),
+           "FITC chol");
+  VIF_CUDA(h, launch_la_logdiag(c.d(L_GV), P.m, P.ld, ldmv, c.s), "log det M_V");
+  VIF_CUDA(h, launch_la_transpose(c.d(L_LVINV), P.mk, P.mk, P.mk, c.d(L_LVT), P.mk, c.s), "transpose");
+  VIF_CUDA(h, launch_gemm_tn(c.d(L_LVT), P.mk, P.mk, c.d(L_LVT), P.mk, P.mk, P.mk, 0, c.d(L_MVINV), P.mk, 1.0, 0, c.s),
+           "M_V^-1");
+  return VIF_OK;
+}
+
+// out = P^{-1} w = D_V^{-1} (w - U M_V^{-1} U^T D_V^{-1} w)
+int la_fitc_solve(LaCtx& c, int ncol, const double* w, double* out) {
+  Handle* h = c.h;
+  const Plan& P = h->P;
+  if (P.mk == 0) {
+    VIF_CUDA(h, launch_la_rowscale(w, c.d(L_DVINV), 0, P.n, ncol, out, c.s), "D_V^-1 w");
+    return VIF_OK;
+  }
+  VIF_CUDA(h, launch_la_tsgemm(c.U(), P.ld, P.mk, P.n, w, ncol, nullptr, c.d(L_DVINV), c.d(L_TSPART), c.d(L_CT), 1.0,
+                               c.s),
+           "U^T D_V^-1 w");
+  VIF_CUDA(h, launch_gemm_tn(c.d(L_CT), P.mk, ncol, c.d(L_MVINV), P.mk, P.mk, P.mk, 0, c.d(L_CT2), P.mk, 1.0, 0, c.s),
+           "M_V^-1 C");
+  VIF_CUDA(h, launch_gemm_tn(c.U(), P.ld, P.n, c.d(L_CT2), P.mk, ncol, P.mk, 0, c.d(L_T1), ncol, 1.0, 0, c.s), "U C");
+  VIF_CUDA(h, launch_la_sub_rowscale(w, c.d(L_T1), c.d(L_DVINV), P.n, ncol, out, c.s), "FITC tail");
+  return VIF_OK;
+}
+
+int la_coldot(LaCtx& c, const double* a, const double* b, int64_t n, int ncol, double* out) {
+  VIF_CUDA(c.h, launch_la_reduce(0, a, b, n, ncol, c.d(L_RPART), out, c.s), "dot");
+  return VIF_OK;
+}
+
+#define LA_TRY(call)               \
+  do {                             \
+    int r_ = (call);               \
+    if (r_ != VIF_OK) return r_;   \
+  } while (0)
+
+// Preconditioned CG on (W^{-1} + Sigma_dagger) x = rhs, ncol independent columns (pcls2 P:322;
+// Saad 2003 Alg. 9.1), readings l3 (stop at ||r|| <= tol ||rhs||).  x holds x0 when warm.  With
+// record, alpha_j / beta_j go to L_HA / L_HB [j][c] for the Lanczos matrices.  iters[c]:
+// iterations of column c.
+int la_pcg(LaCtx& c, int ncol, const double* rhs, double* x, bool warm, double tol, int max_it, const double* winv,
+           bool record, std::vector<int>& iters) {
+  Handle* h = c.h;
+  const Plan& P = h->P;
+  const int64_t tot = P.n * ncol;
+  double* R = c.d(L_R);
+  double* Z = c.d(L_Z);
+  double* Pv = c.d(L_P);
+  double* Q = c.d(L_Q);
+  if (warm) {
+    LA_TRY(la_sigma(c, ncol, x, R, winv));
+    VIF_CUDA(h, launch_la_residual(rhs, tot, R, c.s), "residual");
+  } else {
+    VIF_CUDA(h, cudaMemsetAsync(x, 0, tot * sizeof(double), c.s), "memset x");
+    VIF_CUDA(h, cudaMemcpyAsync(R, rhs, tot * sizeof(double), cudaMemcpyDeviceToDevice, c.s), "copy r");
+  }
+  LA_TRY(la_coldot(c, rhs, rhs, P.n, ncol, c.sc(SC_BN)));
+  LA_TRY(la_coldot(c, R, R, P.n, ncol, c.sc(SC_RR)));
+  LA_TRY(la_fitc_solve(c, ncol, R, Z));
+  LA_TRY(la_coldot(c, R, Z, P.n, ncol, c.sc(SC_RZ)));
+  VIF_CUDA(h, cudaMemcpyAsync(Pv, Z, tot * sizeof(double), cudaMemcpyDeviceToDevice, c.s), "copy p");
+  std::vector<double> bn(ncol), rr(ncol);
+  VIF_CUDA(h, cudaMemcpyAsync(bn.data(), c.sc(SC_BN), ncol * sizeof(double), cudaMemcpyDeviceToHost, c.s), "bn");
+  VIF_CUDA(h, cudaMemcpyAsync(rr.data(), c.sc(SC_RR), ncol * sizeof(double), cudaMemcpyDeviceToHost, c.s), "rr");
+  VIF_CUDA(h, cudaStreamSynchronize(c.s), "sync");
+  std::vector<int> active(ncol);
+  iters.assign(ncol, 0);
+  int nact = 0;
+  for (int k = 0; k < ncol; ++k) {
+    active[k] = bn[k] > 0.0 && sqrt(rr[k]) > tol * sqrt(bn[k]) && max_it > 0;
+    nact += active[k];
+  }
+  VIF_CUDA(h, cudaMemcpyAsync(c.i(L_ACTIVE), active.data(), ncol * sizeof(int), cudaMemcpyHostToDevice, c.s), "active");
+  for (int it = 0; it < max_it && nact > 0; ++it) {
+    LA_TRY(la_sigma(c, ncol, Pv, Q, winv));
+    LA_TRY(la_coldot(c, Pv, Q, P.n, ncol, c.sc(SC_PQ)));
+    VIF_CUDA(h, launch_la_cg_alpha(c.sc(SC_RZ), c.sc(SC_PQ), c.i(L_ACTIVE), ncol, c.sc(SC_ALPHA),
+                                   record ? c.d(L_HA) + (size_t)it * ncol : nullptr, c.s),
+             "alpha");
+    VIF_CUDA(h, launch_la_cg_xr(c.sc(SC_ALPHA), Pv, Q, P.n, ncol, x, R, c.s), "x, r");
+    LA_TRY(la_coldot(c, R, R, P.n, ncol, c.sc(SC_RR)));
+    VIF_CUDA(h, cudaMemcpyAsync(rr.data(), c.sc(SC_RR), ncol * sizeof(double), cudaMemcpyDeviceToHost, c.s), "rr");
+    VIF_CUDA(h, cudaStreamSynchronize(c.s), "sync");
+    bool changed = false;
+    for (int k = 0; k < ncol; ++k) {
+      if (!active[k]) continue;
+      if (!(sqrt(rr[k]) > tol * sqrt(bn[k])) || it + 1 == max_it) {
+        active[k] = 0;
+        iters[k] = it + 1;
+        --nact;
+        changed = true;
+      }
+    }
+    if (nact == 0) break;
+    if (changed)
+      VIF_CUDA(h, cudaMemcpyAsync(c.i(L_ACTIVE), active.data(), ncol * sizeof(int), cudaMemcpyHostToDevice, c.s),
+               "active");
+    LA_TRY(la_fitc_solve(c, ncol, R, Z));
+    LA_TRY(la_coldot(c, R, Z, P.n, ncol, c.sc(SC_RZN)));
+    VIF_CUDA(h, launch_la_cg_beta(c.sc(SC_RZN), c.sc(SC_RZ), c.i(L_ACTIVE), ncol, c.sc(SC_BETA),
+                                  record ? c.d(L_HB) + (size_t)it * ncol : nullptr, c.s),
+             "beta");
+    VIF_CUDA(h, launch_la_cg_p(c.sc(SC_BETA), c.i(L_ACTIVE), Z, P.n, ncol, Pv, c.s), "p");
+  }
+  return VIF_OK;
 }
 
 }  // namespace
@@ -612,6 +836,7 @@ int vif_factor(void* handle, const vif_theta* theta, double* B_out, double* D_ou
   }
   DevStatus* st = h->buf<DevStatus>(B_STATUS);
   int64_t nl = 0;
+  ++h->fgen;
   for (int k = 0; k < S_COUNT; ++k) h->ev_used[k] = false;
   VIF_CUDA(h, launch_reset_status(st, s), "reset status");
   ++nl;
@@ -1130,6 +1355,7 @@ int vif_neighbors(void* handle, const vif_theta* theta, int32_t mv, int32_t* nbr
   std::string err;
   if (!make_params(h, theta, p, err)) return fail(h, VIF_ERR_INVALID_ARG, err);
   cudaStream_t s = h->stream;
+  ++h->fgen;  // reuses the factor's buffers: a prepared Laplace workspace is stale afterwards
   {
     int r = apply_pending(h);
     if (r != VIF_OK) return r;
@@ -1160,6 +1386,214 @@ int vif_neighbors(void* handle, const vif_theta* theta, int32_t mv, int32_t* nbr
   VIF_CUDA(h, cudaMemcpyAsync(&hs, st, sizeof(hs), cudaMemcpyDeviceToHost, s), "status copy");
   VIF_CUDA(h, cudaStreamSynchronize(s), "sync");
   if (hs.km_fail) return fail(h, VIF_ERR_NOT_PD, "Cholesky of K(Z,Z) + jitter failed");
+  return VIF_OK;
+}
+
+// ---------------------------------------------------------------- VIF-Laplace
+int vif_la_workspace_bytes(const vif_dims* dims, int32_t nprobe, int32_t max_cg, size_t* bytes) {
+  Plan P;
+  std::string err;
+  if (!bytes) return fail(nullptr, VIF_ERR_INVALID_ARG, "bytes is NULL");
+  if (nprobe < 0 || nprobe > kLaCols) return fail(nullptr, VIF_ERR_INVALID_ARG, "nprobe must be in [0, 64]");
+  if (max_cg < 1) return fail(nullptr, VIF_ERR_INVALID_ARG, "max_cg must be >= 1");
+  if (!make_plan(dims, true, P, err)) return fail(nullptr, VIF_ERR_INVALID_ARG, err);
+  *bytes = make_la_layout(P, nprobe, max_cg).total;
+  return VIF_OK;
+}
+
+int vif_la_prepare(void* handle, const vif_theta* theta, int32_t nprobe, int32_t max_cg, void* ws, size_t ws_bytes) {
+  Handle* h = reinterpret_cast<Handle*>(handle);
+  if (!h) return fail(nullptr, VIF_ERR_INVALID_ARG, "handle is NULL");
+  const Plan& P = h->P;
+  if (P.world != 1) return fail(h, VIF_ERR_INVALID_ARG, "vif_la_prepare: single-rank handles only in this version");
+  if (nprobe < 0 || nprobe > kLaCols) return fail(h, VIF_ERR_INVALID_ARG, "nprobe must be in [0, 64]");
+  if (max_cg < 1) return fail(h, VIF_ERR_INVALID_ARG, "max_cg must be >= 1");
+  if (!theta) return fail(h, VIF_ERR_INVALID_ARG, "theta is NULL");
+  const LaLayout LL = make_la_layout(P, nprobe, max_cg);
+  if (!ws || ws_bytes < LL.total) {
+    char msg[128];
+    snprintf(msg, sizeof msg, "Laplace workspace too small: need %zu bytes", LL.total);
+    return fail(h, VIF_ERR_NO_MEMORY, msg);
+  }
+  h->la_gen = ~0ull;
+  h->la_nprobe = nprobe;
+  h->la_maxcg = max_cg;
+  h->la_sigma2 = theta->sigma2;
+  LaCtx c = la_ctx(h, ws);
+  // the latent process has no error variance: the VIF factor at nugget 0
+  vif_theta th0 = *theta;
+  th0.nugget = 0.0;
+  int r = vif_factor(handle, &th0, P.mv > 0 ? c.d(L_B) : nullptr, c.d(L_D));
+  if (r != VIF_OK) return r;
+  cudaStream_t s = h->stream;
+  // M_w = I + W_U^T W_U of the latent factor: the full L_M^{-1} for the quadratic term b^T Sigma_dagger^{-1} b
+  VIF_CUDA(h, cudaMemcpyAsync(c.d(L_GM), h->buf<double>(B_G), c.L.size[L_GM], cudaMemcpyDeviceToDevice, s), "copy G");
+  vif_terms t;
+  r = vif_nll(handle, &t);
+  if (r != VIF_OK) return r;
+  VIF_CUDA(h, cudaMemsetAsync(c.base + c.L.off[L_TICKET], 0, c.L.size[L_TICKET], s), "memset ticket");
+  if (P.m > 0) {
+    VIF_CUDA(h, cudaMemsetAsync(c.d(L_LMINV), 0, c.L.size[L_LMINV], s), "memset");
+    VIF_CUDA(h, launch_chol_inv(c.d(L_GM), P.m, P.ld, 1.0, c.d(L_LMINV), P.mk, P.mk, 1, c.d(L_TSCR), c.fitc_fail(),
+                                h->num_sms, s),
+             "chol M (full inverse)");
+  }
+  if (P.mk > 0) VIF_CUDA(h, launch_la_rownorm2(c.U(), P.ld, P.mk, P.n, c.d(L_UN2), s), "||u_i||^2");
+  else VIF_CUDA(h, cudaMemsetAsync(c.d(L_UN2), 0, c.L.size[L_UN2], s), "memset");
+  VIF_CUDA(h, launch_la_transpose_struct(c.nbr(), P.n, P.mv, c.i(L_CNT), c.i(L_CUR), c.i(L_TPTR), c.i(L_TPOS), s),
+           "B^T structure");
+  VIF_CUDA(h, cudaMemsetAsync(c.i(L_FLAGS), 0, c.L.size[L_FLAGS], s), "memset flags");
+  int ff = 0;
+  VIF_CUDA(h, cudaMemcpyAsync(&ff, c.fitc_fail(), sizeof(int), cudaMemcpyDeviceToHost, s), "status");
+  VIF_CUDA(h, cudaStreamSynchronize(s), "sync");
+  if (ff) return fail(h, VIF_ERR_NOT_PD, "Cholesky of M (latent factor) failed");
+  h->la_epoch = 0;
+  h->la_ws = ws;
+  h->la_gen = h->fgen;
+  return VIF_OK;
+}
+
+static int la_check(Handle* h, void* ws) {
+  if (h->la_gen != h->fgen || h->la_ws != ws)
+    return fail(h, VIF_ERR_STATE, "Laplace workspace not prepared for the current factor (call vif_la_prepare)");
+  return VIF_OK;
+}
+
+int vif_la_apply(void* handle, void* ws, int32_t op, int32_t ncol, const double* v, const double* winv, double* out) {
+  Handle* h = reinterpret_cast<Handle*>(handle);
+  if (!h) return fail(nullptr, VIF_ERR_INVALID_ARG, "handle is NULL");
+  LA_TRY(la_check(h, ws));
+  const Plan& P = h->P;
+  if (ncol < 1 || ncol > (h->la_nprobe > 1 ? h->la_nprobe : 1) || !v || !out)
+    return fail(h, VIF_ERR_INVALID_ARG, "vif_la_apply: bad arguments");
+  if ((op == VIF_LA_FITC_SOLVE || op == VIF_LA_A) && !winv)
+    return fail(h, VIF_ERR_INVALID_ARG, "vif_la_apply: winv is required for this operator");
+  LaCtx c = la_ctx(h, ws);
+  switch (op) {
+    case VIF_LA_SIGMA: LA_TRY(la_sigma(c, ncol, v, out, nullptr)); break;
+    case VIF_LA_A: LA_TRY(la_sigma(c, ncol, v, out, winv)); break;
+    case VIF_LA_BINV:
+      VIF_CUDA(h, launch_la_trsv_fwd(c.nbr(), c.d(L_B), P.mv, P.n, ncol, v, nullptr, out, nullptr, nullptr, nullptr,
+                                     c.i(L_FLAGS), ++h->la_epoch, c.ticket(), c.s),
+               "B^-1");
+      break;
+    case VIF_LA_BTINV:
+      VIF_CUDA(h, launch_la_trsv_bwd(c.i(L_TPTR), c.i(L_TPOS), c.d(L_B), P.mv, P.n, ncol, v, out, c.i(L_FLAGS),
+                                     ++h->la_epoch, c.ticket(), c.s),
+               "B^-T");
+      break;
+    case VIF_LA_FITC_SOLVE:
+      LA_TRY(la_fitc_build(c, winv));
+      LA_TRY(la_fitc_solve(c, ncol, v, out));
+      break;
+    default: return fail(h, VIF_ERR_INVALID_ARG, "vif_la_apply: unknown operator");
+  }
+  VIF_CUDA(h, cudaStreamSynchronize(c.s), "sync");
+  int ff = 0;
+  VIF_CUDA(h, cudaMemcpy(&ff, c.fitc_fail(), sizeof(int), cudaMemcpyDeviceToHost), "status");
+  if (ff) return fail(h, VIF_ERR_NOT_PD, "FITC: Cholesky of M_V failed");
+  return VIF_OK;
+}
+
+int vif_la_nll(void* handle, void* ws, const double* y, const vif_la_opts* opts, const double* eps1,
+               const double* eps2, double* b_mode, vif_la_terms* out) {
+  Handle* h = reinterpret_cast<Handle*>(handle);
+  if (!h) return fail(nullptr, VIF_ERR_INVALID_ARG, "handle is NULL");
+  LA_TRY(la_check(h, ws));
+  const Plan& P = h->P;
+  if (!y || !opts || !out) return fail(h, VIF_ERR_INVALID_ARG, "vif_la_nll: NULL argument");
+  const int ell = opts->nprobe;
+  if (ell < 0 || ell > h->la_nprobe) return fail(h, VIF_ERR_INVALID_ARG, "nprobe exceeds the prepared workspace");
+  if (ell > 0 && ((P.m > 0 && !eps1) || !eps2)) return fail(h, VIF_ERR_INVALID_ARG, "probe draws are NULL");
+  if (opts->max_newton < 1 || opts->max_cg < 1 || opts->max_cg > h->la_maxcg)
+    return fail(h, VIF_ERR_INVALID_ARG, "max_newton >= 1 and 1 <= max_cg <= the prepared max_cg");
+  LaCtx c = la_ctx(h, ws);
+  cudaStream_t s = c.s;
+  const int64_t n = P.n;
+  double* fin = c.sc(SC_MISC);  // fin[0..5] as la_finish_kernel, fin[7] = b.a
+  double* bm = c.d(L_BM);
+  VIF_CUDA(h, cudaMemsetAsync(bm, 0, n * sizeof(double), s), "memset b");
+  VIF_CUDA(h, cudaMemsetAsync(c.fitc_fail(), 0, sizeof(int), s), "memset");
+  // Newton's method for the mode through (pcls2), readings l3 / l4
+  double psi_old = 0.0;
+  int it = 0, cg_total = 0;
+  std::vector<int> iters;
+  for (it = 1; it <= opts->max_newton; ++it) {
+    VIF_CUDA(h, launch_la_newton_prep(y, bm, n, c.d(L_W), c.d(L_WINV), c.d(L_V), c.d(L_X), s), "Newton prep");
+    LA_TRY(la_sigma(c, 1, c.d(L_V), c.d(L_RHS), nullptr));
+    LA_TRY(la_fitc_build(c, c.d(L_WINV)));
+    LA_TRY(la_pcg(c, 1, c.d(L_RHS), c.d(L_X), true, opts->cg_tol, opts->max_cg, c.d(L_WINV), false, iters));
+    cg_total += iters[0];
+    VIF_CUDA(h, launch_la_newton_update(c.d(L_X), c.d(L_V), c.d(L_WINV), n, bm, c.d(L_A), s), "Newton update");
+    VIF_CUDA(h, launch_la_reduce(1, y, bm, n, 1, c.d(L_RPART), fin + 0, s), "log p");
+    LA_TRY(la_coldot(c, bm, c.d(L_A), n, 1, fin + 7));
+    double hv[8];
+    VIF_CUDA(h, cudaMemcpyAsync(hv, fin, sizeof(hv), cudaMemcpyDeviceToHost, s), "psi");
+    VIF_CUDA(h, cudaStreamSynchronize(s), "sync");
+    const double psi = hv[0] - 0.5 * hv[7];
+    if (!isfinite(psi)) return fail(h, VIF_ERR_NOT_PD, "Laplace: Newton iterate is not finite");
+    if (it > 1 && fabs(psi - psi_old) <= opts->newton_tol * fabs(psi_old)) break;
+    psi_old = psi;
+  }
+  if (it > opts->max_newton) it = opts->max_newton;
+  // b~^T Sigma_dagger^{-1} b~ = ||D^{-1/2} B b||^2 - ||L_M^{-1} W_U^T D^{-1/2} B b||^2 (Woodbury; l5)
+  double* sv = c.d(L_T1);
+  VIF_CUDA(h, launch_la_bapply(c.nbr(), c.d(L_B), P.mv, n, c.d(L_D), bm, sv, s), "D^-1/2 B b");
+  LA_TRY(la_coldot(c, sv, sv, n, 1, fin + 1));
+  if (P.mk > 0) {
+    VIF_CUDA(h, launch_la_tsgemm(h->buf<double>(B_W), P.ld, P.mk, n, sv, 1, h->ord(0), nullptr, c.d(L_TSPART),
+                                 c.d(L_CT), 1.0, s),
+             "W_U^T s");
+    VIF_CUDA(h, launch_gemm_tn(c.d(L_CT), P.mk, 1, c.d(L_LMINV), P.mk, P.mk, P.mk, 0, c.d(L_CT2), P.mk, 1.0, 0, s),
+             "L_M^-1 c");
+    LA_TRY(la_coldot(c, c.d(L_CT2), c.d(L_CT2), P.mk, 1, fin + 2));
+  } else {
+    VIF_CUDA(h, cudaMemsetAsync(fin + 2, 0, sizeof(double), s), "memset");
+  }
+  int slq_max = 0;
+  double slq_mean = 0.0;
+  if (ell > 0) {
+    // log det(Sigma_dagger W + I) by SLQ (slq_v2), FITC-preconditioned, z_i = D_V^{1/2} eps2 + U eps1
+    VIF_CUDA(h, launch_la_newton_prep(y, bm, n, c.d(L_W), c.d(L_WINV), c.d(L_V), nullptr, s), "W at the mode");
+    LA_TRY(la_fitc_build(c, c.d(L_WINV)));
+    VIF_CUDA(h, launch_la_reduce(2, c.d(L_W), nullptr, n, 1, c.d(L_RPART), fin + 3, s), "log det W");
+    VIF_CUDA(h, launch_la_reduce(2, c.d(L_DV), nullptr, n, 1, c.d(L_RPART), fin + 4, s), "log det D_V");
+    VIF_CUDA(h, launch_la_rowscale(eps2, c.d(L_DV), 1, n, ell, c.d(L_RHS), s), "D_V^1/2 eps2");
+    if (P.mk > 0) {
+      VIF_CUDA(h, cudaMemsetAsync(c.d(L_E1T), 0, (size_t)ell * P.mk * sizeof(double), s), "memset");
+      VIF_CUDA(h, launch_la_transpose(eps1, P.m, ell, ell, c.d(L_E1T), P.mk, s), "eps1^T");
+      VIF_CUDA(h, launch_gemm_tn(c.U(), P.ld, n, c.d(L_E1T), P.mk, ell, P.mk, 0, c.d(L_RHS), ell, 1.0, 1, s),
+               "U eps1");
+    }
+    LA_TRY(la_pcg(c, ell, c.d(L_RHS), c.d(L_X), false, opts->slq_tol, opts->max_cg, c.d(L_WINV), true, iters));
+    for (int k = 0; k < ell; ++k) {
+      slq_max = iters[k] > slq_max ? iters[k] : slq_max;
+      slq_mean += iters[k] / (double)ell;
+    }
+    VIF_CUDA(h, cudaMemcpyAsync(c.i(L_ITERS), iters.data(), ell * sizeof(int), cudaMemcpyHostToDevice, s), "iters");
+    VIF_CUDA(h, launch_la_slq(c.d(L_HA), c.d(L_HB), c.i(L_ITERS), ell, h->la_maxcg, c.d(L_SLQS), c.sc(SC_SLQ), s),
+             "SLQ quadrature");
+  } else {
+    VIF_CUDA(h, cudaMemsetAsync(fin + 3, 0, 3 * sizeof(double), s), "memset");
+  }
+  VIF_CUDA(h, launch_la_finish(fin, c.sc(SC_SLQ), n, ell, c.sc(SC_OUT), s), "finish");
+  if (b_mode) VIF_CUDA(h, cudaMemcpyAsync(b_mode, bm, n * sizeof(double), cudaMemcpyDefault, s), "b copy");
+  double o[6];
+  int ff = 0;
+  VIF_CUDA(h, cudaMemcpyAsync(o, c.sc(SC_OUT), sizeof(o), cudaMemcpyDeviceToHost, s), "terms");
+  VIF_CUDA(h, cudaMemcpyAsync(&ff, c.fitc_fail(), sizeof(int), cudaMemcpyDeviceToHost, s), "status");
+  VIF_CUDA(h, cudaStreamSynchronize(s), "sync");
+  out->nll = ell > 0 ? o[0] : NAN;
+  out->neg_loglik = o[1];
+  out->quad = o[2];
+  out->logdet = ell > 0 ? o[3] : NAN;
+  out->logdet_W = ell > 0 ? o[4] : NAN;
+  out->logdet_P = ell > 0 ? o[5] : NAN;
+  out->newton_iters = it;
+  out->cg_iters = cg_total;
+  out->slq_iters_max = slq_max;
+  out->slq_iters_mean = slq_mean;
+  if (ff) return fail(h, VIF_ERR_NOT_PD, "FITC: Cholesky of M_V failed");
   return VIF_OK;
 }
 

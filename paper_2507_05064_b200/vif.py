@@ -44,6 +44,18 @@ class _Theta(ctypes.Structure):
                 ("jitter", ctypes.c_double)]
 
 
+class _LaOpts(ctypes.Structure):
+    _fields_ = [("max_newton", ctypes.c_int32), ("newton_tol", ctypes.c_double), ("max_cg", ctypes.c_int32),
+                ("cg_tol", ctypes.c_double), ("nprobe", ctypes.c_int32), ("slq_tol", ctypes.c_double)]
+
+
+class _LaTerms(ctypes.Structure):
+    _fields_ = [("nll", ctypes.c_double), ("neg_loglik", ctypes.c_double), ("quad", ctypes.c_double),
+                ("logdet", ctypes.c_double), ("logdet_W", ctypes.c_double), ("logdet_P", ctypes.c_double),
+                ("newton_iters", ctypes.c_int32), ("cg_iters", ctypes.c_int32), ("slq_iters_max", ctypes.c_int32),
+                ("slq_iters_mean", ctypes.c_double)]
+
+
 class _Terms(ctypes.Structure):
     _fields_ = [("nll", ctypes.c_double), ("logdet_D", ctypes.c_double), ("logdet_M", ctypes.c_double),
                 ("quad", ctypes.c_double), ("bad_row", ctypes.c_int64)]
@@ -83,10 +95,15 @@ def load_library():
         lib.vif_predict.argtypes = [P, ctypes.POINTER(_Theta), i64, P, P, P, sz, P, P, P, P]
         lib.vif_neighbors.argtypes = [P, ctypes.POINTER(_Theta), i32, P]
         lib.vif_stage_data.argtypes = [P, P, P, P, P]
+        lib.vif_la_workspace_bytes.argtypes = [ctypes.POINTER(_Dims), i32, i32, ctypes.POINTER(sz)]
+        lib.vif_la_prepare.argtypes = [P, ctypes.POINTER(_Theta), i32, i32, P, sz]
+        lib.vif_la_apply.argtypes = [P, P, i32, i32, P, P, P]
+        lib.vif_la_nll.argtypes = [P, P, P, ctypes.POINTER(_LaOpts), P, P, P, ctypes.POINTER(_LaTerms)]
         for f in ("vif_nccl_unique_id", "vif_workspace_bytes", "vif_partition", "vif_create", "vif_set_data",
                   "vif_factor", "vif_nll", "vif_copy_U", "vif_launch_count", "vif_profile", "vif_stage_times",
                   "vif_grad_workspace_bytes", "vif_grad", "vif_predict_workspace_bytes", "vif_predict",
-                  "vif_neighbors", "vif_stage_data"):
+                  "vif_neighbors", "vif_stage_data", "vif_la_workspace_bytes", "vif_la_prepare", "vif_la_apply",
+                  "vif_la_nll"):
             getattr(lib, f).restype = ctypes.c_int
         _lib = lib
     return _lib
@@ -95,7 +112,9 @@ def load_library():
 EXPORTED = ("vif_nccl_unique_id", "vif_workspace_bytes", "vif_partition", "vif_create", "vif_set_data",
             "vif_factor", "vif_nll", "vif_copy_U", "vif_launch_count", "vif_profile", "vif_stage_times",
             "vif_stage_name", "vif_last_error", "vif_destroy", "vif_grad_workspace_bytes", "vif_grad",
-            "vif_predict_workspace_bytes", "vif_predict", "vif_neighbors", "vif_stage_data")
+            "vif_predict_workspace_bytes", "vif_predict", "vif_neighbors", "vif_stage_data",
+            "vif_la_workspace_bytes", "vif_la_prepare", "vif_la_apply", "vif_la_nll")
+LA_OPS = {"sigma": 0, "A": 1, "binv": 2, "btinv": 3, "fitc_solve": 4}
 NUM_STAGES = 8
 
 
@@ -262,6 +281,57 @@ def vif_neighbors(h, theta: Theta, mv: int, out: torch.Tensor):
     _check(load_library().vif_neighbors(h, ctypes.byref(th), int(mv), _ptr(out)), h)
 
 
+@dataclass
+class LaOpts:
+    """Options of the VIF-Laplace path (readings l3, l4 of DESIGN.md section 13)."""
+    max_newton: int = 50
+    newton_tol: float = 1e-10
+    max_cg: int = 1000
+    cg_tol: float = 1e-10
+    nprobe: int = 0
+    slq_tol: float = 1e-10
+
+
+@dataclass
+class LaTerms:
+    nll: float
+    neg_loglik: float
+    quad: float
+    logdet: float
+    logdet_W: float
+    logdet_P: float
+    newton_iters: int
+    cg_iters: int
+    slq_iters_max: int
+    slq_iters_mean: float
+
+
+def vif_la_workspace_bytes(n, d, m, mv, nprobe, max_cg, rank=0, world=1) -> int:
+    b = ctypes.c_size_t(0)
+    _check(load_library().vif_la_workspace_bytes(ctypes.byref(_dims(n, d, m, mv, rank, world)), int(nprobe),
+                                                 int(max_cg), ctypes.byref(b)))
+    return b.value
+
+
+def vif_la_prepare(h, theta: Theta, nprobe: int, max_cg: int, ws: torch.Tensor):
+    th, keep = theta.to_c()
+    _check(load_library().vif_la_prepare(h, ctypes.byref(th), int(nprobe), int(max_cg), _ptr(ws), ws.numel()), h)
+
+
+def vif_la_apply(h, ws: torch.Tensor, op: str, v: torch.Tensor, out: torch.Tensor, winv=None):
+    ncol = 1 if v.dim() == 1 else v.shape[1]
+    _check(load_library().vif_la_apply(h, _ptr(ws), LA_OPS[op], ncol, _ptr(v), _ptr(winv), _ptr(out)), h)
+
+
+def vif_la_nll(h, ws: torch.Tensor, y: torch.Tensor, opts: LaOpts, eps1=None, eps2=None, b_mode=None) -> LaTerms:
+    o = _LaOpts(opts.max_newton, opts.newton_tol, opts.max_cg, opts.cg_tol, opts.nprobe, opts.slq_tol)
+    t = _LaTerms()
+    _check(load_library().vif_la_nll(h, _ptr(ws), _ptr(y), ctypes.byref(o), _ptr(eps1), _ptr(eps2), _ptr(b_mode),
+                                     ctypes.byref(t)), h)
+    return LaTerms(t.nll, t.neg_loglik, t.quad, t.logdet, t.logdet_W, t.logdet_P, t.newton_iters, t.cg_iters,
+                   t.slq_iters_max, t.slq_iters_mean)
+
+
 def vif_copy_U(h, out: torch.Tensor):
     _check(load_library().vif_copy_U(h, _ptr(out)), h)
 
@@ -368,6 +438,32 @@ class VifModel:
         out = torch.empty((self.n, mv), dtype=torch.int32, device=self.device)
         vif_neighbors(self.handle, theta, mv, out)
         return out
+
+    # ---- VIF-Laplace (Bernoulli-logit latent GP)
+    def la_prepare(self, theta: Theta, nprobe: int = 0, max_cg: int = 1000):
+        """Latent factor at theta (nugget forced to 0) + transposed structure into the Laplace workspace."""
+        nbytes = vif_la_workspace_bytes(self.n, self.d, self.m, self.mv, nprobe, max_cg, self.rank, self.world)
+        ws = getattr(self, "la_workspace", None)
+        if ws is None or ws.numel() < nbytes:
+            ws = self.la_workspace = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
+        vif_la_prepare(self.handle, theta, nprobe, max_cg, ws)
+
+    def la_apply(self, op: str, v, winv=None) -> torch.Tensor:
+        """Sigma_dagger v ("sigma"), (W^{-1} + Sigma_dagger) v ("A"), B^{-1} v, B^{-T} v, P^{-1} v."""
+        v = _as_input(v, torch.float64, self.device)
+        winv = _as_input(winv, torch.float64, self.device)
+        out = torch.empty_like(v)
+        vif_la_apply(self.handle, self.la_workspace, op, v, out, winv)
+        return out
+
+    def la_nll(self, y, opts: LaOpts, eps1=None, eps2=None):
+        """(LaTerms, mode b~ as a device tensor) for labels y in {0, 1}."""
+        y = _as_input(y, torch.float64, self.device)
+        eps1 = _as_input(eps1, torch.float64, self.device)
+        eps2 = _as_input(eps2, torch.float64, self.device)
+        b = torch.empty(self.n, dtype=torch.float64, device=self.device)
+        t = vif_la_nll(self.handle, self.la_workspace, y, opts, eps1, eps2, b)
+        return t, b
 
     def U(self) -> torch.Tensor:
         out = torch.empty((self.n, self.m), dtype=torch.float64, device=self.device)
