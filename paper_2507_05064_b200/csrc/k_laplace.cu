@@ -4,8 +4,8 @@
 // point index (the Vecchia order).  The latent factor B (unit lower triangular, B[i, N(i)] = -A_i),
 // D and the whitened U come from the VIF factor with the error variance removed.
 //
-//   la_trsv_fwd   x = B^{-1} (s o v)        sync-free forward substitution: a warp takes the next
-//                                           row from a ticket counter, waits (acquire) on the
+//   la_trsv_fwd   x = B^{-1} (s o v)        sync-free forward substitution: warp w takes rows
+//                                           w, w + W, ... in order, waits (flag polls) on the
 //                                           ready flags of its m_v neighbours, gathers them, and
 //                                           publishes its row with a release store of the flag;
 //   la_trsv_bwd   y = B^{-T} u              the same on the transposed structure (children lists),
@@ -15,20 +15,33 @@
 //   la_coldot ... per-column dot products (two-stage, fixed order), CG vector updates, FITC rows,
 //                 the Newton step and the SLQ quadrature e_1^T log(T) e_1 (implicit QL on T).
 //
-// Tickets make the schedule deadlock-free: a warp only waits on rows with smaller tickets, which
-// were claimed by warps that are already running.
+// Static row assignment over resident warps makes the schedule deadlock-free: the smallest
+// unfinished row (in solve order) always has its dependencies done.
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdio.h>
+#include <stdlib.h>
+
+#include <algorithm>
+#include <vector>
 
 #include "kernels.h"
+
+namespace cg = cooperative_groups;
 
 namespace vif {
 
 namespace {
 
-__device__ __forceinline__ int ld_acquire(const int* p) {
+// Flag polls are relaxed gpu-scope loads: ld.acquire.gpu compiles to LDG.STRONG + CCTL.IVALL, an L1
+// invalidation per poll (ncu: 426M of them in one multi-column solve, 20x slower).  The data a flag
+// guards is read with __ldcg (LDG.STRONG.GPU, L2) only after the poll loop has observed the flag: the
+// load's issue is control-dependent on the flag value, and the writer's st.release.gpu made the row
+// visible at L2 before the flag.
+__device__ __forceinline__ int ld_relaxed(const int* p) {
   int v;
-  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
 __device__ __forceinline__ void st_release(int* p, int v) {
@@ -98,35 +111,88 @@ __global__ void la_sort_kernel(int64_t n, const int* __restrict__ ptr, int* __re
 }
 
 // ------------------------------------------------------------------ sync-free triangular solves
+// Warp w of W resident warps solves rows w, w + W, w + 2W, ... in that order (static assignment: the
+// smallest unfinished row always has its dependencies done, so every resident warp makes progress).
+// A row waits (relaxed polls with back-off, see ld_relaxed) on the ready flags of the rows it reads, reads them from L2
+// (__ldcg: L1 is not coherent), and publishes its own row with a release store of its flag.
+__device__ __forceinline__ void la_wait(const int* f, int epoch) {
+  if (ld_relaxed(f) == epoch) return;
+  unsigned ns = 8;
+  while (ld_relaxed(f) != epoch) {
+    __nanosleep(ns);
+    ns = ns < 256 ? 2 * ns : 256;
+  }
+}
+
+// acc{0,1} += sum_{k in [k0, k1)} val[k] * x[col[k], c{0,1}] (col < 0 skipped): lane = column; the
+// entry (col, val) is a broadcast load (every lane reads the same address).  The body is branch-free
+// (a skipped entry reads row 0 with weight 0, a lane past ncol reads column ncol - 1 and discards
+// it) so that the unrolled loop keeps 16 gathers per column in flight.
+__device__ __forceinline__ void la_gather_cols(const double* x, int ncol, int c0, const int32_t* __restrict__ col,
+                                               const double* __restrict__ val, int k0, int k1, double& acc0,
+                                               double& acc1) {
+  const int c1 = c0 + 32;
+  const int r0 = c0 < ncol ? c0 : ncol - 1, r1 = c1 < ncol ? c1 : ncol - 1;
+#pragma unroll 16
+  for (int k = k0; k < k1; ++k) {
+    const int j = col[k];
+    const double b = j >= 0 ? val[k] : 0.0;
+    const double* xr = x + (int64_t)(j >= 0 ? j : 0) * ncol;
+    acc0 = fma(b, __ldcg(xr + r0), acc0);
+    acc1 = fma(b, __ldcg(xr + r1), acc1);
+  }
+}
+
+// The level-scheduled kernels read rows written in earlier levels with plain (weak) loads: grid.sync()
+// orders them (and invalidates L1), and weak loads, unlike the strong __ldcg ones, may be reordered, so
+// the unrolled loop below issues all of a chunk's gathers before the first FMA needs one.
+// acc{0,1} += sum over the cnt (<= 32) entries (jl, bl) held by lanes 0..cnt-1 of b * x[j, c{0,1}]
+__device__ __forceinline__ void la_gather_cols_weak(const double* x, int ncol, int c0, int jl, double bl, int cnt,
+                                                    double& acc0, double& acc1) {
+  const int c1 = c0 + 32;
+  const int r0 = c0 < ncol ? c0 : ncol - 1, r1 = c1 < ncol ? c1 : ncol - 1;
+  const bool ok = jl >= 0;  // selects, not branches: the shuffles below need a converged warp
+  jl = ok ? jl : 0;
+  bl = ok ? bl : 0.0;
+  __syncwarp();
+  double x0[32], x1[32], bb[32];
+#pragma unroll
+  for (int q = 0; q < 32; ++q) {
+    const int j = __shfl_sync(0xffffffffu, jl, q);
+    const double bq = __shfl_sync(0xffffffffu, bl, q);
+    bb[q] = q < cnt ? bq : 0.0;
+    const double* xr = x + (int64_t)j * ncol;
+    x0[q] = xr[r0];
+    x1[q] = xr[r1];
+  }
+#pragma unroll
+  for (int q = 0; q < 32; ++q) {
+    acc0 = fma(bb[q], x0[q], acc0);
+    acc1 = fma(bb[q], x1[q], acc1);
+  }
+}
+
 // x_i = s_i v_i - sum_p B[i,p] x_{N(i)_p}   (B x = s o v, B unit lower triangular)
 // optional out2_i = x_i + w2_i * v2_i (the W^{-1} p term of (W^{-1} + Sigma_dagger) p is added there)
+// ncol <= 64 (two columns per lane)
 __global__ void __launch_bounds__(LA_THREADS) la_trsv_fwd_kernel(
     const int32_t* __restrict__ nbr, const double* __restrict__ Bc, int mv, int64_t n, int ncol,
     const double* __restrict__ v, const double* __restrict__ s, double* x, const double* __restrict__ v2,
-    const double* __restrict__ w2, double* __restrict__ out2, int* flags, int epoch,
-    unsigned long long* ticket) {
+    const double* __restrict__ w2, double* __restrict__ out2, int* flags, int epoch) {
   const int lane = threadIdx.x & 31;
-  for (;;) {
-    unsigned long long t = 0;
-    if (lane == 0) t = atomicAdd(ticket, 1ull);
-    t = __shfl_sync(0xffffffffu, t, 0);
-    if ((int64_t)t >= n) break;
-    const int64_t i = (int64_t)t;
+  const int64_t nw = (int64_t)gridDim.x * LA_WARPS;
+  for (int64_t i = (int64_t)blockIdx.x * LA_WARPS + (threadIdx.x >> 5); i < n; i += nw) {
     const int32_t* nb = nbr + i * mv;
     const double* bi = Bc + i * mv;
-    for (int p = lane; p < mv; p += 32) {
-      const int j = nb[p];
-      if (j >= 0)
-        while (ld_acquire(flags + j) != epoch) {
-        }
-    }
-    __syncwarp();
     const double si = s ? s[i] : 1.0;
     if (ncol == 1) {
       double acc = 0.0;
       for (int p = lane; p < mv; p += 32) {
         const int j = nb[p];
-        if (j >= 0) acc = fma(bi[p], __ldcg(x + j), acc);
+        if (j >= 0) {
+          la_wait(flags + j, epoch);
+          acc = fma(bi[p], __ldcg(x + j), acc);
+        }
       }
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
@@ -134,65 +200,286 @@ __global__ void __launch_bounds__(LA_THREADS) la_trsv_fwd_kernel(
         const double xi = si * v[i] - acc;
         __stcg(x + i, xi);
         if (out2) out2[i] = xi + w2[i] * v2[i];
+        st_release(flags + i, epoch);  // orders lane 0's own store of x_i before the flag
       }
     } else {
-      for (int c = lane; c < ncol; c += 32) {
-        double acc = 0.0;
-        for (int p = 0; p < mv; ++p) {
-          const int j = nb[p];
-          if (j >= 0) acc = fma(bi[p], __ldcg(x + (int64_t)j * ncol + c), acc);
-        }
-        const double xi = si * v[i * ncol + c] - acc;
-        __stcg(x + i * ncol + c, xi);
-        if (out2) out2[i * ncol + c] = xi + w2[i] * v2[i * ncol + c];
+      double acc0 = 0.0, acc1 = 0.0;
+      for (int p = lane; p < mv; p += 32) {
+        const int j = nb[p];
+        if (j >= 0) la_wait(flags + j, epoch);
       }
+      __syncwarp();
+      la_gather_cols(x, ncol, lane, nb, bi, 0, mv, acc0, acc1);
+      const int c1 = lane + 32;
+      if (lane < ncol) {
+        const double xi = si * v[i * ncol + lane] - acc0;
+        __stcg(x + i * ncol + lane, xi);
+        if (out2) out2[i * ncol + lane] = xi + w2[i] * v2[i * ncol + lane];
+      }
+      if (c1 < ncol) {
+        const double xi = si * v[i * ncol + c1] - acc1;
+        __stcg(x + i * ncol + c1, xi);
+        if (out2) out2[i * ncol + c1] = xi + w2[i] * v2[i * ncol + c1];
+      }
+      // __syncwarp orders the other lanes' stores before lane 0's release store (bar.warp.sync carries
+      // memory ordering among the participating threads; release is cumulative)
+      __syncwarp();
+      if (lane == 0) st_release(flags + i, epoch);
     }
-    __threadfence();
-    __syncwarp();
-    if (lane == 0) st_release(flags + i, epoch);
   }
 }
 
-// y_j = u_j - sum_{(i,p): N(i)_p = j} B[i,p] y_i   (B^T y = u), rows in decreasing order
+// y_j = u_j - sum_{k in children(j)} tval[k] y_{trow[k]}   (B^T y = u; tval[k] = B[trow[k], p] with
+// N(trow[k])_p = j), rows in decreasing order
 __global__ void __launch_bounds__(LA_THREADS) la_trsv_bwd_kernel(
-    const int* __restrict__ tptr, const int* __restrict__ tpos, const double* __restrict__ Bc, int mv, int64_t n,
-    int ncol, const double* __restrict__ u, double* y, int* flags, int epoch, unsigned long long* ticket) {
+    const int* __restrict__ tptr, const int* __restrict__ trow, const double* __restrict__ tval, int64_t n,
+    int ncol, const double* __restrict__ u, double* y, int* flags, int epoch) {
   const int lane = threadIdx.x & 31;
-  for (;;) {
-    unsigned long long t = 0;
-    if (lane == 0) t = atomicAdd(ticket, 1ull);
-    t = __shfl_sync(0xffffffffu, t, 0);
-    if ((int64_t)t >= n) break;
-    const int64_t j = n - 1 - (int64_t)t;
+  const int64_t nw = (int64_t)gridDim.x * LA_WARPS;
+  for (int64_t t = (int64_t)blockIdx.x * LA_WARPS + (threadIdx.x >> 5); t < n; t += nw) {
+    const int64_t j = n - 1 - t;
     const int a = tptr[j], b = tptr[j + 1];
-    for (int k = a + lane; k < b; k += 32) {
-      const int i = tpos[k] / mv;
-      while (ld_acquire(flags + i) != epoch) {
-      }
-    }
-    __syncwarp();
     if (ncol == 1) {
       double acc = 0.0;
       for (int k = a + lane; k < b; k += 32) {
-        const int e = tpos[k];
-        acc = fma(Bc[e], __ldcg(y + e / mv), acc);
+        const int i = trow[k];
+        la_wait(flags + i, epoch);
+        acc = fma(tval[k], __ldcg(y + i), acc);
       }
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-      if (lane == 0) __stcg(y + j, u[j] - acc);
+      if (lane == 0) {
+        __stcg(y + j, u[j] - acc);
+        st_release(flags + j, epoch);
+      }
     } else {
-      for (int c = lane; c < ncol; c += 32) {
-        double acc = 0.0;
-        for (int k = a; k < b; ++k) {
-          const int e = tpos[k];
-          acc = fma(Bc[e], __ldcg(y + (int64_t)(e / mv) * ncol + c), acc);
-        }
-        __stcg(y + j * ncol + c, u[j * ncol + c] - acc);
+      double acc0 = 0.0, acc1 = 0.0;
+      for (int k = a + lane; k < b; k += 32) la_wait(flags + trow[k], epoch);
+      __syncwarp();
+      la_gather_cols(y, ncol, lane, trow, tval, a, b, acc0, acc1);
+      const int c1 = lane + 32;
+      if (lane < ncol) __stcg(y + j * ncol + lane, u[j * ncol + lane] - acc0);
+      if (c1 < ncol) __stcg(y + j * ncol + c1, u[j * ncol + c1] - acc1);
+      __syncwarp();
+      if (lane == 0) st_release(flags + j, epoch);
+    }
+  }
+}
+
+// transposed values: trow[k] = tpos[k] / mv, tval[k] = Bc[tpos[k]]
+__global__ void la_tvals_kernel(const int* __restrict__ tpos, int64_t nnz, int mv, const double* __restrict__ Bc,
+                                int* __restrict__ trow, double* __restrict__ tval) {
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < nnz; k += (int64_t)gridDim.x * blockDim.x) {
+    const int e = tpos[k];
+    trow[k] = e / mv;
+    tval[k] = Bc[e];
+  }
+}
+
+// ------------------------------------------------------------------ level-scheduled triangular solves
+// Levels of the dependency DAG (once per neighbour structure): forward lev_i = 1 + max_{j in N(i)} lev_j,
+// backward levb_j = 1 + max_{children i} levb_i, computed by the same sync-free scheme as above.
+__global__ void __launch_bounds__(LA_THREADS) la_level_fwd_kernel(const int32_t* __restrict__ nbr, int mv, int64_t n,
+                                                                  int* lev, int* flags, int epoch) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = (int64_t)gridDim.x * LA_WARPS;
+  for (int64_t i = (int64_t)blockIdx.x * LA_WARPS + (threadIdx.x >> 5); i < n; i += nw) {
+    int l = 0;
+    for (int p = lane; p < mv; p += 32) {
+      const int j = nbr[i * mv + p];
+      if (j >= 0) {
+        la_wait(flags + j, epoch);
+        l = max(l, __ldcg(lev + j) + 1);
       }
     }
-    __threadfence();
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) l = max(l, __shfl_xor_sync(0xffffffffu, l, o));
+    if (lane == 0) {
+      __stcg(lev + i, l);
+      st_release(flags + i, epoch);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(LA_THREADS) la_level_bwd_kernel(const int* __restrict__ tptr,
+                                                                  const int* __restrict__ trow, int64_t n, int* lev,
+                                                                  int* flags, int epoch) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = (int64_t)gridDim.x * LA_WARPS;
+  for (int64_t t = (int64_t)blockIdx.x * LA_WARPS + (threadIdx.x >> 5); t < n; t += nw) {
+    const int64_t j = n - 1 - t;
+    int l = 0;
+    for (int k = tptr[j] + lane; k < tptr[j + 1]; k += 32) {
+      const int i = trow[k];
+      la_wait(flags + i, epoch);
+      l = max(l, __ldcg(lev + i) + 1);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) l = max(l, __shfl_xor_sync(0xffffffffu, l, o));
+    if (lane == 0) {
+      __stcg(lev + j, l);
+      st_release(flags + j, epoch);
+    }
+  }
+}
+
+__global__ void la_max_kernel(const int* __restrict__ a, int64_t n, int* __restrict__ out) {
+  int m = 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    m = max(m, a[i]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(out, m);
+}
+
+// bucket rows by level: order[lptr[L] .. lptr[L+1]) = rows of level L (any order inside a level)
+__global__ void la_bucket_count_kernel(const int* __restrict__ key, int64_t n, int* __restrict__ cnt) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    atomicAdd(cnt + key[i], 1);
+}
+__global__ void la_bucket_fill_kernel(const int* __restrict__ key, int64_t n, const int* __restrict__ ptr,
+                                      int* __restrict__ cursor, int* __restrict__ order) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int L = key[i];
+    order[ptr[L] + atomicAdd(cursor + L, 1)] = (int)i;
+  }
+}
+
+// long rows (B^T rows of early points: up to hundreds of children): lanes over entries, 16 columns at
+// a time in registers, summed over the lanes through shared memory; out of line so that it does not
+// change the register allocation of the short-row path
+__device__ __noinline__ void la_long_row(const double* x, int ncol, const int32_t* __restrict__ ecol,
+                                         const double* __restrict__ eval, int k0, int k1, int lane,
+                                         double (*red)[17], double* colsum, double& acc0, double& acc1) {
+  for (int cb = 0; cb < ncol; cb += 16) {
+    double a16[16];
+#pragma unroll
+    for (int c = 0; c < 16; ++c) a16[c] = 0.0;
+    const int cm = ncol - cb < 16 ? ncol - cb : 16;
+    for (int k = k0 + lane; k < k1; k += 32) {
+      const int j = ecol[k];
+      const double b = j >= 0 ? eval[k] : 0.0;
+      const double* xr = x + (int64_t)(j >= 0 ? j : 0) * ncol + cb;
+#pragma unroll
+      for (int c = 0; c < 16; ++c) a16[c] = fma(b, xr[c < cm ? c : 0], a16[c]);
+    }
+#pragma unroll
+    for (int c = 0; c < 16; ++c) red[lane][c] = a16[c];
     __syncwarp();
-    if (lane == 0) st_release(flags + j, epoch);
+    if (lane < cm) {
+      double t = 0.0;
+      for (int l = 0; l < 32; ++l) t += red[l][lane];
+      colsum[cb + lane] = t;
+    }
+    __syncwarp();
+  }
+  acc0 = lane < ncol ? colsum[lane] : 0.0;
+  acc1 = lane + 32 < ncol ? colsum[lane + 32] : 0.0;
+  __syncwarp();
+}
+
+// Entries in level order, so that a row's entries are addressed by its level-sorted position q (no
+// dependent load through the row index): forward ecol/eval[q*mv + p] = nbr/B[order[q]*mv + p];
+// backward eptr2[q] = scan of children counts in order, ecol2/eval2 = trow/tval segments.
+__global__ void la_reorder_fwd_kernel(const int* __restrict__ order, const int32_t* __restrict__ nbr,
+                                      const double* __restrict__ Bc, int64_t n, int mv, int32_t* __restrict__ ecol,
+                                      double* __restrict__ eval) {
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n * mv; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t q = e / mv, p = e % mv;
+    const int64_t src = (int64_t)order[q] * mv + p;
+    ecol[e] = nbr[src];
+    eval[e] = Bc[src];
+  }
+}
+__global__ void la_seglen_kernel(const int* __restrict__ order, const int* __restrict__ tptr, int64_t n,
+                                 int* __restrict__ cnt) {
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < n; q += (int64_t)gridDim.x * blockDim.x) {
+    const int r = order[q];
+    cnt[q] = tptr[r + 1] - tptr[r];
+  }
+}
+__global__ void la_reorder_bwd_kernel(const int* __restrict__ order, const int* __restrict__ tptr,
+                                      const int* __restrict__ trow, const double* __restrict__ tval,
+                                      const int* __restrict__ eptr2, int64_t n, int32_t* __restrict__ ecol,
+                                      double* __restrict__ eval) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t q = (int64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5); q < n;
+       q += (int64_t)gridDim.x * (blockDim.x / 32)) {
+    const int r = order[q];
+    const int a = tptr[r], len = tptr[r + 1] - a, o = eptr2[q];
+    for (int k = lane; k < len; k += 32) {
+      ecol[o + k] = trow[a + k];
+      eval[o + k] = tval[a + k];
+    }
+  }
+}
+
+// One cooperative kernel per solve: level by level (grid.sync between levels), a warp per row.
+// Row r: out_r = s_r v_r - sum_k val[k] out[col[k]] over its entries k (forward: k = r*mv + p with
+// col = N(r)_p, val = B[r,p], entries with col < 0 skipped; backward: k in [tptr[r], tptr[r+1]),
+// col = trow, val = tval).  Reads of other rows go to L2 (__ldcg; rows written in earlier levels).
+template <bool FWD>
+__global__ void __launch_bounds__(LA_THREADS) la_trsv_lvl_kernel(
+    const int* __restrict__ order, const int* __restrict__ lptr, int nlev, const int32_t* __restrict__ ecol,
+    const double* __restrict__ eval, const int* __restrict__ eptr, int mv, int ncol, const double* __restrict__ v,
+    const double* __restrict__ s, double* x, const double* __restrict__ v2, const double* __restrict__ w2,
+    double* __restrict__ out2, unsigned long long* dbg) {
+  cg::grid_group grid = cg::this_grid();
+  __shared__ double sm_red[LA_WARPS][32][17];
+  __shared__ double sm_col[LA_WARPS][64];
+  const int lane = threadIdx.x & 31;
+  const int nw = gridDim.x * LA_WARPS;
+  const int w0 = blockIdx.x * LA_WARPS + (threadIdx.x >> 5);
+  for (int L = 0; L < nlev; ++L) {
+    const int a = lptr[L], b = lptr[L + 1];
+    for (int q = a + w0; q < b; q += nw) {
+      const int64_t r = order[q];
+      const int k0 = FWD ? q * mv : eptr[q];  // entries stored in level order (la_reorder_*)
+      const int k1 = FWD ? k0 + mv : eptr[q + 1];
+      const double sr = s ? s[r] : 1.0;
+      if (ncol == 1) {
+        double acc = 0.0;
+        for (int k = k0 + lane; k < k1; k += 32) {
+          const int j = ecol[k];
+          if (j >= 0) acc = fma(eval[k], x[j], acc);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (lane == 0) {
+          const double xr = sr * v[r] - acc;
+          __stcg(x + r, xr);
+          if (out2) out2[r] = xr + w2[r] * v2[r];
+        }
+      } else {
+        double acc0 = 0.0, acc1 = 0.0;
+        if (k1 - k0 <= 32) {
+          const int k = k0 + lane;
+          const int jl = k < k1 ? ecol[k] : -1;
+          const double bl = k < k1 ? eval[k] : 0.0;
+          la_gather_cols_weak(x, ncol, lane, jl, bl, k1 - k0, acc0, acc1);
+        } else {
+          la_long_row(x, ncol, ecol, eval, k0, k1, lane, sm_red[threadIdx.x >> 5], sm_col[threadIdx.x >> 5], acc0,
+                      acc1);
+        }
+        const int c1 = lane + 32;
+        if (lane < ncol) {
+          const double xr = sr * v[r * ncol + lane] - acc0;
+          __stcg(x + r * ncol + lane, xr);
+          if (out2) out2[r * ncol + lane] = xr + w2[r] * v2[r * ncol + lane];
+        }
+        if (c1 < ncol) {
+          const double xr = sr * v[r * ncol + c1] - acc1;
+          __stcg(x + r * ncol + c1, xr);
+          if (out2) out2[r * ncol + c1] = xr + w2[r] * v2[r * ncol + c1];
+        }
+      }
+    }
+    grid.sync();
+    if (dbg && blockIdx.x == 0 && threadIdx.x == 0) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      dbg[L] = t;
+    }
   }
 }
 
@@ -586,40 +873,48 @@ cudaError_t launch_la_transpose_struct(const int32_t* nbr, int64_t n, int mv, in
 
 static int la_trsv_blocks(const void* fn) {
   static int cached[2] = {0, 0};
-  int idx = fn == (const void*)la_trsv_fwd_kernel ? 0 : 1;
+  const int idx = fn == (const void*)la_trsv_fwd_kernel ? 0 : 1;
   if (!cached[idx]) {
     int per_sm = 0, dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, LA_THREADS, 0);
-    cached[idx] = sms * (per_sm > 0 ? per_sm : 1);
+    // every warp must be resident (static assignment); VIF_LA_TRSV_BPS caps the blocks per SM
+    static const char* cap_env = getenv("VIF_LA_TRSV_BPS");
+    const int cap = cap_env ? atoi(cap_env) : 2;
+    if (per_sm < 1) per_sm = 1;
+    if (cap > 0 && per_sm > cap) per_sm = cap;
+    cached[idx] = sms * per_sm;
   }
   return cached[idx];
 }
 
 cudaError_t launch_la_trsv_fwd(const int32_t* nbr, const double* Bc, int mv, int64_t n, int ncol, const double* v,
                                const double* scale, double* x, const double* v2, const double* w2, double* out2,
-                               int* flags, int epoch, unsigned long long* ticket, cudaStream_t s) {
-  cudaError_t e = cudaMemsetAsync(ticket, 0, sizeof(unsigned long long), s);
-  if (e != cudaSuccess) return e;
+                               int* flags, int epoch, cudaStream_t s) {
+  if (ncol > 64) return cudaErrorInvalidValue;
   int64_t blocks = la_trsv_blocks((const void*)la_trsv_fwd_kernel);
   const int64_t need = (n + LA_WARPS - 1) / LA_WARPS;
   if (blocks > need) blocks = need;
   la_trsv_fwd_kernel<<<(unsigned)blocks, LA_THREADS, 0, s>>>(nbr, Bc, mv, n, ncol, v, scale, x, v2, w2, out2, flags,
-                                                              epoch, ticket);
+                                                              epoch);
   return cudaGetLastError();
 }
 
-cudaError_t launch_la_trsv_bwd(const int* tptr, const int* tpos, const double* Bc, int mv, int64_t n, int ncol,
-                               const double* u, double* y, int* flags, int epoch, unsigned long long* ticket,
-                               cudaStream_t s) {
-  cudaError_t e = cudaMemsetAsync(ticket, 0, sizeof(unsigned long long), s);
-  if (e != cudaSuccess) return e;
+cudaError_t launch_la_trsv_bwd(const int* tptr, const int* trow, const double* tval, int64_t n, int ncol,
+                               const double* u, double* y, int* flags, int epoch, cudaStream_t s) {
+  if (ncol > 64) return cudaErrorInvalidValue;
   int64_t blocks = la_trsv_blocks((const void*)la_trsv_bwd_kernel);
   const int64_t need = (n + LA_WARPS - 1) / LA_WARPS;
   if (blocks > need) blocks = need;
-  la_trsv_bwd_kernel<<<(unsigned)blocks, LA_THREADS, 0, s>>>(tptr, tpos, Bc, mv > 0 ? mv : 1, n, ncol, u, y, flags,
-                                                              epoch, ticket);
+  la_trsv_bwd_kernel<<<(unsigned)blocks, LA_THREADS, 0, s>>>(tptr, trow, tval, n, ncol, u, y, flags, epoch);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_la_tvals(const int* tpos, int64_t nnz, int mv, const double* Bc, int* trow, double* tval,
+                            cudaStream_t s) {
+  if (nnz == 0) return cudaSuccess;
+  la_tvals_kernel<<<grid_for(nnz), 256, 0, s>>>(tpos, nnz, mv, Bc, trow, tval);
   return cudaGetLastError();
 }
 
@@ -765,6 +1060,96 @@ cudaError_t launch_la_bapply(const int32_t* nbr, const double* Bc, int mv, int64
 cudaError_t launch_la_finish(const double* fin, const double* slq, int64_t n, int ell, double* out, cudaStream_t s) {
   la_finish_kernel<<<1, 1, 0, s>>>(fin, slq, n, ell, out);
   return cudaGetLastError();
+}
+
+cudaError_t launch_la_levels(const int32_t* nbr, int mv, int64_t n, const int* tptr, const int* trow, int* lev_f,
+                             int* lev_b, int* flags, int epoch_f, int epoch_b, int* nlev_dev, cudaStream_t s) {
+  int64_t blocks = la_trsv_blocks((const void*)la_trsv_fwd_kernel);
+  const int64_t need = (n + LA_WARPS - 1) / LA_WARPS;
+  if (blocks > need) blocks = need;
+  la_level_fwd_kernel<<<(unsigned)blocks, LA_THREADS, 0, s>>>(nbr, mv, n, lev_f, flags, epoch_f);
+  la_level_bwd_kernel<<<(unsigned)blocks, LA_THREADS, 0, s>>>(tptr, trow, n, lev_b, flags, epoch_b);
+  cudaError_t e = cudaMemsetAsync(nlev_dev, 0, 2 * sizeof(int), s);
+  if (e != cudaSuccess) return e;
+  la_max_kernel<<<grid_for(n), 256, 0, s>>>(lev_f, n, nlev_dev);
+  la_max_kernel<<<grid_for(n), 256, 0, s>>>(lev_b, n, nlev_dev + 1);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_la_reorder(const int* order_f, const int32_t* nbr, const double* Bc, int64_t n, int mv,
+                              int32_t* ecol_f, double* eval_f, const int* order_b, const int* tptr, const int* trow,
+                              const double* tval, int* cnt, int* eptr_b, int32_t* ecol_b, double* eval_b,
+                              cudaStream_t s) {
+  if (mv > 0) la_reorder_fwd_kernel<<<grid_for(n * mv), 256, 0, s>>>(order_f, nbr, Bc, n, mv, ecol_f, eval_f);
+  la_seglen_kernel<<<grid_for(n), 256, 0, s>>>(order_b, tptr, n, cnt);
+  la_scan_kernel<<<1, 1024, 0, s>>>(cnt, n, eptr_b);
+  la_reorder_bwd_kernel<<<grid_for(n * 32), 256, 0, s>>>(order_b, tptr, trow, tval, eptr_b, n, ecol_b, eval_b);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_la_bucket(const int* key, int64_t n, int nkeys, int* cnt, int* cursor, int* ptr, int* order,
+                             cudaStream_t s) {
+  cudaError_t e = cudaMemsetAsync(cnt, 0, (size_t)nkeys * sizeof(int), s);
+  if (e != cudaSuccess) return e;
+  e = cudaMemsetAsync(cursor, 0, (size_t)nkeys * sizeof(int), s);
+  if (e != cudaSuccess) return e;
+  la_bucket_count_kernel<<<grid_for(n), 256, 0, s>>>(key, n, cnt);
+  la_scan_kernel<<<1, 1024, 0, s>>>(cnt, nkeys, ptr);
+  la_bucket_fill_kernel<<<grid_for(n), 256, 0, s>>>(key, n, ptr, cursor, order);
+  return cudaGetLastError();
+}
+
+static int la_lvl_blocks(const void* fn) {
+  static int cached[2] = {0, 0};
+  const int idx = fn == (const void*)la_trsv_lvl_kernel<true> ? 0 : 1;
+  if (!cached[idx]) {
+    int per_sm = 0, dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, LA_THREADS, 0);
+    static const char* cap_env = getenv("VIF_LA_LVL_BPS");
+    const int cap = cap_env ? atoi(cap_env) : 1;
+    if (per_sm < 1) per_sm = 1;
+    if (cap > 0 && per_sm > cap) per_sm = cap;
+    cached[idx] = sms * per_sm;
+  }
+  return cached[idx];
+}
+
+cudaError_t launch_la_trsv_lvl(bool fwd, const int* order, const int* lptr, int nlev, const int32_t* ecol,
+                               const double* eval, const int* eptr, int mv, int ncol, const double* v,
+                               const double* scale, double* x, const double* v2, const double* w2, double* out2,
+                               cudaStream_t s) {
+  if (ncol > 64) return cudaErrorInvalidValue;
+  const void* fn = fwd ? (const void*)la_trsv_lvl_kernel<true> : (const void*)la_trsv_lvl_kernel<false>;
+  const int grid = la_lvl_blocks(fn);
+  static const char* dbg_env = getenv("VIF_LA_DEBUG");
+  static unsigned long long* dbg = nullptr;
+  if (dbg_env && !dbg) cudaMalloc(&dbg, 1 << 20);
+  unsigned long long* dbgp = dbg_env ? dbg : nullptr;
+  void* args[] = {(void*)&order, (void*)&lptr, (void*)&nlev, (void*)&ecol, (void*)&eval, (void*)&eptr, (void*)&mv,
+                  (void*)&ncol, (void*)&v, (void*)&scale, (void*)&x, (void*)&v2, (void*)&w2, (void*)&out2,
+                  (void*)&dbgp};
+  cudaError_t e = cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(LA_THREADS), args, 0, s);
+  if (dbg_env && e == cudaSuccess && nlev > 1 && nlev < 100000) {  // per-level durations (debug)
+    static int calls = 0;
+    if (++calls % 3 == 0) {
+      std::vector<unsigned long long> t(nlev);
+      std::vector<int> lp(nlev + 1);
+      cudaMemcpyAsync(t.data(), dbg, nlev * 8, cudaMemcpyDeviceToHost, s);
+      cudaMemcpyAsync(lp.data(), lptr, (nlev + 1) * 4, cudaMemcpyDeviceToHost, s);
+      cudaStreamSynchronize(s);
+      std::vector<std::pair<double, int>> d;
+      for (int L = 1; L < nlev; ++L) d.push_back({(t[L] - t[L - 1]) * 1e-3, L});
+      std::sort(d.begin(), d.end());
+      double tot = (t[nlev - 1] - t[0]) * 1e-3;
+      fprintf(stderr, "[la dbg] fwd=%d ncol=%d nlev=%d total_us=%.1f median_us=%.2f\n", (int)fwd, ncol, nlev, tot,
+              d[d.size() / 2].first);
+      for (int q = (int)d.size() - 1; q >= 0 && q >= (int)d.size() - 6; --q)
+        fprintf(stderr, "   level %d: %.1f us, %d rows\n", d[q].second, d[q].first, lp[d[q].second + 1] - lp[d[q].second]);
+    }
+  }
+  return e;
 }
 
 }  // namespace vif

@@ -107,9 +107,22 @@ cudaError_t launch_la_transpose_struct(const int32_t* nbr, int64_t n, int mv, in
                                        int* tpos, cudaStream_t s);
 cudaError_t launch_la_trsv_fwd(const int32_t* nbr, const double* Bc, int mv, int64_t n, int ncol, const double* v,
                                const double* scale, double* x, const double* v2, const double* w2, double* out2,
-                               int* flags, int epoch, unsigned long long* ticket, cudaStream_t s);
-cudaError_t launch_la_trsv_bwd(const int* tptr, const int* tpos, const double* Bc, int mv, int64_t n, int ncol,
-                               const double* u, double* y, int* flags, int epoch, unsigned long long* ticket,
+                               int* flags, int epoch, cudaStream_t s);
+cudaError_t launch_la_trsv_bwd(const int* tptr, const int* trow, const double* tval, int64_t n, int ncol,
+                               const double* u, double* y, int* flags, int epoch, cudaStream_t s);
+cudaError_t launch_la_tvals(const int* tpos, int64_t nnz, int mv, const double* Bc, int* trow, double* tval,
+                            cudaStream_t s);
+cudaError_t launch_la_levels(const int32_t* nbr, int mv, int64_t n, const int* tptr, const int* trow, int* lev_f,
+                             int* lev_b, int* flags, int epoch_f, int epoch_b, int* nlev_dev, cudaStream_t s);
+cudaError_t launch_la_reorder(const int* order_f, const int32_t* nbr, const double* Bc, int64_t n, int mv,
+                              int32_t* ecol_f, double* eval_f, const int* order_b, const int* tptr, const int* trow,
+                              const double* tval, int* cnt, int* eptr_b, int32_t* ecol_b, double* eval_b,
+                              cudaStream_t s);
+cudaError_t launch_la_bucket(const int* key, int64_t n, int nkeys, int* cnt, int* cursor, int* ptr, int* order,
+                             cudaStream_t s);
+cudaError_t launch_la_trsv_lvl(bool fwd, const int* order, const int* lptr, int nlev, const int32_t* ecol,
+                               const double* eval, const int* eptr, int mv, int ncol, const double* v,
+                               const double* scale, double* x, const double* v2, const double* w2, double* out2,
                                cudaStream_t s);
 int la_ts_nsplit(int64_t n);
 cudaError_t launch_la_tsgemm(const double* U, int64_t ldu, int mk, int64_t n, const double* V, int ncol,

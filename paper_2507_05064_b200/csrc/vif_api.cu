@@ -235,7 +235,7 @@ struct Handle {
   // VIF-Laplace state (vif_la_prepare): valid while fgen == la_gen (every vif_factor bumps fgen)
   uint64_t fgen = 0, la_gen = ~0ull;
   const void* la_ws = nullptr;
-  int la_epoch = 0, la_nprobe = 0, la_maxcg = 0;
+  int la_epoch = 0, la_nprobe = 0, la_maxcg = 0, la_nlev_f = 0, la_nlev_b = 0;
   double la_sigma2 = 0.0;
   // profiling
   bool prof = false;
@@ -431,7 +431,8 @@ Layout make_pred_layout(const Plan& P, int64_t np) {
 enum LBuf {
   L_B, L_D, L_FLAGS, L_TPTR, L_TPOS, L_CNT, L_CUR, L_TICKET, L_UN2, L_W, L_WINV, L_V, L_BM, L_A, L_DV, L_DVINV,
   L_S, L_GV, L_LVINV, L_LVT, L_MVINV, L_TSCR, L_GPART, L_TSPART, L_CT, L_CT2, L_RPART, L_SC, L_ACTIVE, L_ITERS,
-  L_HA, L_HB, L_SLQS, L_X, L_R, L_Z, L_P, L_Q, L_T1, L_T2, L_RHS, L_E1T, L_GM, L_LMINV, L_COUNT
+  L_HA, L_HB, L_SLQS, L_X, L_R, L_Z, L_P, L_Q, L_T1, L_T2, L_RHS, L_E1T, L_GM, L_LMINV, L_TROW, L_TVAL, L_LEVF,
+  L_LEVB, L_ORDF, L_ORDB, L_LPTRF, L_LPTRB, L_ECF, L_EVF, L_ECB, L_EVB, L_EPB, L_COUNT
 };
 // per-column scalar arrays inside L_SC (each kLaCols doubles)
 enum LScal { SC_RZ, SC_RZN, SC_PQ, SC_ALPHA, SC_BETA, SC_RR, SC_BN, SC_SLQ, SC_MISC, SC_OUT, SC_COUNT };
@@ -455,7 +456,12 @@ LaLayout make_la_layout(const Plan& P, int nprobe, int max_cg) {
       L.size[L_DV] = L.size[L_DVINV] = (size_t)n * D8;
   L.size[L_FLAGS] = L.size[L_CNT] = L.size[L_CUR] = (size_t)n * sizeof(int);
   L.size[L_TPTR] = (size_t)(n + 1) * sizeof(int);
-  L.size[L_TPOS] = (size_t)n * mv1 * sizeof(int);
+  L.size[L_TPOS] = L.size[L_TROW] = (size_t)n * mv1 * sizeof(int);
+  L.size[L_TVAL] = (size_t)n * mv1 * D8;
+  L.size[L_LEVF] = L.size[L_LEVB] = L.size[L_ORDF] = L.size[L_ORDB] = (size_t)n * sizeof(int);
+  L.size[L_LPTRF] = L.size[L_LPTRB] = L.size[L_EPB] = (size_t)(n + 1) * sizeof(int);
+  L.size[L_ECF] = L.size[L_ECB] = (size_t)n * mv1 * sizeof(int);
+  L.size[L_EVF] = L.size[L_EVB] = (size_t)n * mv1 * D8;
   L.size[L_TICKET] = 64;
   L.size[L_S] = (size_t)n * P.ld * D8;
   L.size[L_GV] = (size_t)P.ld * P.ld * D8;
@@ -480,6 +486,12 @@ LaLayout make_la_layout(const Plan& P, int nprobe, int max_cg) {
   return L;
 }
 
+#define LA_TRY(call)               \
+  do {                             \
+    int r_ = (call);               \
+    if (r_ != VIF_OK) return r_;   \
+  } while (0)
+
 // VIF-Laplace helpers: buffers of a prepared workspace and the operators of the iterative path
 struct LaCtx {
   Handle* h;
@@ -501,6 +513,42 @@ LaCtx la_ctx(Handle* h, void* ws) {
   return c;
 }
 
+// B^{-1} (s o v) -> x [out2 = x + w2 o v2] and B^{-T} u -> y: level-scheduled cooperative kernels
+// (default) or the sync-free flag kernels (VIF_LA_SYNCFREE=1)
+bool la_syncfree() {
+  static const char* e = getenv("VIF_LA_SYNCFREE");
+  return e && e[0] == '1';
+}
+
+int la_binv(LaCtx& c, int ncol, const double* v, const double* scale, double* x, const double* v2, const double* w2,
+            double* out2) {
+  Handle* h = c.h;
+  const Plan& P = h->P;
+  if (la_syncfree())
+    VIF_CUDA(h, launch_la_trsv_fwd(c.nbr(), c.d(L_B), P.mv, P.n, ncol, v, scale, x, v2, w2, out2, c.i(L_FLAGS),
+                                   ++h->la_epoch, c.s),
+             "B^-1");
+  else
+    VIF_CUDA(h, launch_la_trsv_lvl(true, c.i(L_ORDF), c.i(L_LPTRF), h->la_nlev_f, c.i(L_ECF), c.d(L_EVF), nullptr,
+                                   P.mv, ncol, v, scale, x, v2, w2, out2, c.s),
+             "B^-1 (levels)");
+  return VIF_OK;
+}
+
+int la_btinv(LaCtx& c, int ncol, const double* u, double* y) {
+  Handle* h = c.h;
+  const Plan& P = h->P;
+  if (la_syncfree())
+    VIF_CUDA(h, launch_la_trsv_bwd(c.i(L_TPTR), c.i(L_TROW), c.d(L_TVAL), P.n, ncol, u, y, c.i(L_FLAGS),
+                                   ++h->la_epoch, c.s),
+             "B^-T");
+  else
+    VIF_CUDA(h, launch_la_trsv_lvl(false, c.i(L_ORDB), c.i(L_LPTRB), h->la_nlev_b, c.i(L_ECB), c.d(L_EVB),
+                                   c.i(L_EPB), P.mv, ncol, u, nullptr, y, nullptr, nullptr, nullptr, c.s),
+             "B^-T (levels)");
+  return VIF_OK;
+}
+
 // out = Sigma_dagger v (+ winv o v): B^{-1} D B^{-T} v + U (U^T v); v, out: n x ncol
 int la_sigma(LaCtx& c, int ncol, const double* v, double* out, const double* winv) {
   Handle* h = c.h;
@@ -509,13 +557,8 @@ int la_sigma(LaCtx& c, int ncol, const double* v, double* out, const double* win
     VIF_CUDA(h, launch_la_tsgemm(c.U(), P.ld, P.mk, P.n, v, ncol, nullptr, nullptr, c.d(L_TSPART), c.d(L_CT), 1.0,
                                  c.s),
              "U^T v");
-  VIF_CUDA(h, launch_la_trsv_bwd(c.i(L_TPTR), c.i(L_TPOS), c.d(L_B), P.mv, P.n, ncol, v, c.d(L_T1), c.i(L_FLAGS),
-                                 ++h->la_epoch, c.ticket(), c.s),
-           "B^-T");
-  double* x = winv ? c.d(L_T2) : out;
-  VIF_CUDA(h, launch_la_trsv_fwd(c.nbr(), c.d(L_B), P.mv, P.n, ncol, c.d(L_T1), c.d(L_D), x, v, winv,
-                                 winv ? out : nullptr, c.i(L_FLAGS), ++h->la_epoch, c.ticket(), c.s),
-           "B^-1");
+  LA_TRY(la_btinv(c, ncol, v, c.d(L_T1)));
+  LA_TRY(la_binv(c, ncol, c.d(L_T1), c.d(L_D), winv ? c.d(L_T2) : out, v, winv, winv ? out : nullptr));
   if (P.mk > 0)
     VIF_CUDA(h, launch_gemm_tn(c.U(), P.ld, P.n, c.d(L_CT), P.mk, ncol, P.mk, 0, out, ncol, 1.0, 1, c.s), "U C");
   return VIF_OK;
@@ -568,12 +611,6 @@ int la_coldot(LaCtx& c, const double* a, const double* b, int64_t n, int ncol, d
   VIF_CUDA(c.h, launch_la_reduce(0, a, b, n, ncol, c.d(L_RPART), out, c.s), "dot");
   return VIF_OK;
 }
-
-#define LA_TRY(call)               \
-  do {                             \
-    int r_ = (call);               \
-    if (r_ != VIF_OK) return r_;   \
-  } while (0)
 
 // Preconditioned CG on (W^{-1} + Sigma_dagger) x = rhs, ncol independent columns (pcls2 P:322;
 // Saad 2003 Alg. 9.1), readings l3 (stop at ||r|| <= tol ||rhs||).  x holds x0 when warm.  With
@@ -1442,7 +1479,35 @@ int vif_la_prepare(void* handle, const vif_theta* theta, int32_t nprobe, int32_t
   else VIF_CUDA(h, cudaMemsetAsync(c.d(L_UN2), 0, c.L.size[L_UN2], s), "memset");
   VIF_CUDA(h, launch_la_transpose_struct(c.nbr(), P.n, P.mv, c.i(L_CNT), c.i(L_CUR), c.i(L_TPTR), c.i(L_TPOS), s),
            "B^T structure");
+  {
+    int nnz = 0;
+    VIF_CUDA(h, cudaMemcpyAsync(&nnz, c.i(L_TPTR) + P.n, sizeof(int), cudaMemcpyDeviceToHost, s), "nnz");
+    VIF_CUDA(h, cudaStreamSynchronize(s), "sync");
+    VIF_CUDA(h, launch_la_tvals(c.i(L_TPOS), nnz, P.mv > 0 ? P.mv : 1, c.d(L_B), c.i(L_TROW), c.d(L_TVAL), s),
+             "B^T values");
+  }
+  // dependency levels of B (forward) and B^T (backward), rows bucketed by level
   VIF_CUDA(h, cudaMemsetAsync(c.i(L_FLAGS), 0, c.L.size[L_FLAGS], s), "memset flags");
+  {
+    int* nlev = c.i(L_ACTIVE);  // scratch: two ints
+    VIF_CUDA(h, launch_la_levels(c.nbr(), P.mv, P.n, c.i(L_TPTR), c.i(L_TROW), c.i(L_LEVF), c.i(L_LEVB), c.i(L_FLAGS),
+                                 1, 2, nlev, s),
+             "levels");
+    int hl[2];
+    VIF_CUDA(h, cudaMemcpyAsync(hl, nlev, sizeof(hl), cudaMemcpyDeviceToHost, s), "levels");
+    VIF_CUDA(h, cudaStreamSynchronize(s), "sync");
+    h->la_nlev_f = hl[0] + 1;
+    h->la_nlev_b = hl[1] + 1;
+    VIF_CUDA(h, launch_la_bucket(c.i(L_LEVF), P.n, h->la_nlev_f, c.i(L_CNT), c.i(L_CUR), c.i(L_LPTRF), c.i(L_ORDF), s),
+             "bucket");
+    VIF_CUDA(h, launch_la_bucket(c.i(L_LEVB), P.n, h->la_nlev_b, c.i(L_CNT), c.i(L_CUR), c.i(L_LPTRB), c.i(L_ORDB), s),
+             "bucket");
+    VIF_CUDA(h, launch_la_reorder(c.i(L_ORDF), c.nbr(), c.d(L_B), P.n, P.mv, c.i(L_ECF), c.d(L_EVF), c.i(L_ORDB),
+                                  c.i(L_TPTR), c.i(L_TROW), c.d(L_TVAL), c.i(L_CNT), c.i(L_EPB), c.i(L_ECB), c.d(L_EVB),
+                                  s),
+             "level-ordered entries");
+  }
+  VIF_CUDA(h, cudaMemsetAsync(c.i(L_FLAGS), 0, c.L.size[L_FLAGS], s), "memset flags");  // solves start at epoch 1
   int ff = 0;
   VIF_CUDA(h, cudaMemcpyAsync(&ff, c.fitc_fail(), sizeof(int), cudaMemcpyDeviceToHost, s), "status");
   VIF_CUDA(h, cudaStreamSynchronize(s), "sync");
@@ -1472,16 +1537,8 @@ int vif_la_apply(void* handle, void* ws, int32_t op, int32_t ncol, const double*
   switch (op) {
     case VIF_LA_SIGMA: LA_TRY(la_sigma(c, ncol, v, out, nullptr)); break;
     case VIF_LA_A: LA_TRY(la_sigma(c, ncol, v, out, winv)); break;
-    case VIF_LA_BINV:
-      VIF_CUDA(h, launch_la_trsv_fwd(c.nbr(), c.d(L_B), P.mv, P.n, ncol, v, nullptr, out, nullptr, nullptr, nullptr,
-                                     c.i(L_FLAGS), ++h->la_epoch, c.ticket(), c.s),
-               "B^-1");
-      break;
-    case VIF_LA_BTINV:
-      VIF_CUDA(h, launch_la_trsv_bwd(c.i(L_TPTR), c.i(L_TPOS), c.d(L_B), P.mv, P.n, ncol, v, out, c.i(L_FLAGS),
-                                     ++h->la_epoch, c.ticket(), c.s),
-               "B^-T");
-      break;
+    case VIF_LA_BINV: LA_TRY(la_binv(c, ncol, v, nullptr, out, nullptr, nullptr, nullptr)); break;
+    case VIF_LA_BTINV: LA_TRY(la_btinv(c, ncol, v, out)); break;
     case VIF_LA_FITC_SOLVE:
       LA_TRY(la_fitc_build(c, winv));
       LA_TRY(la_fitc_solve(c, ncol, v, out));
