@@ -47,6 +47,9 @@ def parse():
     ap.add_argument("--no-grad", action="store_true", help="skip the NLL-gradient timing (vif_grad)")
     ap.add_argument("--npred", type=int, default=100000, help="prediction points for the vif_predict timing (0: skip)")
     ap.add_argument("--no-knn", action="store_true", help="skip the vif_neighbors timing")
+    ap.add_argument("--la-n", type=int, default=100000,
+                    help="points of the VIF-Laplace (Bernoulli) timing, paper recipe P:600 (0: skip)")
+    ap.add_argument("--la-ell", type=int, default=50, help="SLQ probe vectors of the VIF-Laplace timing")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target CPU seconds of the oracle sample")
     return ap.parse_args()
 
@@ -351,6 +354,11 @@ def main():
         model.factor(th[0])  # vif_neighbors invalidates the factor; leave the handle evaluated
         model.nll()
 
+    # ---------------- VIF-Laplace, Bernoulli likelihood (vif_la_*, single GPU) ----------------
+    lap = None
+    if world == 1 and args.la_n > 0:
+        lap = run_laplace(args, dev, stream)
+
     if rank == 0:
         fl = workload_flops(w.nbr, w.m)
         # per-rank share of the row-sharded kernels (strong scaling: each rank does ~1/world of the rows)
@@ -415,6 +423,7 @@ def main():
             "grad": grad,
             "predict": pred,
             "neighbors": knn,
+            "laplace": lap,
             "input_generation_s": {"total": gen_s, **{k: round(v, 3) for k, v in w.timings.items()}},
             "create_s": create_s,
         }
@@ -423,6 +432,73 @@ def main():
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def run_laplace(args, dev, stream):
+    """One L^VIFLA evaluation = vif_la_prepare (latent factor at nugget 0, transposed structure, levels)
+    + vif_la_nll (Newton mode with FITC-preconditioned CG, exact quadratic term, SLQ log-det with ell
+    probes) on the paper's Laplace recipe (d = 5, ARD Gaussian covariance, lambda = 0.15..0.75,
+    binary responses), m = 200 (the paper's best FITC rank k = 200), m_v = 30."""
+    import torch
+    import paper_2507_05064_b200 as p
+    import vifgen
+    n, m, mv, ell = args.la_n, 200, 30, args.la_ell
+    t0 = time.perf_counter()
+    lw = vifgen.make_laplace_workload(n=n, m=m, mv=mv, device=str(dev))
+    gen = time.perf_counter() - t0
+    X, Z, nbr, y = (torch.from_numpy(np.ascontiguousarray(a)).to(dev) for a in (lw.X, lw.Z, lw.nbr, lw.y))
+    eps1, eps2 = vifgen.make_probes(n, m, ell)
+    e1, e2 = torch.from_numpy(eps1).to(dev), torch.from_numpy(eps2).to(dev)
+    lm = p.VifModel(X, Z, nbr, y, device=dev, stream=stream)
+    th = p.Theta(**lw.theta_dict())
+    tol = 1e-6
+    opts = p.LaOpts(max_newton=50, newton_tol=tol, max_cg=1000, cg_tol=tol, nprobe=ell, slq_tol=tol)
+    lm.la_prepare(th, nprobe=ell, max_cg=1000)
+    lm.la_nll(y, opts, e1, e2)  # warm-up
+    reps, times = 2, []
+    for _ in range(reps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize(dev)
+        a.record(stream)
+        lm.la_prepare(th, nprobe=ell, max_cg=1000)
+        t, _ = lm.la_nll(y, opts, e1, e2)
+        b.record(stream)
+        torch.cuda.synchronize(dev)
+        times.append(a.elapsed_time(b))
+    ops = {}
+    for ncol in (1, ell):
+        V = torch.randn(n, ncol, dtype=torch.float64, device=dev) if ncol > 1 else torch.randn(n, dtype=torch.float64, device=dev)
+        for op in ("btinv", "binv", "sigma"):
+            lm.la_apply(op, V)
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            for _ in range(3):
+                lm.la_apply(op, V)
+            b.record(stream)
+            torch.cuda.synchronize(dev)
+            ops[f"{op}_ncol{ncol}_ms"] = a.elapsed_time(b) / 3
+    lm.close()
+    cpu = None
+    if not args.no_cpu_baseline:
+        import oracle
+        from oracle import laplace as la
+        ns = 2000
+        sw = vifgen.make_laplace_workload(n=ns, m=50, mv=mv, device=str(dev))
+        s1, s2 = vifgen.make_probes(ns, 50, ell)
+        c0 = time.perf_counter()
+        la.vifla_nll(sw.X, sw.Z, sw.nbr, sw.y, oracle.Theta(**sw.theta_dict()), eps1=s1, eps2=s2, newton_tol=tol,
+                     cg_tol=tol, slq_tol=tol)
+        cpu = {"s_per_eval": time.perf_counter() - c0, "n": ns, "m": 50, "mv": mv, "ell": ell,
+               "note": "oracle/laplace.py (numpy + scipy sparse triangular solves) on n = 2000 of the same recipe"}
+    return {"n": n, "d": 5, "m": m, "mv": mv, "ell": ell, "tol": tol, "ms_per_eval": statistics.median(times),
+            "points_per_s": n / (statistics.median(times) * 1e-3), "nll": t.nll, "neg_loglik": t.neg_loglik,
+            "quad": t.quad, "logdet": t.logdet, "newton_iters": t.newton_iters, "cg_iters": t.cg_iters,
+            "slq_iters_max": t.slq_iters_max, "slq_iters_mean": t.slq_iters_mean, "operators": ops,
+            "input_generation_s": gen, "cpu_oracle": cpu,
+            "note": "vif_la_prepare + vif_la_nll (Bernoulli-logit VIF-Laplace: Newton + FITC-PCG, pcls2; SLQ "
+                    "log-det slq_v2 with ell probe vectors; P:224-345, App. FITC); every CG iteration applies "
+                    "Sigma_dagger = B^-1 D B^-T + U U^T (two level-scheduled sparse triangular solves, latency-bound "
+                    "by the DAG depth) and the FITC solve"}
 
 
 def run_reference(args, w, cid, world, gen_s):

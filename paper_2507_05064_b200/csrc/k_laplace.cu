@@ -919,8 +919,8 @@ cudaError_t launch_la_tvals(const int* tpos, int64_t nnz, int mv, const double* 
 }
 
 int la_ts_nsplit(int64_t n) {
-  int64_t ns = (n + 4095) / 4096;
-  if (ns > 296) ns = 296;
+  int64_t ns = (n + 511) / 512;  // >= 4 x 148 CTAs with the k tiles: the contraction is HBM-bound
+  if (ns > 592) ns = 592;
   if (ns < 1) ns = 1;
   return (int)ns;
 }
