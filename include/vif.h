@@ -95,6 +95,10 @@ int vif_workspace_bytes(const vif_dims* dims, size_t* bytes);
  * rounds r of [(r*world + rank)*chunk, (r*world + rank + 1)*chunk) intersected with [0, n).
  * Writes *rounds and *chunk; the caller derives the rows. */
 int vif_partition(const vif_dims* dims, int64_t* rounds, int64_t* chunk);
+/* The same map for a created handle (SURVEY 8(b) vif_owned_rows): this rank owns the row chunks
+ * first_chunk, first_chunk + stride, ... (< nchunks), chunk c = rows [c*chunk, (c+1)*chunk) & [0, n).
+ * An emulated multi-rank handle owns every chunk (first 0, stride 1).  Any output may be NULL. */
+int vif_owned_rows(void* handle, int64_t* first_chunk, int64_t* chunk, int32_t* stride, int64_t* nchunks);
 
 /* Create a handle.  `workspace` (device, >= vif_workspace_bytes) is owned by the caller and must
  * outlive the handle.  X (n x d, Vecchia order), Z (m x d), nbr (n x mv int32: nbr[i][k] < i, no

@@ -423,7 +423,7 @@ __global__ void __launch_bounds__(LA_THREADS) la_trsv_lvl_kernel(
     const int* __restrict__ order, const int* __restrict__ lptr, int nlev, const int32_t* __restrict__ ecol,
     const double* __restrict__ eval, const int* __restrict__ eptr, int mv, int ncol, const double* __restrict__ v,
     const double* __restrict__ s, double* x, const double* __restrict__ v2, const double* __restrict__ w2,
-    double* __restrict__ out2, unsigned long long* dbg) {
+    double* __restrict__ out2, int long_min, unsigned long long* dbg) {
   cg::grid_group grid = cg::this_grid();
   __shared__ double sm_red[LA_WARPS][32][17];
   __shared__ double sm_col[LA_WARPS][64];
@@ -452,11 +452,13 @@ __global__ void __launch_bounds__(LA_THREADS) la_trsv_lvl_kernel(
         }
       } else {
         double acc0 = 0.0, acc1 = 0.0;
-        if (k1 - k0 <= 32) {
-          const int k = k0 + lane;
-          const int jl = k < k1 ? ecol[k] : -1;
-          const double bl = k < k1 ? eval[k] : 0.0;
-          la_gather_cols_weak(x, ncol, lane, jl, bl, k1 - k0, acc0, acc1);
+        if (k1 - k0 <= long_min) {
+          for (int kb = k0; kb < k1; kb += 32) {
+            const int k = kb + lane;
+            const int jl = k < k1 ? ecol[k] : -1;
+            const double bl = k < k1 ? eval[k] : 0.0;
+            la_gather_cols_weak(x, ncol, lane, jl, bl, k1 - kb < 32 ? k1 - kb : 32, acc0, acc1);
+          }
         } else {
           la_long_row(x, ncol, ecol, eval, k0, k1, lane, sm_red[threadIdx.x >> 5], sm_col[threadIdx.x >> 5], acc0,
                       acc1);
@@ -949,7 +951,7 @@ cudaError_t launch_la_tsgemm(const double* U, int64_t ldu, int mk, int64_t n, co
 }
 
 int la_red_nsplit(int64_t n) {
-  int64_t ns = (n + 8191) / 8192;
+  int64_t ns = (n + 511) / 512;  // up to 4 CTAs per SM: a dot over n x ell is a bandwidth pass
   if (ns > 592) ns = 592;
   if (ns < 1) ns = 1;
   return (int)ns;
@@ -1127,9 +1129,13 @@ cudaError_t launch_la_trsv_lvl(bool fwd, const int* order, const int* lptr, int 
   static unsigned long long* dbg = nullptr;
   if (dbg_env && !dbg) cudaMalloc(&dbg, 1 << 20);
   unsigned long long* dbgp = dbg_env ? dbg : nullptr;
+  static const char* lm_env = getenv("VIF_LA_LONG");
+  // rows with more entries take the lanes-over-entries path; measured (n = 100k B^T): it pays for
+  // ncol <= 8 (2.9 vs 3.6 ms at ncol 2), chunks of 32 entries win from ncol 16 on (4.7 vs 9.6 ms at 50)
+  int long_min = lm_env ? atoi(lm_env) : (ncol <= 8 ? 32 : 1 << 30);
   void* args[] = {(void*)&order, (void*)&lptr, (void*)&nlev, (void*)&ecol, (void*)&eval, (void*)&eptr, (void*)&mv,
                   (void*)&ncol, (void*)&v, (void*)&scale, (void*)&x, (void*)&v2, (void*)&w2, (void*)&out2,
-                  (void*)&dbgp};
+                  (void*)&long_min, (void*)&dbgp};
   cudaError_t e = cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(LA_THREADS), args, 0, s);
   if (dbg_env && e == cudaSuccess && nlev > 1 && nlev < 100000) {  // per-level durations (debug)
     static int calls = 0;

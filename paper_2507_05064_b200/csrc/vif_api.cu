@@ -717,6 +717,17 @@ int vif_partition(const vif_dims* dims, int64_t* rounds, int64_t* chunk) {
   return VIF_OK;
 }
 
+int vif_owned_rows(void* handle, int64_t* first_chunk, int64_t* chunk, int32_t* stride, int64_t* nchunks) {
+  Handle* h = reinterpret_cast<Handle*>(handle);
+  if (!h) return fail(nullptr, VIF_ERR_INVALID_ARG, "handle is NULL");
+  const Plan& P = h->P;
+  if (first_chunk) *first_chunk = P.emulate ? 0 : P.rank;
+  if (chunk) *chunk = P.chunk;
+  if (stride) *stride = P.emulate ? 1 : P.world;
+  if (nchunks) *nchunks = (P.n + P.chunk - 1) / P.chunk;
+  return VIF_OK;
+}
+
 int vif_create(void** handle, const vif_dims* dims, void* workspace, size_t ws_bytes, const double* X,
                const double* Z, const int32_t* nbr, const double* y, const void* nccl_id, void* cuda_stream) {
   if (!handle) return fail(nullptr, VIF_ERR_INVALID_ARG, "handle is NULL");

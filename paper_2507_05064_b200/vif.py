@@ -95,6 +95,8 @@ def load_library():
         lib.vif_predict.argtypes = [P, ctypes.POINTER(_Theta), i64, P, P, P, sz, P, P, P, P]
         lib.vif_neighbors.argtypes = [P, ctypes.POINTER(_Theta), i32, P]
         lib.vif_stage_data.argtypes = [P, P, P, P, P]
+        lib.vif_owned_rows.argtypes = [P, ctypes.POINTER(i64), ctypes.POINTER(i64), ctypes.POINTER(i32),
+                                       ctypes.POINTER(i64)]
         lib.vif_la_workspace_bytes.argtypes = [ctypes.POINTER(_Dims), i32, i32, ctypes.POINTER(sz)]
         lib.vif_la_prepare.argtypes = [P, ctypes.POINTER(_Theta), i32, i32, P, sz]
         lib.vif_la_apply.argtypes = [P, P, i32, i32, P, P, P]
@@ -102,7 +104,7 @@ def load_library():
         for f in ("vif_nccl_unique_id", "vif_workspace_bytes", "vif_partition", "vif_create", "vif_set_data",
                   "vif_factor", "vif_nll", "vif_copy_U", "vif_launch_count", "vif_profile", "vif_stage_times",
                   "vif_grad_workspace_bytes", "vif_grad", "vif_predict_workspace_bytes", "vif_predict",
-                  "vif_neighbors", "vif_stage_data", "vif_la_workspace_bytes", "vif_la_prepare", "vif_la_apply",
+                  "vif_neighbors", "vif_stage_data", "vif_owned_rows", "vif_la_workspace_bytes", "vif_la_prepare", "vif_la_apply",
                   "vif_la_nll"):
             getattr(lib, f).restype = ctypes.c_int
         _lib = lib
@@ -113,7 +115,7 @@ EXPORTED = ("vif_nccl_unique_id", "vif_workspace_bytes", "vif_partition", "vif_c
             "vif_factor", "vif_nll", "vif_copy_U", "vif_launch_count", "vif_profile", "vif_stage_times",
             "vif_stage_name", "vif_last_error", "vif_destroy", "vif_grad_workspace_bytes", "vif_grad",
             "vif_predict_workspace_bytes", "vif_predict", "vif_neighbors", "vif_stage_data",
-            "vif_la_workspace_bytes", "vif_la_prepare", "vif_la_apply", "vif_la_nll")
+            "vif_la_workspace_bytes", "vif_la_prepare", "vif_la_apply", "vif_la_nll", "vif_owned_rows")
 LA_OPS = {"sigma": 0, "A": 1, "binv": 2, "btinv": 3, "fitc_solve": 4}
 NUM_STAGES = 8
 
@@ -330,6 +332,13 @@ def vif_la_nll(h, ws: torch.Tensor, y: torch.Tensor, opts: LaOpts, eps1=None, ep
                                      ctypes.byref(t)), h)
     return LaTerms(t.nll, t.neg_loglik, t.quad, t.logdet, t.logdet_W, t.logdet_P, t.newton_iters, t.cg_iters,
                    t.slq_iters_max, t.slq_iters_mean)
+
+
+def vif_owned_rows(h):
+    """(first_chunk, chunk, stride, nchunks) of the handle's chunk-cyclic row map."""
+    f, c, st, nc = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int32(), ctypes.c_int64()
+    _check(load_library().vif_owned_rows(h, ctypes.byref(f), ctypes.byref(c), ctypes.byref(st), ctypes.byref(nc)), h)
+    return f.value, c.value, st.value, nc.value
 
 
 def vif_copy_U(h, out: torch.Tensor):

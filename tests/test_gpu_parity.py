@@ -293,3 +293,20 @@ def test_stage_data_pipelined_matches_set_data():
     model.set_data(*ha)
     assert model.evaluate(th).nll == ref[0]
     model.close()
+
+
+@pytest.mark.parametrize("world", [1, 3])
+def test_owned_rows_map(world):
+    """vif_owned_rows describes the chunk-cyclic map: for a single-rank handle the chunks
+    tile [0, n) and agree with vif_partition / owned_rows; an emulated handle owns everything."""
+    import paper_2507_05064_b200 as p
+    w = small(1001, 8, 5, seed=13)
+    dev = torch.device("cuda")
+    X, Z, nbr, y = (torch.from_numpy(np.ascontiguousarray(a)).to(dev) for a in (w.X, w.Z.reshape(-1, w.d), w.nbr, w.y))
+    model = p.VifModel(X, Z, nbr, y, world=world, device=dev)
+    first, chunk, stride, nchunks = p.vif_owned_rows(model.handle)
+    rows = np.concatenate([np.arange(c * chunk, min((c + 1) * chunk, w.n)) for c in range(first, nchunks, stride)])
+    np.testing.assert_array_equal(rows, np.arange(w.n))
+    if world == 1:
+        np.testing.assert_array_equal(np.sort(model.owned_rows()), rows)
+    model.close()
