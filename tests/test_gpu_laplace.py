@@ -146,3 +146,47 @@ def test_state_checks():
     with pytest.raises(p.VifError):
         model.la_apply("sigma", np.ones(300))
     model.close()
+
+
+@pytest.mark.slow
+def test_bench_size_sampled():
+    """bench.py's Laplace workload (n = 100k, d = 5 ARD Gaussian, m = 200, m_v = 30) in its launch
+    configuration: sampled rows against the oracle, and properties that hold at any size.
+      - B^{-1} v and B^{-T} u: the oracle's own B rows (oracle.rows, nugget 0, recomputed from scratch)
+        satisfy (B x)_i = v_i on 300 sampled rows and (B^T y)_j = u_j on 40 sampled columns (all their
+        children rows) to 1e-9 relative to the row scale;
+      - the mode is stationary: b~ = Sigma_dagger (y - pi(b~)) (Sigma_dagger applied by the GPU, whose
+        operator parity is pinned above) to the CG tolerance;
+      - L^VIFLA is finite and equals its three terms."""
+    p = vif()
+    w = vifgen.make_laplace_workload(n=100000, m=200, mv=30, device="cuda")
+    th = p.Theta(**w.theta_dict())
+    model = model_of(w, th, nprobe=50)
+    n, mv = w.n, w.mv
+    rng = np.random.default_rng(5)
+    v = rng.standard_normal(n)
+    x = model.la_apply("binv", v).cpu().numpy()
+    yv = model.la_apply("btinv", v).cpu().numpy()
+    th0 = oracle.Theta(**{**w.theta_dict(), "nugget": 0.0})
+    ri = rng.choice(n, 300, replace=False)
+    _, Br, _ = oracle.rows(w.X, w.Z, w.nbr, th0, ri)
+    nb = w.nbr[ri]
+    Bx = x[ri] + np.sum(np.where(nb >= 0, Br * x[np.maximum(nb, 0)], 0.0), axis=1)
+    scale = np.abs(x[ri]) + np.sum(np.abs(np.where(nb >= 0, Br * x[np.maximum(nb, 0)], 0.0)), axis=1)
+    assert np.max(np.abs(Bx - v[ri]) / scale) < 1e-9
+    cols = rng.choice(n, 40, replace=False)
+    for j in cols:
+        ch, pos = np.nonzero(w.nbr == j)
+        _, Bc, _ = oracle.rows(w.X, w.Z, w.nbr, th0, ch) if len(ch) else (None, np.zeros((0, mv)), None)
+        terms = Bc[np.arange(len(ch)), pos] * yv[ch] if len(ch) else np.zeros(0)
+        res = yv[j] + terms.sum() - v[j]
+        assert abs(res) <= 1e-9 * (abs(yv[j]) + np.abs(terms).sum())
+    eps1, eps2 = vifgen.make_probes(n, 200, 50)
+    opts = p.LaOpts(max_newton=50, newton_tol=1e-10, max_cg=1000, cg_tol=1e-10, nprobe=50, slq_tol=1e-6)
+    t, b = model.la_nll(w.y, opts, eps1, eps2)
+    b = b.cpu().numpy()
+    g = w.y - 1.0 / (1.0 + np.exp(-b))
+    sg = model.la_apply("sigma", g).cpu().numpy()
+    assert np.max(np.abs(sg - b)) <= 1e-6 * np.abs(b).max()
+    assert np.isfinite(t.nll) and t.nll == pytest.approx(t.neg_loglik + 0.5 * t.quad + 0.5 * t.logdet, rel=1e-12)
+    model.close()
