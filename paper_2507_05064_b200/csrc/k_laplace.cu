@@ -545,14 +545,134 @@ __global__ void __launch_bounds__(256) la_tsgemm_kernel(const double* __restrict
   }
 }
 
-// Ct[c][k] = sum_s part[s][c][k] (+ Ct when accum)
+// The same contraction on the FP64 tensor cores for 8 < ncol <= 64: a CTA owns 64 columns of U (k) x
+// 64 columns of V and a row range; per stage 16 rows of U (cp.async) and of diag(rs) V (registers,
+// loaded one stage ahead) in shared memory; warp w computes C rows 8w..8w+7 with 8 DMMA 8x8x4 tiles
+// per 4 rows (A = U^T fragment, B = V fragment; pad 4 doubles: two wavefronts per fragment load).
+constexpr int TD_R = 16, TD_K = 64, TD_N = 64, TD_PAD = 4;
+__global__ void __launch_bounds__(256) la_tsgemm_dmma_kernel(const double* __restrict__ U, int64_t ldu, int mk,
+                                                             int64_t n, const double* __restrict__ V, int ncol,
+                                                             const double* __restrict__ rs, int64_t rows_per,
+                                                             double* __restrict__ part) {
+  __shared__ __align__(16) double Us[2][TD_R][TD_K + TD_PAD];
+  __shared__ __align__(16) double Vs[2][TD_R][TD_N + TD_PAD];
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  const int k0 = blockIdx.y * TD_K;
+  const int64_t r0 = (int64_t)blockIdx.x * rows_per;
+  const int64_t r1 = r0 + rows_per < n ? r0 + rows_per : n;
+  const int nst = (int)((r1 - r0 + TD_R - 1) / TD_R);
+  auto load_u = [&](int b, int64_t rb) {
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      const int e = t + 256 * i;
+      const int rr = e >> 5, c2 = (e & 31) * 2;
+      const int64_t r = rb + rr;
+      const bool ok = r < r1 && k0 + c2 < mk;
+      cp_async16(&Us[b][rr][c2], ok ? U + r * ldu + k0 + c2 : U, ok);
+    }
+    cp_async_commit();
+  };
+  double vreg[4];
+  auto load_v = [&](int64_t rb) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int e = t + 256 * i;
+      const int rr = e >> 6, c = e & 63;
+      const int64_t r = rb + rr;
+      double val = 0.0;
+      if (r < r1 && c < ncol) {
+        val = V[r * ncol + c];
+        if (rs) val *= rs[r];
+      }
+      vreg[i] = val;
+    }
+  };
+  auto store_v = [&](int b) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int e = t + 256 * i;
+      Vs[b][e >> 6][e & 63] = vreg[i];
+    }
+  };
+  double acc[8][2];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) acc[j][0] = acc[j][1] = 0.0;
+  if (nst > 0) {
+    load_u(0, r0);
+    load_v(r0);
+    store_v(0);
+  }
+  for (int st = 0; st < nst; ++st) {
+    const int b = st & 1;
+    const bool more = st + 1 < nst;
+    if (more) {
+      load_u(b ^ 1, r0 + (int64_t)(st + 1) * TD_R);
+      load_v(r0 + (int64_t)(st + 1) * TD_R);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k4 = 0; k4 < TD_R / 4; ++k4) {
+      const int rr = 4 * k4 + (lane & 3);
+      const double a = Us[b][rr][8 * w + (lane >> 2)];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) dmma884(acc[j][0], acc[j][1], a, Vs[b][rr][8 * j + (lane >> 2)]);
+    }
+    __syncthreads();
+    if (more) store_v(b ^ 1);
+  }
+  const int k = k0 + 8 * w + (lane >> 2);
+  if (k < mk) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int c = 8 * j + 2 * (lane & 3) + e;
+        if (c < ncol) part[((size_t)blockIdx.x * ncol + c) * mk + k] = acc[j][e];
+      }
+    }
+  }
+}
+
+// out[r] (+)= alpha sum_k U[r][k] c[k] for one right-hand side (the DMMA gemm_tn would compute a
+// 64-column tile for one useful column): a warp per row, 16-byte loads, c in shared memory.
+__global__ void __launch_bounds__(256) la_gemv_kernel(const double* __restrict__ U, int64_t ldu, int64_t n, int mk,
+                                                      const double* __restrict__ c, double alpha, int accum,
+                                                      double* __restrict__ out) {
+  extern __shared__ double cs[];
+  for (int k = threadIdx.x; k < mk; k += blockDim.x) cs[k] = c[k];
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = (int64_t)gridDim.x * 8;
+  for (int64_t r = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5); r < n; r += nw) {
+    const double2* u2 = reinterpret_cast<const double2*>(U + r * ldu);
+    double acc = 0.0;
+    for (int k2 = lane; 2 * k2 < mk; k2 += 32) {
+      const double2 u = __ldg(u2 + k2);
+      acc = fma(u.x, cs[2 * k2], acc);
+      acc = fma(u.y, cs[2 * k2 + 1], acc);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) out[r] = alpha * acc + (accum ? out[r] : 0.0);
+  }
+}
+
+// Ct[c][k] = alpha sum_s part[s][c][k]: a warp per output, lanes over the splits (fixed order:
+// lane-strided partial sums, then a fixed shuffle tree)
 __global__ void la_tsreduce_kernel(const double* __restrict__ part, int nsplit, int ncol, int mk, double* __restrict__ Ct,
                                    double alpha) {
   const int64_t tot = (int64_t)ncol * mk;
-  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < tot; e += (int64_t)gridDim.x * blockDim.x) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t e = (int64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5); e < tot;
+       e += (int64_t)gridDim.x * (blockDim.x / 32)) {
     double s = 0.0;
-    for (int q = 0; q < nsplit; ++q) s += part[(size_t)q * tot + e];
-    Ct[e] = alpha * s;
+    for (int q = lane; q < nsplit; q += 32) s += part[(size_t)q * tot + e];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) Ct[e] = alpha * s;
   }
 }
 
@@ -938,6 +1058,8 @@ cudaError_t launch_la_tsgemm(const double* U, int64_t ldu, int mk, int64_t n, co
     la_tsgemm_kernel<1><<<grid, 256, 0, s>>>(U, ldu, mk, n, V, ncol, vrow, rs, rows_per, part);
   else if (ncol <= 8)
     la_tsgemm_kernel<8><<<grid, 256, 0, s>>>(U, ldu, mk, n, V, ncol, vrow, rs, rows_per, part);
+  else if (ncol <= 64 && !vrow)
+    la_tsgemm_dmma_kernel<<<grid, 256, 0, s>>>(U, ldu, mk, n, V, ncol, rs, rows_per, part);
   else if (ncol <= 16)
     la_tsgemm_kernel<16><<<grid, 256, 0, s>>>(U, ldu, mk, n, V, ncol, vrow, rs, rows_per, part);
   else if (ncol <= 32)
@@ -946,7 +1068,7 @@ cudaError_t launch_la_tsgemm(const double* U, int64_t ldu, int mk, int64_t n, co
     la_tsgemm_kernel<64><<<grid, 256, 0, s>>>(U, ldu, mk, n, V, ncol, vrow, rs, rows_per, part);
   else
     return cudaErrorInvalidValue;
-  la_tsreduce_kernel<<<grid_for((int64_t)ncol * mk), 256, 0, s>>>(part, ns, ncol, mk, Ct, alpha);
+  la_tsreduce_kernel<<<grid_for((int64_t)ncol * mk * 32), 256, 0, s>>>(part, ns, ncol, mk, Ct, alpha);
   return cudaGetLastError();
 }
 
@@ -1053,6 +1175,16 @@ cudaError_t launch_la_slq(const double* hist_a, const double* hist_b, const int*
   return cudaGetLastError();
 }
 
+cudaError_t launch_la_gemv(const double* U, int64_t ldu, int64_t n, int mk, const double* c, double alpha, int accum,
+                           double* out, cudaStream_t s) {
+  if (mk == 0 || n == 0) return cudaSuccess;
+  if (mk & 1) return cudaErrorInvalidValue;  // mk is a multiple of 8
+  int64_t blocks = (n + 7) / 8;
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  la_gemv_kernel<<<(unsigned)blocks, 256, mk * sizeof(double), s>>>(U, ldu, n, mk, c, alpha, accum, out);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_la_bapply(const int32_t* nbr, const double* Bc, int mv, int64_t n, const double* D, const double* b,
                              double* s, cudaStream_t st) {
   la_bapply_kernel<<<grid_for(n), 256, 0, st>>>(nbr, Bc, mv, n, D, b, s);
@@ -1114,6 +1246,8 @@ static int la_lvl_blocks(const void* fn) {
     if (per_sm < 1) per_sm = 1;
     if (cap > 0 && per_sm > cap) per_sm = cap;
     cached[idx] = sms * per_sm;
+    static const char* ctas_env = getenv("VIF_LA_LVL_CTAS");  // experiment: fewer CTAs, cheaper barrier
+    if (ctas_env && atoi(ctas_env) > 0 && atoi(ctas_env) < cached[idx]) cached[idx] = atoi(ctas_env);
   }
   return cached[idx];
 }

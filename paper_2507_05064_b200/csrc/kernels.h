@@ -156,6 +156,8 @@ cudaError_t launch_la_transpose(const double* in, int rows, int cols, int ldin, 
 cudaError_t launch_la_logdiag(const double* A, int m, int lda, double* out, cudaStream_t s);
 cudaError_t launch_la_slq(const double* hist_a, const double* hist_b, const int* iters, int ncol, int kmax,
                           double* scratch, double* out, cudaStream_t s);
+cudaError_t launch_la_gemv(const double* U, int64_t ldu, int64_t n, int mk, const double* c, double alpha, int accum,
+                           double* out, cudaStream_t s);
 cudaError_t launch_la_bapply(const int32_t* nbr, const double* Bc, int mv, int64_t n, const double* D, const double* b,
                              double* s, cudaStream_t st);
 cudaError_t launch_la_finish(const double* fin, const double* slq, int64_t n, int ell, double* out, cudaStream_t s);

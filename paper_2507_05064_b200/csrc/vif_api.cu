@@ -559,8 +559,12 @@ int la_sigma(LaCtx& c, int ncol, const double* v, double* out, const double* win
              "U^T v");
   LA_TRY(la_btinv(c, ncol, v, c.d(L_T1)));
   LA_TRY(la_binv(c, ncol, c.d(L_T1), c.d(L_D), winv ? c.d(L_T2) : out, v, winv, winv ? out : nullptr));
-  if (P.mk > 0)
-    VIF_CUDA(h, launch_gemm_tn(c.U(), P.ld, P.n, c.d(L_CT), P.mk, ncol, P.mk, 0, out, ncol, 1.0, 1, c.s), "U C");
+  if (P.mk > 0) {
+    if (ncol == 1)
+      VIF_CUDA(h, launch_la_gemv(c.U(), P.ld, P.n, P.mk, c.d(L_CT), 1.0, 1, out, c.s), "U c");
+    else
+      VIF_CUDA(h, launch_gemm_tn(c.U(), P.ld, P.n, c.d(L_CT), P.mk, ncol, P.mk, 0, out, ncol, 1.0, 1, c.s), "U C");
+  }
   return VIF_OK;
 }
 
@@ -602,7 +606,11 @@ int la_fitc_solve(LaCtx& c, int ncol, const double* w, double* out) {
            "U^T D_V^-1 w");
   VIF_CUDA(h, launch_gemm_tn(c.d(L_CT), P.mk, ncol, c.d(L_MVINV), P.mk, P.mk, P.mk, 0, c.d(L_CT2), P.mk, 1.0, 0, c.s),
            "M_V^-1 C");
-  VIF_CUDA(h, launch_gemm_tn(c.U(), P.ld, P.n, c.d(L_CT2), P.mk, ncol, P.mk, 0, c.d(L_T1), ncol, 1.0, 0, c.s), "U C");
+  if (ncol == 1)
+    VIF_CUDA(h, launch_la_gemv(c.U(), P.ld, P.n, P.mk, c.d(L_CT2), 1.0, 0, c.d(L_T1), c.s), "U c");
+  else
+    VIF_CUDA(h, launch_gemm_tn(c.U(), P.ld, P.n, c.d(L_CT2), P.mk, ncol, P.mk, 0, c.d(L_T1), ncol, 1.0, 0, c.s),
+             "U C");
   VIF_CUDA(h, launch_la_sub_rowscale(w, c.d(L_T1), c.d(L_DVINV), P.n, ncol, out, c.s), "FITC tail");
   return VIF_OK;
 }

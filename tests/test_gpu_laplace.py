@@ -46,7 +46,8 @@ def rel_err(a, b):
 
 
 @pytest.mark.parametrize("n,m,mv,ncol", [(700, 37, 13, 1), (700, 37, 13, 5), (513, 64, 31, 8), (400, 0, 12, 3),
-                                         (300, 9, 0, 2), (257, 20, 40, 1)])
+                                         (300, 9, 0, 2), (257, 20, 40, 1), (700, 37, 13, 20), (450, 70, 12, 64),
+                                         (700, 37, 9, 33)])
 def test_operators(n, m, mv, ncol):
     p = vif()
     w = work(n, m, mv, seed=n + mv)
