@@ -418,6 +418,42 @@ __global__ void la_reorder_bwd_kernel(const int* __restrict__ order, const int* 
 // Row r: out_r = s_r v_r - sum_k val[k] out[col[k]] over its entries k (forward: k = r*mv + p with
 // col = N(r)_p, val = B[r,p], entries with col < 0 skipped; backward: k in [tptr[r], tptr[r+1]),
 // col = trow, val = tval).  Reads of other rows go to L2 (__ldcg; rows written in earlier levels).
+// A warp's first row of the next level does not depend on the current level: its index, its first 32
+// entries and its right-hand side are loaded before the barrier, so after it only the gathers of
+// x remain on the row's dependency chain.
+struct LaRowPre {
+  int64_t r;
+  int k0, k1, jl;
+  double bl, sr, v0, v1, w2r, u0, u1;
+};
+
+template <bool FWD>
+__device__ __forceinline__ bool la_row_load(int q, int qend, const int* __restrict__ order,
+                                            const int32_t* __restrict__ ecol, const double* __restrict__ eval,
+                                            const int* __restrict__ eptr, int mv, int ncol,
+                                            const double* __restrict__ v, const double* __restrict__ s,
+                                            const double* __restrict__ v2, const double* __restrict__ w2, int lane,
+                                            LaRowPre& o) {
+  if (q >= qend) return false;
+  o.r = order[q];
+  o.k0 = FWD ? q * mv : eptr[q];
+  o.k1 = FWD ? o.k0 + mv : eptr[q + 1];
+  const int k = o.k0 + lane;
+  o.jl = k < o.k1 ? ecol[k] : -1;
+  o.bl = k < o.k1 ? eval[k] : 0.0;
+  o.sr = s ? s[o.r] : 1.0;
+  const int c0 = ncol == 1 ? 0 : lane, c1 = lane + 32;
+  o.v0 = c0 < ncol ? v[o.r * ncol + c0] : 0.0;
+  o.v1 = c1 < ncol ? v[o.r * ncol + c1] : 0.0;
+  o.w2r = o.u0 = o.u1 = 0.0;
+  if (v2 && w2) {  // only with out2 (the caller passes v2 = v even without the W^{-1} term)
+    o.w2r = w2[o.r];
+    o.u0 = c0 < ncol ? v2[o.r * ncol + c0] : 0.0;
+    o.u1 = c1 < ncol ? v2[o.r * ncol + c1] : 0.0;
+  }
+  return true;
+}
+
 template <bool FWD>
 __global__ void __launch_bounds__(LA_THREADS) la_trsv_lvl_kernel(
     const int* __restrict__ order, const int* __restrict__ lptr, int nlev, const int32_t* __restrict__ ecol,
@@ -430,52 +466,61 @@ __global__ void __launch_bounds__(LA_THREADS) la_trsv_lvl_kernel(
   const int lane = threadIdx.x & 31;
   const int nw = gridDim.x * LA_WARPS;
   const int w0 = blockIdx.x * LA_WARPS + (threadIdx.x >> 5);
+  LaRowPre pre;
+  bool have = la_row_load<FWD>(lptr[0] + w0, lptr[1], order, ecol, eval, eptr, mv, ncol, v, s, v2, w2, lane, pre);
   for (int L = 0; L < nlev; ++L) {
-    const int a = lptr[L], b = lptr[L + 1];
-    for (int q = a + w0; q < b; q += nw) {
-      const int64_t r = order[q];
-      const int k0 = FWD ? q * mv : eptr[q];  // entries stored in level order (la_reorder_*)
-      const int k1 = FWD ? k0 + mv : eptr[q + 1];
-      const double sr = s ? s[r] : 1.0;
+    const int b = lptr[L + 1];
+    int q = lptr[L] + w0;
+    while (have) {
+      const LaRowPre& o = pre;
+      const int64_t r = o.r;
       if (ncol == 1) {
         double acc = 0.0;
-        for (int k = k0 + lane; k < k1; k += 32) {
+        if (o.jl >= 0) acc = o.bl * x[o.jl];
+        for (int k = o.k0 + 32 + lane; k < o.k1; k += 32) {
           const int j = ecol[k];
           if (j >= 0) acc = fma(eval[k], x[j], acc);
         }
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
         if (lane == 0) {
-          const double xr = sr * v[r] - acc;
+          const double xr = o.sr * o.v0 - acc;
           __stcg(x + r, xr);
-          if (out2) out2[r] = xr + w2[r] * v2[r];
+          if (out2) out2[r] = xr + o.w2r * o.u0;
         }
       } else {
         double acc0 = 0.0, acc1 = 0.0;
-        if (k1 - k0 <= long_min) {
-          for (int kb = k0; kb < k1; kb += 32) {
+        if (o.k1 - o.k0 <= long_min) {
+          la_gather_cols_weak(x, ncol, lane, o.jl, o.bl, o.k1 - o.k0 < 32 ? o.k1 - o.k0 : 32, acc0, acc1);
+          for (int kb = o.k0 + 32; kb < o.k1; kb += 32) {
             const int k = kb + lane;
-            const int jl = k < k1 ? ecol[k] : -1;
-            const double bl = k < k1 ? eval[k] : 0.0;
-            la_gather_cols_weak(x, ncol, lane, jl, bl, k1 - kb < 32 ? k1 - kb : 32, acc0, acc1);
+            const int jl = k < o.k1 ? ecol[k] : -1;
+            const double bl = k < o.k1 ? eval[k] : 0.0;
+            la_gather_cols_weak(x, ncol, lane, jl, bl, o.k1 - kb < 32 ? o.k1 - kb : 32, acc0, acc1);
           }
         } else {
-          la_long_row(x, ncol, ecol, eval, k0, k1, lane, sm_red[threadIdx.x >> 5], sm_col[threadIdx.x >> 5], acc0,
-                      acc1);
+          la_long_row(x, ncol, ecol, eval, o.k0, o.k1, lane, sm_red[threadIdx.x >> 5], sm_col[threadIdx.x >> 5],
+                      acc0, acc1);
         }
         const int c1 = lane + 32;
         if (lane < ncol) {
-          const double xr = sr * v[r * ncol + lane] - acc0;
+          const double xr = o.sr * o.v0 - acc0;
           __stcg(x + r * ncol + lane, xr);
-          if (out2) out2[r * ncol + lane] = xr + w2[r] * v2[r * ncol + lane];
+          if (out2) out2[r * ncol + lane] = xr + o.w2r * o.u0;
         }
         if (c1 < ncol) {
-          const double xr = sr * v[r * ncol + c1] - acc1;
+          const double xr = o.sr * o.v1 - acc1;
           __stcg(x + r * ncol + c1, xr);
-          if (out2) out2[r * ncol + c1] = xr + w2[r] * v2[r * ncol + c1];
+          if (out2) out2[r * ncol + c1] = xr + o.w2r * o.u1;
         }
       }
+      q += nw;
+      have = la_row_load<FWD>(q, b, order, ecol, eval, eptr, mv, ncol, v, s, v2, w2, lane, pre);
     }
+    // the first row of the next level: prefetched before the barrier
+    if (L + 1 < nlev)
+      have = la_row_load<FWD>(lptr[L + 1] + w0, lptr[L + 2], order, ecol, eval, eptr, mv, ncol, v, s, v2, w2, lane,
+                              pre);
     grid.sync();
     if (dbg && blockIdx.x == 0 && threadIdx.x == 0) {
       unsigned long long t;
