@@ -519,6 +519,202 @@ __global__ void __launch_bounds__(GW * 32, 4) grad_param_kernel(
   }
 }
 
+// ---- adjoint form of the per-parameter pass ----
+// Every term of a point's contribution is linear in (dC_S, dU_S) with parameter-independent coefficients
+// (from L, A_i, D_i, gam of the state).  With a~ = (-A_i, 1) over S = (N(i), i), gam_k = g_i . U_aug[S_k],
+// beta~ = (C_NN^{-1} gam_N, 0), Dm = D_i^{-1/2}:
+//   dD_i = a~^T dC a~,  dA_i = C_NN^{-1} [dC a~]_N,  so (1/2) dD/D + sum_k dc_k gam_k = tr(M dC) with
+//   M = mu a~ a~^T - Dm (beta~ a~^T + a~ beta~^T) / 2,  mu = 1/(2 D) - Dm^3 (a~ . gam) / 2;
+//   with dC = dK_S (+ I for the nugget) - (dU_S U_S^T + U_S dU_S^T) and the term Dm a~_k g_i . dU_S_k:
+//   contribution = sum_{a,b} w_a a~_b dK_ab + rho . (sum_b a~_b dU_b) + sig . (sum_b beta~_b dU_b),
+//   w = mu a~ - Dm beta~,  rho = -2 mu p + Dm (q + g_i),  sig = Dm p,  p = sum_b a~_b U_b,  q = sum_b beta~_b U_b.
+// The cross-Gram (s^2 m DMMA work per parameter) becomes two gathered sums (2 s m).
+constexpr int ADJ_STRIDE = 40;  // per point: mu, Dm, beta~[0..SP)
+
+template <int RB>
+__global__ void __launch_bounds__(GW * 32) grad_adjoint_kernel(const double* __restrict__ U,
+                                                                const double* __restrict__ Gam, int64_t ldu, int mk,
+                                                                int ld, const int32_t* __restrict__ nbr, int mv,
+                                                                const int64_t* __restrict__ order, int64_t npts,
+                                                                const double* __restrict__ state,
+                                                                double* __restrict__ rho, double* __restrict__ sig,
+                                                                double* __restrict__ adj) {
+  constexpr int SP = RB * 8;
+  constexpr int LP = SP * (SP + 1) / 2;
+  __shared__ int Sidx_all[GW][SP];
+  __shared__ double at_all[GW][SP], bt_all[GW][SP];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t pos = (int64_t)blockIdx.x * GW + warp;
+  if (pos >= npts) return;
+  const int64_t i = order[pos];
+  const int nb0 = lane < mv ? nbr[i * mv + lane] : -1;
+  const int q = __popc(__ballot_sync(0xffffffffu, nb0 >= 0));
+  const int myidx = lane < q ? nb0 : (lane == q ? (int)i : -1);
+  int* Sidx = Sidx_all[warp];
+  double* at = at_all[warp];
+  double* bt = bt_all[warp];
+  if (lane < SP) Sidx[lane] = myidx;
+  const double* st = state + pos * (int64_t)state_doubles<RB>();
+  const double a = lane < SP ? st[LP + lane] : 0.0;
+  const double myinv = lane < SP ? st[LP + SP + lane] : 1.0;
+  const double gam = lane < SP ? st[LP + 2 * SP + lane] : 0.0;
+  const double Di = st[LP + 3 * SP];
+  const double atl = lane < q ? -a : (lane == q ? 1.0 : 0.0);
+  double ag = atl * gam;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) ag += __shfl_xor_sync(0xffffffffu, ag, o);
+  const double Dm = rsqrt_nr(Di);
+  const double mu = 0.5 / Di - 0.5 * Dm * Dm * Dm * ag;
+  // beta = C_NN^{-1} gam_N = L_NN^{-T} L_NN^{-1} gam_N (rows of L packed in the state)
+  double y = lane < q ? gam : 0.0;
+  for (int j = 0; j < q; ++j) {
+    const double yj = __shfl_sync(0xffffffffu, y * myinv, j);
+    if (lane == j) y = yj;
+    else if (lane > j && lane < q) y = fma(-st[lane * (lane + 1) / 2 + j], yj, y);
+  }
+  for (int j = q - 1; j >= 0; --j) {
+    const double xj = __shfl_sync(0xffffffffu, y * myinv, j);
+    if (lane == j) y = xj;
+    else if (lane < j) y = fma(-st[j * (j + 1) / 2 + lane], xj, y);
+  }
+  const double btl = lane < q ? y : 0.0;
+  if (lane < SP) {
+    at[lane] = atl;
+    bt[lane] = btl;
+  }
+  double* ad = adj + pos * (int64_t)ADJ_STRIDE;
+  if (lane < SP) ad[2 + lane] = btl;
+  if (lane == 0) {
+    ad[0] = mu;
+    ad[1] = Dm;
+  }
+  __syncwarp();
+  const int s = q + 1;
+  const double* grow = Gam + pos * (int64_t)ld;
+  double* rrow = rho + pos * (int64_t)mk;
+  double* srow = sig + pos * (int64_t)mk;
+  for (int k = lane; k < mk; k += 32) {
+    double pk = 0.0, qk = 0.0;
+    for (int b = 0; b < s; ++b) {
+      const double u = __ldg(U + (int64_t)Sidx[b] * ldu + k);
+      pk = fma(at[b], u, pk);
+      qk = fma(bt[b], u, qk);
+    }
+    rrow[k] = fma(-2.0 * mu, pk, Dm * (qk + __ldg(grow + k)));
+    srow[k] = Dm * pk;
+  }
+}
+
+template <int FAM, int RB>
+__global__ void __launch_bounds__(GW * 32) grad_param_adj_kernel(
+    const double* __restrict__ dU, int64_t ldu, int mk, const double* __restrict__ X, const int32_t* __restrict__ nbr,
+    int mv, const int64_t* __restrict__ order, int64_t npts, CovParams p, int pidx, const double* __restrict__ state,
+    const double* __restrict__ rho, const double* __restrict__ sig, const double* __restrict__ adj,
+    double* __restrict__ part) {
+  constexpr int SP = RB * 8;
+  constexpr int LP = SP * (SP + 1) / 2;
+  __shared__ int Sidx_all[GW][SP];
+  __shared__ double at_all[GW][SP], bt_all[GW][SP], w_all[GW][SP];
+  __shared__ double xs_all[GW][SP * VIF_MAX_D];
+  __shared__ double wsum[GW];
+  __shared__ double tbl[64];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t pos = (int64_t)blockIdx.x * GW + warp;
+  exp_table_init(tbl, p.sigma2, threadIdx.x);
+  __syncthreads();
+  double contrib = 0.0;
+  if (pos < npts) {
+    const int64_t i = order[pos];
+    const int nb0 = lane < mv ? nbr[i * mv + lane] : -1;
+    const int q = __popc(__ballot_sync(0xffffffffu, nb0 >= 0));
+    const int s = q + 1;
+    const int myidx = lane < q ? nb0 : (lane == q ? (int)i : -1);
+    int* Sidx = Sidx_all[warp];
+    double* at = at_all[warp];
+    double* bt = bt_all[warp];
+    double* wv = w_all[warp];
+    double* xs = xs_all[warp];
+    if (lane < SP) Sidx[lane] = myidx;
+    if (lane < s)
+      for (int k = 0; k < p.d; ++k) xs[lane * p.d + k] = X[(int64_t)myidx * p.d + k] * (fam_scale<FAM>() * p.inv_ls[k]);
+    const double* st = state + pos * (int64_t)state_doubles<RB>();
+    const bool ok = st[LP + 3 * SP + 1] != 0.0;
+    const double* ad = adj + pos * (int64_t)ADJ_STRIDE;
+    const double mu = ad[0], Dm = ad[1];
+    if (lane < SP) {
+      const double atl = lane < q ? -st[LP + lane] : (lane == q ? 1.0 : 0.0);
+      const double btl = ad[2 + lane];
+      at[lane] = atl;
+      bt[lane] = btl;
+      wv[lane] = fma(mu, atl, -Dm * btl);
+    }
+    __syncwarp();
+    // sum_{a,b} w_a a~_b dK_ab over the lower triangle (dK symmetric); nugget: dK = I
+    double acc = 0.0;
+    const int ne = s * (s + 1) / 2;
+    for (int e = lane; e < ne; e += 32) {
+      int r = (int)((sqrtf_fast(8.0f * (float)e + 1.0f) - 1.0f) * 0.5f);
+      if ((r + 1) * (r + 2) / 2 <= e) ++r;
+      if (r * (r + 1) / 2 > e) --r;
+      const int c = e - r * (r + 1) / 2;
+      const double coef = r == c ? wv[r] * at[r] : fma(wv[r], at[c], wv[c] * at[r]);
+      double dk;
+      if (pidx <= p.d) dk = dcov_fast<FAM>(xs + r * p.d, xs + c * p.d, pidx, p, tbl);
+      else dk = r == c ? 1.0 : 0.0;
+      acc = fma(coef, dk, acc);
+    }
+    if (dU) {
+      const double* rrow = rho + pos * (int64_t)mk;
+      const double* srow = sig + pos * (int64_t)mk;
+      for (int k = lane; k < mk; k += 32) {
+        double e1 = 0.0, e2 = 0.0;
+        for (int b = 0; b < s; ++b) {
+          const double du = __ldg(dU + (int64_t)Sidx[b] * ldu + k);
+          e1 = fma(at[b], du, e1);
+          e2 = fma(bt[b], du, e2);
+        }
+        acc = fma(e1, __ldg(rrow + k), fma(e2, __ldg(srow + k), acc));
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    contrib = ok ? acc : __longlong_as_double(0x7ff8000000000000LL);
+  }
+  if (lane == 0) wsum[warp] = contrib;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double sum = 0.0;
+    for (int w = 0; w < GW; ++w) sum += wsum[w];
+    part[blockIdx.x] = sum;
+  }
+}
+
+template <int RB>
+cudaError_t launch_adj_rb(const GradPointArgs& a, cudaStream_t s) {
+  const unsigned blocks = (unsigned)((a.npts + GW - 1) / GW);
+  grad_adjoint_kernel<RB><<<blocks, GW * 32, 0, s>>>(a.U, a.Gam, a.ldu, a.mk, a.ld, a.nbr, a.mv, a.order, a.npts,
+                                                     a.state, a.rho, a.sig, a.adj);
+  return cudaGetLastError();
+}
+
+template <int FAM, int RB>
+cudaError_t launch_param_adj_rb(const GradPointArgs& a, cudaStream_t s) {
+  const unsigned blocks = (unsigned)((a.npts + GW - 1) / GW);
+  grad_param_adj_kernel<FAM, RB><<<blocks, GW * 32, 0, s>>>(a.dU, a.ldu, a.mk, a.X, a.nbr, a.mv, a.order, a.npts,
+                                                            a.p, a.pidx, a.state, a.rho, a.sig, a.adj, a.part);
+  return cudaGetLastError();
+}
+
+template <int FAM>
+cudaError_t launch_param_adj_fam(const GradPointArgs& a, cudaStream_t s) {
+  switch ((a.mv + 1 + 7) / 8) {
+    case 1: return launch_param_adj_rb<FAM, 1>(a, s);
+    case 2: return launch_param_adj_rb<FAM, 2>(a, s);
+    case 3: return launch_param_adj_rb<FAM, 3>(a, s);
+    default: return launch_param_adj_rb<FAM, 4>(a, s);
+  }
+}
+
 template <int FAM, int RB>
 cudaError_t launch_grad_rb(const GradPointArgs& a, bool state_pass, cudaStream_t s) {
   const size_t smem = (size_t)GW * grad_warp_doubles<RB>(a.p.d) * sizeof(double);
@@ -585,6 +781,35 @@ cudaError_t launch_grad_points(const GradPointArgs& a, double* out, cudaStream_t
   if (a.mv > 31) return cudaErrorNotSupported;
   if (a.npts > 0) {
     cudaError_t e = launch_grad_any(a, false, s);
+    if (e != cudaSuccess) return e;
+  }
+  grad_reduce_kernel<<<1, 1024, 0, s>>>(a.part, grad_point_nparts(a.npts), out);
+  return cudaGetLastError();
+}
+
+size_t grad_adj_doubles() { return ADJ_STRIDE; }
+
+cudaError_t launch_grad_adjoint(const GradPointArgs& a, cudaStream_t s) {
+  if (a.mv > 31) return cudaErrorNotSupported;
+  if (a.npts == 0) return cudaSuccess;
+  switch ((a.mv + 1 + 7) / 8) {
+    case 1: return launch_adj_rb<1>(a, s);
+    case 2: return launch_adj_rb<2>(a, s);
+    case 3: return launch_adj_rb<3>(a, s);
+    default: return launch_adj_rb<4>(a, s);
+  }
+}
+
+cudaError_t launch_grad_points_adj(const GradPointArgs& a, double* out, cudaStream_t s) {
+  if (a.mv > 31) return cudaErrorNotSupported;
+  if (a.npts > 0) {
+    cudaError_t e;
+    switch (a.p.family) {
+      case FAM_M12: e = launch_param_adj_fam<FAM_M12>(a, s); break;
+      case FAM_M32: e = launch_param_adj_fam<FAM_M32>(a, s); break;
+      case FAM_M52: e = launch_param_adj_fam<FAM_M52>(a, s); break;
+      default: e = launch_param_adj_fam<FAM_GAUSS>(a, s); break;
+    }
     if (e != cudaSuccess) return e;
   }
   grad_reduce_kernel<<<1, 1024, 0, s>>>(a.part, grad_point_nparts(a.npts), out);

@@ -80,11 +80,18 @@ struct GradPointArgs {
   int pidx;      // 0: sigma_1^2, 1..d: lambda_j, d+1: nugget
   double* part;  // grad_point_nparts(npts) block partials
   double* state; // npts x grad_state_doubles(mv): per-point state of the first pass
+  // adjoint form (k_grad.cu): rho, sig (npts x mk) and mu, Dm, beta~ (npts x grad_adj_doubles())
+  double* rho = nullptr;
+  double* sig = nullptr;
+  double* adj = nullptr;
 };
 int64_t grad_point_nparts(int64_t npts);
 size_t grad_state_doubles(int mv);
 cudaError_t launch_grad_state(const GradPointArgs& a, cudaStream_t s);
 cudaError_t launch_grad_points(const GradPointArgs& a, double* out, cudaStream_t s);
+size_t grad_adj_doubles();
+cudaError_t launch_grad_adjoint(const GradPointArgs& a, cudaStream_t s);
+cudaError_t launch_grad_points_adj(const GradPointArgs& a, double* out, cudaStream_t s);
 cudaError_t launch_dkm(const double* Z, int m, int mk, int pidx, const CovParams& p, double* out, cudaStream_t s);
 cudaError_t launch_phi_low(const double* Phi, int mk, double* out, cudaStream_t s);
 cudaError_t launch_kx_deriv(const double* X, const double* Z, int64_t npos, int m, int mk, int pidx,

@@ -372,7 +372,7 @@ int set_data(Handle* h, const double* X, const double* Z, const int32_t* nbr, co
 
 // ---------------------------------------------------------------- gradient workspace
 enum GBuf { G_Q2, G_GAM, G_DU, G_DKM, G_TT, G_PHI, G_PHILOW, G_LINVM, G_MCOPY, G_TSCR, G_ZH, G_Z, G_PART, G_OUT,
-            G_STATE, G_COUNT };
+            G_STATE, G_RHO, G_SIG, G_ADJ, G_COUNT };
 
 Layout make_grad_layout(const Plan& P) {
   Layout L{};
@@ -388,6 +388,8 @@ Layout make_grad_layout(const Plan& P) {
   L.size[G_PART] = (size_t)grad_point_nparts(P.npos) * D8;
   L.size[G_OUT] = (size_t)(P.d + 2) * (P.emulate ? P.world : 1) * D8;
   L.size[G_STATE] = (size_t)P.npos * grad_state_doubles(P.mv) * D8;
+  L.size[G_RHO] = L.size[G_SIG] = (size_t)P.npos * mk1 * D8;
+  L.size[G_ADJ] = (size_t)P.npos * grad_adj_doubles() * D8;
   size_t off = 0;
   for (int b = 0; b < G_COUNT; ++b) {
     L.off[b] = off;
@@ -1237,7 +1239,14 @@ int vif_grad(void* handle, const vif_theta* theta, void* gws, size_t gws_bytes, 
     a.pidx = -1;
     a.part = gbuf(G_PART);
     a.state = gbuf(G_STATE);
+    a.rho = gbuf(G_RHO);
+    a.sig = gbuf(G_SIG);
+    a.adj = gbuf(G_ADJ);
     VIF_CUDA(h, launch_grad_state(a, s), "gradient state");
+    // adjoint vectors (default) or the cross-Gram pass per parameter (VIF_GRAD_CROSS=1)
+    static const char* cross_env = getenv("VIF_GRAD_CROSS");
+    const bool cross = cross_env && cross_env[0] == '1';
+    if (!cross) VIF_CUDA(h, launch_grad_adjoint(a, s), "gradient adjoint");
     for (int pi = 0; pi < nparam; ++pi) {
       const bool kernel_param = pi <= P.d;
       const double* dUp = nullptr;
@@ -1261,7 +1270,10 @@ int vif_grad(void* handle, const vif_theta* theta, void* gws, size_t gws_bytes, 
       }
       a.dU = dUp;
       a.pidx = pi;
-      VIF_CUDA(h, launch_grad_points(a, gbuf(G_OUT) + (size_t)g * nparam + pi, s), "gradient points");
+      if (cross)
+        VIF_CUDA(h, launch_grad_points(a, gbuf(G_OUT) + (size_t)g * nparam + pi, s), "gradient points");
+      else
+        VIF_CUDA(h, launch_grad_points_adj(a, gbuf(G_OUT) + (size_t)g * nparam + pi, s), "gradient points");
     }
   }
   if (nrep > 1) {
