@@ -82,8 +82,11 @@ __global__ void __launch_bounds__(256) kx_eval_d_kernel(const double* __restrict
 #pragma unroll
     for (int k = 0; k < D; ++k) x[k] = valid ? X[i * D + k] * sc[k] : 0.0;
     double* srow = S + pos * (int64_t)lds;
-#pragma unroll 4
-    for (int b = lane; b < mk; b += 32) {
+    if (!valid) {
+      for (int b = lane; b < mk; b += 32) srow[b] = 0.0;
+      continue;
+    }
+    auto eval = [&](int b) -> double {
       const double* z = kx_zs + b * D;
       double t2;
       {
@@ -95,16 +98,15 @@ __global__ void __launch_bounds__(256) kx_eval_d_kernel(const double* __restrict
           t2 = fma(dk, dk, t2);
         }
       }
-      double v;
-      if (FAM == FAM_GAUSS) {
-        v = sig2_exp_neg(t2, tbl);
-      } else {
-        const double t = sqrt_fast(t2);
-        const double E = sig2_exp_neg(t, tbl);
-        v = FAM == FAM_M12 ? E : (FAM == FAM_M32 ? fma(E, t, E) : fma(E, fma(t2, 1.0 / 3.0, t), E));
-      }
-      srow[b] = (valid && b < m) ? v : 0.0;
-    }
+      if (FAM == FAM_GAUSS) return sig2_exp_neg(t2, tbl);
+      const double t = sqrt_fast(t2);
+      const double E = sig2_exp_neg(t, tbl);
+      return FAM == FAM_M12 ? E : (FAM == FAM_M32 ? fma(E, t, E) : fma(E, fma(t2, 1.0 / 3.0, t), E));
+    };
+    const int mfull = m & ~31;  // columns of whole 32-wide steps: no mask
+#pragma unroll 4
+    for (int b = lane; b < mfull; b += 32) srow[b] = eval(b);
+    for (int b = mfull + lane; b < mk; b += 32) srow[b] = b < m ? eval(b) : 0.0;
     if (valid) {
       double* urow = Uaug + i * (int64_t)ld;
       for (int c = mk + lane; c < ld; c += 32) urow[c] = (c == mk) ? y[i] : 0.0;
