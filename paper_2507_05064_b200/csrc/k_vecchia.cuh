@@ -328,7 +328,9 @@ __host__ __device__ constexpr int vreg_warp_doubles(int d) {
 }
 
 // SELF: the point's own row / coordinates come from Uq / Xq (prediction); false for the factor
-template <int FAM, int RB, int NB, int MINB, bool SELF = false>
+// DD > 0: the input dimension as a compile-time constant (the coordinate loops of the kernel
+// evaluations unroll and their index arithmetic folds; d = 2 is instantiated)
+template <int FAM, int RB, int NB, int MINB, bool SELF = false, int DD = 0>
 __global__ void __launch_bounds__(VW * 32, MINB) vecchia_reg_kernel(
     const double* __restrict__ U, int64_t ldu, int mk, int ld, const double* __restrict__ X,
     const double* __restrict__ Uq, const double* __restrict__ Xq, const int32_t* __restrict__ nbr, int mv, const int64_t* __restrict__ order, int64_t npts, CovParams p,
@@ -344,7 +346,8 @@ __global__ void __launch_bounds__(VW * 32, MINB) vecchia_reg_kernel(
   exp_table_init(tbl, p.sigma2, threadIdx.x);
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  double* C = vsm + warp * vreg_warp_doubles<RB>(p.d);
+  const int dd = DD > 0 ? DD : p.d;
+  double* C = vsm + warp * vreg_warp_doubles<RB>(dd);
   double* colbuf = C + SP * CS;   // [2][SP]
   double* coef = colbuf + 2 * SP; // [SP]
   double* xs = coef + SP;         // [SP][d]
@@ -359,7 +362,7 @@ __global__ void __launch_bounds__(VW * 32, MINB) vecchia_reg_kernel(
   const int s = q + 1;
   const int myidx = lane < q ? nb0 : (lane == q ? (int)i : -1);
   if (lane < SP) Sidx[lane] = myidx;
-  stage_xs<FAM>(X, SELF ? Xq : X, myidx, p.d, p, lane, s, xs);
+  stage_xs<FAM>(X, SELF ? Xq : X, myidx, dd, p, lane, s, xs);
   __syncwarp();
 
   // ---- 1 + 2. Gram on DMMA; the kernel evaluations of step 2 (independent of the Gram) run
@@ -377,7 +380,7 @@ __global__ void __launch_bounds__(VW * 32, MINB) vecchia_reg_kernel(
   {
     double2 f[NB][RB];
     gram_fill<RB, NB>(rp, mk, f);
-    eval_lower<FAM, 4>(xs, s, CS, p.d, p.nugget, tbl, lane, C);
+    eval_lower<FAM, 4>(xs, s, CS, dd, p.nugget, tbl, lane, C);
     if (!(g_vif_debug & 1)) gram_drain<RB, NB>(rp, mk, acc, f);  // debug probe: bit 0 skips the Gram
     __syncwarp();
     int t = 0;
@@ -518,9 +521,11 @@ static cudaError_t launch_rb(const VecchiaArgs& a, cudaStream_t s) {
     if (a.Uself) {
       kern = vecchia_reg_kernel<FAM, RB, 3, 4, true>;
     } else {
+      static const char* gen_env = getenv("VIF_VECCHIA_GENERIC_D");
+      const bool d2 = a.p.d == 2 && !(gen_env && gen_env[0] == '1');
       switch (cfg) {
         case 24: kern = vecchia_reg_kernel<FAM, RB, 2, 4>; break;
-        default: kern = vecchia_reg_kernel<FAM, RB, 3, 4>; break;
+        default: kern = d2 ? vecchia_reg_kernel<FAM, RB, 3, 4, false, 2> : vecchia_reg_kernel<FAM, RB, 3, 4>; break;
       }
     }
     if (smem > 48 * 1024) {
