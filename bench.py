@@ -408,6 +408,9 @@ def main():
                          "flops_per_launch": fl_launch[dom], "avg_launch_ms": stage_avg[kern[dom]],
                          "per_kernel": {k: {"stage": kern[k], "avg_ms": stage_avg[kern[k]], "tflops": achieved[k],
                                             "frac": achieved[k] / FP64_PEAK_TFLOPS} for k in kern},
+                         "contractions_frac": {"U = K(X,Z) L_m^-T (K1)": achieved["ufeat"] / FP64_PEAK_TFLOPS,
+                                               "M Gram W^T W (K4)": achieved["syrk"] / FP64_PEAK_TFLOPS,
+                                               "north_star_target": 0.6},
                          "path_effective_tflops": total_flops / (ms_max * 1e-3) / 1e12 / 1.0,
                          "path_frac": total_flops / (ms_max * 1e-3) / 1e12 / FP64_PEAK_TFLOPS},
             "cpu_baseline": cpu,
