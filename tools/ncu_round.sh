@@ -2,7 +2,7 @@
 # Round-end ncu evidence at the bench configuration (config 3, n = 1M):
 #  1) launch list of the bench command (gpu__time_duration per launch, cold-cache, serialised)
 #  2) ncu --set full (with source) of the dominant kernels: vecchia_reg, gemm_tn, syrk, kx_eval
-CMD="python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-grad --npred 0"
+CMD="python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-grad --npred 0 --no-knn --la-n 0"
 $CMD > gpurun_out/ncu_plain.log 2>&1 && \
 ncu --metrics gpu__time_duration.sum --clock-control none --kernel-name-base demangled -k regex:vif:: -c 60 --csv \
     --log-file gpurun_out/launches.csv $CMD > gpurun_out/ncu_launch.log 2>&1
