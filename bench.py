@@ -471,7 +471,7 @@ def run_laplace(args, dev, stream):
     ops = {}
     for ncol in (1, ell):
         V = torch.randn(n, ncol, dtype=torch.float64, device=dev) if ncol > 1 else torch.randn(n, dtype=torch.float64, device=dev)
-        for op in ("btinv", "binv", "sigma"):
+        for op in ("btinv", "binv", "sigma", "sigma_inv"):
             lm.la_apply(op, V)
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record(stream)

@@ -226,7 +226,8 @@ typedef struct {
   double slq_iters_mean;
 } vif_la_terms;
 
-enum { VIF_LA_SIGMA = 0, VIF_LA_A = 1, VIF_LA_BINV = 2, VIF_LA_BTINV = 3, VIF_LA_FITC_SOLVE = 4 };
+enum { VIF_LA_SIGMA = 0, VIF_LA_A = 1, VIF_LA_BINV = 2, VIF_LA_BTINV = 3, VIF_LA_FITC_SOLVE = 4,
+       VIF_LA_SIGMA_INV = 5, VIF_LA_A1 = 6 };
 
 /* Size of the caller-owned device workspace for up to nprobe (<= 64) probe columns and max_cg CG
  * iterations per solve (~ (8 nprobe + 12 + m_v) n doubles plus n x ld for the FITC rows). */
@@ -239,8 +240,10 @@ int vif_la_prepare(void* handle, const vif_theta* theta, int32_t nprobe, int32_t
                    size_t ws_bytes);
 /* Operators of the path on ncol (<= max(1, nprobe)) device columns v (n x ncol) -> out:
  * VIF_LA_SIGMA Sigma_dagger v;  VIF_LA_A (W^{-1} + Sigma_dagger) v;  VIF_LA_BINV B^{-1} v;
- * VIF_LA_BTINV B^{-T} v;  VIF_LA_FITC_SOLVE P^{-1} v.  winv (device, n): W^{-1}, required by A and
- * FITC_SOLVE.  The triangular solves are sync-free (one warp per row, rows claimed in dependency order,
+ * VIF_LA_BTINV B^{-T} v;  VIF_LA_FITC_SOLVE P^{-1} v;  VIF_LA_SIGMA_INV Sigma_dagger^{-1} v and
+ * VIF_LA_A1 (W + Sigma_dagger^{-1}) v, the operator of (pcls1), by Woodbury with the latent
+ * factor: B^T D^{-1/2} [s - W_U M^{-1} W_U^T s], s = D^{-1/2} B v (sparse products, no solves).
+ * winv (device, n): W^{-1}, required by A, A1 and FITC_SOLVE.  The triangular solves are sync-free (one warp per row, rows claimed in dependency order,
  * release/acquire flags).  Synchronises.  Errors: INVALID_ARG, STATE, NOT_PD (M_V), CUDA. */
 int vif_la_apply(void* handle, void* workspace, int32_t op, int32_t ncol, const double* v, const double* winv,
                  double* out);

@@ -925,6 +925,60 @@ __global__ void la_bapply_kernel(const int32_t* __restrict__ nbr, const double* 
   }
 }
 
+// ---- Sigma_dagger^{-1} v = B^T D^{-1/2} [s - W_U M^{-1} W_U^T s], s = D^{-1/2} B v (Woodbury),
+// the (W + Sigma_dagger^{-1}) operator of (pcls1): sparse products with B and B^T, no solves.
+// s[i, c] = D_i^{-1/2} (v[i, c] + sum_p B[i,p] v[N(i)_p, c])
+__global__ void la_bapply_cols_kernel(const int32_t* __restrict__ nbr, const double* __restrict__ Bc, int mv,
+                                      int64_t n, int ncol, const double* __restrict__ D, const double* __restrict__ v,
+                                      double* __restrict__ s) {
+  const int64_t tot = n * ncol;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < tot; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e / ncol;
+    const int c = (int)(e % ncol);
+    double acc = v[e];
+    for (int p = 0; p < mv; ++p) {
+      const int j = nbr[i * mv + p];
+      if (j >= 0) acc = fma(Bc[i * mv + p], v[(int64_t)j * ncol + c], acc);
+    }
+    s[e] = acc * rsqrt(D[i]);
+  }
+}
+
+// z[i, c] = D_i^{-1/2} (s[i, c] - Y[ipos[i], c])  (Y rows by processing position)
+__global__ void la_woodbury_mid_kernel(const double* __restrict__ s, const double* __restrict__ Y,
+                                       const int* __restrict__ ipos, const double* __restrict__ D, int64_t n, int ncol,
+                                       double* __restrict__ z) {
+  const int64_t tot = n * ncol;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < tot; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e / ncol;
+    const int c = (int)(e % ncol);
+    const double y = Y ? Y[(int64_t)ipos[i] * ncol + c] : 0.0;
+    z[e] = (s[e] - y) * rsqrt(D[i]);
+  }
+}
+
+// out[j, c] = z[j, c] + sum_{children} tval[k] z[trow[k], c]  (+ w_j v[j, c] with w = 1/winv)
+__global__ void la_btapply_cols_kernel(const int* __restrict__ tptr, const int* __restrict__ trow,
+                                       const double* __restrict__ tval, int64_t n, int ncol,
+                                       const double* __restrict__ z, const double* __restrict__ winv,
+                                       const double* __restrict__ v, double* __restrict__ out) {
+  const int64_t tot = n * ncol;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < tot; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t j = e / ncol;
+    const int c = (int)(e % ncol);
+    double acc = z[e];
+    for (int k = tptr[j]; k < tptr[j + 1]; ++k) acc = fma(tval[k], z[(int64_t)trow[k] * ncol + c], acc);
+    if (winv) acc += v[e] / winv[j];
+    out[e] = acc;
+  }
+}
+
+// inverse of the processing order: ipos[order[p]] = p
+__global__ void la_invorder_kernel(const int64_t* __restrict__ order, int64_t n, int* __restrict__ ipos) {
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x)
+    ipos[order[p]] = (int)p;
+}
+
 // fin[0] = log p(y|b~), fin[1] = s.s, fin[2] = z.z, fin[3] = log det W, fin[4] = sum log D_V,
 // fin[5] = log det M_V; slq[c] = e1^T log(T_c) e1.  out = (nll, -log p, quad, logdet, logdet_W, logdet_P)
 // with L = -log p + quad / 2 + logdet / 2 and logdet from slq_v2
@@ -1227,6 +1281,26 @@ cudaError_t launch_la_gemv(const double* U, int64_t ldu, int64_t n, int mk, cons
   int64_t blocks = (n + 7) / 8;
   if (blocks > 148 * 8) blocks = 148 * 8;
   la_gemv_kernel<<<(unsigned)blocks, 256, mk * sizeof(double), s>>>(U, ldu, n, mk, c, alpha, accum, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_la_bapply_cols(const int32_t* nbr, const double* Bc, int mv, int64_t n, int ncol, const double* D,
+                                  const double* v, double* s, cudaStream_t st) {
+  la_bapply_cols_kernel<<<grid_for(n * ncol), 256, 0, st>>>(nbr, Bc, mv, n, ncol, D, v, s);
+  return cudaGetLastError();
+}
+cudaError_t launch_la_woodbury_mid(const double* s, const double* Y, const int* ipos, const double* D, int64_t n,
+                                   int ncol, double* z, cudaStream_t st) {
+  la_woodbury_mid_kernel<<<grid_for(n * ncol), 256, 0, st>>>(s, Y, ipos, D, n, ncol, z);
+  return cudaGetLastError();
+}
+cudaError_t launch_la_btapply_cols(const int* tptr, const int* trow, const double* tval, int64_t n, int ncol,
+                                   const double* z, const double* winv, const double* v, double* out, cudaStream_t st) {
+  la_btapply_cols_kernel<<<grid_for(n * ncol), 256, 0, st>>>(tptr, trow, tval, n, ncol, z, winv, v, out);
+  return cudaGetLastError();
+}
+cudaError_t launch_la_invorder(const int64_t* order, int64_t n, int* ipos, cudaStream_t st) {
+  la_invorder_kernel<<<grid_for(n), 256, 0, st>>>(order, n, ipos);
   return cudaGetLastError();
 }
 

@@ -165,6 +165,13 @@ cudaError_t launch_la_slq(const double* hist_a, const double* hist_b, const int*
                           double* scratch, double* out, cudaStream_t s);
 cudaError_t launch_la_gemv(const double* U, int64_t ldu, int64_t n, int mk, const double* c, double alpha, int accum,
                            double* out, cudaStream_t s);
+cudaError_t launch_la_bapply_cols(const int32_t* nbr, const double* Bc, int mv, int64_t n, int ncol, const double* D,
+                                  const double* v, double* s, cudaStream_t st);
+cudaError_t launch_la_woodbury_mid(const double* s, const double* Y, const int* ipos, const double* D, int64_t n,
+                                   int ncol, double* z, cudaStream_t st);
+cudaError_t launch_la_btapply_cols(const int* tptr, const int* trow, const double* tval, int64_t n, int ncol,
+                                   const double* z, const double* winv, const double* v, double* out, cudaStream_t st);
+cudaError_t launch_la_invorder(const int64_t* order, int64_t n, int* ipos, cudaStream_t st);
 cudaError_t launch_la_bapply(const int32_t* nbr, const double* Bc, int mv, int64_t n, const double* D, const double* b,
                              double* s, cudaStream_t st);
 cudaError_t launch_la_finish(const double* fin, const double* slq, int64_t n, int ell, double* out, cudaStream_t s);

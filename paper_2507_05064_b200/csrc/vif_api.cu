@@ -434,7 +434,8 @@ enum LBuf {
   L_B, L_D, L_FLAGS, L_TPTR, L_TPOS, L_CNT, L_CUR, L_TICKET, L_UN2, L_W, L_WINV, L_V, L_BM, L_A, L_DV, L_DVINV,
   L_S, L_GV, L_LVINV, L_LVT, L_MVINV, L_TSCR, L_GPART, L_TSPART, L_CT, L_CT2, L_RPART, L_SC, L_ACTIVE, L_ITERS,
   L_HA, L_HB, L_SLQS, L_X, L_R, L_Z, L_P, L_Q, L_T1, L_T2, L_RHS, L_E1T, L_GM, L_LMINV, L_TROW, L_TVAL, L_LEVF,
-  L_LEVB, L_ORDF, L_ORDB, L_LPTRF, L_LPTRB, L_ECF, L_EVF, L_ECB, L_EVB, L_EPB, L_COUNT
+  L_LEVB, L_ORDF, L_ORDB, L_LPTRF, L_LPTRB, L_ECF, L_EVF, L_ECB, L_EVB, L_EPB, L_IPOS,
+  L_LMINVT, L_T3, L_COUNT
 };
 // per-column scalar arrays inside L_SC (each kLaCols doubles)
 enum LScal { SC_RZ, SC_RZN, SC_PQ, SC_ALPHA, SC_BETA, SC_RR, SC_BN, SC_SLQ, SC_MISC, SC_OUT, SC_COUNT };
@@ -462,6 +463,9 @@ LaLayout make_la_layout(const Plan& P, int nprobe, int max_cg) {
   L.size[L_TVAL] = (size_t)n * mv1 * D8;
   L.size[L_LEVF] = L.size[L_LEVB] = L.size[L_ORDF] = L.size[L_ORDB] = (size_t)n * sizeof(int);
   L.size[L_LPTRF] = L.size[L_LPTRB] = L.size[L_EPB] = (size_t)(n + 1) * sizeof(int);
+  L.size[L_IPOS] = (size_t)n * sizeof(int);
+  L.size[L_LMINVT] = (size_t)mk1 * mk1 * D8;
+  L.size[L_T3] = (size_t)(P.npos > n ? P.npos : n) * ncol * D8;
   L.size[L_ECF] = L.size[L_ECB] = (size_t)n * mv1 * sizeof(int);
   L.size[L_EVF] = L.size[L_EVB] = (size_t)n * mv1 * D8;
   L.size[L_TICKET] = 64;
@@ -567,6 +571,33 @@ int la_sigma(LaCtx& c, int ncol, const double* v, double* out, const double* win
     else
       VIF_CUDA(h, launch_gemm_tn(c.U(), P.ld, P.n, c.d(L_CT), P.mk, ncol, P.mk, 0, out, ncol, 1.0, 1, c.s), "U C");
   }
+  return VIF_OK;
+}
+
+// out = Sigma_dagger^{-1} v (+ W v with W = 1/winv): the (pcls1) operator W + Sigma_dagger^{-1},
+// Woodbury with the latent factor: B^T D^{-1/2} [s - W_U M^{-1} W_U^T s], s = D^{-1/2} B v
+int la_sigma_inv(LaCtx& c, int ncol, const double* v, double* out, const double* winv) {
+  Handle* h = c.h;
+  const Plan& P = h->P;
+  double* sv = c.d(L_T1);
+  VIF_CUDA(h, launch_la_bapply_cols(c.nbr(), c.d(L_B), P.mv, P.n, ncol, c.d(L_D), v, sv, c.s), "D^-1/2 B v");
+  double* Y = nullptr;
+  if (P.mk > 0) {
+    VIF_CUDA(h, launch_la_tsgemm(h->buf<double>(B_W), P.ld, P.mk, P.n, sv, ncol, h->ord(0), nullptr, c.d(L_TSPART),
+                                 c.d(L_CT), 1.0, c.s),
+             "W_U^T s");
+    VIF_CUDA(h, launch_gemm_tn(c.d(L_CT), P.mk, ncol, c.d(L_LMINV), P.mk, P.mk, P.mk, 0, c.d(L_CT2), P.mk, 1.0, 0, c.s),
+             "L_M^-1 c");
+    VIF_CUDA(h, launch_gemm_tn(c.d(L_CT2), P.mk, ncol, c.d(L_LMINVT), P.mk, P.mk, P.mk, 0, c.d(L_CT), P.mk, 1.0, 0,
+                               c.s),
+             "L_M^-T t");
+    Y = c.d(L_T3);
+    VIF_CUDA(h, launch_gemm_tn(h->buf<double>(B_W), P.ld, P.n, c.d(L_CT), P.mk, ncol, P.mk, 0, Y, ncol, 1.0, 0, c.s),
+             "W_U M^-1 c");
+  }
+  VIF_CUDA(h, launch_la_woodbury_mid(sv, Y, c.i(L_IPOS), c.d(L_D), P.n, ncol, c.d(L_T2), c.s), "Woodbury");
+  VIF_CUDA(h, launch_la_btapply_cols(c.i(L_TPTR), c.i(L_TROW), c.d(L_TVAL), P.n, ncol, c.d(L_T2), winv, v, out, c.s),
+           "B^T D^-1/2 r");
   return VIF_OK;
 }
 
@@ -1505,7 +1536,9 @@ int vif_la_prepare(void* handle, const vif_theta* theta, int32_t nprobe, int32_t
     VIF_CUDA(h, launch_chol_inv(c.d(L_GM), P.m, P.ld, 1.0, c.d(L_LMINV), P.mk, P.mk, 1, c.d(L_TSCR), c.fitc_fail(),
                                 h->num_sms, s),
              "chol M (full inverse)");
+    VIF_CUDA(h, launch_la_transpose(c.d(L_LMINV), P.mk, P.mk, P.mk, c.d(L_LMINVT), P.mk, s), "L_M^-T");
   }
+  VIF_CUDA(h, launch_la_invorder(h->ord(0), P.n, c.i(L_IPOS), s), "inverse order");
   if (P.mk > 0) VIF_CUDA(h, launch_la_rownorm2(c.U(), P.ld, P.mk, P.n, c.d(L_UN2), s), "||u_i||^2");
   else VIF_CUDA(h, cudaMemsetAsync(c.d(L_UN2), 0, c.L.size[L_UN2], s), "memset");
   VIF_CUDA(h, launch_la_transpose_struct(c.nbr(), P.n, P.mv, c.i(L_CNT), c.i(L_CUR), c.i(L_TPTR), c.i(L_TPOS), s),
@@ -1562,7 +1595,7 @@ int vif_la_apply(void* handle, void* ws, int32_t op, int32_t ncol, const double*
   const Plan& P = h->P;
   if (ncol < 1 || ncol > (h->la_nprobe > 1 ? h->la_nprobe : 1) || !v || !out)
     return fail(h, VIF_ERR_INVALID_ARG, "vif_la_apply: bad arguments");
-  if ((op == VIF_LA_FITC_SOLVE || op == VIF_LA_A) && !winv)
+  if ((op == VIF_LA_FITC_SOLVE || op == VIF_LA_A || op == VIF_LA_A1) && !winv)
     return fail(h, VIF_ERR_INVALID_ARG, "vif_la_apply: winv is required for this operator");
   LaCtx c = la_ctx(h, ws);
   switch (op) {
@@ -1574,6 +1607,8 @@ int vif_la_apply(void* handle, void* ws, int32_t op, int32_t ncol, const double*
       LA_TRY(la_fitc_build(c, winv));
       LA_TRY(la_fitc_solve(c, ncol, v, out));
       break;
+    case VIF_LA_SIGMA_INV: LA_TRY(la_sigma_inv(c, ncol, v, out, nullptr)); break;
+    case VIF_LA_A1: LA_TRY(la_sigma_inv(c, ncol, v, out, winv)); break;
     default: return fail(h, VIF_ERR_INVALID_ARG, "vif_la_apply: unknown operator");
   }
   VIF_CUDA(h, cudaStreamSynchronize(c.s), "sync");

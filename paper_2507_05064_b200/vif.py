@@ -116,7 +116,7 @@ EXPORTED = ("vif_nccl_unique_id", "vif_workspace_bytes", "vif_partition", "vif_c
             "vif_stage_name", "vif_last_error", "vif_destroy", "vif_grad_workspace_bytes", "vif_grad",
             "vif_predict_workspace_bytes", "vif_predict", "vif_neighbors", "vif_stage_data",
             "vif_la_workspace_bytes", "vif_la_prepare", "vif_la_apply", "vif_la_nll", "vif_owned_rows")
-LA_OPS = {"sigma": 0, "A": 1, "binv": 2, "btinv": 3, "fitc_solve": 4}
+LA_OPS = {"sigma": 0, "A": 1, "binv": 2, "btinv": 3, "fitc_solve": 4, "sigma_inv": 5, "A1": 6}
 NUM_STAGES = 8
 
 

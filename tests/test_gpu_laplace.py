@@ -1,6 +1,7 @@
 """GPU parity of the VIF-Laplace iterative path against oracle/laplace.py.
 
-Operators (Sigma_dagger, W^{-1} + Sigma_dagger, B^{-1}, B^{-T}, the FITC solve): the triangular solves to
+Operators (Sigma_dagger, W^{-1} + Sigma_dagger, B^{-1}, B^{-T}, the FITC solve, Sigma_dagger^{-1} and
+W + Sigma_dagger^{-1} of pcls1): the triangular solves to
 a backward error of 1e-13 against the GPU's own latent B (|B x - v| / (|B| |x|)), every operator to a forward
 error of 1e-8 relative to the column scale (B and D themselves agree to 1e-9, north_star; the solves
 carry that through dependency chains, observed up to ~2e-9 on ill-conditioned residual factors); the mode, -log p and the quadratic term with both sides' CG and Newton tolerances at
@@ -58,12 +59,15 @@ def test_operators(n, m, mv, ncol):
     V = rng.standard_normal((n, ncol)) if ncol > 1 else rng.standard_normal(n)
     W = la.hess_w(rng.normal(0, 1.5, n))
     winv = 1.0 / W
+    V2 = V.reshape(n, -1)
+    sinv = np.stack([lat.sigma_dagger_inv(V2[:, k]) for k in range(V2.shape[1])], axis=1).reshape(V.shape)
     refs = {"btinv": lat.btinv(V), "binv": lat.binv(V), "sigma": lat.sigma_dagger(V),
             "A": (V / W[:, None] if V.ndim == 2 else V / W) + lat.sigma_dagger(V),
-            "fitc_solve": la.fitc(lat, W).solve(V)}
+            "fitc_solve": la.fitc(lat, W).solve(V),
+            "sigma_inv": sinv, "A1": (V * W[:, None] if V.ndim == 2 else V * W) + sinv}
     errs, gots = {}, {}
     for op, ref in refs.items():
-        got = gots[op] = model.la_apply(op, V, winv=winv if op in ("A", "fitc_solve") else None).cpu().numpy()
+        got = gots[op] = model.la_apply(op, V, winv=winv if op in ("A", "A1", "fitc_solve") else None).cpu().numpy()
         errs[op] = rel_err(got, ref)
     assert max(errs.values()) < 1e-8, errs
     # backward error of the triangular solves against the GPU's own latent B (vif_factor at nugget 0;
@@ -190,4 +194,15 @@ def test_bench_size_sampled():
     sg = model.la_apply("sigma", g).cpu().numpy()
     assert np.max(np.abs(sg - b)) <= 1e-6 * np.abs(b).max()
     assert np.isfinite(t.nll) and t.nll == pytest.approx(t.neg_loglik + 0.5 * t.quad + 0.5 * t.logdet, rel=1e-12)
+    model.close()
+
+
+def test_sigma_inv_inverts_sigma():
+    """Sigma_dagger^{-1} (Woodbury, sparse products) inverts Sigma_dagger (triangular solves) on the GPU."""
+    p = vif()
+    w = work(900, 30, 12, seed=17)
+    model = model_of(w, p.Theta(**w.theta_dict()), nprobe=4)
+    V = np.random.default_rng(3).standard_normal((900, 4))
+    back = model.la_apply("sigma_inv", model.la_apply("sigma", V)).cpu().numpy()
+    assert rel_err(back, V) < 1e-8
     model.close()

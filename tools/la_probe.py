@@ -54,7 +54,7 @@ def main():
     # one Sigma_dagger apply and one FITC solve (ncol = 1 and ell), timed alone
     for ncol in (1, a.ell):
         V = torch.randn(a.n, ncol, dtype=torch.float64, device=dev) if ncol > 1 else torch.randn(a.n, dtype=torch.float64, device=dev)
-        for op in ("btinv", "binv", "sigma"):
+        for op in ("btinv", "binv", "sigma", "sigma_inv"):
             model.la_apply(op, V)
             torch.cuda.synchronize()
             t1 = time.perf_counter()
