@@ -124,7 +124,12 @@ bool make_plan(const vif_dims* dims, bool emulate, Plan& P, std::string& err) {
   P.mk = (int)round_up(P.m, 8);
   P.ycol = P.mk;
   P.ld = (int)round_up(P.mk + 1, 8);
-  if (P.world == 1) {
+  // VIF_NCCL_SINGLE=1 (test only): a single-rank handle given an NCCL id runs the multi-GPU schedule
+  // (8 rounds, per-round all-gather, all-reduce) on a one-rank communicator, exercising the NCCL
+  // plumbing on one GPU without ranks that wait on each other
+  static const char* nccl1 = getenv("VIF_NCCL_SINGLE");
+  const bool single_nccl = P.world == 1 && nccl1 && nccl1[0] == '1';
+  if (P.world == 1 && !single_nccl) {
     // single GPU: R rounds on three streams (K1 of round r+1 and the SYRK of round r-1 run beside
     // the vecchia rows of round r and fill the DMMA pipe while those warps are in their scalar
     // phases); VIF_ROUNDS overrides, 1 = the plain serial schedule
@@ -804,7 +809,9 @@ int vif_create(void** handle, const vif_dims* dims, void* workspace, size_t ws_b
     delete h;
     return fail(nullptr, VIF_ERR_CUDA, m);
   }
-  if (h->P.world > 1 && !h->P.emulate) {
+  static const char* nccl1 = getenv("VIF_NCCL_SINGLE");
+  const bool single_nccl = h->P.world == 1 && nccl_id && nccl1 && nccl1[0] == '1';
+  if ((h->P.world > 1 && !h->P.emulate) || single_nccl) {
     Nccl& N = nccl();
     if (!N.ok) {
       delete h;
@@ -841,7 +848,7 @@ int vif_create(void** handle, const vif_dims* dims, void* workspace, size_t ws_b
     vif_destroy(h);
     return fail(nullptr, VIF_ERR_CUDA, m);
   }
-  if (h->P.world == 1 && h->P.rounds > 1) {
+  if (h->P.world == 1 && h->P.rounds > 1 && !h->comm) {
     e = cudaStreamCreateWithFlags(&h->s_k1, cudaStreamNonBlocking);
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&h->s_sy, cudaStreamNonBlocking);
     h->ev_k1.assign(h->P.rounds, nullptr);
@@ -940,7 +947,7 @@ int vif_factor(void* handle, const vif_theta* theta, double* B_out, double* D_ou
     nl += 2;
   }
   h->mark(S_KM, 1);
-  if (P.world == 1 && P.rounds > 1) {
+  if (P.world == 1 && P.rounds > 1 && !h->comm) {
     // single GPU, R rounds on three streams:
     //   s_k1: K1(0) K1(1) ... K1(R-1)                       (after K0)
     //   s   : [K1(r)] vecchia(r) for r = 0..R-1              (round r conditions on rounds <= r)
@@ -1030,7 +1037,7 @@ int vif_factor(void* handle, const vif_theta* theta, double* B_out, double* D_ou
   // so the all-gather of round r overlaps K1 of later rounds and the vecchia rows of earlier rounds
   // (the rows of round r only condition on predecessors, i.e. on rounds <= r).
   const int nrep = P.emulate ? P.world : 1;
-  const bool nccl_path = P.world > 1 && !P.emulate;
+  const bool nccl_path = h->comm != nullptr;
   const size_t gstride = (size_t)P.ld * P.ld + 8;
   h->mark(S_UFEAT, 0);
   for (int64_t r = 0; r < P.rounds; ++r) {
@@ -1114,7 +1121,7 @@ int vif_factor(void* handle, const vif_theta* theta, double* B_out, double* D_ou
                                    h->buf<double>(B_GSUM), s),
              "emulated all-reduce");
     ++nl;
-  } else if (P.world > 1) {
+  } else if (h->comm) {
     Nccl& N = nccl();
     double* G = h->buf<double>(B_G);
     ncclResult_t rr = N.AllReduce(G, G, (size_t)P.ld * P.ld + 1, ncclFloat64, ncclSum, h->comm, s);
@@ -1309,7 +1316,7 @@ int vif_grad(void* handle, const vif_theta* theta, void* gws, size_t gws_bytes, 
   }
   if (nrep > 1) {
     VIF_CUDA(h, launch_sum_buffers(gbuf(G_OUT), nparam, nrep, nparam, gbuf(G_OUT), s), "emulated all-reduce");
-  } else if (P.world > 1) {
+  } else if (h->comm) {
     Nccl& N = nccl();
     ncclResult_t rr = N.AllReduce(gbuf(G_OUT), gbuf(G_OUT), (size_t)nparam, ncclFloat64, ncclSum, h->comm, s);
     if (rr != ncclSuccess) return fail(h, VIF_ERR_NCCL, std::string("ncclAllReduce: ") + N.GetErrorString(rr));

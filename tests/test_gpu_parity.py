@@ -310,3 +310,45 @@ def test_owned_rows_map(world):
     if world == 1:
         np.testing.assert_array_equal(np.sort(model.owned_rows()), rows)
     model.close()
+
+
+_NCCL1 = r"""
+import json, sys
+import numpy as np, torch
+sys.path.insert(0, {root!r})
+import paper_2507_05064_b200 as p
+import vifgen
+w = vifgen.make_workload(n=3001, d=2, m=24, mv=9, family="matern32", rho=0.15, nugget=0.1, seed=31, device="cuda")
+dev = torch.device("cuda")
+X, Z, nbr, y = (torch.from_numpy(np.ascontiguousarray(a)).to(dev) for a in (w.X, w.Z, w.nbr, w.y))
+nid = p.vif_nccl_unique_id() if {use_nccl} else None
+model = p.VifModel(X, Z, nbr, y, world=1, nccl_id=nid, device=dev)
+th = p.Theta(**w.theta_dict())
+D = torch.zeros(w.n, dtype=torch.float64, device=dev)
+t = model.evaluate(th, None, D)
+_, g = model.grad(th)
+print(json.dumps(dict(nll=t.nll, D=D.cpu().numpy().tolist()[:50], g=list(map(float, g)), rounds=model.rounds)))
+"""
+
+
+def test_nccl_single_rank_schedule():
+    """The multi-GPU schedule (8 rounds, per-round NCCL all-gather, NCCL all-reduce of the Gram and of
+    the gradient sums) on a one-rank communicator (VIF_NCCL_SINGLE=1): exercises the NCCL plumbing on one
+    GPU (no ranks waiting on each other) and must reproduce the single-GPU result."""
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for use in (False, True):
+        env = dict(os.environ, VIF_NCCL_SINGLE="1" if use else "0")
+        r = subprocess.run([sys.executable, "-c", _NCCL1.format(root=root, use_nccl=use)], env=env, capture_output=True,
+                           text=True, timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+        outs.append(json.loads(r.stdout.strip().splitlines()[-1]))
+    a, b = outs
+    assert b["rounds"] == 8 and a["rounds"] >= 1
+    assert b["nll"] == pytest.approx(a["nll"], rel=1e-12)
+    np.testing.assert_array_equal(np.array(b["D"]), np.array(a["D"]))
+    np.testing.assert_allclose(b["g"], a["g"], rtol=1e-11)
