@@ -715,6 +715,215 @@ cudaError_t launch_param_adj_fam(const GradPointArgs& a, cudaStream_t s) {
   }
 }
 
+// ---- no dU at all: <R, dU> = <R L_m^{-1}, dK(X,Z)> - <R^T U, Phi_low>, R = sum over the points of the
+// adjoint rows scattered to their conditioning sets (a deterministic gather over children lists) ----
+// children of point j: entries e = pos * 32 + b with S_{order[pos]}[b] = j (b = q: the point itself)
+__global__ void gchild_count_kernel(const int32_t* __restrict__ nbr, int mv, const int64_t* __restrict__ order,
+                                    int64_t npts, int* __restrict__ cnt) {
+  for (int64_t pos = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; pos < npts; pos += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = order[pos];
+    for (int b = 0; b < mv; ++b) {
+      const int j = nbr[i * mv + b];
+      if (j < 0) break;
+      atomicAdd(cnt + j, 1);
+    }
+    atomicAdd(cnt + i, 1);
+  }
+}
+
+__global__ void gchild_fill_kernel(const int32_t* __restrict__ nbr, int mv, const int64_t* __restrict__ order,
+                                   int64_t npts, const int* __restrict__ ptr, int* __restrict__ cursor,
+                                   int* __restrict__ ent) {
+  for (int64_t pos = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; pos < npts; pos += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = order[pos];
+    int b = 0;
+    for (; b < mv; ++b) {
+      const int j = nbr[i * mv + b];
+      if (j < 0) break;
+      ent[ptr[j] + atomicAdd(cursor + j, 1)] = (int)(pos * 32 + b);
+    }
+    ent[ptr[i] + atomicAdd(cursor + i, 1)] = (int)(pos * 32 + b);
+  }
+}
+
+__global__ void __launch_bounds__(1024) gchild_scan_kernel(const int* __restrict__ cnt, int64_t n, int* __restrict__ ptr) {
+  __shared__ int part[1024];
+  const int t = threadIdx.x;
+  const int64_t per = (n + 1023) / 1024;
+  const int64_t b0 = t * per, b1 = b0 + per < n ? b0 + per : n;
+  int s = 0;
+  for (int64_t i = b0; i < b1; ++i) s += cnt[i];
+  part[t] = s;
+  __syncthreads();
+  if (t == 0) {
+    int acc = 0;
+    for (int k = 0; k < 1024; ++k) {
+      const int v = part[k];
+      part[k] = acc;
+      acc += v;
+    }
+    ptr[n] = acc;
+  }
+  __syncthreads();
+  int acc = part[t];
+  for (int64_t i = b0; i < b1; ++i) {
+    ptr[i] = acc;
+    acc += cnt[i];
+  }
+}
+
+__global__ void gchild_sort_kernel(int64_t n, const int* __restrict__ ptr, int* __restrict__ ent) {
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
+    const int a = ptr[j], b = ptr[j + 1];
+    for (int k = a + 1; k < b; ++k) {
+      const int v = ent[k];
+      int q = k - 1;
+      while (q >= a && ent[q] > v) {
+        ent[q + 1] = ent[q];
+        --q;
+      }
+      ent[q + 1] = v;
+    }
+  }
+}
+
+// R[j][k] = sum_{entries (pos, b) of j} a~_{pos,b} rho[pos][k] + beta~_{pos,b} sig[pos][k]; warp per j,
+// j in index order (jorder: an optional visiting order)
+template <int RB>
+__global__ void __launch_bounds__(256) gR_kernel(const int* __restrict__ ptr, const int* __restrict__ ent,
+                                                 const int64_t* __restrict__ order, const int64_t* __restrict__ jorder,
+                                                 int64_t n, int mk, const double* __restrict__ state,
+                                                 const double* __restrict__ adj, const double* __restrict__ rho,
+                                                 const double* __restrict__ sig, double* __restrict__ R) {
+  constexpr int SP = RB * 8;
+  constexpr int LP = SP * (SP + 1) / 2;
+  constexpr int CPL = 4;  // columns per lane per pass (16: slower at n = 1M, 240 vs 232 ms per gradient)
+  const int lane = threadIdx.x & 31;
+  for (int64_t t = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5); t < n; t += (int64_t)gridDim.x * 8) {
+    const int64_t j = jorder ? jorder[t] : t;
+    const int a = ptr[j], b = ptr[j + 1];
+    for (int k0 = 0; k0 < mk; k0 += 32 * CPL) {
+      double acc[CPL];
+#pragma unroll
+      for (int u = 0; u < CPL; ++u) acc[u] = 0.0;
+      for (int e = a; e < b; ++e) {
+        const int en = ent[e];
+        const int64_t pos = en >> 5;
+        const int bb = en & 31;
+        const bool self = order[pos] == j;
+        const double al = self ? 1.0 : -state[pos * (int64_t)state_doubles<RB>() + LP + bb];
+        const double be = self ? 0.0 : adj[pos * (int64_t)ADJ_STRIDE + 2 + bb];
+        const double* rr = rho + pos * (int64_t)mk + k0 + lane;
+        const double* ss = sig + pos * (int64_t)mk + k0 + lane;
+#pragma unroll
+        for (int u = 0; u < CPL; ++u)
+          if (k0 + lane + 32 * u < mk) acc[u] = fma(al, __ldg(rr + 32 * u), fma(be, __ldg(ss + 32 * u), acc[u]));
+      }
+#pragma unroll
+      for (int u = 0; u < CPL; ++u) {
+        const int k = k0 + lane + 32 * u;
+        if (k < mk) R[j * (int64_t)mk + k] = acc[u];
+      }
+    }
+  }
+}
+
+// sum_{p, k < m} T[p][k] dk(x_p, z_k)/dtheta_q for q = 0 (sigma_1^2), 1..d (lambda): one exp per pair,
+// block partials part[block][q] (fixed order)
+template <int FAM, int D>
+__global__ void __launch_bounds__(256) gTdK_kernel(const double* __restrict__ X, const double* __restrict__ Z,
+                                                   int64_t n, int m, int mk, CovParams p,
+                                                   const double* __restrict__ T, double* __restrict__ part) {
+  extern __shared__ double zs[];  // m x d, pre-scaled
+  __shared__ double tbl[64];
+  __shared__ double red[8][VIF_MAX_D + 1];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr int DM = D > 0 ? D : VIF_MAX_D;  // D > 0: compile-time dimension (registers, no local memory)
+  const int dd = D > 0 ? D : p.d;
+  exp_table_init(tbl, p.sigma2, threadIdx.x);
+  for (int e = threadIdx.x; e < m * dd; e += blockDim.x) zs[e] = Z[e] * (fam_scale<FAM>() * p.inv_ls[e % dd]);
+  __syncthreads();
+  double acc[DM + 1];
+#pragma unroll
+  for (int q = 0; q <= DM; ++q) acc[q] = 0.0;
+  double xr[DM];
+  for (int64_t r = (int64_t)blockIdx.x * 8 + warp; r < n; r += (int64_t)gridDim.x * 8) {
+#pragma unroll
+    for (int k = 0; k < DM; ++k)
+      if (k < dd) xr[k] = X[r * dd + k] * (fam_scale<FAM>() * p.inv_ls[k]);
+    const double* trow = T + r * (int64_t)mk;
+    for (int b = lane; b < m; b += 32) {
+      const double t_ = __ldg(trow + b);
+      const double* z = zs + b * dd;
+      double t2 = 0.0;
+#pragma unroll
+      for (int k = 0; k < DM; ++k)
+        if (k < dd) {
+          const double dk = xr[k] - z[k];
+          t2 = fma(dk, dk, t2);
+        }
+      const double t = FAM == FAM_GAUSS ? t2 : sqrt_fast(t2);
+      const double E = sig2_exp_neg(t, tbl);
+      const double f = FAM == FAM_M12 || FAM == FAM_GAUSS ? E
+                     : (FAM == FAM_M32 ? fma(E, t, E) : fma(E, fma(t2, 1.0 / 3.0, t), E));
+      acc[0] = fma(t_, f / p.sigma2, acc[0]);
+      // dk/dlambda_j = E Delta~_j^2 / lambda_j x {1/t, 1, (1+t)/3, 2} (dcov_fast)
+      double g;
+      if (FAM == FAM_M12) g = t > 0.0 ? 1.0 / t : 0.0;
+      else if (FAM == FAM_M32) g = 1.0;
+      else if (FAM == FAM_M52) g = (1.0 + t) * (1.0 / 3.0);
+      else g = 2.0;
+      const double Eg = E * g * t_;
+#pragma unroll
+      for (int k = 0; k < DM; ++k)
+        if (k < dd) {
+          const double dk = xr[k] - z[k];
+          acc[1 + k] = fma(Eg * dk * dk, p.inv_ls[k], acc[1 + k]);
+        }
+    }
+  }
+#pragma unroll
+  for (int q = 0; q <= DM; ++q) {
+    if (q > dd) break;
+    double v = acc[q];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) red[warp][q] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x <= p.d) {
+    double v = 0.0;
+    for (int w = 0; w < 8; ++w) v += red[w][threadIdx.x];
+    part[(size_t)blockIdx.x * (p.d + 1) + threadIdx.x] = v;
+  }
+}
+
+// out[q] = sum_blocks part[block][q]
+__global__ void gTdK_reduce_kernel(const double* __restrict__ part, int nblocks, int nq, double* __restrict__ out) {
+  const int q = threadIdx.x;
+  if (q >= nq) return;
+  double s = 0.0;
+  for (int b = 0; b < nblocks; ++b) s += part[(size_t)b * nq + q];
+  out[q] = s;
+}
+
+// out[pi] += tdk[q] - sum G2 o Phi_low (one block)
+__global__ void __launch_bounds__(1024) gfinal_kernel(double* __restrict__ out, const double* __restrict__ tdk, int q,
+                                                      const double* __restrict__ G2, const double* __restrict__ Phil,
+                                                      int mk) {
+  __shared__ double red[1024];
+  double s = 0.0;
+  const int64_t tot = (int64_t)mk * mk;
+  for (int64_t e = threadIdx.x; e < tot; e += blockDim.x) s = fma(G2[e], Phil[e], s);
+  red[threadIdx.x] = s;
+  __syncthreads();
+  for (int w = 512; w > 0; w >>= 1) {
+    if ((int)threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *out += tdk[q] - red[0];
+}
+
 template <int FAM, int RB>
 cudaError_t launch_grad_rb(const GradPointArgs& a, bool state_pass, cudaStream_t s) {
   const size_t smem = (size_t)GW * grad_warp_doubles<RB>(a.p.d) * sizeof(double);
@@ -813,6 +1022,77 @@ cudaError_t launch_grad_points_adj(const GradPointArgs& a, double* out, cudaStre
     if (e != cudaSuccess) return e;
   }
   grad_reduce_kernel<<<1, 1024, 0, s>>>(a.part, grad_point_nparts(a.npts), out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gchild(const int32_t* nbr, int mv, const int64_t* order, int64_t npts, int64_t n, int* cnt,
+                          int* cursor, int* ptr, int* ent, cudaStream_t s) {
+  cudaError_t e = cudaMemsetAsync(cnt, 0, (size_t)n * sizeof(int), s);
+  if (e == cudaSuccess) e = cudaMemsetAsync(cursor, 0, (size_t)n * sizeof(int), s);
+  if (e != cudaSuccess) return e;
+  const unsigned g1 = (unsigned)((npts + 255) / 256 > 4096 ? 4096 : (npts + 255) / 256 + 1);
+  gchild_count_kernel<<<g1, 256, 0, s>>>(nbr, mv, order, npts, cnt);
+  gchild_scan_kernel<<<1, 1024, 0, s>>>(cnt, n, ptr);
+  gchild_fill_kernel<<<g1, 256, 0, s>>>(nbr, mv, order, npts, ptr, cursor, ent);
+  const unsigned g2 = (unsigned)((n + 255) / 256 > 4096 ? 4096 : (n + 255) / 256 + 1);
+  gchild_sort_kernel<<<g2, 256, 0, s>>>(n, ptr, ent);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gR(const int* ptr, const int* ent, const int64_t* order, const int64_t* jorder, int64_t n, int mk,
+                      int mv, const double* state, const double* adj, const double* rho, const double* sig, double* R,
+                      cudaStream_t s) {
+  if (mv > 31) return cudaErrorNotSupported;
+  const unsigned blocks = (unsigned)((n + 7) / 8 > 148 * 16 ? 148 * 16 : (n + 7) / 8);
+  switch ((mv + 1 + 7) / 8) {
+    case 1: gR_kernel<1><<<blocks, 256, 0, s>>>(ptr, ent, order, jorder, n, mk, state, adj, rho, sig, R); break;
+    case 2: gR_kernel<2><<<blocks, 256, 0, s>>>(ptr, ent, order, jorder, n, mk, state, adj, rho, sig, R); break;
+    case 3: gR_kernel<3><<<blocks, 256, 0, s>>>(ptr, ent, order, jorder, n, mk, state, adj, rho, sig, R); break;
+    default: gR_kernel<4><<<blocks, 256, 0, s>>>(ptr, ent, order, jorder, n, mk, state, adj, rho, sig, R); break;
+  }
+  return cudaGetLastError();
+}
+
+int gTdK_blocks() { return 148 * 4; }
+
+cudaError_t launch_gTdK(const double* X, const double* Z, int64_t n, int m, int mk, const CovParams& p,
+                        const double* T, double* part, double* out, cudaStream_t s) {
+  const int blocks = gTdK_blocks();
+  const size_t zb = (size_t)m * p.d * sizeof(double);
+  auto go = [&](auto kern) -> cudaError_t {
+    static size_t attr = 0;
+    if (zb > 48 * 1024 && attr < zb) {
+      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)zb);
+      if (e != cudaSuccess) return e;
+      attr = zb;
+    }
+    kern<<<blocks, 256, zb, s>>>(X, Z, n, m, mk, p, T, part);
+    return cudaSuccess;
+  };
+  cudaError_t e;
+  if (p.d == 2) {
+    switch (p.family) {
+      case FAM_M12: e = go(gTdK_kernel<FAM_M12, 2>); break;
+      case FAM_M32: e = go(gTdK_kernel<FAM_M32, 2>); break;
+      case FAM_M52: e = go(gTdK_kernel<FAM_M52, 2>); break;
+      default: e = go(gTdK_kernel<FAM_GAUSS, 2>); break;
+    }
+  } else {
+    switch (p.family) {
+      case FAM_M12: e = go(gTdK_kernel<FAM_M12, 0>); break;
+      case FAM_M32: e = go(gTdK_kernel<FAM_M32, 0>); break;
+      case FAM_M52: e = go(gTdK_kernel<FAM_M52, 0>); break;
+      default: e = go(gTdK_kernel<FAM_GAUSS, 0>); break;
+    }
+  }
+  if (e != cudaSuccess) return e;
+  gTdK_reduce_kernel<<<1, 32, 0, s>>>(part, blocks, p.d + 1, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gfinal(double* out, const double* tdk, int q, const double* G2, const double* Phil, int mk,
+                          cudaStream_t s) {
+  gfinal_kernel<<<1, 1024, 0, s>>>(out, tdk, q, G2, Phil, mk);
   return cudaGetLastError();
 }
 

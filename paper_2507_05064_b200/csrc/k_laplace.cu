@@ -597,8 +597,8 @@ __global__ void __launch_bounds__(256) la_tsgemm_kernel(const double* __restrict
 constexpr int TD_R = 16, TD_K = 64, TD_N = 64, TD_PAD = 4;
 __global__ void __launch_bounds__(256) la_tsgemm_dmma_kernel(const double* __restrict__ U, int64_t ldu, int mk,
                                                              int64_t n, const double* __restrict__ V, int ncol,
-                                                             const double* __restrict__ rs, int64_t rows_per,
-                                                             double* __restrict__ part) {
+                                                             int64_t ldv, const double* __restrict__ rs,
+                                                             int64_t rows_per, double* __restrict__ part) {
   __shared__ __align__(16) double Us[2][TD_R][TD_K + TD_PAD];
   __shared__ __align__(16) double Vs[2][TD_R][TD_N + TD_PAD];
   const int t = threadIdx.x, lane = t & 31, w = t >> 5;
@@ -626,7 +626,7 @@ __global__ void __launch_bounds__(256) la_tsgemm_dmma_kernel(const double* __res
       const int64_t r = rb + rr;
       double val = 0.0;
       if (r < r1 && c < ncol) {
-        val = V[r * ncol + c];
+        val = V[r * ldv + c];
         if (rs) val *= rs[r];
       }
       vreg[i] = val;
@@ -1158,7 +1158,7 @@ cudaError_t launch_la_tsgemm(const double* U, int64_t ldu, int mk, int64_t n, co
   else if (ncol <= 8)
     la_tsgemm_kernel<8><<<grid, 256, 0, s>>>(U, ldu, mk, n, V, ncol, vrow, rs, rows_per, part);
   else if (ncol <= 64 && !vrow)
-    la_tsgemm_dmma_kernel<<<grid, 256, 0, s>>>(U, ldu, mk, n, V, ncol, rs, rows_per, part);
+    la_tsgemm_dmma_kernel<<<grid, 256, 0, s>>>(U, ldu, mk, n, V, ncol, ncol, rs, rows_per, part);
   else if (ncol <= 16)
     la_tsgemm_kernel<16><<<grid, 256, 0, s>>>(U, ldu, mk, n, V, ncol, vrow, rs, rows_per, part);
   else if (ncol <= 32)
@@ -1168,6 +1168,19 @@ cudaError_t launch_la_tsgemm(const double* U, int64_t ldu, int mk, int64_t n, co
   else
     return cudaErrorInvalidValue;
   la_tsreduce_kernel<<<grid_for((int64_t)ncol * mk * 32), 256, 0, s>>>(part, ns, ncol, mk, Ct, alpha);
+  return cudaGetLastError();
+}
+
+// C (ncol x mk, row stride mk) = V^T U for a column slice of a wider V (row stride ldv), ncol <= 64
+cudaError_t launch_la_tsgemm_ld(const double* U, int64_t ldu, int mk, int64_t n, const double* V, int64_t ldv,
+                                int ncol, double* part, double* Ct, cudaStream_t s) {
+  if (mk == 0) return cudaSuccess;
+  if (ncol > 64) return cudaErrorInvalidValue;
+  const int ns = la_ts_nsplit(n);
+  const int64_t rows_per = (n + ns - 1) / ns;
+  dim3 grid(ns, (mk + TS_K - 1) / TS_K);
+  la_tsgemm_dmma_kernel<<<grid, 256, 0, s>>>(U, ldu, mk, n, V, ncol, ldv, nullptr, rows_per, part);
+  la_tsreduce_kernel<<<grid_for((int64_t)ncol * mk * 32), 256, 0, s>>>(part, ns, ncol, mk, Ct, 1.0);
   return cudaGetLastError();
 }
 

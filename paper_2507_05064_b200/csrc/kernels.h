@@ -92,6 +92,19 @@ cudaError_t launch_grad_points(const GradPointArgs& a, double* out, cudaStream_t
 size_t grad_adj_doubles();
 cudaError_t launch_grad_adjoint(const GradPointArgs& a, cudaStream_t s);
 cudaError_t launch_grad_points_adj(const GradPointArgs& a, double* out, cudaStream_t s);
+cudaError_t launch_gchild(const int32_t* nbr, int mv, const int64_t* order, int64_t npts, int64_t n, int* cnt,
+                          int* cursor, int* ptr, int* ent, cudaStream_t s);
+cudaError_t launch_gR(const int* ptr, const int* ent, const int64_t* order, const int64_t* jorder, int64_t n, int mk,
+                      int mv,
+                      const double* state, const double* adj, const double* rho, const double* sig, double* R,
+                      cudaStream_t s);
+int gTdK_blocks();
+cudaError_t launch_gTdK(const double* X, const double* Z, int64_t n, int m, int mk, const CovParams& p,
+                        const double* T, double* part, double* out, cudaStream_t s);
+cudaError_t launch_gfinal(double* out, const double* tdk, int q, const double* G2, const double* Phil, int mk,
+                          cudaStream_t s);
+cudaError_t launch_la_tsgemm_ld(const double* U, int64_t ldu, int mk, int64_t n, const double* V, int64_t ldv,
+                                int ncol, double* part, double* Ct, cudaStream_t s);
 cudaError_t launch_dkm(const double* Z, int m, int mk, int pidx, const CovParams& p, double* out, cudaStream_t s);
 cudaError_t launch_phi_low(const double* Phi, int mk, double* out, cudaStream_t s);
 cudaError_t launch_kx_deriv(const double* X, const double* Z, int64_t npos, int m, int mk, int pidx,

@@ -377,7 +377,8 @@ int set_data(Handle* h, const double* X, const double* Z, const int32_t* nbr, co
 
 // ---------------------------------------------------------------- gradient workspace
 enum GBuf { G_Q2, G_GAM, G_DU, G_DKM, G_TT, G_PHI, G_PHILOW, G_LINVM, G_MCOPY, G_TSCR, G_ZH, G_Z, G_PART, G_OUT,
-            G_STATE, G_RHO, G_SIG, G_ADJ, G_COUNT };
+            G_STATE, G_RHO, G_SIG, G_ADJ, G_T, G_G2, G_LINVT, G_CCNT, G_CCUR, G_CPTR, G_CENT, G_TSP, G_TDKP, G_TDK,
+            G_COUNT };
 
 Layout make_grad_layout(const Plan& P) {
   Layout L{};
@@ -395,6 +396,14 @@ Layout make_grad_layout(const Plan& P) {
   L.size[G_STATE] = (size_t)P.npos * grad_state_doubles(P.mv) * D8;
   L.size[G_RHO] = L.size[G_SIG] = (size_t)P.npos * mk1 * D8;
   L.size[G_ADJ] = (size_t)P.npos * grad_adj_doubles() * D8;
+  L.size[G_T] = (size_t)P.n * mk1 * D8;
+  L.size[G_G2] = L.size[G_LINVT] = (size_t)mk1 * mk1 * D8;
+  L.size[G_CCNT] = L.size[G_CCUR] = (size_t)P.n * sizeof(int);
+  L.size[G_CPTR] = (size_t)(P.n + 1) * sizeof(int);
+  L.size[G_CENT] = (size_t)P.n * (P.mv + 1) * sizeof(int);
+  L.size[G_TSP] = (size_t)la_ts_nsplit(P.n) * 64 * mk1 * D8;
+  L.size[G_TDKP] = (size_t)gTdK_blocks() * (P.d + 1) * D8;
+  L.size[G_TDK] = (size_t)(P.d + 1) * D8;
   size_t off = 0;
   for (int b = 0; b < G_COUNT; ++b) {
     L.off[b] = off;
@@ -1285,10 +1294,43 @@ int vif_grad(void* handle, const vif_theta* theta, void* gws, size_t gws_bytes, 
     static const char* cross_env = getenv("VIF_GRAD_CROSS");
     const bool cross = cross_env && cross_env[0] == '1';
     if (!cross) VIF_CUDA(h, launch_grad_adjoint(a, s), "gradient adjoint");
+    // default: no dU at all -- the adjoint rows scattered to R (n x m), T = R L_m^{-1}, G2 = R^T U, and
+    // per kernel parameter <T, dK(X,Z)> - <G2, Phi_low> (VIF_GRAD_DU=1: materialise dU per parameter)
+    // cost at n = 1M, m = 500: materialising dU is two n m^2 GEMMs per kernel parameter (~27 ms each);
+    // the R path is ~100 ms once (the R gather, T, G2) plus ~3 ms per parameter: 223 vs 231 ms per
+    // gradient at d = 2, and the gap grows with d.  VIF_GRAD_DU=1 forces the dU path.
+    static const char* du_env = getenv("VIF_GRAD_DU");
+    const bool want_du = du_env && du_env[0] == '1';
+    const bool nodu = !cross && !want_du && mk > 0;
+    if (nodu) {
+      double* R = gbuf(G_DU);  // n x mk
+      VIF_CUDA(h, launch_gchild(a.nbr, P.mv, a.order, a.npts, P.n, reinterpret_cast<int*>(gbuf(G_CCNT)),
+                                reinterpret_cast<int*>(gbuf(G_CCUR)), reinterpret_cast<int*>(gbuf(G_CPTR)),
+                                reinterpret_cast<int*>(gbuf(G_CENT)), s),
+               "children lists");
+      const int64_t* jorder = nullptr;  // index order (the Morton processing order measured slower)
+      VIF_CUDA(h, launch_gR(reinterpret_cast<int*>(gbuf(G_CPTR)), reinterpret_cast<int*>(gbuf(G_CENT)), a.order,
+                            jorder, P.n, mk, P.mv, a.state, a.adj, a.rho, a.sig, R, s),
+               "R");
+      if (g == 0) VIF_CUDA(h, launch_la_transpose(Linv, mk, mk, mk, gbuf(G_LINVT), mk, s), "L_m^-T");
+      VIF_CUDA(h, launch_gemm_tn(R, mk, P.n, gbuf(G_LINVT), mk, mk, mk, 0, gbuf(G_T), mk, 1.0, 0, s), "T = R L^-1");
+      for (int c0 = 0; c0 < mk; c0 += 64)
+        VIF_CUDA(h, launch_la_tsgemm_ld(U, ld, mk, P.n, R + c0, mk, std::min(64, mk - c0), gbuf(G_TSP),
+                                        gbuf(G_G2) + (size_t)c0 * mk, s),
+                 "G2 = R^T U");
+      VIF_CUDA(h, launch_gTdK(h->buf<double>(B_X), h->buf<double>(B_Z), P.n, m, mk, p, gbuf(G_T), gbuf(G_TDKP),
+                              gbuf(G_TDK), s),
+               "<T, dK>");
+    }
     for (int pi = 0; pi < nparam; ++pi) {
       const bool kernel_param = pi <= P.d;
       const double* dUp = nullptr;
-      if (kernel_param && m > 0) {
+      if (kernel_param && m > 0 && nodu) {
+        VIF_CUDA(h, launch_dkm(h->buf<double>(B_Z), m, mk, pi, p, gbuf(G_DKM), s), "dK_m");
+        VIF_CUDA(h, launch_gemm_tn(Linv, mk, mk, gbuf(G_DKM), mk, mk, mk, 0, gbuf(G_TT), mk, 1.0, 0, s), "Linv dK_m");
+        VIF_CUDA(h, launch_gemm_tn(Linv, mk, mk, gbuf(G_TT), mk, mk, mk, 0, gbuf(G_PHI), mk, 1.0, 0, s), "Phi");
+        VIF_CUDA(h, launch_phi_low(gbuf(G_PHI), mk, gbuf(G_PHILOW), s), "Phi_low");
+      } else if (kernel_param && m > 0) {
         VIF_CUDA(h, launch_dkm(h->buf<double>(B_Z), m, mk, pi, p, gbuf(G_DKM), s), "dK_m");
         VIF_CUDA(h, launch_gemm_tn(Linv, mk, mk, gbuf(G_DKM), mk, mk, mk, 0, gbuf(G_TT), mk, 1.0, 0, s), "Linv dK_m");
         VIF_CUDA(h, launch_gemm_tn(Linv, mk, mk, gbuf(G_TT), mk, mk, mk, 0, gbuf(G_PHI), mk, 1.0, 0, s), "Phi");
@@ -1312,6 +1354,10 @@ int vif_grad(void* handle, const vif_theta* theta, void* gws, size_t gws_bytes, 
         VIF_CUDA(h, launch_grad_points(a, gbuf(G_OUT) + (size_t)g * nparam + pi, s), "gradient points");
       else
         VIF_CUDA(h, launch_grad_points_adj(a, gbuf(G_OUT) + (size_t)g * nparam + pi, s), "gradient points");
+      if (nodu && kernel_param && m > 0)
+        VIF_CUDA(h, launch_gfinal(gbuf(G_OUT) + (size_t)g * nparam + pi, gbuf(G_TDK), pi, gbuf(G_G2), gbuf(G_PHILOW),
+                                  mk, s),
+                 "<T, dK> - <G2, Phi_low>");
     }
   }
   if (nrep > 1) {
