@@ -929,7 +929,7 @@ cudaError_t launch_grad_rb(const GradPointArgs& a, bool state_pass, cudaStream_t
   const size_t smem = (size_t)GW * grad_warp_doubles<RB>(a.p.d) * sizeof(double);
   const unsigned blocks = (unsigned)((a.npts + GW - 1) / GW);
   if (state_pass) {
-    if (smem > 48 * 1024) {
+    if (smem > 40 * 1024) {  // dynamic + the kernels' static shared memory may pass 48 KB
       cudaError_t e = cudaFuncSetAttribute(grad_state_kernel<FAM, RB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            (int)smem);
       if (e != cudaSuccess) return e;
@@ -938,7 +938,7 @@ cudaError_t launch_grad_rb(const GradPointArgs& a, bool state_pass, cudaStream_t
                                                              a.order, a.npts, a.p, a.state);
   } else {
     const size_t psmem = (size_t)GW * param_warp_doubles<RB>(a.p.d) * sizeof(double);
-    if (psmem > 48 * 1024) {
+    if (psmem > 40 * 1024) {
       cudaError_t e = cudaFuncSetAttribute(grad_param_kernel<FAM, RB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            (int)psmem);
       if (e != cudaSuccess) return e;
@@ -1061,7 +1061,7 @@ cudaError_t launch_gTdK(const double* X, const double* Z, int64_t n, int m, int 
   const size_t zb = (size_t)m * p.d * sizeof(double);
   auto go = [&](auto kern) -> cudaError_t {
     static size_t attr = 0;
-    if (zb > 48 * 1024 && attr < zb) {
+    if (zb > 40 * 1024 && attr < zb) {  // static shared memory comes on top
       cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)zb);
       if (e != cudaSuccess) return e;
       attr = zb;
@@ -1121,7 +1121,7 @@ cudaError_t launch_kx_deriv(const double* X, const double* Z, int64_t npos, int 
   const size_t zbytes = (size_t)m * p.d * sizeof(double);
   auto go = [&](auto kern) -> cudaError_t {
     static size_t attr = 0;
-    if (zbytes > 48 * 1024 && attr < zbytes) {
+    if (zbytes > 40 * 1024 && attr < zbytes) {
       cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)zbytes);
       if (e != cudaSuccess) return e;
       attr = zbytes;

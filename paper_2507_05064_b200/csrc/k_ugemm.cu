@@ -253,7 +253,7 @@ cudaError_t launch_u_features(const double* X, const double* Z, const double* y,
   const size_t zbytes = (size_t)m * p.d * sizeof(double);
   auto go = [&](auto kern) -> cudaError_t {
     static size_t attr = 0;  // one per instantiation of the generic lambda
-    if (zbytes > 48 * 1024 && attr < zbytes) {
+    if (zbytes > 40 * 1024 && attr < zbytes) {
       cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)zbytes);
       if (e != cudaSuccess) return e;
       attr = zbytes;
@@ -270,7 +270,7 @@ cudaError_t launch_u_features(const double* X, const double* Z, const double* y,
     int nb = (int)((npos + 7) / 8);
     if (nb > 148 * 8) nb = 148 * 8;
     static size_t attr = 0;
-    if (zb > 48 * 1024 && attr < zb) {
+    if (zb > 40 * 1024 && attr < zb) {  // static shared memory comes on top
       cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)zb);
       if (e != cudaSuccess) return e;
       attr = zb;

@@ -528,7 +528,7 @@ static cudaError_t launch_rb(const VecchiaArgs& a, cudaStream_t s) {
         default: kern = d2 ? vecchia_reg_kernel<FAM, RB, 3, 4, false, 2> : vecchia_reg_kernel<FAM, RB, 3, 4>; break;
       }
     }
-    if (smem > 48 * 1024) {
+    if (smem > 40 * 1024) {  // static shared memory comes on top
       cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       if (e != cudaSuccess) return e;
     }

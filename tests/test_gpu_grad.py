@@ -85,6 +85,12 @@ def test_grad_mv0_fitc():
     grad_parity(small(600, 40, 0, seed=6))
 
 
+def test_grad_config4_shape():
+    """config 4's dimensions (d = 10, m_v = 20: 12 KB of shared memory per warp in the state pass, over the
+    48 KB default with the static arrays) on a small n."""
+    grad_parity(small(1500, 120, 20, family="matern52", d=10, ard=(0.5, 5.0), seed=44, nugget=0.1))
+
+
 def test_grad_ard_10d():
     grad_parity(small(800, 60, 15, family="matern52", d=10, ard=(0.5, 5.0), seed=7, nugget=0.1))
 
