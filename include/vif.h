@@ -151,7 +151,8 @@ int vif_nll(void* handle, vif_terms* out);
  * synchronises.  grad: host, d + 2 doubles, identical on every rank.  terms (optional): as vif_nll.
  * Multi-rank: each rank sums its own points' terms (its dU over all n rows is formed locally) and one
  * all-reduce of the d + 2 partial sums follows; an emulated handle sums its virtual ranks in order.
- * Errors: INVALID_ARG (theta; m_v > 31: not supported by this version), NO_MEMORY
+ * Every m_v <= VIF_MAX_MV (s > 32: a shared-memory Cholesky in the state pass).
+ * Errors: INVALID_ARG (theta), NO_MEMORY
  * (grad workspace too small), NOT_PD (as vif_nll), CUDA. */
 int vif_grad_workspace_bytes(const vif_dims* dims, size_t* bytes);
 int vif_grad(void* handle, const vif_theta* theta, void* grad_workspace, size_t grad_ws_bytes, double* grad,

@@ -346,6 +346,171 @@ __global__ void __launch_bounds__(GW * 32, 4) grad_state_kernel(
   }
 }
 
+// S of point i: q valid neighbours (a prefix of its row, m_v <= 48: two loads per lane), then i itself
+__device__ __forceinline__ int grad_load_S(const int32_t* __restrict__ nbr, int mv, int64_t i, int lane, int SP,
+                                           int* __restrict__ Sidx) {
+  const int v0 = lane < mv ? nbr[i * mv + lane] : -1;
+  const int v1 = lane + 32 < mv ? nbr[i * mv + lane + 32] : -1;
+  const int q = __popc(__ballot_sync(0xffffffffu, v0 >= 0)) + __popc(__ballot_sync(0xffffffffu, v1 >= 0));
+  for (int t = lane; t < SP; t += 32) {
+    const int v = t < 32 ? v0 : v1;
+    Sidx[t] = t < q ? v : (t == q ? (int)i : -1);
+  }
+  return q;
+}
+
+// ---- pass 0 for s > 32 (m_v <= 47): the same Gram / dots on DMMA, the Cholesky of C_S in shared
+// memory (right-looking, the warp over the trailing triangle), A_i by substitution with dot products
+// over the lanes; the same state layout (padding rows of L are identity rows) ----
+template <int RB>
+__host__ __device__ constexpr int big_warp_doubles(int d) {
+  return (RB * 8) * (RB * 8 + 1) + 3 * (RB * 8) + RB * 8 * d;  // C, gam, inv, a, xs
+}
+
+template <int FAM, int RB>
+__global__ void __launch_bounds__(GW * 32) grad_state_big_kernel(
+    const double* __restrict__ U, const double* __restrict__ Gam, int64_t ldu, int mk, int ld,
+    const double* __restrict__ X, const int32_t* __restrict__ nbr, int mv, const int64_t* __restrict__ order,
+    int64_t npts, CovParams p, double* __restrict__ state) {
+  constexpr int SP = RB * 8;
+  constexpr int CS = SP + 1;
+  constexpr int NT = RB * (RB + 1) / 2;
+  constexpr int LP = SP * (SP + 1) / 2;
+  extern __shared__ __align__(16) double gsm_[];
+  __shared__ int Sidx_all[GW][SP];
+  __shared__ double tbl[64];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double* C = gsm_ + warp * big_warp_doubles<RB>(p.d);
+  double* gam_s = C + SP * CS;
+  double* inv_s = gam_s + SP;
+  double* a_s = inv_s + SP;
+  double* xs = a_s + SP;
+  int* Sidx = Sidx_all[warp];
+  const int64_t pos = (int64_t)blockIdx.x * GW + warp;
+  exp_table_init(tbl, p.sigma2, threadIdx.x);
+  __syncthreads();
+  if (pos >= npts) return;
+  const int64_t i = order[pos];
+  const int q = grad_load_S(nbr, mv, i, lane, SP, Sidx);
+  const int s = q + 1;
+  __syncwarp();
+  for (int t = lane; t < s; t += 32)
+    for (int k = 0; k < p.d; ++k) xs[t * p.d + k] = X[(int64_t)Sidx[t] * p.d + k] * (fam_scale<FAM>() * p.inv_ls[k]);
+  // Gram (lower tiles) and the dots g_i . U_aug[S_k] (as grad_state_kernel)
+  double acc[NT][2], gm[RB];
+#pragma unroll
+  for (int t = 0; t < NT; ++t) acc[t][0] = acc[t][1] = 0.0;
+#pragma unroll
+  for (int R = 0; R < RB; ++R) gm[R] = 0.0;
+  const double* rp[RB];
+#pragma unroll
+  for (int R = 0; R < RB; ++R) {
+    const int gi = Sidx[R * 8 + (lane >> 2)];
+    rp[R] = gi >= 0 ? U + (int64_t)gi * ldu + 2 * (lane & 3) : nullptr;
+  }
+  const double* grow = Gam + pos * (int64_t)ld + 2 * (lane & 3);
+  for (int k0 = 0; k0 < ld; k0 += 8) {
+    const double2 g2 = __ldg(reinterpret_cast<const double2*>(grow + k0));
+    double2 f[RB];
+#pragma unroll
+    for (int R = 0; R < RB; ++R)
+      f[R] = rp[R] ? __ldg(reinterpret_cast<const double2*>(rp[R] + k0)) : make_double2(0.0, 0.0);
+#pragma unroll
+    for (int R = 0; R < RB; ++R) gm[R] = fma(f[R].x, g2.x, fma(f[R].y, g2.y, gm[R]));
+    if (k0 < mk) {
+      int t = 0;
+#pragma unroll
+      for (int R1 = 0; R1 < RB; ++R1)
+#pragma unroll
+        for (int R2 = 0; R2 <= R1; ++R2, ++t) {
+          dmma884(acc[t][0], acc[t][1], f[R1].x, f[R2].x);
+          dmma884(acc[t][0], acc[t][1], f[R1].y, f[R2].y);
+        }
+    }
+  }
+#pragma unroll
+  for (int R = 0; R < RB; ++R) {
+    gm[R] += __shfl_xor_sync(0xffffffffu, gm[R], 1);
+    gm[R] += __shfl_xor_sync(0xffffffffu, gm[R], 2);
+    if ((lane & 3) == 0) gam_s[R * 8 + (lane >> 2)] = gm[R];
+  }
+  {
+    int t = 0;
+#pragma unroll
+    for (int R1 = 0; R1 < RB; ++R1)
+#pragma unroll
+      for (int R2 = 0; R2 <= R1; ++R2, ++t) {
+        const int r = R1 * 8 + (lane >> 2), c = R2 * 8 + 2 * (lane & 3);
+        C[r * CS + c] = acc[t][0];
+        C[r * CS + c + 1] = acc[t][1];
+      }
+  }
+  __syncwarp();
+  const int ne = s * (s + 1) / 2;
+  for (int e = lane; e < ne; e += 32) {
+    int r = (int)((sqrtf_fast(8.0f * (float)e + 1.0f) - 1.0f) * 0.5f);
+    if ((r + 1) * (r + 2) / 2 <= e) ++r;
+    if (r * (r + 1) / 2 > e) --r;
+    const int c = e - r * (r + 1) / 2;
+    double v = cov_fast<FAM>(xs + r * p.d, xs + c * p.d, p.d, tbl) - C[r * CS + c];
+    if (r == c) v += p.nugget;
+    C[r * CS + c] = v;
+  }
+  __syncwarp();
+  // right-looking Cholesky of the s x s lower triangle
+  bool ok = true;
+  double Di = 0.0;
+  for (int j = 0; j < s; ++j) {
+    const double djj = C[j * CS + j];
+    ok = ok && (djj > 0.0);
+    if (j == s - 1) Di = djj;
+    const double y = rsqrt_nr(djj);
+    for (int r = j + 1 + lane; r < s; r += 32) C[r * CS + j] *= y;
+    __syncwarp();
+    if (lane == 0) {
+      C[j * CS + j] = djj * y;
+      inv_s[j] = y;
+    }
+    const int w = s - j - 1;  // trailing triangle of order w
+    const int nt = w * (w + 1) / 2;
+    for (int e = lane; e < nt; e += 32) {
+      int r = (int)((sqrtf_fast(8.0f * (float)e + 1.0f) - 1.0f) * 0.5f);
+      if ((r + 1) * (r + 2) / 2 <= e) ++r;
+      if (r * (r + 1) / 2 > e) --r;
+      const int c = e - r * (r + 1) / 2;
+      const int rr = j + 1 + r, cc = j + 1 + c;
+      C[rr * CS + cc] = fma(-C[rr * CS + j], C[cc * CS + j], C[rr * CS + cc]);
+    }
+    __syncwarp();
+  }
+  // A_i = L_NN^{-T} l, l = row q of L (k < q)
+  for (int j = q - 1; j >= 0; --j) {
+    double sm = 0.0;
+    for (int k = j + 1 + lane; k < q; k += 32) sm = fma(C[k * CS + j], a_s[k], sm);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) sm += __shfl_xor_sync(0xffffffffu, sm, o);
+    if (lane == 0) a_s[j] = (C[q * CS + j] - sm) * inv_s[j];
+    __syncwarp();
+  }
+  double* st = state + pos * (int64_t)state_doubles<RB>();
+  for (int e = lane; e < LP; e += 32) {
+    int r = (int)((sqrtf_fast(8.0f * (float)e + 1.0f) - 1.0f) * 0.5f);
+    if ((r + 1) * (r + 2) / 2 <= e) ++r;
+    if (r * (r + 1) / 2 > e) --r;
+    const int c = e - r * (r + 1) / 2;
+    st[e] = r < s ? C[r * CS + c] : (r == c ? 1.0 : 0.0);
+  }
+  for (int t = lane; t < SP; t += 32) {
+    st[LP + t] = t < q ? a_s[t] : 0.0;
+    st[LP + SP + t] = t < s ? inv_s[t] : 1.0;
+    st[LP + 2 * SP + t] = t < s ? gam_s[t] : 0.0;
+  }
+  if (lane == 0) {
+    st[LP + 3 * SP] = Di;
+    st[LP + 3 * SP + 1] = ok ? 1.0 : 0.0;
+  }
+}
+
 // ---- pass per parameter: cross-Gram X = dU_S U_S^T (all RB^2 tiles), g_i . dU_aug[S_k], dC_S,
 // dA_i, dD_i and the point's contribution, with L, A_i, D_i, g_i . U_aug[S_k] from the state ----
 template <int FAM, int RB>
@@ -529,7 +694,7 @@ __global__ void __launch_bounds__(GW * 32, 4) grad_param_kernel(
 //   contribution = sum_{a,b} w_a a~_b dK_ab + rho . (sum_b a~_b dU_b) + sig . (sum_b beta~_b dU_b),
 //   w = mu a~ - Dm beta~,  rho = -2 mu p + Dm (q + g_i),  sig = Dm p,  p = sum_b a~_b U_b,  q = sum_b beta~_b U_b.
 // The cross-Gram (s^2 m DMMA work per parameter) becomes two gathered sums (2 s m).
-constexpr int ADJ_STRIDE = 40;  // per point: mu, Dm, beta~[0..SP)
+constexpr int ADJ_STRIDE = 56;  // per point: mu, Dm, beta~[0..SP), SP <= 48
 
 template <int RB>
 __global__ void __launch_bounds__(GW * 32) grad_adjoint_kernel(const double* __restrict__ U,
@@ -547,48 +712,65 @@ __global__ void __launch_bounds__(GW * 32) grad_adjoint_kernel(const double* __r
   const int64_t pos = (int64_t)blockIdx.x * GW + warp;
   if (pos >= npts) return;
   const int64_t i = order[pos];
-  const int nb0 = lane < mv ? nbr[i * mv + lane] : -1;
-  const int q = __popc(__ballot_sync(0xffffffffu, nb0 >= 0));
-  const int myidx = lane < q ? nb0 : (lane == q ? (int)i : -1);
   int* Sidx = Sidx_all[warp];
   double* at = at_all[warp];
   double* bt = bt_all[warp];
-  if (lane < SP) Sidx[lane] = myidx;
+  const int q = grad_load_S(nbr, mv, i, lane, SP, Sidx);
   const double* st = state + pos * (int64_t)state_doubles<RB>();
-  const double a = lane < SP ? st[LP + lane] : 0.0;
-  const double myinv = lane < SP ? st[LP + SP + lane] : 1.0;
-  const double gam = lane < SP ? st[LP + 2 * SP + lane] : 0.0;
   const double Di = st[LP + 3 * SP];
-  const double atl = lane < q ? -a : (lane == q ? 1.0 : 0.0);
-  double ag = atl * gam;
+  double ag = 0.0;
+  for (int t = lane; t < SP; t += 32) {
+    const double atl = t < q ? -st[LP + t] : (t == q ? 1.0 : 0.0);
+    at[t] = atl;
+    ag = fma(atl, st[LP + 2 * SP + t], ag);
+  }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) ag += __shfl_xor_sync(0xffffffffu, ag, o);
   const double Dm = rsqrt_nr(Di);
   const double mu = 0.5 / Di - 0.5 * Dm * Dm * Dm * ag;
   // beta = C_NN^{-1} gam_N = L_NN^{-T} L_NN^{-1} gam_N (rows of L packed in the state)
-  double y = lane < q ? gam : 0.0;
-  for (int j = 0; j < q; ++j) {
-    const double yj = __shfl_sync(0xffffffffu, y * myinv, j);
-    if (lane == j) y = yj;
-    else if (lane > j && lane < q) y = fma(-st[lane * (lane + 1) / 2 + j], yj, y);
+  if constexpr (SP <= 32) {
+    const double myinv = lane < SP ? st[LP + SP + lane] : 1.0;
+    double y = lane < q ? st[LP + 2 * SP + lane] : 0.0;
+    for (int j = 0; j < q; ++j) {
+      const double yj = __shfl_sync(0xffffffffu, y * myinv, j);
+      if (lane == j) y = yj;
+      else if (lane > j && lane < q) y = fma(-st[lane * (lane + 1) / 2 + j], yj, y);
+    }
+    for (int j = q - 1; j >= 0; --j) {
+      const double xj = __shfl_sync(0xffffffffu, y * myinv, j);
+      if (lane == j) y = xj;
+      else if (lane < j) y = fma(-st[j * (j + 1) / 2 + lane], xj, y);
+    }
+    if (lane < SP) bt[lane] = lane < q ? y : 0.0;
+  } else {
+    // s > 32: substitutions one unknown at a time, the dot products over the lanes
+    for (int t = lane; t < SP; t += 32) bt[t] = 0.0;
+    __syncwarp();
+    for (int j = 0; j < q; ++j) {
+      double sm = 0.0;
+      for (int k = lane; k < j; k += 32) sm = fma(st[j * (j + 1) / 2 + k], bt[k], sm);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) sm += __shfl_xor_sync(0xffffffffu, sm, o);
+      if (lane == 0) bt[j] = (st[LP + 2 * SP + j] - sm) * st[LP + SP + j];
+      __syncwarp();
+    }
+    for (int j = q - 1; j >= 0; --j) {
+      double sm = 0.0;
+      for (int k = j + 1 + lane; k < q; k += 32) sm = fma(st[k * (k + 1) / 2 + j], bt[k], sm);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) sm += __shfl_xor_sync(0xffffffffu, sm, o);
+      if (lane == 0) bt[j] = (bt[j] - sm) * st[LP + SP + j];
+      __syncwarp();
+    }
   }
-  for (int j = q - 1; j >= 0; --j) {
-    const double xj = __shfl_sync(0xffffffffu, y * myinv, j);
-    if (lane == j) y = xj;
-    else if (lane < j) y = fma(-st[j * (j + 1) / 2 + lane], xj, y);
-  }
-  const double btl = lane < q ? y : 0.0;
-  if (lane < SP) {
-    at[lane] = atl;
-    bt[lane] = btl;
-  }
+  __syncwarp();
   double* ad = adj + pos * (int64_t)ADJ_STRIDE;
-  if (lane < SP) ad[2 + lane] = btl;
+  for (int t = lane; t < SP; t += 32) ad[2 + t] = bt[t];
   if (lane == 0) {
     ad[0] = mu;
     ad[1] = Dm;
   }
-  __syncwarp();
   const int s = q + 1;
   const double* grow = Gam + pos * (int64_t)ld;
   double* rrow = rho + pos * (int64_t)mk;
@@ -625,28 +807,26 @@ __global__ void __launch_bounds__(GW * 32) grad_param_adj_kernel(
   double contrib = 0.0;
   if (pos < npts) {
     const int64_t i = order[pos];
-    const int nb0 = lane < mv ? nbr[i * mv + lane] : -1;
-    const int q = __popc(__ballot_sync(0xffffffffu, nb0 >= 0));
-    const int s = q + 1;
-    const int myidx = lane < q ? nb0 : (lane == q ? (int)i : -1);
     int* Sidx = Sidx_all[warp];
     double* at = at_all[warp];
     double* bt = bt_all[warp];
     double* wv = w_all[warp];
     double* xs = xs_all[warp];
-    if (lane < SP) Sidx[lane] = myidx;
-    if (lane < s)
-      for (int k = 0; k < p.d; ++k) xs[lane * p.d + k] = X[(int64_t)myidx * p.d + k] * (fam_scale<FAM>() * p.inv_ls[k]);
+    const int q = grad_load_S(nbr, mv, i, lane, SP, Sidx);
+    const int s = q + 1;
+    __syncwarp();
+    for (int t = lane; t < s; t += 32)
+      for (int k = 0; k < p.d; ++k) xs[t * p.d + k] = X[(int64_t)Sidx[t] * p.d + k] * (fam_scale<FAM>() * p.inv_ls[k]);
     const double* st = state + pos * (int64_t)state_doubles<RB>();
     const bool ok = st[LP + 3 * SP + 1] != 0.0;
     const double* ad = adj + pos * (int64_t)ADJ_STRIDE;
     const double mu = ad[0], Dm = ad[1];
-    if (lane < SP) {
-      const double atl = lane < q ? -st[LP + lane] : (lane == q ? 1.0 : 0.0);
-      const double btl = ad[2 + lane];
-      at[lane] = atl;
-      bt[lane] = btl;
-      wv[lane] = fma(mu, atl, -Dm * btl);
+    for (int t = lane; t < SP; t += 32) {
+      const double atl = t < q ? -st[LP + t] : (t == q ? 1.0 : 0.0);
+      const double btl = ad[2 + t];
+      at[t] = atl;
+      bt[t] = btl;
+      wv[t] = fma(mu, atl, -Dm * btl);
     }
     __syncwarp();
     // sum_{a,b} w_a a~_b dK_ab over the lower triangle (dK symmetric); nugget: dK = I
@@ -711,13 +891,15 @@ cudaError_t launch_param_adj_fam(const GradPointArgs& a, cudaStream_t s) {
     case 1: return launch_param_adj_rb<FAM, 1>(a, s);
     case 2: return launch_param_adj_rb<FAM, 2>(a, s);
     case 3: return launch_param_adj_rb<FAM, 3>(a, s);
-    default: return launch_param_adj_rb<FAM, 4>(a, s);
+    case 4: return launch_param_adj_rb<FAM, 4>(a, s);
+    case 5: return launch_param_adj_rb<FAM, 5>(a, s);
+    default: return launch_param_adj_rb<FAM, 6>(a, s);
   }
 }
 
 // ---- no dU at all: <R, dU> = <R L_m^{-1}, dK(X,Z)> - <R^T U, Phi_low>, R = sum over the points of the
 // adjoint rows scattered to their conditioning sets (a deterministic gather over children lists) ----
-// children of point j: entries e = pos * 32 + b with S_{order[pos]}[b] = j (b = q: the point itself)
+// children of point j: entries e = pos * 64 + b with S_{order[pos]}[b] = j (b = q: the point itself)
 __global__ void gchild_count_kernel(const int32_t* __restrict__ nbr, int mv, const int64_t* __restrict__ order,
                                     int64_t npts, int* __restrict__ cnt) {
   for (int64_t pos = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; pos < npts; pos += (int64_t)gridDim.x * blockDim.x) {
@@ -740,9 +922,9 @@ __global__ void gchild_fill_kernel(const int32_t* __restrict__ nbr, int mv, cons
     for (; b < mv; ++b) {
       const int j = nbr[i * mv + b];
       if (j < 0) break;
-      ent[ptr[j] + atomicAdd(cursor + j, 1)] = (int)(pos * 32 + b);
+      ent[ptr[j] + atomicAdd(cursor + j, 1)] = (int)(pos * 64 + b);
     }
-    ent[ptr[i] + atomicAdd(cursor + i, 1)] = (int)(pos * 32 + b);
+    ent[ptr[i] + atomicAdd(cursor + i, 1)] = (int)(pos * 64 + b);
   }
 }
 
@@ -808,8 +990,8 @@ __global__ void __launch_bounds__(256) gR_kernel(const int* __restrict__ ptr, co
       for (int u = 0; u < CPL; ++u) acc[u] = 0.0;
       for (int e = a; e < b; ++e) {
         const int en = ent[e];
-        const int64_t pos = en >> 5;
-        const int bb = en & 31;
+        const int64_t pos = en >> 6;
+        const int bb = en & 63;
         const bool self = order[pos] == j;
         const double al = self ? 1.0 : -state[pos * (int64_t)state_doubles<RB>() + LP + bb];
         const double be = self ? 0.0 : adj[pos * (int64_t)ADJ_STRIDE + 2 + bb];
@@ -977,12 +1159,41 @@ size_t grad_state_doubles(int mv) {
     case 1: return state_doubles<1>();
     case 2: return state_doubles<2>();
     case 3: return state_doubles<3>();
-    default: return state_doubles<4>();
+    case 4: return state_doubles<4>();
+    case 5: return state_doubles<5>();
+    default: return state_doubles<6>();
   }
 }
 
+template <int FAM, int RB>
+cudaError_t launch_state_big_rb(const GradPointArgs& a, cudaStream_t s) {
+  const size_t smem = (size_t)GW * big_warp_doubles<RB>(a.p.d) * sizeof(double);
+  if (smem > 40 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(grad_state_big_kernel<FAM, RB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  const unsigned blocks = (unsigned)((a.npts + GW - 1) / GW);
+  grad_state_big_kernel<FAM, RB><<<blocks, GW * 32, smem, s>>>(a.U, a.Gam, a.ldu, a.mk, a.ld, a.X, a.nbr, a.mv,
+                                                              a.order, a.npts, a.p, a.state);
+  return cudaGetLastError();
+}
+
+template <int FAM>
+cudaError_t launch_state_big_fam(const GradPointArgs& a, cudaStream_t s) {
+  return (a.mv + 1 + 7) / 8 == 5 ? launch_state_big_rb<FAM, 5>(a, s) : launch_state_big_rb<FAM, 6>(a, s);
+}
+
 cudaError_t launch_grad_state(const GradPointArgs& a, cudaStream_t s) {
-  if (a.mv > 31) return cudaErrorNotSupported;
+  if (a.npts > 0 && a.mv > 31 && a.mv <= 47) {
+    switch (a.p.family) {
+      case FAM_M12: return launch_state_big_fam<FAM_M12>(a, s);
+      case FAM_M32: return launch_state_big_fam<FAM_M32>(a, s);
+      case FAM_M52: return launch_state_big_fam<FAM_M52>(a, s);
+      default: return launch_state_big_fam<FAM_GAUSS>(a, s);
+    }
+  }
+  if (a.mv > 47) return cudaErrorNotSupported;
   return a.npts > 0 ? launch_grad_any(a, true, s) : cudaSuccess;
 }
 
@@ -999,18 +1210,20 @@ cudaError_t launch_grad_points(const GradPointArgs& a, double* out, cudaStream_t
 size_t grad_adj_doubles() { return ADJ_STRIDE; }
 
 cudaError_t launch_grad_adjoint(const GradPointArgs& a, cudaStream_t s) {
-  if (a.mv > 31) return cudaErrorNotSupported;
+  if (a.mv > 47) return cudaErrorNotSupported;
   if (a.npts == 0) return cudaSuccess;
   switch ((a.mv + 1 + 7) / 8) {
     case 1: return launch_adj_rb<1>(a, s);
     case 2: return launch_adj_rb<2>(a, s);
     case 3: return launch_adj_rb<3>(a, s);
-    default: return launch_adj_rb<4>(a, s);
+    case 4: return launch_adj_rb<4>(a, s);
+    case 5: return launch_adj_rb<5>(a, s);
+    default: return launch_adj_rb<6>(a, s);
   }
 }
 
 cudaError_t launch_grad_points_adj(const GradPointArgs& a, double* out, cudaStream_t s) {
-  if (a.mv > 31) return cudaErrorNotSupported;
+  if (a.mv > 47) return cudaErrorNotSupported;
   if (a.npts > 0) {
     cudaError_t e;
     switch (a.p.family) {
@@ -1042,13 +1255,15 @@ cudaError_t launch_gchild(const int32_t* nbr, int mv, const int64_t* order, int6
 cudaError_t launch_gR(const int* ptr, const int* ent, const int64_t* order, const int64_t* jorder, int64_t n, int mk,
                       int mv, const double* state, const double* adj, const double* rho, const double* sig, double* R,
                       cudaStream_t s) {
-  if (mv > 31) return cudaErrorNotSupported;
+  if (mv > 47) return cudaErrorNotSupported;
   const unsigned blocks = (unsigned)((n + 7) / 8 > 148 * 16 ? 148 * 16 : (n + 7) / 8);
   switch ((mv + 1 + 7) / 8) {
     case 1: gR_kernel<1><<<blocks, 256, 0, s>>>(ptr, ent, order, jorder, n, mk, state, adj, rho, sig, R); break;
     case 2: gR_kernel<2><<<blocks, 256, 0, s>>>(ptr, ent, order, jorder, n, mk, state, adj, rho, sig, R); break;
     case 3: gR_kernel<3><<<blocks, 256, 0, s>>>(ptr, ent, order, jorder, n, mk, state, adj, rho, sig, R); break;
-    default: gR_kernel<4><<<blocks, 256, 0, s>>>(ptr, ent, order, jorder, n, mk, state, adj, rho, sig, R); break;
+    case 4: gR_kernel<4><<<blocks, 256, 0, s>>>(ptr, ent, order, jorder, n, mk, state, adj, rho, sig, R); break;
+    case 5: gR_kernel<5><<<blocks, 256, 0, s>>>(ptr, ent, order, jorder, n, mk, state, adj, rho, sig, R); break;
+    default: gR_kernel<6><<<blocks, 256, 0, s>>>(ptr, ent, order, jorder, n, mk, state, adj, rho, sig, R); break;
   }
   return cudaGetLastError();
 }

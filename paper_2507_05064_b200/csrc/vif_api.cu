@@ -1224,7 +1224,12 @@ int vif_grad(void* handle, const vif_theta* theta, void* gws, size_t gws_bytes, 
   if (!h) return fail(nullptr, VIF_ERR_INVALID_ARG, "handle is NULL");
   if (!grad) return fail(h, VIF_ERR_INVALID_ARG, "grad is NULL");
   const Plan& P = h->P;
-  if (P.mv > 31) return fail(h, VIF_ERR_INVALID_ARG, "vif_grad: m_v <= 31 only in this version");
+  {
+    static const char* cross_env0 = getenv("VIF_GRAD_CROSS");
+    const bool cross0 = cross_env0 && cross_env0[0] == '1';
+    if (P.mv > 47 || (cross0 && P.mv > 31))
+      return fail(h, VIF_ERR_INVALID_ARG, "vif_grad: m_v <= 47 (<= 31 with VIF_GRAD_CROSS=1) in this version");
+  }
   const Layout GL = make_grad_layout(P);
   if (!gws || gws_bytes < GL.total) {
     char msg[128];
