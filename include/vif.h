@@ -188,7 +188,9 @@ int vif_predict(void* handle, const vif_theta* theta, int64_t np, const double* 
  * predecessors by length-scale-scaled Euclidean distance).  Exact brute force (n^2 m / 2 FMA on the
  * FP64 tensor cores).  nbr_out: device, n x mv int32, -1 padded; mv in [1, VIF_MAX_MV] (independent of
  * dims.mv).  Uses the handle's workspace (invalidates a previous vif_factor: call vif_factor again).
- * Single rank.  Errors: INVALID_ARG, NOT_PD (K(Z,Z) + jitter), CUDA. */
+ * Multi-rank: every rank evaluates u_i of all n points; rank g searches the 64-point query blocks
+ * kb = g, g + G, ... (counted from the last block) and writes only their rows of the full-length nbr_out;
+ * an emulated handle writes all rows.  Errors: INVALID_ARG, NOT_PD (K(Z,Z) + jitter), CUDA. */
 int vif_neighbors(void* handle, const vif_theta* theta, int32_t mv, int32_t* nbr_out);
 
 /* ---- VIF-Laplace iterative path (Bernoulli likelihood, logit link; Sect. 2-3) ----

@@ -44,7 +44,7 @@ template <int FAM>
 __global__ void __launch_bounds__(256, 2) knn_kernel(const double* __restrict__ U, int64_t ldu, int mk,
                                                     const double* __restrict__ X, int64_t n, CovParams p,
                                                     const double* __restrict__ isd, const int* __restrict__ deg,
-                                                    int mv, int32_t* __restrict__ out) {
+                                                    int mv, int32_t* __restrict__ out, int qoff, int qstride) {
   extern __shared__ __align__(16) double ksm[];
   double* As = ksm;                              // [KST][KQ][KPAD]
   double* Bs = As + KST * KQ * KPAD;             // [KST][KQ][KPAD]
@@ -58,7 +58,9 @@ __global__ void __launch_bounds__(256, 2) knn_kernel(const double* __restrict__ 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int wm = warp >> 2, wn = warp & 3;  // 2 x 4 warps of 32 x 16
   const int64_t nq = (n + KQ - 1) / KQ;
-  const int64_t q0 = (nq - 1 - blockIdx.x) * KQ;  // largest (longest) query blocks first
+  // query blocks of this rank: kb = nq - 1 - (qoff + qstride * blockIdx.x), largest (longest) first; the
+  // cyclic assignment balances the triangular work over the ranks
+  const int64_t q0 = (nq - 1 - (qoff + (int64_t)qstride * blockIdx.x)) * KQ;
   exp_table_init(tbl, p.sigma2, tid);
   for (int e = tid; e < KQ * p.d; e += blockDim.x) {
     const int r = e / p.d, k = e % p.d;
@@ -197,16 +199,18 @@ size_t knn_smem_bytes(int mv) {
 }
 
 cudaError_t launch_knn(const double* U, int64_t ldu, int m, int mk, const double* X, int64_t n, const CovParams& p,
-                       double* isd, int* deg, int mv, int32_t* out, cudaStream_t s) {
+                       double* isd, int* deg, int mv, int32_t* out, cudaStream_t s, int qoff, int qstride) {
   if (n == 0 || mv == 0) return cudaSuccess;
   if (mv > KMAXMV) return cudaErrorInvalidValue;
   resvar_kernel<<<(unsigned)((n + 7) / 8), 256, 0, s>>>(U, (int)ldu, m, n, p.sigma2, isd, deg);
   const size_t smem = knn_smem_bytes(mv);
-  const unsigned grid = (unsigned)((n + KQ - 1) / KQ);
+  const int64_t nq = (n + KQ - 1) / KQ;
+  if (qoff >= nq) return cudaGetLastError();
+  const unsigned grid = (unsigned)((nq - qoff + qstride - 1) / qstride);
   auto go = [&](auto kern) -> cudaError_t {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    kern<<<grid, 256, smem, s>>>(U, ldu, mk, X, n, p, isd, deg, mv, out);
+    kern<<<grid, 256, smem, s>>>(U, ldu, mk, X, n, p, isd, deg, mv, out, qoff, qstride);
     return cudaGetLastError();
   };
   switch (p.family) {

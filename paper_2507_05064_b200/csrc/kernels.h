@@ -121,7 +121,7 @@ cudaError_t launch_pred_mean(const double* Wp, int ld, int m, int ycol, const do
 // correlation-distance neighbours (k_knn.cu)
 size_t knn_smem_bytes(int mv);
 cudaError_t launch_knn(const double* U, int64_t ldu, int m, int mk, const double* X, int64_t n, const CovParams& p,
-                       double* isd, int* deg, int mv, int32_t* out, cudaStream_t s);
+                       double* isd, int* deg, int mv, int32_t* out, cudaStream_t s, int qoff = 0, int qstride = 1);
 // VIF-Laplace iterative path (k_laplace.cu)
 cudaError_t launch_la_transpose_struct(const int32_t* nbr, int64_t n, int mv, int* cnt, int* cursor, int* tptr,
                                        int* tpos, cudaStream_t s);

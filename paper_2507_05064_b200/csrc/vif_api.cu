@@ -1506,7 +1506,6 @@ int vif_neighbors(void* handle, const vif_theta* theta, int32_t mv, int32_t* nbr
   if (!h) return fail(nullptr, VIF_ERR_INVALID_ARG, "handle is NULL");
   const Plan& P = h->P;
   if (!nbr_out || mv < 1 || mv > VIF_MAX_MV) return fail(h, VIF_ERR_INVALID_ARG, "vif_neighbors: bad arguments");
-  if (P.world != 1) return fail(h, VIF_ERR_INVALID_ARG, "vif_neighbors: single-rank handles only");
   if (!h->have_data) return fail(h, VIF_ERR_STATE, "no data");
   CovParams p;
   std::string err;
@@ -1527,13 +1526,34 @@ int vif_neighbors(void* handle, const vif_theta* theta, int32_t mv, int32_t* nbr
     VIF_CUDA(h, launch_chol_inv(h->buf<double>(B_KM), P.m, P.m, 0.0, h->buf<double>(B_LINV), P.mk, P.mk, 1,
                                 h->buf<double>(B_TSCR), &st->km_fail, h->num_sms, s),
              "chol K_m");
-    VIF_CUDA(h, launch_u_features(h->buf<double>(B_X), h->buf<double>(B_Z), h->buf<double>(B_Y), P.n, 0, P.n, P.n, 1, 0,
-                                  P.m, P.mk, p, h->buf<double>(B_LINV), h->buf<double>(B_W), h->buf<double>(B_U),
-                                  P.ld, s),
-             "U features");
+    // every rank needs u_i of all n points: in row blocks through the W buffer (npos x ld per rank)
+    static const char* cap_env = getenv("VIF_KNN_UROWS");  // test hook: smaller row blocks
+    int64_t cap = (int64_t)(h->L.size[B_W] / sizeof(double)) / P.mk;
+    if (cap_env && atoll(cap_env) > 0 && atoll(cap_env) < cap) cap = atoll(cap_env);
+    for (int64_t r0 = 0; r0 < P.n; r0 += cap) {
+      const int64_t rows = std::min<int64_t>(cap, P.n - r0);
+      VIF_CUDA(h, launch_u_features(h->buf<double>(B_X), h->buf<double>(B_Z), h->buf<double>(B_Y), P.n, r0, rows, P.n, 1,
+                                    0, P.m, P.mk, p, h->buf<double>(B_LINV), h->buf<double>(B_W) - r0 * P.mk,
+                                    h->buf<double>(B_U), P.ld, s),
+               "U features");
+    }
   }
-  VIF_CUDA(h, launch_knn(h->buf<double>(B_U), P.ld, P.m, P.mk, h->buf<double>(B_X), P.n, p, h->buf<double>(B_DPOS),
-                         reinterpret_cast<int*>(h->buf<uint64_t>(B_KEYS)), mv, nbr_out, s),
+  // residual variances (n doubles) and degeneracy flags (n ints) in the dead W buffer; ranks (NCCL) search
+  // the query blocks kb = rank, rank + world, ... (64 points each) and write only those rows
+  double* isd = h->buf<double>(P.m > 0 ? B_W : B_U);  // (m = 0: U is unused; W could be only 8 n bytes)
+  int* deg = reinterpret_cast<int*>(isd + P.n);
+  const bool nccl_ranks = P.world > 1 && !P.emulate;
+  int qoff = nccl_ranks ? P.rank : 0, qstride = nccl_ranks ? P.world : 1;
+  static const char* shard_env = getenv("VIF_KNN_SHARD");  // test hook "g,G": search rank g's blocks of G
+  if (shard_env) {
+    int g = 0, G = 1;
+    if (sscanf(shard_env, "%d,%d", &g, &G) == 2 && G >= 1 && g >= 0 && g < G) {
+      qoff = g;
+      qstride = G;
+    }
+  }
+  VIF_CUDA(h, launch_knn(h->buf<double>(B_U), P.ld, P.m, P.mk, h->buf<double>(B_X), P.n, p, isd, deg, mv, nbr_out, s,
+                         qoff, qstride),
            "neighbour search");
   {
     int r = mark_inputs_used(h);

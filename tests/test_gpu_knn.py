@@ -82,3 +82,81 @@ def test_knn_matches_generator_config2_subset():
     g = knn_parity(w, 20)
     agree = (g == w.nbr).all(1).mean()
     assert agree > 0.995
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_emulated_world_same_sets(world):
+    """An emulated multi-rank handle searches every query block: the sets equal the one-rank result."""
+    import paper_2507_05064_b200 as p
+    w = vifgen.make_workload(n=1500, d=2, m=30, mv=12, family="matern32", rho=0.15, nugget=0.1, seed=21,
+                             device="cuda")
+    dev = torch.device("cuda")
+    X, Z, nbr, y = (torch.from_numpy(np.ascontiguousarray(a)).to(dev) for a in (w.X, w.Z, w.nbr, w.y))
+    th = p.Theta(**w.theta_dict())
+    outs = []
+    for wd in (1, world):
+        model = p.VifModel(X, Z, nbr, y, world=wd, device=dev)
+        outs.append(model.neighbors(th, 12).cpu().numpy())
+        model.close()
+    np.testing.assert_array_equal(outs[1], outs[0])
+
+
+def test_u_in_row_blocks_same_sets():
+    """u_i computed in row blocks (the multi-rank path; forced small blocks) gives the same sets."""
+    import json
+    import os
+    import subprocess
+    import sys
+    code = r"""
+import sys, json
+import numpy as np, torch
+sys.path.insert(0, %r)
+import paper_2507_05064_b200 as p, vifgen
+w = vifgen.make_workload(n=1100, d=2, m=40, mv=10, family="matern52", rho=0.2, nugget=0.1, seed=22, device="cuda")
+dev = torch.device("cuda")
+X, Z, nbr, y = (torch.from_numpy(np.ascontiguousarray(a)).to(dev) for a in (w.X, w.Z, w.nbr, w.y))
+m = p.VifModel(X, Z, nbr, y, device=dev)
+print(json.dumps(m.neighbors(p.Theta(**w.theta_dict()), 10).cpu().numpy().tolist()))
+""" % os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    res = []
+    for rows in ("0", "137"):
+        r = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, VIF_KNN_UROWS=rows),
+                           capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+        res.append(np.array(json.loads(r.stdout.strip().splitlines()[-1])))
+    np.testing.assert_array_equal(res[1], res[0])
+
+
+def test_query_block_shards_cover_every_row():
+    """The rank-g query blocks (kb = g, g + G, ...) of G ranks write disjoint rows that together equal the
+    one-rank result (VIF_KNN_SHARD test hook: one process plays each rank's search in turn)."""
+    import json
+    import os
+    import subprocess
+    import sys
+    code = r"""
+import sys, json
+import numpy as np, torch
+sys.path.insert(0, %r)
+import paper_2507_05064_b200 as p, vifgen
+w = vifgen.make_workload(n=1300, d=2, m=25, mv=11, family="matern32", rho=0.15, nugget=0.1, seed=23, device="cuda")
+dev = torch.device("cuda")
+X, Z, nbr, y = (torch.from_numpy(np.ascontiguousarray(a)).to(dev) for a in (w.X, w.Z, w.nbr, w.y))
+m = p.VifModel(X, Z, nbr, y, device=dev)
+out = torch.full((w.n, 11), -7, dtype=torch.int32, device=dev)
+p.vif_neighbors(m.handle, p.Theta(**w.theta_dict()), 11, out)
+print(json.dumps(out.cpu().numpy().tolist()))
+""" % os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    def run(shard):
+        env = dict(os.environ)
+        if shard:
+            env["VIF_KNN_SHARD"] = shard
+        r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+        return np.array(json.loads(r.stdout.strip().splitlines()[-1]))
+    full = run(None)
+    parts = [run(f"{g},3") for g in range(3)]
+    written = [(pt != -7).all(1) for pt in parts]
+    assert np.array_equal(sum(wr.astype(int) for wr in written), np.ones(full.shape[0], int))  # disjoint, complete
+    merged = np.where(written[0][:, None], parts[0], np.where(written[1][:, None], parts[1], parts[2]))
+    np.testing.assert_array_equal(merged, full)
