@@ -1313,7 +1313,8 @@ int vif_grad(void* handle, const vif_theta* theta, void* gws, size_t gws_bytes, 
                                 reinterpret_cast<int*>(gbuf(G_CCUR)), reinterpret_cast<int*>(gbuf(G_CPTR)),
                                 reinterpret_cast<int*>(gbuf(G_CENT)), s),
                "children lists");
-      const int64_t* jorder = nullptr;  // index order (the Morton processing order measured slower)
+      static const char* jo_env = getenv("VIF_GRAD_RORDER");  // R rows in the Morton order (1-2% faster); 0: index order
+      const int64_t* jorder = (!(jo_env && jo_env[0] == '0') && P.world == 1) ? h->ord(0) : nullptr;
       VIF_CUDA(h, launch_gR(reinterpret_cast<int*>(gbuf(G_CPTR)), reinterpret_cast<int*>(gbuf(G_CENT)), a.order,
                             jorder, P.n, mk, P.mv, a.state, a.adj, a.rho, a.sig, R, s),
                "R");
