@@ -206,3 +206,29 @@ def test_sigma_inv_inverts_sigma():
     back = model.la_apply("sigma_inv", model.la_apply("sigma", V)).cpu().numpy()
     assert rel_err(back, V) < 1e-8
     model.close()
+
+
+def test_truncated_cg_iteration_exact():
+    """CG capped at 6 iterations (Newton solves and probe solves): both sides stop at the same iteration,
+    so the iterates, the Lanczos matrices and L^VIFLA still agree (tests the per-iteration arithmetic,
+    not only the converged answer)."""
+    p = vif()
+    w = work(500, 20, 10, seed=19)
+    th = p.Theta(**w.theta_dict())
+    model = model_of(w, th, nprobe=5, max_cg=6)
+    eps1, eps2 = vifgen.make_probes(w.n, 20, 5)
+    opts = p.LaOpts(max_newton=8, newton_tol=1e-14, max_cg=6, cg_tol=1e-14, nprobe=5, slq_tol=1e-14)
+    t, b = model.la_nll(w.y, opts, eps1, eps2)
+    r = la.vifla_nll(w.X, w.Z, w.nbr, w.y, oracle.Theta(**w.theta_dict()), eps1=eps1, eps2=eps2, newton_tol=1e-14,
+                     max_newton=8, cg_tol=1e-14, max_cg=6, slq_tol=1e-14)
+    assert t.newton_iters == r.newton_iters and t.slq_iters_max == max(r.slq_iters) == 6
+    np.testing.assert_allclose(b.cpu().numpy(), r.b, rtol=1e-9, atol=1e-10 * np.abs(r.b).max())
+    assert t.logdet == pytest.approx(r.logdet, rel=1e-9)
+    assert t.nll == pytest.approx(r.nll, rel=1e-9)
+    model.close()
+
+
+def test_tiny_problem_no_neighbours_no_inducing():
+    """n = 40 with m = 0 and m_v = 0 (B = I, Sigma_dagger = D diagonal) and n = 7 < 32 rows."""
+    for n, m, mv in ((40, 0, 0), (7, 3, 4)):
+        mode_parity(work(n, m, mv, seed=n), nprobe=3)
