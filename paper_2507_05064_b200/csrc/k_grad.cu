@@ -976,12 +976,19 @@ __global__ void __launch_bounds__(256) gR_kernel(const int* __restrict__ ptr, co
                                                  const int64_t* __restrict__ order, const int64_t* __restrict__ jorder,
                                                  int64_t n, int mk, const double* __restrict__ state,
                                                  const double* __restrict__ adj, const double* __restrict__ rho,
-                                                 const double* __restrict__ sig, double* __restrict__ R) {
+                                                 const double* __restrict__ sig, double* __restrict__ R,
+                                                 unsigned long long* __restrict__ next) {
   constexpr int SP = RB * 8;
   constexpr int LP = SP * (SP + 1) / 2;
   constexpr int CPL = 4;  // columns per lane per pass (16: slower at n = 1M, 240 vs 232 ms per gradient)
   const int lane = threadIdx.x & 31;
-  for (int64_t t = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5); t < n; t += (int64_t)gridDim.x * 8) {
+  // rows are handed out by a counter (not grid-strided): warps with long children lists would otherwise
+  // drift apart and the window of rows in flight -- whose adjoint rows should stay in L2 -- would spread
+  for (;;) {
+    unsigned long long tt = 0;
+    if (lane == 0) tt = atomicAdd(next, 1ull);
+    const int64_t t = (int64_t)__shfl_sync(0xffffffffu, tt, 0);
+    if (t >= n) break;
     const int64_t j = jorder ? jorder[t] : t;
     const int a = ptr[j], b = ptr[j + 1];
     for (int k0 = 0; k0 < mk; k0 += 32 * CPL) {
@@ -1254,16 +1261,22 @@ cudaError_t launch_gchild(const int32_t* nbr, int mv, const int64_t* order, int6
 
 cudaError_t launch_gR(const int* ptr, const int* ent, const int64_t* order, const int64_t* jorder, int64_t n, int mk,
                       int mv, const double* state, const double* adj, const double* rho, const double* sig, double* R,
-                      cudaStream_t s) {
+                      unsigned long long* next, cudaStream_t s) {
+  cudaError_t e0 = cudaMemsetAsync(next, 0, sizeof(unsigned long long), s);
+  if (e0 != cudaSuccess) return e0;
   if (mv > 47) return cudaErrorNotSupported;
-  const unsigned blocks = (unsigned)((n + 7) / 8 > 148 * 16 ? 148 * 16 : (n + 7) / 8);
+  // a resident-sized grid: the warps advance through the visiting order together, so the rows they read
+  // (the adjoint rows of nearby points) stay within a window that fits L2; VIF_GR_BLOCKS overrides
+  static const char* gb_env = getenv("VIF_GR_BLOCKS");
+  const int64_t cap = gb_env ? atoll(gb_env) : 148 * 8;
+  const unsigned blocks = (unsigned)((n + 7) / 8 > cap ? cap : (n + 7) / 8);
   switch ((mv + 1 + 7) / 8) {
-    case 1: gR_kernel<1><<<blocks, 256, 0, s>>>(ptr, ent, order, jorder, n, mk, state, adj, rho, sig, R); break;
-    case 2: gR_kernel<2><<<blocks, 256, 0, s>>>(ptr, ent, order, jorder, n, mk, state, adj, rho, sig, R); break;
-    case 3: gR_kernel<3><<<blocks, 256, 0, s>>>(ptr, ent, order, jorder, n, mk, state, adj, rho, sig, R); break;
-    case 4: gR_kernel<4><<<blocks, 256, 0, s>>>(ptr, ent, order, jorder, n, mk, state, adj, rho, sig, R); break;
-    case 5: gR_kernel<5><<<blocks, 256, 0, s>>>(ptr, ent, order, jorder, n, mk, state, adj, rho, sig, R); break;
-    default: gR_kernel<6><<<blocks, 256, 0, s>>>(ptr, ent, order, jorder, n, mk, state, adj, rho, sig, R); break;
+    case 1: gR_kernel<1><<<blocks, 256, 0, s>>>(ptr, ent, order, jorder, n, mk, state, adj, rho, sig, R, next); break;
+    case 2: gR_kernel<2><<<blocks, 256, 0, s>>>(ptr, ent, order, jorder, n, mk, state, adj, rho, sig, R, next); break;
+    case 3: gR_kernel<3><<<blocks, 256, 0, s>>>(ptr, ent, order, jorder, n, mk, state, adj, rho, sig, R, next); break;
+    case 4: gR_kernel<4><<<blocks, 256, 0, s>>>(ptr, ent, order, jorder, n, mk, state, adj, rho, sig, R, next); break;
+    case 5: gR_kernel<5><<<blocks, 256, 0, s>>>(ptr, ent, order, jorder, n, mk, state, adj, rho, sig, R, next); break;
+    default: gR_kernel<6><<<blocks, 256, 0, s>>>(ptr, ent, order, jorder, n, mk, state, adj, rho, sig, R, next); break;
   }
   return cudaGetLastError();
 }

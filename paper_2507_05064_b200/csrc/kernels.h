@@ -97,7 +97,7 @@ cudaError_t launch_gchild(const int32_t* nbr, int mv, const int64_t* order, int6
 cudaError_t launch_gR(const int* ptr, const int* ent, const int64_t* order, const int64_t* jorder, int64_t n, int mk,
                       int mv,
                       const double* state, const double* adj, const double* rho, const double* sig, double* R,
-                      cudaStream_t s);
+                      unsigned long long* next, cudaStream_t s);
 int gTdK_blocks();
 cudaError_t launch_gTdK(const double* X, const double* Z, int64_t n, int m, int mk, const CovParams& p,
                         const double* T, double* part, double* out, cudaStream_t s);

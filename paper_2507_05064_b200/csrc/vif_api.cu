@@ -403,7 +403,7 @@ Layout make_grad_layout(const Plan& P) {
   L.size[G_CENT] = (size_t)P.n * (P.mv + 1) * sizeof(int);
   L.size[G_TSP] = (size_t)la_ts_nsplit(P.n) * 64 * mk1 * D8;
   L.size[G_TDKP] = (size_t)gTdK_blocks() * (P.d + 1) * D8;
-  L.size[G_TDK] = (size_t)(P.d + 1) * D8;
+  L.size[G_TDK] = (size_t)(P.d + 2) * D8;  // + the R gather's row counter
   size_t off = 0;
   for (int b = 0; b < G_COUNT; ++b) {
     L.off[b] = off;
@@ -1316,7 +1316,8 @@ int vif_grad(void* handle, const vif_theta* theta, void* gws, size_t gws_bytes, 
       static const char* jo_env = getenv("VIF_GRAD_RORDER");  // R rows in the Morton order (1-2% faster); 0: index order
       const int64_t* jorder = (!(jo_env && jo_env[0] == '0') && P.world == 1) ? h->ord(0) : nullptr;
       VIF_CUDA(h, launch_gR(reinterpret_cast<int*>(gbuf(G_CPTR)), reinterpret_cast<int*>(gbuf(G_CENT)), a.order,
-                            jorder, P.n, mk, P.mv, a.state, a.adj, a.rho, a.sig, R, s),
+                            jorder, P.n, mk, P.mv, a.state, a.adj, a.rho, a.sig, R,
+                            reinterpret_cast<unsigned long long*>(gbuf(G_TDK) + P.d + 1), s),
                "R");
       if (g == 0) VIF_CUDA(h, launch_la_transpose(Linv, mk, mk, mk, gbuf(G_LINVT), mk, s), "L_m^-T");
       VIF_CUDA(h, launch_gemm_tn(R, mk, P.n, gbuf(G_LINVT), mk, mk, mk, 0, gbuf(G_T), mk, 1.0, 0, s), "T = R L^-1");
