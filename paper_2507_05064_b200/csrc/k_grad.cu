@@ -954,17 +954,19 @@ __global__ void __launch_bounds__(1024) gchild_scan_kernel(const int* __restrict
   }
 }
 
-__global__ void gchild_sort_kernel(int64_t n, const int* __restrict__ ptr, int* __restrict__ ent) {
-  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
+// sort each children list (deterministic order): a warp per list, every element's rank = the number of
+// smaller entries (entries are distinct), elements scattered to their ranks through the second buffer
+__global__ void gchild_sort_kernel(int64_t n, const int* __restrict__ ptr, const int* __restrict__ ent_in,
+                                   int* __restrict__ ent_out) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t j = (int64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5); j < n;
+       j += (int64_t)gridDim.x * (blockDim.x / 32)) {
     const int a = ptr[j], b = ptr[j + 1];
-    for (int k = a + 1; k < b; ++k) {
-      const int v = ent[k];
-      int q = k - 1;
-      while (q >= a && ent[q] > v) {
-        ent[q + 1] = ent[q];
-        --q;
-      }
-      ent[q + 1] = v;
+    for (int k = a + lane; k < b; k += 32) {
+      const int v = ent_in[k];
+      int r = 0;
+      for (int q = a; q < b; ++q) r += ent_in[q] < v;
+      ent_out[a + r] = v;
     }
   }
 }
@@ -1253,9 +1255,10 @@ cudaError_t launch_gchild(const int32_t* nbr, int mv, const int64_t* order, int6
   const unsigned g1 = (unsigned)((npts + 255) / 256 > 4096 ? 4096 : (npts + 255) / 256 + 1);
   gchild_count_kernel<<<g1, 256, 0, s>>>(nbr, mv, order, npts, cnt);
   gchild_scan_kernel<<<1, 1024, 0, s>>>(cnt, n, ptr);
-  gchild_fill_kernel<<<g1, 256, 0, s>>>(nbr, mv, order, npts, ptr, cursor, ent);
-  const unsigned g2 = (unsigned)((n + 255) / 256 > 4096 ? 4096 : (n + 255) / 256 + 1);
-  gchild_sort_kernel<<<g2, 256, 0, s>>>(n, ptr, ent);
+  gchild_fill_kernel<<<g1, 256, 0, s>>>(nbr, mv, order, npts, ptr, cursor, ent + n * (int64_t)(mv + 1));
+  // fill into the scratch half, rank-sort into ent (the caller's ent has room for 2 n (m_v + 1) entries)
+  const unsigned g2 = (unsigned)((n + 7) / 8 > 148 * 16 ? 148 * 16 : (n + 7) / 8);
+  gchild_sort_kernel<<<g2, 256, 0, s>>>(n, ptr, ent + n * (int64_t)(mv + 1), ent);
   return cudaGetLastError();
 }
 

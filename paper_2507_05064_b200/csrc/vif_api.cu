@@ -400,7 +400,7 @@ Layout make_grad_layout(const Plan& P) {
   L.size[G_G2] = L.size[G_LINVT] = (size_t)mk1 * mk1 * D8;
   L.size[G_CCNT] = L.size[G_CCUR] = (size_t)P.n * sizeof(int);
   L.size[G_CPTR] = (size_t)(P.n + 1) * sizeof(int);
-  L.size[G_CENT] = (size_t)P.n * (P.mv + 1) * sizeof(int);
+  L.size[G_CENT] = (size_t)2 * P.n * (P.mv + 1) * sizeof(int);  // sorted entries + the unsorted fill
   L.size[G_TSP] = (size_t)la_ts_nsplit(P.n) * 64 * mk1 * D8;
   L.size[G_TDKP] = (size_t)gTdK_blocks() * (P.d + 1) * D8;
   L.size[G_TDK] = (size_t)(P.d + 2) * D8;  // + the R gather's row counter
