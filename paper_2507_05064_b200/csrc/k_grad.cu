@@ -1013,7 +1013,7 @@ __global__ void __launch_bounds__(256) gR_kernel(const int* __restrict__ ptr, co
 #pragma unroll
       for (int u = 0; u < CPL; ++u) {
         const int k = k0 + lane + 32 * u;
-        if (k < mk) R[j * (int64_t)mk + k] = acc[u];
+        if (k < mk) R[j * (int64_t)mk + (mk - 1 - k)] = acc[u];  // columns reversed (see launch_gR)
       }
     }
   }
@@ -1044,7 +1044,7 @@ __global__ void __launch_bounds__(256) gTdK_kernel(const double* __restrict__ X,
       if (k < dd) xr[k] = X[r * dd + k] * (fam_scale<FAM>() * p.inv_ls[k]);
     const double* trow = T + r * (int64_t)mk;
     for (int b = lane; b < m; b += 32) {
-      const double t_ = __ldg(trow + b);
+      const double t_ = __ldg(trow + (mk - 1 - b));  // T stored with reversed columns
       const double* z = zs + b * dd;
       double t2 = 0.0;
 #pragma unroll
@@ -1089,6 +1089,17 @@ __global__ void __launch_bounds__(256) gTdK_kernel(const double* __restrict__ X,
   }
 }
 
+// Bp[k'][c'] = Linv[mk-1-c'][mk-1-k']: with R's columns reversed, T = R L_m^{-1} becomes a product with a
+// lower-triangular right operand (T'[p][k'] = sum_{c' <= k'} R'[p][c'] Bp[k'][c'], T' = T with reversed
+// columns), so the triangular GEMM skips half the work
+__global__ void grev_linv_kernel(const double* __restrict__ Linv, int mk, double* __restrict__ Bp) {
+  const int64_t tot = (int64_t)mk * mk;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < tot; e += (int64_t)gridDim.x * blockDim.x) {
+    const int kp = (int)(e / mk), cp = (int)(e % mk);
+    Bp[e] = Linv[(int64_t)(mk - 1 - cp) * mk + (mk - 1 - kp)];
+  }
+}
+
 // out[q] = sum_blocks part[block][q]
 __global__ void gTdK_reduce_kernel(const double* __restrict__ part, int nblocks, int nq, double* __restrict__ out) {
   const int q = threadIdx.x;
@@ -1105,7 +1116,10 @@ __global__ void __launch_bounds__(1024) gfinal_kernel(double* __restrict__ out, 
   __shared__ double red[1024];
   double s = 0.0;
   const int64_t tot = (int64_t)mk * mk;
-  for (int64_t e = threadIdx.x; e < tot; e += blockDim.x) s = fma(G2[e], Phil[e], s);
+  for (int64_t e = threadIdx.x; e < tot; e += blockDim.x) {
+    const int64_t c = e / mk, k = e % mk;  // G2 stored with reversed rows (R's reversed columns)
+    s = fma(G2[(mk - 1 - c) * mk + k], Phil[e], s);
+  }
   red[threadIdx.x] = s;
   __syncthreads();
   for (int w = 512; w > 0; w >>= 1) {
@@ -1318,6 +1332,12 @@ cudaError_t launch_gTdK(const double* X, const double* Z, int64_t n, int m, int 
   }
   if (e != cudaSuccess) return e;
   gTdK_reduce_kernel<<<1, 32, 0, s>>>(part, blocks, p.d + 1, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_grev_linv(const double* Linv, int mk, double* Bp, cudaStream_t s) {
+  const int64_t tot = (int64_t)mk * mk;
+  grev_linv_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(Linv, mk, Bp);
   return cudaGetLastError();
 }
 

@@ -101,6 +101,7 @@ cudaError_t launch_gR(const int* ptr, const int* ent, const int64_t* order, cons
 int gTdK_blocks();
 cudaError_t launch_gTdK(const double* X, const double* Z, int64_t n, int m, int mk, const CovParams& p,
                         const double* T, double* part, double* out, cudaStream_t s);
+cudaError_t launch_grev_linv(const double* Linv, int mk, double* Bp, cudaStream_t s);
 cudaError_t launch_gfinal(double* out, const double* tdk, int q, const double* G2, const double* Phil, int mk,
                           cudaStream_t s);
 cudaError_t launch_la_tsgemm_ld(const double* U, int64_t ldu, int mk, int64_t n, const double* V, int64_t ldv,

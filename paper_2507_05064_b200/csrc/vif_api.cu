@@ -1319,8 +1319,9 @@ int vif_grad(void* handle, const vif_theta* theta, void* gws, size_t gws_bytes, 
                             jorder, P.n, mk, P.mv, a.state, a.adj, a.rho, a.sig, R,
                             reinterpret_cast<unsigned long long*>(gbuf(G_TDK) + P.d + 1), s),
                "R");
-      if (g == 0) VIF_CUDA(h, launch_la_transpose(Linv, mk, mk, mk, gbuf(G_LINVT), mk, s), "L_m^-T");
-      VIF_CUDA(h, launch_gemm_tn(R, mk, P.n, gbuf(G_LINVT), mk, mk, mk, 0, gbuf(G_T), mk, 1.0, 0, s), "T = R L^-1");
+      // R has reversed columns, so T = R L_m^{-1} is a triangular product (T with reversed columns)
+      if (g == 0) VIF_CUDA(h, launch_grev_linv(Linv, mk, gbuf(G_LINVT), s), "reversed L_m^-1");
+      VIF_CUDA(h, launch_gemm_tn(R, mk, P.n, gbuf(G_LINVT), mk, mk, mk, 1, gbuf(G_T), mk, 1.0, 0, s), "T = R L^-1");
       for (int c0 = 0; c0 < mk; c0 += 64)
         VIF_CUDA(h, launch_la_tsgemm_ld(U, ld, mk, P.n, R + c0, mk, std::min(64, mk - c0), gbuf(G_TSP),
                                         gbuf(G_G2) + (size_t)c0 * mk, s),
