@@ -278,20 +278,23 @@ cudaError_t launch_u_features(const double* X, const double* Z, const double* y,
     kern<<<nb, 256, zb, s>>>(X, Z, y, n, npos, chunk, world, rank, pos0, m, mk, p, S + pos0 * lds, lds, Uaug, ld);
     return cudaSuccess;
   };
+#define VIF_KX_D(DV)                                                      \
+  switch (p.family) {                                                     \
+    case FAM_M12: e0 = god(kx_eval_d_kernel<FAM_M12, DV>, DV); break;     \
+    case FAM_M32: e0 = god(kx_eval_d_kernel<FAM_M32, DV>, DV); break;     \
+    case FAM_M52: e0 = god(kx_eval_d_kernel<FAM_M52, DV>, DV); break;     \
+    default: e0 = god(kx_eval_d_kernel<FAM_GAUSS, DV>, DV); break;        \
+  }
+  // the benchmark configurations' dimensions (d = 2: configs 1-3; 3: config 5; 5: the Laplace
+  // workload; 10: config 4)
   if (!generic && p.d == 2) {
-    switch (p.family) {
-      case FAM_M12: e0 = god(kx_eval_d_kernel<FAM_M12, 2>, 2); break;
-      case FAM_M32: e0 = god(kx_eval_d_kernel<FAM_M32, 2>, 2); break;
-      case FAM_M52: e0 = god(kx_eval_d_kernel<FAM_M52, 2>, 2); break;
-      default: e0 = god(kx_eval_d_kernel<FAM_GAUSS, 2>, 2); break;
-    }
+    VIF_KX_D(2)
   } else if (!generic && p.d == 3) {
-    switch (p.family) {
-      case FAM_M12: e0 = god(kx_eval_d_kernel<FAM_M12, 3>, 3); break;
-      case FAM_M32: e0 = god(kx_eval_d_kernel<FAM_M32, 3>, 3); break;
-      case FAM_M52: e0 = god(kx_eval_d_kernel<FAM_M52, 3>, 3); break;
-      default: e0 = god(kx_eval_d_kernel<FAM_GAUSS, 3>, 3); break;
-    }
+    VIF_KX_D(3)
+  } else if (!generic && p.d == 5) {
+    VIF_KX_D(5)
+  } else if (!generic && p.d == 10) {
+    VIF_KX_D(10)
   } else {
     switch (p.family) {
       case FAM_M12: e0 = go(kx_eval_kernel<FAM_M12>); break;
@@ -300,6 +303,7 @@ cudaError_t launch_u_features(const double* X, const double* Z, const double* y,
       default: e0 = go(kx_eval_kernel<FAM_GAUSS>); break;
     }
   }
+#undef VIF_KX_D
   if (e0 != cudaSuccess) return e0;
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess || mk == 0) return e;

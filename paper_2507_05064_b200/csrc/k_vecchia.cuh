@@ -32,26 +32,32 @@ constexpr int VW = 4;  // warps per block
 __constant__ int g_vif_debug;
 
 template <int RB>
-__host__ __device__ constexpr int vecchia_warp_doubles() {
-  return RB * 8 * (RB * 8 + 1) + RB * 8;  // C (SP x (SP+1)) + coef (SP)
+__host__ __device__ constexpr int vecchia_warp_doubles(int d) {
+  // L (packed lower triangle) + coef (SP) + an 8 x 8 block inverse + the pre-scaled coordinates (SP x d)
+  return RB * 8 * (RB * 8 + 1) / 2 + RB * 8 + 64 + RB * 8 * d;
 }
 
 template <int FAM, int RB, int NB>
-__global__ void __launch_bounds__(VW * 32) vecchia_smem_kernel(
+__global__ void __launch_bounds__(VW * 32, 3) vecchia_smem_kernel(
     const double* __restrict__ U, int64_t ldu, int mk, int ld, const double* __restrict__ X,
     const double* __restrict__ Uq, const double* __restrict__ Xq, const int32_t* __restrict__ nbr, int mv, const int64_t* __restrict__ order, int64_t npts, CovParams p,
     double* __restrict__ W, int64_t ldw, double* __restrict__ Dpos, double* __restrict__ B_out,
     double* __restrict__ D_out, DevStatus* __restrict__ st) {
   constexpr int SP = RB * 8;
-  constexpr int CS = SP + 1;
   constexpr int NT = RB * (RB + 1) / 2;
   extern __shared__ __align__(16) double vsm[];
+  auto li = [](int r, int c) { return r * (r + 1) / 2 + c; };  // packed lower-triangle index
   __shared__ int Sidx_all[VW][SP];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  double* C = vsm + warp * vecchia_warp_doubles<RB>();
-  double* coef = C + SP * CS;
+  double* C = vsm + warp * vecchia_warp_doubles<RB>(p.d);
+  double* coef = C + SP * (SP + 1) / 2;
+  double* linv = coef + SP;
+  double* xs = linv + 64;
+  __shared__ double tbl[64];
   int* Sidx = Sidx_all[warp];
   const int64_t pos = (int64_t)blockIdx.x * VW + warp;
+  exp_table_init(tbl, p.sigma2, threadIdx.x);
+  __syncthreads();
   if (pos >= npts) return;
   const int64_t i = order[pos];
 
@@ -63,6 +69,10 @@ __global__ void __launch_bounds__(VW * 32) vecchia_smem_kernel(
   if (lane < SP) Sidx[lane] = lane < q ? nb0 : (lane == q ? (int)i : -1);
   if (lane + 32 < SP) Sidx[lane + 32] = lane + 32 < q ? nb1 : (lane + 32 == q ? (int)i : -1);
   __syncwarp();
+  // pre-scaled coordinates of S for cov_fast
+  for (int t = lane; t < s; t += 32)
+    for (int k = 0; k < p.d; ++k)
+      xs[t * p.d + k] = (t == q ? Xq : X)[(int64_t)Sidx[t] * p.d + k] * (fam_scale<FAM>() * p.inv_ls[k]);
 
   // ---- 1. Gram on DMMA ----
   double acc[NT][2];
@@ -108,56 +118,118 @@ __global__ void __launch_bounds__(VW * 32) vecchia_smem_kernel(
     }
   }
 
-  // ---- 2. residual covariance block into shared memory (lower part) ----
+  // ---- 2. residual covariance block C_S - U_S U_S^T + nugget I, kept in the DMMA fragment layout
+  //         (lane (g, t) of tile (R1, R2) holds rows R1*8+g, columns R2*8+2t, +1); padding rows and
+  //         columns are identity ----
+  const int g8 = lane >> 2, t4 = lane & 3;
   {
     int t = 0;
 #pragma unroll
     for (int R1 = 0; R1 < RB; ++R1)
 #pragma unroll
       for (int R2 = 0; R2 <= R1; ++R2, ++t) {
-        const int r = R1 * 8 + (lane >> 2);
+        const int r = R1 * 8 + g8;
 #pragma unroll
         for (int j = 0; j < 2; ++j) {
-          const int c = R2 * 8 + 2 * (lane & 3) + j;
-          if (c <= r) {
-            double v;
-            if (r < s) {
-              const int gr = Sidx[r], gc = Sidx[c];
-              v = cov<FAM>((r == q ? Xq : X) + (int64_t)gr * p.d, (c == q ? Xq : X) + (int64_t)gc * p.d, p) - acc[t][j];
-              if (r == c) v += p.nugget;
-            } else {
-              v = r == c ? 1.0 : 0.0;
-            }
-            C[r * CS + c] = v;
+          const int c = R2 * 8 + 2 * t4 + j;
+          double v = r == c ? 1.0 : 0.0;
+          if (c <= r && r < s) {
+            v = cov_fast<FAM>(xs + r * p.d, xs + c * p.d, p.d, tbl) - acc[t][j];
+            if (r == c) v += p.nugget;
           }
+          acc[t][j] = v;
         }
       }
   }
-  __syncwarp();
 
-  // ---- 3. Cholesky of C_S (i last) ----
+  // ---- 3. blocked right-looking Cholesky of C_S (i last), 8 x 8 blocks.  Block column J: the
+  //         diagonal block is factored (and inverted) redundantly by every lane from shared memory;
+  //         the panel L_RJ = C_RJ L_JJ^{-T} and the trailing update C_R1R2 -= L_R1J L_R2J^T are
+  //         DMMA products on the fragments (k-slot t <-> column 2t / 2t+1, so both operands are the
+  //         lane's own fragment entries).  L ends in C (packed lower triangle) for steps 4-5. ----
   bool ok = true;
   double Di = 0.0;
-  for (int j = 0; j < s; ++j) {
-    const double djj = C[j * CS + j];
-    if (!(djj > 0.0)) {
-      ok = false;
-      break;
+#pragma unroll
+  for (int J = 0; J < RB; ++J) {
+    const int tJJ = J * (J + 1) / 2 + J;
+    if (2 * t4 <= g8) C[li(J * 8 + g8, J * 8 + 2 * t4)] = acc[tJJ][0];
+    if (2 * t4 + 1 <= g8) C[li(J * 8 + g8, J * 8 + 2 * t4 + 1)] = acc[tJJ][1];
+    __syncwarp();
+    double Lb[8][8];
+#pragma unroll
+    for (int r = 0; r < 8; ++r)
+#pragma unroll
+      for (int c = 0; c <= r; ++c) Lb[r][c] = C[li(J * 8 + r, J * 8 + c)];
+    double inv[8];
+#pragma unroll
+    for (int jj = 0; jj < 8; ++jj) {
+      const double djj = Lb[jj][jj];
+      if (J * 8 + jj < s) ok = ok && (djj > 0.0);
+      if (J * 8 + jj == q) Di = djj;
+      const double y = rsqrt_nr(djj);
+      inv[jj] = y;
+      Lb[jj][jj] = djj * y;
+#pragma unroll
+      for (int r = jj + 1; r < 8; ++r) Lb[r][jj] *= y;
+#pragma unroll
+      for (int r = jj + 1; r < 8; ++r)
+#pragma unroll
+        for (int c = jj + 1; c <= r; ++c) Lb[r][c] = fma(-Lb[r][jj], Lb[c][jj], Lb[r][c]);
     }
-    Di = djj;
-    const double ljj = sqrt(djj);
-    __syncwarp();
-    for (int r = lane; r < s; r += 32)
-      if (r > j) C[r * CS + j] /= ljj;
-    if (lane == 0) C[j * CS + j] = ljj;
-    __syncwarp();
-    for (int r = lane; r < s; r += 32)
-      if (r > j) {
-        const double lrj = C[r * CS + j];
-        for (int c = j + 1; c <= r; ++c) C[r * CS + c] -= lrj * C[c * CS + j];
+    __syncwarp();  // every lane has read the block
+#pragma unroll
+    for (int r = 0; r < 8; ++r)
+#pragma unroll
+      for (int c = 0; c <= r; ++c) C[li(J * 8 + r, J * 8 + c)] = Lb[r][c];  // same value from every lane
+    if (J + 1 < RB) {
+      // column jj of L_JJ^{-1} by forward substitution, into linv (same value from every lane)
+#pragma unroll
+      for (int jj = 0; jj < 8; ++jj) {
+        double col[8];
+        col[jj] = inv[jj];
+#pragma unroll
+        for (int r = jj + 1; r < 8; ++r) {
+          double sm = 0.0;
+#pragma unroll
+          for (int k = jj; k < r; ++k) sm = fma(Lb[r][k], col[k], sm);
+          col[r] = -sm * inv[r];
+        }
+#pragma unroll
+        for (int r = jj; r < 8; ++r) linv[r * 8 + jj] = col[r];
       }
-    __syncwarp();
+      __syncwarp();
+      const double li0 = 2 * t4 <= g8 ? linv[g8 * 8 + 2 * t4] : 0.0;
+      const double li1 = 2 * t4 + 1 <= g8 ? linv[g8 * 8 + 2 * t4 + 1] : 0.0;
+#pragma unroll
+      for (int R = J + 1; R < RB; ++R) {
+        const int tRJ = R * (R + 1) / 2 + J;
+        double n0 = 0.0, n1 = 0.0;
+        dmma884(n0, n1, acc[tRJ][0], li0);
+        dmma884(n0, n1, acc[tRJ][1], li1);
+        acc[tRJ][0] = n0;
+        acc[tRJ][1] = n1;
+      }
+#pragma unroll
+      for (int R1 = J + 1; R1 < RB; ++R1)
+#pragma unroll
+        for (int R2 = J + 1; R2 <= R1; ++R2) {
+          const int t12 = R1 * (R1 + 1) / 2 + R2, t1 = R1 * (R1 + 1) / 2 + J, t2 = R2 * (R2 + 1) / 2 + J;
+          dmma884(acc[t12][0], acc[t12][1], -acc[t1][0], acc[t2][0]);
+          dmma884(acc[t12][0], acc[t12][1], -acc[t1][1], acc[t2][1]);
+        }
+      __syncwarp();  // linv is rewritten by the next block column
+    }
   }
+  // the panels of L into C (the diagonal blocks are there already)
+#pragma unroll
+  for (int R = 1; R < RB; ++R)
+#pragma unroll
+    for (int J = 0; J < R; ++J) {
+      const int tRJ = R * (R + 1) / 2 + J;
+      C[li(R * 8 + g8, J * 8 + 2 * t4)] = acc[tRJ][0];
+      C[li(R * 8 + g8, J * 8 + 2 * t4 + 1)] = acc[tRJ][1];
+    }
+  __syncwarp();
   if (!ok) {
     if (lane == 0) atomicMin(&st->bad_row, (unsigned long long)i);
     for (int c = 2 * lane; c < ld; c += 64) *reinterpret_cast<double2*>(W + pos * ldw + c) = make_double2(0.0, 0.0);
@@ -168,52 +240,62 @@ __global__ void __launch_bounds__(VW * 32) vecchia_smem_kernel(
     return;
   }
 
-  // ---- 4. A_i^T = L_NN^{-T} l,  l = row s-1 of L ----
+  // ---- 4. A_i^T = L_NN^{-T} l, l = row q of L; lane k holds x_k and x_{k+32} (branch-free shuffles) ----
   {
-    double a0 = lane < q ? C[q * CS + lane] : 0.0;
-    double a1 = lane + 32 < q ? C[q * CS + lane + 32] : 0.0;
+    const double inv0 = lane < s ? 1.0 / C[li(lane, lane)] : 0.0;
+    const double inv1 = lane + 32 < s ? 1.0 / C[li(lane + 32, lane + 32)] : 0.0;
+    double a0 = lane < q ? C[li(q, lane)] : 0.0;
+    double a1 = lane + 32 < q ? C[li(q, lane + 32)] : 0.0;
     for (int j = q - 1; j >= 0; --j) {
-      if (lane == (j & 31)) {
-        const double x = (j < 32 ? a0 : a1) / C[j * CS + j];
-        coef[j] = x;
-      }
-      __syncwarp();
-      const double xj = coef[j];
-      if (lane < j) a0 -= C[j * CS + lane] * xj;
-      if (lane + 32 < j) a1 -= C[j * CS + lane + 32] * xj;
+      const double* Lj = C + li(j, 0);  // (reads past column j stay inside the triangle: j < SP - 1)
+      const double xj = __shfl_sync(0xffffffffu, j < 32 ? a0 * inv0 : a1 * inv1, j & 31);
+      const double l0 = Lj[lane], l1 = Lj[(lane + 32) < SP ? lane + 32 : lane];
+      a0 = lane == j ? xj : (lane < j ? fma(-l0, xj, a0) : a0);
+      a1 = lane + 32 == j ? xj : (lane + 32 < j ? fma(-l1, xj, a1) : a1);
     }
-    __syncwarp();
+    const double rs = rsqrt_nr(Di);
+    // coefficients of the W row: -A_ik / sqrt(D) for k < q, 1 / sqrt(D) for i itself, 0 beyond
+    if (lane < SP) coef[lane] = lane < q ? -a0 * rs : (lane == q ? rs : 0.0);
+    if (lane + 32 < SP) coef[lane + 32] = lane + 32 < q ? -a1 * rs : (lane + 32 == q ? rs : 0.0);
+    if (B_out) {
+      if (lane < mv) B_out[i * mv + lane] = lane < q ? -a0 : 0.0;
+      if (lane + 32 < mv) B_out[i * mv + lane + 32] = lane + 32 < q ? -a1 : 0.0;
+    }
   }
+  __syncwarp();
 
-  // ---- 5. w_i, r_i:  (u_i - sum_k A_ik u_{N_k}) / sqrt(D_i) over ld columns ----
-  const double rs = 1.0 / sqrt(Di);
-  const double* ui = Uq + i * ldu;
-  for (int c = 2 * lane; c < ld; c += 64) {
-    double2 o = __ldg(reinterpret_cast<const double2*>(ui + c));
-    int k = 0;
-    for (; k + 4 <= q; k += 4) {
-      double2 u[4];
+  // ---- 5. w_i, r_i over ld columns: 512 columns per pass (8 chunks of 64 per lane-pair), rows two
+  //         at a time -> 16 independent 16-byte loads in flight per lane ----
+  for (int c0 = 0; c0 < ld; c0 += 512) {
+    double2 o[8];
 #pragma unroll
-      for (int t = 0; t < 4; ++t) u[t] = __ldg(reinterpret_cast<const double2*>(U + (int64_t)Sidx[k + t] * ldu + c));
+    for (int t = 0; t < 8; ++t) o[t] = make_double2(0.0, 0.0);
+    for (int k = 0; k < s; k += 2) {
+      double2 u0[8], u1[8];
+      const double* r0 = (k == q ? Uq : U) + (int64_t)Sidx[k] * ldu + c0 + 2 * lane;
+      const bool has1 = k + 1 < s;
+      const double* r1 = has1 ? (k + 1 == q ? Uq : U) + (int64_t)Sidx[k + 1] * ldu + c0 + 2 * lane : r0;
 #pragma unroll
-      for (int t = 0; t < 4; ++t) {
-        const double x = coef[k + t];
-        o.x = fma(-x, u[t].x, o.x);
-        o.y = fma(-x, u[t].y, o.y);
+      for (int t = 0; t < 8; ++t) {
+        const bool in = c0 + 2 * lane + 64 * t < ld;
+        u0[t] = in ? __ldg(reinterpret_cast<const double2*>(r0 + 64 * t)) : make_double2(0.0, 0.0);
+        u1[t] = (in && has1) ? __ldg(reinterpret_cast<const double2*>(r1 + 64 * t)) : make_double2(0.0, 0.0);
+      }
+      const double f0 = coef[k], f1 = has1 ? coef[k + 1] : 0.0;
+#pragma unroll
+      for (int t = 0; t < 8; ++t) {
+        o[t].x = fma(f0, u0[t].x, o[t].x);
+        o[t].y = fma(f0, u0[t].y, o[t].y);
+        o[t].x = fma(f1, u1[t].x, o[t].x);
+        o[t].y = fma(f1, u1[t].y, o[t].y);
       }
     }
-    for (; k < q; ++k) {
-      const double2 u = __ldg(reinterpret_cast<const double2*>(U + (int64_t)Sidx[k] * ldu + c));
-      const double x = coef[k];
-      o.x = fma(-x, u.x, o.x);
-      o.y = fma(-x, u.y, o.y);
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      const int c = c0 + 2 * lane + 64 * t;
+      if (c < ld) *reinterpret_cast<double2*>(W + pos * ldw + c) = o[t];
     }
-    o.x *= rs;
-    o.y *= rs;
-    *reinterpret_cast<double2*>(W + pos * ldw + c) = o;
   }
-  if (B_out)
-    for (int k = lane; k < mv; k += 32) B_out[i * mv + k] = k < q ? -coef[k] : 0.0;
   if (lane == 0) {
     Dpos[pos] = Di;
     if (D_out) D_out[i] = Di;
@@ -507,7 +589,6 @@ __global__ void __launch_bounds__(VW * 32, MINB) vecchia_reg_kernel(
 
 template <int FAM, int RB>
 static cudaError_t launch_rb(const VecchiaArgs& a, cudaStream_t s) {
-  constexpr int NB = RB <= 4 ? 2 : 1;
   const unsigned blocks = (unsigned)((a.npts + VW - 1) / VW);
   // s <= 32: the per-warp register kernel.  Measured and rejected on B200 (profiles/r01_notes.md):
   // warp-specialised Gram / solver warps (register ring or cp.async shared-memory ring) and a
@@ -522,11 +603,10 @@ static cudaError_t launch_rb(const VecchiaArgs& a, cudaStream_t s) {
       kern = vecchia_reg_kernel<FAM, RB, 3, 4, true>;
     } else {
       static const char* gen_env = getenv("VIF_VECCHIA_GENERIC_D");
-      const bool d2 = a.p.d == 2 && !(gen_env && gen_env[0] == '1');
-      switch (cfg) {
-        case 24: kern = vecchia_reg_kernel<FAM, RB, 2, 4>; break;
-        default: kern = d2 ? vecchia_reg_kernel<FAM, RB, 3, 4, false, 2> : vecchia_reg_kernel<FAM, RB, 3, 4>; break;
-      }
+      const int dd = (gen_env && gen_env[0] == '1') ? 0 : a.p.d;
+      if (cfg == 24) kern = vecchia_reg_kernel<FAM, RB, 2, 4>;
+      else if (dd == 2) kern = vecchia_reg_kernel<FAM, RB, 3, 4, false, 2>;
+      else kern = vecchia_reg_kernel<FAM, RB, 3, 4>;
     }
     if (smem > 40 * 1024) {  // static shared memory comes on top
       cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -545,15 +625,16 @@ static cudaError_t launch_rb(const VecchiaArgs& a, cudaStream_t s) {
     kern<<<blocks, VW * 32, smem, s>>>(a.U, a.ldu, a.mk, a.ld, a.X, a.Uself ? a.Uself : a.U, a.Xself ? a.Xself : a.X,
                                        a.nbr, a.mv, a.order, a.npts, a.p, a.W, a.ldw, a.Dpos, a.B_out, a.D_out, a.st);
   } else {
-    const size_t smem = (size_t)VW * vecchia_warp_doubles<RB>() * sizeof(double);
-    static bool attr = false;
-    if (!attr) {
-      cudaError_t e = cudaFuncSetAttribute(vecchia_smem_kernel<FAM, RB, NB>,
-                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const size_t smem = (size_t)VW * vecchia_warp_doubles<RB>(a.p.d) * sizeof(double);
+    static const char* nb_env = getenv("VIF_SMEM_NB");  // A/B hook: Gram ring depth 1 or 2
+    auto kern = (nb_env && nb_env[0] == '2') ? vecchia_smem_kernel<FAM, RB, 2> : vecchia_smem_kernel<FAM, RB, 1>;
+    static size_t attr = 0;
+    if (attr < smem) {
+      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       if (e != cudaSuccess) return e;
-      attr = true;
+      attr = smem;
     }
-    vecchia_smem_kernel<FAM, RB, NB><<<blocks, VW * 32, smem, s>>>(a.U, a.ldu, a.mk, a.ld, a.X, a.Uself ? a.Uself : a.U,
+    kern<<<blocks, VW * 32, smem, s>>>(a.U, a.ldu, a.mk, a.ld, a.X, a.Uself ? a.Uself : a.U,
                                                                    a.Xself ? a.Xself : a.X, a.nbr, a.mv,
                                                                    a.order, a.npts, a.p, a.W, a.ldw, a.Dpos,
                                                                    a.B_out, a.D_out, a.st);

@@ -82,6 +82,7 @@ def test_config1_full_parity():
     (2500, 64, 31, "matern52", 3),     # RB = 4 (s = 32), m multiple of 64
     (1777, 130, 20, "matern12", 2),    # RB = 3, several GEMM col tiles + ragged
     (1200, 16, 40, "gaussian", 4),     # RB = 6 (s = 41)
+    (1100, 25, 36, "matern12", 3),     # RB = 5 (s = 37)
     (900, 9, 47, "matern32", 1),       # max m_v, d = 1
     (2049, 200, 15, "matern52", 5),    # several 64-col SYRK tiles
 ])
@@ -172,10 +173,12 @@ def test_invalid_neighbors_rejected():
     assert e.value.status == 1 and "row 100" in e.value.msg
 
 
-def test_not_pd_reports_row():
+@pytest.mark.parametrize("width", [2, 35])  # register kernel / blocked shared-memory kernel (m_v > 31)
+def test_not_pd_reports_row(width):
     p = vif()
     X = np.array([[0.1, 0.1], [0.5, 0.5], [0.5, 0.5], [0.7, 0.2]])
-    nbr = np.array([[-1, -1], [0, -1], [1, 0], [2, 1]], np.int32)
+    nbr = np.full((4, width), -1, np.int32)
+    nbr[:, :2] = [[-1, -1], [0, -1], [1, 0], [2, 1]]
     dev = torch.device("cuda")
     model = p.VifModel(torch.from_numpy(X).to(dev), torch.zeros((0, 2), dtype=torch.float64, device=dev),
                        torch.from_numpy(nbr).to(dev), torch.zeros(4, dtype=torch.float64, device=dev))
