@@ -154,13 +154,130 @@ __global__ void morton_kernel(const double* __restrict__ X, int64_t n, int d, in
   }
 }
 
+// ---- d > 3: Morton code over the K = min(d, 8) input dimensions along which the given
+// neighbour sets are tightest (ranked by r_k = E[(x_ik - x_{N(i)_1,k})^2] / Var(x_k), the
+// neighbours' spread relative to the data's), each scaled by its neighbour spread delta_k so that
+// the Morton cells follow the shape of the neighbourhoods.  No hyperparameter enters: the
+// neighbour sets carry the (ARD) correlation geometry.  Only the processing order changes (it is a
+// permutation of independent rows), so the results do not depend on it beyond summation order. ----
+constexpr int OD_MAX = 8;
+
+__global__ void nbr_spread_kernel(const double* __restrict__ X, int64_t n, int d, const int32_t* __restrict__ nbr,
+                                  int mv, double* __restrict__ acc) {
+  __shared__ double red[3 * VIF_MAX_D];
+  for (int t = threadIdx.x; t < 3 * VIF_MAX_D; t += blockDim.x) red[t] = 0.0;
+  __syncthreads();
+  double a[3 * VIF_MAX_D];
+#pragma unroll
+  for (int t = 0; t < 3 * VIF_MAX_D; ++t) a[t] = 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int j = nbr[i * mv];
+#pragma unroll
+    for (int k = 0; k < VIF_MAX_D; ++k)
+      if (k < d) {
+        const double x = X[i * d + k];
+        a[3 * k + 1] += x;
+        a[3 * k + 2] = fma(x, x, a[3 * k + 2]);
+        if (j >= 0) {
+          const double df = x - X[(int64_t)j * d + k];
+          a[3 * k] = fma(df, df, a[3 * k]);
+        }
+      }
+  }
+#pragma unroll
+  for (int t = 0; t < 3 * VIF_MAX_D; ++t)
+    if (t < 3 * d) {
+      double v = a[t];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      if ((threadIdx.x & 31) == 0) atomicAdd(&red[t], v);
+    }
+  __syncthreads();
+  for (int t = threadIdx.x; t < 3 * d; t += blockDim.x) atomicAdd(&acc[t], red[t]);
+}
+
+// prm: [0..K) selected dims, [8..8+K) lo, [16..16+K) scale (to 48/K-bit cells), [24] = K (K <= 8)
+__global__ void order_dims_kernel(const double* __restrict__ acc, int64_t n, int d, int kmax,
+                                  double* __restrict__ prm) {
+  if (threadIdx.x != 0) return;
+  double r[VIF_MAX_D], sd[VIF_MAX_D], mu[VIF_MAX_D];
+  bool used[VIF_MAX_D];
+  for (int k = 0; k < d; ++k) {
+    mu[k] = acc[3 * k + 1] / (double)n;
+    const double var = fmax(acc[3 * k + 2] / (double)n - mu[k] * mu[k], 1e-300);
+    sd[k] = sqrt(var);
+    r[k] = acc[3 * k] / var;
+    used[k] = false;
+  }
+  const int K = d < kmax ? d : kmax;
+  const int bits = 48 / K;
+  double width = 0.0;  // widest selected dimension in units of its neighbour spread
+  int sel[OD_MAX];
+  double dl[OD_MAX];
+  for (int t = 0; t < K; ++t) {
+    int best = -1;
+    for (int k = 0; k < d; ++k)
+      if (!used[k] && (best < 0 || r[k] < r[best])) best = k;
+    used[best] = true;
+    sel[t] = best;
+    dl[t] = sqrt(acc[3 * best] / (double)n);
+    if (!(dl[t] > 0.0)) dl[t] = sd[best] > 0.0 ? sd[best] : 1.0;
+    width = fmax(width, 16.0 * sd[best] / dl[t]);
+  }
+  for (int t = 0; t < K; ++t) {
+    prm[t] = (double)sel[t];
+    prm[8 + t] = mu[sel[t]] - 8.0 * sd[sel[t]];
+    prm[16 + t] = (double)((1ULL << bits) - 1) / (width * dl[t]);
+  }
+  prm[24] = (double)K;
+}
+
+__global__ void morton_nd_kernel(const double* __restrict__ X, int64_t n, int d, int64_t npos, int64_t chunk,
+                                 int world, int rank, const double* __restrict__ prm, uint64_t* __restrict__ keys,
+                                 int64_t* __restrict__ vals) {
+  const int K = (int)prm[24];
+  const int bits = 48 / K;
+  const double cmax = (double)((1ULL << bits) - 1);
+  for (int64_t pos = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; pos < npos;
+       pos += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = (pos / chunk) * (int64_t)world * chunk + (int64_t)rank * chunk + pos % chunk;
+    uint64_t key = ~0ULL;
+    if (i < n) {
+      uint64_t c[OD_MAX];
+      for (int t = 0; t < K; ++t) {
+        const double v = (X[i * d + (int)prm[t]] - prm[8 + t]) * prm[16 + t];
+        c[t] = (uint64_t)fmin(fmax(v, 0.0), cmax);
+      }
+      uint64_t m = 0;
+      for (int b = bits - 1; b >= 0; --b)
+        for (int t = 0; t < K; ++t) m = (m << 1) | ((c[t] >> b) & 1ULL);
+      key = ((uint64_t)(pos / chunk) << 48) | (m & 0xffffffffffffULL);
+    }
+    keys[pos] = key;
+    vals[pos] = i;
+  }
+}
+
 size_t order_temp_bytes(int64_t npos) { return (size_t)(16u << 20) + (size_t)npos * 4; }
 
 cudaError_t launch_order(const double* X, int64_t n, int d, int64_t npos, int64_t chunk, int world, int rank,
                          double* bbox, uint64_t* keys, uint64_t* keys_alt, int64_t* vals, int64_t* vals_alt,
-                         void* temp, size_t temp_bytes, int64_t** order_out, cudaStream_t s) {
-  bbox_partial_kernel<<<BB_BLOCKS, 256, 0, s>>>(X, n, d, bbox);
-  morton_kernel<<<296, 256, 0, s>>>(X, n, d, npos, chunk, world, rank, bbox, keys, vals);
+                         void* temp, size_t temp_bytes, int64_t** order_out, cudaStream_t s, const int32_t* nbr,
+                         int mv) {
+  static const char* nd_env = getenv("VIF_ORDER_ND");  // 0: the first three coordinates for every d
+  const bool nd = d > 3 && nbr != nullptr && mv > 0 && n > 1 && !(nd_env && nd_env[0] == '0');
+  if (nd) {
+    cudaError_t e = cudaMemsetAsync(bbox, 0, 3 * VIF_MAX_D * sizeof(double), s);
+    if (e != cudaSuccess) return e;
+    nbr_spread_kernel<<<296, 256, 0, s>>>(X, n, d, nbr, mv, bbox);
+    static const char* k_env = getenv("VIF_ORDER_K");  // A/B hook: dimensions in the code (1..8), default 8
+    const int kmax = k_env ? (atoi(k_env) < 1 ? 1 : (atoi(k_env) > OD_MAX ? OD_MAX : atoi(k_env))) : OD_MAX;
+    order_dims_kernel<<<1, 32, 0, s>>>(bbox, n, d, kmax, bbox + 64);
+    morton_nd_kernel<<<296, 256, 0, s>>>(X, n, d, npos, chunk, world, rank, bbox + 64, keys, vals);
+  } else {
+    bbox_partial_kernel<<<BB_BLOCKS, 256, 0, s>>>(X, n, d, bbox);
+    morton_kernel<<<296, 256, 0, s>>>(X, n, d, npos, chunk, world, rank, bbox, keys, vals);
+  }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   cub::DoubleBuffer<uint64_t> dk(keys, keys_alt);

@@ -195,7 +195,8 @@ cudaError_t launch_validate(const double* X, int64_t n, int d, const double* Z, 
 size_t order_temp_bytes(int64_t npos);
 cudaError_t launch_order(const double* X, int64_t n, int d, int64_t npos, int64_t chunk, int world, int rank,
                          double* bbox, uint64_t* keys, uint64_t* keys_alt, int64_t* vals, int64_t* vals_alt,
-                         void* temp, size_t temp_bytes, int64_t** order_out, cudaStream_t s);
+                         void* temp, size_t temp_bytes, int64_t** order_out, cudaStream_t s,
+                         const int32_t* nbr = nullptr, int mv = 0);
 cudaError_t launch_sum_buffers(const double* src, int64_t count, int nbuf, int64_t stride, double* dst,
                                cudaStream_t s);
 cudaError_t launch_reset_status(DevStatus* st, cudaStream_t s);

@@ -313,7 +313,7 @@ int compute_orders(Handle* h, int sl, cudaStream_t strm, bool staging = false) {
                              h->buf<double>(staging ? B_SBBOX : B_BBOX), h->buf<uint64_t>(staging ? B_SKEYS : B_KEYS),
                              h->buf<uint64_t>(staging ? B_SKEYS2 : B_KEYS2), h->buf<int64_t>(staging ? B_SVALS : B_VALS),
                              h->buf<int64_t>(staging ? B_SVALS2 : B_VALS2), h->buf<void>(staging ? B_STEMP : B_TEMP),
-                             h->L.size[B_TEMP], &sorted, strm),
+                             h->L.size[B_TEMP], &sorted, strm, h->buf_slot<int32_t>(B_NBR, sl), P.mv),
              "order");
     int64_t* dst = h->buf_slot<int64_t>(B_ORDER, sl) + (size_t)g * P.npos;
     VIF_CUDA(h, cudaMemcpyAsync(dst, sorted, P.npos * sizeof(int64_t), cudaMemcpyDeviceToDevice, strm), "order copy");
