@@ -126,9 +126,10 @@ def test_n1_scalar():
         assert_parity(w, want_U=m > 0)
 
 
-@pytest.mark.parametrize("world", [2, 3, 4])
-def test_emulated_sharding_matches_single(world):
-    w = small(5003, 48, 10, seed=11)
+@pytest.mark.parametrize("world,d", [(2, 2), (3, 2), (4, 2), (3, 6)])
+def test_emulated_sharding_matches_single(world, d):
+    """d = 6 takes the neighbour-driven processing order (d > 3) on every emulated rank."""
+    w = small(5003, 48, 10, seed=11, d=d, ard=(0.3, 3.0) if d > 3 else None)
     t1, B1, D1, _, _ = run_gpu(w, world=1)
     tg, Bg, Dg, _, _ = run_gpu(w, world=world)
     assert tg.nll == pytest.approx(t1.nll, rel=1e-12)
