@@ -182,7 +182,7 @@ __host__ __device__ constexpr int param_warp_doubles(int d) {
 // 1/L_jj, g_i . U_aug[S_k], D_i, ok
 template <int RB>
 __host__ __device__ constexpr int state_doubles() {
-  return (RB * 8) * (RB * 8 + 1) / 2 + 3 * (RB * 8) + 2;
+  return vif_state_doubles<RB>();
 }
 
 // per-warp setup shared by both passes: S, its (unscaled) coordinates, row pointers
@@ -1174,6 +1174,64 @@ cudaError_t launch_grad_any(const GradPointArgs& a, bool state_pass, cudaStream_
 }
 
 }  // namespace
+
+// g_i . U_aug[S_k] (k < s) into a state whose L, A_i, 1/L_jj, D_i the factor wrote: warp per point,
+// lane (g, t) reads columns 2t, 2t+1 of row R*8+g of every 8-column step (as grad_state_kernel)
+template <int RB>
+__global__ void __launch_bounds__(GW * 32) grad_gam_kernel(const double* __restrict__ U, const double* __restrict__ Gam,
+                                                          int64_t ldu, int ld, const int32_t* __restrict__ nbr,
+                                                          int mv, const int64_t* __restrict__ order, int64_t npts,
+                                                          double* __restrict__ state) {
+  constexpr int SP = RB * 8;
+  constexpr int LP = SP * (SP + 1) / 2;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t pos = (int64_t)blockIdx.x * GW + warp;
+  if (pos >= npts) return;
+  const int64_t i = order[pos];
+  const int nb0 = lane < mv ? nbr[i * mv + lane] : -1;
+  const int q = __popc(__ballot_sync(0xffffffffu, nb0 >= 0));
+  const double* rp[RB];
+#pragma unroll
+  for (int R = 0; R < RB; ++R) {
+    const int row = R * 8 + (lane >> 2);
+    const int gi = __shfl_sync(0xffffffffu, nb0, row & 31);
+    const int64_t idx = row < q ? gi : (row == q ? i : -1);
+    rp[R] = idx >= 0 ? U + idx * ldu + 2 * (lane & 3) : nullptr;
+  }
+  const double* grow = Gam + pos * (int64_t)ld + 2 * (lane & 3);
+  double gm[RB];
+#pragma unroll
+  for (int R = 0; R < RB; ++R) gm[R] = 0.0;
+#pragma unroll 4
+  for (int k0 = 0; k0 < ld; k0 += 8) {
+    const double2 g2 = __ldg(reinterpret_cast<const double2*>(grow + k0));
+#pragma unroll
+    for (int R = 0; R < RB; ++R) {
+      const double2 f = rp[R] ? __ldg(reinterpret_cast<const double2*>(rp[R] + k0)) : make_double2(0.0, 0.0);
+      gm[R] = fma(f.x, g2.x, fma(f.y, g2.y, gm[R]));
+    }
+  }
+  double* st = state + pos * (int64_t)vif_state_doubles<RB>();
+#pragma unroll
+  for (int R = 0; R < RB; ++R) {
+    gm[R] += __shfl_xor_sync(0xffffffffu, gm[R], 1);
+    gm[R] += __shfl_xor_sync(0xffffffffu, gm[R], 2);
+    if ((lane & 3) == 0) st[LP + 2 * SP + R * 8 + (lane >> 2)] = gm[R];
+  }
+}
+
+cudaError_t launch_grad_gam(const GradPointArgs& a, cudaStream_t s) {
+  if (a.npts <= 0) return cudaSuccess;
+  const unsigned blocks = (unsigned)((a.npts + GW - 1) / GW);
+  switch ((a.mv + 1 + 7) / 8) {
+    case 1: grad_gam_kernel<1><<<blocks, GW * 32, 0, s>>>(a.U, a.Gam, a.ldu, a.ld, a.nbr, a.mv, a.order, a.npts, a.state); break;
+    case 2: grad_gam_kernel<2><<<blocks, GW * 32, 0, s>>>(a.U, a.Gam, a.ldu, a.ld, a.nbr, a.mv, a.order, a.npts, a.state); break;
+    case 3: grad_gam_kernel<3><<<blocks, GW * 32, 0, s>>>(a.U, a.Gam, a.ldu, a.ld, a.nbr, a.mv, a.order, a.npts, a.state); break;
+    case 4: grad_gam_kernel<4><<<blocks, GW * 32, 0, s>>>(a.U, a.Gam, a.ldu, a.ld, a.nbr, a.mv, a.order, a.npts, a.state); break;
+    default: return cudaErrorInvalidValue;  // m_v > 31: the state pass computes everything
+  }
+  return cudaGetLastError();
+}
 
 int64_t grad_point_nparts(int64_t npts) { return (npts + GW - 1) / GW; }
 

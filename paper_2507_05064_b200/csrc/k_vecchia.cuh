@@ -417,7 +417,7 @@ __global__ void __launch_bounds__(VW * 32, MINB) vecchia_reg_kernel(
     const double* __restrict__ U, int64_t ldu, int mk, int ld, const double* __restrict__ X,
     const double* __restrict__ Uq, const double* __restrict__ Xq, const int32_t* __restrict__ nbr, int mv, const int64_t* __restrict__ order, int64_t npts, CovParams p,
     double* __restrict__ W, int64_t ldw, double* __restrict__ Dpos, double* __restrict__ B_out,
-    double* __restrict__ D_out, DevStatus* __restrict__ st) {
+    double* __restrict__ D_out, DevStatus* __restrict__ st, double* __restrict__ gstate) {
   constexpr int SP = RB * 8;
   constexpr int CS = SP + 1;
   constexpr int NT = RB * (RB + 1) / 2;
@@ -546,6 +546,24 @@ __global__ void __launch_bounds__(VW * 32, MINB) vecchia_reg_kernel(
     // coefficients of the W row: -A_ik / sqrt(D) for k < q, 1 / sqrt(D) for i itself, 0 beyond
     if (lane < SP) coef[lane] = lane < q ? -a * rs : (lane == q ? rs : 0.0);
     if (B_out && lane < mv) B_out[i * mv + lane] = lane < q ? -a : 0.0;
+    if (gstate) {  // vif_grad: L (packed, identity padding rows), A_i, 1/L_jj, D_i for its first pass
+      constexpr int LP = SP * (SP + 1) / 2;
+      double* sp = gstate + pos * (int64_t)vif_state_doubles<RB>();
+      for (int e = lane; e < LP; e += 32) {
+        int r = (int)((sqrtf_fast(8.0f * (float)e + 1.0f) - 1.0f) * 0.5f);
+        if ((r + 1) * (r + 2) / 2 <= e) ++r;
+        if (r * (r + 1) / 2 > e) --r;
+        sp[e] = C[r * CS + e - r * (r + 1) / 2];
+      }
+      if (lane < SP) {
+        sp[LP + lane] = lane < q ? a : 0.0;
+        sp[LP + SP + lane] = inv_diag;
+      }
+      if (lane == 0) {
+        sp[LP + 3 * SP] = Di;
+        sp[LP + 3 * SP + 1] = 1.0;
+      }
+    }
   }
   __syncwarp();
 
@@ -623,7 +641,8 @@ static cudaError_t launch_rb(const VecchiaArgs& a, cudaStream_t s) {
       }
     }
     kern<<<blocks, VW * 32, smem, s>>>(a.U, a.ldu, a.mk, a.ld, a.X, a.Uself ? a.Uself : a.U, a.Xself ? a.Xself : a.X,
-                                       a.nbr, a.mv, a.order, a.npts, a.p, a.W, a.ldw, a.Dpos, a.B_out, a.D_out, a.st);
+                                       a.nbr, a.mv, a.order, a.npts, a.p, a.W, a.ldw, a.Dpos, a.B_out, a.D_out, a.st,
+                                       a.state);
   } else {
     const size_t smem = (size_t)VW * vecchia_warp_doubles<RB>(a.p.d) * sizeof(double);
     static const char* nb_env = getenv("VIF_SMEM_NB");  // A/B hook: Gram ring depth 1 or 2

@@ -28,7 +28,17 @@ struct VecchiaArgs {
   // prediction points whose neighbours are training rows of U / X); NULL = U / X
   const double* Uself = nullptr;
   const double* Xself = nullptr;
+  // gradient (vif_grad, m_v <= 31): the factor's rows also write the per-point state of the gradient's
+  // first pass (vif_state_doubles layout, by position; the g_i dots are left to launch_grad_gam)
+  double* state = nullptr;
 };
+
+// per-point gradient state, by position: L (packed lower, SP = 8 RB rows incl. the identity padding),
+// A_i, 1/L_jj, g_i . U_aug[S_k], D_i, ok
+template <int RB>
+__host__ __device__ constexpr int vif_state_doubles() {
+  return (RB * 8) * (RB * 8 + 1) / 2 + 3 * (RB * 8) + 2;
+}
 
 // K0 / K5
 cudaError_t launch_build_km(const double* Z, int m, const CovParams& p, double* Km, cudaStream_t s);
@@ -87,6 +97,8 @@ struct GradPointArgs {
 };
 int64_t grad_point_nparts(int64_t npts);
 size_t grad_state_doubles(int mv);
+// the g_i . U_aug[S_k] slots of a state written by the factor (VecchiaArgs::state)
+cudaError_t launch_grad_gam(const GradPointArgs& a, cudaStream_t s);
 cudaError_t launch_grad_state(const GradPointArgs& a, cudaStream_t s);
 cudaError_t launch_grad_points(const GradPointArgs& a, double* out, cudaStream_t s);
 size_t grad_adj_doubles();

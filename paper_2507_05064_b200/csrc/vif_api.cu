@@ -242,6 +242,8 @@ struct Handle {
   const void* la_ws = nullptr;
   int la_epoch = 0, la_nprobe = 0, la_maxcg = 0, la_nlev_f = 0, la_nlev_b = 0;
   double la_sigma2 = 0.0;
+  // set by vif_grad around its vif_factor call: the vecchia rows also write the gradient state there
+  double* grad_state = nullptr;
   // profiling
   bool prof = false;
   cudaEvent_t ev[S_COUNT][2] = {};
@@ -1006,6 +1008,7 @@ int vif_factor(void* handle, const vif_theta* theta, double* B_out, double* D_ou
         a.B_out = B_out;
         a.D_out = D_out;
         a.st = st;
+        a.state = h->grad_state ? h->grad_state + (size_t)off * grad_state_doubles(P.mv) : nullptr;
         VIF_CUDA(h, launch_vecchia(a, s), "vecchia");
         ++nl;
       }
@@ -1101,6 +1104,7 @@ int vif_factor(void* handle, const vif_theta* theta, double* B_out, double* D_ou
         a.B_out = B_out;
         a.D_out = D_out;
         a.st = st;
+        a.state = h->grad_state ? h->grad_state + (size_t)off * grad_state_doubles(P.mv) : nullptr;
         VIF_CUDA(h, launch_vecchia(a, s), "vecchia");
         ++nl;
       }
@@ -1241,7 +1245,14 @@ int vif_grad(void* handle, const vif_theta* theta, void* gws, size_t gws_bytes, 
   CovParams p;
   std::string err;
   if (!make_params(h, theta, p, err)) return fail(h, VIF_ERR_INVALID_ARG, err);
+  // m_v <= 31 on one (real) rank per process: the factor's vecchia rows write L, A_i, 1/L_jj, D_i of the
+  // state (same rows, same arithmetic as the NLL) and only the g_i dots remain for the state pass;
+  // VIF_GRAD_STATE=1 recomputes everything in the state pass instead
+  static const char* gs_env = getenv("VIF_GRAD_STATE");
+  const bool state_ff = P.mv <= 31 && !P.emulate && !(gs_env && gs_env[0] == '1');
+  h->grad_state = state_ff ? gbuf(G_STATE) : nullptr;
   int r = vif_factor(handle, theta, nullptr, nullptr);
+  h->grad_state = nullptr;
   if (r != VIF_OK) return r;
   cudaStream_t s = h->stream;
   const int m = P.m, mk = P.mk, ld = P.ld;
@@ -1294,7 +1305,8 @@ int vif_grad(void* handle, const vif_theta* theta, void* gws, size_t gws_bytes, 
     a.rho = gbuf(G_RHO);
     a.sig = gbuf(G_SIG);
     a.adj = gbuf(G_ADJ);
-    VIF_CUDA(h, launch_grad_state(a, s), "gradient state");
+    if (state_ff) VIF_CUDA(h, launch_grad_gam(a, s), "gradient state (dots)");
+    else VIF_CUDA(h, launch_grad_state(a, s), "gradient state");
     // adjoint vectors (default) or the cross-Gram pass per parameter (VIF_GRAD_CROSS=1)
     static const char* cross_env = getenv("VIF_GRAD_CROSS");
     const bool cross = cross_env && cross_env[0] == '1';
