@@ -1176,7 +1176,8 @@ cudaError_t launch_grad_any(const GradPointArgs& a, bool state_pass, cudaStream_
 }  // namespace
 
 // g_i . U_aug[S_k] (k < s) into a state whose L, A_i, 1/L_jj, D_i the factor wrote: warp per point,
-// lane (g, t) reads columns 2t, 2t+1 of row R*8+g of every 8-column step (as grad_state_kernel)
+// lanes over columns (each load instruction reads 512 contiguous bytes of one row), one partial sum
+// per row in registers, then a transposing butterfly (31 shuffles) leaves the sum for row k in lane k
 template <int RB>
 __global__ void __launch_bounds__(GW * 32) grad_gam_kernel(const double* __restrict__ U, const double* __restrict__ Gam,
                                                           int64_t ldu, int ld, const int32_t* __restrict__ nbr,
@@ -1184,40 +1185,47 @@ __global__ void __launch_bounds__(GW * 32) grad_gam_kernel(const double* __restr
                                                           double* __restrict__ state) {
   constexpr int SP = RB * 8;
   constexpr int LP = SP * (SP + 1) / 2;
+  static_assert(SP <= 32, "one row per lane");
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t pos = (int64_t)blockIdx.x * GW + warp;
   if (pos >= npts) return;
   const int64_t i = order[pos];
   const int nb0 = lane < mv ? nbr[i * mv + lane] : -1;
   const int q = __popc(__ballot_sync(0xffffffffu, nb0 >= 0));
-  const double* rp[RB];
+  const int64_t myrow = lane < q ? (int64_t)nb0 : (lane == q ? i : 0);  // rows past s: never loaded
+  double v[32];
 #pragma unroll
-  for (int R = 0; R < RB; ++R) {
-    const int row = R * 8 + (lane >> 2);
-    const int gi = __shfl_sync(0xffffffffu, nb0, row & 31);
-    const int64_t idx = row < q ? gi : (row == q ? i : -1);
-    rp[R] = idx >= 0 ? U + idx * ldu + 2 * (lane & 3) : nullptr;
-  }
-  const double* grow = Gam + pos * (int64_t)ld + 2 * (lane & 3);
-  double gm[RB];
+  for (int k = 0; k < 32; ++k) v[k] = 0.0;
+  const double* grow = Gam + pos * (int64_t)ld;
+  for (int c0 = 0; c0 < ld; c0 += 64) {  // warp-uniform trip count (the shuffles below need all lanes)
+    const int c = c0 + 2 * lane;
+    const bool in = c < ld;
+    const double2 g2 = in ? __ldg(reinterpret_cast<const double2*>(grow + c)) : make_double2(0.0, 0.0);
 #pragma unroll
-  for (int R = 0; R < RB; ++R) gm[R] = 0.0;
-#pragma unroll 4
-  for (int k0 = 0; k0 < ld; k0 += 8) {
-    const double2 g2 = __ldg(reinterpret_cast<const double2*>(grow + k0));
+    for (int kb = 0; kb < SP; kb += 16) {  // 16 rows' loads in flight per lane
+      double2 u[16];
 #pragma unroll
-    for (int R = 0; R < RB; ++R) {
-      const double2 f = rp[R] ? __ldg(reinterpret_cast<const double2*>(rp[R] + k0)) : make_double2(0.0, 0.0);
-      gm[R] = fma(f.x, g2.x, fma(f.y, g2.y, gm[R]));
+      for (int k = 0; k < 16; ++k) {
+        const int64_t r = __shfl_sync(0xffffffffu, myrow, (kb + k) & 31);
+        u[k] = (in && kb + k < SP && kb + k <= q) ? __ldg(reinterpret_cast<const double2*>(U + r * ldu + c))
+                                                  : make_double2(0.0, 0.0);
+      }
+#pragma unroll
+      for (int k = 0; k < 16; ++k)
+        if (kb + k < SP) v[kb + k] = fma(u[k].x, g2.x, fma(u[k].y, g2.y, v[kb + k]));
     }
   }
-  double* st = state + pos * (int64_t)vif_state_doubles<RB>();
 #pragma unroll
-  for (int R = 0; R < RB; ++R) {
-    gm[R] += __shfl_xor_sync(0xffffffffu, gm[R], 1);
-    gm[R] += __shfl_xor_sync(0xffffffffu, gm[R], 2);
-    if ((lane & 3) == 0) st[LP + 2 * SP + R * 8 + (lane >> 2)] = gm[R];
+  for (int o = 16; o >= 1; o >>= 1) {
+    const bool upper = (lane & o) != 0;
+#pragma unroll
+    for (int k = 0; k < o; ++k) {
+      const double send = upper ? v[k] : v[k + o];
+      const double keep = upper ? v[k + o] : v[k];
+      v[k] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+    }
   }
+  if (lane < SP) state[pos * (int64_t)vif_state_doubles<RB>() + LP + 2 * SP + lane] = v[0];
 }
 
 cudaError_t launch_grad_gam(const GradPointArgs& a, cudaStream_t s) {
