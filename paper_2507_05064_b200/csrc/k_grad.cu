@@ -982,7 +982,10 @@ __global__ void __launch_bounds__(256) gR_kernel(const int* __restrict__ ptr, co
                                                  unsigned long long* __restrict__ next) {
   constexpr int SP = RB * 8;
   constexpr int LP = SP * (SP + 1) / 2;
-  constexpr int CPL = 4;  // columns per lane per pass (16: slower at n = 1M, 240 vs 232 ms per gradient)
+  // 16 columns per lane per pass (mk <= 512: one pass); the entries' metadata (position, a~, beta~) is
+  // loaded by the lanes in parallel, 32 entries at a time, and broadcast by shuffles, so the row loads
+  // of consecutive entries carry no dependent-load chain
+  constexpr int CPL = 16;
   const int lane = threadIdx.x & 31;
   // rows are handed out by a counter (not grid-strided): warps with long children lists would otherwise
   // drift apart and the window of rows in flight -- whose adjoint rows should stay in L2 -- would spread
@@ -997,18 +1000,34 @@ __global__ void __launch_bounds__(256) gR_kernel(const int* __restrict__ ptr, co
       double acc[CPL];
 #pragma unroll
       for (int u = 0; u < CPL; ++u) acc[u] = 0.0;
-      for (int e = a; e < b; ++e) {
-        const int en = ent[e];
-        const int64_t pos = en >> 6;
-        const int bb = en & 63;
-        const bool self = order[pos] == j;
-        const double al = self ? 1.0 : -state[pos * (int64_t)state_doubles<RB>() + LP + bb];
-        const double be = self ? 0.0 : adj[pos * (int64_t)ADJ_STRIDE + 2 + bb];
-        const double* rr = rho + pos * (int64_t)mk + k0 + lane;
-        const double* ss = sig + pos * (int64_t)mk + k0 + lane;
+      for (int e0 = a; e0 < b; e0 += 32) {
+        int64_t mypos = 0;
+        double myal = 0.0, mybe = 0.0;
+        if (e0 + lane < b) {
+          const int en = ent[e0 + lane];
+          mypos = en >> 6;
+          const int bb = en & 63;
+          const bool self = order[mypos] == j;
+          myal = self ? 1.0 : -state[mypos * (int64_t)state_doubles<RB>() + LP + bb];
+          mybe = self ? 0.0 : adj[mypos * (int64_t)ADJ_STRIDE + 2 + bb];
+        }
+        const int ne = min(32, b - e0);
+        for (int q = 0; q < ne; ++q) {
+          const int64_t pos = __shfl_sync(0xffffffffu, mypos, q);
+          const double al = __shfl_sync(0xffffffffu, myal, q);
+          const double be = __shfl_sync(0xffffffffu, mybe, q);
+          const double* rr = rho + pos * (int64_t)mk + k0 + lane;
+          const double* ss = sig + pos * (int64_t)mk + k0 + lane;
+          double rv[CPL], sv[CPL];
 #pragma unroll
-        for (int u = 0; u < CPL; ++u)
-          if (k0 + lane + 32 * u < mk) acc[u] = fma(al, __ldg(rr + 32 * u), fma(be, __ldg(ss + 32 * u), acc[u]));
+          for (int u = 0; u < CPL; ++u) {
+            const bool in = k0 + lane + 32 * u < mk;
+            rv[u] = in ? __ldg(rr + 32 * u) : 0.0;
+            sv[u] = in ? __ldg(ss + 32 * u) : 0.0;
+          }
+#pragma unroll
+          for (int u = 0; u < CPL; ++u) acc[u] = fma(al, rv[u], fma(be, sv[u], acc[u]));
+        }
       }
 #pragma unroll
       for (int u = 0; u < CPL; ++u) {
