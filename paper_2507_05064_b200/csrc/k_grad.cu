@@ -1197,6 +1197,7 @@ cudaError_t launch_grad_any(const GradPointArgs& a, bool state_pass, cudaStream_
 // g_i . U_aug[S_k] (k < s) into a state whose L, A_i, 1/L_jj, D_i the factor wrote: warp per point,
 // lanes over columns (each load instruction reads 512 contiguous bytes of one row), one partial sum
 // per row in registers, then a transposing butterfly (31 shuffles) leaves the sum for row k in lane k
+// (s > 32: rows 32.. in a second pass over the columns)
 template <int RB>
 __global__ void __launch_bounds__(GW * 32) grad_gam_kernel(const double* __restrict__ U, const double* __restrict__ Gam,
                                                           int64_t ldu, int ld, const int32_t* __restrict__ nbr,
@@ -1204,47 +1205,56 @@ __global__ void __launch_bounds__(GW * 32) grad_gam_kernel(const double* __restr
                                                           double* __restrict__ state) {
   constexpr int SP = RB * 8;
   constexpr int LP = SP * (SP + 1) / 2;
-  static_assert(SP <= 32, "one row per lane");
+  constexpr int NH = (SP + 31) / 32;  // halves of 32 rows (s > 32: two passes over the columns)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t pos = (int64_t)blockIdx.x * GW + warp;
   if (pos >= npts) return;
   const int64_t i = order[pos];
   const int nb0 = lane < mv ? nbr[i * mv + lane] : -1;
-  const int q = __popc(__ballot_sync(0xffffffffu, nb0 >= 0));
-  const int64_t myrow = lane < q ? (int64_t)nb0 : (lane == q ? i : 0);  // rows past s: never loaded
-  double v[32];
-#pragma unroll
-  for (int k = 0; k < 32; ++k) v[k] = 0.0;
+  const int nb1 = lane + 32 < mv ? nbr[i * mv + lane + 32] : -1;
+  const int q = __popc(__ballot_sync(0xffffffffu, nb0 >= 0)) + __popc(__ballot_sync(0xffffffffu, nb1 >= 0));
   const double* grow = Gam + pos * (int64_t)ld;
-  for (int c0 = 0; c0 < ld; c0 += 64) {  // warp-uniform trip count (the shuffles below need all lanes)
-    const int c = c0 + 2 * lane;
-    const bool in = c < ld;
-    const double2 g2 = in ? __ldg(reinterpret_cast<const double2*>(grow + c)) : make_double2(0.0, 0.0);
+  double* st = state + pos * (int64_t)vif_state_doubles<RB>();
 #pragma unroll
-    for (int kb = 0; kb < SP; kb += 16) {  // 16 rows' loads in flight per lane
-      double2 u[16];
+  for (int h = 0; h < NH; ++h) {
+    constexpr int HR = SP < 32 ? SP : 32;  // rows per half
+    const int row = 32 * h + lane;
+    const int nb = h == 0 ? nb0 : nb1;
+    const int64_t myrow = row < q ? (int64_t)nb : (row == q ? i : 0);  // rows past s: never loaded
+    double v[32];
 #pragma unroll
-      for (int k = 0; k < 16; ++k) {
-        const int64_t r = __shfl_sync(0xffffffffu, myrow, (kb + k) & 31);
-        u[k] = (in && kb + k < SP && kb + k <= q) ? __ldg(reinterpret_cast<const double2*>(U + r * ldu + c))
-                                                  : make_double2(0.0, 0.0);
+    for (int k = 0; k < 32; ++k) v[k] = 0.0;
+    for (int c0 = 0; c0 < ld; c0 += 64) {  // warp-uniform trip count (the shuffles below need all lanes)
+      const int c = c0 + 2 * lane;
+      const bool in = c < ld;
+      const double2 g2 = in ? __ldg(reinterpret_cast<const double2*>(grow + c)) : make_double2(0.0, 0.0);
+#pragma unroll
+      for (int kb = 0; kb < HR; kb += 16) {  // 16 rows' loads in flight per lane
+        double2 u[16];
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+          const int64_t r = __shfl_sync(0xffffffffu, myrow, (kb + k) & 31);
+          const int kr = 32 * h + kb + k;
+          u[k] = (in && kb + k < HR && kr < SP && kr <= q) ? __ldg(reinterpret_cast<const double2*>(U + r * ldu + c))
+                                                          : make_double2(0.0, 0.0);
+        }
+#pragma unroll
+        for (int k = 0; k < 16; ++k)
+          if (kb + k < HR) v[kb + k] = fma(u[k].x, g2.x, fma(u[k].y, g2.y, v[kb + k]));
       }
-#pragma unroll
-      for (int k = 0; k < 16; ++k)
-        if (kb + k < SP) v[kb + k] = fma(u[k].x, g2.x, fma(u[k].y, g2.y, v[kb + k]));
     }
-  }
 #pragma unroll
-  for (int o = 16; o >= 1; o >>= 1) {
-    const bool upper = (lane & o) != 0;
+    for (int o = 16; o >= 1; o >>= 1) {
+      const bool upper = (lane & o) != 0;
 #pragma unroll
-    for (int k = 0; k < o; ++k) {
-      const double send = upper ? v[k] : v[k + o];
-      const double keep = upper ? v[k + o] : v[k];
-      v[k] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+      for (int k = 0; k < o; ++k) {
+        const double send = upper ? v[k] : v[k + o];
+        const double keep = upper ? v[k + o] : v[k];
+        v[k] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+      }
     }
+    if (row < SP) st[LP + 2 * SP + row] = v[0];
   }
-  if (lane < SP) state[pos * (int64_t)vif_state_doubles<RB>() + LP + 2 * SP + lane] = v[0];
 }
 
 cudaError_t launch_grad_gam(const GradPointArgs& a, cudaStream_t s) {
@@ -1255,7 +1265,9 @@ cudaError_t launch_grad_gam(const GradPointArgs& a, cudaStream_t s) {
     case 2: grad_gam_kernel<2><<<blocks, GW * 32, 0, s>>>(a.U, a.Gam, a.ldu, a.ld, a.nbr, a.mv, a.order, a.npts, a.state); break;
     case 3: grad_gam_kernel<3><<<blocks, GW * 32, 0, s>>>(a.U, a.Gam, a.ldu, a.ld, a.nbr, a.mv, a.order, a.npts, a.state); break;
     case 4: grad_gam_kernel<4><<<blocks, GW * 32, 0, s>>>(a.U, a.Gam, a.ldu, a.ld, a.nbr, a.mv, a.order, a.npts, a.state); break;
-    default: return cudaErrorInvalidValue;  // m_v > 31: the state pass computes everything
+    case 5: grad_gam_kernel<5><<<blocks, GW * 32, 0, s>>>(a.U, a.Gam, a.ldu, a.ld, a.nbr, a.mv, a.order, a.npts, a.state); break;
+    case 6: grad_gam_kernel<6><<<blocks, GW * 32, 0, s>>>(a.U, a.Gam, a.ldu, a.ld, a.nbr, a.mv, a.order, a.npts, a.state); break;
+    default: return cudaErrorInvalidValue;  // m_v <= 47
   }
   return cudaGetLastError();
 }

@@ -42,7 +42,7 @@ __global__ void __launch_bounds__(VW * 32, 3) vecchia_smem_kernel(
     const double* __restrict__ U, int64_t ldu, int mk, int ld, const double* __restrict__ X,
     const double* __restrict__ Uq, const double* __restrict__ Xq, const int32_t* __restrict__ nbr, int mv, const int64_t* __restrict__ order, int64_t npts, CovParams p,
     double* __restrict__ W, int64_t ldw, double* __restrict__ Dpos, double* __restrict__ B_out,
-    double* __restrict__ D_out, DevStatus* __restrict__ st) {
+    double* __restrict__ D_out, DevStatus* __restrict__ st, double* __restrict__ gstate) {
   constexpr int SP = RB * 8;
   constexpr int NT = RB * (RB + 1) / 2;
   extern __shared__ __align__(16) double vsm[];
@@ -260,6 +260,23 @@ __global__ void __launch_bounds__(VW * 32, 3) vecchia_smem_kernel(
     if (B_out) {
       if (lane < mv) B_out[i * mv + lane] = lane < q ? -a0 : 0.0;
       if (lane + 32 < mv) B_out[i * mv + lane + 32] = lane + 32 < q ? -a1 : 0.0;
+    }
+    if (gstate) {  // vif_grad: L (packed like C, identity padding rows), A_i, 1/L_jj, D_i for its first pass
+      constexpr int LP = SP * (SP + 1) / 2;
+      double* sp = gstate + pos * (int64_t)vif_state_doubles<RB>();
+      for (int e = lane; e < LP; e += 32) sp[e] = C[e];
+      if (lane < SP) {
+        sp[LP + lane] = lane < q ? a0 : 0.0;
+        sp[LP + SP + lane] = lane < s ? inv0 : 1.0;
+      }
+      if (lane + 32 < SP) {
+        sp[LP + lane + 32] = lane + 32 < q ? a1 : 0.0;
+        sp[LP + SP + lane + 32] = lane + 32 < s ? inv1 : 1.0;
+      }
+      if (lane == 0) {
+        sp[LP + 3 * SP] = Di;
+        sp[LP + 3 * SP + 1] = 1.0;
+      }
     }
   }
   __syncwarp();
@@ -656,7 +673,7 @@ static cudaError_t launch_rb(const VecchiaArgs& a, cudaStream_t s) {
     kern<<<blocks, VW * 32, smem, s>>>(a.U, a.ldu, a.mk, a.ld, a.X, a.Uself ? a.Uself : a.U,
                                                                    a.Xself ? a.Xself : a.X, a.nbr, a.mv,
                                                                    a.order, a.npts, a.p, a.W, a.ldw, a.Dpos,
-                                                                   a.B_out, a.D_out, a.st);
+                                                                   a.B_out, a.D_out, a.st, a.state);
   }
   return cudaGetLastError();
 }

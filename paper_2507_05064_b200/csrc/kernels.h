@@ -28,7 +28,7 @@ struct VecchiaArgs {
   // prediction points whose neighbours are training rows of U / X); NULL = U / X
   const double* Uself = nullptr;
   const double* Xself = nullptr;
-  // gradient (vif_grad, m_v <= 31): the factor's rows also write the per-point state of the gradient's
+  // gradient (vif_grad, one rank per process): the factor's rows also write the per-point state of the gradient's
   // first pass (vif_state_doubles layout, by position; the g_i dots are left to launch_grad_gam)
   double* state = nullptr;
 };

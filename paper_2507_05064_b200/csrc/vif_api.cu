@@ -1245,11 +1245,11 @@ int vif_grad(void* handle, const vif_theta* theta, void* gws, size_t gws_bytes, 
   CovParams p;
   std::string err;
   if (!make_params(h, theta, p, err)) return fail(h, VIF_ERR_INVALID_ARG, err);
-  // m_v <= 31 on one (real) rank per process: the factor's vecchia rows write L, A_i, 1/L_jj, D_i of the
+  // one (real) rank per process: the factor's vecchia rows write L, A_i, 1/L_jj, D_i of the
   // state (same rows, same arithmetic as the NLL) and only the g_i dots remain for the state pass;
   // VIF_GRAD_STATE=1 recomputes everything in the state pass instead
   static const char* gs_env = getenv("VIF_GRAD_STATE");
-  const bool state_ff = P.mv <= 31 && !P.emulate && !(gs_env && gs_env[0] == '1');
+  const bool state_ff = P.mv <= 47 && !P.emulate && !(gs_env && gs_env[0] == '1');
   h->grad_state = state_ff ? gbuf(G_STATE) : nullptr;
   int r = vif_factor(handle, theta, nullptr, nullptr);
   h->grad_state = nullptr;
