@@ -973,8 +973,11 @@ __global__ void gchild_sort_kernel(int64_t n, const int* __restrict__ ptr, const
 
 // R[j][k] = sum_{entries (pos, b) of j} a~_{pos,b} rho[pos][k] + beta~_{pos,b} sig[pos][k]; warp per j,
 // j in index order (jorder: an optional visiting order)
-template <int RB>
-__global__ void __launch_bounds__(256) gR_kernel(const int* __restrict__ ptr, const int* __restrict__ ent,
+// CPL as a template parameter: nvcc then issues all 2 CPL row loads of an entry before its FMAs (140
+// registers, one 8-warp block per SM: 148 vs 159 ms per gradient at config 3 against 72 registers and
+// 24 warps with the loads interleaved; 64-register / 4-block variants 151-152 ms)
+template <int RB, int CPL = 16, int MINB = 1>
+__global__ void __launch_bounds__(256, MINB) gR_kernel(const int* __restrict__ ptr, const int* __restrict__ ent,
                                                  const int64_t* __restrict__ order, const int64_t* __restrict__ jorder,
                                                  int64_t n, int mk, const double* __restrict__ state,
                                                  const double* __restrict__ adj, const double* __restrict__ rho,
@@ -985,7 +988,6 @@ __global__ void __launch_bounds__(256) gR_kernel(const int* __restrict__ ptr, co
   // 16 columns per lane per pass (mk <= 512: one pass); the entries' metadata (position, a~, beta~) is
   // loaded by the lanes in parallel, 32 entries at a time, and broadcast by shuffles, so the row loads
   // of consecutive entries carry no dependent-load chain
-  constexpr int CPL = 16;
   const int lane = threadIdx.x & 31;
   // rows are handed out by a counter (not grid-strided): warps with long children lists would otherwise
   // drift apart and the window of rows in flight -- whose adjoint rows should stay in L2 -- would spread
