@@ -235,7 +235,8 @@ def test_config3_full_nll_and_sampled_rows():
 
 def test_rounds_schedule_same_result():
     """The optional single-GPU round schedule (VIF_ROUNDS, three streams) gives the serial result:
-    B and D bit-identical, NLL to 1e-12 (only the SYRK summation order differs).  The knob is read
+    B and D bit-identical, NLL to 1e-12 and the gradient to 1e-10 (only the SYRK summation order
+    differs).  The knob is read
     once per process, hence the subprocess."""
     import json
     import os
@@ -251,7 +252,8 @@ dev = torch.device("cuda")
 m = p.VifModel(*(torch.from_numpy(np.ascontiguousarray(a)).to(dev) for a in (w.X, w.Z, w.nbr, w.y)))
 B = torch.zeros((w.n, w.mv), dtype=torch.float64, device=dev); D = torch.zeros(w.n, dtype=torch.float64, device=dev)
 t = m.evaluate(p.Theta(**w.theta_dict()), B, D)
-np.save(sys.argv[1], np.concatenate([B.cpu().numpy().ravel(), D.cpu().numpy(), [t.nll]]))
+_, g = m.grad(p.Theta(**w.theta_dict()))  # the factor inside vif_grad writes the gradient state per round
+np.save(sys.argv[1], np.concatenate([B.cpu().numpy().ravel(), D.cpu().numpy(), [t.nll], g]))
 ''' % os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     outs = []
     for R in ("1", "4"):
@@ -260,8 +262,10 @@ np.save(sys.argv[1], np.concatenate([B.cpu().numpy().ravel(), D.cpu().numpy(), [
         subprocess.run([sys.executable, "-c", code, path], env=env, check=True)
         outs.append(np.load(path))
     a, b = outs
-    assert np.array_equal(a[:-1], b[:-1])
-    assert b[-1] == pytest.approx(a[-1], rel=1e-12)
+    k = a.size - 4  # B, D | NLL | gradient (sigma_1^2, lambda_1, lambda_2, sigma^2)
+    assert np.array_equal(a[:k - 1], b[:k - 1])
+    assert b[k - 1] == pytest.approx(a[k - 1], rel=1e-12)
+    np.testing.assert_allclose(b[k:], a[k:], rtol=1e-10)
 
 
 def test_stage_data_pipelined_matches_set_data():
