@@ -37,8 +37,8 @@ __host__ __device__ constexpr int vecchia_warp_doubles(int d) {
   return RB * 8 * (RB * 8 + 1) / 2 + RB * 8 + 64 + RB * 8 * d;
 }
 
-template <int FAM, int RB, int NB>
-__global__ void __launch_bounds__(VW * 32, 3) vecchia_smem_kernel(
+template <int FAM, int RB, int NB, int MINB = 3>
+__global__ void __launch_bounds__(VW * 32, MINB) vecchia_smem_kernel(
     const double* __restrict__ U, int64_t ldu, int mk, int ld, const double* __restrict__ X,
     const double* __restrict__ Uq, const double* __restrict__ Xq, const int32_t* __restrict__ nbr, int mv, const int64_t* __restrict__ order, int64_t npts, CovParams p,
     double* __restrict__ W, int64_t ldw, double* __restrict__ Dpos, double* __restrict__ B_out,
@@ -623,59 +623,71 @@ __global__ void __launch_bounds__(VW * 32, MINB) vecchia_reg_kernel(
 }
 
 template <int FAM, int RB>
-static cudaError_t launch_rb(const VecchiaArgs& a, cudaStream_t s) {
+static cudaError_t launch_reg(const VecchiaArgs& a, cudaStream_t s) {
   const unsigned blocks = (unsigned)((a.npts + VW - 1) / VW);
+  const size_t smem = (size_t)VW * vreg_warp_doubles<RB>(a.p.d) * sizeof(double);
+  // VIF_VREG_CFG = "<ring depth><min blocks/SM>" for A/B runs; default "34"
+  static const char* cfg_env = getenv("VIF_VREG_CFG");
+  const int cfg = cfg_env ? atoi(cfg_env) : 34;
+  decltype(&vecchia_reg_kernel<FAM, RB, 3, 4>) kern;
+  if (a.Uself) {
+    kern = vecchia_reg_kernel<FAM, RB, 3, 4, true>;
+  } else {
+    static const char* gen_env = getenv("VIF_VECCHIA_GENERIC_D");
+    const int dd = (gen_env && gen_env[0] == '1') ? 0 : a.p.d;
+    if (cfg == 24) kern = vecchia_reg_kernel<FAM, RB, 2, 4>;
+    else if (dd == 2) kern = vecchia_reg_kernel<FAM, RB, 3, 4, false, 2>;
+    else kern = vecchia_reg_kernel<FAM, RB, 3, 4>;
+  }
+  if (smem > 40 * 1024) {  // static shared memory comes on top
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  {
+    const char* dbg = getenv("VIF_DEBUG_VECCHIA");
+    static int last = 0;
+    const int v = dbg ? atoi(dbg) : 0;
+    if (v != last) {
+      cudaMemcpyToSymbolAsync(g_vif_debug, &v, sizeof(int), 0, cudaMemcpyHostToDevice, s);
+      cudaStreamSynchronize(s);
+      last = v;
+    }
+  }
+  kern<<<blocks, VW * 32, smem, s>>>(a.U, a.ldu, a.mk, a.ld, a.X, a.Uself ? a.Uself : a.U, a.Xself ? a.Xself : a.X,
+                                     a.nbr, a.mv, a.order, a.npts, a.p, a.W, a.ldw, a.Dpos, a.B_out, a.D_out, a.st,
+                                     a.state);
+  return cudaGetLastError();
+}
+
+template <int FAM, int RB>
+static cudaError_t launch_smem(const VecchiaArgs& a, cudaStream_t s, int minb4) {
+  const unsigned blocks = (unsigned)((a.npts + VW - 1) / VW);
+  const size_t smem = (size_t)VW * vecchia_warp_doubles<RB>(a.p.d) * sizeof(double);
+  static const char* nb_env = getenv("VIF_SMEM_NB");  // A/B hook: Gram ring depth 1 or 2
+  auto kern = (nb_env && nb_env[0] == '2') ? vecchia_smem_kernel<FAM, RB, 2> : vecchia_smem_kernel<FAM, RB, 1>;
+  if (minb4) kern = vecchia_smem_kernel<FAM, RB, 1, 4>;
+  {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  kern<<<blocks, VW * 32, smem, s>>>(a.U, a.ldu, a.mk, a.ld, a.X, a.Uself ? a.Uself : a.U,
+                                                                 a.Xself ? a.Xself : a.X, a.nbr, a.mv,
+                                                                 a.order, a.npts, a.p, a.W, a.ldw, a.Dpos,
+                                                                 a.B_out, a.D_out, a.st, a.state);
+  return cudaGetLastError();
+}
+
+template <int FAM, int RB>
+static cudaError_t launch_rb(const VecchiaArgs& a, cudaStream_t s) {
   // s <= 32: the per-warp register kernel.  Measured and rejected on B200 (profiles/r01_notes.md):
   // warp-specialised Gram / solver warps (register ring or cp.async shared-memory ring) and a
   // mixed-precision (FP32 Cholesky + FP64 refinement) solver.
+  static const char* blk_env = getenv("VIF_VECCHIA_BLOCKED");  // A/B: blocked DMMA Cholesky for s <= 32 too
+  const int blk = blk_env ? atoi(blk_env) : 0;
   if constexpr (RB <= 4) {
-    const size_t smem = (size_t)VW * vreg_warp_doubles<RB>(a.p.d) * sizeof(double);
-    // VIF_VREG_CFG = "<ring depth><min blocks/SM>" for A/B runs; default "34"
-    static const char* cfg_env = getenv("VIF_VREG_CFG");
-    const int cfg = cfg_env ? atoi(cfg_env) : 34;
-    decltype(&vecchia_reg_kernel<FAM, RB, 3, 4>) kern;
-    if (a.Uself) {
-      kern = vecchia_reg_kernel<FAM, RB, 3, 4, true>;
-    } else {
-      static const char* gen_env = getenv("VIF_VECCHIA_GENERIC_D");
-      const int dd = (gen_env && gen_env[0] == '1') ? 0 : a.p.d;
-      if (cfg == 24) kern = vecchia_reg_kernel<FAM, RB, 2, 4>;
-      else if (dd == 2) kern = vecchia_reg_kernel<FAM, RB, 3, 4, false, 2>;
-      else kern = vecchia_reg_kernel<FAM, RB, 3, 4>;
-    }
-    if (smem > 40 * 1024) {  // static shared memory comes on top
-      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      if (e != cudaSuccess) return e;
-    }
-    {
-      const char* dbg = getenv("VIF_DEBUG_VECCHIA");
-      static int last = 0;
-      const int v = dbg ? atoi(dbg) : 0;
-      if (v != last) {
-        cudaMemcpyToSymbolAsync(g_vif_debug, &v, sizeof(int), 0, cudaMemcpyHostToDevice, s);
-        cudaStreamSynchronize(s);
-        last = v;
-      }
-    }
-    kern<<<blocks, VW * 32, smem, s>>>(a.U, a.ldu, a.mk, a.ld, a.X, a.Uself ? a.Uself : a.U, a.Xself ? a.Xself : a.X,
-                                       a.nbr, a.mv, a.order, a.npts, a.p, a.W, a.ldw, a.Dpos, a.B_out, a.D_out, a.st,
-                                       a.state);
-  } else {
-    const size_t smem = (size_t)VW * vecchia_warp_doubles<RB>(a.p.d) * sizeof(double);
-    static const char* nb_env = getenv("VIF_SMEM_NB");  // A/B hook: Gram ring depth 1 or 2
-    auto kern = (nb_env && nb_env[0] == '2') ? vecchia_smem_kernel<FAM, RB, 2> : vecchia_smem_kernel<FAM, RB, 1>;
-    static size_t attr = 0;
-    if (attr < smem) {
-      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      if (e != cudaSuccess) return e;
-      attr = smem;
-    }
-    kern<<<blocks, VW * 32, smem, s>>>(a.U, a.ldu, a.mk, a.ld, a.X, a.Uself ? a.Uself : a.U,
-                                                                   a.Xself ? a.Xself : a.X, a.nbr, a.mv,
-                                                                   a.order, a.npts, a.p, a.W, a.ldw, a.Dpos,
-                                                                   a.B_out, a.D_out, a.st, a.state);
+    if (blk == 0) return launch_reg<FAM, RB>(a, s);
   }
-  return cudaGetLastError();
+  return launch_smem<FAM, RB>(a, s, blk == 4);
 }
 
 template <int FAM>
