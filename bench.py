@@ -9,8 +9,9 @@ rewritten every step, far larger than the 126 MB L2.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config 3] [--impl vif|reference]
 
-Multi-GPU: launched by torchrun, one process per GPU; rows are sharded chunk-cyclically, U is
-all-gathered and the Gram all-reduced by NCCL inside libvif; the problem size stays n = 1M
+Multi-GPU: one process per GPU, launched by torchrun -- or by `bench.py --gpus N` itself, which
+re-executes under torch.distributed.run when WORLD_SIZE is unset; rows are sharded chunk-cyclically,
+U is all-gathered and the Gram all-reduced by NCCL inside libvif; the problem size stays n = 1M
 (strong scaling).  Rank 0 prints one JSON line.
 """
 from __future__ import annotations
@@ -159,10 +160,79 @@ def cpu_oracle_sample(w, target_s):
     return ns2 / dt2, oracle.num_threads(), ns2, dt2
 
 
+_ONE_THREAD = r'''
+import json, sys, time
+import numpy as np
+sys.path.insert(0, sys.argv[1])
+import oracle
+z = np.load(sys.argv[2])
+th = oracle.Theta(**json.loads(str(z["theta"])))
+ns = int(sys.argv[3])
+t = time.perf_counter()
+oracle.factor_nll(z["X"][:ns], z["Z"], z["nbr"][:ns], z["y"][:ns], th, want_BD=False)
+print(json.dumps({"s": time.perf_counter() - t, "threads": oracle.num_threads()}))
+'''
+
+
+def cpu_oracle_one_thread(dev, target_s=6.0):
+    """SURVEY 8(d) / BASELINE.md section 3: the oracle on ONE host thread (OMP_NUM_THREADS=1, separate
+    process) on a prefix of config 2, a per-core figure beside the all-core cpu_baseline."""
+    import tempfile
+    import vifgen
+    w2 = vifgen.make_config(2, device=str(dev))
+    td = {**w2.theta_dict(), "lengthscale": [float(v) for v in w2.lengthscale]}
+    path = os.path.join(tempfile.gettempdir(), f"vif_cfg2_{os.getpid()}.npz")
+    np.savez(path, X=w2.X, Z=w2.Z, nbr=w2.nbr, y=w2.y, theta=json.dumps(td))
+    env = dict(os.environ, OMP_NUM_THREADS="1")
+    try:
+        ns = 2000
+        r = json.loads(subprocess.run([sys.executable, "-c", _ONE_THREAD, ROOT, path, str(ns)], env=env, check=True,
+                                      capture_output=True, text=True).stdout.strip().splitlines()[-1])
+        ns = int(min(w2.n, max(ns, ns * target_s / max(r["s"], 1e-3))))
+        r = json.loads(subprocess.run([sys.executable, "-c", _ONE_THREAD, ROOT, path, str(ns)], env=env, check=True,
+                                      capture_output=True, text=True).stdout.strip().splitlines()[-1])
+    finally:
+        os.remove(path)
+    fl = sum(workload_flops(w2.nbr[:ns], w2.m).values())
+    return {"value": ns / r["s"], "unit": "points/s", "cores": r["threads"], "kind": "oracle",
+            "gflops": fl / r["s"] / 1e9,
+            "sample": f"oracle (C, OMP_NUM_THREADS=1) on the first {ns} points of config 2 (n = 100k, m = 200, "
+                      f"m_v = 20), {r['s']:.1f} s"}
+
+
+def grad_flops(nbr, m, d, ld):
+    """FP64 work of one vif_grad as this library organises it (DESIGN.md section 10; FMA = 2): the factor
+    (SURVEY 8(d) F) + Gamma = W (2Q) (2 n ld^2) + T = R L_m^{-1} (n m^2, triangular) + G2 = R^T U (2 n m^2) + the
+    gathered dots, adjoint rows and R scatter (~10 s m per point) + per kernel parameter the s(s-1)/2 point-pass
+    derivative evaluations and the n m fused dK evaluations contracted with T (2 n m).  Not a lower bound: the
+    method's minimum for the gradient is not fixed by the paper."""
+    n = nbr.shape[0]
+    s = (nbr >= 0).sum(1).astype(np.float64) + 1.0 if nbr.shape[1] > 0 else np.ones(n)
+    f = sum(workload_flops(nbr, m).values())
+    dense = 2.0 * n * ld * ld + n * float(m) * m + 2.0 * n * float(m) * m
+    gathers = float(np.sum(10.0 * s * m))
+    per_param = (d + 1) * (2.0 * n * m)
+    return {"total": f + dense + gathers + per_param, "factor": f, "dense_contractions": dense, "gathers": gathers,
+            "per_parameter": per_param}
+
+
 # ------------------------------------------------------------------------------------ main
+def relaunch_multi_gpu(args):
+    """`python bench.py --gpus N` outside torchrun: start N ranks (one process per GPU) through
+    torch.distributed.run on this node and return its exit code; rank 0 prints the JSON line."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(29500 + (os.getpid() % 1000)),
+           os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def main():
     args = parse()
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        sys.exit(relaunch_multi_gpu(args))
     world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world != args.gpus:
+        sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world} (launch one rank per GPU)")
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     import torch
@@ -246,22 +316,24 @@ def main():
     sampler = ClockSampler(local)
     barrier()
     torch.cuda.synchronize(dev)
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
     with sampler:
-        e0.record(stream)
+        ev[0].record(stream)
         last = None
         for k in range(args.steps):
             last = step(k)
-        e1.record(stream)
+            ev[k + 1].record(stream)
         torch.cuda.synchronize(dev)
     barrier()
-    ms = e0.elapsed_time(e1) / args.steps
+    step_ms = [ev[k].elapsed_time(ev[k + 1]) for k in range(args.steps)]
+    ms = statistics.median(step_ms)          # median of >= 10 steps
+    ms_mean = ev[0].elapsed_time(ev[-1]) / args.steps
     stages, nev = model.stage_times()
     model.profile(False)
-    ms_t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    ms_t = torch.tensor([ms, ms_mean], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
-    ms_max = float(ms_t.item())
+    ms_max, ms_mean_max = float(ms_t[0].item()), float(ms_t[1].item())
 
     # ---------------- end-to-end through the public API with HOST buffers ----------------
     hX, hZ, hnbr, hy = (torch.from_numpy(np.ascontiguousarray(a)).pin_memory() for a in (w.X, w.Z, w.nbr, w.y))
@@ -307,7 +379,13 @@ def main():
         g1.record(stream)
         torch.cuda.synchronize(dev)
         gms = g0.elapsed_time(g1) / g_steps
+        gf = grad_flops(w.nbr, w.m, w.d, (((w.m + 7) // 8 * 8 + 1) + 7) // 8 * 8)
         grad = {"ms_per_eval": gms, "points_per_s": w.n / (gms * 1e-3), "params": len(gvec),
+                "ratio_to_evaluation": gms / ms_max,
+                "roofline": {"bound": "tensor", "flops_per_eval": gf, "achieved": gf["total"] / (gms * 1e-3) / 1e12,
+                             "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                             "frac": gf["total"] / (gms * 1e-3) / 1e12 / FP64_PEAK_TFLOPS,
+                             "note": "flops of the library's gradient algorithm (bench.grad_flops), whole call"},
                 "grad_at_theta1": [float(x) for x in gvec],
                 "note": "vif_grad: factor + NLL + d+2 partial derivatives (sigma_1^2, lambda_1..d, sigma^2; "
                         "P:126-133, App. A), device events around the synchronous calls"}
@@ -385,7 +463,12 @@ def main():
             cpu = {"value": v, "unit": "points/s", "cores": cores, "kind": "oracle",
                    "sample": f"oracle (C, OpenMP, {cores} threads) on the first {ns} points of the same workload "
                              f"(same Z, theta, m, m_v; neighbours are predecessors so the prefix is self-contained); "
-                             f"{dt:.1f} s"}
+                             f"{dt:.1f} s",
+                   "gflops": sum(workload_flops(w.nbr[:ns], w.m).values()) / dt / 1e9}
+            try:
+                cpu["one_thread_config2"] = cpu_oracle_one_thread(dev)
+            except Exception as e:  # reported, never fatal for the bench line
+                cpu["one_thread_config2"] = {"error": str(e)[-300:]}
         out = {
             "metric": METRIC,
             "value": w.n / (ms_max * 1e-3),
@@ -394,6 +477,9 @@ def main():
             "steps": args.steps,
             "warmup": args.warmup,
             "ms_per_step": ms_max,
+            "ms_per_step_mean": ms_mean_max,
+            "timing": f"median of {args.steps} per-step CUDA-event intervals on the library stream (max over ranks); "
+                      f"mean {ms_mean_max:.3f} ms",
             "higher_is_better": True,
             "scaling": "strong",
             "vs_baseline": None,

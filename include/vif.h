@@ -115,7 +115,8 @@ int vif_create(void** handle, const vif_dims* dims, void* workspace, size_t ws_b
 
 /* (Re)load the inputs (same layout/pointer rules as vif_create; NULL leaves a part unchanged).
  * Enqueued on the handle's stream.  validate = 1 also checks finiteness and the neighbour-list
- * rules on the device and synchronises (INVALID_ARG with vif_last_error naming the row). */
+ * rules on the device and synchronises (INVALID_ARG with vif_last_error naming the row).
+ * New inputs invalidate a prepared VIF-Laplace workspace (vif_la_* then return VIF_ERR_STATE). */
 int vif_set_data(void* handle, const double* X, const double* Z, const int32_t* nbr, const double* y,
                  int32_t validate);
 
@@ -137,7 +138,12 @@ int vif_stage_data(void* handle, const double* X, const double* Z, const int32_t
 int vif_factor(void* handle, const vif_theta* theta, double* B_out, double* D_out);
 
 /* Finish the NLL (Cholesky of M_w, z = L_M^{-1} v, quad, log-dets),
- * synchronise the stream and return the terms (same value on every rank).
+ * synchronise the stream and return the terms (same value on every rank).  Multi-rank: the failing
+ * row of a residual block is found on the rank that owns it; vif_factor's all-reduce also takes the
+ * minimum failing row over the ranks, so every rank returns NOT_PD with the same bad_row.  With a
+ * communicator the wait polls ncclCommGetAsyncError and gives up after VIF_NCCL_TIMEOUT_S seconds
+ * (environment, default 600): the communicator is aborted and this and every later call on the
+ * handle return VIF_ERR_NCCL (a dead or hung peer never blocks the caller forever).
  * Errors: STATE (no vif_factor since create), NOT_PD (terms->bad_row says where), CUDA, NCCL. */
 int vif_nll(void* handle, vif_terms* out);
 
@@ -145,12 +151,15 @@ int vif_nll(void* handle, vif_terms* out);
  * theta = (sigma_1^2, lambda_1, ..., lambda_d, sigma^2): d + 2 partial derivatives; the jitter is
  * held fixed (an isotropic range rho has dNLL/drho = sum_j dNLL/dlambda_j).
  * vif_grad_workspace_bytes: size of the second, caller-owned device workspace the gradient needs
- * (Q (ld x ld), g rows and dU (n x ld each), m x m scratch; ld = roundup(roundup(m,8)+1, 8)).
- * vif_grad runs vif_factor + vif_nll at theta, then per parameter dK(Z,Z), Phi = L_m^{-1} dK_m
- * L_m^{-T}, dK(X,Z), dU and one pass over the points (Gram, cross-Gram, Cholesky, dA_i, dD_i), and
- * synchronises.  grad: host, d + 2 doubles, identical on every rank.  terms (optional): as vif_nll.
- * Multi-rank: each rank sums its own points' terms (its dU over all n rows is formed locally) and one
- * all-reduce of the d + 2 partial sums follows; an emulated handle sums its virtual ranks in order.
+ * (Q (ld x ld), g rows and R (n x ld each), the per-point state, m x m scratch;
+ * ld = roundup(roundup(m,8)+1, 8)).
+ * vif_grad runs vif_factor + vif_nll at theta (the factor's rows also write the per-point state:
+ * L, A_i, D_i), then the adjoint rows of every point, R = their scatter over the conditioning sets,
+ * T = R L_m^{-1} and G2 = R^T U once, and per parameter Phi = L_m^{-1} dK_m L_m^{-T},
+ * <T, dK(X,Z)> - <G2, Phi_low> and one pass over the points (dK_S, dA_i, dD_i in adjoint form;
+ * DESIGN.md section 10), and synchronises.  grad: host, d + 2 doubles, identical on every rank.
+ * terms (optional): as vif_nll.  Multi-rank: each rank sums its own points' terms and one all-reduce
+ * of the d + 2 partial sums follows; an emulated handle sums its virtual ranks in order.
  * Every m_v <= VIF_MAX_MV (s > 32: a shared-memory Cholesky in the state pass).
  * Errors: INVALID_ARG (theta), NO_MEMORY
  * (grad workspace too small), NOT_PD (as vif_nll), CUDA. */
@@ -166,7 +175,9 @@ int vif_grad(void* handle, const vif_theta* theta, void* grad_workspace, size_t 
  *   var_p = D_p + e_p^T M_w^{-1} e_p,                    u_p = L_m^{-1} k(Z, x_p),
  *   A_p = C_{p,N} C_{N,N}^{-1},  D_p = C_pp - A_p C_{N,p}   (residual covariance C as in vif_factor,
  *   C_pp = sigma_1^2 + sigma^2 - |u_p|^2: the response; the latent b_p has var_p - sigma^2).
- * vif_predict runs vif_factor + vif_nll at theta, then the prediction features (kx_eval + triangular
+ * vif_predict validates the prediction inputs (finite Xp; nbrp rows of distinct indices in [0, n),
+ * -1 only trailing: INVALID_ARG naming the row), runs vif_factor + vif_nll at theta, then the
+ * prediction features (kx_eval + triangular
  * GEMM), the per-point Vecchia rows of the prediction points against the training rows (the factor's
  * kernel), e_p M_w^{-1} e_p by one triangular GEMM with L_M^{-1}, and mu / var; synchronises.
  * Xp: np x d (device or host), nbrp: np x m_v training indices in [0, n), -1 only as trailing pad
@@ -174,7 +185,7 @@ int vif_grad(void* handle, const vif_theta* theta, void* grad_workspace, size_t 
  * mu (device, np, required); var, Dp (device, np, optional); Bp (device, np x m_v, optional: -A_p).
  * Multi-rank: every rank passes all np inputs and full-length outputs; rank g predicts the contiguous
  * slice [g ceil(np/G), (g+1) ceil(np/G)) and writes only that slice (as vif_factor's B_out / D_out).
- * Errors: INVALID_ARG (np < 1, NULL), NO_MEMORY (workspace), NOT_PD (training factor, or a
+ * Errors: INVALID_ARG (np < 1, NULL, invalid Xp / nbrp), NO_MEMORY (workspace), NOT_PD (training factor, or a
  * prediction block: the message names the prediction row), CUDA. */
 int vif_predict_workspace_bytes(const vif_dims* dims, int64_t np, size_t* bytes);
 int vif_predict(void* handle, const vif_theta* theta, int64_t np, const double* Xp, const int32_t* nbrp,
@@ -246,8 +257,9 @@ int vif_la_prepare(void* handle, const vif_theta* theta, int32_t nprobe, int32_t
  * VIF_LA_BTINV B^{-T} v;  VIF_LA_FITC_SOLVE P^{-1} v;  VIF_LA_SIGMA_INV Sigma_dagger^{-1} v and
  * VIF_LA_A1 (W + Sigma_dagger^{-1}) v, the operator of (pcls1), by Woodbury with the latent
  * factor: B^T D^{-1/2} [s - W_U M^{-1} W_U^T s], s = D^{-1/2} B v (sparse products, no solves).
- * winv (device, n): W^{-1}, required by A, A1 and FITC_SOLVE.  The triangular solves are sync-free (one warp per row, rows claimed in dependency order,
- * release/acquire flags).  Synchronises.  Errors: INVALID_ARG, STATE, NOT_PD (M_V), CUDA. */
+ * winv (device, n): W^{-1}, required by A, A1 and FITC_SOLVE.  The triangular solves are
+ * level-scheduled (dependency levels of B / B^T from vif_la_prepare, one grid barrier per level).
+ * Synchronises.  Errors: INVALID_ARG, STATE, NOT_PD (M_V), CUDA. */
 int vif_la_apply(void* handle, void* workspace, int32_t op, int32_t ncol, const double* v, const double* winv,
                  double* out);
 /* Mode, quadratic term and (with opts.nprobe > 0) the SLQ log-determinant and L^VIFLA.  y: device, n

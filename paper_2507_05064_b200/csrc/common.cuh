@@ -12,6 +12,9 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <mutex>
+#include <unordered_map>
+
 #ifndef VIF_MAX_D
 #define VIF_MAX_D 16
 #endif
@@ -196,6 +199,30 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
       "}\n" ::"r"(smem_u32(bar)),
       "r"(parity)
       : "memory");
+}
+
+// Opt `fn` into `bytes` of dynamic shared memory (host).  The attribute belongs to the function
+// (per device), so the record is keyed on (device, function pointer) -- never a static per call
+// site, which would be shared by every kernel a templated launcher passes through it.  Below 40 KB
+// nothing is needed (48 KB default minus the static arrays the kernels declare).
+inline cudaError_t smem_optin(const void* fn, size_t bytes) {
+  if (bytes <= 40 * 1024) return cudaSuccess;
+  static std::mutex mu;
+  static std::unordered_map<uint64_t, size_t> done;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  const uint64_t key = reinterpret_cast<uint64_t>(fn) ^ ((uint64_t)dev << 56);
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = done.find(key);
+  if (it != done.end() && it->second >= bytes) return cudaSuccess;
+  e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e == cudaSuccess) done[key] = bytes;
+  return e;
+}
+template <typename K>
+inline cudaError_t smem_optin(K* fn, size_t bytes) {
+  return smem_optin(reinterpret_cast<const void*>(fn), bytes);
 }
 
 // Device-side status shared by all kernels of one evaluation.

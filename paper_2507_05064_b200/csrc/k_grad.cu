@@ -95,24 +95,6 @@ __global__ void phi_low_kernel(const double* __restrict__ Phi, int mk, double* _
   out[e] = b < a ? Phi[e] : (b == a ? 0.5 * Phi[e] : 0.0);
 }
 
-// S[pos][b] = dk(x_pos, z_b)/dtheta_p (single rank: row i = pos), zero for b in [m, mk)
-template <int FAM>
-__global__ void __launch_bounds__(256) kx_deriv_kernel(const double* __restrict__ X, const double* __restrict__ Z,
-                                                       int64_t npos, int m, int mk, int pidx, CovParams p,
-                                                       double* __restrict__ S) {
-  extern __shared__ double zs[];  // m x d
-  __shared__ double xrow[8][VIF_MAX_D];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t pos = (int64_t)blockIdx.x * 8 + warp;
-  for (int e = threadIdx.x; e < m * p.d; e += blockDim.x) zs[e] = Z[e];
-  if (lane < p.d) xrow[warp][lane] = pos < npos ? X[pos * p.d + lane] : 0.0;
-  __syncthreads();
-  if (pos >= npos) return;
-  double* srow = S + pos * (int64_t)mk;
-#pragma unroll 4
-  for (int b = lane; b < mk; b += 32) srow[b] = b < m ? dcov<FAM>(xrow[warp], zs + b * p.d, pidx, p) : 0.0;
-}
-
 // zh = Linv g (g = G[ycol][0..m)), Linv lower (ld ldi)
 __global__ void zhalf_kernel(const double* __restrict__ Linv, int ldi, const double* __restrict__ G, int ldg,
                              int ycol, int m, double* __restrict__ zh) {
@@ -173,10 +155,6 @@ constexpr int GW = 4;  // warps (points) per block
 template <int RB>
 __host__ __device__ constexpr int grad_warp_doubles(int d) {
   return 2 * (RB * 8) * (RB * 8 + 1) + 3 * (RB * 8) + RB * 8 * d;  // C, dC (or X), abuf, gam, gamd, xs
-}
-template <int RB>
-__host__ __device__ constexpr int param_warp_doubles(int d) {
-  return (RB * 8) * (RB * 8 + 1) + 3 * (RB * 8) + RB * 8 * d;  // dC, abuf, gam, gamd, xs
 }
 // per-point state of pass 0, by position: L (packed lower, SP rows incl. the identity padding), A_i,
 // 1/L_jj, g_i . U_aug[S_k], D_i, ok
@@ -508,179 +486,6 @@ __global__ void __launch_bounds__(GW * 32) grad_state_big_kernel(
   if (lane == 0) {
     st[LP + 3 * SP] = Di;
     st[LP + 3 * SP + 1] = ok ? 1.0 : 0.0;
-  }
-}
-
-// ---- pass per parameter: cross-Gram X = dU_S U_S^T (all RB^2 tiles), g_i . dU_aug[S_k], dC_S,
-// dA_i, dD_i and the point's contribution, with L, A_i, D_i, g_i . U_aug[S_k] from the state ----
-template <int FAM, int RB>
-__global__ void __launch_bounds__(GW * 32, 4) grad_param_kernel(
-    const double* __restrict__ U, const double* __restrict__ dU, const double* __restrict__ Gam, int64_t ldu, int mk,
-    int ld, const double* __restrict__ X, const int32_t* __restrict__ nbr, int mv, const int64_t* __restrict__ order,
-    int64_t npts, CovParams p, int pidx, const double* __restrict__ state, double* __restrict__ part) {
-  constexpr int SP = RB * 8;
-  constexpr int CS = SP + 1;
-  extern __shared__ __align__(16) double gsm_[];
-  __shared__ int Sidx_all[GW][SP];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  double* dC = gsm_ + warp * param_warp_doubles<RB>(p.d);  // L comes from the state (global, L1)
-  double* abuf = dC + SP * CS;
-  double* gam_s = abuf + SP;
-  double* gamd_s = gam_s + SP;
-  double* xs = gamd_s + SP;
-  int* Sidx = Sidx_all[warp];
-  const int64_t pos = (int64_t)blockIdx.x * GW + warp;
-  constexpr int LP = SP * (SP + 1) / 2;
-  __shared__ double wsum[GW];
-  __shared__ double tbl[64];
-  exp_table_init(tbl, p.sigma2, threadIdx.x);
-  __syncthreads();
-  double contrib = 0.0;
-  if (pos < npts) {
-    const int64_t i = order[pos];
-    const int nb0 = lane < mv ? nbr[i * mv + lane] : -1;
-    const int q = __popc(__ballot_sync(0xffffffffu, nb0 >= 0));
-    const int s = q + 1;
-    const int myidx = lane < q ? nb0 : (lane == q ? (int)i : -1);
-    if (lane < SP) Sidx[lane] = myidx;
-    if (lane < s)
-      for (int k = 0; k < p.d; ++k) xs[lane * p.d + k] = X[(int64_t)myidx * p.d + k] * (fam_scale<FAM>() * p.inv_ls[k]);
-    if (lane < SP) gamd_s[lane] = 0.0;
-    __syncwarp();
-    if (dU) {
-      // symmetric cross-Gram dG = dU_S U_S^T + U_S dU_S^T on the RB(RB+1)/2 lower tiles (two DMMAs per
-      // tile and k-step) and the g_i . dU_aug dots; loads of chunk k + 8 are issued before the DMMAs of
-      // chunk k (two register stages)
-      constexpr int NT = RB * (RB + 1) / 2;
-      double dacc[NT][2], gmd[RB];
-#pragma unroll
-      for (int t = 0; t < NT; ++t) dacc[t][0] = dacc[t][1] = 0.0;
-#pragma unroll
-      for (int R = 0; R < RB; ++R) gmd[R] = 0.0;
-      const double* rp[RB];
-      const double* drp[RB];
-#pragma unroll
-      for (int R = 0; R < RB; ++R) {
-        const int gi = Sidx[R * 8 + (lane >> 2)];
-        rp[R] = gi >= 0 ? U + (int64_t)gi * ldu + 2 * (lane & 3) : nullptr;
-        drp[R] = gi >= 0 ? dU + (int64_t)gi * ldu + 2 * (lane & 3) : nullptr;
-      }
-      const double* grow = Gam + pos * (int64_t)ld + 2 * (lane & 3);
-      double2 f[RB], df[RB], g2;
-      auto load = [&](int k0, double2 (&ff)[RB], double2 (&dff)[RB], double2& gg) {
-        gg = k0 < ld ? __ldg(reinterpret_cast<const double2*>(grow + k0)) : make_double2(0.0, 0.0);
-#pragma unroll
-        for (int R = 0; R < RB; ++R) {
-          ff[R] = (rp[R] && k0 < ld) ? __ldg(reinterpret_cast<const double2*>(rp[R] + k0)) : make_double2(0.0, 0.0);
-          dff[R] = (drp[R] && k0 < ld) ? __ldg(reinterpret_cast<const double2*>(drp[R] + k0)) : make_double2(0.0, 0.0);
-        }
-      };
-      load(0, f, df, g2);
-      for (int k0 = 0; k0 < ld; k0 += 8) {
-        double2 fn[RB], dfn[RB], gn;
-        load(k0 + 8, fn, dfn, gn);
-#pragma unroll
-        for (int R = 0; R < RB; ++R) gmd[R] = fma(df[R].x, g2.x, fma(df[R].y, g2.y, gmd[R]));
-        if (k0 < mk) {
-          int t = 0;
-#pragma unroll
-          for (int R1 = 0; R1 < RB; ++R1)
-#pragma unroll
-            for (int R2 = 0; R2 <= R1; ++R2, ++t) {
-              dmma884(dacc[t][0], dacc[t][1], df[R1].x, f[R2].x);
-              dmma884(dacc[t][0], dacc[t][1], df[R1].y, f[R2].y);
-              dmma884(dacc[t][0], dacc[t][1], f[R1].x, df[R2].x);
-              dmma884(dacc[t][0], dacc[t][1], f[R1].y, df[R2].y);
-            }
-        }
-#pragma unroll
-        for (int R = 0; R < RB; ++R) {
-          f[R] = fn[R];
-          df[R] = dfn[R];
-        }
-        g2 = gn;
-      }
-#pragma unroll
-      for (int R = 0; R < RB; ++R) {
-        gmd[R] += __shfl_xor_sync(0xffffffffu, gmd[R], 1);
-        gmd[R] += __shfl_xor_sync(0xffffffffu, gmd[R], 2);
-        if ((lane & 3) == 0) gamd_s[R * 8 + (lane >> 2)] = gmd[R];
-      }
-      // dG lower tiles into dC
-      int t = 0;
-#pragma unroll
-      for (int R1 = 0; R1 < RB; ++R1)
-#pragma unroll
-        for (int R2 = 0; R2 <= R1; ++R2, ++t) {
-          const int r = R1 * 8 + (lane >> 2), c = R2 * 8 + 2 * (lane & 3);
-          dC[r * CS + c] = dacc[t][0];
-          dC[r * CS + c + 1] = dacc[t][1];
-        }
-    }
-    __syncwarp();
-    // dC_S (lower) = dK + [nugget] I - dG
-    const int ne = s * (s + 1) / 2;
-    for (int e = lane; e < ne; e += 32) {
-      int r = (int)((sqrtf_fast(8.0f * (float)e + 1.0f) - 1.0f) * 0.5f);
-      if ((r + 1) * (r + 2) / 2 <= e) ++r;
-      if (r * (r + 1) / 2 > e) --r;
-      const int c = e - r * (r + 1) / 2;
-      double v = pidx <= p.d ? dcov_fast<FAM>(xs + r * p.d, xs + c * p.d, pidx, p, tbl) : 0.0;
-      if (dU) v -= dC[r * CS + c];
-      if (r == c && pidx == p.d + 1) v += 1.0;
-      dC[r * CS + c] = v;
-    }
-    __syncwarp();
-    // state: A, 1/L_jj, gam, D, ok; rows of L are read from it directly (packed lower)
-    const double* st = state + pos * (int64_t)state_doubles<RB>();
-    const double a = lane < SP ? st[LP + lane] : 0.0;
-    const double myinv = lane < SP ? st[LP + SP + lane] : 1.0;
-    if (lane < SP) gam_s[lane] = st[LP + 2 * SP + lane];
-    const double Di = st[LP + 3 * SP];
-    const bool ok = st[LP + 3 * SP + 1] != 0.0;
-    if (lane < SP) abuf[lane] = a;
-    __syncwarp();
-    double crow[SP];
-#pragma unroll
-    for (int c = 0; c < SP; ++c) crow[c] = (lane < SP && c <= lane) ? st[lane * (lane + 1) / 2 + c] : 0.0;
-    // u = dC_NN A^T, b = dC_Ni - u, dD_i
-    double u = 0.0;
-    if (lane < q)
-      for (int c = 0; c < q; ++c) u = fma(dC[c <= lane ? lane * CS + c : c * CS + lane], abuf[c], u);
-    double bv = lane < q ? dC[q * CS + lane] - u : 0.0;
-    double dterm = lane < q ? fma(-2.0 * a, dC[q * CS + lane], a * u) : 0.0;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) dterm += __shfl_xor_sync(0xffffffffu, dterm, o);
-    const double dD = dC[q * CS + q] + dterm;
-#pragma unroll
-    for (int j = 0; j < SP; ++j) {
-      if (j < q) {
-        const double zj = __shfl_sync(0xffffffffu, bv * myinv, j);
-        if (lane == j) bv = zj;
-        else if (lane > j) bv = fma(-crow[j], zj, bv);
-      }
-    }
-    for (int j = q - 1; j >= 0; --j) {
-      const double xj = __shfl_sync(0xffffffffu, bv * myinv, j);
-      if (lane == j) bv = xj;
-      else if (lane < j) bv = fma(-st[j * (j + 1) / 2 + lane], xj, bv);
-    }
-    const double da = lane < q ? bv : 0.0;
-    const double rs = rsqrt_nr(Di);
-    const double hD = 0.5 * dD / Di;
-    const double ck = lane < q ? -a * rs : (lane == q ? rs : 0.0);
-    const double dck = (lane < q ? -da * rs : 0.0) - ck * hD;
-    double cl = lane <= q ? fma(dck, gam_s[lane], ck * gamd_s[lane]) : 0.0;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) cl += __shfl_xor_sync(0xffffffffu, cl, o);
-    contrib = ok ? hD + cl : __longlong_as_double(0x7ff8000000000000LL);
-  }
-  if (lane == 0) wsum[warp] = contrib;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double sum = 0.0;
-    for (int w = 0; w < GW; ++w) sum += wsum[w];
-    part[blockIdx.x] = sum;
   }
 }
 
@@ -1151,46 +956,34 @@ __global__ void __launch_bounds__(1024) gfinal_kernel(double* __restrict__ out, 
 }
 
 template <int FAM, int RB>
-cudaError_t launch_grad_rb(const GradPointArgs& a, bool state_pass, cudaStream_t s) {
+cudaError_t launch_grad_rb(const GradPointArgs& a, cudaStream_t s) {
   const size_t smem = (size_t)GW * grad_warp_doubles<RB>(a.p.d) * sizeof(double);
   const unsigned blocks = (unsigned)((a.npts + GW - 1) / GW);
-  if (state_pass) {
-    if (smem > 40 * 1024) {  // dynamic + the kernels' static shared memory may pass 48 KB
-      cudaError_t e = cudaFuncSetAttribute(grad_state_kernel<FAM, RB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           (int)smem);
-      if (e != cudaSuccess) return e;
-    }
-    grad_state_kernel<FAM, RB><<<blocks, GW * 32, smem, s>>>(a.U, a.Gam, a.ldu, a.mk, a.ld, a.X, a.nbr, a.mv,
-                                                             a.order, a.npts, a.p, a.state);
-  } else {
-    const size_t psmem = (size_t)GW * param_warp_doubles<RB>(a.p.d) * sizeof(double);
-    if (psmem > 40 * 1024) {
-      cudaError_t e = cudaFuncSetAttribute(grad_param_kernel<FAM, RB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           (int)psmem);
-      if (e != cudaSuccess) return e;
-    }
-    grad_param_kernel<FAM, RB><<<blocks, GW * 32, psmem, s>>>(a.U, a.dU, a.Gam, a.ldu, a.mk, a.ld, a.X, a.nbr, a.mv,
-                                                             a.order, a.npts, a.p, a.pidx, a.state, a.part);
+  {
+    cudaError_t e = smem_optin(grad_state_kernel<FAM, RB>, smem);  // + the kernel's static shared memory
+    if (e != cudaSuccess) return e;
   }
+  grad_state_kernel<FAM, RB><<<blocks, GW * 32, smem, s>>>(a.U, a.Gam, a.ldu, a.mk, a.ld, a.X, a.nbr, a.mv,
+                                                           a.order, a.npts, a.p, a.state);
   return cudaGetLastError();
 }
 
 template <int FAM>
-cudaError_t launch_grad_fam(const GradPointArgs& a, bool state_pass, cudaStream_t s) {
+cudaError_t launch_grad_fam(const GradPointArgs& a, cudaStream_t s) {
   switch ((a.mv + 1 + 7) / 8) {
-    case 1: return launch_grad_rb<FAM, 1>(a, state_pass, s);
-    case 2: return launch_grad_rb<FAM, 2>(a, state_pass, s);
-    case 3: return launch_grad_rb<FAM, 3>(a, state_pass, s);
-    default: return launch_grad_rb<FAM, 4>(a, state_pass, s);
+    case 1: return launch_grad_rb<FAM, 1>(a, s);
+    case 2: return launch_grad_rb<FAM, 2>(a, s);
+    case 3: return launch_grad_rb<FAM, 3>(a, s);
+    default: return launch_grad_rb<FAM, 4>(a, s);
   }
 }
 
-cudaError_t launch_grad_any(const GradPointArgs& a, bool state_pass, cudaStream_t s) {
+cudaError_t launch_grad_any(const GradPointArgs& a, cudaStream_t s) {
   switch (a.p.family) {
-    case FAM_M12: return launch_grad_fam<FAM_M12>(a, state_pass, s);
-    case FAM_M32: return launch_grad_fam<FAM_M32>(a, state_pass, s);
-    case FAM_M52: return launch_grad_fam<FAM_M52>(a, state_pass, s);
-    default: return launch_grad_fam<FAM_GAUSS>(a, state_pass, s);
+    case FAM_M12: return launch_grad_fam<FAM_M12>(a, s);
+    case FAM_M32: return launch_grad_fam<FAM_M32>(a, s);
+    case FAM_M52: return launch_grad_fam<FAM_M52>(a, s);
+    default: return launch_grad_fam<FAM_GAUSS>(a, s);
   }
 }
 
@@ -1316,17 +1109,7 @@ cudaError_t launch_grad_state(const GradPointArgs& a, cudaStream_t s) {
     }
   }
   if (a.mv > 47) return cudaErrorNotSupported;
-  return a.npts > 0 ? launch_grad_any(a, true, s) : cudaSuccess;
-}
-
-cudaError_t launch_grad_points(const GradPointArgs& a, double* out, cudaStream_t s) {
-  if (a.mv > 31) return cudaErrorNotSupported;
-  if (a.npts > 0) {
-    cudaError_t e = launch_grad_any(a, false, s);
-    if (e != cudaSuccess) return e;
-  }
-  grad_reduce_kernel<<<1, 1024, 0, s>>>(a.part, grad_point_nparts(a.npts), out);
-  return cudaGetLastError();
+  return a.npts > 0 ? launch_grad_any(a, s) : cudaSuccess;
 }
 
 size_t grad_adj_doubles() { return ADJ_STRIDE; }
@@ -1404,11 +1187,9 @@ cudaError_t launch_gTdK(const double* X, const double* Z, int64_t n, int m, int 
   const int blocks = gTdK_blocks();
   const size_t zb = (size_t)m * p.d * sizeof(double);
   auto go = [&](auto kern) -> cudaError_t {
-    static size_t attr = 0;
-    if (zb > 40 * 1024 && attr < zb) {  // static shared memory comes on top
-      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)zb);
+    {
+      cudaError_t e = smem_optin(kern, zb);  // static shared memory comes on top
       if (e != cudaSuccess) return e;
-      attr = zb;
     }
     kern<<<blocks, 256, zb, s>>>(X, Z, n, m, mk, p, T, part);
     return cudaSuccess;
@@ -1462,29 +1243,6 @@ cudaError_t launch_phi_low(const double* Phi, int mk, double* out, cudaStream_t 
   const int64_t tot = (int64_t)mk * mk;
   phi_low_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(Phi, mk, out);
   return cudaGetLastError();
-}
-
-cudaError_t launch_kx_deriv(const double* X, const double* Z, int64_t npos, int m, int mk, int pidx,
-                            const CovParams& p, double* S, cudaStream_t s) {
-  if (npos == 0) return cudaSuccess;
-  const unsigned blocks = (unsigned)((npos + 7) / 8);
-  const size_t zbytes = (size_t)m * p.d * sizeof(double);
-  auto go = [&](auto kern) -> cudaError_t {
-    static size_t attr = 0;
-    if (zbytes > 40 * 1024 && attr < zbytes) {
-      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)zbytes);
-      if (e != cudaSuccess) return e;
-      attr = zbytes;
-    }
-    kern<<<blocks, 256, zbytes, s>>>(X, Z, npos, m, mk, pidx, p, S);
-    return cudaGetLastError();
-  };
-  switch (p.family) {
-    case FAM_M12: return go(kx_deriv_kernel<FAM_M12>);
-    case FAM_M32: return go(kx_deriv_kernel<FAM_M32>);
-    case FAM_M52: return go(kx_deriv_kernel<FAM_M52>);
-    default: return go(kx_deriv_kernel<FAM_GAUSS>);
-  }
 }
 
 // Prediction (Prop. 1; App. C.1): for the prediction row [w_p, r_p] (computed with y_p = 0,

@@ -4,18 +4,17 @@
 // point index (the Vecchia order).  The latent factor B (unit lower triangular, B[i, N(i)] = -A_i),
 // D and the whitened U come from the VIF factor with the error variance removed.
 //
-//   la_trsv_fwd   x = B^{-1} (s o v)        sync-free forward substitution: warp w takes rows
-//                                           w, w + W, ... in order, waits (flag polls) on the
-//                                           ready flags of its m_v neighbours, gathers them, and
-//                                           publishes its row with a release store of the flag;
-//   la_trsv_bwd   y = B^{-T} u              the same on the transposed structure (children lists),
-//                                           rows taken in decreasing order;
+//   la_level_*    dependency levels of B / B^T (once per neighbour structure): sync-free, warp w
+//                 takes rows w, w + W, ... in order, waits (flag polls) on the ready flags of the
+//                 rows it depends on and publishes its own with a release store;
+//   la_trsv_lvl   x = B^{-1} (s o v), y = B^{-T} u: level-scheduled cooperative solves (one grid
+//                 barrier per level, rows bucketed and their entries stored in level order);
 //   la_tsgemm     C = U^T diag(rs) V        tall-skinny split-row contraction (m x ncol), two-stage
 //                                           deterministic reduction;
 //   la_coldot ... per-column dot products (two-stage, fixed order), CG vector updates, FITC rows,
 //                 the Newton step and the SLQ quadrature e_1^T log(T) e_1 (implicit QL on T).
 //
-// Static row assignment over resident warps makes the schedule deadlock-free: the smallest
+// Static row assignment over resident warps makes the level pass deadlock-free: the smallest
 // unfinished row (in solve order) always has its dependencies done.
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
@@ -110,36 +109,14 @@ __global__ void la_sort_kernel(int64_t n, const int* __restrict__ ptr, int* __re
   }
 }
 
-// ------------------------------------------------------------------ sync-free triangular solves
-// Warp w of W resident warps solves rows w, w + W, w + 2W, ... in that order (static assignment: the
-// smallest unfinished row always has its dependencies done, so every resident warp makes progress).
-// A row waits (relaxed polls with back-off, see ld_relaxed) on the ready flags of the rows it reads, reads them from L2
-// (__ldcg: L1 is not coherent), and publishes its own row with a release store of its flag.
+// ------------------------------------------------------------------ flag waits (level pass)
+// A row waits (relaxed polls with back-off, see ld_relaxed) on the ready flags of the rows it depends on.
 __device__ __forceinline__ void la_wait(const int* f, int epoch) {
   if (ld_relaxed(f) == epoch) return;
   unsigned ns = 8;
   while (ld_relaxed(f) != epoch) {
     __nanosleep(ns);
     ns = ns < 256 ? 2 * ns : 256;
-  }
-}
-
-// acc{0,1} += sum_{k in [k0, k1)} val[k] * x[col[k], c{0,1}] (col < 0 skipped): lane = column; the
-// entry (col, val) is a broadcast load (every lane reads the same address).  The body is branch-free
-// (a skipped entry reads row 0 with weight 0, a lane past ncol reads column ncol - 1 and discards
-// it) so that the unrolled loop keeps 16 gathers per column in flight.
-__device__ __forceinline__ void la_gather_cols(const double* x, int ncol, int c0, const int32_t* __restrict__ col,
-                                               const double* __restrict__ val, int k0, int k1, double& acc0,
-                                               double& acc1) {
-  const int c1 = c0 + 32;
-  const int r0 = c0 < ncol ? c0 : ncol - 1, r1 = c1 < ncol ? c1 : ncol - 1;
-#pragma unroll 16
-  for (int k = k0; k < k1; ++k) {
-    const int j = col[k];
-    const double b = j >= 0 ? val[k] : 0.0;
-    const double* xr = x + (int64_t)(j >= 0 ? j : 0) * ncol;
-    acc0 = fma(b, __ldcg(xr + r0), acc0);
-    acc1 = fma(b, __ldcg(xr + r1), acc1);
   }
 }
 
@@ -169,100 +146,6 @@ __device__ __forceinline__ void la_gather_cols_weak(const double* x, int ncol, i
   for (int q = 0; q < 32; ++q) {
     acc0 = fma(bb[q], x0[q], acc0);
     acc1 = fma(bb[q], x1[q], acc1);
-  }
-}
-
-// x_i = s_i v_i - sum_p B[i,p] x_{N(i)_p}   (B x = s o v, B unit lower triangular)
-// optional out2_i = x_i + w2_i * v2_i (the W^{-1} p term of (W^{-1} + Sigma_dagger) p is added there)
-// ncol <= 64 (two columns per lane)
-__global__ void __launch_bounds__(LA_THREADS) la_trsv_fwd_kernel(
-    const int32_t* __restrict__ nbr, const double* __restrict__ Bc, int mv, int64_t n, int ncol,
-    const double* __restrict__ v, const double* __restrict__ s, double* x, const double* __restrict__ v2,
-    const double* __restrict__ w2, double* __restrict__ out2, int* flags, int epoch) {
-  const int lane = threadIdx.x & 31;
-  const int64_t nw = (int64_t)gridDim.x * LA_WARPS;
-  for (int64_t i = (int64_t)blockIdx.x * LA_WARPS + (threadIdx.x >> 5); i < n; i += nw) {
-    const int32_t* nb = nbr + i * mv;
-    const double* bi = Bc + i * mv;
-    const double si = s ? s[i] : 1.0;
-    if (ncol == 1) {
-      double acc = 0.0;
-      for (int p = lane; p < mv; p += 32) {
-        const int j = nb[p];
-        if (j >= 0) {
-          la_wait(flags + j, epoch);
-          acc = fma(bi[p], __ldcg(x + j), acc);
-        }
-      }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-      if (lane == 0) {
-        const double xi = si * v[i] - acc;
-        __stcg(x + i, xi);
-        if (out2) out2[i] = xi + w2[i] * v2[i];
-        st_release(flags + i, epoch);  // orders lane 0's own store of x_i before the flag
-      }
-    } else {
-      double acc0 = 0.0, acc1 = 0.0;
-      for (int p = lane; p < mv; p += 32) {
-        const int j = nb[p];
-        if (j >= 0) la_wait(flags + j, epoch);
-      }
-      __syncwarp();
-      la_gather_cols(x, ncol, lane, nb, bi, 0, mv, acc0, acc1);
-      const int c1 = lane + 32;
-      if (lane < ncol) {
-        const double xi = si * v[i * ncol + lane] - acc0;
-        __stcg(x + i * ncol + lane, xi);
-        if (out2) out2[i * ncol + lane] = xi + w2[i] * v2[i * ncol + lane];
-      }
-      if (c1 < ncol) {
-        const double xi = si * v[i * ncol + c1] - acc1;
-        __stcg(x + i * ncol + c1, xi);
-        if (out2) out2[i * ncol + c1] = xi + w2[i] * v2[i * ncol + c1];
-      }
-      // __syncwarp orders the other lanes' stores before lane 0's release store (bar.warp.sync carries
-      // memory ordering among the participating threads; release is cumulative)
-      __syncwarp();
-      if (lane == 0) st_release(flags + i, epoch);
-    }
-  }
-}
-
-// y_j = u_j - sum_{k in children(j)} tval[k] y_{trow[k]}   (B^T y = u; tval[k] = B[trow[k], p] with
-// N(trow[k])_p = j), rows in decreasing order
-__global__ void __launch_bounds__(LA_THREADS) la_trsv_bwd_kernel(
-    const int* __restrict__ tptr, const int* __restrict__ trow, const double* __restrict__ tval, int64_t n,
-    int ncol, const double* __restrict__ u, double* y, int* flags, int epoch) {
-  const int lane = threadIdx.x & 31;
-  const int64_t nw = (int64_t)gridDim.x * LA_WARPS;
-  for (int64_t t = (int64_t)blockIdx.x * LA_WARPS + (threadIdx.x >> 5); t < n; t += nw) {
-    const int64_t j = n - 1 - t;
-    const int a = tptr[j], b = tptr[j + 1];
-    if (ncol == 1) {
-      double acc = 0.0;
-      for (int k = a + lane; k < b; k += 32) {
-        const int i = trow[k];
-        la_wait(flags + i, epoch);
-        acc = fma(tval[k], __ldcg(y + i), acc);
-      }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-      if (lane == 0) {
-        __stcg(y + j, u[j] - acc);
-        st_release(flags + j, epoch);
-      }
-    } else {
-      double acc0 = 0.0, acc1 = 0.0;
-      for (int k = a + lane; k < b; k += 32) la_wait(flags + trow[k], epoch);
-      __syncwarp();
-      la_gather_cols(y, ncol, lane, trow, tval, a, b, acc0, acc1);
-      const int c1 = lane + 32;
-      if (lane < ncol) __stcg(y + j * ncol + lane, u[j * ncol + lane] - acc0);
-      if (c1 < ncol) __stcg(y + j * ncol + c1, u[j * ncol + c1] - acc1);
-      __syncwarp();
-      if (lane == 0) st_release(flags + j, epoch);
-    }
   }
 }
 
@@ -1092,46 +975,6 @@ cudaError_t launch_la_transpose_struct(const int32_t* nbr, int64_t n, int mv, in
   return cudaGetLastError();
 }
 
-static int la_trsv_blocks(const void* fn) {
-  static int cached[2] = {0, 0};
-  const int idx = fn == (const void*)la_trsv_fwd_kernel ? 0 : 1;
-  if (!cached[idx]) {
-    int per_sm = 0, dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, LA_THREADS, 0);
-    // every warp must be resident (static assignment); VIF_LA_TRSV_BPS caps the blocks per SM
-    static const char* cap_env = getenv("VIF_LA_TRSV_BPS");
-    const int cap = cap_env ? atoi(cap_env) : 2;
-    if (per_sm < 1) per_sm = 1;
-    if (cap > 0 && per_sm > cap) per_sm = cap;
-    cached[idx] = sms * per_sm;
-  }
-  return cached[idx];
-}
-
-cudaError_t launch_la_trsv_fwd(const int32_t* nbr, const double* Bc, int mv, int64_t n, int ncol, const double* v,
-                               const double* scale, double* x, const double* v2, const double* w2, double* out2,
-                               int* flags, int epoch, cudaStream_t s) {
-  if (ncol > 64) return cudaErrorInvalidValue;
-  int64_t blocks = la_trsv_blocks((const void*)la_trsv_fwd_kernel);
-  const int64_t need = (n + LA_WARPS - 1) / LA_WARPS;
-  if (blocks > need) blocks = need;
-  la_trsv_fwd_kernel<<<(unsigned)blocks, LA_THREADS, 0, s>>>(nbr, Bc, mv, n, ncol, v, scale, x, v2, w2, out2, flags,
-                                                              epoch);
-  return cudaGetLastError();
-}
-
-cudaError_t launch_la_trsv_bwd(const int* tptr, const int* trow, const double* tval, int64_t n, int ncol,
-                               const double* u, double* y, int* flags, int epoch, cudaStream_t s) {
-  if (ncol > 64) return cudaErrorInvalidValue;
-  int64_t blocks = la_trsv_blocks((const void*)la_trsv_bwd_kernel);
-  const int64_t need = (n + LA_WARPS - 1) / LA_WARPS;
-  if (blocks > need) blocks = need;
-  la_trsv_bwd_kernel<<<(unsigned)blocks, LA_THREADS, 0, s>>>(tptr, trow, tval, n, ncol, u, y, flags, epoch);
-  return cudaGetLastError();
-}
-
 cudaError_t launch_la_tvals(const int* tpos, int64_t nnz, int mv, const double* Bc, int* trow, double* tval,
                             cudaStream_t s) {
   if (nnz == 0) return cudaSuccess;
@@ -1330,7 +1173,20 @@ cudaError_t launch_la_finish(const double* fin, const double* slq, int64_t n, in
 
 cudaError_t launch_la_levels(const int32_t* nbr, int mv, int64_t n, const int* tptr, const int* trow, int* lev_f,
                              int* lev_b, int* flags, int epoch_f, int epoch_b, int* nlev_dev, cudaStream_t s) {
-  int64_t blocks = la_trsv_blocks((const void*)la_trsv_fwd_kernel);
+  // static row assignment over resident warps (deadlock-free only if every warp is resident): at most
+  // the occupancy, capped at two blocks per SM
+  static int cached = 0;
+  if (!cached) {
+    int per_sm = 0, dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, la_level_fwd_kernel, LA_THREADS, 0);
+    int per_sm_b = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_b, la_level_bwd_kernel, LA_THREADS, 0);
+    per_sm = std::min(std::min(per_sm, per_sm_b), 2);
+    cached = sms * std::max(per_sm, 1);
+  }
+  int64_t blocks = cached;
   const int64_t need = (n + LA_WARPS - 1) / LA_WARPS;
   if (blocks > need) blocks = need;
   la_level_fwd_kernel<<<(unsigned)blocks, LA_THREADS, 0, s>>>(nbr, mv, n, lev_f, flags, epoch_f);

@@ -49,6 +49,36 @@ cudaError_t launch_validate(const double* X, int64_t n, int d, const double* Z, 
   return cudaGetLastError();
 }
 
+// prediction inputs (reading p1): finite coordinates; each neighbour row holds distinct training
+// indices in [0, ntrain), -1 only as trailing padding (the vecchia kernel counts the leading valid
+// entries and gathers them unchecked)
+__global__ void validate_pred_kernel(const double* __restrict__ Xp, int64_t np, int d, const int32_t* __restrict__ nbrp,
+                                     int mv, int64_t ntrain, DevStatus* st) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < np; i += (int64_t)gridDim.x * blockDim.x) {
+    bool bad = false;
+    for (int k = 0; k < d; ++k) bad |= !isfinite(Xp[i * d + k]);
+    const int32_t* row = nbrp + i * mv;
+    bool pad = false;
+    for (int k = 0; k < mv; ++k) {
+      const int32_t j = row[k];
+      if (j < 0) {
+        bad |= j != -1;
+        pad = true;
+      } else {
+        bad |= pad || j >= ntrain;
+        for (int t = 0; t < k; ++t) bad |= row[t] == j;
+      }
+    }
+    if (bad) atomicMin(&st->bad_input, (unsigned long long)i);
+  }
+}
+
+cudaError_t launch_validate_pred(const double* Xp, int64_t np, int d, const int32_t* nbrp, int mv, int64_t ntrain,
+                                 DevStatus* st, cudaStream_t s) {
+  validate_pred_kernel<<<296, 256, 0, s>>>(Xp, np, d, nbrp, mv, ntrain, st);
+  return cudaGetLastError();
+}
+
 __global__ void reset_status_kernel(DevStatus* st) {
   st->bad_row = ~0ULL;
   st->bad_input = ~0ULL;

@@ -164,11 +164,9 @@ cudaError_t launch_syrk(const double* W, int64_t ldw, int64_t nrows, int ncols, 
   const int nt = syrk_ntiles(ncols);
   const int64_t rps = nrows > 0 ? (nrows + nsplit - 1) / nsplit : 0;
   const size_t smem = (size_t)2 * SS * SK * SPAD * sizeof(double);
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(syrk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  {
+    cudaError_t e = smem_optin(syrk_kernel, smem);
     if (e != cudaSuccess) return e;
-    attr = true;
   }
   syrk_kernel<<<nt * nsplit, 128, smem, s>>>(W, ldw, nrows, ncols, nt, rps, Gpart);
   const int64_t tot = (int64_t)nt * ST * ST;
@@ -182,11 +180,9 @@ cudaError_t launch_syrk_part(const double* W, int64_t ldw, int64_t nrows, int nc
   const int nt = syrk_ntiles(ncols);
   const int64_t rps = nrows > 0 ? (nrows + nsplit - 1) / nsplit : 0;
   const size_t smem = (size_t)2 * SS * SK * SPAD * sizeof(double);
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(syrk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  {
+    cudaError_t e = smem_optin(syrk_kernel, smem);
     if (e != cudaSuccess) return e;
-    attr = true;
   }
   syrk_kernel<<<nt * nsplit, 128, smem, s>>>(W, ldw, nrows, ncols, nt, rps, Gpart);
   return cudaGetLastError();

@@ -252,11 +252,9 @@ cudaError_t launch_u_features(const double* X, const double* Z, const double* y,
   const int blocks = (int)((npos + 7) / 8);
   const size_t zbytes = (size_t)m * p.d * sizeof(double);
   auto go = [&](auto kern) -> cudaError_t {
-    static size_t attr = 0;  // one per instantiation of the generic lambda
-    if (zbytes > 40 * 1024 && attr < zbytes) {
-      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)zbytes);
+    {
+      cudaError_t e = smem_optin(kern, zbytes);
       if (e != cudaSuccess) return e;
-      attr = zbytes;
     }
     kern<<<blocks, 256, zbytes, s>>>(X, Z, y, n, npos, chunk, world, rank, pos0, m, mk, p, S + pos0 * lds, lds,
                                      Uaug, ld);
@@ -269,11 +267,9 @@ cudaError_t launch_u_features(const double* X, const double* Z, const double* y,
     const size_t zb = (size_t)mk * D * sizeof(double);
     int nb = (int)((npos + 7) / 8);
     if (nb > 148 * 8) nb = 148 * 8;
-    static size_t attr = 0;
-    if (zb > 40 * 1024 && attr < zb) {  // static shared memory comes on top
-      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)zb);
+    {
+      cudaError_t e = smem_optin(kern, zb);  // static shared memory comes on top
       if (e != cudaSuccess) return e;
-      attr = zb;
     }
     kern<<<nb, 256, zb, s>>>(X, Z, y, n, npos, chunk, world, rank, pos0, m, mk, p, S + pos0 * lds, lds, Uaug, ld);
     return cudaSuccess;
@@ -307,18 +303,9 @@ cudaError_t launch_u_features(const double* X, const double* Z, const double* y,
   if (e0 != cudaSuccess) return e0;
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess || mk == 0) return e;
-  // default: this file's 128x64 / 8-warp / 2-CTA kernel; VIF_GEMM128=1 selects the 128x128 engine
-  // of k_gemm.cu (measured slower on B200, profiles/r01_notes.md)
-  static const char* e128 = getenv("VIF_GEMM128");
-  if (e128 && e128[0] == '1')
-    return launch_gemm_tn_tri(S + pos0 * lds, lds, npos, Linv, mk, mk, Uaug, ld, n, chunk, world, rank, pos0, s);
   const size_t smem = (size_t)GST * (GBM + GBN) * GPAD * sizeof(double);
-  static bool attr_set = false;
-  if (!attr_set) {
-    e = cudaFuncSetAttribute(gemm_tn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    attr_set = true;
-  }
+  e = smem_optin(gemm_tn_kernel, smem);
+  if (e != cudaSuccess) return e;
   const unsigned grid = (unsigned)(((npos + GBM - 1) / GBM) * ((mk + GBN - 1) / GBN));
   gemm_tn_kernel<<<grid, 256, smem, s>>>(S + pos0 * lds, lds, npos, Linv, mk, mk, mk, 1, Uaug, ld, n, chunk, world, rank,
                                          pos0, 1.0, 0);
@@ -331,11 +318,9 @@ cudaError_t launch_gemm_tn(const double* A, int64_t lda, int64_t nrows, const do
                            int tri, double* C, int64_t ldc, double alpha, int accum, cudaStream_t s) {
   if (nrows == 0 || N == 0) return cudaSuccess;
   const size_t smem = (size_t)GST * (GBM + GBN) * GPAD * sizeof(double);
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(gemm_tn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  {
+    cudaError_t e = smem_optin(gemm_tn_kernel, smem);
     if (e != cudaSuccess) return e;
-    attr_set = true;
   }
   const unsigned grid = (unsigned)(((nrows + GBM - 1) / GBM) * ((N + GBN - 1) / GBN));
   gemm_tn_kernel<<<grid, 256, smem, s>>>(A, lda, nrows, B, ldb, N, K, tri, C, ldc, nrows, nrows, 1, 0, 0, alpha, accum);

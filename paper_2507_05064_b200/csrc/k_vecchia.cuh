@@ -626,21 +626,18 @@ template <int FAM, int RB>
 static cudaError_t launch_reg(const VecchiaArgs& a, cudaStream_t s) {
   const unsigned blocks = (unsigned)((a.npts + VW - 1) / VW);
   const size_t smem = (size_t)VW * vreg_warp_doubles<RB>(a.p.d) * sizeof(double);
-  // VIF_VREG_CFG = "<ring depth><min blocks/SM>" for A/B runs; default "34"
-  static const char* cfg_env = getenv("VIF_VREG_CFG");
-  const int cfg = cfg_env ? atoi(cfg_env) : 34;
+  // ring depth 3, 4 blocks (16 warps) per SM (measured: depth 2 / 5 blocks slower, profiles/r01_notes.md)
   decltype(&vecchia_reg_kernel<FAM, RB, 3, 4>) kern;
   if (a.Uself) {
     kern = vecchia_reg_kernel<FAM, RB, 3, 4, true>;
   } else {
-    static const char* gen_env = getenv("VIF_VECCHIA_GENERIC_D");
+    static const char* gen_env = getenv("VIF_VECCHIA_GENERIC_D");  // A/B: runtime-d loops at d = 2 too
     const int dd = (gen_env && gen_env[0] == '1') ? 0 : a.p.d;
-    if (cfg == 24) kern = vecchia_reg_kernel<FAM, RB, 2, 4>;
-    else if (dd == 2) kern = vecchia_reg_kernel<FAM, RB, 3, 4, false, 2>;
+    if (dd == 2) kern = vecchia_reg_kernel<FAM, RB, 3, 4, false, 2>;
     else kern = vecchia_reg_kernel<FAM, RB, 3, 4>;
   }
-  if (smem > 40 * 1024) {  // static shared memory comes on top
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  {
+    cudaError_t e = smem_optin(kern, smem);  // static shared memory comes on top
     if (e != cudaSuccess) return e;
   }
   {
@@ -660,14 +657,13 @@ static cudaError_t launch_reg(const VecchiaArgs& a, cudaStream_t s) {
 }
 
 template <int FAM, int RB>
-static cudaError_t launch_smem(const VecchiaArgs& a, cudaStream_t s, int minb4) {
+static cudaError_t launch_smem(const VecchiaArgs& a, cudaStream_t s) {
   const unsigned blocks = (unsigned)((a.npts + VW - 1) / VW);
   const size_t smem = (size_t)VW * vecchia_warp_doubles<RB>(a.p.d) * sizeof(double);
-  static const char* nb_env = getenv("VIF_SMEM_NB");  // A/B hook: Gram ring depth 1 or 2
-  auto kern = (nb_env && nb_env[0] == '2') ? vecchia_smem_kernel<FAM, RB, 2> : vecchia_smem_kernel<FAM, RB, 1>;
-  if (minb4) kern = vecchia_smem_kernel<FAM, RB, 1, 4>;
+  // Gram ring depth 1 (a 2-deep ring measured slower at 12 warps/SM, profiles/r01_notes.md)
+  auto kern = vecchia_smem_kernel<FAM, RB, 1>;
   {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = smem_optin(kern, smem);
     if (e != cudaSuccess) return e;
   }
   kern<<<blocks, VW * 32, smem, s>>>(a.U, a.ldu, a.mk, a.ld, a.X, a.Uself ? a.Uself : a.U,
@@ -682,12 +678,10 @@ static cudaError_t launch_rb(const VecchiaArgs& a, cudaStream_t s) {
   // s <= 32: the per-warp register kernel.  Measured and rejected on B200 (profiles/r01_notes.md):
   // warp-specialised Gram / solver warps (register ring or cp.async shared-memory ring) and a
   // mixed-precision (FP32 Cholesky + FP64 refinement) solver.
-  static const char* blk_env = getenv("VIF_VECCHIA_BLOCKED");  // A/B: blocked DMMA Cholesky for s <= 32 too
-  const int blk = blk_env ? atoi(blk_env) : 0;
-  if constexpr (RB <= 4) {
-    if (blk == 0) return launch_reg<FAM, RB>(a, s);
-  }
-  return launch_smem<FAM, RB>(a, s, blk == 4);
+  // (the blocked DMMA Cholesky of the s > 32 kernel measured slower for s <= 32: 9.8-10.5 vs 8.2 ms at
+  // n = 300k, profiles/r02_union_probe.json)
+  if constexpr (RB <= 4) return launch_reg<FAM, RB>(a, s);
+  else return launch_smem<FAM, RB>(a, s);
 }
 
 template <int FAM>

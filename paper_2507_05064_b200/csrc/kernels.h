@@ -64,15 +64,6 @@ cudaError_t launch_syrk_part(const double* W, int64_t ldw, int64_t nrows, int nc
                              cudaStream_t s);
 cudaError_t launch_syrk_reduce(const double* Gpart, int ntiles, int nsplit_total, int ncols, double* G, int ldg,
                                cudaStream_t s);
-// K1b / K4 on the 128x128 engine (k_gemm.cu)
-cudaError_t launch_gemm_tn_tri(const double* S, int64_t lds, int64_t npos, const double* Linv, int ldl, int N,
-                               double* U, int64_t ldu, int64_t n, int64_t chunk, int world, int rank,
-                               int64_t pos0, cudaStream_t s);
-int syrk_nt_ntiles(int ncols);
-int syrk_nt_nsplit(int ncols, int64_t nrows, int num_sms);
-size_t syrk_nt_part_doubles(int ncols, int nsplit);
-cudaError_t launch_syrk_nt(const double* W, int64_t ldw, int64_t nrows, int ncols, int nsplit, double* Gpart,
-                           double* G, int ldg, cudaStream_t s);
 // gradient (k_grad.cu)
 struct GradPointArgs {
   const double* U;
@@ -100,7 +91,6 @@ size_t grad_state_doubles(int mv);
 // the g_i . U_aug[S_k] slots of a state written by the factor (VecchiaArgs::state)
 cudaError_t launch_grad_gam(const GradPointArgs& a, cudaStream_t s);
 cudaError_t launch_grad_state(const GradPointArgs& a, cudaStream_t s);
-cudaError_t launch_grad_points(const GradPointArgs& a, double* out, cudaStream_t s);
 size_t grad_adj_doubles();
 cudaError_t launch_grad_adjoint(const GradPointArgs& a, cudaStream_t s);
 cudaError_t launch_grad_points_adj(const GradPointArgs& a, double* out, cudaStream_t s);
@@ -120,8 +110,6 @@ cudaError_t launch_la_tsgemm_ld(const double* U, int64_t ldu, int mk, int64_t n,
                                 int ncol, double* part, double* Ct, cudaStream_t s);
 cudaError_t launch_dkm(const double* Z, int m, int mk, int pidx, const CovParams& p, double* out, cudaStream_t s);
 cudaError_t launch_phi_low(const double* Phi, int mk, double* out, cudaStream_t s);
-cudaError_t launch_kx_deriv(const double* X, const double* Z, int64_t npos, int m, int mk, int pidx,
-                            const CovParams& p, double* S, cudaStream_t s);
 cudaError_t launch_grad_q(const double* LinvM, int ldi, const double* G, int ldg, int ycol, int m, int ld,
                           double* zh, double* z, double* Q2, cudaStream_t s);
 cudaError_t launch_gemm_tn(const double* A, int64_t lda, int64_t nrows, const double* B, int64_t ldb, int N, int K,
@@ -138,11 +126,6 @@ cudaError_t launch_knn(const double* U, int64_t ldu, int m, int mk, const double
 // VIF-Laplace iterative path (k_laplace.cu)
 cudaError_t launch_la_transpose_struct(const int32_t* nbr, int64_t n, int mv, int* cnt, int* cursor, int* tptr,
                                        int* tpos, cudaStream_t s);
-cudaError_t launch_la_trsv_fwd(const int32_t* nbr, const double* Bc, int mv, int64_t n, int ncol, const double* v,
-                               const double* scale, double* x, const double* v2, const double* w2, double* out2,
-                               int* flags, int epoch, cudaStream_t s);
-cudaError_t launch_la_trsv_bwd(const int* tptr, const int* trow, const double* tval, int64_t n, int ncol,
-                               const double* u, double* y, int* flags, int epoch, cudaStream_t s);
 cudaError_t launch_la_tvals(const int* tpos, int64_t nnz, int mv, const double* Bc, int* trow, double* tval,
                             cudaStream_t s);
 cudaError_t launch_la_levels(const int32_t* nbr, int mv, int64_t n, const int* tptr, const int* trow, int* lev_f,
@@ -204,6 +187,8 @@ cudaError_t launch_la_finish(const double* fin, const double* slq, int64_t n, in
 // misc
 cudaError_t launch_validate(const double* X, int64_t n, int d, const double* Z, int m, const double* y,
                             const int32_t* nbr, int mv, DevStatus* st, cudaStream_t s);
+cudaError_t launch_validate_pred(const double* Xp, int64_t np, int d, const int32_t* nbrp, int mv, int64_t ntrain,
+                                 DevStatus* st, cudaStream_t s);
 size_t order_temp_bytes(int64_t npos);
 cudaError_t launch_order(const double* X, int64_t n, int d, int64_t npos, int64_t chunk, int world, int rank,
                          double* bbox, uint64_t* keys, uint64_t* keys_alt, int64_t* vals, int64_t* vals_alt,

@@ -17,7 +17,9 @@
 #include <stdio.h>
 #include <string.h>
 
+#include <chrono>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/vif.h"
@@ -46,6 +48,8 @@ struct Nccl {
   ncclResult_t (*GroupStart)() = nullptr;
   ncclResult_t (*GroupEnd)() = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
+  ncclResult_t (*CommGetAsyncError)(ncclComm_t, ncclResult_t*) = nullptr;
+  ncclResult_t (*CommAbort)(ncclComm_t) = nullptr;
   bool ok = false;
 };
 
@@ -64,8 +68,10 @@ Nccl& nccl() {
       n.GroupStart = (decltype(n.GroupStart))dlsym(n.lib, "ncclGroupStart");
       n.GroupEnd = (decltype(n.GroupEnd))dlsym(n.lib, "ncclGroupEnd");
       n.GetErrorString = (decltype(n.GetErrorString))dlsym(n.lib, "ncclGetErrorString");
+      n.CommGetAsyncError = (decltype(n.CommGetAsyncError))dlsym(n.lib, "ncclCommGetAsyncError");
+      n.CommAbort = (decltype(n.CommAbort))dlsym(n.lib, "ncclCommAbort");
       n.ok = n.GetUniqueId && n.CommInitRank && n.AllGather && n.AllReduce && n.CommDestroy && n.GroupStart &&
-             n.GroupEnd && n.GetErrorString;
+             n.GroupEnd && n.GetErrorString && n.CommGetAsyncError && n.CommAbort;
     }
   }
   return n;
@@ -78,7 +84,7 @@ struct Plan {
   bool emulate;
   int mk, ycol, ld;
   int64_t rounds, chunk, npos, npad;
-  int nsplit, nsplit_old, nsplit_round;
+  int nsplit, nsplit_round;
   std::vector<int64_t> n_own;
 };
 
@@ -153,8 +159,7 @@ bool make_plan(const vif_dims* dims, bool emulate, Plan& P, std::string& err) {
       const int64_t cnt = P.n - start;
       P.n_own[g] += cnt <= 0 ? 0 : (cnt < P.chunk ? cnt : P.chunk);
     }
-  P.nsplit = syrk_nt_nsplit(P.ld, P.npos, kPlanSMs);
-  P.nsplit_old = syrk_nsplit(P.ld, P.npos, kPlanSMs);
+  P.nsplit = syrk_nsplit(P.ld, P.npos, kPlanSMs);
   P.nsplit_round = syrk_nsplit(P.ld, P.chunk, kPlanSMs);
   return true;
 }
@@ -178,7 +183,7 @@ Layout make_layout(const Plan& P) {
   L.size[B_ORDER] = (size_t)nrep * P.npos * sizeof(int64_t);
   L.size[B_KEYS] = L.size[B_KEYS2] = L.size[B_VALS] = L.size[B_VALS2] = (size_t)P.npos * 8;
   L.size[B_TEMP] = order_temp_bytes(P.npos);
-  L.size[B_GPART] = std::max(std::max(syrk_nt_part_doubles(P.ld, P.nsplit), syrk_part_doubles(P.ld, P.nsplit_old)),
+  L.size[B_GPART] = std::max(syrk_part_doubles(P.ld, P.nsplit),
                              (size_t)P.rounds * syrk_part_doubles(P.ld, P.nsplit_round)) * D8;
   L.size[B_G] = nrep * gsz;
   L.size[B_GSUM] = gsz;
@@ -221,6 +226,7 @@ struct Handle {
   cudaStream_t stream = nullptr;
   int num_sms = 148;
   ncclComm_t comm = nullptr;
+  bool comm_dead = false;                    // aborted after an asynchronous error / timeout
   cudaStream_t cstream = nullptr;            // communication stream (world > 1 with NCCL)
   std::vector<cudaEvent_t> ev_k1, ev_ag;     // per round: K1 done / all-gather done
   // single-GPU rounds: K1 and SYRK streams, round events (vecchia done), K0 / SYRK done
@@ -283,6 +289,49 @@ int cuda_fail(Handle* h, cudaError_t e, const char* where) {
     if (e_ != cudaSuccess) return cuda_fail(h, e_, where); \
   } while (0)
 
+// Wait for the work on `s`.  Without a communicator: cudaStreamSynchronize.  With one (world > 1), a
+// peer that died or hung would leave a collective on the stream forever, so the wait polls the stream
+// and ncclCommGetAsyncError, and gives up after VIF_NCCL_TIMEOUT_S seconds (default 600): the
+// communicator is aborted (its kernels exit, the stream drains) and the call returns VIF_ERR_NCCL;
+// the handle's later collective calls fail with VIF_ERR_NCCL too.
+int wait_stream(Handle* h, cudaStream_t s) {
+  if (!h->comm) {
+    if (h->comm_dead) return fail(h, VIF_ERR_NCCL, "the communicator was aborted by an earlier error");
+    VIF_CUDA(h, cudaStreamSynchronize(s), "sync");
+    return VIF_OK;
+  }
+  static const char* tenv = getenv("VIF_NCCL_TIMEOUT_S");
+  const double limit = tenv ? atof(tenv) : 600.0;
+  Nccl& N = nccl();
+  const auto t0 = std::chrono::steady_clock::now();
+  unsigned spin = 0;
+  for (;;) {
+    const cudaError_t q = cudaStreamQuery(s);
+    if (q == cudaSuccess) return VIF_OK;
+    if (q != cudaErrorNotReady) return cuda_fail(h, q, "sync");
+    ncclResult_t ar = ncclSuccess;
+    N.CommGetAsyncError(h->comm, &ar);
+    const double el = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    if ((ar != ncclSuccess && ar != ncclInProgress) || el > limit) {
+      std::string msg = ar != ncclSuccess && ar != ncclInProgress
+                            ? std::string("NCCL asynchronous error: ") + N.GetErrorString(ar)
+                            : std::string("NCCL collective did not complete within VIF_NCCL_TIMEOUT_S");
+      N.CommAbort(h->comm);
+      h->comm = nullptr;
+      h->comm_dead = true;
+      cudaStreamSynchronize(s);  // the aborted collectives return; the stream drains
+      return fail(h, VIF_ERR_NCCL, msg);
+    }
+    if (++spin > 64) std::this_thread::sleep_for(std::chrono::microseconds(20));
+  }
+}
+
+#define VIF_WAIT(h, s)                 \
+  do {                                 \
+    const int w_ = wait_stream(h, s);  \
+    if (w_ != VIF_OK) return w_;       \
+  } while (0)
+
 bool make_params(const Handle* h, const vif_theta* th, CovParams& p, std::string& err) {
   if (!th) { err = "theta is NULL"; return false; }
   if (th->d != h->P.d) { err = "theta.d != dims.d"; return false; }
@@ -329,6 +378,7 @@ int apply_pending(Handle* h) {
   VIF_CUDA(h, cudaStreamWaitEvent(h->stream, h->ev_ready[h->pending], 0), "event wait");
   h->slot = h->pending;
   h->pending = -1;
+  ++h->fgen;  // new inputs: a prepared Laplace workspace no longer matches them
   return VIF_OK;
 }
 
@@ -356,6 +406,7 @@ int set_data(Handle* h, const double* X, const double* Z, const int32_t* nbr, co
   if (X || Z || nbr || y) {
     h->have_data = h->have_data || (X && y && (nbr || P.mv == 0) && (Z || P.m == 0));
     h->factored = h->finished = false;
+    ++h->fgen;  // a prepared Laplace workspace (la_check) was built from the old inputs
   }
   if (validate) {
     DevStatus* st = h->buf<DevStatus>(B_STATUS);
@@ -365,7 +416,7 @@ int set_data(Handle* h, const double* X, const double* Z, const int32_t* nbr, co
              "validate");
     DevStatus hs;
     VIF_CUDA(h, cudaMemcpyAsync(&hs, st, sizeof(hs), cudaMemcpyDeviceToHost, s), "status copy");
-    VIF_CUDA(h, cudaStreamSynchronize(s), "sync");
+    VIF_WAIT(h, s);
     if (hs.bad_input != ~0ULL) {
       char msg[160];
       snprintf(msg, sizeof msg, "invalid input at row %llu (non-finite X/y or neighbour rule: N(i) < i, unique, -1 only trailing)",
@@ -536,22 +587,12 @@ LaCtx la_ctx(Handle* h, void* ws) {
 }
 
 // B^{-1} (s o v) -> x [out2 = x + w2 o v2] and B^{-T} u -> y: level-scheduled cooperative kernels
-// (default) or the sync-free flag kernels (VIF_LA_SYNCFREE=1)
-bool la_syncfree() {
-  static const char* e = getenv("VIF_LA_SYNCFREE");
-  return e && e[0] == '1';
-}
 
 int la_binv(LaCtx& c, int ncol, const double* v, const double* scale, double* x, const double* v2, const double* w2,
             double* out2) {
   Handle* h = c.h;
   const Plan& P = h->P;
-  if (la_syncfree())
-    VIF_CUDA(h, launch_la_trsv_fwd(c.nbr(), c.d(L_B), P.mv, P.n, ncol, v, scale, x, v2, w2, out2, c.i(L_FLAGS),
-                                   ++h->la_epoch, c.s),
-             "B^-1");
-  else
-    VIF_CUDA(h, launch_la_trsv_lvl(true, c.i(L_ORDF), c.i(L_LPTRF), h->la_nlev_f, c.i(L_ECF), c.d(L_EVF), nullptr,
+  VIF_CUDA(h, launch_la_trsv_lvl(true, c.i(L_ORDF), c.i(L_LPTRF), h->la_nlev_f, c.i(L_ECF), c.d(L_EVF), nullptr,
                                    P.mv, ncol, v, scale, x, v2, w2, out2, c.s),
              "B^-1 (levels)");
   return VIF_OK;
@@ -560,12 +601,7 @@ int la_binv(LaCtx& c, int ncol, const double* v, const double* scale, double* x,
 int la_btinv(LaCtx& c, int ncol, const double* u, double* y) {
   Handle* h = c.h;
   const Plan& P = h->P;
-  if (la_syncfree())
-    VIF_CUDA(h, launch_la_trsv_bwd(c.i(L_TPTR), c.i(L_TROW), c.d(L_TVAL), P.n, ncol, u, y, c.i(L_FLAGS),
-                                   ++h->la_epoch, c.s),
-             "B^-T");
-  else
-    VIF_CUDA(h, launch_la_trsv_lvl(false, c.i(L_ORDB), c.i(L_LPTRB), h->la_nlev_b, c.i(L_ECB), c.d(L_EVB),
+  VIF_CUDA(h, launch_la_trsv_lvl(false, c.i(L_ORDB), c.i(L_LPTRB), h->la_nlev_b, c.i(L_ECB), c.d(L_EVB),
                                    c.i(L_EPB), P.mv, ncol, u, nullptr, y, nullptr, nullptr, nullptr, c.s),
              "B^-T (levels)");
   return VIF_OK;
@@ -697,7 +733,7 @@ int la_pcg(LaCtx& c, int ncol, const double* rhs, double* x, bool warm, double t
   std::vector<double> bn(ncol), rr(ncol);
   VIF_CUDA(h, cudaMemcpyAsync(bn.data(), c.sc(SC_BN), ncol * sizeof(double), cudaMemcpyDeviceToHost, c.s), "bn");
   VIF_CUDA(h, cudaMemcpyAsync(rr.data(), c.sc(SC_RR), ncol * sizeof(double), cudaMemcpyDeviceToHost, c.s), "rr");
-  VIF_CUDA(h, cudaStreamSynchronize(c.s), "sync");
+  VIF_WAIT(h, c.s);
   std::vector<int> active(ncol);
   iters.assign(ncol, 0);
   int nact = 0;
@@ -715,7 +751,7 @@ int la_pcg(LaCtx& c, int ncol, const double* rhs, double* x, bool warm, double t
     VIF_CUDA(h, launch_la_cg_xr(c.sc(SC_ALPHA), Pv, Q, P.n, ncol, x, R, c.s), "x, r");
     LA_TRY(la_coldot(c, R, R, P.n, ncol, c.sc(SC_RR)));
     VIF_CUDA(h, cudaMemcpyAsync(rr.data(), c.sc(SC_RR), ncol * sizeof(double), cudaMemcpyDeviceToHost, c.s), "rr");
-    VIF_CUDA(h, cudaStreamSynchronize(c.s), "sync");
+    VIF_WAIT(h, c.s);
     bool changed = false;
     for (int k = 0; k < ncol; ++k) {
       if (!active[k]) continue;
@@ -932,6 +968,7 @@ int vif_factor(void* handle, const vif_theta* theta, double* B_out, double* D_ou
   Handle* h = reinterpret_cast<Handle*>(handle);
   if (!h) return fail(nullptr, VIF_ERR_INVALID_ARG, "handle is NULL");
   if (!h->have_data) return fail(h, VIF_ERR_STATE, "no data: pass X, Z, nbr, y to vif_create or vif_set_data");
+  if (h->comm_dead) return fail(h, VIF_ERR_NCCL, "the communicator was aborted by an earlier error");
   CovParams p;
   std::string err;
   if (!make_params(h, theta, p, err)) return fail(h, VIF_ERR_INVALID_ARG, err);
@@ -1113,14 +1150,7 @@ int vif_factor(void* handle, const vif_theta* theta, double* B_out, double* D_ou
     h->mark(S_VECCHIA, 1);
     double* G = h->buf<double>(B_G) + g * gstride;
     h->mark(S_SYRK, 0);
-    // default: 64x64 / 4-warp SYRK (k_syrk.cu); VIF_SYRK128=1 selects the 128x128 engine
-    static const char* syrk128 = getenv("VIF_SYRK128");
-    if (!(syrk128 && syrk128[0] == '1'))
-      VIF_CUDA(h, launch_syrk(Wg, P.ld, npts, P.ld, P.nsplit_old, h->buf<double>(B_GPART), G, P.ld, s),
-               "syrk");
-    else
-      VIF_CUDA(h, launch_syrk_nt(Wg, P.ld, npts, P.ld, P.nsplit, h->buf<double>(B_GPART), G, P.ld, s),
-               "syrk");
+    VIF_CUDA(h, launch_syrk(Wg, P.ld, npts, P.ld, P.nsplit, h->buf<double>(B_GPART), G, P.ld, s), "syrk");
     h->mark(S_SYRK, 1);
     h->mark(S_REDUCE, 0);
     VIF_CUDA(h, launch_logd_sum(Dg, npts, h->buf<double>(B_PART), kLogdParts,
@@ -1137,7 +1167,18 @@ int vif_factor(void* handle, const vif_theta* theta, double* B_out, double* D_ou
   } else if (h->comm) {
     Nccl& N = nccl();
     double* G = h->buf<double>(B_G);
-    ncclResult_t rr = N.AllReduce(G, G, (size_t)P.ld * P.ld + 1, ncclFloat64, ncclSum, h->comm, s);
+    // the Gram + sum log D, and the failure state: a NOT_PD row is found on the rank that owns it, so
+    // the minimum failing row is reduced too -- every rank then returns the same status from vif_nll
+    // (and vif_grad never has ranks entering its own all-reduce while another has returned)
+    DevStatus* st_dev = h->buf<DevStatus>(B_STATUS);
+    ncclResult_t rr = N.GroupStart();
+    if (rr == ncclSuccess) rr = N.AllReduce(G, G, (size_t)P.ld * P.ld + 1, ncclFloat64, ncclSum, h->comm, s);
+    if (rr == ncclSuccess)
+      rr = N.AllReduce(&st_dev->bad_row, &st_dev->bad_row, 1, ncclUint64, ncclMin, h->comm, s);
+    {
+      const ncclResult_t r2 = N.GroupEnd();
+      if (rr == ncclSuccess) rr = r2;
+    }
     if (rr != ncclSuccess) return fail(h, VIF_ERR_NCCL, std::string("ncclAllReduce: ") + N.GetErrorString(rr));
   }
   h->mark(S_REDUCE, 1);
@@ -1181,7 +1222,7 @@ int vif_nll(void* handle, vif_terms* out) {
   DevStatus hs;
   VIF_CUDA(h, cudaMemcpyAsync(ht, terms, sizeof(ht), cudaMemcpyDeviceToHost, s), "terms copy");
   VIF_CUDA(h, cudaMemcpyAsync(&hs, st, sizeof(hs), cudaMemcpyDeviceToHost, s), "status copy");
-  VIF_CUDA(h, cudaStreamSynchronize(s), "sync");
+  VIF_WAIT(h, s);
   if (h->prof) {
     for (int k = 0; k < S_COUNT; ++k) {
       if (!h->ev_used[k]) continue;
@@ -1228,12 +1269,7 @@ int vif_grad(void* handle, const vif_theta* theta, void* gws, size_t gws_bytes, 
   if (!h) return fail(nullptr, VIF_ERR_INVALID_ARG, "handle is NULL");
   if (!grad) return fail(h, VIF_ERR_INVALID_ARG, "grad is NULL");
   const Plan& P = h->P;
-  {
-    static const char* cross_env0 = getenv("VIF_GRAD_CROSS");
-    const bool cross0 = cross_env0 && cross_env0[0] == '1';
-    if (P.mv > 47 || (cross0 && P.mv > 31))
-      return fail(h, VIF_ERR_INVALID_ARG, "vif_grad: m_v <= 47 (<= 31 with VIF_GRAD_CROSS=1) in this version");
-  }
+  if (P.mv > 47) return fail(h, VIF_ERR_INVALID_ARG, "vif_grad: m_v <= 47 in this version");
   const Layout GL = make_grad_layout(P);
   if (!gws || gws_bytes < GL.total) {
     char msg[128];
@@ -1272,20 +1308,16 @@ int vif_grad(void* handle, const vif_theta* theta, void* gws, size_t gws_bytes, 
   }
   VIF_CUDA(h, launch_grad_q(gbuf(G_LINVM), mk, G, ld, P.ycol, m, ld, gbuf(G_ZH), gbuf(G_Z), gbuf(G_Q2), s), "Q");
   // Per rank (every virtual rank of an emulated handle): Gamma = W (2Q) for its rows by processing position,
-  // the per-point state, then one pass per parameter.  dU = dK(X,Z) L^-T - U Phi_low^T is needed on all n
-  // rows (neighbours live on any rank); each rank forms it itself, in row blocks through the rank's own
-  // W, which is dead once Gamma is formed.
+  // the per-point state, the adjoint rows and R, then one pass per parameter.
   const int nrep = P.emulate ? P.world : 1;
   const double* Linv = h->buf<double>(B_LINV);
   const double* U = h->buf<double>(B_U);
   const int nparam = P.d + 2;
-  // columns mk..ld-1 of dU (the y column and the padding) stay zero: d y / d theta = 0
-  VIF_CUDA(h, cudaMemsetAsync(gbuf(G_DU), 0, GL.size[G_DU], s), "memset dU");
+  VIF_CUDA(h, cudaMemsetAsync(gbuf(G_DU), 0, GL.size[G_DU], s), "memset R");
   for (int g = 0; g < nrep; ++g) {
     const int rank = P.emulate ? g : P.rank;
     double* W = h->buf<double>(B_W) + (size_t)g * P.npos * ld;
     VIF_CUDA(h, launch_gemm_tn(W, ld, P.npos, gbuf(G_Q2), ld, ld, ld, 0, gbuf(G_GAM), ld, 1.0, 0, s), "Gamma");
-    double* S = W;
     GradPointArgs a;
     a.U = U;
     a.dU = nullptr;
@@ -1307,19 +1339,11 @@ int vif_grad(void* handle, const vif_theta* theta, void* gws, size_t gws_bytes, 
     a.adj = gbuf(G_ADJ);
     if (state_ff) VIF_CUDA(h, launch_grad_gam(a, s), "gradient state (dots)");
     else VIF_CUDA(h, launch_grad_state(a, s), "gradient state");
-    // adjoint vectors (default) or the cross-Gram pass per parameter (VIF_GRAD_CROSS=1)
-    static const char* cross_env = getenv("VIF_GRAD_CROSS");
-    const bool cross = cross_env && cross_env[0] == '1';
-    if (!cross) VIF_CUDA(h, launch_grad_adjoint(a, s), "gradient adjoint");
-    // default: no dU at all -- the adjoint rows scattered to R (n x m), T = R L_m^{-1}, G2 = R^T U, and
-    // per kernel parameter <T, dK(X,Z)> - <G2, Phi_low> (VIF_GRAD_DU=1: materialise dU per parameter)
-    // cost at n = 1M, m = 500: materialising dU is two n m^2 GEMMs per kernel parameter (~27 ms each);
-    // the R path is ~100 ms once (the R gather, T, G2) plus ~3 ms per parameter: 223 vs 231 ms per
-    // gradient at d = 2, and the gap grows with d.  VIF_GRAD_DU=1 forces the dU path.
-    static const char* du_env = getenv("VIF_GRAD_DU");
-    const bool want_du = du_env && du_env[0] == '1';
-    const bool nodu = !cross && !want_du && mk > 0;
-    if (nodu) {
+    VIF_CUDA(h, launch_grad_adjoint(a, s), "gradient adjoint");
+    // no dU at all: the adjoint rows scattered to R (n x m), T = R L_m^{-1}, G2 = R^T U, and per kernel
+    // parameter <T, dK(X,Z)> - <G2, Phi_low> (at n = 1M, m = 500 materialising dU per
+    // parameter cost two n m^2 GEMMs each; the R path is ~100 ms once plus ~3 ms per parameter)
+    if (mk > 0) {
       double* R = gbuf(G_DU);  // n x mk
       VIF_CUDA(h, launch_gchild(a.nbr, P.mv, a.order, a.npts, P.n, reinterpret_cast<int*>(gbuf(G_CCNT)),
                                 reinterpret_cast<int*>(gbuf(G_CCUR)), reinterpret_cast<int*>(gbuf(G_CPTR)),
@@ -1344,37 +1368,16 @@ int vif_grad(void* handle, const vif_theta* theta, void* gws, size_t gws_bytes, 
     }
     for (int pi = 0; pi < nparam; ++pi) {
       const bool kernel_param = pi <= P.d;
-      const double* dUp = nullptr;
-      if (kernel_param && m > 0 && nodu) {
+      if (kernel_param && m > 0) {
         VIF_CUDA(h, launch_dkm(h->buf<double>(B_Z), m, mk, pi, p, gbuf(G_DKM), s), "dK_m");
         VIF_CUDA(h, launch_gemm_tn(Linv, mk, mk, gbuf(G_DKM), mk, mk, mk, 0, gbuf(G_TT), mk, 1.0, 0, s), "Linv dK_m");
         VIF_CUDA(h, launch_gemm_tn(Linv, mk, mk, gbuf(G_TT), mk, mk, mk, 0, gbuf(G_PHI), mk, 1.0, 0, s), "Phi");
         VIF_CUDA(h, launch_phi_low(gbuf(G_PHI), mk, gbuf(G_PHILOW), s), "Phi_low");
-      } else if (kernel_param && m > 0) {
-        VIF_CUDA(h, launch_dkm(h->buf<double>(B_Z), m, mk, pi, p, gbuf(G_DKM), s), "dK_m");
-        VIF_CUDA(h, launch_gemm_tn(Linv, mk, mk, gbuf(G_DKM), mk, mk, mk, 0, gbuf(G_TT), mk, 1.0, 0, s), "Linv dK_m");
-        VIF_CUDA(h, launch_gemm_tn(Linv, mk, mk, gbuf(G_TT), mk, mk, mk, 0, gbuf(G_PHI), mk, 1.0, 0, s), "Phi");
-        VIF_CUDA(h, launch_phi_low(gbuf(G_PHI), mk, gbuf(G_PHILOW), s), "Phi_low");
-        const int64_t blk = std::max<int64_t>(1, (P.npos * ld) / mk);  // rows of dK(X,Z) that fit in S
-        for (int64_t r0 = 0; r0 < P.n; r0 += blk) {
-          const int64_t rows = std::min<int64_t>(blk, P.n - r0);
-          double* dUr = gbuf(G_DU) + (size_t)r0 * ld;
-          VIF_CUDA(h, launch_kx_deriv(h->buf<double>(B_X) + (size_t)r0 * P.d, h->buf<double>(B_Z), rows, m, mk, pi, p,
-                                      S, s),
-                   "dK(X,Z)");
-          VIF_CUDA(h, launch_gemm_tn(S, mk, rows, Linv, mk, mk, mk, 1, dUr, ld, 1.0, 0, s), "dK L^-T");
-          VIF_CUDA(h, launch_gemm_tn(U + (size_t)r0 * ld, ld, rows, gbuf(G_PHILOW), mk, mk, mk, 1, dUr, ld, -1.0, 1, s),
-                   "U Phi^T");
-        }
-        dUp = gbuf(G_DU);
       }
-      a.dU = dUp;
+      a.dU = nullptr;
       a.pidx = pi;
-      if (cross)
-        VIF_CUDA(h, launch_grad_points(a, gbuf(G_OUT) + (size_t)g * nparam + pi, s), "gradient points");
-      else
-        VIF_CUDA(h, launch_grad_points_adj(a, gbuf(G_OUT) + (size_t)g * nparam + pi, s), "gradient points");
-      if (nodu && kernel_param && m > 0)
+      VIF_CUDA(h, launch_grad_points_adj(a, gbuf(G_OUT) + (size_t)g * nparam + pi, s), "gradient points");
+      if (kernel_param && m > 0)
         VIF_CUDA(h, launch_gfinal(gbuf(G_OUT) + (size_t)g * nparam + pi, gbuf(G_TDK), pi, gbuf(G_G2), gbuf(G_PHILOW),
                                   mk, s),
                  "<T, dK> - <G2, Phi_low>");
@@ -1392,7 +1395,7 @@ int vif_grad(void* handle, const vif_theta* theta, void* gws, size_t gws_bytes, 
     if (r2 != VIF_OK) return r2;
   }
   VIF_CUDA(h, cudaMemcpyAsync(grad, gbuf(G_OUT), (size_t)(P.d + 2) * 8, cudaMemcpyDeviceToHost, s), "grad copy");
-  VIF_CUDA(h, cudaStreamSynchronize(s), "sync");
+  VIF_WAIT(h, s);
   for (int pi = 0; pi < P.d + 2; ++pi)
     if (!isfinite(grad[pi])) return fail(h, VIF_ERR_NOT_PD, "gradient: a residual block or M is not positive definite");
   return VIF_OK;
@@ -1428,6 +1431,7 @@ int vif_predict(void* handle, const vif_theta* theta, int64_t np, const double* 
   cudaStream_t s = h->stream;
   // ranks (NCCL) predict contiguous slices of the prediction points and write only their slice of the
   // outputs; an emulated multi-rank handle (one process) predicts all of them
+  const double* Xp0 = Xp;
   {
     const int64_t per = P.emulate ? np : (np + P.world - 1) / P.world;
     const int64_t lo = P.emulate ? 0 : std::min<int64_t>(np, P.rank * per);
@@ -1444,6 +1448,23 @@ int vif_predict(void* handle, const vif_theta* theta, int64_t np, const double* 
     VIF_CUDA(h, cudaMemcpyAsync(pbuf(P_X), Xp, (size_t)np * P.d * 8, cudaMemcpyDefault, s), "copy Xp");
     if (P.mv > 0)
       VIF_CUDA(h, cudaMemcpyAsync(pbuf(P_NBR), nbrp, (size_t)np * P.mv * 4, cudaMemcpyDefault, s), "copy nbrp");
+    // the prediction rows are gathered unchecked by the vecchia kernel: validate them first
+    DevStatus* st0 = h->buf<DevStatus>(B_STATUS);
+    VIF_CUDA(h, launch_reset_status(st0, s), "reset status");
+    VIF_CUDA(h, launch_validate_pred(pbuf(P_X), np, P.d, reinterpret_cast<const int32_t*>(pbuf(P_NBR)),
+                                     P.mv > 0 ? P.mv : 0, P.n, st0, s),
+             "validate prediction inputs");
+    DevStatus hs0;
+    VIF_CUDA(h, cudaMemcpyAsync(&hs0, st0, sizeof(hs0), cudaMemcpyDeviceToHost, s), "status copy");
+    VIF_WAIT(h, s);
+    if (hs0.bad_input != ~0ULL) {
+      char msg[192];
+      snprintf(msg, sizeof msg,
+               "invalid prediction input at row %llu (non-finite Xp, or a neighbour outside [0, n), repeated, or "
+               "-1 before a valid entry)",
+               hs0.bad_input + (unsigned long long)(Xp - Xp0) / (unsigned long long)P.d);
+      return fail(h, VIF_ERR_INVALID_ARG, msg);
+    }
   }
   int r = vif_factor(handle, theta, nullptr, nullptr);
   if (r != VIF_OK) return r;
@@ -1507,7 +1528,7 @@ int vif_predict(void* handle, const vif_theta* theta, int64_t np, const double* 
   }
   DevStatus hs;
   VIF_CUDA(h, cudaMemcpyAsync(&hs, st, sizeof(hs), cudaMemcpyDeviceToHost, s), "status copy");
-  VIF_CUDA(h, cudaStreamSynchronize(s), "sync");
+  VIF_WAIT(h, s);
   if (hs.bad_row != ~0ULL) {
     char msg[128];
     snprintf(msg, sizeof msg, "residual block of prediction point %llu is not positive definite", hs.bad_row);
@@ -1576,7 +1597,7 @@ int vif_neighbors(void* handle, const vif_theta* theta, int32_t mv, int32_t* nbr
   }
   DevStatus hs;
   VIF_CUDA(h, cudaMemcpyAsync(&hs, st, sizeof(hs), cudaMemcpyDeviceToHost, s), "status copy");
-  VIF_CUDA(h, cudaStreamSynchronize(s), "sync");
+  VIF_WAIT(h, s);
   if (hs.km_fail) return fail(h, VIF_ERR_NOT_PD, "Cholesky of K(Z,Z) + jitter failed");
   return VIF_OK;
 }
@@ -1639,7 +1660,7 @@ int vif_la_prepare(void* handle, const vif_theta* theta, int32_t nprobe, int32_t
   {
     int nnz = 0;
     VIF_CUDA(h, cudaMemcpyAsync(&nnz, c.i(L_TPTR) + P.n, sizeof(int), cudaMemcpyDeviceToHost, s), "nnz");
-    VIF_CUDA(h, cudaStreamSynchronize(s), "sync");
+    VIF_WAIT(h, s);
     VIF_CUDA(h, launch_la_tvals(c.i(L_TPOS), nnz, P.mv > 0 ? P.mv : 1, c.d(L_B), c.i(L_TROW), c.d(L_TVAL), s),
              "B^T values");
   }
@@ -1652,7 +1673,7 @@ int vif_la_prepare(void* handle, const vif_theta* theta, int32_t nprobe, int32_t
              "levels");
     int hl[2];
     VIF_CUDA(h, cudaMemcpyAsync(hl, nlev, sizeof(hl), cudaMemcpyDeviceToHost, s), "levels");
-    VIF_CUDA(h, cudaStreamSynchronize(s), "sync");
+    VIF_WAIT(h, s);
     h->la_nlev_f = hl[0] + 1;
     h->la_nlev_b = hl[1] + 1;
     VIF_CUDA(h, launch_la_bucket(c.i(L_LEVF), P.n, h->la_nlev_f, c.i(L_CNT), c.i(L_CUR), c.i(L_LPTRF), c.i(L_ORDF), s),
@@ -1667,7 +1688,7 @@ int vif_la_prepare(void* handle, const vif_theta* theta, int32_t nprobe, int32_t
   VIF_CUDA(h, cudaMemsetAsync(c.i(L_FLAGS), 0, c.L.size[L_FLAGS], s), "memset flags");  // solves start at epoch 1
   int ff = 0;
   VIF_CUDA(h, cudaMemcpyAsync(&ff, c.fitc_fail(), sizeof(int), cudaMemcpyDeviceToHost, s), "status");
-  VIF_CUDA(h, cudaStreamSynchronize(s), "sync");
+  VIF_WAIT(h, s);
   if (ff) return fail(h, VIF_ERR_NOT_PD, "Cholesky of M (latent factor) failed");
   h->la_epoch = 0;
   h->la_ws = ws;
@@ -1704,7 +1725,7 @@ int vif_la_apply(void* handle, void* ws, int32_t op, int32_t ncol, const double*
     case VIF_LA_A1: LA_TRY(la_sigma_inv(c, ncol, v, out, winv)); break;
     default: return fail(h, VIF_ERR_INVALID_ARG, "vif_la_apply: unknown operator");
   }
-  VIF_CUDA(h, cudaStreamSynchronize(c.s), "sync");
+  VIF_WAIT(h, c.s);
   int ff = 0;
   VIF_CUDA(h, cudaMemcpy(&ff, c.fitc_fail(), sizeof(int), cudaMemcpyDeviceToHost), "status");
   if (ff) return fail(h, VIF_ERR_NOT_PD, "FITC: Cholesky of M_V failed");
@@ -1745,7 +1766,7 @@ int vif_la_nll(void* handle, void* ws, const double* y, const vif_la_opts* opts,
     LA_TRY(la_coldot(c, bm, c.d(L_A), n, 1, fin + 7));
     double hv[8];
     VIF_CUDA(h, cudaMemcpyAsync(hv, fin, sizeof(hv), cudaMemcpyDeviceToHost, s), "psi");
-    VIF_CUDA(h, cudaStreamSynchronize(s), "sync");
+    VIF_WAIT(h, s);
     const double psi = hv[0] - 0.5 * hv[7];
     if (!isfinite(psi)) return fail(h, VIF_ERR_NOT_PD, "Laplace: Newton iterate is not finite");
     if (it > 1 && fabs(psi - psi_old) <= opts->newton_tol * fabs(psi_old)) break;
@@ -1798,7 +1819,7 @@ int vif_la_nll(void* handle, void* ws, const double* y, const vif_la_opts* opts,
   int ff = 0;
   VIF_CUDA(h, cudaMemcpyAsync(o, c.sc(SC_OUT), sizeof(o), cudaMemcpyDeviceToHost, s), "terms");
   VIF_CUDA(h, cudaMemcpyAsync(&ff, c.fitc_fail(), sizeof(int), cudaMemcpyDeviceToHost, s), "status");
-  VIF_CUDA(h, cudaStreamSynchronize(s), "sync");
+  VIF_WAIT(h, s);
   out->nll = ell > 0 ? o[0] : NAN;
   out->neg_loglik = o[1];
   out->quad = o[2];
@@ -1822,7 +1843,7 @@ int vif_copy_U(void* handle, double* out) {
   VIF_CUDA(h, cudaMemcpy2DAsync(out, (size_t)P.m * 8, h->buf<double>(B_U), (size_t)P.ld * 8, (size_t)P.m * 8, P.n,
                                 cudaMemcpyDefault, h->stream),
            "copy U");
-  VIF_CUDA(h, cudaStreamSynchronize(h->stream), "sync");
+  VIF_WAIT(h, h->stream);
   return VIF_OK;
 }
 

@@ -399,12 +399,31 @@ class VifModel:
                                  rank=rank, world=world, nccl_id=nccl_id, stream=stream)
         self.rounds, self.chunk = vif_partition(self.n, self.d, self.m, self.mv, rank, world)
 
+    def _inputs(self, X, Z, nbr, y):
+        """Marshal new inputs like the constructor does (dtype, contiguity, device or pinned host) and check
+        their sizes against the handle's dims; a mismatch raises instead of reading a wrong byte count."""
+        X = _as_input(X, torch.float64, self.device)
+        Z = _as_input(Z, torch.float64, self.device) if self.m > 0 else None
+        nbr = _as_input(nbr, torch.int32, self.device) if self.mv > 0 else None
+        y = _as_input(y, torch.float64, self.device)
+        for name, t, want in (("X", X, self.n * self.d), ("Z", Z, self.m * self.d), ("nbr", nbr, self.n * self.mv),
+                              ("y", y, self.n)):
+            if t is not None and t.numel() != want:
+                raise ValueError(f"{name} has {t.numel()} elements, the handle needs {want}")
+        return X, Z, nbr, y
+
     def set_data(self, X=None, Z=None, nbr=None, y=None, validate=False):
+        X, Z, nbr, y = self._inputs(X, Z, nbr, y)
         vif_set_data(self.handle, X, Z, nbr, y, validate)
+        self._staged = (X, Z, nbr, y)  # the copies are asynchronous on the library's stream
 
     def stage_data(self, X, Z, nbr, y):
         """Inputs of the next evaluation (pinned host or device tensors), copied while this one runs."""
-        vif_stage_data(self.handle, X, Z if self.m > 0 else None, nbr if self.mv > 0 else None, y)
+        X, Z, nbr, y = self._inputs(X, Z, nbr, y)
+        vif_stage_data(self.handle, X, Z, nbr, y)
+        # keep the sources alive until the copy stream has read them (the next staging call at the
+        # earliest waits for the slot's previous evaluation, which waited for these copies)
+        self._staged_prev, self._staged = getattr(self, "_staged", None), (X, Z, nbr, y)
 
     def factor(self, theta: Theta, B_out=None, D_out=None):
         vif_factor(self.handle, theta, B_out, D_out)

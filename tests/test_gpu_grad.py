@@ -139,6 +139,13 @@ def test_grad_repeat_deterministic_and_matches_nll():
 
 
 @pytest.mark.slow
+def test_grad_config4_recipe_m1000():
+    """m = 1000 (ld = 1008: the gradient buffers, R, T, G2 and the Q / Gamma GEMMs beyond 512 columns) at the
+    config-4 recipe (d = 10 ARD Matern 5/2, m_v = 20), n = 3000, all 12 partial derivatives vs the oracle."""
+    grad_parity(vifgen.make_config(4, device="cuda", n=3000))
+
+
+@pytest.mark.slow
 def test_grad_config2_full():
     grad_parity(vifgen.make_config(2, device="cuda"))
 

@@ -231,6 +231,26 @@ def test_config3_full_nll_and_sampled_rows():
     assert t.logdet_M >= 0 and t.quad >= 0
     r = oracle_run(w)
     check_terms(t, r.nll, r.logdet_D, r.logdet_M, r.quad)
+    # the full oracle factor is at hand: every one of the 1M rows of B and D, not only the sample
+    check_D(D, r.D)
+    check_B(B, r.B)
+
+
+@pytest.mark.parametrize("cid,n", [(4, 12000), (5, 9000)])
+def test_large_m_config_recipes_parity(cid, n):
+    """BASELINE configs 4 (d = 10, ARD Matern 5/2, m = 1000, m_v = 20) and 5 (d = 3, Matern 1/2, m = 1500,
+    m_v = 40: the s > 32 kernel) at n of ~10k with their own recipes: the W pass beyond 512 columns (ld = 1008 /
+    1512), K1 and the SYRK at ld > 512, chol_inv beyond 16 tiles -- NLL, every B and D row and U against the
+    oracle."""
+    w = vifgen.make_config(cid, device="cuda", n=n)
+    assert w.m == (1000 if cid == 4 else 1500)
+    assert_parity(w, want_U=True)
+
+
+def test_large_m_emulated_sharding():
+    """m = 1000 on three emulated ranks (per-rank SYRK partials at ld = 1008, rank-ordered reduction)."""
+    w = vifgen.make_config(4, device="cuda", n=6000)
+    assert_parity(w, world=3, want_U=False)
 
 
 def test_rounds_schedule_same_result():

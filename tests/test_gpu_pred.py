@@ -94,3 +94,10 @@ def test_pred_single_point_and_repeat():
 @pytest.mark.slow
 def test_pred_config3_vs_oracle():
     pred_parity(vifgen.make_config(3, device="cuda"), npred=2000)
+
+
+@pytest.mark.parametrize("cid,n", [(4, 8000), (5, 6000)])
+def test_pred_large_m_config_recipes(cid, n):
+    """m = 1000 (config 4: 10-D prediction inputs, N(0, I)) and m = 1500 with m_v = 40 (config 5): the prediction
+    features, rows and the L_M^{-T} product beyond 512 columns."""
+    pred_parity(vifgen.make_config(cid, device="cuda", n=n), npred=400, x="normal" if cid == 4 else "uniform")
