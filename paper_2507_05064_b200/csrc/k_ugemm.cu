@@ -10,6 +10,7 @@
 //   i = (p / chunk) * world * chunk + rank * chunk + p % chunk.
 #include "common.cuh"
 #include "kernels.h"
+#include "tma.cuh"
 #include <stdlib.h>
 
 namespace vif {
@@ -114,105 +115,126 @@ __global__ void __launch_bounds__(256) kx_eval_d_kernel(const double* __restrict
   }
 }
 
-// C[row(p)][c] = sum_k A[p][k] B[c][k], A: npos x K (lda), B: N x K (ldb); B lower-triangular when tri.
-// 128 x 64 CTA tile, BK = 32, 8 warps (4 x 2) of 32 x 32, 3-stage cp.async pipeline.
-// smem rows padded to 40 doubles (320 B = 64 mod 128 B) so the 16-byte fragment loads
-// (k-pair per lane, see below) are bank-conflict free.
+// C[row(p)][c] (+)= alpha sum_k A[p][k] B[c][k], A: npos x K (lda), B: N x K (ldb); B lower-triangular
+// (B[c][k] = 0 for k > c) when tri, so K-tiles past a column block's last column are skipped.
+//
+// Blackwell tile movement: a producer warp streams BK = 16-wide k-slices of the A rows (128 x 16) and B
+// rows (BN x 16) with cp.async.bulk.tensor (boxes of 16 doubles x rows, SWIZZLE_128B) through a GS-stage
+// shared-memory ring, completing on per-stage "full" mbarriers; (BM / 32) x (BN / 32) consumer warps of
+// 32 x 32 wait on "full", run the DMMAs and release the stage on its "empty" mbarrier (no CTA barrier in
+// the main loop).  One CTA per SM: 96 x 128 tiles (12 consumer warps + the producer = 13 warps, at most
+// 4 per SMSP, so 128 registers each), or 128 x 64 for N <= 64.
+//
+// Fragments (k contiguous in both operands): lane l holds row l/4 of an 8-row block and the k-pair
+// kk + 2(l%4) + {0,1} (one 16-byte load), used as two k-steps with the same k permutation on both
+// operands.  Under the 128-B swizzle the 8 rows x 4 chunks of a fragment load hit every bank 4 times:
+// four wavefronts for 512 bytes, conflict-free.
 namespace {
-// BK = 16 keeps the ring at 110 KB so two CTAs (16 warps) share an SM and one CTA's prologue /
-// epilogue overlaps the other's main loop (rows padded to 24 doubles = 64 mod 128 B)
-constexpr int GBM = 128, GBN = 64, GBK = 16, GST = 3, GPAD = GBK + 8;
-constexpr int GCH = GBK / 2;  // 16-byte chunks per tile row
-}
+constexpr int GBK = 16, GS = 4;
+template <int BM, int BN>
+struct GemmCfg {
+  static constexpr int WM = BM / 32;                 // consumer warp rows
+  static constexpr int NCW = WM * (BN / 32);         // consumer warps
+  static constexpr int THREADS = 32 * (NCW + 1);
+  static constexpr int ABYTES = BM * 128;           // one stage of A: BM rows x 16 doubles
+  static constexpr int BBYTES = BN * 128;
+  static constexpr int STAGE = ABYTES + BBYTES;
+  static constexpr size_t SMEM = (size_t)GS * STAGE + 1024 + 2 * GS * 8;
+};
+}  // namespace
 
-__global__ void __launch_bounds__(256, 2) gemm_tn_kernel(const double* __restrict__ A, int64_t lda, int64_t npos,
-                                                      const double* __restrict__ B, int64_t ldb, int N, int K,
-                                                      int tri, double* __restrict__ C, int64_t ldc, int64_t n,
-                                                      int64_t chunk, int world, int rank, int64_t pos0,
-                                                      double alpha, int accum) {
-  extern __shared__ __align__(16) double gsm[];
-  double* As = gsm;                            // [GST][GBM][GPAD]
-  double* Bs = gsm + GST * GBM * GPAD;         // [GST][GBN][GPAD]
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int wm = warp >> 1, wn = warp & 1;     // 4 x 2 warps
-  // 1-D grid, column block fastest: the ncb CTAs that share an A row block run together and
-  // read it from L2 instead of DRAM
-  const int ncb = (N + GBN - 1) / GBN;
-  const int64_t row0 = (int64_t)(blockIdx.x / ncb) * GBM;
-  const int col0 = (blockIdx.x % ncb) * GBN;
+template <int BM, int BN>
+__global__ void __launch_bounds__(GemmCfg<BM, BN>::THREADS, 1) gemm_tn_tma_kernel(
+    const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int64_t npos, int N, int K,
+    int tri, double* __restrict__ C, int64_t ldc, int64_t n, int64_t chunk, int world, int rank, int64_t pos0,
+    double alpha, int accum) {
+  using Cfg = GemmCfg<BM, BN>;
+  extern __shared__ uint8_t g_raw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(g_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(sm + GS * Cfg::STAGE);
+  uint64_t* empty = full + GS;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // 1-D grid, column block fastest: the CTAs sharing an A row block run together (A from L2)
+  const int ncb = (N + BN - 1) / BN;
+  const int64_t row0 = (int64_t)(blockIdx.x / ncb) * BM;
+  const int col0 = (blockIdx.x % ncb) * BN;
   int kend = K;
-  if (tri && col0 + GBN < kend) kend = col0 + GBN;
+  if (tri && col0 + BN < kend) kend = col0 + BN;
   const int nkt = (kend + GBK - 1) / GBK;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < GS; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], Cfg::NCW);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  if (warp == Cfg::NCW) {  // ---------------- producer ----------------
+    if (lane == 0) {
+      tma_prefetch_desc(&tmA);
+      tma_prefetch_desc(&tmB);
+      for (int kt = 0; kt < nkt; ++kt) {
+        const int s = kt % GS;
+        if (kt >= GS) mbar_wait(&empty[s], ((kt / GS) + 1) & 1);
+        mbar_expect_tx(&full[s], Cfg::STAGE);
+        uint8_t* st = sm + s * Cfg::STAGE;
+        tma_load_2d(st, &tmA, kt * GBK, (int)row0, &full[s]);
+        tma_load_2d(st + Cfg::ABYTES, &tmB, kt * GBK, col0, &full[s]);
+      }
+    }
+    return;
+  }
+
+  // ---------------- consumers: (BM/32) x (BN/32) warps of 32 x 32 ----------------
+  const int wm = warp % Cfg::WM, wn = warp / Cfg::WM;
   // a warp's 32 columns end at col0 + 32 (wn + 1): with a triangular B it skips later K-tiles
   const int kend_w = tri ? min(kend, col0 + 32 * (wn + 1)) : kend;
-
-  auto load_stage = [&](int st, int kt) {
-    const int k0 = kt * GBK;
-    double* as = As + st * GBM * GPAD;
-    double* bs = Bs + st * GBN * GPAD;
-#pragma unroll
-    for (int j = 0; j < GBM * GCH / 256; ++j) {  // A: GBM rows x GCH chunks of 16 B
-      const int e = tid + j * 256;
-      const int r = e / GCH, c2 = (e % GCH) * 2;
-      const int64_t gr = row0 + r;
-      const bool ok = gr < npos && k0 + c2 < kend;
-      const double* src = ok ? A + gr * lda + k0 + c2 : A;
-      cp_async16(as + r * GPAD + c2, src, ok);
-    }
-#pragma unroll
-    for (int j = 0; j < GBN * GCH / 256; ++j) {  // B: GBN rows x GCH chunks
-      const int e = tid + j * 256;
-      const int r = e / GCH, c2 = (e % GCH) * 2;
-      const int gc = col0 + r;
-      const bool ok = gc < N && k0 + c2 < kend;
-      const double* src = ok ? B + (int64_t)gc * ldb + k0 + c2 : B;
-      cp_async16(bs + r * GPAD + c2, src, ok);
-    }
-  };
-
+  const int nkt_w = (kend_w + GBK - 1) / GBK;
   double acc[4][4][2];
 #pragma unroll
   for (int a = 0; a < 4; ++a)
 #pragma unroll
     for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
-
+  const int fr = lane >> 2, t4 = lane & 3;
+  // byte offsets inside a stage of the 16-byte fragment loads: row (block*8 + fr), k-pair chunk kh*4 + t4
+  uint32_t offA[2][4], offB[2][4];
 #pragma unroll
-  for (int s = 0; s < GST - 1; ++s) {
-    if (s < nkt) load_stage(s, s);
-    cp_async_commit();
-  }
-  const int fr = lane >> 2, fk = (lane & 3) * 2;
+  for (int kh = 0; kh < 2; ++kh)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int ra = wm * 32 + q * 8 + fr, rb = wn * 32 + q * 8 + fr;
+      offA[kh][q] = (uint32_t)(ra * 128 + (((kh * 4 + t4) ^ (ra & 7)) << 4));
+      offB[kh][q] = (uint32_t)(Cfg::ABYTES + rb * 128 + (((kh * 4 + t4) ^ (rb & 7)) << 4));
+    }
+  const uint32_t sbase = smem_u32(sm);
   for (int kt = 0; kt < nkt; ++kt) {
-    cp_async_wait<GST - 2>();
-    __syncthreads();
-    {
-      const int nk = kt + GST - 1;
-      if (nk < nkt) load_stage(nk % GST, nk);
-      cp_async_commit();
+    const int s = kt % GS;
+    mbar_wait(&full[s], (kt / GS) & 1);
+    if (kt < nkt_w) {
+      const uint32_t st = sbase + s * Cfg::STAGE;
+#pragma unroll
+      for (int kh = 0; kh < 2; ++kh) {
+        double2 af[4], bf[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          af[q] = lds_f64x2(st + offA[kh][q]);
+          bf[q] = lds_f64x2(st + offB[kh][q]);
+        }
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int b = 0; b < 4; ++b) dmma884(acc[a][b][0], acc[a][b][1], af[a].x, bf[b].x);
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int b = 0; b < 4; ++b) dmma884(acc[a][b][0], acc[a][b][1], af[a].y, bf[b].y);
+      }
     }
-    if (kt * GBK >= kend_w) continue;
-    const double* as = As + (kt % GST) * GBM * GPAD + (wm * 32 + fr) * GPAD + fk;
-    const double* bs = Bs + (kt % GST) * GBN * GPAD + (wn * 32 + fr) * GPAD + fk;
-#pragma unroll
-    for (int kk = 0; kk < GBK; kk += 8) {
-      // each lane holds k = kk + fk + {0,1} of its row: two k-steps of 4 with a consistent
-      // permutation of k on both operands (the contraction is order-independent)
-      double2 af[4], bf[4];
-#pragma unroll
-      for (int t = 0; t < 4; ++t) af[t] = *reinterpret_cast<const double2*>(as + t * 8 * GPAD + kk);
-#pragma unroll
-      for (int t = 0; t < 4; ++t) bf[t] = *reinterpret_cast<const double2*>(bs + t * 8 * GPAD + kk);
-#pragma unroll
-      for (int a = 0; a < 4; ++a)
-#pragma unroll
-        for (int b = 0; b < 4; ++b) dmma884(acc[a][b][0], acc[a][b][1], af[a].x, bf[b].x);
-#pragma unroll
-      for (int a = 0; a < 4; ++a)
-#pragma unroll
-        for (int b = 0; b < 4; ++b) dmma884(acc[a][b][0], acc[a][b][1], af[a].y, bf[b].y);
-    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
   }
-  cp_async_wait<0>();
   const bool pair = !((N | ldc) & 1);  // 16-byte stores need an even N and ldc
   // epilogue: lane holds C[fr][2*(lane&3) + {0,1}] of each 8x8 tile
 #pragma unroll
@@ -223,7 +245,7 @@ __global__ void __launch_bounds__(256, 2) gemm_tn_kernel(const double* __restric
     if (i >= n) continue;
 #pragma unroll
     for (int b = 0; b < 4; ++b) {
-      const int c = col0 + wn * 32 + b * 8 + (lane & 3) * 2;
+      const int c = col0 + wn * 32 + b * 8 + t4 * 2;
       if (c < N) {
         if (pair) {
           double2* dst = reinterpret_cast<double2*>(C + i * ldc + c);
@@ -242,6 +264,31 @@ __global__ void __launch_bounds__(256, 2) gemm_tn_kernel(const double* __restric
       }
     }
   }
+}
+
+// host: the TMA GEMM on A (npos x K, lda) and B (N x K, ldb); 96 x 128 tiles, 128 x 64 when N <= 64
+static cudaError_t gemm_tn_tma(const double* A, int64_t lda, int64_t npos, const double* B, int64_t ldb, int N, int K,
+                               int tri, double* C, int64_t ldc, int64_t n, int64_t chunk, int world, int rank,
+                               int64_t pos0, double alpha, int accum, cudaStream_t s) {
+  if (npos <= 0 || N <= 0) return cudaSuccess;
+  if (K <= 0) return cudaErrorInvalidValue;
+  auto go = [&](auto kern, auto cfg) -> cudaError_t {
+    using Cfg = decltype(cfg);
+    constexpr int BM = Cfg::WM * 32, BN = Cfg::NCW / Cfg::WM * 32;
+    CUtensorMap ta, tb;
+    cudaError_t e = make_tmap_f64(&ta, A, (uint64_t)npos, (uint64_t)K, (uint64_t)lda, BM);
+    if (e != cudaSuccess) return e;
+    e = make_tmap_f64(&tb, B, (uint64_t)N, (uint64_t)K, (uint64_t)ldb, BN);
+    if (e != cudaSuccess) return e;
+    e = smem_optin(kern, Cfg::SMEM);
+    if (e != cudaSuccess) return e;
+    const unsigned grid = (unsigned)(((npos + BM - 1) / BM) * ((N + BN - 1) / BN));
+    kern<<<grid, Cfg::THREADS, Cfg::SMEM, s>>>(ta, tb, npos, N, K, tri, C, ldc, n, chunk, world, rank, pos0, alpha,
+                                                accum);
+    return cudaGetLastError();
+  };
+  if (N <= 64) return go(gemm_tn_tma_kernel<128, 64>, GemmCfg<128, 64>{});
+  return go(gemm_tn_tma_kernel<96, 128>, GemmCfg<96, 128>{});
 }
 
 cudaError_t launch_u_features(const double* X, const double* Z, const double* y, int64_t n, int64_t pos0,
@@ -303,28 +350,15 @@ cudaError_t launch_u_features(const double* X, const double* Z, const double* y,
   if (e0 != cudaSuccess) return e0;
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess || mk == 0) return e;
-  const size_t smem = (size_t)GST * (GBM + GBN) * GPAD * sizeof(double);
-  e = smem_optin(gemm_tn_kernel, smem);
-  if (e != cudaSuccess) return e;
-  const unsigned grid = (unsigned)(((npos + GBM - 1) / GBM) * ((mk + GBN - 1) / GBN));
-  gemm_tn_kernel<<<grid, 256, smem, s>>>(S + pos0 * lds, lds, npos, Linv, mk, mk, mk, 1, Uaug, ld, n, chunk, world, rank,
-                                         pos0, 1.0, 0);
-  return cudaGetLastError();
+  return gemm_tn_tma(S + pos0 * lds, lds, npos, Linv, mk, mk, mk, 1, Uaug, ld, n, chunk, world, rank, pos0, 1.0, 0,
+                     s);
 }
 
 // C[p][c] (+)= alpha sum_k A[p][k] B[c][k] for p < nrows, c < N (single rank: row p -> p); B lower
 // triangular (k <= c) when tri.  Used by the gradient path (dU, Phi, Gamma).
 cudaError_t launch_gemm_tn(const double* A, int64_t lda, int64_t nrows, const double* B, int64_t ldb, int N, int K,
                            int tri, double* C, int64_t ldc, double alpha, int accum, cudaStream_t s) {
-  if (nrows == 0 || N == 0) return cudaSuccess;
-  const size_t smem = (size_t)GST * (GBM + GBN) * GPAD * sizeof(double);
-  {
-    cudaError_t e = smem_optin(gemm_tn_kernel, smem);
-    if (e != cudaSuccess) return e;
-  }
-  const unsigned grid = (unsigned)(((nrows + GBM - 1) / GBM) * ((N + GBN - 1) / GBN));
-  gemm_tn_kernel<<<grid, 256, smem, s>>>(A, lda, nrows, B, ldb, N, K, tri, C, ldc, nrows, nrows, 1, 0, 0, alpha, accum);
-  return cudaGetLastError();
+  return gemm_tn_tma(A, lda, nrows, B, ldb, N, K, tri, C, ldc, nrows, nrows, 1, 0, 0, alpha, accum, s);
 }
 
 }  // namespace vif

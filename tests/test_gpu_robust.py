@@ -113,7 +113,7 @@ def test_predict_invalid_neighbours_rejected():
     Xp, nbrp = vifgen.make_prediction(w, 50, device="cuda")
     model = p.VifModel(*dev_inputs(w))
     th = p.Theta(**w.theta_dict())
-    mu, _ = model.predict(th, Xp, nbrp)
+    mu = model.predict(th, Xp, nbrp)
     assert np.all(np.isfinite(mu.cpu().numpy()))
     for bad, row in (("range", 11), ("middle", 20), ("dup", 33), ("nan", 44)):
         b = nbrp.copy()
@@ -129,7 +129,7 @@ def test_predict_invalid_neighbours_rejected():
         with pytest.raises(p.VifError) as e:
             model.predict(th, Xb, b)
         assert e.value.status == 1 and f"row {row}" in e.value.msg, e.value.msg
-    mu2, _ = model.predict(th, Xp, nbrp)  # the handle is still usable
+    mu2 = model.predict(th, Xp, nbrp)  # the handle is still usable
     assert torch.equal(mu, mu2)
     model.close()
 
