@@ -1,10 +1,11 @@
 // k_syrk.cu -- K4: G = [W r]^T [W r] over the rank's rows ("M"; whitened, reading c4).
 //
 // Tall-skinny FP64 DMMA SYRK.  The output is the (ld x ld) lower triangle in 64 x 64 tiles (ld = 512 at
-// m = 500 -> 36 tiles); the rows are split into `nsplit` contiguous slabs (multiples of SK rows) and the
-// grid is tiles x splits, sized to ONE wave of two CTAs per SM: every tile of a split reads the same
-// rows at the same time, so each row of W leaves HBM about once and is served to the other tiles from
-// L2.  Every CTA writes its partial tile; a deterministic reduction sums the splits in a fixed order.
+// m = 500 -> 36 tiles); the rows are split into contiguous slabs (multiples of SK rows) and the grid of
+// (tile, split) items is sized to ONE wave of two CTAs per SM: every tile of a split reads the same rows at
+// about the same time, so
+// each row of W leaves HBM about once and is served to the other tiles from L2.  Every CTA writes its
+// partial tile; a deterministic reduction sums the splits in a fixed order.
 //
 // Tile movement (Blackwell TMA): a producer warp streams the two 64-column slabs of W for the tile
 // (one for a diagonal tile) through an SS-stage shared-memory ring with cp.async.bulk.tensor (boxes of
@@ -20,6 +21,10 @@
 #include "common.cuh"
 #include "kernels.h"
 #include "tma.cuh"
+
+#include <stdlib.h>
+
+#include <algorithm>
 
 namespace vif {
 
@@ -42,19 +47,32 @@ __device__ __forceinline__ void tile_ij(int t, int& I, int& J) {
 }
 
 __global__ void __launch_bounds__(32 * (NCONS + 1), SYRK_CTAS_PER_SM)
-    syrk_tma_kernel(const __grid_constant__ CUtensorMap tmW, int64_t nrows, int ntiles, int64_t rows_per_split,
-                    double* __restrict__ Gpart) {
+    syrk_tma_kernel(const __grid_constant__ CUtensorMap tmW, int64_t nrows, int nt1, int sd, int so, int64_t rps_d,
+                    int64_t rps_o, double* __restrict__ Gpart) {
   extern __shared__ uint8_t syrk_raw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(syrk_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(sm + SS * 2 * SLAB);
   uint64_t* empty = full + SS;
-  const int t = blockIdx.x % ntiles;
-  const int split = blockIdx.x / ntiles;
-  int I, J;
-  tile_ij(t, I, J);
+  // work items: the nt1 diagonal tiles x sd row splits first, then the off-diagonal tiles x so splits
+  int I, J, split;
+  int64_t rps;
+  if ((int)blockIdx.x < nt1 * sd) {
+    I = J = blockIdx.x / sd;
+    split = blockIdx.x % sd;
+    rps = rps_d;
+  } else {
+    const int o = blockIdx.x - nt1 * sd;
+    const int to = o / so;  // off-diagonal tile number in row-major order of the strict lower triangle
+    split = o % so;
+    int i = 1;
+    while (i * (i + 1) / 2 <= to) ++i;
+    I = i;
+    J = to - i * (i - 1) / 2;
+    rps = rps_o;
+  }
   const bool diag = I == J;
-  const int64_t r0 = (int64_t)split * rows_per_split;
-  int64_t r1 = r0 + rows_per_split;
+  const int64_t r0 = (int64_t)split * rps;
+  int64_t r1 = r0 + rps;
   if (r1 > nrows) r1 = nrows;
   const int nkt = r0 < r1 ? (int)((r1 - r0 + SK - 1) / SK) : 0;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -160,9 +178,10 @@ __global__ void __launch_bounds__(32 * (NCONS + 1), SYRK_CTAS_PER_SM)
     }
 }
 
-// G[a][b] (a >= b tile-wise) = sum over splits in order
-__global__ void syrk_reduce_kernel(const double* __restrict__ Gpart, int ntiles, int nsplit, int ncols,
-                                   double* __restrict__ G, int ldg) {
+// G[a][b] (a >= b tile-wise) = sum over the tile's work items in order, launch by launch (rounds)
+__global__ void syrk_reduce_kernel(const double* __restrict__ Gpart, int nt1, int sd, int so, int nlaunch,
+                                   int ncols, double* __restrict__ G, int ldg) {
+  const int ntiles = nt1 * (nt1 + 1) / 2;
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= (int64_t)ntiles * ST * ST) return;
   const int t = (int)(e / (ST * ST));
@@ -171,8 +190,12 @@ __global__ void syrk_reduce_kernel(const double* __restrict__ Gpart, int ntiles,
   tile_ij(t, I, J);
   const int a = I * ST + rc / ST, b = J * ST + rc % ST;
   if (a >= ncols || b >= ncols) return;
+  const int items = nt1 * sd + (ntiles - nt1) * so;
+  const int first = I == J ? I * sd : nt1 * sd + (t - I) * so;  // t - I = off-diagonal tiles before t
+  const int cnt = I == J ? sd : so;
   double s = 0.0;
-  for (int sp = 0; sp < nsplit; ++sp) s += Gpart[((size_t)sp * ntiles + t) * ST * ST + rc];
+  for (int l = 0; l < nlaunch; ++l)
+    for (int k = 0; k < cnt; ++k) s += Gpart[((size_t)l * items + first + k) * ST * ST + rc];
   G[(size_t)a * ldg + b] = s;
 }
 
@@ -181,54 +204,70 @@ int syrk_ntiles(int ncols) {
   return nt1 * (nt1 + 1) / 2;
 }
 
-// Split count: the smallest with a last wave >= 97% full (time ~ waves / nsplit), else the best up to 64;
-// never fewer than SK rows per split.
-int syrk_nsplit(int ncols, int64_t nrows, int num_sms) {
-  const int nt = syrk_ntiles(ncols);
-  const int64_t slots = (int64_t)SYRK_CTAS_PER_SM * num_sms;
-  const int64_t max_by_rows = (nrows + 4 * SK - 1) / (4 * SK);
-  int64_t best = 1;
-  double best_cost = 1e300;
-  for (int64_t ns = 1; ns <= 64; ++ns) {
-    const int64_t waves = (nt * ns + slots - 1) / slots;
-    const double cost = (double)waves / (double)ns;
-    const double fill = (double)(nt * ns) / (double)(waves * slots);
-    if (cost < best_cost - 1e-12) {
-      best_cost = cost;
-      best = ns;
-    }
-    if (fill >= 0.97) {
-      best = ns;
-      break;
-    }
-  }
-  if (best > max_by_rows) best = max_by_rows;
-  if (best < 1) best = 1;
-  return (int)best;
+// Split plan: `so` row splits per off-diagonal tile and sd(so) per diagonal tile (equal DMMA work per CTA),
+// the largest so whose CTAs all fit one wave of SYRK_CTAS_PER_SM per SM; never fewer than 4 SK rows per split.
+// The same number of splits for diagonal and off-diagonal tiles (measured at config 3, profiles/r02_notes.md:
+// 8.35 ms; skipping the upper 8 x 8 blocks of the diagonal sub-tiles 8.79 ms; fewer, longer diagonal splits
+// for equal work per CTA 10.5 ms -- the per-warp DMMA stream, not the CTA's total, sets the time)
+static int syrk_diag_splits(int so) { return so; }
+
+static int syrk_items(int ncols, int so) {
+  const int nt1 = (ncols + ST - 1) / ST;
+  return nt1 * syrk_diag_splits(so) + (nt1 * (nt1 - 1) / 2) * so;
 }
 
-size_t syrk_part_doubles(int ncols, int nsplit) { return (size_t)syrk_ntiles(ncols) * nsplit * ST * ST; }
+int syrk_nsplit(int ncols, int64_t nrows, int num_sms) {
+  // one wave if possible: the largest so whose items all fit (ld = 512: 36 tiles x 8 splits = 288 CTAs); else
+  // the plan with the smallest makespan ~ waves x the per-CTA rows (so <= 64)
+  const int64_t slots = (int64_t)SYRK_CTAS_PER_SM * num_sms;
+  const int64_t max_by_rows = std::max<int64_t>(1, (nrows + 4 * SK - 1) / (4 * SK));
+  if (syrk_items(ncols, 1) <= slots) {
+    int best = 1;
+    for (int so = 2; so <= 256 && so <= max_by_rows && syrk_items(ncols, so) <= slots; ++so) best = so;
+    return best;
+  }
+  int best = 1;
+  double best_cost = 1e300;
+  for (int so = 1; so <= 64 && so <= max_by_rows; ++so) {
+    const int64_t items = syrk_items(ncols, so);
+    const double waves = (double)((items + slots - 1) / slots);
+    const double cost = waves / so;
+    if (cost < best_cost * (1.0 - 1e-9)) {
+      best_cost = cost;
+      best = so;
+    }
+  }
+  return best;
+}
+
+size_t syrk_part_doubles(int ncols, int nsplit) { return (size_t)syrk_items(ncols, nsplit) * ST * ST; }
 
 // partials only (the reduction over splits, and over rounds, is launch_syrk_reduce)
 cudaError_t launch_syrk_part(const double* W, int64_t ldw, int64_t nrows, int ncols, int nsplit, double* Gpart,
                              cudaStream_t s) {
-  const int nt = syrk_ntiles(ncols);
+  const int nt1 = (ncols + ST - 1) / ST;
+  const int so = nsplit, sd = syrk_diag_splits(so);
   if (nrows <= 0) return cudaMemsetAsync(Gpart, 0, syrk_part_doubles(ncols, nsplit) * sizeof(double), s);
-  int64_t rps = (nrows + nsplit - 1) / nsplit;
-  rps = (rps + SK - 1) / SK * SK;  // stages never straddle two splits
+  auto rps_of = [&](int ns) {
+    int64_t r = (nrows + ns - 1) / ns;
+    return (r + SK - 1) / SK * SK;  // stages never straddle two splits
+  };
   CUtensorMap tm;
   cudaError_t e = make_tmap_f64(&tm, W, (uint64_t)nrows, (uint64_t)ncols, (uint64_t)ldw, SK);
   if (e != cudaSuccess) return e;
   e = smem_optin(syrk_tma_kernel, SYRK_SMEM);
   if (e != cudaSuccess) return e;
-  syrk_tma_kernel<<<nt * nsplit, 32 * (NCONS + 1), SYRK_SMEM, s>>>(tm, nrows, nt, rps, Gpart);
+  syrk_tma_kernel<<<syrk_items(ncols, so), 32 * (NCONS + 1), SYRK_SMEM, s>>>(tm, nrows, nt1, sd, so, rps_of(sd), rps_of(so),
+                                                                  Gpart);
   return cudaGetLastError();
 }
 
-cudaError_t launch_syrk_reduce(const double* Gpart, int ntiles, int nsplit_total, int ncols, double* G, int ldg,
+cudaError_t launch_syrk_reduce(const double* Gpart, int ncols, int nsplit, int nlaunch, double* G, int ldg,
                                cudaStream_t s) {
-  const int64_t tot = (int64_t)ntiles * ST * ST;
-  syrk_reduce_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(Gpart, ntiles, nsplit_total, ncols, G, ldg);
+  const int nt1 = (ncols + ST - 1) / ST;
+  const int64_t tot = (int64_t)syrk_ntiles(ncols) * ST * ST;
+  syrk_reduce_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(Gpart, nt1, syrk_diag_splits(nsplit), nsplit,
+                                                                   nlaunch, ncols, G, ldg);
   return cudaGetLastError();
 }
 
@@ -236,7 +275,7 @@ cudaError_t launch_syrk(const double* W, int64_t ldw, int64_t nrows, int ncols, 
                         double* G, int ldg, cudaStream_t s) {
   cudaError_t e = launch_syrk_part(W, ldw, nrows, ncols, nsplit, Gpart, s);
   if (e != cudaSuccess) return e;
-  return launch_syrk_reduce(Gpart, syrk_ntiles(ncols), nsplit, ncols, G, ldg, s);
+  return launch_syrk_reduce(Gpart, ncols, nsplit, 1, G, ldg, s);
 }
 
 }  // namespace vif

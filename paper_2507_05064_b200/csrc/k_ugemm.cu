@@ -122,7 +122,8 @@ __global__ void __launch_bounds__(256) kx_eval_d_kernel(const double* __restrict
 // rows (BN x 16) with cp.async.bulk.tensor (boxes of 16 doubles x rows, SWIZZLE_128B) through a GS-stage
 // shared-memory ring, completing on per-stage "full" mbarriers; (BM / 32) x (BN / 32) consumer warps of
 // 32 x 32 wait on "full", run the DMMAs and release the stage on its "empty" mbarrier (no CTA barrier in
-// the main loop).  One CTA per SM: 96 x 128 tiles (12 consumer warps + the producer = 13 warps, at most
+// the main loop).  Persistent: one CTA per SM walks a static tile schedule, and the producer runs ahead
+// into the next tile while the consumers store the last one.  96 x 128 tiles (12 consumer warps + the producer = 13 warps, at most
 // 4 per SMSP, so 128 registers each), or 128 x 64 for N <= 64.
 //
 // Fragments (k contiguous in both operands): lane l holds row l/4 of an 8-row block and the k-pair
@@ -154,13 +155,19 @@ __global__ void __launch_bounds__(GemmCfg<BM, BN>::THREADS, 1) gemm_tn_tma_kerne
   uint64_t* full = reinterpret_cast<uint64_t*>(sm + GS * Cfg::STAGE);
   uint64_t* empty = full + GS;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  // 1-D grid, column block fastest: the CTAs sharing an A row block run together (A from L2)
+  // persistent CTAs, static schedule: CTA b takes tiles b, b + G, b + 2G, ...; tile t -> row block t / ncb and
+  // column block (t + t / ncb) % ncb, so the G tiles in flight at once cover few row blocks (A from L2) and a
+  // CTA's sequence rotates through the column blocks (a triangular B makes them cost 1 : 2 : ... : ncb)
   const int ncb = (N + BN - 1) / BN;
-  const int64_t row0 = (int64_t)(blockIdx.x / ncb) * BM;
-  const int col0 = (blockIdx.x % ncb) * BN;
-  int kend = K;
-  if (tri && col0 + BN < kend) kend = col0 + BN;
-  const int nkt = (kend + GBK - 1) / GBK;
+  const int ntiles = (int)(((npos + BM - 1) / BM) * ncb);
+  auto tile_of = [&](int t, int64_t& row0, int& col0, int& nkt) {
+    const int rb = t / ncb;
+    row0 = (int64_t)rb * BM;
+    col0 = ((t + rb) % ncb) * BN;
+    int kend = K;
+    if (tri && col0 + BN < kend) kend = col0 + BN;
+    nkt = (kend + GBK - 1) / GBK;
+  };
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < GS; ++s) {
@@ -171,17 +178,23 @@ __global__ void __launch_bounds__(GemmCfg<BM, BN>::THREADS, 1) gemm_tn_tma_kerne
   }
   __syncthreads();
 
-  if (warp == Cfg::NCW) {  // ---------------- producer ----------------
+  if (warp == Cfg::NCW) {  // ---------------- producer: runs ahead across tile boundaries ----------------
     if (lane == 0) {
       tma_prefetch_desc(&tmA);
       tma_prefetch_desc(&tmB);
-      for (int kt = 0; kt < nkt; ++kt) {
-        const int s = kt % GS;
-        if (kt >= GS) mbar_wait(&empty[s], ((kt / GS) + 1) & 1);
-        mbar_expect_tx(&full[s], Cfg::STAGE);
-        uint8_t* st = sm + s * Cfg::STAGE;
-        tma_load_2d(st, &tmA, kt * GBK, (int)row0, &full[s]);
-        tma_load_2d(st + Cfg::ABYTES, &tmB, kt * GBK, col0, &full[s]);
+      int it = 0;  // global stage counter of this CTA
+      for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        int64_t row0;
+        int col0, nkt;
+        tile_of(t, row0, col0, nkt);
+        for (int kt = 0; kt < nkt; ++kt, ++it) {
+          const int s = it % GS;
+          if (it >= GS) mbar_wait(&empty[s], (unsigned)(((it / GS) + 1) & 1));
+          mbar_expect_tx(&full[s], Cfg::STAGE);
+          uint8_t* st = sm + s * Cfg::STAGE;
+          tma_load_2d(st, &tmA, kt * GBK, (int)row0, &full[s]);
+          tma_load_2d(st + Cfg::ABYTES, &tmB, kt * GBK, col0, &full[s]);
+        }
       }
     }
     return;
@@ -189,14 +202,6 @@ __global__ void __launch_bounds__(GemmCfg<BM, BN>::THREADS, 1) gemm_tn_tma_kerne
 
   // ---------------- consumers: (BM/32) x (BN/32) warps of 32 x 32 ----------------
   const int wm = warp % Cfg::WM, wn = warp / Cfg::WM;
-  // a warp's 32 columns end at col0 + 32 (wn + 1): with a triangular B it skips later K-tiles
-  const int kend_w = tri ? min(kend, col0 + 32 * (wn + 1)) : kend;
-  const int nkt_w = (kend_w + GBK - 1) / GBK;
-  double acc[4][4][2];
-#pragma unroll
-  for (int a = 0; a < 4; ++a)
-#pragma unroll
-    for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
   const int fr = lane >> 2, t4 = lane & 3;
   // byte offsets inside a stage of the 16-byte fragment loads: row (block*8 + fr), k-pair chunk kh*4 + t4
   uint32_t offA[2][4], offB[2][4];
@@ -209,57 +214,71 @@ __global__ void __launch_bounds__(GemmCfg<BM, BN>::THREADS, 1) gemm_tn_tma_kerne
       offB[kh][q] = (uint32_t)(Cfg::ABYTES + rb * 128 + (((kh * 4 + t4) ^ (rb & 7)) << 4));
     }
   const uint32_t sbase = smem_u32(sm);
-  for (int kt = 0; kt < nkt; ++kt) {
-    const int s = kt % GS;
-    mbar_wait(&full[s], (kt / GS) & 1);
-    if (kt < nkt_w) {
-      const uint32_t st = sbase + s * Cfg::STAGE;
-#pragma unroll
-      for (int kh = 0; kh < 2; ++kh) {
-        double2 af[4], bf[4];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          af[q] = lds_f64x2(st + offA[kh][q]);
-          bf[q] = lds_f64x2(st + offB[kh][q]);
-        }
-#pragma unroll
-        for (int a = 0; a < 4; ++a)
-#pragma unroll
-          for (int b = 0; b < 4; ++b) dmma884(acc[a][b][0], acc[a][b][1], af[a].x, bf[b].x);
-#pragma unroll
-        for (int a = 0; a < 4; ++a)
-#pragma unroll
-          for (int b = 0; b < 4; ++b) dmma884(acc[a][b][0], acc[a][b][1], af[a].y, bf[b].y);
-      }
-    }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[s]);
-  }
   const bool pair = !((N | ldc) & 1);  // 16-byte stores need an even N and ldc
-  // epilogue: lane holds C[fr][2*(lane&3) + {0,1}] of each 8x8 tile
+  int it = 0;
+  for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    int64_t row0;
+    int col0, nkt;
+    tile_of(t, row0, col0, nkt);
+    // a warp's 32 columns end at col0 + 32 (wn + 1): with a triangular B it skips later K-tiles
+    int kend_w = tri ? min(K, col0 + 32 * (wn + 1)) : K;
+    const int nkt_w = (kend_w + GBK - 1) / GBK;
+    double acc[4][4][2];
 #pragma unroll
-  for (int a = 0; a < 4; ++a) {
-    const int64_t p = row0 + wm * 32 + a * 8 + fr;
-    if (p >= npos) continue;
-    const int64_t i = pos_to_row(pos0 + p, chunk, world, rank);
-    if (i >= n) continue;
+    for (int a = 0; a < 4; ++a)
 #pragma unroll
-    for (int b = 0; b < 4; ++b) {
-      const int c = col0 + wn * 32 + b * 8 + t4 * 2;
-      if (c < N) {
-        if (pair) {
-          double2* dst = reinterpret_cast<double2*>(C + i * ldc + c);
-          double2 v = make_double2(alpha * acc[a][b][0], alpha * acc[a][b][1]);
-          if (accum) {  // C += alpha A B^T (gradient path)
-            const double2 o = *dst;
-            v.x += o.x;
-            v.y += o.y;
+      for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+    for (int kt = 0; kt < nkt; ++kt, ++it) {
+      const int s = it % GS;
+      mbar_wait(&full[s], (unsigned)((it / GS) & 1));
+      if (kt < nkt_w) {
+        const uint32_t st = sbase + s * Cfg::STAGE;
+#pragma unroll
+        for (int kh = 0; kh < 2; ++kh) {
+          double2 af[4], bf[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            af[q] = lds_f64x2(st + offA[kh][q]);
+            bf[q] = lds_f64x2(st + offB[kh][q]);
           }
-          *dst = v;
-        } else {  // odd N or ldc (Laplace path: one right-hand side)
-          double* dst = C + i * ldc + c;
-          dst[0] = alpha * acc[a][b][0] + (accum ? dst[0] : 0.0);
-          if (c + 1 < N) dst[1] = alpha * acc[a][b][1] + (accum ? dst[1] : 0.0);
+#pragma unroll
+          for (int a = 0; a < 4; ++a)
+#pragma unroll
+            for (int b = 0; b < 4; ++b) dmma884(acc[a][b][0], acc[a][b][1], af[a].x, bf[b].x);
+#pragma unroll
+          for (int a = 0; a < 4; ++a)
+#pragma unroll
+            for (int b = 0; b < 4; ++b) dmma884(acc[a][b][0], acc[a][b][1], af[a].y, bf[b].y);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+    }
+    // epilogue (the producer is already filling the next tile's stages): lane holds C[fr][2*(lane&3) + {0,1}]
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+      const int64_t p = row0 + wm * 32 + a * 8 + fr;
+      if (p >= npos) continue;
+      const int64_t i = pos_to_row(pos0 + p, chunk, world, rank);
+      if (i >= n) continue;
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        const int c = col0 + wn * 32 + b * 8 + t4 * 2;
+        if (c < N) {
+          if (pair) {
+            double2* dst = reinterpret_cast<double2*>(C + i * ldc + c);
+            double2 v = make_double2(alpha * acc[a][b][0], alpha * acc[a][b][1]);
+            if (accum) {  // C += alpha A B^T (gradient path)
+              const double2 o = *dst;
+              v.x += o.x;
+              v.y += o.y;
+            }
+            *dst = v;
+          } else {  // odd N or ldc (Laplace path: one right-hand side)
+            double* dst = C + i * ldc + c;
+            dst[0] = alpha * acc[a][b][0] + (accum ? dst[0] : 0.0);
+            if (c + 1 < N) dst[1] = alpha * acc[a][b][1] + (accum ? dst[1] : 0.0);
+          }
         }
       }
     }
@@ -282,7 +301,11 @@ static cudaError_t gemm_tn_tma(const double* A, int64_t lda, int64_t npos, const
     if (e != cudaSuccess) return e;
     e = smem_optin(kern, Cfg::SMEM);
     if (e != cudaSuccess) return e;
-    const unsigned grid = (unsigned)(((npos + BM - 1) / BM) * ((N + BN - 1) / BN));
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int64_t tiles = ((npos + BM - 1) / BM) * ((N + BN - 1) / BN);
+    const unsigned grid = (unsigned)std::min<int64_t>(tiles, sms);  // persistent: one CTA per SM
     kern<<<grid, Cfg::THREADS, Cfg::SMEM, s>>>(ta, tb, npos, N, K, tri, C, ldc, n, chunk, world, rank, pos0, alpha,
                                                 accum);
     return cudaGetLastError();

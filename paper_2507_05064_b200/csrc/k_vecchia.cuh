@@ -23,7 +23,6 @@
 #include "kernels.h"
 #include <stdlib.h>
 
-#include <type_traits>
 
 namespace vif {
 
@@ -624,286 +623,6 @@ __global__ void __launch_bounds__(VW * 32, MINB) vecchia_reg_kernel(
   }
 }
 
-// ------------------------------------------------------------------------------------------
-// Software-pipelined register variant (s <= 32, m >= 8 s): every warp runs a sequence of points (point
-// k+1 = point k + all warps of the grid, so the points in flight stay Morton-adjacent) and interleaves, in
-// one instruction stream, the scalar phases of point k -- the SP Cholesky pivots, the back substitution and
-// the W pass -- with the DMMA Gram of point k+1 (8-column chunks of the register ring, one or two per
-// pivot / substitution step / W row pair).  The dependent FP64 chains of the scalar phases (each step waits
-// ~25-40 cycles behind DMMAs on the SMSP's FP64 unit, tools/dmma_mix.cu) then run in the shadow of the next
-// point's DMMAs instead of idling the tensor pipe (the register kernel sits at ~72% of the
-// shared FP64-pipe bound for exactly that reason).  One C buffer per warp: the next point's K(X_S, X_S) is
-// evaluated into it after the current point's back substitution has consumed L.
-#ifndef VPIPE_MINB
-#define VPIPE_MINB 2  // CTAs (4 warps) per SM: 255 registers, no spills (3 CTAs: 168 registers, 2 KB of spills)
-#endif
-template <int RB>
-__host__ __device__ constexpr int vpipe_warp_doubles(int d) {
-  return RB * 8 * (RB * 8 + 1) + 2 * RB * 8 + RB * 8 + 2 * RB * 8 * d;  // C, colbuf[2], coef, xs[2]
-}
-
-template <int FAM, int RB, int DD>
-__global__ void __launch_bounds__(VW * 32, VPIPE_MINB) vecchia_pipe_kernel(
-    const double* __restrict__ U, int64_t ldu, int mk, int ld, const double* __restrict__ X,
-    const int32_t* __restrict__ nbr, int mv, const int64_t* __restrict__ order, int64_t npts, CovParams p,
-    double* __restrict__ W, int64_t ldw, double* __restrict__ Dpos, double* __restrict__ B_out,
-    double* __restrict__ D_out, DevStatus* __restrict__ st, double* __restrict__ gstate) {
-  constexpr int SP = RB * 8;
-  constexpr int CS = SP + 1;
-  constexpr int NT = RB * (RB + 1) / 2;
-  constexpr int NB = 2;  // ring depth (8-column chunks in flight per row block)
-  static_assert(SP <= 32 && SP % NB == 0, "register pipeline needs s <= 32");
-  extern __shared__ __align__(16) double vsm[];
-  __shared__ int Sidx_all[VW][2][SP];
-  __shared__ double tbl[64];
-  exp_table_init(tbl, p.sigma2, threadIdx.x);
-  __syncthreads();
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int dd = DD > 0 ? DD : p.d;
-  double* C = vsm + warp * vpipe_warp_doubles<RB>(dd);
-  double* colbuf = C + SP * CS;  // [2][SP]
-  double* coef = colbuf + 2 * SP;  // [SP]
-  double* xsb = coef + SP;         // [2][SP][d]
-  const int64_t NW = (int64_t)gridDim.x * VW;
-  int64_t pos = (int64_t)blockIdx.x * VW + warp;
-  if (pos >= npts) return;
-  const int nch = mk / 8;  // 8-column chunks of the Gram (mk is a multiple of 8)
-
-  double acc[NT][2];
-  const double* rp[RB];
-  double2 f[NB][RB];
-  // one 8-column chunk c of the Gram of the point in the ring (slot b = c % NB, a compile-time constant)
-  auto gram_step = [&](auto bc, int c) {
-    constexpr int b = decltype(bc)::value;
-    if (c < nch) {
-      int t = 0;
-#pragma unroll
-      for (int R1 = 0; R1 < RB; ++R1)
-#pragma unroll
-        for (int R2 = 0; R2 <= R1; ++R2, ++t) dmma884(acc[t][0], acc[t][1], f[b][R1].x, f[b][R2].x);
-      t = 0;
-#pragma unroll
-      for (int R1 = 0; R1 < RB; ++R1)
-#pragma unroll
-        for (int R2 = 0; R2 <= R1; ++R2, ++t) dmma884(acc[t][0], acc[t][1], f[b][R1].y, f[b][R2].y);
-      const int kn = (c + NB) * 8;
-#pragma unroll
-      for (int R = 0; R < RB; ++R)
-        f[b][R] = (rp[R] != nullptr && kn < mk) ? __ldg(reinterpret_cast<const double2*>(rp[R] + kn))
-                                                : make_double2(0.0, 0.0);
-    }
-  };
-  auto gram_group = [&](int& g) {  // NB consecutive chunks starting at a multiple of NB
-    gram_step(std::integral_constant<int, 0>{}, g);
-    gram_step(std::integral_constant<int, 1>{}, g + 1);
-    g += NB;
-  };
-  // conditioning set of the point at position ps into buffer b; row pointers and the first NB ring chunks
-  auto setup = [&](int64_t ps, int b, int& qo, int64_t& io) {
-    const int64_t ii = order[ps];
-    const int nb0 = lane < mv ? nbr[ii * mv + lane] : -1;
-    const int qq = __popc(__ballot_sync(0xffffffffu, nb0 >= 0));
-    const int myidx = lane < qq ? nb0 : (lane == qq ? (int)ii : -1);
-    int* Sidx = Sidx_all[warp][b];
-    if (lane < SP) Sidx[lane] = myidx;
-    stage_xs<FAM>(X, X, myidx, dd, p, lane, qq + 1, xsb + b * SP * dd);
-    __syncwarp();
-#pragma unroll
-    for (int R = 0; R < RB; ++R) {
-      const int gi = Sidx[R * 8 + (lane >> 2)];
-      rp[R] = gi >= 0 ? U + (int64_t)gi * ldu + 2 * (lane & 3) : nullptr;
-    }
-    gram_fill<RB, NB>(rp, mk, f);
-    qo = qq;
-    io = ii;
-  };
-  // C -= acc on the lower triangle of rows < s (C holds K(X_S, X_S) + sigma^2 I)
-  auto finish_c = [&](int sn) {
-    __syncwarp();
-    int t = 0;
-#pragma unroll
-    for (int R1 = 0; R1 < RB; ++R1)
-#pragma unroll
-      for (int R2 = 0; R2 <= R1; ++R2, ++t) {
-        const int r = R1 * 8 + (lane >> 2), c = R2 * 8 + 2 * (lane & 3);
-        if (r < sn) {
-          if (c <= r) C[r * CS + c] -= acc[t][0];
-          if (c + 1 <= r) C[r * CS + c + 1] -= acc[t][1];
-        }
-      }
-    __syncwarp();
-  };
-
-  // ---- prologue: the first point's C_S in full ----
-  int cur = 0, q;
-  int64_t i;
-  setup(pos, 0, q, i);
-#pragma unroll
-  for (int t = 0; t < NT; ++t) acc[t][0] = acc[t][1] = 0.0;
-  eval_lower<FAM, 4>(xsb, q + 1, CS, dd, p.nugget, tbl, lane, C);
-  {
-    int g = 0;
-    while (g < nch) gram_group(g);
-  }
-  finish_c(q + 1);
-
-  for (;;) {
-    const int64_t npos = pos + NW;
-    const bool has_next = npos < npts;
-    const int nxt = cur ^ 1;
-    const int s = q + 1;
-    // ---- A: the next point's conditioning set and ring (its Gram runs inside B-F) ----
-    int qn = 0;
-    int64_t in = 0;
-#pragma unroll
-    for (int t = 0; t < NT; ++t) acc[t][0] = acc[t][1] = 0.0;
-    if (has_next) {
-      setup(npos, nxt, qn, in);
-    } else {
-#pragma unroll
-      for (int R = 0; R < RB; ++R) rp[R] = nullptr;
-    }
-    const int nchn = has_next ? nch : 0;
-    // ---- B + C: Cholesky of the current C_S (row `lane` in registers) || Gram chunks 0..SP-1 of the next ----
-    double crow[SP];
-#pragma unroll
-    for (int c = 0; c < SP; ++c) {
-      double v = 0.0;
-      if (lane < s) {
-        if (c <= lane) v = C[lane * CS + c];
-      } else if (c == lane) {
-        v = 1.0;
-      }
-      crow[c] = v;
-    }
-    bool ok = true;
-    double Di = 0.0, myinv = 1.0;
-#pragma unroll
-    for (int j = 0; j < SP; ++j) {
-      const double djj = __shfl_sync(0xffffffffu, crow[j], j);
-      if (j < s) {
-        ok = ok && (djj > 0.0);
-        if (j == s - 1) Di = djj;
-      }
-      const double y = rsqrt_nr(djj);
-      const double lrj = crow[j] * y;
-      crow[j] = lrj;
-      if (lane == j) myinv = y;
-      if (j + 1 < SP) {
-        double* cb = colbuf + (j & 1) * SP;
-        if (lane < SP) cb[lane] = lrj;
-        __syncwarp();
-#pragma unroll
-        for (int c = j + 1; c < SP; ++c) crow[c] = fma(-lrj, cb[c], crow[c]);
-      }
-      if (j % NB == 0) gram_step(std::integral_constant<int, 0>{}, j);
-      else gram_step(std::integral_constant<int, 1>{}, j);
-    }
-    int g = SP;  // next Gram chunk (a multiple of NB)
-    // rows of L to shared memory (row-major) for the back substitution
-    __syncwarp();
-#pragma unroll
-    for (int c = 0; c < SP; ++c)
-      if (lane < SP) C[lane * CS + c] = crow[c];
-    __syncwarp();
-    const int qb = ok ? q : 0;  // a failed point writes a zero W row (coef = 0) and no B row
-    // ---- D: A_i^T = L_NN^{-T} l (lane k holds x_k) || Gram chunks ----
-    double a = lane < qb ? C[q * CS + lane] : 0.0;
-    for (int j = qb - 1; j >= 0;) {
-      {
-        const double xj = __shfl_sync(0xffffffffu, a * myinv, j);
-        if (lane == j) a = xj;
-        else if (lane < j) a = fma(-C[j * CS + lane], xj, a);
-        --j;
-      }
-      if (j >= 0) {
-        const double xj = __shfl_sync(0xffffffffu, a * myinv, j);
-        if (lane == j) a = xj;
-        else if (lane < j) a = fma(-C[j * CS + lane], xj, a);
-        --j;
-      }
-      gram_group(g);
-    }
-    // ---- E: coefficients of the W row, B row, gradient state ----
-    if (ok) {
-      const double rs = rsqrt_nr(Di);
-      if (lane < SP) coef[lane] = lane < q ? -a * rs : (lane == q ? rs : 0.0);
-      if (B_out && lane < mv) B_out[i * mv + lane] = lane < q ? -a : 0.0;
-      if (gstate) {
-        constexpr int LP = SP * (SP + 1) / 2;
-        double* sp = gstate + pos * (int64_t)vif_state_doubles<RB>();
-        for (int e = lane; e < LP; e += 32) {
-          int r = (int)((sqrtf_fast(8.0f * (float)e + 1.0f) - 1.0f) * 0.5f);
-          if ((r + 1) * (r + 2) / 2 <= e) ++r;
-          if (r * (r + 1) / 2 > e) --r;
-          sp[e] = C[r * CS + e - r * (r + 1) / 2];
-        }
-        if (lane < SP) {
-          sp[LP + lane] = lane < q ? a : 0.0;
-          sp[LP + SP + lane] = myinv;
-        }
-        if (lane == 0) {
-          sp[LP + 3 * SP] = Di;
-          sp[LP + 3 * SP + 1] = 1.0;
-        }
-      }
-    } else {
-      if (lane < SP) coef[lane] = 0.0;
-      if (lane == 0) atomicMin(&st->bad_row, (unsigned long long)i);
-    }
-    __syncwarp();
-    // ---- E': K(X_S, X_S) + sigma^2 I of the next point into C (L is no longer needed) ----
-    if (has_next) eval_lower<FAM, 4>(xsb + nxt * SP * dd, qn + 1, CS, dd, p.nugget, tbl, lane, C);
-    // ---- F: w_i, r_i over ld columns (rows two at a time, 16 loads in flight per lane) || Gram chunks ----
-    {
-      const int* Sidx = Sidx_all[warp][cur];
-      for (int c0 = 0; c0 < ld; c0 += 512) {
-        double2 o[8];
-#pragma unroll
-        for (int t = 0; t < 8; ++t) o[t] = make_double2(0.0, 0.0);
-        for (int k = 0; k < s; k += 2) {
-          double2 u0[8], u1[8];
-          const double* r0 = U + (int64_t)Sidx[k] * ldu + c0 + 2 * lane;
-          const bool has1 = k + 1 < s;
-          const double* r1 = has1 ? U + (int64_t)Sidx[k + 1] * ldu + c0 + 2 * lane : r0;
-#pragma unroll
-          for (int t = 0; t < 8; ++t) {
-            const bool inr = c0 + 2 * lane + 64 * t < ld;
-            u0[t] = inr ? __ldg(reinterpret_cast<const double2*>(r0 + 64 * t)) : make_double2(0.0, 0.0);
-            u1[t] = (inr && has1) ? __ldg(reinterpret_cast<const double2*>(r1 + 64 * t)) : make_double2(0.0, 0.0);
-          }
-          if (g < nchn) gram_group(g);
-          const double f0 = coef[k], f1 = has1 ? coef[k + 1] : 0.0;
-#pragma unroll
-          for (int t = 0; t < 8; ++t) {
-            o[t].x = fma(f0, u0[t].x, o[t].x);
-            o[t].y = fma(f0, u0[t].y, o[t].y);
-            o[t].x = fma(f1, u1[t].x, o[t].x);
-            o[t].y = fma(f1, u1[t].y, o[t].y);
-          }
-        }
-#pragma unroll
-        for (int t = 0; t < 8; ++t) {
-          const int c = c0 + 2 * lane + 64 * t;
-          if (c < ld) *reinterpret_cast<double2*>(W + pos * ldw + c) = o[t];
-        }
-      }
-    }
-    if (lane == 0) {
-      Dpos[pos] = ok ? Di : 1.0;
-      if (D_out) D_out[i] = ok ? Di : __longlong_as_double(0x7ff8000000000000LL);
-    }
-    if (!has_next) break;
-    // ---- G: the rest of the next point's Gram; C_S = K + sigma^2 I - G_S ----
-    while (g < nchn) gram_group(g);
-    finish_c(qn + 1);
-    pos = npos;
-    q = qn;
-    i = in;
-    cur = nxt;
-  }
-}
-
 template <int FAM, int RB>
 static cudaError_t launch_reg(const VecchiaArgs& a, cudaStream_t s) {
   const unsigned blocks = (unsigned)((a.npts + VW - 1) / VW);
@@ -956,37 +675,13 @@ static cudaError_t launch_smem(const VecchiaArgs& a, cudaStream_t s) {
 }
 
 template <int FAM, int RB>
-static cudaError_t launch_pipe(const VecchiaArgs& a, cudaStream_t s) {
-  const size_t smem = (size_t)VW * vpipe_warp_doubles<RB>(a.p.d) * sizeof(double);
-  auto kern = a.p.d == 2 ? vecchia_pipe_kernel<FAM, RB, 2> : vecchia_pipe_kernel<FAM, RB, 0>;
-  {
-    cudaError_t e = smem_optin(kern, smem);
-    if (e != cudaSuccess) return e;
-  }
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int64_t need = (a.npts + VW - 1) / VW;
-  const unsigned blocks = (unsigned)std::min<int64_t>(need, (int64_t)sms * VPIPE_MINB);
-  kern<<<blocks, VW * 32, smem, s>>>(a.U, a.ldu, a.mk, a.ld, a.X, a.nbr, a.mv, a.order, a.npts, a.p, a.W, a.ldw,
-                                     a.Dpos, a.B_out, a.D_out, a.st, a.state);
-  return cudaGetLastError();
-}
-
-template <int FAM, int RB>
 static cudaError_t launch_rb(const VecchiaArgs& a, cudaStream_t s) {
   // s <= 32: the per-warp register kernel.  Measured and rejected on B200 (profiles/r01_notes.md):
   // warp-specialised Gram / solver warps (register ring or cp.async shared-memory ring) and a
   // mixed-precision (FP32 Cholesky + FP64 refinement) solver.
-  // (the blocked DMMA Cholesky of the s > 32 kernel measured slower for s <= 32: 9.8-10.5 vs 8.2 ms at
-  // n = 300k, profiles/r02_union_probe.json)
-  if constexpr (RB >= 3 && RB <= 4) {
-    // the software-pipelined kernel for the factor (not prediction: its self row comes from other buffers)
-    // when the Gram is long enough to hide a point's scalar phases (VIF_VECCHIA_PIPE=0 disables it)
-    static const char* pe = getenv("VIF_VECCHIA_PIPE");
-    const bool pipe = !(pe && pe[0] == '0');
-    if (pipe && !a.Uself && a.mk >= 8 * RB * 8) return launch_pipe<FAM, RB>(a, s);
-  }
+  // (measured slower for s <= 32, profiles/r02_notes.md: the blocked DMMA Cholesky of the s > 32 kernel,
+  // 9.8-10.5 vs 8.2 ms at n = 300k; a software-pipelined warp that overlaps point k's Cholesky / solve / W
+  // pass with point k+1's Gram chunk by chunk, 46.7 vs 27.8 ms at n = 1M -- 242 registers, 8 warps per SM)
   if constexpr (RB <= 4) return launch_reg<FAM, RB>(a, s);
   else return launch_smem<FAM, RB>(a, s);
 }

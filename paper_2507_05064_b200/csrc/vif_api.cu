@@ -1003,7 +1003,6 @@ int vif_factor(void* handle, const vif_theta* theta, double* B_out, double* D_ou
     //   s   : [all SYRK] fixed-order reduction of the R x nsplit partials, sum log D
     // The K1 scratch of round r is the W rows of round r (row stride ld), so it never overlaps the W
     // rows that earlier rounds' vecchia launches are writing.
-    const int nt = syrk_ntiles(P.ld);
     const size_t part_round = syrk_part_doubles(P.ld, P.nsplit_round);
     VIF_CUDA(h, cudaEventRecord(h->ev_k0, s), "event");
     VIF_CUDA(h, cudaStreamWaitEvent(h->s_k1, h->ev_k0, 0), "event wait");
@@ -1065,7 +1064,7 @@ int vif_factor(void* handle, const vif_theta* theta, double* B_out, double* D_ou
     VIF_CUDA(h, cudaEventRecord(h->ev_sy, h->s_sy), "event");
     VIF_CUDA(h, cudaStreamWaitEvent(s, h->ev_sy, 0), "event wait");
     h->mark(S_SYRK, 0);
-    VIF_CUDA(h, launch_syrk_reduce(h->buf<double>(B_GPART), nt, (int)(P.rounds * P.nsplit_round), P.ld, G, P.ld, s),
+    VIF_CUDA(h, launch_syrk_reduce(h->buf<double>(B_GPART), P.ld, P.nsplit_round, (int)P.rounds, G, P.ld, s),
              "syrk reduce");
     h->mark(S_SYRK, 1);
     h->mark(S_REDUCE, 0);
@@ -1588,9 +1587,20 @@ int vif_neighbors(void* handle, const vif_theta* theta, int32_t mv, int32_t* nbr
       qstride = G;
     }
   }
-  VIF_CUDA(h, launch_knn(h->buf<double>(B_U), P.ld, P.m, P.mk, h->buf<double>(B_X), P.n, p, isd, deg, mv, nbr_out, s,
-                         qoff, qstride),
-           "neighbour search");
+  // exact sub-quadratic search (metric pruning of Morton clusters, k_knn.cu) for d <= 3 beyond the first
+  // VIF_KNN_PREFIX (default 65536) rows, which -- and every d > 3 -- take the brute force (the early rows'
+  // neighbours are far away: no cluster can be pruned for them); scratch: the rest of the buffer holding isd
+  static const char* pre_env = getenv("VIF_KNN_PREFIX");  // test hook: a small prefix exercises the pruning
+  const int64_t prefix = pre_env && atoll(pre_env) > 0 ? atoll(pre_env) : 65536;
+  {
+    const Buf sb = P.m > 0 ? B_W : B_U;
+    const size_t used = ((size_t)P.n * 12 + 255) / 256 * 256;
+    char* scr = reinterpret_cast<char*>(isd) + used;
+    const size_t avail = h->L.size[sb] > used ? h->L.size[sb] - used : 0;
+    VIF_CUDA(h, launch_knn_pruned(h->buf<double>(B_U), P.ld, P.m, P.mk, h->buf<double>(B_X), P.n, p, isd, deg, mv,
+                                  nbr_out, s, qoff, qstride, scr, avail, prefix),
+             "neighbour search");
+  }
   {
     int r = mark_inputs_used(h);
     if (r != VIF_OK) return r;
