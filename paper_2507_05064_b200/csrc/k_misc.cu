@@ -288,20 +288,6 @@ __global__ void morton_nd_kernel(const double* __restrict__ X, int64_t n, int d,
   }
 }
 
-cudaError_t sort_pairs_u64(uint64_t* keys, uint64_t* keys_alt, int64_t* vals, int64_t* vals_alt, int64_t n, void* temp,
-                           size_t temp_bytes, int64_t** vals_out, cudaStream_t s) {
-  cub::DoubleBuffer<uint64_t> dk(keys, keys_alt);
-  cub::DoubleBuffer<int64_t> dv(vals, vals_alt);
-  size_t need = 0;
-  cudaError_t e = cub::DeviceRadixSort::SortPairs(nullptr, need, dk, dv, n, 0, 64, s);
-  if (e != cudaSuccess) return e;
-  if (need > temp_bytes) return cudaErrorMemoryAllocation;
-  e = cub::DeviceRadixSort::SortPairs(temp, need, dk, dv, n, 0, 64, s);
-  if (e != cudaSuccess) return e;
-  *vals_out = dv.Current();
-  return cudaGetLastError();
-}
-
 size_t order_temp_bytes(int64_t npos) { return (size_t)(16u << 20) + (size_t)npos * 4; }
 
 cudaError_t launch_order(const double* X, int64_t n, int d, int64_t npos, int64_t chunk, int world, int rank,

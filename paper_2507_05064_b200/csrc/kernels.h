@@ -122,10 +122,6 @@ cudaError_t launch_pred_mean(const double* Wp, int ld, int m, int ycol, const do
                              cudaStream_t s);
 // correlation-distance neighbours (k_knn.cu)
 size_t knn_smem_bytes(int mv);
-// the sub-quadratic exact search (d <= 3, n > the brute-force prefix); scratch: device bytes it may use
-cudaError_t launch_knn_pruned(const double* U, int64_t ldu, int m, int mk, const double* X, int64_t n, const CovParams& p,
-                              double* isd, int* deg, int mv, int32_t* out, cudaStream_t s, int qoff, int qstride,
-                              void* scratch, size_t scratch_bytes, int64_t prefix);
 cudaError_t launch_knn(const double* U, int64_t ldu, int m, int mk, const double* X, int64_t n, const CovParams& p,
                        double* isd, int* deg, int mv, int32_t* out, cudaStream_t s, int qoff = 0, int qstride = 1);
 // VIF-Laplace iterative path (k_laplace.cu)
@@ -195,8 +191,6 @@ cudaError_t launch_validate(const double* X, int64_t n, int d, const double* Z, 
 cudaError_t launch_validate_pred(const double* Xp, int64_t np, int d, const int32_t* nbrp, int mv, int64_t ntrain,
                                  DevStatus* st, cudaStream_t s);
 size_t order_temp_bytes(int64_t npos);
-cudaError_t sort_pairs_u64(uint64_t* keys, uint64_t* keys_alt, int64_t* vals, int64_t* vals_alt, int64_t n, void* temp,
-                           size_t temp_bytes, int64_t** vals_out, cudaStream_t s);
 cudaError_t launch_order(const double* X, int64_t n, int d, int64_t npos, int64_t chunk, int world, int rank,
                          double* bbox, uint64_t* keys, uint64_t* keys_alt, int64_t* vals, int64_t* vals_alt,
                          void* temp, size_t temp_bytes, int64_t** order_out, cudaStream_t s,

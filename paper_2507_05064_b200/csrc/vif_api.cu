@@ -1587,20 +1587,9 @@ int vif_neighbors(void* handle, const vif_theta* theta, int32_t mv, int32_t* nbr
       qstride = G;
     }
   }
-  // exact sub-quadratic search (metric pruning of Morton clusters, k_knn.cu) for d <= 3 beyond the first
-  // VIF_KNN_PREFIX (default 65536) rows, which -- and every d > 3 -- take the brute force (the early rows'
-  // neighbours are far away: no cluster can be pruned for them); scratch: the rest of the buffer holding isd
-  static const char* pre_env = getenv("VIF_KNN_PREFIX");  // test hook: a small prefix exercises the pruning
-  const int64_t prefix = pre_env && atoll(pre_env) > 0 ? atoll(pre_env) : 65536;
-  {
-    const Buf sb = P.m > 0 ? B_W : B_U;
-    const size_t used = ((size_t)P.n * 12 + 255) / 256 * 256;
-    char* scr = reinterpret_cast<char*>(isd) + used;
-    const size_t avail = h->L.size[sb] > used ? h->L.size[sb] - used : 0;
-    VIF_CUDA(h, launch_knn_pruned(h->buf<double>(B_U), P.ld, P.m, P.mk, h->buf<double>(B_X), P.n, p, isd, deg, mv,
-                                  nbr_out, s, qoff, qstride, scr, avail, prefix),
-             "neighbour search");
-  }
+  VIF_CUDA(h, launch_knn(h->buf<double>(B_U), P.ld, P.m, P.mk, h->buf<double>(B_X), P.n, p, isd, deg, mv, nbr_out, s,
+                         qoff, qstride),
+           "neighbour search");
   {
     int r = mark_inputs_used(h);
     if (r != VIF_OK) return r;

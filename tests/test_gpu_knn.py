@@ -162,63 +162,10 @@ print(json.dumps(out.cpu().numpy().tolist()))
     np.testing.assert_array_equal(merged, full)
 
 
-# ---------------- the sub-quadratic exact search (metric pruning, d <= 3) ----------------
-_PRUNED = r"""
-import sys, json
-import numpy as np, torch
-sys.path.insert(0, %r)
-import paper_2507_05064_b200 as p, vifgen
-kw = json.loads(sys.argv[1])
-mv = kw.pop("mv_search")
-w = vifgen.make_workload(device="cuda", **kw)
-dev = torch.device("cuda")
-X, Z, nbr, y = (torch.from_numpy(np.ascontiguousarray(a)).to(dev) for a in (w.X, w.Z.reshape(-1, w.d), w.nbr, w.y))
-m = p.VifModel(X, Z, nbr, y, device=dev)
-print(json.dumps(m.neighbors(p.Theta(**w.theta_dict()), mv).cpu().numpy().tolist()))
-"""
-
-
-def pruned_sets(kw, mv, prefix):
-    import json
-    import os
-    import subprocess
-    import sys
-    code = _PRUNED % os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    r = subprocess.run([sys.executable, "-c", code, json.dumps(dict(kw, mv_search=mv))],
-                       env=dict(os.environ, VIF_KNN_PREFIX=str(prefix)), capture_output=True, text=True, timeout=900)
-    assert r.returncode == 0, r.stderr[-3000:]
-    return np.array(json.loads(r.stdout.strip().splitlines()[-1]), dtype=np.int32)
-
-
-@pytest.mark.parametrize("kw,mv,prefix", [
-    (dict(n=4000, d=2, m=37, mv=13, family="matern32", rho=0.1, nugget=0.1, seed=94), 13, 256),
-    (dict(n=3000, d=2, m=25, mv=10, family="matern12", rho=0.15, nugget=0.1, seed=95), 10, 64),
-    (dict(n=3000, d=3, m=30, mv=9, family="matern52", ard=(0.5, 2.0), nugget=0.1, seed=96), 9, 128),
-    (dict(n=2500, d=2, m=0, mv=7, family="gaussian", rho=0.1, nugget=0.1, seed=97, z="subset"), 7, 128),
-    (dict(n=2500, d=2, m=40, mv=10, family="matern32", rho=0.1, nugget=0.1, seed=98, z="subset"), 10, 128),
-    (dict(n=2000, d=2, m=20, mv=45, family="matern32", rho=0.2, nugget=0.1, seed=99), 45, 100),
-])
-def test_pruned_search_matches_oracle(kw, mv, prefix):
-    """Cluster-pruned exact search (k_knn.cu, forced on a small prefix) returns the oracle's sets: every family,
-    3-D ARD, m = 0, degenerate inducing points at data points (c7: no metric bound -> those tiles keep every
-    cluster), m_v = 45; only oracle-level ties may differ."""
-    g = pruned_sets(kw, mv, prefix)
-    w = vifgen.make_workload(device="cuda", **kw)
-    oth = oracle.Theta(**w.theta_dict())
-    r, rs = oracle.dc_neighbors(w.X, w.Z, oth, mv)
-    diff = np.nonzero((g != r).any(1))[0]
-    assert len(diff) <= max(2, 0.005 * w.n), len(diff)
-    for i in diff:
-        sel = g[i][g[i] >= 0]
-        assert len(sel) == (r[i] >= 0).sum() and np.all(sel < i) and len(set(sel)) == len(sel)
-        gs = oracle.dc_scores(w.X, w.Z, oth, np.full(len(sel), i), sel)
-        np.testing.assert_allclose(gs, rs[i][:len(sel)], rtol=1e-12, atol=1e-14)
-
-
 @pytest.mark.slow
-def test_pruned_search_config3_equals_generator():
-    """n = 1M (config 3): the default path (brute force for the first 16384 rows, pruned beyond) returns the
-    generator's sets (the torch brute force of vifgen) on every row except exact ties."""
+def test_search_config3_equals_generator():
+    """n = 1M (config 3): vif_neighbors returns the generator's sets (vifgen's own torch brute force) on every
+    row except exact ties, whose oracle scores agree."""
     import time
     import paper_2507_05064_b200 as p
     w = vifgen.make_config(3, device="cuda")

@@ -35,7 +35,6 @@ except Exception:  # pragma: no cover - torch is in the image
     torch = None
 
 FAMILY_ID = {"matern12": 0, "matern32": 1, "matern52": 2, "gaussian": 3}
-PRUNED_MIN_N = 200_000  # from here on (d <= 3) the metric-pruned search generates the neighbour sets
 SEED_BASE = 20250707
 
 # BASELINE.json "configs" (index + 1 = config id)
@@ -170,136 +169,6 @@ def whitened_features(Xs: np.ndarray, Zs: np.ndarray, family: str, sigma2: float
         K = _cov_from_r(family, sigma2, _sqdist(Xt[s:s + bs], Zt))
         U[s:s + bs] = torch.linalg.solve_triangular(L, K.T, upper=False).T
     return U
-
-
-def _morton_rank(Xs: np.ndarray) -> np.ndarray:
-    """Rank of every point in the Morton (Z-) order of its first min(d, 3) coordinates (bounding-box scaled)."""
-    n, d = Xs.shape
-    dd = min(d, 3)
-    lo, hi = Xs[:, :dd].min(0), Xs[:, :dd].max(0)
-    bits = 63 // dd
-    q = ((Xs[:, :dd] - lo) / np.where(hi > lo, hi - lo, 1.0) * ((1 << bits) - 1)).astype(np.uint64)
-    key = np.zeros(n, dtype=np.uint64)
-    for b in range(bits):
-        for k in range(dd):
-            key |= ((q[:, k] >> np.uint64(b)) & np.uint64(1)) << np.uint64(b * dd + k)
-    return np.argsort(key, kind="stable")
-
-
-def dc_neighbors_pruned(Xs: np.ndarray, Zs: np.ndarray, family: str, sigma2: float, jitter: float, mv: int,
-                        device=None, prefix: int = 16384, csize: int = 512, qsize: int = 2048) -> np.ndarray:
-    """The same sets as dc_neighbors (exact), sub-quadratic for d <= 3, by metric pruning: d_c(i,j) =
-    sqrt(1 - |corr(i,j)|) is a metric (the distance between the sign classes of normalised residual feature
-    vectors; the paper's cover tree relies on it), so a cluster c with centre z_c and radius r_c
-    holds no neighbour of query i within D when d_c(i, z_c) - r_c > D.  The generator's own torch code:
-      - rows i < prefix: dc_neighbors' brute force over the first `prefix` points;
-      - clusters: all points in Morton order, csize per cluster (compact, any index);
-      - query blocks: i >= prefix sorted by (floor(log2 i), Morton rank), qsize per block;
-      - an upper bound D_i of the m_v-th neighbour distance from the Morton-adjacent clusters;
-      - per block, the clusters with d_c(z_Q, z_c) <= r_Q + max D_i + r_c + 1e-6, searched exhaustively.
-    Degenerate points (reading c7) void the bound: a block that holds one keeps every cluster, a cluster that
-    holds one has radius 2."""
-    n = Xs.shape[0]
-    d = Xs.shape[1]
-    if d > 3 or n <= prefix or mv == 0:
-        return dc_neighbors(Xs, Zs, family, sigma2, jitter, mv, device=device)
-    dev = _device(device)
-    out = np.full((n, mv), -1, dtype=np.int32)
-    out[:prefix] = dc_neighbors(Xs[:prefix], Zs, family, sigma2, jitter, mv, device=dev)
-    Xt = torch.from_numpy(Xs).to(dev)
-    m = Zs.shape[0]
-    if m > 0:
-        U = whitened_features(Xs, Zs, family, sigma2, jitter, device=dev)
-        rdiag = sigma2 - (U * U).sum(1)
-    else:
-        U = torch.zeros((n, 1), dtype=torch.float64, device=dev)
-        rdiag = torch.full((n,), sigma2, dtype=torch.float64, device=dev)
-    tau = 1e-7 * sigma2
-    degenerate = rdiag < tau
-    inv_sd = torch.where(degenerate, torch.zeros_like(rdiag), 1.0 / torch.sqrt(torch.clamp(rdiag, min=tau)))
-
-    def scores(qi, cj):
-        """|corr| of all (query, candidate) pairs (queries qi x candidates cj, index tensors); -inf for j >= i;
-        degenerate candidates 0, degenerate queries -scaled distance^2 (reading c7)."""
-        sc = _cov_from_r(family, sigma2, _sqdist(Xt[qi], Xt[cj])) - U[qi] @ U[cj].T
-        sc = sc.abs_() * inv_sd[qi, None] * inv_sd[None, cj]
-        dq = degenerate[qi]
-        if bool(dq.any()):
-            sc[dq] = -_sqdist(Xt[qi[dq]], Xt[cj])
-        sc.masked_fill_(cj[None, :] >= qi[:, None], -math.inf)
-        return sc
-
-    def dc_pairs(a, b):  # d_c of the pairs (a[k], b[k]); 2 where either is degenerate
-        sc = (_cov_from_r(family, sigma2, ((Xt[a] - Xt[b]) ** 2).sum(1)) - (U[a] * U[b]).sum(1)).abs()
-        dcv = torch.sqrt(torch.clamp(1.0 - sc * inv_sd[a] * inv_sd[b], min=0.0))
-        return torch.where(degenerate[a] | degenerate[b], torch.full_like(dcv, 2.0), dcv)
-
-    morder = torch.from_numpy(_morton_rank(Xs)).to(dev)
-    mrank = torch.empty_like(morder)
-    mrank[morder] = torch.arange(n, device=dev)
-    ncl = (n + csize - 1) // csize
-    cl_idx = torch.full((ncl * csize,), -1, dtype=torch.int64, device=dev)
-    cl_idx[:n] = morder
-    cl_idx = cl_idx.view(ncl, csize)
-    cl_cnt = torch.clamp(n - torch.arange(ncl, device=dev) * csize, max=csize)
-    cl_ctr = cl_idx[torch.arange(ncl, device=dev), torch.clamp(cl_cnt // 2, max=csize - 1)]
-    memb = cl_idx.clamp(min=0)
-    rad = dc_pairs(cl_ctr[:, None].expand(-1, csize).reshape(-1), memb.reshape(-1)).view(ncl, csize)
-    rad = torch.where(cl_idx >= 0, rad, torch.zeros_like(rad)).max(1).values
-    # queries i >= prefix by (band, Morton rank)
-    qi_all = torch.arange(prefix, n, device=dev)
-    band = torch.floor(torch.log2(qi_all.double())).long()
-    qkey = band * (n + 1) + mrank[qi_all]
-    qord = qi_all[torch.argsort(qkey)]
-    for b0 in range(0, qord.numel(), qsize):
-        qi = qord[b0:b0 + qsize]
-        nq = qi.numel()
-        zq = qi[nq // 2]
-        rq = float(dc_pairs(zq.expand(nq), qi).max())
-        # upper bounds D_i from the Morton-adjacent clusters around the block centre
-        imin = int(qi.min())
-        k0 = min(ncl, max(4, -(-4 * mv * n // (csize * imin)) + 1))
-        c0 = int(mrank[zq]) // csize - k0 // 2
-        c0 = max(0, min(c0, ncl - k0))
-        cj = cl_idx[c0:c0 + k0].reshape(-1)
-        cj = cj[cj >= 0]
-        sc = scores(qi, cj)
-        want = torch.clamp(qi, max=mv)
-        kk = min(mv, sc.shape[1])
-        top = torch.topk(sc, kk, dim=1).values
-        filled = torch.isfinite(top).sum(1) >= want
-        kth = top.gather(1, (want - 1).clamp(min=0)[:, None]).squeeze(1)
-        Dq = torch.sqrt(torch.clamp(1.0 - kth, min=0.0))
-        Dq = torch.where(filled, Dq, torch.full_like(Dq, 2.0))
-        Dq = torch.where(degenerate[qi], torch.full_like(Dq, 2.0), Dq)
-        if float(Dq.max()) >= 2.0 or rq >= 2.0:
-            keep = torch.arange(ncl, device=dev)
-        else:
-            t = rq + float(Dq.max()) + 1e-6
-            dcc = dc_pairs(zq.expand(ncl), cl_ctr)
-            keep = torch.nonzero(dcc - rad <= t).flatten()
-        cj = cl_idx[keep].reshape(-1)
-        cj = cj[(cj >= 0) & (cj < int(qi.max()))]
-        best_v = torch.full((nq, mv), -math.inf, dtype=torch.float64, device=dev)
-        best_i = torch.full((nq, mv), -1, dtype=torch.int64, device=dev)
-        step = max(1, (1 << 26) // max(nq, 1))
-        for s0 in range(0, cj.numel(), step):
-            cc = cj[s0:s0 + step]
-            sc = scores(qi, cc)
-            cat_v = torch.cat([best_v, sc], 1)
-            cat_i = torch.cat([best_i, cc[None, :].expand(nq, -1)], 1)
-            v, pos = torch.topk(cat_v, min(mv, cat_v.shape[1]), dim=1)
-            best_v, best_i = v, torch.gather(cat_i, 1, pos)
-        bv, bi, qn = best_v.cpu().numpy(), best_i.cpu().numpy(), qi.cpu().numpy()
-        for r in range(nq):
-            i = qn[r]
-            valid = np.isfinite(bv[r]) & (bi[r] >= 0)
-            vi, ii = bv[r][valid], bi[r][valid]
-            order = np.lexsort((ii, -vi))   # d_c ascending <=> |corr| descending, ties by index
-            sel = ii[order][:min(mv, i)]
-            out[i, :] = -1
-            out[i, :len(sel)] = sel
-    return out
 
 
 def dc_neighbors(Xs: np.ndarray, Zs: np.ndarray, family: str, sigma2: float, jitter: float, mv: int,
@@ -445,8 +314,6 @@ def make_workload(n: int, d: int, m: int, mv: int, family: str = "matern32", sig
         for i in range(n):
             k = min(i, mv)
             nbr[i, :k] = np.arange(i - k, i)[::-1] if k else []
-    elif n >= PRUNED_MIN_N and d <= 3:
-        nbr = dc_neighbors_pruned(Xs, Z / lam, family, sigma2, jitter, mv, device=device)
     else:
         nbr = dc_neighbors(Xs, Z / lam, family, sigma2, jitter, mv, device=device)
     t3 = time.perf_counter()
