@@ -137,10 +137,13 @@ __device__ __forceinline__ void la_gather_cols_weak(const double* x, int ncol, i
   for (int q = 0; q < 32; ++q) {
     const int j = __shfl_sync(0xffffffffu, jl, q);
     const double bq = __shfl_sync(0xffffffffu, bl, q);
-    bb[q] = q < cnt ? bq : 0.0;
+    const bool use = q < cnt && __shfl_sync(0xffffffffu, (int)ok, q);
+    bb[q] = use ? bq : 0.0;
+    // an unused slot loads row 0 (a safe address) and discards it: 0 x (a not yet written row) could be NaN
     const double* xr = x + (int64_t)j * ncol;
-    x0[q] = xr[r0];
-    x1[q] = xr[r1];
+    const double a0 = xr[r0], a1 = xr[r1];
+    x0[q] = use ? a0 : 0.0;
+    x1[q] = use ? a1 : 0.0;
   }
 #pragma unroll
   for (int q = 0; q < 32; ++q) {
@@ -243,8 +246,12 @@ __device__ __noinline__ void la_long_row(const double* x, int ncol, const int32_
       const int j = ecol[k];
       const double b = j >= 0 ? eval[k] : 0.0;
       const double* xr = x + (int64_t)(j >= 0 ? j : 0) * ncol + cb;
+      // a padding entry (j < 0) must not touch x: 0 x (a not yet written row) could be NaN
 #pragma unroll
-      for (int c = 0; c < 16; ++c) a16[c] = fma(b, xr[c < cm ? c : 0], a16[c]);
+      for (int c = 0; c < 16; ++c) {
+        const double xv = xr[c < cm ? c : 0];
+        a16[c] = j >= 0 ? fma(b, xv, a16[c]) : a16[c];
+      }
     }
 #pragma unroll
     for (int c = 0; c < 16; ++c) red[lane][c] = a16[c];
