@@ -1021,19 +1021,6 @@ cudaError_t launch_la_tsgemm(const double* U, int64_t ldu, int mk, int64_t n, co
   return cudaGetLastError();
 }
 
-// C (ncol x mk, row stride mk) = V^T U for a column slice of a wider V (row stride ldv), ncol <= 64
-cudaError_t launch_la_tsgemm_ld(const double* U, int64_t ldu, int mk, int64_t n, const double* V, int64_t ldv,
-                                int ncol, double* part, double* Ct, cudaStream_t s) {
-  if (mk == 0) return cudaSuccess;
-  if (ncol > 64) return cudaErrorInvalidValue;
-  const int ns = la_ts_nsplit(n);
-  const int64_t rows_per = (n + ns - 1) / ns;
-  dim3 grid(ns, (mk + TS_K - 1) / TS_K);
-  la_tsgemm_dmma_kernel<<<grid, 256, 0, s>>>(U, ldu, mk, n, V, ncol, ldv, nullptr, rows_per, part);
-  la_tsreduce_kernel<<<grid_for((int64_t)ncol * mk * 32), 256, 0, s>>>(part, ns, ncol, mk, Ct, 1.0);
-  return cudaGetLastError();
-}
-
 int la_red_nsplit(int64_t n) {
   int64_t ns = (n + 511) / 512;  // up to 4 CTAs per SM: a dot over n x ell is a bandwidth pass
   if (ns > 592) ns = 592;

@@ -46,9 +46,11 @@ __device__ __forceinline__ void tile_ij(int t, int& I, int& J) {
   J = t - i * (i + 1) / 2;
 }
 
+// ntc = 0: the SYRK (lower tiles of W^T W, tmW = tmB = W).  ntc > 0: the general C = A^T B over the same rows
+// (tmW = A, tmB = B; every tile of an nt1 x ntc grid, so row splits each, no diagonal shortcut).
 __global__ void __launch_bounds__(32 * (NCONS + 1), SYRK_CTAS_PER_SM)
-    syrk_tma_kernel(const __grid_constant__ CUtensorMap tmW, int64_t nrows, int nt1, int sd, int so, int64_t rps_d,
-                    int64_t rps_o, double* __restrict__ Gpart) {
+    syrk_tma_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmB, int64_t nrows,
+                    int nt1, int ntc, int sd, int so, int64_t rps_d, int64_t rps_o, double* __restrict__ Gpart) {
   extern __shared__ uint8_t syrk_raw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(syrk_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(sm + SS * 2 * SLAB);
@@ -56,7 +58,13 @@ __global__ void __launch_bounds__(32 * (NCONS + 1), SYRK_CTAS_PER_SM)
   // work items: the nt1 diagonal tiles x sd row splits first, then the off-diagonal tiles x so splits
   int I, J, split;
   int64_t rps;
-  if ((int)blockIdx.x < nt1 * sd) {
+  if (ntc > 0) {
+    const int t = blockIdx.x / so;
+    split = blockIdx.x % so;
+    I = t / ntc;
+    J = t % ntc;
+    rps = rps_o;
+  } else if ((int)blockIdx.x < nt1 * sd) {
     I = J = blockIdx.x / sd;
     split = blockIdx.x % sd;
     rps = rps_d;
@@ -70,7 +78,7 @@ __global__ void __launch_bounds__(32 * (NCONS + 1), SYRK_CTAS_PER_SM)
     J = to - i * (i - 1) / 2;
     rps = rps_o;
   }
-  const bool diag = I == J;
+  const bool diag = ntc == 0 && I == J;
   const int64_t r0 = (int64_t)split * rps;
   int64_t r1 = r0 + rps;
   if (r1 > nrows) r1 = nrows;
@@ -90,6 +98,7 @@ __global__ void __launch_bounds__(32 * (NCONS + 1), SYRK_CTAS_PER_SM)
     // ---------------- producer: one elected lane issues the TMA boxes of every stage ----------------
     if (lane == 0) {
       tma_prefetch_desc(&tmW);
+      if (ntc > 0) tma_prefetch_desc(&tmB);
       const uint32_t bytes = diag ? SLAB : 2 * SLAB;
       for (int kt = 0; kt < nkt; ++kt) {
         const int s = kt % SS;
@@ -101,7 +110,8 @@ __global__ void __launch_bounds__(32 * (NCONS + 1), SYRK_CTAS_PER_SM)
         for (int b = 0; b < 4; ++b) tma_load_2d(a + b * BOXB, &tmW, I * ST + 16 * b, row, &full[s]);
         if (!diag) {
 #pragma unroll
-          for (int b = 0; b < 4; ++b) tma_load_2d(a + SLAB + b * BOXB, &tmW, J * ST + 16 * b, row, &full[s]);
+          for (int b = 0; b < 4; ++b)
+            tma_load_2d(a + SLAB + b * BOXB, ntc > 0 ? &tmB : &tmW, J * ST + 16 * b, row, &full[s]);
         }
       }
     }
@@ -257,8 +267,8 @@ cudaError_t launch_syrk_part(const double* W, int64_t ldw, int64_t nrows, int nc
   if (e != cudaSuccess) return e;
   e = smem_optin(syrk_tma_kernel, SYRK_SMEM);
   if (e != cudaSuccess) return e;
-  syrk_tma_kernel<<<syrk_items(ncols, so), 32 * (NCONS + 1), SYRK_SMEM, s>>>(tm, nrows, nt1, sd, so, rps_of(sd), rps_of(so),
-                                                                  Gpart);
+  syrk_tma_kernel<<<syrk_items(ncols, so), 32 * (NCONS + 1), SYRK_SMEM, s>>>(tm, tm, nrows, nt1, 0, sd, so, rps_of(sd),
+                                                                             rps_of(so), Gpart);
   return cudaGetLastError();
 }
 
@@ -268,6 +278,60 @@ cudaError_t launch_syrk_reduce(const double* Gpart, int ncols, int nsplit, int n
   const int64_t tot = (int64_t)syrk_ntiles(ncols) * ST * ST;
   syrk_reduce_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(Gpart, nt1, syrk_diag_splits(nsplit), nsplit,
                                                                    nlaunch, ncols, G, ldg);
+  return cudaGetLastError();
+}
+
+// C (M x N, ldc) = A^T B, A: nrows x M (lda), B: nrows x N (ldb): the tall-skinny contraction over rows
+__global__ void gemm_tt_reduce_kernel(const double* __restrict__ part, int ntc, int so, int M, int N,
+                                      double* __restrict__ C, int64_t ldc) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int nt1 = (M + ST - 1) / ST;
+  if (e >= (int64_t)nt1 * ntc * ST * ST) return;
+  const int t = (int)(e / (ST * ST)), rc = (int)(e % (ST * ST));
+  const int a = (t / ntc) * ST + rc / ST, b = (t % ntc) * ST + rc % ST;
+  if (a >= M || b >= N) return;
+  double acc = 0.0;
+  for (int k = 0; k < so; ++k) acc += part[((size_t)t * so + k) * ST * ST + rc];
+  C[(size_t)a * ldc + b] = acc;
+}
+
+int gemm_tt_nsplit(int M, int N, int64_t nrows, int num_sms) {
+  const int tiles = ((M + ST - 1) / ST) * ((N + ST - 1) / ST);
+  const int64_t slots = (int64_t)SYRK_CTAS_PER_SM * num_sms;
+  const int64_t max_by_rows = std::max<int64_t>(1, (nrows + 4 * SK - 1) / (4 * SK));
+  int64_t so = std::max<int64_t>(1, slots / tiles);
+  if (so > max_by_rows) so = max_by_rows;
+  return (int)so;
+}
+
+size_t gemm_tt_part_doubles(int M, int N, int nsplit) {
+  return (size_t)((M + ST - 1) / ST) * ((N + ST - 1) / ST) * nsplit * ST * ST;
+}
+
+cudaError_t launch_gemm_tt(const double* A, int64_t lda, int M, const double* B, int64_t ldb, int N, int64_t nrows,
+                           int nsplit, double* part, double* C, int64_t ldc, cudaStream_t s) {
+  if (M <= 0 || N <= 0) return cudaSuccess;
+  const int nt1 = (M + ST - 1) / ST, ntc = (N + ST - 1) / ST;
+  const int so = nsplit;
+  if (nrows <= 0) {
+    for (int a = 0; a < M; ++a) {
+      cudaError_t e = cudaMemsetAsync(C + (size_t)a * ldc, 0, (size_t)N * sizeof(double), s);
+      if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+  }
+  int64_t rps = (nrows + so - 1) / so;
+  rps = (rps + SK - 1) / SK * SK;
+  CUtensorMap ta, tb;
+  cudaError_t e = make_tmap_f64(&ta, A, (uint64_t)nrows, (uint64_t)M, (uint64_t)lda, SK);
+  if (e != cudaSuccess) return e;
+  e = make_tmap_f64(&tb, B, (uint64_t)nrows, (uint64_t)N, (uint64_t)ldb, SK);
+  if (e != cudaSuccess) return e;
+  e = smem_optin(syrk_tma_kernel, SYRK_SMEM);
+  if (e != cudaSuccess) return e;
+  syrk_tma_kernel<<<nt1 * ntc * so, 32 * (NCONS + 1), SYRK_SMEM, s>>>(ta, tb, nrows, nt1, ntc, so, so, rps, rps, part);
+  const int64_t tot = (int64_t)nt1 * ntc * ST * ST;
+  gemm_tt_reduce_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(part, ntc, so, M, N, C, ldc);
   return cudaGetLastError();
 }
 

@@ -31,6 +31,8 @@ struct VecchiaArgs {
   // gradient (vif_grad, one rank per process): the factor's rows also write the per-point state of the gradient's
   // first pass (vif_state_doubles layout, by position; the g_i dots are left to launch_grad_gam)
   double* state = nullptr;
+  // SMs to leave free of vecchia CTAs (multi-GPU: room for the all-gather kernels running beside); 0 = all
+  int reserve_sms = 0;
 };
 
 // per-point gradient state, by position: L (packed lower, SP = 8 RB rows incl. the identity padding),
@@ -62,6 +64,11 @@ cudaError_t launch_syrk(const double* W, int64_t ldw, int64_t nrows, int ncols, 
                         double* G, int ldg, cudaStream_t s);
 cudaError_t launch_syrk_part(const double* W, int64_t ldw, int64_t nrows, int ncols, int nsplit, double* Gpart,
                              cudaStream_t s);
+// C (M x N, ldc) = A^T B over nrows rows (A: lda, B: ldb) on the SYRK's TMA engine, all tiles, nsplit row splits
+int gemm_tt_nsplit(int M, int N, int64_t nrows, int num_sms);
+size_t gemm_tt_part_doubles(int M, int N, int nsplit);
+cudaError_t launch_gemm_tt(const double* A, int64_t lda, int M, const double* B, int64_t ldb, int N, int64_t nrows,
+                           int nsplit, double* part, double* C, int64_t ldc, cudaStream_t s);
 // sums the partials of nlaunch consecutive launch_syrk_part calls (same ncols, nsplit) into G
 cudaError_t launch_syrk_reduce(const double* Gpart, int ncols, int nsplit, int nlaunch, double* G, int ldg,
                                cudaStream_t s);
@@ -107,8 +114,6 @@ cudaError_t launch_gTdK(const double* X, const double* Z, int64_t n, int m, int 
 cudaError_t launch_grev_linv(const double* Linv, int mk, double* Bp, cudaStream_t s);
 cudaError_t launch_gfinal(double* out, const double* tdk, int q, const double* G2, const double* Phil, int mk,
                           cudaStream_t s);
-cudaError_t launch_la_tsgemm_ld(const double* U, int64_t ldu, int mk, int64_t n, const double* V, int64_t ldv,
-                                int ncol, double* part, double* Ct, cudaStream_t s);
 cudaError_t launch_dkm(const double* Z, int m, int mk, int pidx, const CovParams& p, double* out, cudaStream_t s);
 cudaError_t launch_phi_low(const double* Phi, int mk, double* out, cudaStream_t s);
 cudaError_t launch_grad_q(const double* LinvM, int ldi, const double* G, int ldg, int ycol, int m, int ld,

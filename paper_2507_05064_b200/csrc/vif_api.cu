@@ -332,6 +332,15 @@ int wait_stream(Handle* h, cudaStream_t s) {
     if (w_ != VIF_OK) return w_;       \
   } while (0)
 
+// SMs the vecchia rows leave free: with a communicator the per-round all-gathers (SM kernels) run beside them,
+// and a vecchia launch that fills every SM's register file starves them (tools/corun_probe.py: an SM copy
+// beside the factor ran 2.8x slower).  VIF_RESERVE_SMS overrides (also on one GPU, for that probe).
+int reserve_sms(const Handle* h) {
+  static const char* e = getenv("VIF_RESERVE_SMS");
+  if (e) return atoi(e) > 0 ? atoi(e) : 0;
+  return h->comm ? 8 : 0;
+}
+
 bool make_params(const Handle* h, const vif_theta* th, CovParams& p, std::string& err) {
   if (!th) { err = "theta is NULL"; return false; }
   if (th->d != h->P.d) { err = "theta.d != dims.d"; return false; }
@@ -454,7 +463,7 @@ Layout make_grad_layout(const Plan& P) {
   L.size[G_CCNT] = L.size[G_CCUR] = (size_t)P.n * sizeof(int);
   L.size[G_CPTR] = (size_t)(P.n + 1) * sizeof(int);
   L.size[G_CENT] = (size_t)2 * P.n * (P.mv + 1) * sizeof(int);  // sorted entries + the unsorted fill
-  L.size[G_TSP] = (size_t)la_ts_nsplit(P.n) * 64 * mk1 * D8;
+  L.size[G_TSP] = gemm_tt_part_doubles((int)mk1, (int)mk1, gemm_tt_nsplit((int)mk1, (int)mk1, P.n, kPlanSMs)) * D8;
   L.size[G_TDKP] = (size_t)gTdK_blocks() * (P.d + 1) * D8;
   L.size[G_TDK] = (size_t)(P.d + 2) * D8;  // + the R gather's row counter
   size_t off = 0;
@@ -1045,6 +1054,7 @@ int vif_factor(void* handle, const vif_theta* theta, double* B_out, double* D_ou
         a.D_out = D_out;
         a.st = st;
         a.state = h->grad_state ? h->grad_state + (size_t)off * grad_state_doubles(P.mv) : nullptr;
+        a.reserve_sms = reserve_sms(h);
         VIF_CUDA(h, launch_vecchia(a, s), "vecchia");
         ++nl;
       }
@@ -1141,6 +1151,7 @@ int vif_factor(void* handle, const vif_theta* theta, double* B_out, double* D_ou
         a.D_out = D_out;
         a.st = st;
         a.state = h->grad_state ? h->grad_state + (size_t)off * grad_state_doubles(P.mv) : nullptr;
+        a.reserve_sms = reserve_sms(h);
         VIF_CUDA(h, launch_vecchia(a, s), "vecchia");
         ++nl;
       }
@@ -1357,10 +1368,9 @@ int vif_grad(void* handle, const vif_theta* theta, void* gws, size_t gws_bytes, 
       // R has reversed columns, so T = R L_m^{-1} is a triangular product (T with reversed columns)
       if (g == 0) VIF_CUDA(h, launch_grev_linv(Linv, mk, gbuf(G_LINVT), s), "reversed L_m^-1");
       VIF_CUDA(h, launch_gemm_tn(R, mk, P.n, gbuf(G_LINVT), mk, mk, mk, 1, gbuf(G_T), mk, 1.0, 0, s), "T = R L^-1");
-      for (int c0 = 0; c0 < mk; c0 += 64)
-        VIF_CUDA(h, launch_la_tsgemm_ld(U, ld, mk, P.n, R + c0, mk, std::min(64, mk - c0), gbuf(G_TSP),
-                                        gbuf(G_G2) + (size_t)c0 * mk, s),
-                 "G2 = R^T U");
+      VIF_CUDA(h, launch_gemm_tt(R, mk, mk, U, ld, mk, P.n, gemm_tt_nsplit(mk, mk, P.n, kPlanSMs), gbuf(G_TSP),
+                                 gbuf(G_G2), mk, s),
+               "G2 = R^T U");
       VIF_CUDA(h, launch_gTdK(h->buf<double>(B_X), h->buf<double>(B_Z), P.n, m, mk, p, gbuf(G_T), gbuf(G_TDKP),
                               gbuf(G_TDK), s),
                "<T, dK>");

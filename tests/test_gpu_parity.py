@@ -346,7 +346,7 @@ import numpy as np, torch
 sys.path.insert(0, {root!r})
 import paper_2507_05064_b200 as p
 import vifgen
-w = vifgen.make_workload(n=3001, d=2, m=24, mv=9, family="matern32", rho=0.15, nugget=0.1, seed=31, device="cuda")
+w = vifgen.make_workload(n=3001, d=2, m=24, mv={mv}, family="matern32", rho=0.15, nugget=0.1, seed=31, device="cuda")
 dev = torch.device("cuda")
 X, Z, nbr, y = (torch.from_numpy(np.ascontiguousarray(a)).to(dev) for a in (w.X, w.Z, w.nbr, w.y))
 nid = p.vif_nccl_unique_id() if {use_nccl} else None
@@ -359,10 +359,12 @@ print(json.dumps(dict(nll=t.nll, D=D.cpu().numpy().tolist()[:50], g=list(map(flo
 """
 
 
-def test_nccl_single_rank_schedule():
+@pytest.mark.parametrize("mv", [9, 35])
+def test_nccl_single_rank_schedule(mv):
     """The multi-GPU schedule (8 rounds, per-round NCCL all-gather, NCCL all-reduce of the Gram and of
     the gradient sums) on a one-rank communicator (VIF_NCCL_SINGLE=1): exercises the NCCL plumbing on one
-    GPU (no ranks waiting on each other) and must reproduce the single-GPU result."""
+    GPU (no ranks waiting on each other) and must reproduce the single-GPU result.  With a communicator the
+    vecchia rows leave 8 SMs free (grid-strided register and shared-memory kernels: m_v = 9 and 35)."""
     import json
     import os
     import subprocess
@@ -371,7 +373,7 @@ def test_nccl_single_rank_schedule():
     outs = []
     for use in (False, True):
         env = dict(os.environ, VIF_NCCL_SINGLE="1" if use else "0")
-        r = subprocess.run([sys.executable, "-c", _NCCL1.format(root=root, use_nccl=use)], env=env, capture_output=True,
+        r = subprocess.run([sys.executable, "-c", _NCCL1.format(root=root, use_nccl=use, mv=mv)], env=env, capture_output=True,
                            text=True, timeout=600)
         assert r.returncode == 0, r.stderr[-2000:]
         outs.append(json.loads(r.stdout.strip().splitlines()[-1]))

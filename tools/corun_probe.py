@@ -7,6 +7,7 @@ GPU we replay that traffic beside a full vif_factor + vif_nll (config-3 recipe, 
   sm_copy     + the same bytes moved by an SM kernel (torch's copy kernel, 16 chunks) on a side stream (what
               NCCL's SM-based all-gather kernels need: CTAs on the SMs the vecchia kernel fills).
 Reported: evaluation time (events on the library stream), the side copy's time, and both run alone.
+VIF_RESERVE_SMS=k (environment) makes the vecchia rows leave k SMs free, as multi-GPU handles do.
   python tools/corun_probe.py [n]"""
 import json
 import os
@@ -78,7 +79,7 @@ def timed(kind, reps=3):
 
 
 model.evaluate(th)
-out = {"n": n, "side_bytes": nbytes}
+out = {"n": n, "side_bytes": nbytes, "reserve_sms": os.environ.get("VIF_RESERVE_SMS", "0")}
 out["alone_ms"] = timed("alone")[0]
 for kind in ("ce_copy", "sm_copy"):
     torch.cuda.synchronize()
