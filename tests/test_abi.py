@@ -47,11 +47,19 @@ def test_library_is_sm100a():
 
 
 def test_sass_uses_fp64_tensor_core():
+    """The contractions run on the FP64 tensor pipe (DMMA), and the TMA GEMM / SYRK engines move their tiles
+    with bulk tensor copies (UTMALDG) synchronised by mbarriers (SYNCS)."""
     import subprocess
     out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "-sass",
                           os.path.join(ROOT, "paper_2507_05064_b200", "libvif.so")],
                          capture_output=True, text=True).stdout
     assert "DMMA.8x8x4" in out
+    for kern in ("gemm_tn_tma_kernel", "syrk_tma_kernel"):
+        i = out.find(kern)
+        assert i >= 0, kern
+        j = out.find("Function :", i + 1)
+        body = out[i:j if j > 0 else len(out)]
+        assert "UTMALDG" in body and "SYNCS" in body and "DMMA" in body, kern
 
 
 def test_workspace_and_partition_host_only(p):
