@@ -131,19 +131,20 @@ __device__ __forceinline__ void la_gather_cols_weak(const double* x, int ncol, i
   const bool ok = jl >= 0;  // selects, not branches: the shuffles below need a converged warp
   jl = ok ? jl : 0;
   bl = ok ? bl : 0.0;
-  __syncwarp();
+  // the valid entries are a prefix of the lanes (neighbour lists are -1 padded at the end only; children
+  // lists have no padding), so slot q is used iff q < lim
+  const int lim = min(cnt, __popc(__ballot_sync(0xffffffffu, ok)));
   double x0[32], x1[32], bb[32];
 #pragma unroll
   for (int q = 0; q < 32; ++q) {
     const int j = __shfl_sync(0xffffffffu, jl, q);
     const double bq = __shfl_sync(0xffffffffu, bl, q);
-    const bool use = q < cnt && __shfl_sync(0xffffffffu, (int)ok, q);
-    bb[q] = use ? bq : 0.0;
+    bb[q] = q < lim ? bq : 0.0;
     // an unused slot loads row 0 (a safe address) and discards it: 0 x (a not yet written row) could be NaN
     const double* xr = x + (int64_t)j * ncol;
     const double a0 = xr[r0], a1 = xr[r1];
-    x0[q] = use ? a0 : 0.0;
-    x1[q] = use ? a1 : 0.0;
+    x0[q] = q < lim ? a0 : 0.0;
+    x1[q] = q < lim ? a1 : 0.0;
   }
 #pragma unroll
   for (int q = 0; q < 32; ++q) {

@@ -23,8 +23,6 @@
 #include "kernels.h"
 #include <stdlib.h>
 
-#include <algorithm>
-
 
 namespace vif {
 
@@ -40,7 +38,7 @@ __host__ __device__ constexpr int vecchia_warp_doubles(int d) {
   return RB * 8 * (RB * 8 + 1) / 2 + RB * 8 + 64 + RB * 8 * d;
 }
 
-template <int FAM, int RB, int NB, int MINB = 3, bool GS = false>
+template <int FAM, int RB, int NB, int MINB = 3>
 __global__ void __launch_bounds__(VW * 32, MINB) vecchia_smem_kernel(
     const double* __restrict__ U, int64_t ldu, int mk, int ld, const double* __restrict__ X,
     const double* __restrict__ Uq, const double* __restrict__ Xq, const int32_t* __restrict__ nbr, int mv, const int64_t* __restrict__ order, int64_t npts, CovParams p,
@@ -58,13 +56,10 @@ __global__ void __launch_bounds__(VW * 32, MINB) vecchia_smem_kernel(
   double* xs = linv + 64;
   __shared__ double tbl[64];
   int* Sidx = Sidx_all[warp];
+  const int64_t pos = (int64_t)blockIdx.x * VW + warp;
   exp_table_init(tbl, p.sigma2, threadIdx.x);
   __syncthreads();
-  // one point per warp; with GS grid-strided, so that a launch on fewer CTAs (SMs left free for the
-  // collectives of a multi-GPU run, VecchiaArgs::reserve_sms) still covers every point
-  int64_t pos = (int64_t)blockIdx.x * VW + warp;
   if (pos >= npts) return;
-  do {
   const int64_t i = order[pos];
 
   // ---- conditioning set ----
@@ -243,7 +238,7 @@ __global__ void __launch_bounds__(VW * 32, MINB) vecchia_smem_kernel(
       Dpos[pos] = 1.0;
       if (D_out) D_out[i] = __longlong_as_double(0x7ff8000000000000LL);
     }
-    continue;
+    return;
   }
 
   // ---- 4. A_i^T = L_NN^{-T} l, l = row q of L; lane k holds x_k and x_{k+32} (branch-free shuffles) ----
@@ -323,7 +318,6 @@ __global__ void __launch_bounds__(VW * 32, MINB) vecchia_smem_kernel(
     Dpos[pos] = Di;
     if (D_out) D_out[i] = Di;
   }
-  } while (GS && (pos += (int64_t)gridDim.x * VW) < npts);  // points
 }
 
 
@@ -436,7 +430,7 @@ __host__ __device__ constexpr int vreg_warp_doubles(int d) {
 // SELF: the point's own row / coordinates come from Uq / Xq (prediction); false for the factor
 // DD > 0: the input dimension as a compile-time constant (the coordinate loops of the kernel
 // evaluations unroll and their index arithmetic folds; d = 2 is instantiated)
-template <int FAM, int RB, int NB, int MINB, bool SELF = false, int DD = 0, bool GS = false>
+template <int FAM, int RB, int NB, int MINB, bool SELF = false, int DD = 0>
 __global__ void __launch_bounds__(VW * 32, MINB) vecchia_reg_kernel(
     const double* __restrict__ U, int64_t ldu, int mk, int ld, const double* __restrict__ X,
     const double* __restrict__ Uq, const double* __restrict__ Xq, const int32_t* __restrict__ nbr, int mv, const int64_t* __restrict__ order, int64_t npts, CovParams p,
@@ -458,10 +452,8 @@ __global__ void __launch_bounds__(VW * 32, MINB) vecchia_reg_kernel(
   double* coef = colbuf + 2 * SP; // [SP]
   double* xs = coef + SP;         // [SP][d]
   int* Sidx = Sidx_all[warp];
-  // one point per warp; with GS grid-strided (see vecchia_smem_kernel)
-  int64_t pos = (int64_t)blockIdx.x * VW + warp;
+  const int64_t pos = (int64_t)blockIdx.x * VW + warp;
   if (pos >= npts) return;
-  do {
   const int64_t i = order[pos];
 
   // ---- conditioning set and its (pre-scaled) coordinates ----
@@ -505,7 +497,7 @@ __global__ void __launch_bounds__(VW * 32, MINB) vecchia_reg_kernel(
     __syncwarp();
     if (g_vif_debug & 2) {  // debug probe: bit 1 skips steps 3-5 (timing only; outputs invalid)
       if (lane == 0) Dpos[pos] = 1.0 + 1e-30 * C[0];
-      continue;
+      return;
     }
   }
 
@@ -551,7 +543,7 @@ __global__ void __launch_bounds__(VW * 32, MINB) vecchia_reg_kernel(
       Dpos[pos] = 1.0;
       if (D_out) D_out[i] = __longlong_as_double(0x7ff8000000000000LL);
     }
-    continue;
+    return;
   }
   // rows of L to shared memory (row-major) for the back substitution
 #pragma unroll
@@ -629,24 +621,11 @@ __global__ void __launch_bounds__(VW * 32, MINB) vecchia_reg_kernel(
     Dpos[pos] = Di;
     if (D_out) D_out[i] = Di;
   }
-  } while (GS && (pos += (int64_t)gridDim.x * VW) < npts);  // points
-}
-
-// one CTA (4 warps) per 4 points; with reserve_sms > 0 at most (SMs - reserve) x `per_sm` CTAs, grid-strided,
-// so the blocks never occupy the reserved SMs' share (the collectives' kernels of a multi-GPU run find room)
-static unsigned vecchia_blocks(const VecchiaArgs& a, int per_sm) {
-  const int64_t need = (a.npts + VW - 1) / VW;
-  if (a.reserve_sms <= 0) return (unsigned)need;
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int64_t cap = (int64_t)std::max(1, sms - a.reserve_sms) * per_sm;
-  return (unsigned)std::min<int64_t>(need, cap);
 }
 
 template <int FAM, int RB>
 static cudaError_t launch_reg(const VecchiaArgs& a, cudaStream_t s) {
-  const unsigned blocks = vecchia_blocks(a, 4);
+  const unsigned blocks = (unsigned)((a.npts + VW - 1) / VW);
   const size_t smem = (size_t)VW * vreg_warp_doubles<RB>(a.p.d) * sizeof(double);
   // ring depth 3, 4 blocks (16 warps) per SM (measured: depth 2 / 5 blocks slower, profiles/r01_notes.md)
   decltype(&vecchia_reg_kernel<FAM, RB, 3, 4>) kern;
@@ -655,9 +634,8 @@ static cudaError_t launch_reg(const VecchiaArgs& a, cudaStream_t s) {
   } else {
     static const char* gen_env = getenv("VIF_VECCHIA_GENERIC_D");  // A/B: runtime-d loops at d = 2 too
     const int dd = (gen_env && gen_env[0] == '1') ? 0 : a.p.d;
-    const bool gs = a.reserve_sms > 0;
-    if (dd == 2) kern = gs ? vecchia_reg_kernel<FAM, RB, 3, 4, false, 2, true> : vecchia_reg_kernel<FAM, RB, 3, 4, false, 2>;
-    else kern = gs ? vecchia_reg_kernel<FAM, RB, 3, 4, false, 0, true> : vecchia_reg_kernel<FAM, RB, 3, 4>;
+    if (dd == 2) kern = vecchia_reg_kernel<FAM, RB, 3, 4, false, 2>;
+    else kern = vecchia_reg_kernel<FAM, RB, 3, 4>;
   }
   {
     cudaError_t e = smem_optin(kern, smem);  // static shared memory comes on top
@@ -681,10 +659,10 @@ static cudaError_t launch_reg(const VecchiaArgs& a, cudaStream_t s) {
 
 template <int FAM, int RB>
 static cudaError_t launch_smem(const VecchiaArgs& a, cudaStream_t s) {
-  const unsigned blocks = vecchia_blocks(a, 3);
+  const unsigned blocks = (unsigned)((a.npts + VW - 1) / VW);
   const size_t smem = (size_t)VW * vecchia_warp_doubles<RB>(a.p.d) * sizeof(double);
   // Gram ring depth 1 (a 2-deep ring measured slower at 12 warps/SM, profiles/r01_notes.md)
-  auto kern = a.reserve_sms > 0 ? vecchia_smem_kernel<FAM, RB, 1, 3, true> : vecchia_smem_kernel<FAM, RB, 1>;
+  auto kern = vecchia_smem_kernel<FAM, RB, 1>;
   {
     cudaError_t e = smem_optin(kern, smem);
     if (e != cudaSuccess) return e;

@@ -31,8 +31,6 @@ struct VecchiaArgs {
   // gradient (vif_grad, one rank per process): the factor's rows also write the per-point state of the gradient's
   // first pass (vif_state_doubles layout, by position; the g_i dots are left to launch_grad_gam)
   double* state = nullptr;
-  // SMs to leave free of vecchia CTAs (multi-GPU: room for the all-gather kernels running beside); 0 = all
-  int reserve_sms = 0;
 };
 
 // per-point gradient state, by position: L (packed lower, SP = 8 RB rows incl. the identity padding),

@@ -332,15 +332,6 @@ int wait_stream(Handle* h, cudaStream_t s) {
     if (w_ != VIF_OK) return w_;       \
   } while (0)
 
-// SMs the vecchia rows leave free: with a communicator the per-round all-gathers (SM kernels) run beside them,
-// and a vecchia launch that fills every SM's register file starves them (tools/corun_probe.py: an SM copy
-// beside the factor ran 2.8x slower).  VIF_RESERVE_SMS overrides (also on one GPU, for that probe).
-int reserve_sms(const Handle* h) {
-  static const char* e = getenv("VIF_RESERVE_SMS");
-  if (e) return atoi(e) > 0 ? atoi(e) : 0;
-  return h->comm ? 8 : 0;
-}
-
 bool make_params(const Handle* h, const vif_theta* th, CovParams& p, std::string& err) {
   if (!th) { err = "theta is NULL"; return false; }
   if (th->d != h->P.d) { err = "theta.d != dims.d"; return false; }
@@ -1054,7 +1045,6 @@ int vif_factor(void* handle, const vif_theta* theta, double* B_out, double* D_ou
         a.D_out = D_out;
         a.st = st;
         a.state = h->grad_state ? h->grad_state + (size_t)off * grad_state_doubles(P.mv) : nullptr;
-        a.reserve_sms = reserve_sms(h);
         VIF_CUDA(h, launch_vecchia(a, s), "vecchia");
         ++nl;
       }
@@ -1151,7 +1141,6 @@ int vif_factor(void* handle, const vif_theta* theta, double* B_out, double* D_ou
         a.D_out = D_out;
         a.st = st;
         a.state = h->grad_state ? h->grad_state + (size_t)off * grad_state_doubles(P.mv) : nullptr;
-        a.reserve_sms = reserve_sms(h);
         VIF_CUDA(h, launch_vecchia(a, s), "vecchia");
         ++nl;
       }

@@ -363,8 +363,8 @@ print(json.dumps(dict(nll=t.nll, D=D.cpu().numpy().tolist()[:50], g=list(map(flo
 def test_nccl_single_rank_schedule(mv):
     """The multi-GPU schedule (8 rounds, per-round NCCL all-gather, NCCL all-reduce of the Gram and of
     the gradient sums) on a one-rank communicator (VIF_NCCL_SINGLE=1): exercises the NCCL plumbing on one
-    GPU (no ranks waiting on each other) and must reproduce the single-GPU result.  With a communicator the
-    vecchia rows leave 8 SMs free (grid-strided register and shared-memory kernels: m_v = 9 and 35)."""
+    GPU (no ranks waiting on each other) and must reproduce the single-GPU result (the register kernel at
+    m_v = 9, the shared-memory kernel at m_v = 35)."""
     import json
     import os
     import subprocess
