@@ -151,6 +151,13 @@ def test_grad_config2_full():
 
 
 @pytest.mark.slow
+def test_grad_config3_recipe_vs_oracle():
+    """The config-3 recipe (m = 500, m_v = 30, Matern 3/2 in 2-D) at n = 200k against the oracle's gradient
+    (the full n = 1M is checked by finite differences below: the oracle would need ~15 min there)."""
+    grad_parity(vifgen.make_config(3, device="cuda", n=200000))
+
+
+@pytest.mark.slow
 def test_grad_config3_vs_gpu_finite_differences():
     """n = 1M: analytic GPU gradient vs Richardson central differences of the GPU NLL."""
     w = vifgen.make_config(3, device="cuda")
