@@ -872,7 +872,13 @@ int vif_create(void** handle, const vif_dims* dims, void* workspace, size_t ws_b
       delete h;
       return fail(nullptr, VIF_ERR_NCCL, m);
     }
-    e = cudaStreamCreateWithFlags(&h->cstream, cudaStreamNonBlocking);
+    // the communication stream at the highest priority: the block scheduler then hands freed SMs to the
+    // all-gather kernels first instead of to queued vecchia CTAs (tools/corun_probe.py, CORUN_PRIORITY)
+    {
+      int lo = 0, hi = 0;
+      e = cudaDeviceGetStreamPriorityRange(&lo, &hi);
+      if (e == cudaSuccess) e = cudaStreamCreateWithPriority(&h->cstream, cudaStreamNonBlocking, hi);
+    }
     h->ev_k1.assign(h->P.rounds, nullptr);
     h->ev_ag.assign(h->P.rounds, nullptr);
     for (int64_t k = 0; k < h->P.rounds && e == cudaSuccess; ++k) {
