@@ -122,6 +122,19 @@ def per_point_flops(s, m):
             "syrk": (m + 1.0) * (m + 2.0)}                            # A6
 
 
+INT8_PEAK_TOPS = 2 * 1665.1  # MEASURED_PEAKS.json bf16_tflops (burst) x the guide's nominal int8 : bf16 ratio of 2
+
+
+def syrk_int8_ops(n, m):
+    """int8 tensor-core ops (2 per MAC) the K4 Gram executes on the integer-slice engine (k_ozaki.cu): 28 digit
+    products per (128 x 64 tile, row) over the tiles touching the lower triangle of the ld x ld Gram"""
+    ld = -(-(((m + 7) // 8) * 8 + 1) // 8) * 8
+    nI, nJ = -(-ld // 128), -(-ld // 64)
+    tiles = sum(min(2 * i + 2, nJ) for i in range(nI))
+    nrp = -(-n // 64) * 64
+    return 2.0 * 28 * nrp * tiles * 128 * 64
+
+
 def workload_flops(nbr, m):
     s = (nbr >= 0).sum(1).astype(np.float64) + 1.0 if nbr.shape[1] > 0 else np.ones(nbr.shape[0])
     f = per_point_flops(s, m)
@@ -492,8 +505,21 @@ def main():
                          "peak_source": "measured FP64 DMMA peak on this pool's B200 (tools/microbench_fp64.cu; "
                                         "MEASURED_PEAKS.json has no FP64 entry); cuBLAS DGEMM 35.5",
                          "flops_per_launch": fl_launch[dom], "avg_launch_ms": stage_avg[kern[dom]],
-                         "per_kernel": {k: {"stage": kern[k], "avg_ms": stage_avg[kern[k]], "tflops": achieved[k],
-                                            "frac": achieved[k] / FP64_PEAK_TFLOPS} for k in kern},
+                         "per_kernel": dict({k: {"stage": kern[k], "avg_ms": stage_avg[kern[k]], "tflops": achieved[k],
+                                                 "frac": achieved[k] / FP64_PEAK_TFLOPS} for k in kern},
+                                            syrk={"stage": kern["syrk"], "avg_ms": stage_avg[kern["syrk"]],
+                                                  "tflops": achieved["syrk"],
+                                                  "frac": achieved["syrk"] / FP64_PEAK_TFLOPS,
+                                                  "engine": "FP64 emulated by int8 digit slices on tcgen05.mma.kind::i8 "
+                                                            "(k_ozaki.cu): tflops/frac are FP64-equivalent (the "
+                                                            "algorithmic FP64 flops / time, vs the DMMA peak)",
+                                                  "int8_tops": syrk_int8_ops(w.n / world, w.m) /
+                                                  (stage_avg[kern["syrk"]] * 1e-3) / 1e12,
+                                                  "int8_peak_tops": INT8_PEAK_TOPS,
+                                                  "int8_frac": syrk_int8_ops(w.n / world, w.m) /
+                                                  (stage_avg[kern["syrk"]] * 1e-3) / 1e12 / INT8_PEAK_TOPS,
+                                                  "int8_note": "stage time includes the column-maximum and slicing "
+                                                               "passes (HBM-bound, ~2.4 of 5.9 ms at config 3)"}),
                          "contractions_frac": {"U = K(X,Z) L_m^-T (K1)": achieved["ufeat"] / FP64_PEAK_TFLOPS,
                                                "M Gram W^T W (K4)": achieved["syrk"] / FP64_PEAK_TFLOPS,
                                                "north_star_target": 0.6},

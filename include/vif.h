@@ -272,6 +272,20 @@ int vif_la_nll(void* handle, void* workspace, const double* y, const vif_la_opts
 /* Debug / parity: copy the whitened features U (n x m, row-major) to `out` (device or host). */
 int vif_copy_U(void* handle, double* out);
 
+/* The Gram matrix G = W^T W of a device matrix (A6 / K4, "M": the contraction the factor runs on its
+ * rows [W r]), exposed on its own for tests and benchmarks.
+ *   W: device, nrows x ncols row-major, leading dimension ldw doubles (even; W 16-byte aligned);
+ *   G: device, ncols x ncols row-major, leading dimension ldg: the lower triangle (a >= b) is written (entries
+ *      above the diagonal inside diagonal tiles may be written too, with their symmetric values);
+ *   engine: 0 = integer tensor cores (int8 digit slices on tcgen05.mma.kind::i8, exact int32 level sums,
+ *      k_ozaki.cu; ncols <= 4096), 1 = FP64 DMMA (k_syrk.cu);
+ *   stream: cudaStream_t (NULL = legacy default stream); scratch is taken with cudaMallocAsync on it and
+ *      released the same way (the device's default memory pool is set to keep freed memory).  Enqueued only: the caller synchronises.  A non-finite entry of W makes G NaN.
+ * Errors: VIF_ERR_INVALID_ARG (NULL pointers, ncols < 1, nrows < 0, ldw < ncols or odd, ldg < ncols,
+ * engine 0 with ncols > 4096), VIF_ERR_CUDA. */
+int vif_gram(const double* W, int64_t ldw, int64_t nrows, int32_t ncols, double* G, int64_t ldg, int32_t engine,
+             void* stream);
+
 /* Number of GPU kernel launches the last vif_factor + vif_nll pair enqueued (for bench.py). */
 int vif_launch_count(void* handle, int64_t* count);
 

@@ -1,0 +1,380 @@
+// k_ozaki.cu -- K4 on the integer tensor cores: G = [W r]^T [W r] ("M"; whitened, reading c4) as an
+// exact sum of int8 x int8 products (an Ozaki-type splitting of FP64 into integer digit slices).
+//
+// Why.  FP64 has no tcgen05 kind; the FP64 tensor path is warp-level DMMA at 37.1 TF/s.  tcgen05 kind::i8
+// runs at ~2.9 POPS on this B200 (tools/tc_i8_probe.cu), so an FP64 product rebuilt from 28 int8 products
+// runs at ~100 TF/s FP64-equivalent -- 2.7x the DMMA peak -- with int32 accumulation that is EXACT.
+//
+// Splitting (per column a of W, global over the rows): e_a = exponent with max_k |W_ka| < 2^(e_a - 1);
+// X_ka = rint(W_ka 2^(55 - e_a)) (|X| <= 2^54, one rounding of 2^-55 relative to the column maximum);
+// X = sum_{p=0..6} d_p 256^(6-p) with balanced digits d_1..d_6 in [-128, 127] and |d_0| <= 65.  Then
+//     W_ka W_kb = 2^(e_a + e_b - 14) sum_{p,q} d_p(a) d_q(b) 2^(-8(p+q)),
+// truncated to the levels L = p + q <= 6 (28 products; the dropped levels are below 2^-51 of the
+// column-maximum product, measured at config 3: |G - G_exact| <= 1e-16 |G|max, the same as FP64).
+// Level L's products sum in int32: at most 7 pairs x 2^14 x rows -- exact for <= 16,384 rows per
+// accumulation (OZ_CHUNK).
+//
+// Kernels.  (1) oz_colmax: column maxima (atomicMax on the bit patterns of |W|).  (2) oz_slice: W ->
+// digit slices Ws[p][a][k] (int8, k contiguous: the K-major tcgen05 operand), through a shared-memory
+// transpose of 64 x 64 tiles.  (3) oz_syrk_kernel: persistent, one CTA per SM, units = (128 x 64 output
+// tile, row split of <= 16,384 rows); warp 0 streams TMA boxes {32 rows of k, 128 or 64 columns, 7 slices}
+// through a 4-stage ring; warp 1 issues per stage 10 tcgen05.mma.kind::i8: A slice p (128 columns of W)
+// times the CONCATENATED B slices 0..6-p (64 columns each, contiguous in shared memory), accumulating
+// into TMEM columns 64p.. -- so level L lands in columns [64L, 64L + 64) (448 of the 512 TMEM columns)
+// without any bookkeeping; warps 2-5 drain the 7 levels per unit (tcgen05.ld), combine them in FP64
+// (Horner in 2^-8) and write the unit's partial tile.  (4) oz_reduce: deterministic sum over the splits,
+// scaled by 2^(e_a + e_b - 14).
+#include "common.cuh"
+#include "kernels.h"
+#include "tc.cuh"
+#include "tma.cuh"
+
+#include <algorithm>
+
+namespace vif {
+
+namespace {
+constexpr int OZ_S = 7;           // digit slices
+constexpr int OZ_BM = 128;        // tile rows (a) = TMEM lanes
+constexpr int OZ_BN = 64;         // tile columns (b) per level
+constexpr int OZ_BK = 32;         // k (rows of W) per stage = one MMA K
+constexpr int OZ_STAGES = 4;
+constexpr int OZ_CHUNK = 16384;   // rows per int32 accumulation
+constexpr int OZ_A_BYTES = OZ_S * OZ_BM * OZ_BK;
+constexpr int OZ_B_BYTES = OZ_S * OZ_BN * OZ_BK;
+constexpr int OZ_STAGE_BYTES = OZ_A_BYTES + OZ_B_BYTES;
+constexpr size_t OZ_SMEM = (size_t)OZ_STAGES * OZ_STAGE_BYTES + 1024 + 256;
+constexpr int OZ_TROWS = 64;      // slicer tile
+}  // namespace
+
+// scale exponent of a column from its maximum (bit pattern of a non-negative double): max < 2^(e - 1);
+// clamped so that 2^(55 - e) stays a normal double
+__device__ __forceinline__ int oz_exp(unsigned long long bits) {
+  const double mx = __longlong_as_double((long long)bits);
+  if (!(mx > 0.0)) return 0;
+  int e;
+  frexp(mx, &e);
+  return max(e + 1, -960);
+}
+
+// lower tiles (I, J) of the (ceil(ncols/128) x ceil(ncols/64)) grid that touch the lower triangle: J <= 2I + 1
+__host__ __device__ __forceinline__ void oz_tile(int t, int nJ, int& I, int& J) {
+  int i = 0;
+  for (;;) {
+    const int c = min(2 * i + 2, nJ);
+    if (t < c) break;
+    t -= c;
+    ++i;
+  }
+  I = i;
+  J = t;
+}
+
+static int oz_ntiles(int nI, int nJ) {
+  int t = 0;
+  for (int i = 0; i < nI; ++i) t += std::min(2 * i + 2, nJ);
+  return t;
+}
+
+__global__ void __launch_bounds__(256) oz_colmax_kernel(const double* __restrict__ W, int64_t ldw, int64_t nrows,
+                                                        int ncols, int64_t rows_per_cta,
+                                                        unsigned long long* __restrict__ cmax) {
+  const int64_t r0 = (int64_t)blockIdx.x * rows_per_cta;
+  const int64_t r1 = min(nrows, r0 + rows_per_cta);
+  for (int c = threadIdx.x; c < ncols; c += blockDim.x) {
+    double m0 = 0.0, m1 = 0.0, m2 = 0.0, m3 = 0.0;
+    int64_t r = r0;
+    for (; r + 3 < r1; r += 4) {
+      m0 = fmax(m0, fabs(W[r * ldw + c]));
+      m1 = fmax(m1, fabs(W[(r + 1) * ldw + c]));
+      m2 = fmax(m2, fabs(W[(r + 2) * ldw + c]));
+      m3 = fmax(m3, fabs(W[(r + 3) * ldw + c]));
+    }
+    for (; r < r1; ++r) m0 = fmax(m0, fabs(W[r * ldw + c]));
+    m0 = fmax(fmax(m0, m1), fmax(m2, m3));
+    if (m0 > 0.0) atomicMax(&cmax[c], (unsigned long long)__double_as_longlong(m0));
+  }
+}
+
+// W rows [0, nrows) -> Ws[kb][p][a][k mod 32] for a < ncp, k < nrp (zero digits outside the matrix); a
+// non-finite entry sets *flag (the reduction then returns NaN, as the FP64 contraction would).
+// Digits without a carry chain: with Y = X + 0x808080808080 the six low bytes y_j of Y give d = y_j - 128
+// (= y_j ^ 0x80 as a signed byte) and the top digit is Y >> 48 (arithmetic): X = sum_j (y_j - 128) 256^j +
+// (Y >> 48) 256^6.  A thread owns one column and 16 rows; byte j of four rows is packed into one word with
+// three byte permutes and stored to the transposed tile T[p][col][rows] (word stride 17: conflict-free).
+__global__ void __launch_bounds__(256) oz_slice_kernel(const double* __restrict__ W, int64_t ldw, int64_t nrows,
+                                                       int ncols, const unsigned long long* __restrict__ cmax,
+                                                       int8_t* __restrict__ Ws, int64_t ncp, int* __restrict__ flag) {
+  __shared__ uint32_t T[OZ_S][64][OZ_TROWS / 4 + 1];
+  const int64_t r0 = (int64_t)blockIdx.x * OZ_TROWS;
+  const int c0 = blockIdx.y * 64;
+  const int col = threadIdx.x & 63, rg = threadIdx.x >> 6;  // rows rg*16 .. rg*16 + 15
+  const int c = c0 + col;
+  const double sc = c < ncols ? ldexp(1.0, 55 - oz_exp(cmax[c])) : 0.0;
+  bool bad = false;
+#pragma unroll
+  for (int g = 0; g < 4; ++g) {
+    uint32_t lo[4], hi[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int64_t r = r0 + rg * 16 + g * 4 + i;
+      double w = (r < nrows && c < ncols) ? W[r * ldw + c] : 0.0;
+      if (!isfinite(w)) {
+        bad = true;
+        w = 0.0;
+      }
+      const long long Y = __double2ll_rn(w * sc) + 0x808080808080LL;
+      lo[i] = (uint32_t)Y;
+      hi[i] = (uint32_t)((unsigned long long)Y >> 32);
+    }
+    const int wi = rg * 4 + g;
+    // slice p >= 1 <-> byte j = 6 - p of Y (biased); slice 0 <-> byte 6 (hi byte 2, unbiased)
+#pragma unroll
+    for (int p = 1; p < OZ_S; ++p) {
+      const int j = 6 - p;
+      const uint32_t* src = j < 4 ? lo : hi;
+      const uint32_t sel = (uint32_t)((j & 3) | (((j & 3) + 4) << 4));
+      const uint32_t x = __byte_perm(src[0], src[1], sel), y = __byte_perm(src[2], src[3], sel);
+      T[p][col][wi] = __byte_perm(x, y, 0x5410) ^ 0x80808080u;
+    }
+    {
+      const uint32_t x = __byte_perm(hi[0], hi[1], 0x62), y = __byte_perm(hi[2], hi[3], 0x62);
+      T[0][col][wi] = __byte_perm(x, y, 0x5410);
+    }
+  }
+  if (bad) atomicOr(flag, 1);
+  __syncthreads();
+  // out: for each k-block kb of the tile and slice p, columns c0..c0+63 are 2 KB contiguous (32 B each)
+  constexpr int NKB = OZ_TROWS / OZ_BK;
+  for (int e = threadIdx.x; e < NKB * OZ_S * 64 * (OZ_BK / 4); e += blockDim.x) {
+    const int w = e % (OZ_BK / 4), cl = (e / (OZ_BK / 4)) % 64;
+    const int p = (e / (OZ_BK / 4 * 64)) % OZ_S, kb = e / (OZ_BK / 4 * 64 * OZ_S);
+    const int64_t kbg = blockIdx.x * NKB + kb;
+    *reinterpret_cast<uint32_t*>(Ws + (((kbg * OZ_S + p) * ncp + c0 + cl) * OZ_BK) + 4 * w) =
+        T[p][cl][kb * (OZ_BK / 4) + w];
+  }
+}
+
+__global__ void __launch_bounds__(192, 1)
+    oz_syrk_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int nunits,
+                   int ntiles, int nJ, int64_t rps, int64_t nrp, double* __restrict__ Gpart) {
+  extern __shared__ uint8_t oz_raw[];
+  uint8_t* st = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(oz_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(st + OZ_STAGES * OZ_STAGE_BYTES);
+  uint64_t* empty = full + OZ_STAGES;
+  uint64_t* tfull = empty + OZ_STAGES;
+  uint64_t* tempty = tfull + 1;
+  uint32_t* tbase = reinterpret_cast<uint32_t*>(tempty + 1);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < OZ_STAGES; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    mbar_init(tfull, 1);
+    mbar_init(tempty, 128);
+    fence_mbar_init();
+  }
+  if (warp == 1) tc_alloc<512>(tbase);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tbase;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      tma_prefetch_desc(&tmA);
+      tma_prefetch_desc(&tmB);
+      int64_t it = 0;
+      for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
+        int I, J;
+        oz_tile(u % ntiles, nJ, I, J);
+        const int64_t k0 = (int64_t)(u / ntiles) * rps, k1 = min(nrp, k0 + rps);
+        for (int64_t k = k0; k < k1; k += OZ_BK, ++it) {
+          const int s = (int)(it % OZ_STAGES);
+          if (it >= OZ_STAGES) mbar_wait(&empty[s], (uint32_t)(((it / OZ_STAGES) - 1) & 1));
+          uint8_t* a = st + s * OZ_STAGE_BYTES;
+          mbar_expect_tx(&full[s], OZ_STAGE_BYTES);
+          tma_load_4d(a, &tmA, 0, I * OZ_BM, 0, (int)(k / OZ_BK), &full[s]);
+          tma_load_4d(a + OZ_A_BYTES, &tmB, 0, J * OZ_BN, 0, (int)(k / OZ_BK), &full[s]);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    int64_t it = 0;
+    int ul = 0;
+    for (int u = blockIdx.x; u < nunits; u += gridDim.x, ++ul) {
+      const int64_t k0 = (int64_t)(u / ntiles) * rps, k1 = min(nrp, k0 + rps);
+      if (ul > 0) mbar_wait(tempty, (uint32_t)((ul - 1) & 1));  // the epilogue has drained the last unit
+      tc_fence_after();
+      for (int64_t k = k0; k < k1; k += OZ_BK, ++it) {
+        const int s = (int)(it % OZ_STAGES);
+        mbar_wait(&full[s], (uint32_t)((it / OZ_STAGES) & 1));
+        tc_fence_after();
+        if (lane == 0) {
+          const uint32_t a0 = smem_u32(st + s * OZ_STAGE_BYTES), b0 = a0 + OZ_A_BYTES;
+          const uint32_t first = k == k0;
+#pragma unroll
+          for (int p = 0; p < OZ_S; ++p) {
+#pragma unroll
+            for (int q0 = 0; q0 < OZ_S - p; q0 += 4) {
+              const int nq = min(4, OZ_S - p - q0);
+              // slice 0 of A initialises every level on the unit's first stage; everything else accumulates
+              tc_mma_i8(tmem + (uint32_t)(OZ_BN * (p + q0)), tc_desc_sw32(a0 + p * OZ_BM * OZ_BK),
+                        tc_desc_sw32(b0 + q0 * OZ_BN * OZ_BK), tc_idesc_i8(OZ_BM, OZ_BN * nq),
+                        (!first) | (p > 0));
+            }
+          }
+          tc_commit(&empty[s]);
+          if (k + OZ_BK >= k1) tc_commit(tfull);
+        }
+        __syncwarp();
+      }
+    }
+  } else {
+    const int q = warp & 3;  // the TMEM lane quarter this warp may read
+    const int row = q * 32 + lane;
+    int ul = 0;
+    for (int u = blockIdx.x; u < nunits; u += gridDim.x, ++ul) {
+      mbar_wait(tfull, (uint32_t)(ul & 1));
+      tc_fence_after();
+      double* out = Gpart + ((size_t)u * OZ_BM + row) * OZ_BN;
+#pragma unroll 1
+      for (int h = 0; h < OZ_BN / 32; ++h) {
+        double t[32];
+        uint32_t v[32];
+        const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(h * 32);
+        tc_ld32(ta + (uint32_t)((OZ_S - 1) * OZ_BN), v);
+        tc_wait_ld();
+#pragma unroll
+        for (int j = 0; j < 32; ++j) t[j] = (double)(int)v[j];
+#pragma unroll 1
+        for (int L = OZ_S - 2; L >= 0; --L) {
+          tc_ld32(ta + (uint32_t)(L * OZ_BN), v);
+          tc_wait_ld();
+#pragma unroll
+          for (int j = 0; j < 32; ++j) t[j] = fma(t[j], 0.00390625, (double)(int)v[j]);
+        }
+#pragma unroll
+        for (int j = 0; j < 32; j += 2) *reinterpret_cast<double2*>(out + h * 32 + j) = make_double2(t[j], t[j + 1]);
+      }
+      tc_fence_before();
+      mbar_arrive(tempty);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 1) tc_free<512>(tmem);
+}
+
+__global__ void oz_reduce_kernel(const double* __restrict__ Gpart, int ntiles, int nsplit, int nJ, int ncols,
+                                 const unsigned long long* __restrict__ cmax, const int* __restrict__ flag,
+                                 double* __restrict__ G, int64_t ldg, int accumulate) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= (int64_t)ntiles * OZ_BM * OZ_BN) return;
+  const int t = (int)(e / (OZ_BM * OZ_BN));
+  const int i = (int)((e / OZ_BN) % OZ_BM), j = (int)(e % OZ_BN);
+  int I, J;
+  oz_tile(t, nJ, I, J);
+  const int a = I * OZ_BM + i, b = J * OZ_BN + j;
+  if (a >= ncols || b >= ncols) return;
+  double s = 0.0;
+  for (int sp = 0; sp < nsplit; ++sp) s += Gpart[(((size_t)sp * ntiles + t) * OZ_BM + i) * OZ_BN + j];
+  double v = ldexp(s, oz_exp(cmax[a]) + oz_exp(cmax[b]) - 14);
+  if (*flag) v = __longlong_as_double(0x7ff8000000000000LL);
+  G[(size_t)a * ldg + b] = accumulate ? G[(size_t)a * ldg + b] + v : v;
+}
+
+// ------------------------------------------------------------------ host
+namespace {
+struct OzPlan {
+  int nI, nJ, ntiles, nsplit;
+  int64_t ncp, nrp, rps;
+};
+
+OzPlan oz_plan(int ncols, int64_t nrows, int sms) {
+  OzPlan P{};
+  P.nI = (ncols + OZ_BM - 1) / OZ_BM;
+  P.nJ = (ncols + OZ_BN - 1) / OZ_BN;
+  P.ntiles = oz_ntiles(P.nI, P.nJ);
+  P.ncp = (int64_t)P.nI * OZ_BM;
+  P.nrp = std::max<int64_t>(OZ_TROWS, (nrows + OZ_TROWS - 1) / OZ_TROWS * OZ_TROWS);
+  // row splits of <= OZ_CHUNK rows (multiples of OZ_BK); among 1-2x the minimum count, the smallest makespan
+  // (waves of `sms` units x rows per unit)
+  const int64_t smin = (P.nrp + OZ_CHUNK - 1) / OZ_CHUNK;
+  double best = 1e300;
+  for (int64_t ns = smin; ns <= 2 * smin; ++ns) {
+    int64_t rps = (P.nrp + ns - 1) / ns;
+    rps = (rps + OZ_BK - 1) / OZ_BK * OZ_BK;
+    const int64_t nsp = (P.nrp + rps - 1) / rps;
+    const int64_t units = nsp * P.ntiles;
+    const double cost = (double)((units + sms - 1) / sms) * (double)rps;
+    if (cost < best * (1.0 - 1e-9)) {
+      best = cost;
+      P.nsplit = (int)nsp;
+      P.rps = rps;
+    }
+  }
+  return P;
+}
+}  // namespace
+
+bool syrk_i8_supported(int ncols) { return ncols >= 1 && ncols <= 4096; }
+
+size_t syrk_i8_ws_bytes(int ncols, int64_t cap_rows) {
+  const OzPlan P = oz_plan(ncols, cap_rows, 148);
+  return (size_t)OZ_S * P.ncp * P.nrp;
+}
+
+// every chunk of <= cap_rows rows plans at most 2 x its minimum split count (oz_plan)
+size_t syrk_i8_part_doubles(int ncols, int64_t cap_rows) {
+  const OzPlan P = oz_plan(ncols, cap_rows, 148);
+  const int64_t smin = (P.nrp + OZ_CHUNK - 1) / OZ_CHUNK;
+  return (size_t)(2 * smin) * P.ntiles * OZ_BM * OZ_BN;
+}
+
+size_t syrk_i8_aux_bytes(int ncols) { return (size_t)((ncols + 127) / 128 * 128) * 8 + 256; }
+
+cudaError_t launch_syrk_i8(const double* W, int64_t ldw, int64_t nrows, int ncols, int8_t* ws, int64_t cap_rows,
+                           double* Gpart, void* aux, double* G, int ldg, int sms, cudaStream_t s) {
+  if (!syrk_i8_supported(ncols) || cap_rows < 1 || (ldw & 1) || (reinterpret_cast<uintptr_t>(W) & 15))
+    return cudaErrorInvalidValue;
+  unsigned long long* cmax = reinterpret_cast<unsigned long long*>(aux);
+  const int ncp0 = (ncols + 127) / 128 * 128;
+  int* flag = reinterpret_cast<int*>(cmax + ncp0);
+  cudaError_t e = cudaMemsetAsync(aux, 0, syrk_i8_aux_bytes(ncols), s);
+  if (e != cudaSuccess) return e;
+  if (nrows > 0) {
+    const int ctas = 4 * sms;
+    const int64_t rpc = (nrows + ctas - 1) / ctas;
+    oz_colmax_kernel<<<(unsigned)((nrows + rpc - 1) / rpc), 256, 0, s>>>(W, ldw, nrows, ncols, rpc, cmax);
+  }
+  e = smem_optin(oz_syrk_kernel, OZ_SMEM);
+  if (e != cudaSuccess) return e;
+  int64_t done = 0;
+  int chunk = 0;
+  do {
+    const int64_t rows = std::min<int64_t>(cap_rows, nrows - done);
+    const OzPlan P = oz_plan(ncols, rows, sms);
+    dim3 gs((unsigned)(P.nrp / OZ_TROWS), (unsigned)(P.ncp / 64));
+    oz_slice_kernel<<<gs, 256, 0, s>>>(W + (size_t)done * ldw, ldw, rows, ncols, cmax, ws, P.ncp, flag);
+    CUtensorMap ta, tb;
+    e = make_tmap_i8_slices(&ta, ws, (uint64_t)(P.nrp / OZ_BK), (uint64_t)P.ncp, OZ_S, OZ_BM);
+    if (e != cudaSuccess) return e;
+    e = make_tmap_i8_slices(&tb, ws, (uint64_t)(P.nrp / OZ_BK), (uint64_t)P.ncp, OZ_S, OZ_BN);
+    if (e != cudaSuccess) return e;
+    const int units = P.nsplit * P.ntiles;
+    oz_syrk_kernel<<<std::min(units, sms), 192, OZ_SMEM, s>>>(ta, tb, units, P.ntiles, P.nJ, P.rps, P.nrp, Gpart);
+    const int64_t tot = (int64_t)P.ntiles * OZ_BM * OZ_BN;
+    oz_reduce_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(Gpart, P.ntiles, P.nsplit, P.nJ, ncols, cmax, flag,
+                                                                   G, ldg, chunk > 0);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    done += rows;
+    ++chunk;
+  } while (done < nrows);
+  return cudaSuccess;
+}
+
+}  // namespace vif

@@ -67,6 +67,15 @@ int gemm_tt_nsplit(int M, int N, int64_t nrows, int num_sms);
 size_t gemm_tt_part_doubles(int M, int N, int nsplit);
 cudaError_t launch_gemm_tt(const double* A, int64_t lda, int M, const double* B, int64_t ldb, int N, int64_t nrows,
                            int nsplit, double* part, double* C, int64_t ldc, cudaStream_t s);
+// K4 on the integer tensor cores (k_ozaki.cu): int8 digit slices of W, tcgen05.mma.kind::i8, exact int32
+// level sums; rows processed in chunks of <= cap_rows (ws: syrk_i8_ws_bytes, Gpart: syrk_i8_part_doubles,
+// aux: syrk_i8_aux_bytes)
+bool syrk_i8_supported(int ncols);
+size_t syrk_i8_ws_bytes(int ncols, int64_t cap_rows);
+size_t syrk_i8_part_doubles(int ncols, int64_t cap_rows);
+size_t syrk_i8_aux_bytes(int ncols);
+cudaError_t launch_syrk_i8(const double* W, int64_t ldw, int64_t nrows, int ncols, int8_t* ws, int64_t cap_rows,
+                           double* Gpart, void* aux, double* G, int ldg, int sms, cudaStream_t s);
 // sums the partials of nlaunch consecutive launch_syrk_part calls (same ncols, nsplit) into G
 cudaError_t launch_syrk_reduce(const double* Gpart, int ncols, int nsplit, int nlaunch, double* G, int ldg,
                                cudaStream_t s);

@@ -42,4 +42,21 @@ cudaError_t make_tmap_f64(CUtensorMap* map, const double* base, uint64_t rows, u
   return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
 
+cudaError_t make_tmap_i8_slices(CUtensorMap* map, const int8_t* base, uint64_t nkb, uint64_t rows, uint32_t nslice,
+                                uint32_t box_rows) {
+  EncodeTiled enc = encode_fn();
+  if (!enc) return cudaErrorNotSupported;
+  if ((reinterpret_cast<uintptr_t>(base) & 15) || nkb == 0 || box_rows < 1 || box_rows > 256 || rows == 0 ||
+      nslice == 0 || nslice > 256)
+    return cudaErrorInvalidValue;
+  const cuuint64_t dims[4] = {32, rows, nslice, nkb};
+  const cuuint64_t strides[3] = {32, 32 * rows, 32 * rows * nslice};
+  const cuuint32_t box[4] = {32, box_rows, nslice, 1};
+  const cuuint32_t estr[4] = {1, 1, 1, 1};
+  const CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, const_cast<int8_t*>(base), dims, strides, box, estr,
+                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+
 }  // namespace vif

@@ -22,6 +22,12 @@ namespace vif {
 cudaError_t make_tmap_f64(CUtensorMap* map, const double* base, uint64_t rows, uint64_t cols, uint64_t ld,
                           uint32_t box_rows);
 
+// 4-D map over int8 digit slices stored [nkb][nslice][rows][32] (blocks of 32 k-values, each block holding
+// every slice and row contiguously): box = {32 B of k, box_rows rows, all nslice slices, 1 block}, SWIZZLE_32B
+// (the K-major tcgen05 operand layout, tc.cuh); one box reads nslice contiguous runs of box_rows x 32 B
+cudaError_t make_tmap_i8_slices(CUtensorMap* map, const int8_t* base, uint64_t nkb, uint64_t rows, uint32_t nslice,
+                                uint32_t box_rows);
+
 // ------------------------------------------------------------------ device
 __device__ __forceinline__ uint32_t swz_off(int r, int c) {
   return (uint32_t)(r * 128 + ((((c >> 1) ^ (r & 7)) & 7) << 4) + (c & 1) * 8);

@@ -13,6 +13,7 @@
 // beyond the CUDA driver.
 #include <dlfcn.h>
 #include <math.h>
+#include <stdlib.h>
 #include <nccl.h>
 #include <stdio.h>
 #include <string.h>
@@ -85,12 +86,14 @@ struct Plan {
   int mk, ycol, ld;
   int64_t rounds, chunk, npos, npad;
   int nsplit, nsplit_round;
+  bool syrk_i8;    // K4 on the integer tensor cores (k_ozaki.cu); VIF_SYRK_FP64=1 keeps the DMMA SYRK
+  int64_t oz_cap;  // rows per digit-slice chunk
   std::vector<int64_t> n_own;
 };
 
 enum Buf {
   B_X, B_Z, B_NBR, B_Y, B_KM, B_LINV, B_U, B_W, B_DPOS, B_ORDER, B_KEYS, B_KEYS2, B_VALS, B_VALS2, B_TEMP,
-  B_GPART, B_G, B_GSUM, B_LINVM, B_TSCR, B_PART, B_BBOX, B_TERMS, B_STATUS,
+  B_GPART, B_G, B_GSUM, B_LINVM, B_TSCR, B_PART, B_BBOX, B_TERMS, B_STATUS, B_WS, B_OZAUX,
   // second input slot (vif_stage_data: inputs of the next evaluation copied while this one runs)
   B_X2, B_Z2, B_NBR2, B_Y2, B_ORDER2,
   // sort scratch of the staging path (its sort runs on the copy stream, beside the main stream's work)
@@ -161,6 +164,11 @@ bool make_plan(const vif_dims* dims, bool emulate, Plan& P, std::string& err) {
     }
   P.nsplit = syrk_nsplit(P.ld, P.npos, kPlanSMs);
   P.nsplit_round = syrk_nsplit(P.ld, P.chunk, kPlanSMs);
+  {
+    const char* f = getenv("VIF_SYRK_FP64");
+    P.syrk_i8 = syrk_i8_supported(P.ld) && !(f && f[0] == '1');
+    P.oz_cap = std::min<int64_t>(std::max<int64_t>(P.npos, 1), (int64_t)1 << 20);
+  }
   return true;
 }
 
@@ -185,6 +193,11 @@ Layout make_layout(const Plan& P) {
   L.size[B_TEMP] = order_temp_bytes(P.npos);
   L.size[B_GPART] = std::max(syrk_part_doubles(P.ld, P.nsplit),
                              (size_t)P.rounds * syrk_part_doubles(P.ld, P.nsplit_round)) * D8;
+  if (P.syrk_i8) {
+    L.size[B_GPART] = std::max(L.size[B_GPART], syrk_i8_part_doubles(P.ld, P.oz_cap) * D8);
+    L.size[B_WS] = syrk_i8_ws_bytes(P.ld, P.oz_cap);
+    L.size[B_OZAUX] = syrk_i8_aux_bytes(P.ld);
+  }
   L.size[B_G] = nrep * gsz;
   L.size[B_GSUM] = gsz;
   L.size[B_LINVM] = (size_t)mk1 * mk1 * D8;
@@ -216,7 +229,7 @@ Layout make_layout(const Plan& P) {
 enum Stage { S_KM = 0, S_UFEAT, S_GATHER, S_VECCHIA, S_SYRK, S_REDUCE, S_CHOLM, S_FINISH, S_COUNT };
 const char* kStageNames[S_COUNT] = {
     "K0 K_m + chol/inv (cooperative)", "K1 U features (kx_eval + gemm_tn)", "A2 U all-gather (NCCL)",
-    "K2+K3 vecchia rows (gather + DMMA Gram + chol + W row)", "K4 syrk (DMMA split-K + reduce)",
+    "K2+K3 vecchia rows (gather + DMMA Gram + chol + W row)", "K4 syrk (int8 digit slices on tcgen05; DMMA with VIF_SYRK_FP64=1)",
     "A6/A7 sum log D + all-reduce", "K5 chol/inv of M (cooperative)", "K5 finish (z, quad, NLL)"};
 
 struct Handle {
@@ -1155,13 +1168,19 @@ int vif_factor(void* handle, const vif_theta* theta, double* B_out, double* D_ou
     h->mark(S_VECCHIA, 1);
     double* G = h->buf<double>(B_G) + g * gstride;
     h->mark(S_SYRK, 0);
-    VIF_CUDA(h, launch_syrk(Wg, P.ld, npts, P.ld, P.nsplit, h->buf<double>(B_GPART), G, P.ld, s), "syrk");
+    if (P.syrk_i8)
+      VIF_CUDA(h, launch_syrk_i8(Wg, P.ld, npts, P.ld, h->buf<int8_t>(B_WS), P.oz_cap, h->buf<double>(B_GPART),
+                                 h->buf<char>(B_OZAUX), G, P.ld, kPlanSMs, s),
+               "syrk (int8 slices)");
+    else
+      VIF_CUDA(h, launch_syrk(Wg, P.ld, npts, P.ld, P.nsplit, h->buf<double>(B_GPART), G, P.ld, s), "syrk");
     h->mark(S_SYRK, 1);
     h->mark(S_REDUCE, 0);
     VIF_CUDA(h, launch_logd_sum(Dg, npts, h->buf<double>(B_PART), kLogdParts,
                                 G + (size_t)P.ld * P.ld, s),
              "logd");
-    nl += 4;
+    // DMMA: syrk part + reduce; int8 slices: colmax + per chunk (slice, tcgen05 syrk, reduce); + logd (2)
+    nl += P.syrk_i8 ? 3 + 3 * (int)((std::max<int64_t>(npts, 1) + P.oz_cap - 1) / P.oz_cap) : 4;
   }
   // A7
   if (P.emulate) {
@@ -1848,6 +1867,47 @@ int vif_copy_U(void* handle, double* out) {
                                 cudaMemcpyDefault, h->stream),
            "copy U");
   VIF_WAIT(h, h->stream);
+  return VIF_OK;
+}
+
+int vif_gram(const double* W, int64_t ldw, int64_t nrows, int32_t ncols, double* G, int64_t ldg, int32_t engine,
+             void* stream) {
+  if (!W || !G || ncols < 1 || nrows < 0 || ldw < ncols || (ldw & 1) || ldg < ncols || engine < 0 || engine > 1 ||
+      (engine == 0 && !syrk_i8_supported(ncols)) || (reinterpret_cast<uintptr_t>(W) & 15))
+    return fail(nullptr, VIF_ERR_INVALID_ARG, "vif_gram: invalid argument");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  char* scratch = nullptr;
+  size_t ws = 0, part = 0, aux = 0;
+  int nsplit = 0;
+  const int64_t cap = std::min<int64_t>(std::max<int64_t>(nrows, 1), (int64_t)1 << 20);
+  if (engine == 0) {
+    ws = (syrk_i8_ws_bytes(ncols, cap) + 255) / 256 * 256;
+    part = syrk_i8_part_doubles(ncols, cap) * sizeof(double);
+    aux = syrk_i8_aux_bytes(ncols);
+  } else {
+    nsplit = syrk_nsplit(ncols, nrows, kPlanSMs);
+    part = syrk_part_doubles(ncols, nsplit) * sizeof(double);
+  }
+  {
+    // keep freed scratch in the device's default pool between calls (no re-mapping of GBs per call)
+    int dev = 0;
+    cudaMemPool_t pool;
+    if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t thr = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+  }
+  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&scratch), ws + part + aux + 256, s);
+  if (e != cudaSuccess) return fail(nullptr, VIF_ERR_CUDA, std::string("vif_gram: ") + cudaGetErrorString(e));
+  double* gpart = reinterpret_cast<double*>(scratch + ws);
+  if (engine == 0)
+    e = launch_syrk_i8(W, ldw, nrows, ncols, reinterpret_cast<int8_t*>(scratch), cap, gpart,
+                       scratch + ws + (part + 255) / 256 * 256, G, (int)ldg, kPlanSMs, s);
+  else
+    e = launch_syrk(W, ldw, nrows, ncols, nsplit, gpart, G, (int)ldg, s);
+  const cudaError_t e2 = cudaFreeAsync(scratch, s);
+  if (e == cudaSuccess) e = e2;
+  if (e != cudaSuccess) return fail(nullptr, VIF_ERR_CUDA, std::string("vif_gram: ") + cudaGetErrorString(e));
   return VIF_OK;
 }
 

@@ -81,6 +81,7 @@ def load_library():
         lib.vif_nll.argtypes = [P, ctypes.POINTER(_Terms)]
         lib.vif_copy_U.argtypes = [P, P]
         lib.vif_launch_count.argtypes = [P, ctypes.POINTER(i64)]
+        lib.vif_gram.argtypes = [P, i64, i64, i32, P, i64, i32, P]
         lib.vif_last_error.argtypes = [P]
         lib.vif_last_error.restype = ctypes.c_char_p
         lib.vif_profile.argtypes = [P, i32]
@@ -103,7 +104,7 @@ def load_library():
         lib.vif_la_nll.argtypes = [P, P, P, ctypes.POINTER(_LaOpts), P, P, P, ctypes.POINTER(_LaTerms)]
         for f in ("vif_nccl_unique_id", "vif_workspace_bytes", "vif_partition", "vif_create", "vif_set_data",
                   "vif_factor", "vif_nll", "vif_copy_U", "vif_launch_count", "vif_profile", "vif_stage_times",
-                  "vif_grad_workspace_bytes", "vif_grad", "vif_predict_workspace_bytes", "vif_predict",
+                  "vif_gram", "vif_grad_workspace_bytes", "vif_grad", "vif_predict_workspace_bytes", "vif_predict",
                   "vif_neighbors", "vif_stage_data", "vif_owned_rows", "vif_la_workspace_bytes", "vif_la_prepare", "vif_la_apply",
                   "vif_la_nll"):
             getattr(lib, f).restype = ctypes.c_int
@@ -115,7 +116,7 @@ EXPORTED = ("vif_nccl_unique_id", "vif_workspace_bytes", "vif_partition", "vif_c
             "vif_factor", "vif_nll", "vif_copy_U", "vif_launch_count", "vif_profile", "vif_stage_times",
             "vif_stage_name", "vif_last_error", "vif_destroy", "vif_grad_workspace_bytes", "vif_grad",
             "vif_predict_workspace_bytes", "vif_predict", "vif_neighbors", "vif_stage_data",
-            "vif_la_workspace_bytes", "vif_la_prepare", "vif_la_apply", "vif_la_nll", "vif_owned_rows")
+            "vif_la_workspace_bytes", "vif_la_prepare", "vif_la_apply", "vif_la_nll", "vif_owned_rows", "vif_gram")
 LA_OPS = {"sigma": 0, "A": 1, "binv": 2, "btinv": 3, "fitc_solve": 4, "sigma_inv": 5, "A1": 6}
 NUM_STAGES = 8
 
@@ -343,6 +344,26 @@ def vif_owned_rows(h):
 
 def vif_copy_U(h, out: torch.Tensor):
     _check(load_library().vif_copy_U(h, _ptr(out)), h)
+
+
+GRAM_ENGINES = {"int8": 0, "fp64": 1}
+
+
+def vif_gram(W: torch.Tensor, engine: str = "int8", stream: Optional[torch.cuda.Stream] = None) -> torch.Tensor:
+    """G = W^T W (lower triangle written; the rest mirrored here) for a CUDA float64 matrix W (nrows x ncols,
+    row stride even).  engine: "int8" (tcgen05 integer slices) or "fp64" (DMMA).  Stream-ordered on `stream`
+    (default: the current stream)."""
+    if not (isinstance(W, torch.Tensor) and W.is_cuda and W.dtype == torch.float64 and W.dim() == 2):
+        raise TypeError("W must be a 2-D CUDA float64 tensor")
+    if W.stride(1) != 1:
+        W = W.contiguous()
+    if W.stride(0) % 2:
+        W = torch.nn.functional.pad(W, (0, 1))[:, :W.shape[1]]
+    n, c = W.shape
+    G = torch.zeros((c, c), dtype=torch.float64, device=W.device)
+    s = (stream or torch.cuda.current_stream(W.device)).cuda_stream
+    _check(load_library().vif_gram(_ptr(W), W.stride(0), n, c, _ptr(G), c, GRAM_ENGINES[engine], s))
+    return torch.tril(G) + torch.tril(G, -1).T
 
 
 def vif_launch_count(h) -> int:

@@ -1,0 +1,92 @@
+"""vif_gram: G = W^T W (A6 / K4, "M") on the integer tensor cores (int8 digit slices, tcgen05 kind::i8,
+k_ozaki.cu) and on the FP64 DMMA engine, against an exact reference.
+
+The reference is computed in float128-free exact arithmetic where it matters: each G entry is a plain dot
+product; numpy's float64 matmul (pairwise/blocked summation) has error ~ k * 2^-53 * sum|w_a||w_b|, so the
+comparison tolerance is derived from that bound (plus the slices' 2^-54 column-relative representation)."""
+import numpy as np
+import pytest
+import torch
+
+import paper_2507_05064_b200 as p
+
+pytestmark = pytest.mark.gpu
+
+
+def _ref(W):
+    return W.T @ W
+
+
+def _bound(W):
+    A = np.abs(W)
+    k = W.shape[0]
+    # FP64 reference error + slice representation (2^-54 of the column maximum per factor) per term
+    cm = A.max(0)
+    return 4 * k * 2.0 ** -52 * (A.T @ A) + 4 * k * 2.0 ** -53 * np.outer(cm, cm) + 1e-300
+
+
+@pytest.mark.parametrize("engine", ["int8", "fp64"])
+@pytest.mark.parametrize("n,c", [(1, 1), (7, 3), (100, 64), (1000, 130), (40000, 512), (20000, 333), (70000, 1001)])
+def test_gram_matches_reference(engine, n, c):
+    rng = np.random.default_rng(n * 7919 + c)
+    W = rng.standard_normal((n, c)) * np.exp(rng.uniform(-3, 3, size=c))  # columns of very different scales
+    Wt = torch.from_numpy(W).cuda()
+    G = p.vif_gram(Wt, engine).cpu().numpy()
+    torch.cuda.synchronize()
+    R = _ref(W)
+    err = np.abs(G - R)
+    assert np.all(err <= _bound(W)), (engine, float((err / _bound(W)).max()))
+
+
+def test_gram_multichunk_and_int32_limit():
+    """more rows than one digit-slice chunk (2^20) and than one int32 accumulation (16,384 rows) with every
+    entry at the digit extremes: the level sums would overflow int32 if a unit ever spanned more rows"""
+    n, c = (1 << 20) + 4099, 72
+    W = torch.full((n, c), -1.0, dtype=torch.float64, device="cuda")
+    W[::2] = 1.0 - 2.0 ** -40
+    G = p.vif_gram(W, "int8").cpu().numpy()
+    Wh = W.cpu().numpy()
+    R = Wh.T @ Wh
+    assert np.allclose(G, R, rtol=1e-13, atol=0)
+
+
+def test_gram_nonfinite_gives_nan():
+    W = torch.randn(5000, 64, dtype=torch.float64, device="cuda")
+    W[1234, 5] = float("nan")
+    G = p.vif_gram(W, "int8").cpu().numpy()
+    assert np.isnan(G).all()
+
+
+def test_gram_engines_agree_on_factor_rows():
+    """the two engines on a W with the structure of the factor's rows (whitened residual rows + y column)"""
+    rng = np.random.default_rng(3)
+    n, c = 200000, 505
+    W = rng.standard_normal((n, c)) * np.linspace(0.01, 3.0, c)
+    Wt = torch.from_numpy(W).cuda()
+    Gi = p.vif_gram(Wt, "int8").cpu().numpy()
+    Gf = p.vif_gram(Wt, "fp64").cpu().numpy()
+    assert np.max(np.abs(Gi - Gf)) <= 1e-12 * np.abs(Gf).max()
+
+
+@pytest.mark.parametrize("cid,n", [(1, None), (4, 20000)])
+def test_factor_engines_agree(monkeypatch, cid, n):
+    """vif_factor + vif_nll with the integer-slice K4 (default) and with the DMMA K4 (VIF_SYRK_FP64=1, read at
+    vif_create): the NLL terms agree to 1e-12 relative (config 4 recipe: m = 1000, ld = 1008)"""
+    import sys, os
+    sys.path.insert(0, os.path.join(os.path.dirname(__file__), ".."))
+    import vifgen
+    w = vifgen.make_config(cid, device="cuda", n=n)
+    th = p.Theta(**w.theta_dict())
+    dev = torch.device("cuda")
+    res = {}
+    for eng in ("int8", "fp64"):
+        if eng == "fp64":
+            monkeypatch.setenv("VIF_SYRK_FP64", "1")
+        else:
+            monkeypatch.delenv("VIF_SYRK_FP64", raising=False)
+        m = p.VifModel(*(torch.from_numpy(np.ascontiguousarray(a)).to(dev) for a in (w.X, w.Z, w.nbr, w.y)))
+        t = m.evaluate(th)
+        res[eng] = (t.nll, t.logdet_D, t.logdet_M, t.quad)
+        m.close()
+    for a, b in zip(res["int8"], res["fp64"]):
+        assert abs(a - b) <= 1e-12 * max(abs(b), 1.0), (res,)
