@@ -161,6 +161,11 @@ __device__ __forceinline__ double cov_fast(const double* __restrict__ a, const d
   return fma(E, fma(t2, 1.0 / 3.0, t), E);  // (1 + t + t^2/3) E
 }
 
+// processing position p of a rank -> global row (rows sharded chunk-cyclically over `world` ranks)
+__device__ __forceinline__ int64_t pos_to_row(int64_t p, int64_t chunk, int world, int rank) {
+  return (p / chunk) * (int64_t)world * chunk + (int64_t)rank * chunk + p % chunk;
+}
+
 // D(8x8) += A(8x4) * B(4x8), FP64 tensor core
 __device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double b) {
   asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"

@@ -44,6 +44,10 @@ constexpr int OZ_A_BYTES = OZ_S * OZ_BM * OZ_BK;
 constexpr int OZ_B_BYTES = OZ_S * OZ_BN * OZ_BK;
 constexpr int OZ_STAGE_BYTES = OZ_A_BYTES + OZ_B_BYTES;
 constexpr size_t OZ_SMEM = (size_t)OZ_STAGES * OZ_STAGE_BYTES + 1024 + 256;
+constexpr int OZ_EPI_LD = 33;  // staging row stride (doubles): conflict-free column writes and row reads
+constexpr int OZ_GEPI = 8;     // epilogue warps of the K1 GEMM: two per TMEM lane quarter (16-column chunks)
+constexpr int OZ_GLD = 17;     // their staging row stride (doubles)
+constexpr size_t OZ_GEMM_SMEM = OZ_SMEM + (size_t)OZ_GEPI * 32 * OZ_GLD * 8 + 512;
 constexpr int OZ_TROWS = 64;      // slicer tile
 }  // namespace
 
@@ -155,6 +159,45 @@ __global__ void __launch_bounds__(256) oz_slice_kernel(const double* __restrict_
   }
 }
 
+// One stage of MMAs (issued by one thread): A slice p (OZ_BM rows) times the concatenated B slices
+// 0..6-p (OZ_BN rows each, contiguous in shared memory) into TMEM columns OZ_BN p ..: level L = p + q lands in
+// columns [OZ_BN L, OZ_BN (L + 1)).  On the first stage of a tile slice 0 of A initialises every level.
+__device__ __forceinline__ void oz_issue_stage(uint32_t tmem, uint32_t a0, bool first) {
+  const uint32_t b0 = a0 + OZ_A_BYTES;
+#pragma unroll
+  for (int p = 0; p < OZ_S; ++p) {
+#pragma unroll
+    for (int q0 = 0; q0 < OZ_S - p; q0 += 4) {
+      const int nq = min(4, OZ_S - p - q0);
+      tc_mma_i8(tmem + (uint32_t)(OZ_BN * (p + q0)), tc_desc_sw32(a0 + p * OZ_BM * OZ_BK),
+                tc_desc_sw32(b0 + q0 * OZ_BN * OZ_BK), tc_idesc_i8(OZ_BM, OZ_BN * nq), (!first) | (p > 0));
+    }
+  }
+}
+
+// int32 -> double, exact: 2^52 + 2^31 + v has v + 2^31 in its low mantissa bits (one LOP + one DADD on the
+// FP64 pipe instead of a conversion)
+__device__ __forceinline__ double oz_i2d(uint32_t v) {
+  return __hiloint2double(0x43300000, (int)(v ^ 0x80000000u)) - 4503601774854144.0;
+}
+
+// 32 accumulator columns of this thread's TMEM lane (ta = lane quarter + column), all 7 levels combined in
+// FP64: t = sum_L acc_L 2^(-8L) (Horner from the last level)
+__device__ __forceinline__ void oz_drain32(uint32_t ta, double (&t)[32]) {
+  uint32_t v[32];
+  tc_ld32(ta + (uint32_t)((OZ_S - 1) * OZ_BN), v);
+  tc_wait_ld();
+#pragma unroll
+  for (int j = 0; j < 32; ++j) t[j] = oz_i2d(v[j]);
+#pragma unroll 1
+  for (int L = OZ_S - 2; L >= 0; --L) {
+    tc_ld32(ta + (uint32_t)(L * OZ_BN), v);
+    tc_wait_ld();
+#pragma unroll
+    for (int j = 0; j < 32; ++j) t[j] = fma(t[j], 0.00390625, oz_i2d(v[j]));
+  }
+}
+
 __global__ void __launch_bounds__(192, 1)
     oz_syrk_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int nunits,
                    int ntiles, int nJ, int64_t rps, int64_t nrp, double* __restrict__ Gpart) {
@@ -212,19 +255,7 @@ __global__ void __launch_bounds__(192, 1)
         mbar_wait(&full[s], (uint32_t)((it / OZ_STAGES) & 1));
         tc_fence_after();
         if (lane == 0) {
-          const uint32_t a0 = smem_u32(st + s * OZ_STAGE_BYTES), b0 = a0 + OZ_A_BYTES;
-          const uint32_t first = k == k0;
-#pragma unroll
-          for (int p = 0; p < OZ_S; ++p) {
-#pragma unroll
-            for (int q0 = 0; q0 < OZ_S - p; q0 += 4) {
-              const int nq = min(4, OZ_S - p - q0);
-              // slice 0 of A initialises every level on the unit's first stage; everything else accumulates
-              tc_mma_i8(tmem + (uint32_t)(OZ_BN * (p + q0)), tc_desc_sw32(a0 + p * OZ_BM * OZ_BK),
-                        tc_desc_sw32(b0 + q0 * OZ_BN * OZ_BK), tc_idesc_i8(OZ_BM, OZ_BN * nq),
-                        (!first) | (p > 0));
-            }
-          }
+          oz_issue_stage(tmem, smem_u32(st + s * OZ_STAGE_BYTES), k == k0);
           tc_commit(&empty[s]);
           if (k + OZ_BK >= k1) tc_commit(tfull);
         }
@@ -242,19 +273,7 @@ __global__ void __launch_bounds__(192, 1)
 #pragma unroll 1
       for (int h = 0; h < OZ_BN / 32; ++h) {
         double t[32];
-        uint32_t v[32];
-        const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(h * 32);
-        tc_ld32(ta + (uint32_t)((OZ_S - 1) * OZ_BN), v);
-        tc_wait_ld();
-#pragma unroll
-        for (int j = 0; j < 32; ++j) t[j] = (double)(int)v[j];
-#pragma unroll 1
-        for (int L = OZ_S - 2; L >= 0; --L) {
-          tc_ld32(ta + (uint32_t)(L * OZ_BN), v);
-          tc_wait_ld();
-#pragma unroll
-          for (int j = 0; j < 32; ++j) t[j] = fma(t[j], 0.00390625, (double)(int)v[j]);
-        }
+        oz_drain32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(h * 32), t);
 #pragma unroll
         for (int j = 0; j < 32; j += 2) *reinterpret_cast<double2*>(out + h * 32 + j) = make_double2(t[j], t[j + 1]);
       }
@@ -284,6 +303,278 @@ __global__ void oz_reduce_kernel(const double* __restrict__ Gpart, int ntiles, i
   double v = ldexp(s, oz_exp(cmax[a]) + oz_exp(cmax[b]) - 14);
   if (*flag) v = __longlong_as_double(0x7ff8000000000000LL);
   G[(size_t)a * ldg + b] = accumulate ? G[(size_t)a * ldg + b] + v : v;
+}
+
+
+// ================================================================== K1 on the integer tensor cores
+// U_aug[i][j] = sum_{k <= j} S[p][k] Linv[j][k] (reading c4), S = K(X, Z) with i = row(p):
+// both operands are split per ROW (of S: position p; of Linv: output column j) -- the scale factors then
+// sit outside the k sum: U = 2^(e_p + e_j - 14) sum_L acc_L 2^(-8L).
+
+// K1a: one warp per position.  Pass 1 finds the row's smallest scaled distance t2 to the inducing points
+// (2D + 1 operations per column, no exponential): the row maximum of S is the covariance at that distance,
+// which fixes the row's scale e_p before any value is formed.  Pass 2 evaluates S and writes the digit
+// slices Ss[kb][q][pos][k mod 32] straight from registers: lane l evaluates the four consecutive columns
+// 128t + 4l + j (one 4-byte store per slice), reading Z from a permuted table (column b at 128 (b/128) +
+// 32 (b%4) + (b%128)/4, so the lanes of a step read consecutive entries; padding columns sit at 1e100 and
+// evaluate to 0).  Also writes the y column and the zero pad columns of U_aug (as kx_eval does).
+template <int FAM, int D>
+__global__ void __launch_bounds__(256) kx_slice_kernel(const double* __restrict__ X, const double* __restrict__ Z,
+                                                       const double* __restrict__ y, int64_t n, int64_t npos,
+                                                       int64_t chunk, int world, int rank, int64_t pos0, int m,
+                                                       int mk, int KP, CovParams p, int8_t* __restrict__ Ss,
+                                                       int64_t kbA, int* __restrict__ erow,
+                                                       double* __restrict__ Uaug, int ld) {
+  extern __shared__ double kxs_sm[];  // KPr x D, permuted
+  __shared__ double tbl[64];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int KPr = (KP + 127) & ~127;
+  double* zs = kxs_sm;
+  exp_table_init(tbl, p.sigma2, threadIdx.x);
+  double sc[D];
+#pragma unroll
+  for (int k = 0; k < D; ++k) sc[k] = fam_scale<FAM>() * p.inv_ls[k];
+  for (int b = threadIdx.x; b < KPr; b += blockDim.x) {
+    const int q = (b & ~127) + 32 * (b & 3) + ((b & 127) >> 2);
+#pragma unroll
+    for (int k = 0; k < D; ++k) zs[q * D + k] = b < m ? Z[b * D + k] * sc[k] : 1e100;
+  }
+  __syncthreads();
+  auto cov_t2 = [&](double t2) -> double {
+    if (FAM == FAM_GAUSS) return sig2_exp_neg(t2, tbl);
+    const double t = sqrt_fast(t2);
+    const double E = sig2_exp_neg(t, tbl);
+    return FAM == FAM_M12 ? E : (FAM == FAM_M32 ? fma(E, t, E) : fma(E, fma(t2, 1.0 / 3.0, t), E));
+  };
+  for (int64_t pos = (int64_t)blockIdx.x * 8 + warp; pos < npos; pos += (int64_t)gridDim.x * 8) {
+    const int64_t i = pos_to_row(pos0 + pos, chunk, world, rank);
+    if (i >= n) continue;  // padding position: its output rows are never written
+    double x[D];
+#pragma unroll
+    for (int k = 0; k < D; ++k) x[k] = X[i * D + k] * sc[k];
+    auto dist2 = [&](int q) -> double {
+      const double* z = zs + q * D;
+      const double d0 = x[0] - z[0];
+      double t2 = d0 * d0;
+#pragma unroll
+      for (int k = 1; k < D; ++k) {
+        const double dk = x[k] - z[k];
+        t2 = fma(dk, dk, t2);
+      }
+      return t2;
+    };
+    double t2min = 1e300;
+#pragma unroll 4
+    for (int q = lane; q < KPr; q += 32) t2min = fmin(t2min, dist2(q));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) t2min = fmin(t2min, __shfl_xor_sync(0xffffffffu, t2min, o));
+    const double rmax = cov_t2(t2min);  // the covariance decreases with the distance
+    const int er = oz_exp((unsigned long long)__double_as_longlong(rmax));
+    if (lane == 0) erow[pos] = er;
+    const double scl = ldexp(1.0, 55 - er);
+    for (int t = 0; t < KPr / 128; ++t) {
+      uint32_t lo[4], hi[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const double v = cov_t2(dist2(128 * t + 32 * j + lane));
+        const long long Y = __double2ll_rn(v * scl) + 0x808080808080LL;
+        lo[j] = (uint32_t)Y;
+        hi[j] = (uint32_t)((unsigned long long)Y >> 32);
+      }
+      const int b0 = 128 * t + 4 * lane;
+      if (b0 >= KP) continue;
+      // row-block-major: [R][kb][q][128 rows][32 B] -- a row block's slices are one contiguous 7 x 4 KB x kb run
+      int8_t* dst = Ss + ((((pos >> 7) * kbA + (b0 >> 5)) * OZ_S) * OZ_BM + (pos & 127)) * OZ_BK + (b0 & 31);
+#pragma unroll
+      for (int q = 1; q < OZ_S; ++q) {
+        const int j = 6 - q;
+        const uint32_t* src = j < 4 ? lo : hi;
+        const uint32_t sel = (uint32_t)((j & 3) | (((j & 3) + 4) << 4));
+        const uint32_t xx = __byte_perm(src[0], src[1], sel), yy = __byte_perm(src[2], src[3], sel);
+        *reinterpret_cast<uint32_t*>(dst + q * OZ_BM * OZ_BK) = __byte_perm(xx, yy, 0x5410) ^ 0x80808080u;
+      }
+      {
+        const uint32_t xx = __byte_perm(hi[0], hi[1], 0x62), yy = __byte_perm(hi[2], hi[3], 0x62);
+        *reinterpret_cast<uint32_t*>(dst) = __byte_perm(xx, yy, 0x5410);
+      }
+    }
+    {
+      double* urow = Uaug + i * (int64_t)ld;
+      for (int c = mk + lane; c < ld; c += 32) urow[c] = (c == mk) ? y[i] : 0.0;
+    }
+  }
+}
+
+// rows of a small row-major matrix A (nrows x ncols, lda) -> digit slices out[kb][q][r][k mod 32] for
+// r < nrows_p, k < 32 nkb (zeros outside A), with the per-row scale 2^e_r in rscale[r]; one warp per row
+__global__ void __launch_bounds__(256) oz_rows_slice_kernel(const double* __restrict__ A, int64_t lda, int nrows,
+                                                            int ncols, int nrows_p, int nkb, int8_t* __restrict__ out,
+                                                            double* __restrict__ rscale) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int r = blockIdx.x * 8 + warp;
+  if (r >= nrows_p) return;
+  const int KP = nkb * OZ_BK;
+  double mx = 0.0;
+  for (int b = lane; b < KP; b += 32)
+    if (r < nrows && b < ncols) mx = fmax(mx, fabs(A[(int64_t)r * lda + b]));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  const int er = oz_exp((unsigned long long)__double_as_longlong(mx));
+  if (lane == 0) rscale[r] = ldexp(1.0, er);
+  const double scl = ldexp(1.0, 55 - er);
+  for (int b = lane; b < KP; b += 32) {
+    const double v = (r < nrows && b < ncols) ? A[(int64_t)r * lda + b] : 0.0;
+    long long X = __double2ll_rn(v * scl);
+    int8_t* dst = out + (((int64_t)(b >> 5) * OZ_S) * nrows_p + r) * OZ_BK + (b & 31);
+#pragma unroll
+    for (int q = OZ_S - 1; q >= 1; --q) {
+      int d = (int)(X & 255);
+      d -= (d & 128) << 1;
+      dst[(int64_t)q * nrows_p * OZ_BK] = (int8_t)d;
+      X = (X - d) >> 8;
+    }
+    dst[0] = (int8_t)X;
+  }
+}
+
+// 16 accumulator columns, all 7 levels: the 7 TMEM loads are in flight together (one wait)
+__device__ __forceinline__ void oz_drain16(uint32_t ta, double (&t)[16]) {
+  uint32_t v[OZ_S][16];
+#pragma unroll
+  for (int L = 0; L < OZ_S; ++L) tc_ld16(ta + (uint32_t)(L * OZ_BN), v[L]);
+  tc_wait_ld();
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    double a = oz_i2d(v[OZ_S - 1][j]);
+#pragma unroll
+    for (int L = OZ_S - 2; L >= 0; --L) a = fma(a, 0.00390625, oz_i2d(v[L][j]));
+    t[j] = a;
+  }
+}
+
+// K1b: persistent; unit = a row block R of 128 positions with all its column tiles J = nJ-1 .. 0 (every unit
+// has the same triangular work, and the row block's A slices stay in L2 from tile to tile); per tile the
+// k-blocks 0 .. kend(J) - 1; epilogue scales by 2^(e_p - 14) * 2^(e_j) and
+// writes U_aug rows (global row of each position) for columns j < ncols_out.
+__global__ void __launch_bounds__(64 + 32 * OZ_GEPI, 1)
+    oz_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int nR, int nJ,
+                   int kbmax, int tri, const int* __restrict__ erow, const double* __restrict__ cscale,
+                   double* __restrict__ Uaug, int ld, int64_t n, int64_t chunk, int world, int rank, int64_t pos0,
+                   int64_t npos, int ncols_out) {
+  extern __shared__ uint8_t oz_raw[];
+  uint8_t* st = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(oz_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(st + OZ_STAGES * OZ_STAGE_BYTES);
+  uint64_t* empty = full + OZ_STAGES;
+  uint64_t* tfull = empty + OZ_STAGES;
+  uint64_t* tempty = tfull + 1;
+  uint32_t* tbase = reinterpret_cast<uint32_t*>(tempty + 1);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < OZ_STAGES; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    mbar_init(tfull, 1);
+    mbar_init(tempty, 32 * OZ_GEPI);
+    fence_mbar_init();
+  }
+  if (warp == 1) tc_alloc<512>(tbase);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tbase;
+  const int nunits = nR;  // unit = one row block, all its column tiles (largest first): A stays in L2 between tiles
+  auto kend = [&](int J) { return tri ? min(kbmax, 2 * J + 2) : kbmax; };
+
+  if (warp == 0) {
+    if (lane == 0) {
+      tma_prefetch_desc(&tmA);
+      tma_prefetch_desc(&tmB);
+      int64_t it = 0;
+      for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
+        const int R = u;
+        for (int J = nJ - 1; J >= 0; --J) {
+          for (int kb = 0; kb < kend(J); ++kb, ++it) {
+            const int s = (int)(it % OZ_STAGES);
+            if (it >= OZ_STAGES) mbar_wait(&empty[s], (uint32_t)(((it / OZ_STAGES) - 1) & 1));
+            uint8_t* a = st + s * OZ_STAGE_BYTES;
+            mbar_expect_tx(&full[s], OZ_STAGE_BYTES);
+            tma_load_4d(a, &tmA, 0, 0, 0, R * kbmax + kb, &full[s]);
+            tma_load_4d(a + OZ_A_BYTES, &tmB, 0, J * OZ_BN, 0, kb, &full[s]);
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    int64_t it = 0;
+    int tl = 0;
+    for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
+      for (int J = nJ - 1; J >= 0; --J) {
+        if (tl > 0) mbar_wait(tempty, (uint32_t)((tl - 1) & 1));
+        tc_fence_after();
+        const int ke = kend(J);
+        for (int kb = 0; kb < ke; ++kb, ++it) {
+          const int s = (int)(it % OZ_STAGES);
+          mbar_wait(&full[s], (uint32_t)((it / OZ_STAGES) & 1));
+          tc_fence_after();
+          if (lane == 0) {
+            oz_issue_stage(tmem, smem_u32(st + s * OZ_STAGE_BYTES), kb == 0);
+            tc_commit(&empty[s]);
+            if (kb + 1 == ke) tc_commit(tfull);
+          }
+          __syncwarp();
+        }
+        ++tl;
+      }
+    }
+  } else {
+    const int q = warp & 3;              // TMEM lane quarter (rows q*32 ..)
+    const int hh = (warp - 2) >> 2;      // column half of every tile this warp drains
+    const int row = q * 32 + lane;
+    double* stg = reinterpret_cast<double*>(reinterpret_cast<uint8_t*>(tbase) + 256) + (size_t)(warp - 2) * 32 * OZ_GLD;
+    int tl = 0;
+    for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
+      const int R = u;
+      const int64_t pos = (int64_t)R * OZ_BM + row;
+      int64_t i = n;
+      double rs = 0.0;
+      if (pos < npos) {
+        i = pos_to_row(pos0 + pos, chunk, world, rank);
+        rs = ldexp(1.0, erow[pos] - 14);
+      }
+      for (int J = nJ - 1; J >= 0; --J) {
+        mbar_wait(tfull, (uint32_t)(tl & 1));
+        tc_fence_after();
+        double t[2][16];
+        oz_drain16(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(hh * 32), t[0]);
+        oz_drain16(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(hh * 32 + 16), t[1]);
+        tc_fence_before();
+        mbar_arrive(tempty);  // TMEM read: the MMA warp may start the next tile
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+#pragma unroll
+          for (int j = 0; j < 16; ++j) stg[lane * OZ_GLD + j] = t[c][j] * rs;
+          __syncwarp();
+          // two rows per step: lanes 0-15 row r, 16-31 row r + 1, 16 consecutive columns (128 B) each
+          const int jc = J * OZ_BN + hh * 32 + c * 16 + (lane & 15);
+          const double cs = jc < ncols_out ? cscale[jc] : 0.0;
+#pragma unroll 4
+          for (int r = 0; r < 32; r += 2) {
+            const int rr = r + (lane >> 4);
+            const int64_t pr = (int64_t)R * OZ_BM + q * 32 + rr;
+            const int64_t ir = __shfl_sync(0xffffffffu, i, rr);
+            if (pr < npos && ir < n && jc < ncols_out) __stcs(Uaug + ir * (int64_t)ld + jc, stg[rr * OZ_GLD + (lane & 15)] * cs);
+          }
+          __syncwarp();
+        }
+        ++tl;
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 1) tc_free<512>(tmem);
 }
 
 // ------------------------------------------------------------------ host
@@ -374,6 +665,82 @@ cudaError_t launch_syrk_i8(const double* W, int64_t ldw, int64_t nrows, int ncol
     done += rows;
     ++chunk;
   } while (done < nrows);
+  return cudaSuccess;
+}
+
+// ------------------------------------------------------------------ K1 host
+bool ufeat_i8_supported(int d, int mk) { return (d == 2 || d == 3 || d == 5 || d == 10) && mk >= 8 && mk <= 4096; }
+
+static int64_t k1_nposp(int64_t rows) { return std::max<int64_t>(OZ_BM, (rows + OZ_BM - 1) / OZ_BM * OZ_BM); }
+static int k1_kb(int mk) { return (mk + OZ_BK - 1) / OZ_BK; }
+static int k1_nJ(int mk) { return (mk + OZ_BN - 1) / OZ_BN; }
+
+size_t ufeat_i8_ws_bytes(int mk, int64_t cap_rows) { return (size_t)OZ_S * k1_nposp(cap_rows) * k1_kb(mk) * OZ_BK; }
+
+size_t ufeat_i8_aux_bytes(int mk, int64_t cap_rows) {
+  const size_t lsl = (size_t)OZ_S * k1_nJ(mk) * OZ_BN * k1_kb(mk) * OZ_BK;  // Linv slices
+  return (lsl + 255) / 256 * 256 + (size_t)k1_nJ(mk) * OZ_BN * 8 + (size_t)k1_nposp(cap_rows) * 4 + 512;
+}
+
+cudaError_t launch_u_features_i8(const double* X, const double* Z, const double* y, int64_t n, int64_t pos0,
+                                 int64_t npos, int64_t chunk, int world, int rank, int m, int mk, const CovParams& p,
+                                 const double* Linv, double* Uaug, int ld, int8_t* ws, int64_t cap_rows, void* aux,
+                                 int sms, cudaStream_t s) {
+  if (!ufeat_i8_supported(p.d, mk) || cap_rows < 1) return cudaErrorInvalidValue;
+  if (npos <= 0) return cudaSuccess;
+  const int kb = k1_kb(mk), nJ = k1_nJ(mk), KP = kb * OZ_BK;
+  char* a = reinterpret_cast<char*>(aux);
+  int8_t* lsl = reinterpret_cast<int8_t*>(a);
+  const size_t lsl_b = ((size_t)OZ_S * nJ * OZ_BN * KP + 255) / 256 * 256;
+  double* cscale = reinterpret_cast<double*>(a + lsl_b);
+  int* erow = reinterpret_cast<int*>(a + lsl_b + (size_t)nJ * OZ_BN * 8);
+  // B: the rows of Linv (output columns j), once per call
+  oz_rows_slice_kernel<<<(nJ * OZ_BN + 7) / 8, 256, 0, s>>>(Linv, mk, mk, mk, nJ * OZ_BN, kb, lsl, cscale);
+  CUtensorMap tb;
+  cudaError_t e = make_tmap_i8_slices(&tb, lsl, (uint64_t)kb, (uint64_t)nJ * OZ_BN, OZ_S, OZ_BN);
+  if (e != cudaSuccess) return e;
+  e = smem_optin(oz_gemm_kernel, OZ_GEMM_SMEM);
+  if (e != cudaSuccess) return e;
+  const size_t kx_smem = (size_t)((KP + 127) / 128 * 128) * p.d * 8;
+  for (int64_t c0 = 0; c0 < npos; c0 += cap_rows) {
+    const int64_t rows = std::min<int64_t>(cap_rows, npos - c0);
+    const int64_t nposp = k1_nposp(rows);
+    int nb = (int)std::min<int64_t>((rows + 7) / 8, (int64_t)sms * 4);
+    auto go = [&](auto kern) -> cudaError_t {
+      cudaError_t e1 = smem_optin(kern, kx_smem);
+      if (e1 != cudaSuccess) return e1;
+      kern<<<nb, 256, kx_smem, s>>>(X, Z, y, n, rows, chunk, world, rank, pos0 + c0, m, mk, KP, p, ws, (int64_t)kb,
+                                    erow, Uaug, ld);
+      return cudaGetLastError();
+    };
+#define VIF_KXS(DV)                                                 \
+  switch (p.family) {                                               \
+    case FAM_M12: e = go(kx_slice_kernel<FAM_M12, DV>); break;      \
+    case FAM_M32: e = go(kx_slice_kernel<FAM_M32, DV>); break;      \
+    case FAM_M52: e = go(kx_slice_kernel<FAM_M52, DV>); break;      \
+    default: e = go(kx_slice_kernel<FAM_GAUSS, DV>); break;         \
+  }
+    if (p.d == 2) {
+      VIF_KXS(2)
+    } else if (p.d == 3) {
+      VIF_KXS(3)
+    } else if (p.d == 5) {
+      VIF_KXS(5)
+    } else {
+      VIF_KXS(10)
+    }
+#undef VIF_KXS
+    if (e != cudaSuccess) return e;
+    CUtensorMap ta;
+    e = make_tmap_i8_slices(&ta, ws, (uint64_t)kb * (nposp / OZ_BM), (uint64_t)OZ_BM, OZ_S, OZ_BM);
+    if (e != cudaSuccess) return e;
+    const int nR = (int)(nposp / OZ_BM);
+    const int units = nR;
+    oz_gemm_kernel<<<std::min(units, sms), 64 + 32 * OZ_GEPI, OZ_GEMM_SMEM, s>>>(ta, tb, nR, nJ, kb, 1, erow, cscale, Uaug, ld, n, chunk,
+                                                               world, rank, pos0 + c0, rows, mk);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
   return cudaSuccess;
 }
 

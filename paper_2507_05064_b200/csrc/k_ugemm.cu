@@ -15,10 +15,6 @@
 
 namespace vif {
 
-__device__ __forceinline__ int64_t pos_to_row(int64_t p, int64_t chunk, int world, int rank) {
-  return (p / chunk) * (int64_t)world * chunk + (int64_t)rank * chunk + p % chunk;
-}
-
 template <int FAM>
 __global__ void __launch_bounds__(256) kx_eval_kernel(const double* __restrict__ X, const double* __restrict__ Z,
                                                       const double* __restrict__ y, int64_t n, int64_t npos,

@@ -52,6 +52,15 @@ cudaError_t launch_finish(const double* G, int ld, int m, int ycol, const double
 cudaError_t launch_u_features(const double* X, const double* Z, const double* y, int64_t n, int64_t pos0,
                               int64_t npos, int64_t chunk, int world, int rank, int m, int mk, const CovParams& p,
                               const double* Linv, double* S, double* Uaug, int ld, cudaStream_t s, int lds = 0);
+// K1 on the integer tensor cores (k_ozaki.cu): S = K(X,Z) evaluated straight into int8 digit slices with a
+// per-row scale, Linv rows sliced per output column, tcgen05.mma.kind::i8 triangular GEMM; d in {2,3,5,10}
+bool ufeat_i8_supported(int d, int mk);
+size_t ufeat_i8_ws_bytes(int mk, int64_t cap_rows);
+size_t ufeat_i8_aux_bytes(int mk, int64_t cap_rows);
+cudaError_t launch_u_features_i8(const double* X, const double* Z, const double* y, int64_t n, int64_t pos0,
+                                 int64_t npos, int64_t chunk, int world, int rank, int m, int mk, const CovParams& p,
+                                 const double* Linv, double* Uaug, int ld, int8_t* ws, int64_t cap_rows, void* aux,
+                                 int sms, cudaStream_t s);
 // K2 + K3
 cudaError_t launch_vecchia(const VecchiaArgs& a, cudaStream_t s);
 // K4

@@ -87,13 +87,14 @@ struct Plan {
   int64_t rounds, chunk, npos, npad;
   int nsplit, nsplit_round;
   bool syrk_i8;    // K4 on the integer tensor cores (k_ozaki.cu); VIF_SYRK_FP64=1 keeps the DMMA SYRK
+  bool k1_i8;      // K1 on the integer tensor cores (k_ozaki.cu); VIF_UFEAT_FP64=1 keeps kx_eval + DMMA GEMM
   int64_t oz_cap;  // rows per digit-slice chunk
   std::vector<int64_t> n_own;
 };
 
 enum Buf {
   B_X, B_Z, B_NBR, B_Y, B_KM, B_LINV, B_U, B_W, B_DPOS, B_ORDER, B_KEYS, B_KEYS2, B_VALS, B_VALS2, B_TEMP,
-  B_GPART, B_G, B_GSUM, B_LINVM, B_TSCR, B_PART, B_BBOX, B_TERMS, B_STATUS, B_WS, B_OZAUX,
+  B_GPART, B_G, B_GSUM, B_LINVM, B_TSCR, B_PART, B_BBOX, B_TERMS, B_STATUS, B_WS, B_OZAUX, B_OZK1,
   // second input slot (vif_stage_data: inputs of the next evaluation copied while this one runs)
   B_X2, B_Z2, B_NBR2, B_Y2, B_ORDER2,
   // sort scratch of the staging path (its sort runs on the copy stream, beside the main stream's work)
@@ -168,6 +169,8 @@ bool make_plan(const vif_dims* dims, bool emulate, Plan& P, std::string& err) {
     const char* f = getenv("VIF_SYRK_FP64");
     P.syrk_i8 = syrk_i8_supported(P.ld) && !(f && f[0] == '1');
     P.oz_cap = std::min<int64_t>(std::max<int64_t>(P.npos, 1), (int64_t)1 << 20);
+    const char* fk = getenv("VIF_UFEAT_FP64");
+    P.k1_i8 = P.mk > 0 && ufeat_i8_supported(P.d, P.mk) && !(fk && fk[0] == '1');
   }
   return true;
 }
@@ -197,6 +200,10 @@ Layout make_layout(const Plan& P) {
     L.size[B_GPART] = std::max(L.size[B_GPART], syrk_i8_part_doubles(P.ld, P.oz_cap) * D8);
     L.size[B_WS] = syrk_i8_ws_bytes(P.ld, P.oz_cap);
     L.size[B_OZAUX] = syrk_i8_aux_bytes(P.ld);
+  }
+  if (P.k1_i8) {
+    L.size[B_WS] = std::max(L.size[B_WS], ufeat_i8_ws_bytes(P.mk, P.oz_cap));
+    L.size[B_OZK1] = ufeat_i8_aux_bytes(P.mk, P.oz_cap);
   }
   L.size[B_G] = nrep * gsz;
   L.size[B_GSUM] = gsz;
@@ -228,7 +235,7 @@ Layout make_layout(const Plan& P) {
 
 enum Stage { S_KM = 0, S_UFEAT, S_GATHER, S_VECCHIA, S_SYRK, S_REDUCE, S_CHOLM, S_FINISH, S_COUNT };
 const char* kStageNames[S_COUNT] = {
-    "K0 K_m + chol/inv (cooperative)", "K1 U features (kx_eval + gemm_tn)", "A2 U all-gather (NCCL)",
+    "K0 K_m + chol/inv (cooperative)", "K1 U features (int8 slices on tcgen05; kx_eval + DMMA gemm_tn with VIF_UFEAT_FP64=1)", "A2 U all-gather (NCCL)",
     "K2+K3 vecchia rows (gather + DMMA Gram + chol + W row)", "K4 syrk (int8 digit slices on tcgen05; DMMA with VIF_SYRK_FP64=1)",
     "A6/A7 sum log D + all-reduce", "K5 chol/inv of M (cooperative)", "K5 finish (z, quad, NLL)"};
 
@@ -1110,11 +1117,20 @@ int vif_factor(void* handle, const vif_theta* theta, double* B_out, double* D_ou
   for (int64_t r = 0; r < P.rounds; ++r) {
     for (int g = 0; g < nrep; ++g) {
       const int rank = P.emulate ? g : P.rank;
-      VIF_CUDA(h, launch_u_features(h->buf<double>(B_X), h->buf<double>(B_Z), h->buf<double>(B_Y), P.n, r * P.chunk,
-                                    P.chunk, P.chunk, P.world, rank, P.m, P.mk, p, h->buf<double>(B_LINV),
-                                    h->buf<double>(B_W), h->buf<double>(B_U), P.ld, s),
-               "U features");
-      nl += P.mk > 0 ? 2 : 1;
+      if (P.k1_i8) {
+        VIF_CUDA(h, launch_u_features_i8(h->buf<double>(B_X), h->buf<double>(B_Z), h->buf<double>(B_Y), P.n,
+                                         r * P.chunk, P.chunk, P.chunk, P.world, rank, P.m, P.mk, p,
+                                         h->buf<double>(B_LINV), h->buf<double>(B_U), P.ld, h->buf<int8_t>(B_WS),
+                                         P.oz_cap, h->buf<char>(B_OZK1), kPlanSMs, s),
+                 "U features (int8 slices)");
+        nl += 1 + 2 * (int)((P.chunk + P.oz_cap - 1) / P.oz_cap);
+      } else {
+        VIF_CUDA(h, launch_u_features(h->buf<double>(B_X), h->buf<double>(B_Z), h->buf<double>(B_Y), P.n,
+                                      r * P.chunk, P.chunk, P.chunk, P.world, rank, P.m, P.mk, p,
+                                      h->buf<double>(B_LINV), h->buf<double>(B_W), h->buf<double>(B_U), P.ld, s),
+                 "U features");
+        nl += P.mk > 0 ? 2 : 1;
+      }
     }
     if (nccl_path) {
       Nccl& N = nccl();

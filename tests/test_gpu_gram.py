@@ -70,23 +70,29 @@ def test_gram_engines_agree_on_factor_rows():
 
 @pytest.mark.parametrize("cid,n", [(1, None), (4, 20000)])
 def test_factor_engines_agree(monkeypatch, cid, n):
-    """vif_factor + vif_nll with the integer-slice K4 (default) and with the DMMA K4 (VIF_SYRK_FP64=1, read at
-    vif_create): the NLL terms agree to 1e-12 relative (config 4 recipe: m = 1000, ld = 1008)"""
+    """vif_factor + vif_nll with the integer-slice K1 and K4 (default) and with the DMMA K1 and K4
+    (VIF_UFEAT_FP64=1, VIF_SYRK_FP64=1, read at vif_create): U rows agree to 1e-12 (normwise: the oracle
+    parity bound of U; measured 1.1e-13 at config 4's m = 1000) and the NLL terms
+    to 1e-12 relative (config 4 recipe: d = 10, m = 1000, ld = 1008)"""
     import sys, os
     sys.path.insert(0, os.path.join(os.path.dirname(__file__), ".."))
     import vifgen
     w = vifgen.make_config(cid, device="cuda", n=n)
     th = p.Theta(**w.theta_dict())
     dev = torch.device("cuda")
-    res = {}
+    res, U = {}, {}
     for eng in ("int8", "fp64"):
-        if eng == "fp64":
-            monkeypatch.setenv("VIF_SYRK_FP64", "1")
-        else:
-            monkeypatch.delenv("VIF_SYRK_FP64", raising=False)
+        for var in ("VIF_SYRK_FP64", "VIF_UFEAT_FP64"):
+            if eng == "fp64":
+                monkeypatch.setenv(var, "1")
+            else:
+                monkeypatch.delenv(var, raising=False)
         m = p.VifModel(*(torch.from_numpy(np.ascontiguousarray(a)).to(dev) for a in (w.X, w.Z, w.nbr, w.y)))
         t = m.evaluate(th)
         res[eng] = (t.nll, t.logdet_D, t.logdet_M, t.quad)
+        U[eng] = m.U().cpu().numpy()
         m.close()
     for a, b in zip(res["int8"], res["fp64"]):
         assert abs(a - b) <= 1e-12 * max(abs(b), 1.0), (res,)
+    du = np.linalg.norm(U["int8"] - U["fp64"], axis=1) / np.maximum(np.linalg.norm(U["fp64"], axis=1), 1e-300)
+    assert du.max() <= 1e-12, du.max()

@@ -256,7 +256,8 @@ def test_large_m_emulated_sharding():
 def test_rounds_schedule_same_result():
     """The optional single-GPU round schedule (VIF_ROUNDS, three streams) gives the serial result:
     B and D bit-identical, NLL to 1e-12 and the gradient to 1e-10 (only the SYRK summation order
-    differs).  The knob is read
+    differs).  The round schedule keeps the FP64 DMMA K1 (kx_eval + gemm_tn), so both runs use it
+    (VIF_UFEAT_FP64=1) for the bit-identical comparison of B and D.  The knobs are read
     once per process, hence the subprocess."""
     import json
     import os
@@ -278,7 +279,7 @@ np.save(sys.argv[1], np.concatenate([B.cpu().numpy().ravel(), D.cpu().numpy(), [
     outs = []
     for R in ("1", "4"):
         path = f"/tmp/vif_rounds_{R}.npy"
-        env = dict(os.environ, VIF_ROUNDS=R)
+        env = dict(os.environ, VIF_ROUNDS=R, VIF_UFEAT_FP64="1")
         subprocess.run([sys.executable, "-c", code, path], env=env, check=True)
         outs.append(np.load(path))
     a, b = outs
