@@ -200,7 +200,7 @@ __device__ __forceinline__ void oz_drain32(uint32_t ta, double (&t)[32]) {
 
 __global__ void __launch_bounds__(192, 1)
     oz_syrk_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int nunits,
-                   int ntiles, int nJ, int64_t rps, int64_t nrp, double* __restrict__ Gpart) {
+                   int ntiles, int nJ, int fullgrid, int64_t rps, int64_t nrp, double* __restrict__ Gpart) {
   extern __shared__ uint8_t oz_raw[];
   uint8_t* st = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(oz_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(st + OZ_STAGES * OZ_STAGE_BYTES);
@@ -231,7 +231,12 @@ __global__ void __launch_bounds__(192, 1)
       int64_t it = 0;
       for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
         int I, J;
-        oz_tile(u % ntiles, nJ, I, J);
+        if (fullgrid) {
+          I = (u % ntiles) / nJ;
+          J = (u % ntiles) % nJ;
+        } else {
+          oz_tile(u % ntiles, nJ, I, J);
+        }
         const int64_t k0 = (int64_t)(u / ntiles) * rps, k1 = min(nrp, k0 + rps);
         for (int64_t k = k0; k < k1; k += OZ_BK, ++it) {
           const int s = (int)(it % OZ_STAGES);
@@ -287,24 +292,31 @@ __global__ void __launch_bounds__(192, 1)
   if (warp == 1) tc_free<512>(tmem);
 }
 
-__global__ void oz_reduce_kernel(const double* __restrict__ Gpart, int ntiles, int nsplit, int nJ, int ncols,
-                                 const unsigned long long* __restrict__ cmax, const int* __restrict__ flag,
+// G[a][b] (a < M, b < N) = 2^(e_a + e_b - 14) sum over the row splits (fixed order); full: every tile of the
+// nI x nJ grid (C = A^T B), else the lower tiles of the SYRK (oz_tile)
+__global__ void oz_reduce_kernel(const double* __restrict__ Gpart, int ntiles, int nsplit, int nJ, int full, int M,
+                                 int N, const unsigned long long* __restrict__ cmaxA,
+                                 const unsigned long long* __restrict__ cmaxB, const int* __restrict__ flag,
                                  double* __restrict__ G, int64_t ldg, int accumulate) {
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= (int64_t)ntiles * OZ_BM * OZ_BN) return;
   const int t = (int)(e / (OZ_BM * OZ_BN));
   const int i = (int)((e / OZ_BN) % OZ_BM), j = (int)(e % OZ_BN);
   int I, J;
-  oz_tile(t, nJ, I, J);
+  if (full) {
+    I = t / nJ;
+    J = t % nJ;
+  } else {
+    oz_tile(t, nJ, I, J);
+  }
   const int a = I * OZ_BM + i, b = J * OZ_BN + j;
-  if (a >= ncols || b >= ncols) return;
+  if (a >= M || b >= N) return;
   double s = 0.0;
   for (int sp = 0; sp < nsplit; ++sp) s += Gpart[(((size_t)sp * ntiles + t) * OZ_BM + i) * OZ_BN + j];
-  double v = ldexp(s, oz_exp(cmax[a]) + oz_exp(cmax[b]) - 14);
+  double v = ldexp(s, oz_exp(cmaxA[a]) + oz_exp(cmaxB[b]) - 14);
   if (*flag) v = __longlong_as_double(0x7ff8000000000000LL);
   G[(size_t)a * ldg + b] = accumulate ? G[(size_t)a * ldg + b] + v : v;
 }
-
 
 // ================================================================== K1 on the integer tensor cores
 // U_aug[i][j] = sum_{k <= j} S[p][k] Linv[j][k] (reading c4), S = K(X, Z) with i = row(p):
@@ -405,6 +417,57 @@ __global__ void __launch_bounds__(256) kx_slice_kernel(const double* __restrict_
   }
 }
 
+
+// rows of a general row-major matrix A (M x K, lda) -> digit slices with a per-row scale, in the row-block-major
+// layout of the K1 GEMM ([R][kb][q][128 rows][32 B], R = row / 128) and e_r in erow (INT_MAX: the row holds a
+// non-finite value -- the GEMM then writes NaN for it); one warp per row, two passes over the row (the second
+// from L1/L2): the maximum, then four consecutive columns per lane packed into one 4-byte store per slice
+__global__ void __launch_bounds__(256) oz_rowslice_kernel(const double* __restrict__ A, int64_t lda, int64_t M,
+                                                          int K, int KP, int8_t* __restrict__ out,
+                                                          int* __restrict__ erow) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int kbA = KP / OZ_BK;
+  for (int64_t r = (int64_t)blockIdx.x * 8 + warp; r < M; r += (int64_t)gridDim.x * 8) {
+    const double* a = A + r * lda;
+    double mx = 0.0;
+    bool bad = false;
+    for (int b = lane; b < K; b += 32) {
+      const double v = a[b];
+      bad |= !isfinite(v);
+      mx = fmax(mx, fabs(v));
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    bad = __any_sync(0xffffffffu, bad);
+    const int er = oz_exp((unsigned long long)__double_as_longlong(mx));
+    if (lane == 0) erow[r] = bad ? 0x7fffffff : er;
+    const double scl = bad ? 0.0 : ldexp(1.0, 55 - er);
+    for (int b0 = 4 * lane; b0 < KP; b0 += 128) {
+      uint32_t lo[4], hi[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const double v = b0 + j < K ? a[b0 + j] : 0.0;
+        const long long Y = __double2ll_rn(v * scl) + 0x808080808080LL;
+        lo[j] = (uint32_t)Y;
+        hi[j] = (uint32_t)((unsigned long long)Y >> 32);
+      }
+      int8_t* dst = out + ((((r >> 7) * kbA + (b0 >> 5)) * OZ_S) * OZ_BM + (r & 127)) * OZ_BK + (b0 & 31);
+#pragma unroll
+      for (int q = 1; q < OZ_S; ++q) {
+        const int j = 6 - q;
+        const uint32_t* src = j < 4 ? lo : hi;
+        const uint32_t sel = (uint32_t)((j & 3) | (((j & 3) + 4) << 4));
+        const uint32_t xx = __byte_perm(src[0], src[1], sel), yy = __byte_perm(src[2], src[3], sel);
+        *reinterpret_cast<uint32_t*>(dst + q * OZ_BM * OZ_BK) = __byte_perm(xx, yy, 0x5410) ^ 0x80808080u;
+      }
+      {
+        const uint32_t xx = __byte_perm(hi[0], hi[1], 0x62), yy = __byte_perm(hi[2], hi[3], 0x62);
+        *reinterpret_cast<uint32_t*>(dst) = __byte_perm(xx, yy, 0x5410);
+      }
+    }
+  }
+}
+
 // rows of a small row-major matrix A (nrows x ncols, lda) -> digit slices out[kb][q][r][k mod 32] for
 // r < nrows_p, k < 32 nkb (zeros outside A), with the per-row scale 2^e_r in rscale[r]; one warp per row
 __global__ void __launch_bounds__(256) oz_rows_slice_kernel(const double* __restrict__ A, int64_t lda, int nrows,
@@ -415,13 +478,19 @@ __global__ void __launch_bounds__(256) oz_rows_slice_kernel(const double* __rest
   if (r >= nrows_p) return;
   const int KP = nkb * OZ_BK;
   double mx = 0.0;
+  bool bad = false;
   for (int b = lane; b < KP; b += 32)
-    if (r < nrows && b < ncols) mx = fmax(mx, fabs(A[(int64_t)r * lda + b]));
+    if (r < nrows && b < ncols) {
+      const double v = A[(int64_t)r * lda + b];
+      bad |= !isfinite(v);
+      mx = fmax(mx, fabs(v));
+    }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  bad = __any_sync(0xffffffffu, bad);
   const int er = oz_exp((unsigned long long)__double_as_longlong(mx));
-  if (lane == 0) rscale[r] = ldexp(1.0, er);
-  const double scl = ldexp(1.0, 55 - er);
+  if (lane == 0) rscale[r] = bad ? __longlong_as_double(0x7ff8000000000000LL) : ldexp(1.0, er);
+  const double scl = bad ? 0.0 : ldexp(1.0, 55 - er);
   for (int b = lane; b < KP; b += 32) {
     const double v = (r < nrows && b < ncols) ? A[(int64_t)r * lda + b] : 0.0;
     long long X = __double2ll_rn(v * scl);
@@ -540,7 +609,8 @@ __global__ void __launch_bounds__(64 + 32 * OZ_GEPI, 1)
       double rs = 0.0;
       if (pos < npos) {
         i = pos_to_row(pos0 + pos, chunk, world, rank);
-        rs = ldexp(1.0, erow[pos] - 14);
+        const int er = erow[pos];
+        rs = er == 0x7fffffff ? __longlong_as_double(0x7ff8000000000000LL) : ldexp(1.0, er - 14);
       }
       for (int J = nJ - 1; J >= 0; --J) {
         mbar_wait(tfull, (uint32_t)(tl & 1));
@@ -584,11 +654,11 @@ struct OzPlan {
   int64_t ncp, nrp, rps;
 };
 
-OzPlan oz_plan(int ncols, int64_t nrows, int sms) {
+OzPlan oz_plan(int ncols, int64_t nrows, int sms, int ncolsB = 0) {
   OzPlan P{};
   P.nI = (ncols + OZ_BM - 1) / OZ_BM;
-  P.nJ = (ncols + OZ_BN - 1) / OZ_BN;
-  P.ntiles = oz_ntiles(P.nI, P.nJ);
+  P.nJ = ((ncolsB > 0 ? ncolsB : ncols) + OZ_BN - 1) / OZ_BN;
+  P.ntiles = ncolsB > 0 ? P.nI * P.nJ : oz_ntiles(P.nI, P.nJ);
   P.ncp = (int64_t)P.nI * OZ_BM;
   P.nrp = std::max<int64_t>(OZ_TROWS, (nrows + OZ_TROWS - 1) / OZ_TROWS * OZ_TROWS);
   // row splits of <= OZ_CHUNK rows (multiples of OZ_BK); among 1-2x the minimum count, the smallest makespan
@@ -656,10 +726,10 @@ cudaError_t launch_syrk_i8(const double* W, int64_t ldw, int64_t nrows, int ncol
     e = make_tmap_i8_slices(&tb, ws, (uint64_t)(P.nrp / OZ_BK), (uint64_t)P.ncp, OZ_S, OZ_BN);
     if (e != cudaSuccess) return e;
     const int units = P.nsplit * P.ntiles;
-    oz_syrk_kernel<<<std::min(units, sms), 192, OZ_SMEM, s>>>(ta, tb, units, P.ntiles, P.nJ, P.rps, P.nrp, Gpart);
+    oz_syrk_kernel<<<std::min(units, sms), 192, OZ_SMEM, s>>>(ta, tb, units, P.ntiles, P.nJ, 0, P.rps, P.nrp, Gpart);
     const int64_t tot = (int64_t)P.ntiles * OZ_BM * OZ_BN;
-    oz_reduce_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(Gpart, P.ntiles, P.nsplit, P.nJ, ncols, cmax, flag,
-                                                                   G, ldg, chunk > 0);
+    oz_reduce_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(Gpart, P.ntiles, P.nsplit, P.nJ, 0, ncols, ncols,
+                                                                   cmax, cmax, flag, G, ldg, chunk > 0);
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     done += rows;
@@ -741,6 +811,119 @@ cudaError_t launch_u_features_i8(const double* X, const double* Z, const double*
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
   }
+  return cudaSuccess;
+}
+
+
+// ------------------------------------------------------------------ general C = A B^T on the integer tensor cores
+size_t gemm_i8_ws_bytes(int K, int64_t cap_rows) { return (size_t)OZ_S * k1_nposp(cap_rows) * k1_kb(K) * OZ_BK; }
+
+size_t gemm_i8_aux_bytes(int N, int K, int64_t cap_rows) { return ufeat_i8_aux_bytes(std::max(N, K), cap_rows); }
+
+cudaError_t launch_gemm_tn_i8(const double* A, int64_t lda, int64_t M, const double* B, int64_t ldb, int N, int K,
+                              int tri, double* C, int64_t ldc, int8_t* ws, int64_t cap_rows, void* aux, int sms,
+                              cudaStream_t s) {
+  if (N < 1 || K < 1 || N > 4096 || K > 4096 || cap_rows < 1) return cudaErrorInvalidValue;
+  if (M <= 0) return cudaSuccess;
+  const int kb = k1_kb(K), nJ = k1_nJ(N), KP = kb * OZ_BK;
+  char* a = reinterpret_cast<char*>(aux);
+  int8_t* bsl = reinterpret_cast<int8_t*>(a);
+  const size_t bsl_b = ((size_t)OZ_S * nJ * OZ_BN * KP + 255) / 256 * 256;
+  double* cscale = reinterpret_cast<double*>(a + bsl_b);
+  int* erow = reinterpret_cast<int*>(a + bsl_b + (size_t)nJ * OZ_BN * 8);
+  oz_rows_slice_kernel<<<(nJ * OZ_BN + 7) / 8, 256, 0, s>>>(B, ldb, N, K, nJ * OZ_BN, kb, bsl, cscale);
+  CUtensorMap tb;
+  cudaError_t e = make_tmap_i8_slices(&tb, bsl, (uint64_t)kb, (uint64_t)nJ * OZ_BN, OZ_S, OZ_BN);
+  if (e != cudaSuccess) return e;
+  e = smem_optin(oz_gemm_kernel, OZ_GEMM_SMEM);
+  if (e != cudaSuccess) return e;
+  for (int64_t c0 = 0; c0 < M; c0 += cap_rows) {
+    const int64_t rows = std::min<int64_t>(cap_rows, M - c0);
+    const int64_t nposp = k1_nposp(rows);
+    const int nb = (int)std::min<int64_t>((rows + 7) / 8, (int64_t)sms * 8);
+    oz_rowslice_kernel<<<nb, 256, 0, s>>>(A + c0 * lda, lda, rows, K, KP, ws, erow);
+    CUtensorMap ta;
+    e = make_tmap_i8_slices(&ta, ws, (uint64_t)kb * (nposp / OZ_BM), (uint64_t)OZ_BM, OZ_S, OZ_BM);
+    if (e != cudaSuccess) return e;
+    const int nR = (int)(nposp / OZ_BM);
+    // identity row map: pos_to_row(p, chunk = rows, world = 1, rank = 0) = p
+    oz_gemm_kernel<<<std::min(nR, sms), 64 + 32 * OZ_GEPI, OZ_GEMM_SMEM, s>>>(
+        ta, tb, nR, nJ, kb, tri, erow, cscale, C + c0 * ldc, (int)ldc, rows, rows, 1, 0, 0, rows, N);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
+// ------------------------------------------------------------------ C = A^T B over rows on the integer tensor cores
+// A: nrows x M (lda), B: nrows x N (ldb); C (M x N, ldc).  Per-column scales of A and B (global over the rows),
+// digit slices of both in ws (rows in chunks so that both fit), the SYRK kernel over every (128 x 64) tile,
+// reduction with the two exponent sets.
+size_t gemm_tt_i8_aux_bytes(int M, int N) {
+  return (size_t)((M + 127) / 128 * 128 + (N + 127) / 128 * 128) * 8 + 256;
+}
+
+size_t gemm_tt_i8_part_doubles(int M, int N, int64_t chunk_rows) {
+  const OzPlan P = oz_plan(M, chunk_rows, 148, N);
+  const int64_t smin = (P.nrp + OZ_CHUNK - 1) / OZ_CHUNK;
+  return (size_t)(2 * smin) * P.ntiles * OZ_BM * OZ_BN;
+}
+
+// rows per chunk so that the slices of A and B fit ws_bytes
+int64_t gemm_tt_i8_chunk(int M, int N, size_t ws_bytes) {
+  const int64_t ncpA = (M + 127) / 128 * 128, ncpB = (N + 127) / 128 * 128;
+  int64_t c = (int64_t)(ws_bytes / ((size_t)OZ_S * (ncpA + ncpB)));
+  c = c / OZ_TROWS * OZ_TROWS;
+  return c;
+}
+
+cudaError_t launch_gemm_tt_i8(const double* A, int64_t lda, int M, const double* B, int64_t ldb, int N, int64_t nrows,
+                              double* C, int64_t ldc, int8_t* ws, size_t ws_bytes, double* Gpart, void* aux, int sms,
+                              cudaStream_t s) {
+  if (M < 1 || N < 1 || M > 4096 || N > 4096 || (lda & 1) || (ldb & 1) ||
+      (reinterpret_cast<uintptr_t>(A) & 15) || (reinterpret_cast<uintptr_t>(B) & 15))
+    return cudaErrorInvalidValue;
+  const int64_t crows = gemm_tt_i8_chunk(M, N, ws_bytes);
+  if (crows < OZ_TROWS) return cudaErrorInvalidValue;
+  const int ncpA = (M + 127) / 128 * 128, ncpB = (N + 127) / 128 * 128;
+  unsigned long long* cmaxA = reinterpret_cast<unsigned long long*>(aux);
+  unsigned long long* cmaxB = cmaxA + ncpA;
+  int* flag = reinterpret_cast<int*>(cmaxB + ncpB);
+  cudaError_t e = cudaMemsetAsync(aux, 0, gemm_tt_i8_aux_bytes(M, N), s);
+  if (e != cudaSuccess) return e;
+  if (nrows > 0) {
+    const int ctas = 4 * sms;
+    const int64_t rpc = (nrows + ctas - 1) / ctas;
+    oz_colmax_kernel<<<(unsigned)((nrows + rpc - 1) / rpc), 256, 0, s>>>(A, lda, nrows, M, rpc, cmaxA);
+    oz_colmax_kernel<<<(unsigned)((nrows + rpc - 1) / rpc), 256, 0, s>>>(B, ldb, nrows, N, rpc, cmaxB);
+  }
+  e = smem_optin(oz_syrk_kernel, OZ_SMEM);
+  if (e != cudaSuccess) return e;
+  int64_t done = 0;
+  int chunk = 0;
+  do {
+    const int64_t rows = std::min<int64_t>(crows, nrows - done);
+    const OzPlan P = oz_plan(M, rows, sms, N);
+    int8_t* wsB = ws + (size_t)OZ_S * ncpA * P.nrp;
+    oz_slice_kernel<<<dim3((unsigned)(P.nrp / OZ_TROWS), (unsigned)(ncpA / 64)), 256, 0, s>>>(
+        A + (size_t)done * lda, lda, rows, M, cmaxA, ws, ncpA, flag);
+    oz_slice_kernel<<<dim3((unsigned)(P.nrp / OZ_TROWS), (unsigned)(ncpB / 64)), 256, 0, s>>>(
+        B + (size_t)done * ldb, ldb, rows, N, cmaxB, wsB, ncpB, flag);
+    CUtensorMap ta, tb;
+    e = make_tmap_i8_slices(&ta, ws, (uint64_t)(P.nrp / OZ_BK), (uint64_t)ncpA, OZ_S, OZ_BM);
+    if (e != cudaSuccess) return e;
+    e = make_tmap_i8_slices(&tb, wsB, (uint64_t)(P.nrp / OZ_BK), (uint64_t)ncpB, OZ_S, OZ_BN);
+    if (e != cudaSuccess) return e;
+    const int units = P.nsplit * P.ntiles;
+    oz_syrk_kernel<<<std::min(units, sms), 192, OZ_SMEM, s>>>(ta, tb, units, P.ntiles, P.nJ, 1, P.rps, P.nrp, Gpart);
+    const int64_t tot = (int64_t)P.ntiles * OZ_BM * OZ_BN;
+    oz_reduce_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(Gpart, P.ntiles, P.nsplit, P.nJ, 1, M, N, cmaxA,
+                                                                   cmaxB, flag, C, ldc, chunk > 0);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    done += rows;
+    ++chunk;
+  } while (done < nrows);
   return cudaSuccess;
 }
 

@@ -61,6 +61,21 @@ cudaError_t launch_u_features_i8(const double* X, const double* Z, const double*
                                  int64_t npos, int64_t chunk, int world, int rank, int m, int mk, const CovParams& p,
                                  const double* Linv, double* Uaug, int ld, int8_t* ws, int64_t cap_rows, void* aux,
                                  int sms, cudaStream_t s);
+// C (M x N, ldc) = A B^T, A: M x K (lda), B: N x K (ldb; lower triangular when tri: B[j][k] = 0 for k > j),
+// on the integer tensor cores (int8 digit slices, per-row scales); rows in chunks of <= cap_rows
+size_t gemm_i8_ws_bytes(int K, int64_t cap_rows);
+size_t gemm_i8_aux_bytes(int N, int K, int64_t cap_rows);
+cudaError_t launch_gemm_tn_i8(const double* A, int64_t lda, int64_t M, const double* B, int64_t ldb, int N, int K,
+                              int tri, double* C, int64_t ldc, int8_t* ws, int64_t cap_rows, void* aux, int sms,
+                              cudaStream_t s);
+// C (M x N, ldc) = A^T B over nrows rows (A: lda, B: ldb) on the integer tensor cores; rows in chunks whose
+// slices of A and B fit ws_bytes; Gpart: gemm_tt_i8_part_doubles(M, N, gemm_tt_i8_chunk(M, N, ws_bytes))
+size_t gemm_tt_i8_aux_bytes(int M, int N);
+size_t gemm_tt_i8_part_doubles(int M, int N, int64_t chunk_rows);
+int64_t gemm_tt_i8_chunk(int M, int N, size_t ws_bytes);
+cudaError_t launch_gemm_tt_i8(const double* A, int64_t lda, int M, const double* B, int64_t ldb, int N, int64_t nrows,
+                              double* C, int64_t ldc, int8_t* ws, size_t ws_bytes, double* Gpart, void* aux, int sms,
+                              cudaStream_t s);
 // K2 + K3
 cudaError_t launch_vecchia(const VecchiaArgs& a, cudaStream_t s);
 // K4

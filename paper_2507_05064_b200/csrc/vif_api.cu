@@ -88,6 +88,7 @@ struct Plan {
   int nsplit, nsplit_round;
   bool syrk_i8;    // K4 on the integer tensor cores (k_ozaki.cu); VIF_SYRK_FP64=1 keeps the DMMA SYRK
   bool k1_i8;      // K1 on the integer tensor cores (k_ozaki.cu); VIF_UFEAT_FP64=1 keeps kx_eval + DMMA GEMM
+  bool grad_i8;    // the gradient's n x m^2 GEMMs (Gamma, T) likewise; VIF_GRAD_FP64=1 keeps the DMMA GEMMs
   int64_t oz_cap;  // rows per digit-slice chunk
   std::vector<int64_t> n_own;
 };
@@ -171,6 +172,8 @@ bool make_plan(const vif_dims* dims, bool emulate, Plan& P, std::string& err) {
     P.oz_cap = std::min<int64_t>(std::max<int64_t>(P.npos, 1), (int64_t)1 << 20);
     const char* fk = getenv("VIF_UFEAT_FP64");
     P.k1_i8 = P.mk > 0 && ufeat_i8_supported(P.d, P.mk) && !(fk && fk[0] == '1');
+    const char* fg = getenv("VIF_GRAD_FP64");
+    P.grad_i8 = P.mk > 0 && P.ld <= 4096 && !(fg && fg[0] == '1');
   }
   return true;
 }
@@ -204,6 +207,13 @@ Layout make_layout(const Plan& P) {
   if (P.k1_i8) {
     L.size[B_WS] = std::max(L.size[B_WS], ufeat_i8_ws_bytes(P.mk, P.oz_cap));
     L.size[B_OZK1] = ufeat_i8_aux_bytes(P.mk, P.oz_cap);
+  }
+  if (P.grad_i8) {
+    L.size[B_WS] = std::max(L.size[B_WS], gemm_i8_ws_bytes(P.ld, P.oz_cap));
+    // G2 = R^T U slices both operands (mk columns each) per row chunk: at least half the chunk of the others
+    const int64_t ncp = (P.mk + 127) / 128 * 128, rows = std::min<int64_t>(P.n, P.oz_cap / 2 + 64);
+    L.size[B_WS] = std::max(L.size[B_WS], (size_t)7 * 2 * ncp * (size_t)((rows + 63) / 64 * 64));
+    L.size[B_OZK1] = std::max(L.size[B_OZK1], gemm_i8_aux_bytes(P.ld, P.ld, P.oz_cap));
   }
   L.size[B_G] = nrep * gsz;
   L.size[B_GSUM] = gsz;
@@ -475,6 +485,11 @@ Layout make_grad_layout(const Plan& P) {
   L.size[G_CPTR] = (size_t)(P.n + 1) * sizeof(int);
   L.size[G_CENT] = (size_t)2 * P.n * (P.mv + 1) * sizeof(int);  // sorted entries + the unsorted fill
   L.size[G_TSP] = gemm_tt_part_doubles((int)mk1, (int)mk1, gemm_tt_nsplit((int)mk1, (int)mk1, P.n, kPlanSMs)) * D8;
+  if (P.grad_i8) {
+    const size_t ws = make_layout(P).size[B_WS];
+    L.size[G_TSP] = std::max(L.size[G_TSP], gemm_tt_i8_part_doubles((int)mk1, (int)mk1,
+                                                                    gemm_tt_i8_chunk((int)mk1, (int)mk1, ws)) * D8);
+  }
   L.size[G_TDKP] = (size_t)gTdK_blocks() * (P.d + 1) * D8;
   L.size[G_TDK] = (size_t)(P.d + 2) * D8;  // + the R gather's row counter
   size_t off = 0;
@@ -1357,7 +1372,12 @@ int vif_grad(void* handle, const vif_theta* theta, void* gws, size_t gws_bytes, 
   for (int g = 0; g < nrep; ++g) {
     const int rank = P.emulate ? g : P.rank;
     double* W = h->buf<double>(B_W) + (size_t)g * P.npos * ld;
-    VIF_CUDA(h, launch_gemm_tn(W, ld, P.npos, gbuf(G_Q2), ld, ld, ld, 0, gbuf(G_GAM), ld, 1.0, 0, s), "Gamma");
+    if (P.grad_i8)
+      VIF_CUDA(h, launch_gemm_tn_i8(W, ld, P.npos, gbuf(G_Q2), ld, ld, ld, 0, gbuf(G_GAM), ld, h->buf<int8_t>(B_WS),
+                                    P.oz_cap, h->buf<char>(B_OZK1), kPlanSMs, s),
+               "Gamma (int8 slices)");
+    else
+      VIF_CUDA(h, launch_gemm_tn(W, ld, P.npos, gbuf(G_Q2), ld, ld, ld, 0, gbuf(G_GAM), ld, 1.0, 0, s), "Gamma");
     GradPointArgs a;
     a.U = U;
     a.dU = nullptr;
@@ -1397,10 +1417,20 @@ int vif_grad(void* handle, const vif_theta* theta, void* gws, size_t gws_bytes, 
                "R");
       // R has reversed columns, so T = R L_m^{-1} is a triangular product (T with reversed columns)
       if (g == 0) VIF_CUDA(h, launch_grev_linv(Linv, mk, gbuf(G_LINVT), s), "reversed L_m^-1");
-      VIF_CUDA(h, launch_gemm_tn(R, mk, P.n, gbuf(G_LINVT), mk, mk, mk, 1, gbuf(G_T), mk, 1.0, 0, s), "T = R L^-1");
-      VIF_CUDA(h, launch_gemm_tt(R, mk, mk, U, ld, mk, P.n, gemm_tt_nsplit(mk, mk, P.n, kPlanSMs), gbuf(G_TSP),
-                                 gbuf(G_G2), mk, s),
-               "G2 = R^T U");
+      if (P.grad_i8)
+        VIF_CUDA(h, launch_gemm_tn_i8(R, mk, P.n, gbuf(G_LINVT), mk, mk, mk, 1, gbuf(G_T), mk, h->buf<int8_t>(B_WS),
+                                      P.oz_cap, h->buf<char>(B_OZK1), kPlanSMs, s),
+                 "T = R L^-1 (int8 slices)");
+      else
+        VIF_CUDA(h, launch_gemm_tn(R, mk, P.n, gbuf(G_LINVT), mk, mk, mk, 1, gbuf(G_T), mk, 1.0, 0, s), "T = R L^-1");
+      if (P.grad_i8)
+        VIF_CUDA(h, launch_gemm_tt_i8(R, mk, mk, U, ld, mk, P.n, gbuf(G_G2), mk, h->buf<int8_t>(B_WS), h->L.size[B_WS],
+                                      gbuf(G_TSP), h->buf<char>(B_OZK1), kPlanSMs, s),
+                 "G2 = R^T U (int8 slices)");
+      else
+        VIF_CUDA(h, launch_gemm_tt(R, mk, mk, U, ld, mk, P.n, gemm_tt_nsplit(mk, mk, P.n, kPlanSMs), gbuf(G_TSP),
+                                   gbuf(G_G2), mk, s),
+                 "G2 = R^T U");
       VIF_CUDA(h, launch_gTdK(h->buf<double>(B_X), h->buf<double>(B_Z), P.n, m, mk, p, gbuf(G_T), gbuf(G_TDKP),
                               gbuf(G_TDK), s),
                "<T, dK>");

@@ -70,8 +70,8 @@ def test_gram_engines_agree_on_factor_rows():
 
 @pytest.mark.parametrize("cid,n", [(1, None), (4, 20000)])
 def test_factor_engines_agree(monkeypatch, cid, n):
-    """vif_factor + vif_nll with the integer-slice K1 and K4 (default) and with the DMMA K1 and K4
-    (VIF_UFEAT_FP64=1, VIF_SYRK_FP64=1, read at vif_create): U rows agree to 1e-12 (normwise: the oracle
+    """vif_factor + vif_nll + vif_grad with the integer-slice contractions (default) and with the DMMA ones
+    (VIF_UFEAT_FP64=1, VIF_SYRK_FP64=1, VIF_GRAD_FP64=1, read at vif_create): U rows agree to 1e-12 (normwise: the oracle
     parity bound of U; measured 1.1e-13 at config 4's m = 1000) and the NLL terms
     to 1e-12 relative (config 4 recipe: d = 10, m = 1000, ld = 1008)"""
     import sys, os
@@ -80,9 +80,9 @@ def test_factor_engines_agree(monkeypatch, cid, n):
     w = vifgen.make_config(cid, device="cuda", n=n)
     th = p.Theta(**w.theta_dict())
     dev = torch.device("cuda")
-    res, U = {}, {}
+    res, U, G = {}, {}, {}
     for eng in ("int8", "fp64"):
-        for var in ("VIF_SYRK_FP64", "VIF_UFEAT_FP64"):
+        for var in ("VIF_SYRK_FP64", "VIF_UFEAT_FP64", "VIF_GRAD_FP64"):
             if eng == "fp64":
                 monkeypatch.setenv(var, "1")
             else:
@@ -91,8 +91,11 @@ def test_factor_engines_agree(monkeypatch, cid, n):
         t = m.evaluate(th)
         res[eng] = (t.nll, t.logdet_D, t.logdet_M, t.quad)
         U[eng] = m.U().cpu().numpy()
+        G[eng] = np.asarray(m.grad(th)[1])
         m.close()
     for a, b in zip(res["int8"], res["fp64"]):
         assert abs(a - b) <= 1e-12 * max(abs(b), 1.0), (res,)
     du = np.linalg.norm(U["int8"] - U["fp64"], axis=1) / np.maximum(np.linalg.norm(U["fp64"], axis=1), 1e-300)
     assert du.max() <= 1e-12, du.max()
+    # the gradient (its Gamma, T and G2 contractions on the integer engines too) to 1e-9 of the largest component
+    np.testing.assert_allclose(G["int8"], G["fp64"], rtol=0, atol=1e-9 * np.abs(G["fp64"]).max())
