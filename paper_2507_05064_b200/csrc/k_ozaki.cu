@@ -148,14 +148,19 @@ __global__ void __launch_bounds__(256) oz_slice_kernel(const double* __restrict_
   }
   if (bad) atomicOr(flag, 1);
   __syncthreads();
-  // out: for each k-block kb of the tile and slice p, columns c0..c0+63 are 2 KB contiguous (32 B each)
+  // out: for each k-block kb of the tile and slice p, columns c0..c0+63 are 2 KB contiguous (32 B each);
+  // 16-byte stores (half h of a column's 32 bytes), a warp instruction writes 512 contiguous bytes
   constexpr int NKB = OZ_TROWS / OZ_BK;
-  for (int e = threadIdx.x; e < NKB * OZ_S * 64 * (OZ_BK / 4); e += blockDim.x) {
-    const int w = e % (OZ_BK / 4), cl = (e / (OZ_BK / 4)) % 64;
-    const int p = (e / (OZ_BK / 4 * 64)) % OZ_S, kb = e / (OZ_BK / 4 * 64 * OZ_S);
+  static_assert(NKB * OZ_S * 64 * 2 % 256 == 0, "whole iterations");
+#pragma unroll
+  for (int it = 0; it < NKB * OZ_S * 64 * 2 / 256; ++it) {
+    const int e = it * 256 + threadIdx.x;
+    const int h = e & 1, cl = (e >> 1) & 63, pk = e >> 7;
+    const int p = pk % OZ_S, kb = pk / OZ_S;
     const int64_t kbg = blockIdx.x * NKB + kb;
-    *reinterpret_cast<uint32_t*>(Ws + (((kbg * OZ_S + p) * ncp + c0 + cl) * OZ_BK) + 4 * w) =
-        T[p][cl][kb * (OZ_BK / 4) + w];
+    const uint32_t* tw = &T[p][cl][kb * (OZ_BK / 4) + 4 * h];
+    *reinterpret_cast<uint4*>(Ws + (((kbg * OZ_S + p) * ncp + c0 + cl) * OZ_BK) + 16 * h) =
+        make_uint4(tw[0], tw[1], tw[2], tw[3]);
   }
 }
 
@@ -448,6 +453,73 @@ __global__ void __launch_bounds__(256) oz_rowslice_kernel(const double* __restri
       for (int j = 0; j < 4; ++j) {
         const double v = b0 + j < K ? a[b0 + j] : 0.0;
         const long long Y = __double2ll_rn(v * scl) + 0x808080808080LL;
+        lo[j] = (uint32_t)Y;
+        hi[j] = (uint32_t)((unsigned long long)Y >> 32);
+      }
+      int8_t* dst = out + ((((r >> 7) * kbA + (b0 >> 5)) * OZ_S) * OZ_BM + (r & 127)) * OZ_BK + (b0 & 31);
+#pragma unroll
+      for (int q = 1; q < OZ_S; ++q) {
+        const int j = 6 - q;
+        const uint32_t* src = j < 4 ? lo : hi;
+        const uint32_t sel = (uint32_t)((j & 3) | (((j & 3) + 4) << 4));
+        const uint32_t xx = __byte_perm(src[0], src[1], sel), yy = __byte_perm(src[2], src[3], sel);
+        *reinterpret_cast<uint32_t*>(dst + q * OZ_BM * OZ_BK) = __byte_perm(xx, yy, 0x5410) ^ 0x80808080u;
+      }
+      {
+        const uint32_t xx = __byte_perm(hi[0], hi[1], 0x62), yy = __byte_perm(hi[2], hi[3], 0x62);
+        *reinterpret_cast<uint32_t*>(dst) = __byte_perm(xx, yy, 0x5410);
+      }
+    }
+  }
+}
+
+// The same for rows of <= 128 NCH columns, one read: lane l loads columns 128 t + 4 l .. + 3 of every 128-column
+// block t (16-byte loads; a warp instruction covers 1 KB contiguous), all NCH x 4 values stay in registers for
+// the maximum and the digit split, and every load of the row is issued before the first is used
+template <int NCH>
+__global__ void __launch_bounds__(256) oz_rowslice_reg_kernel(const double* __restrict__ A, int64_t lda, int64_t M,
+                                                              int K, int KP, int8_t* __restrict__ out,
+                                                              int* __restrict__ erow) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int kbA = KP / OZ_BK;
+  for (int64_t r = (int64_t)blockIdx.x * 8 + warp; r < M; r += (int64_t)gridDim.x * 8) {
+    const double* a = A + r * lda;
+    double v[NCH][4];
+#pragma unroll
+    for (int t = 0; t < NCH; ++t) {
+      const int b0 = 128 * t + 4 * lane;
+      if (b0 + 3 < K) {
+        const double2 x = __ldcs(reinterpret_cast<const double2*>(a + b0));
+        const double2 y = __ldcs(reinterpret_cast<const double2*>(a + b0 + 2));
+        v[t][0] = x.x; v[t][1] = x.y; v[t][2] = y.x; v[t][3] = y.y;
+      } else {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) v[t][j] = b0 + j < K ? a[b0 + j] : 0.0;
+      }
+    }
+    double mx = 0.0;
+    bool bad = false;
+#pragma unroll
+    for (int t = 0; t < NCH; ++t)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        bad |= !isfinite(v[t][j]);
+        mx = fmax(mx, fabs(v[t][j]));
+      }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    bad = __any_sync(0xffffffffu, bad);
+    const int er = oz_exp((unsigned long long)__double_as_longlong(mx));
+    if (lane == 0) erow[r] = bad ? 0x7fffffff : er;
+    const double scl = bad ? 0.0 : ldexp(1.0, 55 - er);
+#pragma unroll
+    for (int t = 0; t < NCH; ++t) {
+      const int b0 = 128 * t + 4 * lane;
+      if (b0 >= KP) continue;
+      uint32_t lo[4], hi[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const long long Y = __double2ll_rn(v[t][j] * scl) + 0x808080808080LL;
         lo[j] = (uint32_t)Y;
         hi[j] = (uint32_t)((unsigned long long)Y >> 32);
       }
@@ -841,7 +913,14 @@ cudaError_t launch_gemm_tn_i8(const double* A, int64_t lda, int64_t M, const dou
     const int64_t rows = std::min<int64_t>(cap_rows, M - c0);
     const int64_t nposp = k1_nposp(rows);
     const int nb = (int)std::min<int64_t>((rows + 7) / 8, (int64_t)sms * 8);
-    oz_rowslice_kernel<<<nb, 256, 0, s>>>(A + c0 * lda, lda, rows, K, KP, ws, erow);
+    // rows of <= 512 columns from registers in one read (16-byte loads need lda even and A 16-byte aligned)
+    const bool reg = KP <= 512 && (lda & 1) == 0 && (reinterpret_cast<uintptr_t>(A) & 15) == 0;
+    if (reg && KP <= 256)
+      oz_rowslice_reg_kernel<2><<<nb, 256, 0, s>>>(A + c0 * lda, lda, rows, K, KP, ws, erow);
+    else if (reg)
+      oz_rowslice_reg_kernel<4><<<nb, 256, 0, s>>>(A + c0 * lda, lda, rows, K, KP, ws, erow);
+    else
+      oz_rowslice_kernel<<<nb, 256, 0, s>>>(A + c0 * lda, lda, rows, K, KP, ws, erow);
     CUtensorMap ta;
     e = make_tmap_i8_slices(&ta, ws, (uint64_t)kb * (nposp / OZ_BM), (uint64_t)OZ_BM, OZ_S, OZ_BM);
     if (e != cudaSuccess) return e;
