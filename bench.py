@@ -135,6 +135,15 @@ def syrk_int8_ops(n, m):
     return 2.0 * 28 * nrp * tiles * 128 * 64
 
 
+def ufeat_int8_ops(n, m):
+    """int8 tensor-core ops (2 per MAC) of the K1 GEMM on the integer-slice engine (k_ozaki.cu oz_gemm_kernel): per
+    128-row block, 64-column tiles J with the triangular k range min(kb, 2J + 2) blocks of 32, 28 digit products each"""
+    mk = -(-m // 8) * 8
+    kb, nJ = -(-mk // 32), -(-mk // 64)
+    kblocks = sum(min(kb, 2 * J + 2) for J in range(nJ))
+    return 2.0 * 28 * (-(-n // 128)) * kblocks * 128 * 64 * 32
+
+
 def workload_flops(nbr, m):
     s = (nbr >= 0).sum(1).astype(np.float64) + 1.0 if nbr.shape[1] > 0 else np.ones(nbr.shape[0])
     f = per_point_flops(s, m)
@@ -507,6 +516,21 @@ def main():
                          "flops_per_launch": fl_launch[dom], "avg_launch_ms": stage_avg[kern[dom]],
                          "per_kernel": dict({k: {"stage": kern[k], "avg_ms": stage_avg[kern[k]], "tflops": achieved[k],
                                                  "frac": achieved[k] / FP64_PEAK_TFLOPS} for k in kern},
+                                            ufeat={"stage": kern["ufeat"], "avg_ms": stage_avg[kern["ufeat"]],
+                                                   "tflops": achieved["ufeat"],
+                                                   "frac": achieved["ufeat"] / FP64_PEAK_TFLOPS,
+                                                   "engine": "FP64 emulated by int8 digit slices on "
+                                                             "tcgen05.mma.kind::i8 (k_ozaki.cu): tflops/frac are "
+                                                             "FP64-equivalent (algorithmic FP64 flops / time, vs the "
+                                                             "DMMA peak)",
+                                                   "int8_tops": ufeat_int8_ops(w.n / world, w.m) /
+                                                   (stage_avg[kern["ufeat"]] * 1e-3) / 1e12,
+                                                   "int8_peak_tops": INT8_PEAK_TOPS,
+                                                   "int8_frac": ufeat_int8_ops(w.n / world, w.m) /
+                                                   (stage_avg[kern["ufeat"]] * 1e-3) / 1e12 / INT8_PEAK_TOPS,
+                                                   "int8_note": "stage time includes kx_slice (the kernel "
+                                                                "evaluations written as digit slices, ~2.0 of 5.6 ms "
+                                                                "at config 3)"},
                                             syrk={"stage": kern["syrk"], "avg_ms": stage_avg[kern["syrk"]],
                                                   "tflops": achieved["syrk"],
                                                   "frac": achieved["syrk"] / FP64_PEAK_TFLOPS,
