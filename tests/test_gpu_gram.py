@@ -99,3 +99,38 @@ def test_factor_engines_agree(monkeypatch, cid, n):
     assert du.max() <= 1e-12, du.max()
     # the gradient (its Gamma, T and G2 contractions on the integer engines too) to 1e-9 of the largest component
     np.testing.assert_allclose(G["int8"], G["fp64"], rtol=0, atol=1e-9 * np.abs(G["fp64"]).max())
+
+
+def _exact_gram(W):
+    """G = W^T W in exact rational arithmetic: every double is m * 2^e with integer m, so each product and sum is
+    an exact Python integer at a common exponent; returns the exactly rounded float64 G"""
+    from fractions import Fraction
+    n, c = W.shape
+    F = [[Fraction(float(v)) for v in row] for row in W]
+    G = np.zeros((c, c))
+    for a in range(c):
+        for b in range(a + 1):
+            s = sum(F[k][a] * F[k][b] for k in range(n))
+            G[a, b] = G[b, a] = float(s)
+    return G
+
+
+def test_gram_int8_error_within_reading_c18_bound():
+    """DESIGN reading c18: per entry |G_int8 - G_exact| <= K * 2^-54 * max|w_a| * max|w_b| + 2^-52 |G_exact|
+    (one rounding of each operand to 55 bits of its column maximum, dropped digit levels below 2^-51 of the
+    product of the maxima, exact int32 level sums, FP64 combination), checked against an exact rational
+    reference on columns spanning 2^-200 .. 2^200 and rows spanning 2^-20 .. 2^20 (a column-relative bound:
+    small entries of a column carry the column maximum's absolute precision, like FP64's own dot-product bound)"""
+    rng = np.random.default_rng(2507)
+    n, c = 257, 24
+    W = rng.standard_normal((n, c))
+    W *= np.exp2(rng.uniform(-20, 20, size=(n, 1)))
+    W *= np.exp2(np.linspace(-200, 200, c))[None, :]
+    W[:, 7] = 0.0  # an all-zero column
+    G = p.vif_gram(torch.from_numpy(W).cuda(), "int8").cpu().numpy()
+    E = _exact_gram(W)
+    cm = np.abs(W).max(0)
+    bound = n * 2.0 ** -54 * np.outer(cm, cm) + 2.0 ** -52 * np.abs(E)
+    err = np.abs(G - E)
+    assert np.all(err <= bound), float(np.max(err / np.maximum(bound, 1e-300)))
+    assert np.all(G[7] == 0.0) and np.all(G[:, 7] == 0.0)

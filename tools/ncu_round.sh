@@ -1,7 +1,7 @@
 #!/bin/bash
 # Round-end ncu evidence at the bench configuration (config 3, n = 1M):
 #  1) launch list of the bench command (gpu__time_duration per launch, cold-cache, serialised)
-#  2) ncu --set full (with source) of the dominant kernels: vecchia_reg, the TMA GEMM and SYRK, kx_eval
+#  2) ncu --set full (with source) of the dominant kernels: vecchia_reg and the integer-slice K1 / K4 kernels
 # usage: bash tools/ncu_round.sh <tag>   (outputs gpurun_out/<tag>_*)
 T=${1:-round}
 CMD="python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-grad --npred 0 --no-knn --la-n 0"
@@ -11,6 +11,6 @@ ncu --metrics gpu__time_duration.sum --clock-control none --kernel-name-base dem
 echo "launch list rc=$?"
 $CMD > gpurun_out/${T}_ncu_plain2.log 2>&1 && \
 ncu --set full --clock-control none --import-source on --kernel-name-base demangled \
-    -k regex:"vecchia_reg_kernel|gemm_tn_tma|syrk_tma|kx_eval" -s 4 -c 4 -o gpurun_out/${T}_prof $CMD \
+    -k regex:"vecchia_reg_kernel|oz_gemm|oz_syrk|kx_slice" -s 4 -c 4 -o gpurun_out/${T}_prof $CMD \
     > gpurun_out/${T}_ncu_full.log 2>&1
 echo "ncu full rc=$?"
