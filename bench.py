@@ -449,7 +449,8 @@ def main():
         same = float((g.cpu().numpy() == w.nbr).all(1).mean())
         knn = {"s": ks, "rows_equal_to_generator": same, "generator_s": w.timings.get("neighbors"),
                "tflops": w.n * (w.n - 1) / 2 * w.m * 2 / ks / 1e12,
-               "note": "vif_neighbors: exact d_c neighbour sets (P:499-513) by brute force on DMMA (n^2 m / 2 FMA); "
+               "note": "vif_neighbors: exact d_c neighbour sets (P:499-513) by brute force (n^2 m / 2 FMA), the Gram "
+                       "blocks as int8 digit-slice products on tcgen05 (reading c18; tflops = FP64-equivalent); "
                        "generator_s = the torch brute force of the input generator (vifgen) on the same GPU"}
         model.factor(th[0])  # vif_neighbors invalidates the factor; leave the handle evaluated
         model.nll()

@@ -194,6 +194,13 @@ __global__ void __launch_bounds__(256, 2) knn_kernel(const double* __restrict__ 
 
 static_assert(2 * KST * KQ * KPAD >= KQ * (KQ + 1), "score tile must fit in the staging buffers");
 
+cudaError_t launch_knn_resvar(const double* U, int64_t ldu, int m, int64_t n, const CovParams& p, double* isd,
+                              int* deg, cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  resvar_kernel<<<(unsigned)((n + 7) / 8), 256, 0, s>>>(U, (int)ldu, m, n, p.sigma2, isd, deg);
+  return cudaGetLastError();
+}
+
 size_t knn_smem_bytes(int mv) {
   return sizeof(double) * ((size_t)2 * KST * KQ * KPAD + (size_t)KQ * mv) + sizeof(int) * (size_t)KQ * mv;
 }

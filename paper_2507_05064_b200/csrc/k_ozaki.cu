@@ -1006,4 +1006,252 @@ cudaError_t launch_gemm_tt_i8(const double* A, int64_t lda, int M, const double*
   return cudaSuccess;
 }
 
+
+// ================================================================== neighbour search on the integer tensor cores
+// vif_neighbors (readings c5-c7): the same exhaustive search as knn_kernel (k_knn.cu) with the
+// Gram blocks u_Q u_C^T of the whitened features as exact int8 digit-slice products (reading c18): the rows of
+// U are split per row (oz_rowslice), a CTA owns 128 consecutive queries and sweeps the candidate tiles of 64
+// predecessors.  Warp 0 streams {32 k, 128 query rows, 7 slices} and {32 k, 64 candidate rows, 7 slices} TMA
+// boxes through a 3-stage ring, warp 1 issues the 10 MMAs per stage into the 7 level accumulators (TMEM
+// columns [64 L, 64 L + 64)), warps 2-5 (one thread per query = its TMEM lane) drain 16 candidates at a
+// time, form rho_c = k(x_i, x_j) - u_i.u_j and the score |rho_c| / sqrt(rho_ii rho_jj) exactly as knn_kernel
+// does (16 independent chains), and merge the few that beat the query's threshold (in increasing index: ties
+// keep the lower index) into its sorted top-m_v list in shared memory.
+namespace {
+constexpr int KN_STAGES = 3;
+constexpr int KN_Q = 128, KN_C = 64;
+constexpr int KN_MAXMV = 47;
+}  // namespace
+
+size_t knn_i8_smem_bytes(int mv) {
+  return (size_t)KN_STAGES * OZ_STAGE_BYTES + 1024 + 256 + (size_t)KN_Q * mv * (sizeof(double) + sizeof(int)) + 8 +
+         (size_t)KN_C * (VIF_MAX_D + 2) * sizeof(double);
+}
+
+template <int FAM>
+__global__ void __launch_bounds__(192, 1)
+    knn_i8_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmC, int kbmax,
+                  const int* __restrict__ erow, const double* __restrict__ X, int64_t n, CovParams p,
+                  const double* __restrict__ isd, const int* __restrict__ deg, int mv, int32_t* __restrict__ out,
+                  int qoff, int qstride) {
+  extern __shared__ uint8_t oz_raw[];
+  uint8_t* st = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(oz_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(st + KN_STAGES * OZ_STAGE_BYTES);
+  uint64_t* empty = full + KN_STAGES;
+  uint64_t* tfull = empty + KN_STAGES;
+  uint64_t* tempty = tfull + 1;
+  uint32_t* tbase = reinterpret_cast<uint32_t*>(tempty + 1);
+  double* lv = reinterpret_cast<double*>(st + KN_STAGES * OZ_STAGE_BYTES + 256);  // [KN_Q][mv] list scores
+  int* li = reinterpret_cast<int*>(lv + KN_Q * mv);                                // [KN_Q][mv] list indices
+  double* xc = reinterpret_cast<double*>(li + ((KN_Q * mv + 1) & ~1));             // [KN_C][VIF_MAX_D]
+  double* isc = xc + KN_C * VIF_MAX_D;                                             // [KN_C]
+  double* esc = isc + KN_C;                                                        // [KN_C] 2^e_j
+  __shared__ double tbl[64];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t nq = (n + KN_Q - 1) / KN_Q;
+  const int64_t qb = nq - 1 - (qoff + (int64_t)qstride * blockIdx.x);  // longest sweeps first
+  const int64_t q0 = qb * KN_Q;
+  const int64_t qe = q0 + KN_Q < n ? q0 + KN_Q : n;
+  const int ntile = (int)((qe - 1 + KN_C - 1) / KN_C);  // candidates j < i <= min(q0 + 127, n - 1)
+  exp_table_init(tbl, p.sigma2, threadIdx.x);
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < KN_STAGES; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    mbar_init(tfull, 1);
+    mbar_init(tempty, 128);
+    fence_mbar_init();
+  }
+  if (warp == 1) tc_alloc<512>(tbase);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tbase;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      tma_prefetch_desc(&tmQ);
+      tma_prefetch_desc(&tmC);
+      int64_t it = 0;
+      for (int t = 0; t < ntile; ++t)
+        for (int kb = 0; kb < kbmax; ++kb, ++it) {
+          const int s = (int)(it % KN_STAGES);
+          if (it >= KN_STAGES) mbar_wait(&empty[s], (uint32_t)(((it / KN_STAGES) - 1) & 1));
+          uint8_t* a = st + s * OZ_STAGE_BYTES;
+          mbar_expect_tx(&full[s], OZ_STAGE_BYTES);
+          tma_load_4d(a, &tmQ, 0, 0, 0, (int)(qb * kbmax + kb), &full[s]);
+          tma_load_4d(a + OZ_A_BYTES, &tmC, 0, (t & 1) * KN_C, 0, (t >> 1) * kbmax + kb, &full[s]);
+        }
+    }
+  } else if (warp == 1) {
+    int64_t it = 0;
+    for (int t = 0; t < ntile; ++t) {
+      if (t > 0) mbar_wait(tempty, (uint32_t)((t - 1) & 1));
+      tc_fence_after();
+      for (int kb = 0; kb < kbmax; ++kb, ++it) {
+        const int s = (int)(it % KN_STAGES);
+        mbar_wait(&full[s], (uint32_t)((it / KN_STAGES) & 1));
+        tc_fence_after();
+        if (lane == 0) {
+          oz_issue_stage(tmem, smem_u32(st + s * OZ_STAGE_BYTES), kb == 0);
+          tc_commit(&empty[s]);
+          if (kb + 1 == kbmax) tc_commit(tfull);
+        }
+        __syncwarp();
+      }
+    }
+  } else {
+    const int q = warp & 3;  // TMEM lane quarter
+    const int r = q * 32 + lane, et = threadIdx.x - 64;  // query row of the block; epilogue thread 0..127
+    const int64_t i = q0 + r;
+    const int d = p.d;
+    double xq[VIF_MAX_D];
+#pragma unroll
+    for (int k = 0; k < VIF_MAX_D; ++k)
+      xq[k] = (k < d && i < n) ? X[i * d + k] * (fam_scale<FAM>() * p.inv_ls[k]) : 0.0;
+    const double isq = i < n ? isd[i] : 0.0;
+    const bool dgq = i < n && deg[i] != 0;
+    const double eq = i < n ? ldexp(1.0, erow[i] - 14) : 0.0;
+    const double inv_fs2 = 1.0 / (fam_scale<FAM>() * fam_scale<FAM>());
+    double* v = lv + r * mv;
+    int* ix = li + r * mv;
+    int k = 0;
+    double thr = -INFINITY;
+    for (int t = 0; t < ntile; ++t) {
+      const int64_t c0 = (int64_t)t * KN_C;
+      asm volatile("bar.sync 1, 128;" ::: "memory");  // the previous tile's candidate data is no longer read
+      for (int e = et; e < KN_C * d; e += 128) {
+        const int c = e / d, kk = e % d;
+        xc[c * VIF_MAX_D + kk] = c0 + c < n ? X[(c0 + c) * d + kk] * (fam_scale<FAM>() * p.inv_ls[kk]) : 0.0;
+      }
+      if (et < KN_C) {
+        const int64_t j = c0 + et;
+        isc[et] = j < n ? isd[j] : 0.0;
+        esc[et] = j < n ? ldexp(1.0, erow[j]) : 0.0;
+      }
+      asm volatile("bar.sync 1, 128;" ::: "memory");  // xc, isc, esc of this tile visible
+      mbar_wait(tfull, (uint32_t)(t & 1));
+      tc_fence_after();
+#pragma unroll 1
+      for (int h = 0; h < KN_C / 16; ++h) {
+        double g[16];
+        oz_drain16(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(h * 16), g);
+        if (h + 1 == KN_C / 16) {
+          tc_fence_before();
+          mbar_arrive(tempty);  // TMEM read: the MMA warp may start the next tile
+        }
+        // the 16 scores as independent chains (ILP)
+        double sc[16];
+        {
+          double t2[16];
+#pragma unroll
+          for (int jj = 0; jj < 16; ++jj) {
+            const double d0 = xq[0] - xc[(h * 16 + jj) * VIF_MAX_D];
+            t2[jj] = d0 * d0;
+          }
+          for (int kk = 1; kk < d; ++kk)
+#pragma unroll
+            for (int jj = 0; jj < 16; ++jj) {
+              const double dk = xq[kk] - xc[(h * 16 + jj) * VIF_MAX_D + kk];
+              t2[jj] = fma(dk, dk, t2[jj]);
+            }
+#pragma unroll
+          for (int jj = 0; jj < 16; ++jj) {
+            const int c = h * 16 + jj;
+            double cv;
+            if (FAM == FAM_GAUSS) {
+              cv = sig2_exp_neg(t2[jj], tbl);
+            } else {
+              const double tt = sqrt_fast(t2[jj]);
+              const double E = sig2_exp_neg(tt, tbl);
+              cv = FAM == FAM_M12 ? E : (FAM == FAM_M32 ? fma(E, tt, E) : fma(E, fma(t2[jj], 1.0 / 3.0, tt), E));
+            }
+            const double uu = g[jj] * eq * esc[c];
+            sc[jj] = dgq ? -t2[jj] * inv_fs2 : (isc[c] == 0.0 ? 0.0 : fabs(cv - uu) * isq * isc[c]);
+          }
+        }
+        // candidates that can enter the list at the current threshold (it only rises): usually none once the
+        // list is full; the rest in increasing index order, unrolled so the scores stay in registers
+        unsigned msk = 0;
+#pragma unroll
+        for (int jj = 0; jj < 16; ++jj) {
+          const int64_t j = c0 + h * 16 + jj;
+          if (j < i && i < n && (k < mv || sc[jj] > thr)) msk |= 1u << jj;
+        }
+        if (msk) {
+#pragma unroll
+          for (int jj = 0; jj < 16; ++jj) {
+            const double scj = sc[jj];
+            if (((msk >> jj) & 1u) && (k < mv || scj > thr)) {
+              int pos = k < mv ? k : mv - 1;
+              while (pos > 0 && scj > v[pos - 1]) {
+                v[pos] = v[pos - 1];
+                ix[pos] = ix[pos - 1];
+                --pos;
+              }
+              v[pos] = scj;
+              ix[pos] = (int)(c0 + h * 16 + jj);
+              if (k < mv) ++k;
+              thr = k < mv ? -INFINITY : v[mv - 1];
+            }
+          }
+        }
+      }
+    }
+    if (i < n)
+      for (int kk = 0; kk < mv; ++kk) out[i * mv + kk] = kk < k ? ix[kk] : -1;
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 1) tc_free<512>(tmem);
+}
+
+bool knn_i8_supported(int mv, int64_t n) { return mv >= 1 && mv <= KN_MAXMV && n >= 2; }
+
+size_t knn_i8_ws_bytes(int mk, int64_t n) {
+  return (size_t)OZ_S * (size_t)((n + OZ_BM - 1) / OZ_BM * OZ_BM) * (size_t)k1_kb(mk) * OZ_BK;
+}
+
+// U (n x mk, ldu; rows in the processing order) -> per-row digit slices in ws, exponents in erow (n ints), then the
+// search; isd / deg as knn_kernel's resvar pass writes them (launch_knn_resvar)
+cudaError_t launch_knn_i8(const double* U, int64_t ldu, int mk, const double* X, int64_t n, const CovParams& p,
+                          const double* isd, const int* deg, int mv, int32_t* out, int8_t* ws, int* erow, int sms,
+                          cudaStream_t s, int qoff, int qstride) {
+  if (!knn_i8_supported(mv, n) || mk < 1) return cudaErrorInvalidValue;
+  const int kb = k1_kb(mk), KP = kb * OZ_BK;
+  const int64_t nposp = (n + OZ_BM - 1) / OZ_BM * OZ_BM;
+  const int nb = (int)std::min<int64_t>((n + 7) / 8, (int64_t)sms * 8);
+  const bool reg = KP <= 512 && (ldu & 1) == 0 && (reinterpret_cast<uintptr_t>(U) & 15) == 0;
+  if (reg && KP <= 256)
+    oz_rowslice_reg_kernel<2><<<nb, 256, 0, s>>>(U, ldu, n, mk, KP, ws, erow);
+  else if (reg)
+    oz_rowslice_reg_kernel<4><<<nb, 256, 0, s>>>(U, ldu, n, mk, KP, ws, erow);
+  else
+    oz_rowslice_kernel<<<nb, 256, 0, s>>>(U, ldu, n, mk, KP, ws, erow);
+  // rows n .. nposp - 1 of the last block hold stale digits: their queries and candidates are masked
+  CUtensorMap tq, tc;
+  cudaError_t e = make_tmap_i8_slices(&tq, ws, (uint64_t)kb * (nposp / OZ_BM), (uint64_t)OZ_BM, OZ_S, OZ_BM);
+  if (e != cudaSuccess) return e;
+  e = make_tmap_i8_slices(&tc, ws, (uint64_t)kb * (nposp / OZ_BM), (uint64_t)OZ_BM, OZ_S, KN_C);
+  if (e != cudaSuccess) return e;
+  const int64_t nq = (n + KN_Q - 1) / KN_Q;
+  if (qoff >= nq) return cudaGetLastError();
+  const unsigned grid = (unsigned)((nq - qoff + qstride - 1) / qstride);
+  const size_t smem = knn_i8_smem_bytes(mv);
+  auto go = [&](auto kern) -> cudaError_t {
+    cudaError_t e1 = smem_optin(kern, smem);
+    if (e1 != cudaSuccess) return e1;
+    kern<<<grid, 192, smem, s>>>(tq, tc, kb, erow, X, n, p, isd, deg, mv, out, qoff, qstride);
+    return cudaGetLastError();
+  };
+  switch (p.family) {
+    case FAM_M12: return go(knn_i8_kernel<FAM_M12>);
+    case FAM_M32: return go(knn_i8_kernel<FAM_M32>);
+    case FAM_M52: return go(knn_i8_kernel<FAM_M52>);
+    default: return go(knn_i8_kernel<FAM_GAUSS>);
+  }
+}
+
 }  // namespace vif

@@ -158,6 +158,15 @@ cudaError_t launch_pred_mean(const double* Wp, int ld, int m, int ycol, const do
                              cudaStream_t s);
 // correlation-distance neighbours (k_knn.cu)
 size_t knn_smem_bytes(int mv);
+// the same search with the Gram blocks on the integer tensor cores (k_ozaki.cu, reading c18): U rows sliced into
+// ws (knn_i8_ws_bytes) with their exponents in erow (n ints); isd / deg from launch_knn_resvar
+bool knn_i8_supported(int mv, int64_t n);
+size_t knn_i8_ws_bytes(int mk, int64_t n);
+cudaError_t launch_knn_i8(const double* U, int64_t ldu, int mk, const double* X, int64_t n, const CovParams& p,
+                          const double* isd, const int* deg, int mv, int32_t* out, int8_t* ws, int* erow, int sms,
+                          cudaStream_t s, int qoff, int qstride);
+cudaError_t launch_knn_resvar(const double* U, int64_t ldu, int m, int64_t n, const CovParams& p, double* isd,
+                              int* deg, cudaStream_t s);
 cudaError_t launch_knn(const double* U, int64_t ldu, int m, int mk, const double* X, int64_t n, const CovParams& p,
                        double* isd, int* deg, int mv, int32_t* out, cudaStream_t s, int qoff = 0, int qstride = 1);
 // VIF-Laplace iterative path (k_laplace.cu)

@@ -1657,9 +1657,23 @@ int vif_neighbors(void* handle, const vif_theta* theta, int32_t mv, int32_t* nbr
       qstride = G;
     }
   }
-  VIF_CUDA(h, launch_knn(h->buf<double>(B_U), P.ld, P.m, P.mk, h->buf<double>(B_X), P.n, p, isd, deg, mv, nbr_out, s,
-                         qoff, qstride),
-           "neighbour search");
+  // the Gram blocks on the integer tensor cores when the slice workspace holds all n rows (reading c18);
+  // VIF_KNN_FP64=1: the DMMA kernel
+  static const char* kf_env = getenv("VIF_KNN_FP64");
+  const bool knn_i8 = P.m > 0 && !(kf_env && kf_env[0] == '1') && knn_i8_supported(mv, P.n) &&
+                      h->L.size[B_WS] >= knn_i8_ws_bytes(P.mk, P.n) &&
+                      h->L.size[B_W] >= (size_t)P.n * (sizeof(double) + 2 * sizeof(int));
+  if (knn_i8) {
+    int* erow = deg + P.n;  // row exponents of the digit slices, after isd and deg in the dead W buffer
+    VIF_CUDA(h, launch_knn_resvar(h->buf<double>(B_U), P.ld, P.m, P.n, p, isd, deg, s), "residual variances");
+    VIF_CUDA(h, launch_knn_i8(h->buf<double>(B_U), P.ld, P.mk, h->buf<double>(B_X), P.n, p, isd, deg, mv, nbr_out,
+                              h->buf<int8_t>(B_WS), erow, h->num_sms, s, qoff, qstride),
+             "neighbour search (int8 slices)");
+  } else {
+    VIF_CUDA(h, launch_knn(h->buf<double>(B_U), P.ld, P.m, P.mk, h->buf<double>(B_X), P.n, p, isd, deg, mv, nbr_out,
+                           s, qoff, qstride),
+             "neighbour search");
+  }
   {
     int r = mark_inputs_used(h);
     if (r != VIF_OK) return r;

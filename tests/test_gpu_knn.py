@@ -185,3 +185,42 @@ def test_search_config3_equals_generator():
         np.testing.assert_allclose(np.sort(a), np.sort(b), rtol=1e-12, atol=1e-14)
     print(f"vif_neighbors n = 1M: {dt:.2f} s")
     model.close()
+
+
+@pytest.mark.parametrize("family,n,m,mv", [("matern32", 3000, 60, 20), ("gaussian", 2500, 130, 31), ("matern12", 1200, 8, 47)])
+def test_int8_and_dmma_engines_agree(family, n, m, mv):
+    """vif_neighbors with the Gram blocks on the integer tensor cores (default, reading c18) and on DMMA
+    (VIF_KNN_FP64=1, read once per process: subprocesses): the same sets on every row except scores equal
+    to rounding, where both choices carry the same oracle score"""
+    import json
+    import os
+    import subprocess
+    import sys
+    code = r"""
+import sys, json
+import numpy as np, torch
+sys.path.insert(0, %r)
+import paper_2507_05064_b200 as p, vifgen
+w = vifgen.make_workload(n=%d, d=2, m=%d, mv=%d, family=%r, rho=0.15, nugget=0.1, seed=77, device="cuda")
+dev = torch.device("cuda")
+X, Z, nbr, y = (torch.from_numpy(np.ascontiguousarray(a)).to(dev) for a in (w.X, w.Z, w.nbr, w.y))
+m = p.VifModel(X, Z, nbr, y, device=dev)
+print(json.dumps(m.neighbors(p.Theta(**w.theta_dict()), %d).cpu().numpy().tolist()))
+""" % (os.path.dirname(os.path.dirname(os.path.abspath(__file__))), n, m, mv, family, mv)
+    outs = []
+    for fp64 in ("0", "1"):
+        env = dict(os.environ, VIF_KNN_FP64=fp64)
+        r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+        outs.append(np.array(json.loads(r.stdout.strip().splitlines()[-1])))
+    a, b = outs
+    w = vifgen.make_workload(n=n, d=2, m=m, mv=mv, family=family, rho=0.15, nugget=0.1, seed=77, device="cuda")
+    diff = np.nonzero((a != b).any(1))[0]
+    assert len(diff) <= max(2, 0.005 * n), len(diff)
+    oth = oracle.Theta(**w.theta_dict())
+    for i in diff:
+        sa, sb = a[i][a[i] >= 0], b[i][b[i] >= 0]
+        assert len(sa) == len(sb) and np.all(sa < i) and len(set(sa)) == len(sa)
+        ga = oracle.dc_scores(w.X, w.Z, oth, np.full(len(sa), i), sa)
+        gb = oracle.dc_scores(w.X, w.Z, oth, np.full(len(sb), i), sb)
+        np.testing.assert_allclose(ga, gb, rtol=1e-12, atol=1e-14)
