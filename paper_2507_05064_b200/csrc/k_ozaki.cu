@@ -1023,27 +1023,30 @@ constexpr int KN_Q = 128, KN_C = 64;
 constexpr int KN_MAXMV = 47;
 }  // namespace
 
-size_t knn_i8_smem_bytes(int mv) {
-  return (size_t)KN_STAGES * OZ_STAGE_BYTES + 1024 + 256 + (size_t)KN_Q * mv * (sizeof(double) + sizeof(int)) + 8 +
-         (size_t)KN_C * (VIF_MAX_D + 2) * sizeof(double);
+// shared memory of the variant: ST ring stages, NH = EW / 4 partial lists per query, the tile's candidates
+static size_t knn_i8_smem(int mv, int EW, int ST) {
+  return (size_t)ST * OZ_STAGE_BYTES + 1024 + 256 + (size_t)(EW / 4) * KN_Q * mv * (sizeof(double) + sizeof(int)) +
+         8 + (size_t)KN_C * (VIF_MAX_D + 2) * sizeof(double);
 }
 
-template <int FAM>
-__global__ void __launch_bounds__(192, 1)
+template <int FAM, int EW, int ST>
+__global__ void __launch_bounds__(64 + 32 * EW, 1)
     knn_i8_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmC, int kbmax,
                   const int* __restrict__ erow, const double* __restrict__ X, int64_t n, CovParams p,
                   const double* __restrict__ isd, const int* __restrict__ deg, int mv, int32_t* __restrict__ out,
                   int qoff, int qstride) {
   extern __shared__ uint8_t oz_raw[];
   uint8_t* st = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(oz_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(st + KN_STAGES * OZ_STAGE_BYTES);
-  uint64_t* empty = full + KN_STAGES;
+  constexpr int NH = EW / 4;  // epilogue warps per TMEM lane quarter: each takes 64 / NH candidates of a tile
+  constexpr int CW = KN_C / NH;
+  uint64_t* full = reinterpret_cast<uint64_t*>(st + ST * OZ_STAGE_BYTES);
+  uint64_t* empty = full + ST;
   uint64_t* tfull = empty + KN_STAGES;
   uint64_t* tempty = tfull + 1;
   uint32_t* tbase = reinterpret_cast<uint32_t*>(tempty + 1);
-  double* lv = reinterpret_cast<double*>(st + KN_STAGES * OZ_STAGE_BYTES + 256);  // [KN_Q][mv] list scores
-  int* li = reinterpret_cast<int*>(lv + KN_Q * mv);                                // [KN_Q][mv] list indices
-  double* xc = reinterpret_cast<double*>(li + ((KN_Q * mv + 1) & ~1));             // [KN_C][VIF_MAX_D]
+  double* lv = reinterpret_cast<double*>(st + ST * OZ_STAGE_BYTES + 256);  // [NH][KN_Q][mv] list scores
+  int* li = reinterpret_cast<int*>(lv + NH * KN_Q * mv);                     // [NH][KN_Q][mv] list indices
+  double* xc = reinterpret_cast<double*>(li + ((NH * KN_Q * mv + 1) & ~1));  // [KN_C][VIF_MAX_D]
   double* isc = xc + KN_C * VIF_MAX_D;                                             // [KN_C]
   double* esc = isc + KN_C;                                                        // [KN_C] 2^e_j
   __shared__ double tbl[64];
@@ -1055,12 +1058,12 @@ __global__ void __launch_bounds__(192, 1)
   const int ntile = (int)((qe - 1 + KN_C - 1) / KN_C);  // candidates j < i <= min(q0 + 127, n - 1)
   exp_table_init(tbl, p.sigma2, threadIdx.x);
   if (threadIdx.x == 0) {
-    for (int i = 0; i < KN_STAGES; ++i) {
+    for (int i = 0; i < ST; ++i) {
       mbar_init(&full[i], 1);
       mbar_init(&empty[i], 1);
     }
     mbar_init(tfull, 1);
-    mbar_init(tempty, 128);
+    mbar_init(tempty, 32 * EW);
     fence_mbar_init();
   }
   if (warp == 1) tc_alloc<512>(tbase);
@@ -1076,8 +1079,8 @@ __global__ void __launch_bounds__(192, 1)
       int64_t it = 0;
       for (int t = 0; t < ntile; ++t)
         for (int kb = 0; kb < kbmax; ++kb, ++it) {
-          const int s = (int)(it % KN_STAGES);
-          if (it >= KN_STAGES) mbar_wait(&empty[s], (uint32_t)(((it / KN_STAGES) - 1) & 1));
+          const int s = (int)(it % ST);
+          if (it >= ST) mbar_wait(&empty[s], (uint32_t)(((it / ST) - 1) & 1));
           uint8_t* a = st + s * OZ_STAGE_BYTES;
           mbar_expect_tx(&full[s], OZ_STAGE_BYTES);
           tma_load_4d(a, &tmQ, 0, 0, 0, (int)(qb * kbmax + kb), &full[s]);
@@ -1090,8 +1093,8 @@ __global__ void __launch_bounds__(192, 1)
       if (t > 0) mbar_wait(tempty, (uint32_t)((t - 1) & 1));
       tc_fence_after();
       for (int kb = 0; kb < kbmax; ++kb, ++it) {
-        const int s = (int)(it % KN_STAGES);
-        mbar_wait(&full[s], (uint32_t)((it / KN_STAGES) & 1));
+        const int s = (int)(it % ST);
+        mbar_wait(&full[s], (uint32_t)((it / ST) & 1));
         tc_fence_after();
         if (lane == 0) {
           oz_issue_stage(tmem, smem_u32(st + s * OZ_STAGE_BYTES), kb == 0);
@@ -1103,7 +1106,8 @@ __global__ void __launch_bounds__(192, 1)
     }
   } else {
     const int q = warp & 3;  // TMEM lane quarter
-    const int r = q * 32 + lane, et = threadIdx.x - 64;  // query row of the block; epilogue thread 0..127
+    const int r = q * 32 + lane, et = threadIdx.x - 64;  // query row of the block; epilogue thread
+    const int hh = (warp - 2) >> 2;                       // which CW candidates of every tile
     const int64_t i = q0 + r;
     const int d = p.d;
     double xq[VIF_MAX_D];
@@ -1114,14 +1118,14 @@ __global__ void __launch_bounds__(192, 1)
     const bool dgq = i < n && deg[i] != 0;
     const double eq = i < n ? ldexp(1.0, erow[i] - 14) : 0.0;
     const double inv_fs2 = 1.0 / (fam_scale<FAM>() * fam_scale<FAM>());
-    double* v = lv + r * mv;
-    int* ix = li + r * mv;
+    double* v = lv + (hh * KN_Q + r) * mv;
+    int* ix = li + (hh * KN_Q + r) * mv;
     int k = 0;
     double thr = -INFINITY;
     for (int t = 0; t < ntile; ++t) {
       const int64_t c0 = (int64_t)t * KN_C;
-      asm volatile("bar.sync 1, 128;" ::: "memory");  // the previous tile's candidate data is no longer read
-      for (int e = et; e < KN_C * d; e += 128) {
+      asm volatile("bar.sync 1, %0;" ::"n"(32 * EW) : "memory");  // the previous tile's candidates no longer read
+      for (int e = et; e < KN_C * d; e += 32 * EW) {
         const int c = e / d, kk = e % d;
         xc[c * VIF_MAX_D + kk] = c0 + c < n ? X[(c0 + c) * d + kk] * (fam_scale<FAM>() * p.inv_ls[kk]) : 0.0;
       }
@@ -1130,14 +1134,14 @@ __global__ void __launch_bounds__(192, 1)
         isc[et] = j < n ? isd[j] : 0.0;
         esc[et] = j < n ? ldexp(1.0, erow[j]) : 0.0;
       }
-      asm volatile("bar.sync 1, 128;" ::: "memory");  // xc, isc, esc of this tile visible
+      asm volatile("bar.sync 1, %0;" ::"n"(32 * EW) : "memory");  // xc, isc, esc of this tile visible
       mbar_wait(tfull, (uint32_t)(t & 1));
       tc_fence_after();
 #pragma unroll 1
-      for (int h = 0; h < KN_C / 16; ++h) {
+      for (int h = hh * (CW / 16); h < (hh + 1) * (CW / 16); ++h) {
         double g[16];
         oz_drain16(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(h * 16), g);
-        if (h + 1 == KN_C / 16) {
+        if (h + 1 == (hh + 1) * (CW / 16)) {
           tc_fence_before();
           mbar_arrive(tempty);  // TMEM read: the MMA warp may start the next tile
         }
@@ -1199,8 +1203,36 @@ __global__ void __launch_bounds__(192, 1)
         }
       }
     }
-    if (i < n)
-      for (int kk = 0; kk < mv; ++kk) out[i * mv + kk] = kk < k ? ix[kk] : -1;
+    if constexpr (NH == 1) {
+      if (i < n)
+        for (int kk = 0; kk < mv; ++kk) out[i * mv + kk] = kk < k ? ix[kk] : -1;
+    } else {
+      // two partial lists per query (candidates 0..31 and 32..63 of every tile), each sorted by (score desc,
+      // index asc): merged by the first half's thread, equal scores taking the smaller index
+      __shared__ int kcnt[2][KN_Q];
+      kcnt[hh][r] = k;
+      asm volatile("bar.sync 1, %0;" ::"n"(32 * EW) : "memory");
+      if (hh == 0 && i < n) {
+        const double* va = lv + r * mv;
+        const int* xa = li + r * mv;
+        const double* vb = lv + (KN_Q + r) * mv;
+        const int* xb = li + (KN_Q + r) * mv;
+        const int ka = kcnt[0][r], kb2 = kcnt[1][r];
+        int pa = 0, pb = 0;
+        for (int kk = 0; kk < mv; ++kk) {
+          int o = -1;
+          if (pa < ka && pb < kb2) {
+            const bool ta = va[pa] > vb[pb] || (va[pa] == vb[pb] && xa[pa] < xb[pb]);
+            o = ta ? xa[pa++] : xb[pb++];
+          } else if (pa < ka) {
+            o = xa[pa++];
+          } else if (pb < kb2) {
+            o = xb[pb++];
+          }
+          out[i * mv + kk] = o;
+        }
+      }
+    }
   }
   tc_fence_before();
   __syncthreads();
@@ -1239,19 +1271,25 @@ cudaError_t launch_knn_i8(const double* U, int64_t ldu, int mk, const double* X,
   const int64_t nq = (n + KN_Q - 1) / KN_Q;
   if (qoff >= nq) return cudaGetLastError();
   const unsigned grid = (unsigned)((nq - qoff + qstride - 1) / qstride);
-  const size_t smem = knn_i8_smem_bytes(mv);
-  auto go = [&](auto kern) -> cudaError_t {
+  // 8 epilogue warps (two per TMEM lane quarter, each scoring half of every tile into its own partial lists) and
+  // a 2-stage ring when their lists fit beside it; else 4 epilogue warps and 3 stages (VIF_KNN_EW=4 forces it)
+  static const char* ew_env = getenv("VIF_KNN_EW");
+  const bool wide = knn_i8_smem(mv, 8, 2) <= 227 * 1024 && !(ew_env && ew_env[0] == '4');
+  auto go = [&](auto kern, int ew, int stg) -> cudaError_t {
+    const size_t smem = knn_i8_smem(mv, ew, stg);
     cudaError_t e1 = smem_optin(kern, smem);
     if (e1 != cudaSuccess) return e1;
-    kern<<<grid, 192, smem, s>>>(tq, tc, kb, erow, X, n, p, isd, deg, mv, out, qoff, qstride);
+    kern<<<grid, 64 + 32 * ew, smem, s>>>(tq, tc, kb, erow, X, n, p, isd, deg, mv, out, qoff, qstride);
     return cudaGetLastError();
   };
+#define VIF_KNNI8(F) (wide ? go(knn_i8_kernel<F, 8, 2>, 8, 2) : go(knn_i8_kernel<F, 4, KN_STAGES>, 4, KN_STAGES))
   switch (p.family) {
-    case FAM_M12: return go(knn_i8_kernel<FAM_M12>);
-    case FAM_M32: return go(knn_i8_kernel<FAM_M32>);
-    case FAM_M52: return go(knn_i8_kernel<FAM_M52>);
-    default: return go(knn_i8_kernel<FAM_GAUSS>);
+    case FAM_M12: return VIF_KNNI8(FAM_M12);
+    case FAM_M32: return VIF_KNNI8(FAM_M32);
+    case FAM_M52: return VIF_KNNI8(FAM_M52);
+    default: return VIF_KNNI8(FAM_GAUSS);
   }
+#undef VIF_KNNI8
 }
 
 }  // namespace vif
