@@ -1660,14 +1660,22 @@ int vif_neighbors(void* handle, const vif_theta* theta, int32_t mv, int32_t* nbr
   // the Gram blocks on the integer tensor cores when the slice workspace holds all n rows (reading c18);
   // VIF_KNN_FP64=1: the DMMA kernel
   static const char* kf_env = getenv("VIF_KNN_FP64");
-  const bool knn_i8 = P.m > 0 && !(kf_env && kf_env[0] == '1') && knn_i8_supported(mv, P.n) &&
-                      h->L.size[B_WS] >= knn_i8_ws_bytes(P.mk, P.n) &&
-                      h->L.size[B_W] >= (size_t)P.n * (sizeof(double) + 2 * sizeof(int));
+  // the slices go to the digit-slice workspace when it holds n rows (n <= 2^20), else behind isd, deg and erow in
+  // the dead W buffer (n x ld doubles: 7 slices of KP bytes fit for m >= 32)
+  const size_t wmeta = ((size_t)P.n * (sizeof(double) + 2 * sizeof(int)) + 1023) / 1024 * 1024;
+  int8_t* kslices = nullptr;
+  static const char* kw_env = getenv("VIF_KNN_WSLICES");  // test hook: the W-buffer placement at any n
+  if (h->L.size[B_WS] >= knn_i8_ws_bytes(P.mk, P.n) && !(kw_env && kw_env[0] == '1'))
+    kslices = h->buf<int8_t>(B_WS);
+  else if (P.m > 0 && h->L.size[B_W] >= wmeta + knn_i8_ws_bytes(P.mk, P.n))
+    kslices = reinterpret_cast<int8_t*>(h->buf<char>(B_W) + wmeta);
+  const bool knn_i8 = P.m > 0 && !(kf_env && kf_env[0] == '1') && knn_i8_supported(mv, P.n) && kslices &&
+                      h->L.size[B_W] >= wmeta;
   if (knn_i8) {
     int* erow = deg + P.n;  // row exponents of the digit slices, after isd and deg in the dead W buffer
     VIF_CUDA(h, launch_knn_resvar(h->buf<double>(B_U), P.ld, P.m, P.n, p, isd, deg, s), "residual variances");
     VIF_CUDA(h, launch_knn_i8(h->buf<double>(B_U), P.ld, P.mk, h->buf<double>(B_X), P.n, p, isd, deg, mv, nbr_out,
-                              h->buf<int8_t>(B_WS), erow, h->num_sms, s, qoff, qstride),
+                              kslices, erow, h->num_sms, s, qoff, qstride),
              "neighbour search (int8 slices)");
   } else {
     VIF_CUDA(h, launch_knn(h->buf<double>(B_U), P.ld, P.m, P.mk, h->buf<double>(B_X), P.n, p, isd, deg, mv, nbr_out,

@@ -187,7 +187,7 @@ def test_search_config3_equals_generator():
     model.close()
 
 
-@pytest.mark.parametrize("family,n,m,mv", [("matern32", 3000, 60, 20), ("gaussian", 2500, 130, 31), ("matern12", 1200, 8, 47)])
+@pytest.mark.parametrize("family,n,m,mv", [("matern32", 3000, 60, 20), ("gaussian", 2500, 250, 31), ("matern12", 1200, 8, 47)])
 def test_int8_and_dmma_engines_agree(family, n, m, mv):
     """vif_neighbors with the Gram blocks on the integer tensor cores (default, reading c18) and on DMMA
     (VIF_KNN_FP64=1, read once per process: subprocesses): the same sets on every row except scores equal
@@ -209,7 +209,8 @@ print(json.dumps(m.neighbors(p.Theta(**w.theta_dict()), %d).cpu().numpy().tolist
 """ % (os.path.dirname(os.path.dirname(os.path.abspath(__file__))), n, m, mv, family, mv)
     outs = []
     for fp64 in ("0", "1"):
-        env = dict(os.environ, VIF_KNN_FP64=fp64)
+        # the int8 run places its digit slices in the W buffer (the n > 2^20 placement) for the largest case
+        env = dict(os.environ, VIF_KNN_FP64=fp64, VIF_KNN_WSLICES="1" if m >= 100 else "0")
         r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
         assert r.returncode == 0, r.stderr[-2000:]
         outs.append(np.array(json.loads(r.stdout.strip().splitlines()[-1])))
