@@ -56,29 +56,6 @@ __device__ __forceinline__ double dcov(const double* __restrict__ a, const doubl
 // with Delta~_j = a~_j - b~_j and E = sigma_1^2 e^{-t}:  dk/dsigma_1^2 = k / sigma_1^2;
 // dk/dlambda_j = E Delta~_j^2 / lambda_j x {1/t (M12), 1 (M32), (1+t)/3 (M52), 2 (Gaussian, t = r^2)}.
 template <int FAM>
-__device__ __forceinline__ double dcov_fast(const double* __restrict__ a, const double* __restrict__ b, int pidx,
-                                            const CovParams& p, const double* __restrict__ tbl) {
-  double t2 = 0.0;
-  for (int k = 0; k < p.d; ++k) {
-    const double dk = a[k] - b[k];
-    t2 = fma(dk, dk, t2);
-  }
-  const double t = FAM == FAM_GAUSS ? t2 : sqrt_fast(t2);
-  const double E = sig2_exp_neg(t, tbl);
-  if (pidx == 0) {
-    const double f = FAM == FAM_M12 || FAM == FAM_GAUSS ? E : (FAM == FAM_M32 ? fma(E, t, E) : fma(E, fma(t2, 1.0 / 3.0, t), E));
-    return f / p.sigma2;
-  }
-  const int j = pidx - 1;
-  const double dj = a[j] - b[j];
-  const double g = E * dj * dj * p.inv_ls[j];
-  if (FAM == FAM_M12) return t > 0.0 ? g / t : 0.0;
-  if (FAM == FAM_M32) return g;
-  if (FAM == FAM_M52) return fma(g, t, g) * (1.0 / 3.0);
-  return 2.0 * g;
-}
-
-template <int FAM>
 __global__ void dkm_kernel(const double* __restrict__ Z, int m, int mk, int pidx, CovParams p,
                            double* __restrict__ out) {
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -592,50 +569,54 @@ __global__ void __launch_bounds__(GW * 32) grad_adjoint_kernel(const double* __r
   }
 }
 
+// The same point terms for EVERY parameter in one pass (the default; no dU): per pair (r, c) of the lower
+// triangle the distance, the table exponential (cov_fast's) and the family factor are formed once and feed the
+// derivatives dk/dsigma_1^2 = k / sigma_1^2, dk/dlambda_j = E Delta~_j^2 / lambda_j x {1/t, 1, (1+t)/3, 2}
+// (Matern 1/2, 3/2, 5/2, Gaussian) and dk/dsigma^2 = I (one pass per parameter before round 2: the sums are
+// bit-identical, the pass 3x cheaper).  part[pi * nblocks + block]: block partials.
 template <int FAM, int RB>
-__global__ void __launch_bounds__(GW * 32) grad_param_adj_kernel(
-    const double* __restrict__ dU, int64_t ldu, int mk, const double* __restrict__ X, const int32_t* __restrict__ nbr,
-    int mv, const int64_t* __restrict__ order, int64_t npts, CovParams p, int pidx, const double* __restrict__ state,
-    const double* __restrict__ rho, const double* __restrict__ sig, const double* __restrict__ adj,
-    double* __restrict__ part) {
+__global__ void __launch_bounds__(GW * 32) grad_param_adj_all_kernel(
+    const double* __restrict__ X, const int32_t* __restrict__ nbr, int mv, const int64_t* __restrict__ order,
+    int64_t npts, CovParams p, const double* __restrict__ state, const double* __restrict__ adj,
+    double* __restrict__ part, int64_t nblocks) {
   constexpr int SP = RB * 8;
   constexpr int LP = SP * (SP + 1) / 2;
+  constexpr int NPM = VIF_MAX_D + 2;
   __shared__ int Sidx_all[GW][SP];
-  __shared__ double at_all[GW][SP], bt_all[GW][SP], w_all[GW][SP];
+  __shared__ double at_all[GW][SP], w_all[GW][SP];
   __shared__ double xs_all[GW][SP * VIF_MAX_D];
-  __shared__ double wsum[GW];
+  __shared__ double wsum[GW][NPM];
   __shared__ double tbl[64];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t pos = (int64_t)blockIdx.x * GW + warp;
+  const int d = p.d;
   exp_table_init(tbl, p.sigma2, threadIdx.x);
   __syncthreads();
-  double contrib = 0.0;
+  double acc[NPM];
+#pragma unroll
+  for (int k = 0; k < NPM; ++k) acc[k] = 0.0;
+  bool ok = true;
   if (pos < npts) {
     const int64_t i = order[pos];
     int* Sidx = Sidx_all[warp];
     double* at = at_all[warp];
-    double* bt = bt_all[warp];
     double* wv = w_all[warp];
     double* xs = xs_all[warp];
     const int q = grad_load_S(nbr, mv, i, lane, SP, Sidx);
     const int s = q + 1;
     __syncwarp();
     for (int t = lane; t < s; t += 32)
-      for (int k = 0; k < p.d; ++k) xs[t * p.d + k] = X[(int64_t)Sidx[t] * p.d + k] * (fam_scale<FAM>() * p.inv_ls[k]);
+      for (int k = 0; k < d; ++k) xs[t * d + k] = X[(int64_t)Sidx[t] * d + k] * (fam_scale<FAM>() * p.inv_ls[k]);
     const double* st = state + pos * (int64_t)state_doubles<RB>();
-    const bool ok = st[LP + 3 * SP + 1] != 0.0;
+    ok = st[LP + 3 * SP + 1] != 0.0;
     const double* ad = adj + pos * (int64_t)ADJ_STRIDE;
     const double mu = ad[0], Dm = ad[1];
     for (int t = lane; t < SP; t += 32) {
       const double atl = t < q ? -st[LP + t] : (t == q ? 1.0 : 0.0);
-      const double btl = ad[2 + t];
       at[t] = atl;
-      bt[t] = btl;
-      wv[t] = fma(mu, atl, -Dm * btl);
+      wv[t] = fma(mu, atl, -Dm * ad[2 + t]);
     }
     __syncwarp();
-    // sum_{a,b} w_a a~_b dK_ab over the lower triangle (dK symmetric); nugget: dK = I
-    double acc = 0.0;
     const int ne = s * (s + 1) / 2;
     for (int e = lane; e < ne; e += 32) {
       int r = (int)((sqrtf_fast(8.0f * (float)e + 1.0f) - 1.0f) * 0.5f);
@@ -643,34 +624,71 @@ __global__ void __launch_bounds__(GW * 32) grad_param_adj_kernel(
       if (r * (r + 1) / 2 > e) --r;
       const int c = e - r * (r + 1) / 2;
       const double coef = r == c ? wv[r] * at[r] : fma(wv[r], at[c], wv[c] * at[r]);
-      double dk;
-      if (pidx <= p.d) dk = dcov_fast<FAM>(xs + r * p.d, xs + c * p.d, pidx, p, tbl);
-      else dk = r == c ? 1.0 : 0.0;
-      acc = fma(coef, dk, acc);
-    }
-    if (dU) {
-      const double* rrow = rho + pos * (int64_t)mk;
-      const double* srow = sig + pos * (int64_t)mk;
-      for (int k = lane; k < mk; k += 32) {
-        double e1 = 0.0, e2 = 0.0;
-        for (int b = 0; b < s; ++b) {
-          const double du = __ldg(dU + (int64_t)Sidx[b] * ldu + k);
-          e1 = fma(at[b], du, e1);
-          e2 = fma(bt[b], du, e2);
-        }
-        acc = fma(e1, __ldg(rrow + k), fma(e2, __ldg(srow + k), acc));
+      const double* xa = xs + r * d;
+      const double* xb = xs + c * d;
+      double t2 = 0.0;
+      for (int k = 0; k < d; ++k) {
+        const double dk = xa[k] - xb[k];
+        t2 = fma(dk, dk, t2);
       }
-    }
+      const double t = FAM == FAM_GAUSS ? t2 : sqrt_fast(t2);
+      const double E = sig2_exp_neg(t, tbl);
+      const double f = FAM == FAM_M12 || FAM == FAM_GAUSS ? E : (FAM == FAM_M32 ? fma(E, t, E) : fma(E, fma(t2, 1.0 / 3.0, t), E));
+      acc[0] = fma(coef, f / p.sigma2, acc[0]);
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    contrib = ok ? acc : __longlong_as_double(0x7ff8000000000000LL);
+      for (int j = 0; j < VIF_MAX_D; ++j) {
+        if (j < d) {
+          const double dj = xa[j] - xb[j];
+          const double g = E * dj * dj * p.inv_ls[j];
+          double dkj;
+          if (FAM == FAM_M12) dkj = t > 0.0 ? g / t : 0.0;
+          else if (FAM == FAM_M32) dkj = g;
+          else if (FAM == FAM_M52) dkj = fma(g, t, g) * (1.0 / 3.0);
+          else dkj = 2.0 * g;
+          acc[1 + j] = fma(coef, dkj, acc[1 + j]);
+        }
+      }
+      acc[NPM - 1] = fma(coef, r == c ? 1.0 : 0.0, acc[NPM - 1]);  // nugget: dK = I
+    }
   }
-  if (lane == 0) wsum[warp] = contrib;
+#pragma unroll
+  for (int k = 0; k < NPM; ++k) {
+    double v = acc[k];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    acc[k] = ok ? v : __longlong_as_double(0x7ff8000000000000LL);
+  }
+  if (lane == 0) {
+#pragma unroll
+    for (int k = 0; k < NPM; ++k) wsum[warp][k] = acc[k];
+  }
   __syncthreads();
-  if (threadIdx.x == 0) {
+  const int np = d + 2;
+  if ((int)threadIdx.x < np) {
+    const int k = (int)threadIdx.x == np - 1 ? NPM - 1 : (int)threadIdx.x;  // the nugget sits in the last slot
     double sum = 0.0;
-    for (int w = 0; w < GW; ++w) sum += wsum[w];
-    part[blockIdx.x] = sum;
+    for (int w = 0; w < GW; ++w) sum += wsum[w][k];
+    part[(int64_t)threadIdx.x * nblocks + blockIdx.x] = sum;
+  }
+}
+
+template <int FAM, int RB>
+cudaError_t launch_param_adj_all_rb(const GradPointArgs& a, cudaStream_t s) {
+  const unsigned blocks = (unsigned)((a.npts + GW - 1) / GW);
+  grad_param_adj_all_kernel<FAM, RB><<<blocks, GW * 32, 0, s>>>(a.X, a.nbr, a.mv, a.order, a.npts, a.p, a.state,
+                                                                a.adj, a.part, (int64_t)blocks);
+  return cudaGetLastError();
+}
+
+template <int FAM>
+cudaError_t launch_param_adj_all_fam(const GradPointArgs& a, cudaStream_t s) {
+  switch ((a.mv + 1 + 7) / 8) {
+    case 1: return launch_param_adj_all_rb<FAM, 1>(a, s);
+    case 2: return launch_param_adj_all_rb<FAM, 2>(a, s);
+    case 3: return launch_param_adj_all_rb<FAM, 3>(a, s);
+    case 4: return launch_param_adj_all_rb<FAM, 4>(a, s);
+    case 5: return launch_param_adj_all_rb<FAM, 5>(a, s);
+    default: return launch_param_adj_all_rb<FAM, 6>(a, s);
   }
 }
 
@@ -680,26 +698,6 @@ cudaError_t launch_adj_rb(const GradPointArgs& a, cudaStream_t s) {
   grad_adjoint_kernel<RB><<<blocks, GW * 32, 0, s>>>(a.U, a.Gam, a.ldu, a.mk, a.ld, a.nbr, a.mv, a.order, a.npts,
                                                      a.state, a.rho, a.sig, a.adj);
   return cudaGetLastError();
-}
-
-template <int FAM, int RB>
-cudaError_t launch_param_adj_rb(const GradPointArgs& a, cudaStream_t s) {
-  const unsigned blocks = (unsigned)((a.npts + GW - 1) / GW);
-  grad_param_adj_kernel<FAM, RB><<<blocks, GW * 32, 0, s>>>(a.dU, a.ldu, a.mk, a.X, a.nbr, a.mv, a.order, a.npts,
-                                                            a.p, a.pidx, a.state, a.rho, a.sig, a.adj, a.part);
-  return cudaGetLastError();
-}
-
-template <int FAM>
-cudaError_t launch_param_adj_fam(const GradPointArgs& a, cudaStream_t s) {
-  switch ((a.mv + 1 + 7) / 8) {
-    case 1: return launch_param_adj_rb<FAM, 1>(a, s);
-    case 2: return launch_param_adj_rb<FAM, 2>(a, s);
-    case 3: return launch_param_adj_rb<FAM, 3>(a, s);
-    case 4: return launch_param_adj_rb<FAM, 4>(a, s);
-    case 5: return launch_param_adj_rb<FAM, 5>(a, s);
-    default: return launch_param_adj_rb<FAM, 6>(a, s);
-  }
 }
 
 // ---- no dU at all: <R, dU> = <R L_m^{-1}, dK(X,Z)> - <R^T U, Phi_low>, R = sum over the points of the
@@ -884,7 +882,7 @@ __global__ void __launch_bounds__(256) gTdK_kernel(const double* __restrict__ X,
       const double f = FAM == FAM_M12 || FAM == FAM_GAUSS ? E
                      : (FAM == FAM_M32 ? fma(E, t, E) : fma(E, fma(t2, 1.0 / 3.0, t), E));
       acc[0] = fma(t_, f / p.sigma2, acc[0]);
-      // dk/dlambda_j = E Delta~_j^2 / lambda_j x {1/t, 1, (1+t)/3, 2} (dcov_fast)
+      // dk/dlambda_j = E Delta~_j^2 / lambda_j x {1/t, 1, (1+t)/3, 2} (as grad_param_adj_all_kernel)
       double g;
       if (FAM == FAM_M12) g = t > 0.0 ? 1.0 / t : 0.0;
       else if (FAM == FAM_M32) g = 1.0;
@@ -1127,19 +1125,21 @@ cudaError_t launch_grad_adjoint(const GradPointArgs& a, cudaStream_t s) {
   }
 }
 
-cudaError_t launch_grad_points_adj(const GradPointArgs& a, double* out, cudaStream_t s) {
-  if (a.mv > 47) return cudaErrorNotSupported;
+// every parameter's point terms in one pass (no dU): out[0 .. d+1]; a.part holds (d + 2) x grad_point_nparts(npts)
+cudaError_t launch_grad_points_adj_all(const GradPointArgs& a, double* out, cudaStream_t s) {
+  if (a.mv > 47 || a.dU) return cudaErrorNotSupported;
+  const int64_t nb = grad_point_nparts(a.npts);
   if (a.npts > 0) {
     cudaError_t e;
     switch (a.p.family) {
-      case FAM_M12: e = launch_param_adj_fam<FAM_M12>(a, s); break;
-      case FAM_M32: e = launch_param_adj_fam<FAM_M32>(a, s); break;
-      case FAM_M52: e = launch_param_adj_fam<FAM_M52>(a, s); break;
-      default: e = launch_param_adj_fam<FAM_GAUSS>(a, s); break;
+      case FAM_M12: e = launch_param_adj_all_fam<FAM_M12>(a, s); break;
+      case FAM_M32: e = launch_param_adj_all_fam<FAM_M32>(a, s); break;
+      case FAM_M52: e = launch_param_adj_all_fam<FAM_M52>(a, s); break;
+      default: e = launch_param_adj_all_fam<FAM_GAUSS>(a, s); break;
     }
     if (e != cudaSuccess) return e;
   }
-  grad_reduce_kernel<<<1, 1024, 0, s>>>(a.part, grad_point_nparts(a.npts), out);
+  for (int pi = 0; pi < a.p.d + 2; ++pi) grad_reduce_kernel<<<1, 1024, 0, s>>>(a.part + pi * nb, nb, out + pi);
   return cudaGetLastError();
 }
 

@@ -117,8 +117,7 @@ struct GradPointArgs {
   const int64_t* order;
   int64_t npts;
   CovParams p;
-  int pidx;      // 0: sigma_1^2, 1..d: lambda_j, d+1: nugget
-  double* part;  // grad_point_nparts(npts) block partials
+  double* part;  // (d + 2) x grad_point_nparts(npts) block partials
   double* state; // npts x grad_state_doubles(mv): per-point state of the first pass
   // adjoint form (k_grad.cu): rho, sig (npts x mk) and mu, Dm, beta~ (npts x grad_adj_doubles())
   double* rho = nullptr;
@@ -126,13 +125,14 @@ struct GradPointArgs {
   double* adj = nullptr;
 };
 int64_t grad_point_nparts(int64_t npts);
+// all d + 2 parameters' point terms in one pass (no dU); a.part: (d + 2) x grad_point_nparts(npts) doubles
+cudaError_t launch_grad_points_adj_all(const GradPointArgs& a, double* out, cudaStream_t s);
 size_t grad_state_doubles(int mv);
 // the g_i . U_aug[S_k] slots of a state written by the factor (VecchiaArgs::state)
 cudaError_t launch_grad_gam(const GradPointArgs& a, cudaStream_t s);
 cudaError_t launch_grad_state(const GradPointArgs& a, cudaStream_t s);
 size_t grad_adj_doubles();
 cudaError_t launch_grad_adjoint(const GradPointArgs& a, cudaStream_t s);
-cudaError_t launch_grad_points_adj(const GradPointArgs& a, double* out, cudaStream_t s);
 cudaError_t launch_gchild(const int32_t* nbr, int mv, const int64_t* order, int64_t npts, int64_t n, int* cnt,
                           int* cursor, int* ptr, int* ent, cudaStream_t s);
 cudaError_t launch_gR(const int* ptr, const int* ent, const int64_t* order, const int64_t* jorder, int64_t n, int mk,

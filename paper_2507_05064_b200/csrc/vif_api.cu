@@ -474,7 +474,7 @@ Layout make_grad_layout(const Plan& P) {
       (size_t)mk1 * mk1 * D8;
   L.size[G_MCOPY] = (size_t)P.ld * P.ld * D8;
   L.size[G_ZH] = L.size[G_Z] = (size_t)mk1 * D8;
-  L.size[G_PART] = (size_t)grad_point_nparts(P.npos) * D8;
+  L.size[G_PART] = (size_t)(P.d + 2) * grad_point_nparts(P.npos) * D8;
   L.size[G_OUT] = (size_t)(P.d + 2) * (P.emulate ? P.world : 1) * D8;
   L.size[G_STATE] = (size_t)P.npos * grad_state_doubles(P.mv) * D8;
   L.size[G_RHO] = L.size[G_SIG] = (size_t)P.npos * mk1 * D8;
@@ -1391,7 +1391,6 @@ int vif_grad(void* handle, const vif_theta* theta, void* gws, size_t gws_bytes, 
     a.order = h->ord(g);
     a.npts = P.n_own[rank];
     a.p = p;
-    a.pidx = -1;
     a.part = gbuf(G_PART);
     a.state = gbuf(G_STATE);
     a.rho = gbuf(G_RHO);
@@ -1435,6 +1434,9 @@ int vif_grad(void* handle, const vif_theta* theta, void* gws, size_t gws_bytes, 
                               gbuf(G_TDK), s),
                "<T, dK>");
     }
+    // the point terms of every parameter in one pass (bit-identical to one pass per parameter)
+    a.dU = nullptr;
+    VIF_CUDA(h, launch_grad_points_adj_all(a, gbuf(G_OUT) + (size_t)g * nparam, s), "gradient points");
     for (int pi = 0; pi < nparam; ++pi) {
       const bool kernel_param = pi <= P.d;
       if (kernel_param && m > 0) {
@@ -1443,9 +1445,6 @@ int vif_grad(void* handle, const vif_theta* theta, void* gws, size_t gws_bytes, 
         VIF_CUDA(h, launch_gemm_tn(Linv, mk, mk, gbuf(G_TT), mk, mk, mk, 0, gbuf(G_PHI), mk, 1.0, 0, s), "Phi");
         VIF_CUDA(h, launch_phi_low(gbuf(G_PHI), mk, gbuf(G_PHILOW), s), "Phi_low");
       }
-      a.dU = nullptr;
-      a.pidx = pi;
-      VIF_CUDA(h, launch_grad_points_adj(a, gbuf(G_OUT) + (size_t)g * nparam + pi, s), "gradient points");
       if (kernel_param && m > 0)
         VIF_CUDA(h, launch_gfinal(gbuf(G_OUT) + (size_t)g * nparam + pi, gbuf(G_TDK), pi, gbuf(G_G2), gbuf(G_PHILOW),
                                   mk, s),
