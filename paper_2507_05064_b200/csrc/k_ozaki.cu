@@ -100,6 +100,17 @@ __global__ void __launch_bounds__(256) oz_colmax_kernel(const double* __restrict
   }
 }
 
+// cmax[c] = max over the 64 interleaved copies written by the vecchia W pass (bit patterns of |w| >= 0 order
+// like the values; a NaN pattern exceeds every finite one, as oz_colmax_kernel's atomicMax would keep it)
+__global__ void oz_colmax_fold_kernel(const unsigned long long* __restrict__ c64, int ncols,
+                                      unsigned long long* __restrict__ cmax) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= ncols) return;
+  unsigned long long m = 0;
+  for (int k = 0; k < 64; ++k) m = max(m, c64[(size_t)k * ncols + c]);
+  cmax[c] = m;
+}
+
 // W rows [0, nrows) -> Ws[kb][p][a][k mod 32] for a < ncp, k < nrp (zero digits outside the matrix); a
 // non-finite entry sets *flag (the reduction then returns NaN, as the FP64 contraction would).
 // Digits without a carry chain: with Y = X + 0x808080808080 the six low bytes y_j of Y give d = y_j - 128
@@ -770,7 +781,8 @@ size_t syrk_i8_part_doubles(int ncols, int64_t cap_rows) {
 size_t syrk_i8_aux_bytes(int ncols) { return (size_t)((ncols + 127) / 128 * 128) * 8 + 256; }
 
 cudaError_t launch_syrk_i8(const double* W, int64_t ldw, int64_t nrows, int ncols, int8_t* ws, int64_t cap_rows,
-                           double* Gpart, void* aux, double* G, int ldg, int sms, cudaStream_t s) {
+                           double* Gpart, void* aux, double* G, int ldg, int sms, cudaStream_t s,
+                           const unsigned long long* cmax64) {
   if (!syrk_i8_supported(ncols) || cap_rows < 1 || (ldw & 1) || (reinterpret_cast<uintptr_t>(W) & 15))
     return cudaErrorInvalidValue;
   unsigned long long* cmax = reinterpret_cast<unsigned long long*>(aux);
@@ -778,7 +790,10 @@ cudaError_t launch_syrk_i8(const double* W, int64_t ldw, int64_t nrows, int ncol
   int* flag = reinterpret_cast<int*>(cmax + ncp0);
   cudaError_t e = cudaMemsetAsync(aux, 0, syrk_i8_aux_bytes(ncols), s);
   if (e != cudaSuccess) return e;
-  if (nrows > 0) {
+  if (cmax64) {
+    // the column maxima came with the rows (the vecchia W pass): fold the 64 copies
+    oz_colmax_fold_kernel<<<(ncols + 255) / 256, 256, 0, s>>>(cmax64, ncols, cmax);
+  } else if (nrows > 0) {
     const int ctas = 4 * sms;
     const int64_t rpc = (nrows + ctas - 1) / ctas;
     oz_colmax_kernel<<<(unsigned)((nrows + rpc - 1) / rpc), 256, 0, s>>>(W, ldw, nrows, ncols, rpc, cmax);

@@ -43,7 +43,8 @@ __global__ void __launch_bounds__(VW * 32, MINB) vecchia_smem_kernel(
     const double* __restrict__ U, int64_t ldu, int mk, int ld, const double* __restrict__ X,
     const double* __restrict__ Uq, const double* __restrict__ Xq, const int32_t* __restrict__ nbr, int mv, const int64_t* __restrict__ order, int64_t npts, CovParams p,
     double* __restrict__ W, int64_t ldw, double* __restrict__ Dpos, double* __restrict__ B_out,
-    double* __restrict__ D_out, DevStatus* __restrict__ st, double* __restrict__ gstate) {
+    double* __restrict__ D_out, DevStatus* __restrict__ st, double* __restrict__ gstate,
+    unsigned long long* __restrict__ cmax) {
   constexpr int SP = RB * 8;
   constexpr int NT = RB * (RB + 1) / 2;
   extern __shared__ __align__(16) double vsm[];
@@ -313,6 +314,17 @@ __global__ void __launch_bounds__(VW * 32, MINB) vecchia_smem_kernel(
       const int c = c0 + 2 * lane + 64 * t;
       if (c < ld) *reinterpret_cast<double2*>(W + pos * ldw + c) = o[t];
     }
+    if (cmax) {  // K4's column maxima of |W| (bit patterns), 64 interleaved copies to spread the atomics
+      unsigned long long* cm = cmax + (size_t)(pos & 63) * ld;
+#pragma unroll
+      for (int t = 0; t < 8; ++t) {
+        const int c = c0 + 2 * lane + 64 * t;
+        if (c < ld) {
+          atomicMax(cm + c, (unsigned long long)__double_as_longlong(fabs(o[t].x)));
+          atomicMax(cm + c + 1, (unsigned long long)__double_as_longlong(fabs(o[t].y)));
+        }
+      }
+    }
   }
   if (lane == 0) {
     Dpos[pos] = Di;
@@ -435,7 +447,8 @@ __global__ void __launch_bounds__(VW * 32, MINB) vecchia_reg_kernel(
     const double* __restrict__ U, int64_t ldu, int mk, int ld, const double* __restrict__ X,
     const double* __restrict__ Uq, const double* __restrict__ Xq, const int32_t* __restrict__ nbr, int mv, const int64_t* __restrict__ order, int64_t npts, CovParams p,
     double* __restrict__ W, int64_t ldw, double* __restrict__ Dpos, double* __restrict__ B_out,
-    double* __restrict__ D_out, DevStatus* __restrict__ st, double* __restrict__ gstate) {
+    double* __restrict__ D_out, DevStatus* __restrict__ st, double* __restrict__ gstate,
+    unsigned long long* __restrict__ cmax) {
   constexpr int SP = RB * 8;
   constexpr int CS = SP + 1;
   constexpr int NT = RB * (RB + 1) / 2;
@@ -616,6 +629,17 @@ __global__ void __launch_bounds__(VW * 32, MINB) vecchia_reg_kernel(
       const int c = c0 + 2 * lane + 64 * t;
       if (c < ld) *reinterpret_cast<double2*>(W + pos * ldw + c) = o[t];
     }
+    if (cmax) {  // K4's column maxima of |W| (bit patterns), 64 interleaved copies to spread the atomics
+      unsigned long long* cm = cmax + (size_t)(pos & 63) * ld;
+#pragma unroll
+      for (int t = 0; t < 8; ++t) {
+        const int c = c0 + 2 * lane + 64 * t;
+        if (c < ld) {
+          atomicMax(cm + c, (unsigned long long)__double_as_longlong(fabs(o[t].x)));
+          atomicMax(cm + c + 1, (unsigned long long)__double_as_longlong(fabs(o[t].y)));
+        }
+      }
+    }
   }
   if (lane == 0) {
     Dpos[pos] = Di;
@@ -653,7 +677,7 @@ static cudaError_t launch_reg(const VecchiaArgs& a, cudaStream_t s) {
   }
   kern<<<blocks, VW * 32, smem, s>>>(a.U, a.ldu, a.mk, a.ld, a.X, a.Uself ? a.Uself : a.U, a.Xself ? a.Xself : a.X,
                                      a.nbr, a.mv, a.order, a.npts, a.p, a.W, a.ldw, a.Dpos, a.B_out, a.D_out, a.st,
-                                     a.state);
+                                     a.state, a.cmax);
   return cudaGetLastError();
 }
 
@@ -670,7 +694,7 @@ static cudaError_t launch_smem(const VecchiaArgs& a, cudaStream_t s) {
   kern<<<blocks, VW * 32, smem, s>>>(a.U, a.ldu, a.mk, a.ld, a.X, a.Uself ? a.Uself : a.U,
                                                                  a.Xself ? a.Xself : a.X, a.nbr, a.mv,
                                                                  a.order, a.npts, a.p, a.W, a.ldw, a.Dpos,
-                                                                 a.B_out, a.D_out, a.st, a.state);
+                                                                 a.B_out, a.D_out, a.st, a.state, a.cmax);
   return cudaGetLastError();
 }
 

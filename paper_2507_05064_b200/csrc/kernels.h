@@ -31,6 +31,9 @@ struct VecchiaArgs {
   // gradient (vif_grad, one rank per process): the factor's rows also write the per-point state of the gradient's
   // first pass (vif_state_doubles layout, by position; the g_i dots are left to launch_grad_gam)
   double* state = nullptr;
+  // K4 on the integer tensor cores: column maxima of |W| (bit patterns) accumulated by the W pass into 64
+  // interleaved copies of ld entries (copy pos mod 64; zeroed by the caller), or nullptr
+  unsigned long long* cmax = nullptr;
 };
 
 // per-point gradient state, by position: L (packed lower, SP = 8 RB rows incl. the identity padding),
@@ -99,7 +102,8 @@ size_t syrk_i8_ws_bytes(int ncols, int64_t cap_rows);
 size_t syrk_i8_part_doubles(int ncols, int64_t cap_rows);
 size_t syrk_i8_aux_bytes(int ncols);
 cudaError_t launch_syrk_i8(const double* W, int64_t ldw, int64_t nrows, int ncols, int8_t* ws, int64_t cap_rows,
-                           double* Gpart, void* aux, double* G, int ldg, int sms, cudaStream_t s);
+                           double* Gpart, void* aux, double* G, int ldg, int sms, cudaStream_t s,
+                           const unsigned long long* cmax64 = nullptr);
 // sums the partials of nlaunch consecutive launch_syrk_part calls (same ncols, nsplit) into G
 cudaError_t launch_syrk_reduce(const double* Gpart, int ncols, int nsplit, int nlaunch, double* G, int ldg,
                                cudaStream_t s);

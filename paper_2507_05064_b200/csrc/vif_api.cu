@@ -202,7 +202,8 @@ Layout make_layout(const Plan& P) {
   if (P.syrk_i8) {
     L.size[B_GPART] = std::max(L.size[B_GPART], syrk_i8_part_doubles(P.ld, P.oz_cap) * D8);
     L.size[B_WS] = syrk_i8_ws_bytes(P.ld, P.oz_cap);
-    L.size[B_OZAUX] = syrk_i8_aux_bytes(P.ld);
+    // + the vecchia W pass' column maxima of |W| (64 interleaved copies, see VecchiaArgs::cmax)
+    L.size[B_OZAUX] = (syrk_i8_aux_bytes(P.ld) + 255) / 256 * 256 + (size_t)64 * P.ld * sizeof(unsigned long long);
   }
   if (P.k1_i8) {
     L.size[B_WS] = std::max(L.size[B_WS], ufeat_i8_ws_bytes(P.mk, P.oz_cap));
@@ -1166,6 +1167,12 @@ int vif_factor(void* handle, const vif_theta* theta, double* B_out, double* D_ou
     const int64_t npts = P.n_own[rank];
     double* Wg = h->buf<double>(B_W) + (size_t)g * P.npos * P.ld;
     double* Dg = h->buf<double>(B_DPOS) + (size_t)g * P.npos;
+    // K4's column maxima come with the W rows (one handle, one W): no separate pass over W
+    unsigned long long* c64 = nullptr;
+    if (P.syrk_i8 && nrep == 1) {
+      c64 = reinterpret_cast<unsigned long long*>(h->buf<char>(B_OZAUX) + (syrk_i8_aux_bytes(P.ld) + 255) / 256 * 256);
+      VIF_CUDA(h, cudaMemsetAsync(c64, 0, (size_t)64 * P.ld * sizeof(unsigned long long), s), "memset cmax");
+    }
     h->mark(S_VECCHIA, 0);
     int64_t off = 0;
     for (int64_t r = 0; r < P.rounds; ++r) {
@@ -1191,6 +1198,7 @@ int vif_factor(void* handle, const vif_theta* theta, double* B_out, double* D_ou
         a.D_out = D_out;
         a.st = st;
         a.state = h->grad_state ? h->grad_state + (size_t)off * grad_state_doubles(P.mv) : nullptr;
+        a.cmax = c64;
         VIF_CUDA(h, launch_vecchia(a, s), "vecchia");
         ++nl;
       }
@@ -1201,7 +1209,7 @@ int vif_factor(void* handle, const vif_theta* theta, double* B_out, double* D_ou
     h->mark(S_SYRK, 0);
     if (P.syrk_i8)
       VIF_CUDA(h, launch_syrk_i8(Wg, P.ld, npts, P.ld, h->buf<int8_t>(B_WS), P.oz_cap, h->buf<double>(B_GPART),
-                                 h->buf<char>(B_OZAUX), G, P.ld, kPlanSMs, s),
+                                 h->buf<char>(B_OZAUX), G, P.ld, kPlanSMs, s, c64),
                "syrk (int8 slices)");
     else
       VIF_CUDA(h, launch_syrk(Wg, P.ld, npts, P.ld, P.nsplit, h->buf<double>(B_GPART), G, P.ld, s), "syrk");
