@@ -391,26 +391,17 @@ __global__ void __launch_bounds__(256) kx_slice_kernel(const double* __restrict_
       }
       return t2;
     };
-    double t2min = 1e300;
-#pragma unroll 4
-    for (int q = lane; q < KPr; q += 32) t2min = fmin(t2min, dist2(q));
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) t2min = fmin(t2min, __shfl_xor_sync(0xffffffffu, t2min, o));
-    const double rmax = cov_t2(t2min);  // the covariance decreases with the distance
-    const int er = oz_exp((unsigned long long)__double_as_longlong(rmax));
-    if (lane == 0) erow[pos] = er;
-    const double scl = ldexp(1.0, 55 - er);
-    for (int t = 0; t < KPr / 128; ++t) {
+    // the four consecutive columns 128 t + 4 lane + j (values v[j]) as 7 digit slices, one 4-byte store each
+    auto emit = [&](int t, const double (&v)[4], double scl) {
       uint32_t lo[4], hi[4];
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
-        const double v = cov_t2(dist2(128 * t + 32 * j + lane));
-        const long long Y = __double2ll_rn(v * scl) + 0x808080808080LL;
+        const long long Y = __double2ll_rn(v[j] * scl) + 0x808080808080LL;
         lo[j] = (uint32_t)Y;
         hi[j] = (uint32_t)((unsigned long long)Y >> 32);
       }
       const int b0 = 128 * t + 4 * lane;
-      if (b0 >= KP) continue;
+      if (b0 >= KP) return;
       // row-block-major: [R][kb][q][128 rows][32 B] -- a row block's slices are one contiguous 7 x 4 KB x kb run
       int8_t* dst = Ss + ((((pos >> 7) * kbA + (b0 >> 5)) * OZ_S) * OZ_BM + (pos & 127)) * OZ_BK + (b0 & 31);
 #pragma unroll
@@ -424,6 +415,46 @@ __global__ void __launch_bounds__(256) kx_slice_kernel(const double* __restrict_
       {
         const uint32_t xx = __byte_perm(hi[0], hi[1], 0x62), yy = __byte_perm(hi[2], hi[3], 0x62);
         *reinterpret_cast<uint32_t*>(dst) = __byte_perm(xx, yy, 0x5410);
+      }
+    };
+    if (KPr <= 512) {
+      // <= 512 columns: the 16 scaled squared distances of pass 1 stay in registers for pass 2
+      double t2c[16];
+      double t2min = 1e300;
+#pragma unroll
+      for (int u = 0; u < 16; ++u) {
+        t2c[u] = 32 * u < KPr ? dist2(lane + 32 * u) : 1e300;
+        t2min = fmin(t2min, t2c[u]);
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) t2min = fmin(t2min, __shfl_xor_sync(0xffffffffu, t2min, o));
+      const int er = oz_exp((unsigned long long)__double_as_longlong(cov_t2(t2min)));
+      if (lane == 0) erow[pos] = er;
+      const double scl = ldexp(1.0, 55 - er);
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        if (128 * t < KPr) {
+          double v[4];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) v[j] = cov_t2(t2c[4 * t + j]);
+          emit(t, v, scl);
+        }
+      }
+    } else {
+      double t2min = 1e300;
+#pragma unroll 4
+      for (int q = lane; q < KPr; q += 32) t2min = fmin(t2min, dist2(q));
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) t2min = fmin(t2min, __shfl_xor_sync(0xffffffffu, t2min, o));
+      const double rmax = cov_t2(t2min);  // the covariance decreases with the distance
+      const int er = oz_exp((unsigned long long)__double_as_longlong(rmax));
+      if (lane == 0) erow[pos] = er;
+      const double scl = ldexp(1.0, 55 - er);
+      for (int t = 0; t < KPr / 128; ++t) {
+        double v[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) v[j] = cov_t2(dist2(128 * t + 32 * j + lane));
+        emit(t, v, scl);
       }
     }
     {
@@ -862,10 +893,13 @@ cudaError_t launch_u_features_i8(const double* X, const double* Z, const double*
   for (int64_t c0 = 0; c0 < npos; c0 += cap_rows) {
     const int64_t rows = std::min<int64_t>(cap_rows, npos - c0);
     const int64_t nposp = k1_nposp(rows);
-    int nb = (int)std::min<int64_t>((rows + 7) / 8, (int64_t)sms * 4);
     auto go = [&](auto kern) -> cudaError_t {
       cudaError_t e1 = smem_optin(kern, kx_smem);
       if (e1 != cudaSuccess) return e1;
+      int per_sm = 0;  // one full wave of resident blocks (the rows are grid-strided)
+      e1 = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, kx_smem);
+      if (e1 != cudaSuccess) return e1;
+      const int nb = (int)std::min<int64_t>((rows + 7) / 8, (int64_t)sms * std::max(per_sm, 1));
       kern<<<nb, 256, kx_smem, s>>>(X, Z, y, n, rows, chunk, world, rank, pos0 + c0, m, mk, KP, p, ws, (int64_t)kb,
                                     erow, Uaug, ld);
       return cudaGetLastError();
@@ -1044,7 +1078,7 @@ static size_t knn_i8_smem(int mv, int EW, int ST) {
          8 + (size_t)KN_C * (VIF_MAX_D + 2) * sizeof(double);
 }
 
-template <int FAM, int EW, int ST>
+template <int FAM, int EW, int ST, int DD = 0>
 __global__ void __launch_bounds__(64 + 32 * EW, 1)
     knn_i8_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmC, int kbmax,
                   const int* __restrict__ erow, const double* __restrict__ X, int64_t n, CovParams p,
@@ -1124,7 +1158,7 @@ __global__ void __launch_bounds__(64 + 32 * EW, 1)
     const int r = q * 32 + lane, et = threadIdx.x - 64;  // query row of the block; epilogue thread
     const int hh = (warp - 2) >> 2;                       // which CW candidates of every tile
     const int64_t i = q0 + r;
-    const int d = p.d;
+    const int d = DD > 0 ? DD : p.d;  // d = 2 as a compile-time constant: coordinates in registers
     double xq[VIF_MAX_D];
 #pragma unroll
     for (int k = 0; k < VIF_MAX_D; ++k)
@@ -1297,7 +1331,10 @@ cudaError_t launch_knn_i8(const double* U, int64_t ldu, int mk, const double* X,
     kern<<<grid, 64 + 32 * ew, smem, s>>>(tq, tc, kb, erow, X, n, p, isd, deg, mv, out, qoff, qstride);
     return cudaGetLastError();
   };
-#define VIF_KNNI8(F) (wide ? go(knn_i8_kernel<F, 8, 2>, 8, 2) : go(knn_i8_kernel<F, 4, KN_STAGES>, 4, KN_STAGES))
+#define VIF_KNNI8(F)                                                                               \
+  (wide ? (p.d == 2 ? go(knn_i8_kernel<F, 8, 2, 2>, 8, 2) : go(knn_i8_kernel<F, 8, 2>, 8, 2))      \
+        : (p.d == 2 ? go(knn_i8_kernel<F, 4, KN_STAGES, 2>, 4, KN_STAGES)                          \
+                    : go(knn_i8_kernel<F, 4, KN_STAGES>, 4, KN_STAGES)))
   switch (p.family) {
     case FAM_M12: return VIF_KNNI8(FAM_M12);
     case FAM_M32: return VIF_KNNI8(FAM_M32);
