@@ -187,8 +187,9 @@ def test_search_config3_equals_generator():
     model.close()
 
 
-@pytest.mark.parametrize("family,n,m,mv", [("matern32", 3000, 60, 20), ("gaussian", 2500, 250, 31), ("matern12", 1200, 8, 47)])
-def test_int8_and_dmma_engines_agree(family, n, m, mv):
+@pytest.mark.parametrize("family,n,m,mv,d,rho", [("matern32", 3000, 60, 20, 2, 0.15), ("gaussian", 2500, 250, 31, 2, 0.15),
+                                                  ("matern12", 1200, 8, 47, 2, 0.15), ("matern52", 2000, 100, 15, 5, 0.6)])
+def test_int8_and_dmma_engines_agree(family, n, m, mv, d, rho):
     """vif_neighbors with the Gram blocks on the integer tensor cores (default, reading c18) and on DMMA
     (VIF_KNN_FP64=1, read once per process: subprocesses): the same sets on every row except scores equal
     to rounding, where both choices carry the same oracle score"""
@@ -201,12 +202,12 @@ import sys, json
 import numpy as np, torch
 sys.path.insert(0, %r)
 import paper_2507_05064_b200 as p, vifgen
-w = vifgen.make_workload(n=%d, d=2, m=%d, mv=%d, family=%r, rho=0.15, nugget=0.1, seed=77, device="cuda")
+w = vifgen.make_workload(n=%d, d=%d, m=%d, mv=%d, family=%r, rho=%r, nugget=0.1, seed=77, device="cuda")
 dev = torch.device("cuda")
 X, Z, nbr, y = (torch.from_numpy(np.ascontiguousarray(a)).to(dev) for a in (w.X, w.Z, w.nbr, w.y))
 m = p.VifModel(X, Z, nbr, y, device=dev)
 print(json.dumps(m.neighbors(p.Theta(**w.theta_dict()), %d).cpu().numpy().tolist()))
-""" % (os.path.dirname(os.path.dirname(os.path.abspath(__file__))), n, m, mv, family, mv)
+""" % (os.path.dirname(os.path.dirname(os.path.abspath(__file__))), n, d, m, mv, family, rho, mv)
     outs = []
     for fp64 in ("0", "1"):
         # the int8 run places its digit slices in the W buffer (the n > 2^20 placement) for the largest case
@@ -215,7 +216,7 @@ print(json.dumps(m.neighbors(p.Theta(**w.theta_dict()), %d).cpu().numpy().tolist
         assert r.returncode == 0, r.stderr[-2000:]
         outs.append(np.array(json.loads(r.stdout.strip().splitlines()[-1])))
     a, b = outs
-    w = vifgen.make_workload(n=n, d=2, m=m, mv=mv, family=family, rho=0.15, nugget=0.1, seed=77, device="cuda")
+    w = vifgen.make_workload(n=n, d=d, m=m, mv=mv, family=family, rho=rho, nugget=0.1, seed=77, device="cuda")
     diff = np.nonzero((a != b).any(1))[0]
     assert len(diff) <= max(2, 0.005 * n), len(diff)
     oth = oracle.Theta(**w.theta_dict())
