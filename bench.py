@@ -544,7 +544,7 @@ def main():
                                                   "int8_frac": syrk_int8_ops(w.n / world, w.m) /
                                                   (stage_avg[kern["syrk"]] * 1e-3) / 1e12 / INT8_PEAK_TOPS,
                                                   "int8_note": "stage time includes the digit-slicing pass over W "
-                                                               "(~1.3 of 4.8 ms at config 3; the column maxima come "
+                                                               "(~1.4 of 4.8 ms at config 3; the column maxima come "
                                                                "with the vecchia W rows)"}),
                          "contractions_frac": {"U = K(X,Z) L_m^-T (K1)": achieved["ufeat"] / FP64_PEAK_TFLOPS,
                                                "M Gram W^T W (K4)": achieved["syrk"] / FP64_PEAK_TFLOPS,
