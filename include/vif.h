@@ -196,8 +196,9 @@ int vif_predict(void* handle, const vif_theta* theta, int64_t np, const double* 
  * smallest d_c(i,j) = sqrt(1 - |rho_c(i,j)| / sqrt(rho_c(i,i) rho_c(j,j))), rho_c = k - u_i.u_j at theta
  * (no nugget), ranked by (d_c, index); i <= mv: all predecessors; readings c5-c7 (a point
  * whose residual variance is below 1e-7 sigma_1^2 scores d_c = 1 as a candidate and ranks its own
- * predecessors by length-scale-scaled Euclidean distance).  Exact brute force (n^2 m / 2 FMA on the
- * FP64 tensor cores).  nbr_out: device, n x mv int32, -1 padded; mv in [1, VIF_MAX_MV] (independent of
+ * predecessors by length-scale-scaled Euclidean distance).  Exact brute force (n^2 m / 2 FMA): the Gram
+ * blocks u_i.u_j as exact int8 digit-slice products on the integer tensor cores when m > 0 (DESIGN reading
+ * c18; environment VIF_KNN_FP64=1 selects the FP64 DMMA kernel), scores and ranking in FP64.  nbr_out: device, n x mv int32, -1 padded; mv in [1, VIF_MAX_MV] (independent of
  * dims.mv).  Uses the handle's workspace (invalidates a previous vif_factor: call vif_factor again).
  * Multi-rank: every rank evaluates u_i of all n points; rank g searches the 64-point query blocks
  * kb = g, g + G, ... (counted from the last block) and writes only their rows of the full-length nbr_out;
