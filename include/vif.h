@@ -200,8 +200,8 @@ int vif_predict(void* handle, const vif_theta* theta, int64_t np, const double* 
  * blocks u_i.u_j as exact int8 digit-slice products on the integer tensor cores when m > 0 (DESIGN reading
  * c18; environment VIF_KNN_FP64=1 selects the FP64 DMMA kernel), scores and ranking in FP64.  nbr_out: device, n x mv int32, -1 padded; mv in [1, VIF_MAX_MV] (independent of
  * dims.mv).  Uses the handle's workspace (invalidates a previous vif_factor: call vif_factor again).
- * Multi-rank: every rank evaluates u_i of all n points; rank g searches the 64-point query blocks
- * kb = g, g + G, ... (counted from the last block) and writes only their rows of the full-length nbr_out;
+ * Multi-rank: every rank evaluates u_i of all n points; rank g searches the query blocks (128 points on
+ * the integer engine, 64 on DMMA) kb = g, g + G, ... (counted from the last block) and writes only their rows of the full-length nbr_out;
  * an emulated handle writes all rows.  Errors: INVALID_ARG, NOT_PD (K(Z,Z) + jitter), CUDA. */
 int vif_neighbors(void* handle, const vif_theta* theta, int32_t mv, int32_t* nbr_out);
 
