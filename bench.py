@@ -122,6 +122,23 @@ def per_point_flops(s, m):
             "syrk": (m + 1.0) * (m + 2.0)}                            # A6
 
 
+def vecchia_executed_flops(nbr, m):
+    """FP64 flops the vecchia kernel EXECUTES per launch (k_vecchia.cuh, s <= 32): the Gram on 8 x 8 DMMA tiles of
+    the RB = ceil(s / 8) row blocks (RB (RB + 1) / 2 tiles x 64 entries x mk, the padding included), the Cholesky of
+    the padded 8 RB rows, the back substitution and the W row over the ld columns -- against the algorithmic
+    count of per_point_flops, which counts only the s (s + 1) / 2 needed Gram entries"""
+    mk = -(-m // 8) * 8
+    ld = -(-(mk + 1) // 8) * 8
+    s = (nbr >= 0).sum(1).astype(np.float64) + 1.0 if nbr.shape[1] > 0 else np.ones(nbr.shape[0])
+    rb = np.ceil(s / 8.0)
+    sp = 8.0 * rb
+    gram = rb * (rb + 1) / 2 * 64 * mk * 2.0
+    chol = sp ** 3 / 3.0
+    solve = (s - 1) ** 2
+    wrow = 2.0 * s * ld
+    return float(np.sum(gram + chol + solve + wrow))
+
+
 INT8_PEAK_TOPS = 2 * 1665.1  # MEASURED_PEAKS.json bf16_tflops (burst) x the guide's nominal int8 : bf16 ratio of 2
 
 
@@ -515,6 +532,15 @@ def main():
                          "peak_source": "measured FP64 DMMA peak on this pool's B200 (tools/microbench_fp64.cu; "
                                         "MEASURED_PEAKS.json has no FP64 entry); cuBLAS DGEMM 35.5",
                          "flops_per_launch": fl_launch[dom], "avg_launch_ms": stage_avg[kern[dom]],
+                         "executed": ({"flops_per_launch": vecchia_executed_flops(w.nbr, w.m) * share,
+                                       "tflops": vecchia_executed_flops(w.nbr, w.m) * share /
+                                       (stage_avg[kern["vecchia"]] * 1e-3) / 1e12,
+                                       "frac": vecchia_executed_flops(w.nbr, w.m) * share /
+                                       (stage_avg[kern["vecchia"]] * 1e-3) / 1e12 / FP64_PEAK_TFLOPS,
+                                       "note": "flops the kernel executes (8 x 8 DMMA tile padding of the s x s "
+                                               "Gram, padded Cholesky, W row over ld columns); frac above counts "
+                                               "only the algorithmic flops"}
+                                      if dom == "vecchia" and w.mv <= 31 else None),
                          "per_kernel": dict({k: {"stage": kern[k], "avg_ms": stage_avg[kern[k]], "tflops": achieved[k],
                                                  "frac": achieved[k] / FP64_PEAK_TFLOPS} for k in kern},
                                             ufeat={"stage": kern["ufeat"], "avg_ms": stage_avg[kern["ufeat"]],
