@@ -116,3 +116,23 @@ def test_knob_matches_oracle(refs, wname, env):
         assert len(sel) == (rn[i] >= 0).sum() and np.all(sel < i) and len(set(sel)) == len(sel)
         gs = oracle.dc_scores(w.X, w.Z, oth, np.full(len(sel), i), sel)
         np.testing.assert_allclose(gs, rs[i][:len(sel)], rtol=1e-12, atol=1e-14)
+
+
+@pytest.mark.parametrize("env", [
+    {"VIF_LA_LONG": "8"},                                # lanes-over-entries rows from 8 entries on, every ncol
+    {"VIF_LA_LONG": "1000000"},                          # never
+    {"VIF_LA_LVL_BPS": "2", "VIF_LA_LVL_CTAS": "40"},    # two CTAs per SM allowed, grid capped at 40 CTAs
+], ids=lambda v: "+".join(f"{k}={x}" for k, x in v.items()))
+def test_laplace_solve_launch_knobs(env):
+    """The launch-shape knobs of the level-scheduled triangular solves (k_laplace.cu, section 13): the
+    operator, mode and SLQ parity cases of test_gpu_laplace.py (each against oracle/laplace.py) rerun in a
+    process with the knob set."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    r = subprocess.run([sys.executable, "-m", "pytest", os.path.join(ROOT, "tests", "test_gpu_laplace.py"), "-q", "-x",
+                        "-m", "gpu", "-k", "test_operators or test_mode_shapes or test_slq_logdet or "
+                        "test_sigma_inv_inverts_sigma"],
+                       env=dict(os.environ, **env), capture_output=True, text=True, timeout=1500, cwd=ROOT)
+    tail = r.stdout[-1500:] + r.stderr[-500:]
+    assert r.returncode == 0, tail
+    assert " passed" in r.stdout and " failed" not in r.stdout and " skipped" not in r.stdout, tail
